@@ -1,0 +1,209 @@
+"""CPU oracle for the SPDP Gibbs sweep — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product path (``paper_1510_06549_b200``) never imports, links or executes
+anything under ``oracle/``; the two share no code.
+
+The arithmetic lives in ``spdp_oracle.c`` (plain C, fp64, log space), which
+cites the paper passage each function follows.  This module only builds it
+with gcc and marshals arguments through ctypes.
+
+Parity status of every oracle function is listed in DESIGN.md §4; each one
+is pinned by a ``-m "not gpu"`` test in ``tests/test_oracle_*.py``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "spdp_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+P = C.c_void_p
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", _SRC, "-o", _LIB, "-lm"])
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(_LIB)
+        L.or_philox.argtypes = [P, P, P]
+        L.or_log_stirling.restype = C.c_double
+        L.or_log_stirling.argtypes = [C.c_double, C.c_int, C.c_int]
+        L.or_create.restype = P
+        L.or_create.argtypes = [C.c_int, C.c_int, C.c_int, P, C.c_double, P, P, C.c_uint64]
+        L.or_destroy.argtypes = [P]
+        L.or_load.restype = C.c_int
+        L.or_load.argtypes = [P, C.c_int64, C.c_int32, P, P, P, P, P, P]
+        L.or_sweep_seq.restype = C.c_int
+        L.or_sweep_seq.argtypes = [P, C.c_int64]
+        L.or_sweep_par.restype = C.c_int
+        L.or_sweep_par.argtypes = [P, C.c_int, C.c_int, P, P, C.c_int64]
+        L.or_get.argtypes = [P] + [P] * 6
+        L.or_sweep_index.restype = C.c_uint32
+        L.or_sweep_index.argtypes = [P]
+        L.or_set_sweep_index.argtypes = [P, C.c_uint32]
+        L.or_stats.argtypes = [P, P]
+        L.or_conditional.restype = C.c_int
+        L.or_conditional.argtypes = [P, C.c_int64, C.c_int, P]
+        L.or_debug_token.restype = C.c_int
+        L.or_debug_token.argtypes = [P, C.c_int64, C.c_uint32, P, P, P, P]
+        L.or_perplexity.restype = C.c_double
+        L.or_perplexity.argtypes = [P]
+        L.or_log_joint.restype = C.c_double
+        L.or_log_joint.argtypes = [P]
+        L.or_check_invariants.restype = C.c_int
+        L.or_check_invariants.argtypes = [P]
+        L.or_partition.argtypes = [P, C.c_int, P]
+        L.or_word_prob.restype = C.c_double
+        L.or_word_prob.argtypes = [P, C.c_int32, C.c_int32]
+        L.or_chain_codes.restype = C.c_int
+        L.or_chain_codes.argtypes = [P, C.c_int64, C.c_int, C.c_int, P]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def philox(ctr, key):
+    """Philox4x32-10 of a 4-word counter and 2-word key (both uint32)."""
+    c = np.asarray(ctr, np.uint32); k = np.asarray(key, np.uint32); out = np.zeros(4, np.uint32)
+    lib().or_philox(_ptr(c), _ptr(k), _ptr(out))
+    return out
+
+
+def log_stirling(a: float, n: int, m: int) -> float:
+    """log S^n_{m,a} by the recursion of PAPER.md:1454-1455 (fp64, log space)."""
+    return lib().or_log_stirling(float(a), int(n), int(m))
+
+
+class Oracle:
+    """Sequential (mode S) and wave-snapshot (mode P) SPDP Gibbs sampler."""
+
+    def __init__(self, num_groups, vocab, num_topics, alpha, beta, discount, concentration, seed):
+        L = lib()
+        I, V, K = int(num_groups), int(vocab), int(num_topics)
+        al = np.asarray(alpha, np.float64)
+        al = np.full((I, K), float(al)) if al.ndim == 0 else al.reshape(I, K).astype(np.float64)
+        a = np.asarray(discount, np.float64); a = np.full(I, float(a)) if a.ndim == 0 else a.astype(np.float64)
+        b = np.asarray(concentration, np.float64); b = np.full(I, float(b)) if b.ndim == 0 else b.astype(np.float64)
+        self._keep = (np.ascontiguousarray(al), np.ascontiguousarray(a), np.ascontiguousarray(b))
+        self.I, self.V, self.K = I, V, K
+        self.h = L.or_create(I, V, K, _ptr(self._keep[0]), float(beta), _ptr(self._keep[1]), _ptr(self._keep[2]),
+                             C.c_uint64(int(seed) & (2**64 - 1)))
+        if not self.h:
+            raise ValueError("or_create: invalid parameters")
+        self.N = 0
+        self.D = 0
+
+    def close(self):
+        if self.h:
+            lib().or_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, group, doc, word, num_docs, z_init=None, r_init=None, t_init=None):
+        g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
+        w = np.ascontiguousarray(word, np.int32)
+        z = None if z_init is None else np.ascontiguousarray(z_init, np.int32)
+        r = None if r_init is None else np.ascontiguousarray(r_init, np.uint8)
+        t = None if t_init is None else np.ascontiguousarray(np.asarray(t_init).reshape(-1), np.int32)
+        rc = lib().or_load(self.h, len(w), int(num_docs), _ptr(g), _ptr(d), _ptr(w), _ptr(z), _ptr(r), _ptr(t))
+        if rc != 0:
+            raise ValueError(f"or_load failed ({rc})")
+        self.N, self.D = len(w), int(num_docs)
+
+    def sweep_seq(self, max_tokens: int = -1):
+        if lib().or_sweep_seq(self.h, int(max_tokens)) != 0:
+            raise RuntimeError("or_sweep_seq failed")
+
+    def sweep_par(self, waves: int = 1, shards: int = 1, force_zr=None, want_margin=False, max_tokens: int = -1):
+        f = None if force_zr is None else np.ascontiguousarray(force_zr, np.int32)
+        mg = np.full(self.N, np.inf) if want_margin else None
+        if lib().or_sweep_par(self.h, int(waves), int(shards), _ptr(f), _ptr(mg), int(max_tokens)) != 0:
+            raise RuntimeError("or_sweep_par failed")
+        return mg
+
+    @property
+    def sweep_index(self) -> int:
+        return int(lib().or_sweep_index(self.h))
+
+    @sweep_index.setter
+    def sweep_index(self, v: int):
+        lib().or_set_sweep_index(self.h, int(v))
+
+    def stats(self):
+        s = np.zeros(8, np.int64)
+        lib().or_stats(self.h, _ptr(s))
+        return {"keeps": int(s[0]), "moved": int(s[1]), "clamped": int(s[2]), "forced_differ": int(s[3])}
+
+    def state(self):
+        """dict of z [N], r [N], n [D,K], m [I,V,K], t [I,V,K], Q [K,V]."""
+        I, V, K = self.I, self.V, self.K
+        z = np.zeros(self.N, np.int32); r = np.zeros(self.N, np.uint8)
+        n = np.zeros((self.D, K), np.int32); m = np.zeros((I, V, K), np.int32); t = np.zeros((I, V, K), np.int32)
+        Q = np.zeros((K, V), np.int32)
+        lib().or_get(self.h, _ptr(z), _ptr(r), _ptr(n), _ptr(m), _ptr(t), _ptr(Q))
+        return {"z": z, "r": r, "n": n, "m": m, "t": t, "Q": Q}
+
+    def conditional(self, tok: int, r_rem: int):
+        p = np.zeros(2 * self.K)
+        rc = lib().or_conditional(self.h, int(tok), int(r_rem), _ptr(p))
+        return None if rc != 0 else p
+
+    def debug_token(self, tok: int, sweep: int):
+        p = np.zeros(2 * self.K); info = np.zeros(4, np.int32); u = C.c_double(); mg = C.c_double()
+        rc = lib().or_debug_token(self.h, int(tok), int(sweep), _ptr(p), _ptr(info), C.byref(u), C.byref(mg))
+        if rc != 0:
+            raise RuntimeError("or_debug_token failed")
+        return {"prob": p, "r_rem": int(info[0]), "keep": int(info[1]), "z": int(info[2]), "r": int(info[3]),
+                "u": u.value, "margin": mg.value}
+
+    def perplexity(self) -> float:
+        return float(lib().or_perplexity(self.h))
+
+    def log_joint(self) -> float:
+        return float(lib().or_log_joint(self.h))
+
+    def word_prob(self, doc: int, word: int) -> float:
+        return float(lib().or_word_prob(self.h, int(doc), int(word)))
+
+    def chain_codes(self, nsweeps: int, waves: int = -1, tbase: int = 5):
+        out = np.zeros(int(nsweeps), np.int64)
+        if lib().or_chain_codes(self.h, int(nsweeps), int(waves), int(tbase), _ptr(out)) != 0:
+            raise RuntimeError("or_chain_codes failed")
+        return out
+
+    def check_invariants(self) -> int:
+        return int(lib().or_check_invariants(self.h))
+
+    def partition(self, shards: int):
+        out = np.zeros(self.D, np.int32)
+        lib().or_partition(self.h, int(shards), _ptr(out))
+        return out
+
+
+def from_corpus(corpus, num_topics, alpha=0.1, beta=0.1, discount=0.7, concentration=100.0, seed=7,
+                z_init=None, r_init=None, t_init=None) -> Oracle:
+    o = Oracle(corpus.num_groups, corpus.vocab, num_topics, alpha, beta, discount, concentration, seed)
+    o.load(corpus.group, corpus.doc, corpus.word, corpus.num_docs, z_init, r_init, t_init)
+    return o

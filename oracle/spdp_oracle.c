@@ -1,0 +1,755 @@
+/*
+ * oracle/spdp_oracle.c — plain, slow, CPU reference for the SPDP Gibbs sweep.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code with paper_1510_06549_b200/ (own Philox, own Stirling
+ * numbers, own partition and wave plan), and the product path never calls it.
+ *
+ * Everything is fp64, and the sampler weights are formed in log space.
+ * Citations are PAPER.md line numbers (P:<line>) with the section / equation /
+ * algorithm they fall in; "reading cN" refers to DESIGN.md §3 (readings of
+ * the paper), which follows SURVEY.md §8(c).
+ *
+ *  - Generalised Stirling numbers S^N_{M,a}: P:1452-1457 (§2.4.5):
+ *      S^{N+1}_M = S^N_{M-1} + (N - M a) S^N_M,  S^N_M = 0 for M > N,
+ *      S^N_0 = delta_{N,0}.  Kept as log S in a lower-triangular table.
+ *  - Pochhammer symbols (x|y)_N = prod_{n<N} (x + n y), (x)_N = (x|1)_N:
+ *      P:1452-1453.
+ *  - Conditionals Eq. SPDP-sampling-w-z-r0 and
+ *      Eq. SPDP-sampling-w-z-r1 with identity P,
+ *      so q_{ikwv} = t_{ikw}[v=w] and sum_i sum_w q_{ikwv} = Q_{kv}.
+ *  - Algorithm 1 "SPDP Full Gibbs Sampling" = or_sweep_seq,
+ *      plus the keep rule (reading c5).
+ *  - Parallel framework (§3.3, P:2210-2233, P:2289-2299, P:2370-2386,
+ *      P:2411-2427; Alg.3/Alg.4) with the deterministic
+ *      wave-snapshot reading (reading c13) = or_sweep_par.
+ *  - Estimators Eqs. spdp-topic-doc-estimate,
+ *      spdp-word-topic-estimate, spdp-group-word-topic-estimate
+ *      (reading c16) and the perplexity of §3.2 (P:1978-2007,
+ *      reading c17) = or_perplexity.
+ *  - Joint p(W,Z,T) from the blocked-Gibbs joint with the
+ *      C(m,t) factor of Eq. SPDP-table-to-head summed out
+ *      = or_log_joint (reading c1, c2).
+ *  - Philox4x32-10 counter-based RNG (reading c11; Salmon et al. 2011).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ */
+/* Philox4x32-10                                                       */
+/* ------------------------------------------------------------------ */
+void or_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; round++) {
+        if (round > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * x0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * x2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t y0 = hi1 ^ x1 ^ k0, y1 = lo1, y2 = hi0 ^ x3 ^ k1, y3 = lo0;
+        x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+    }
+    out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+static void rng_token(uint64_t seed, uint32_t tok, uint32_t sweep, uint32_t x[4]) {
+    uint32_t ctr[4] = {tok, sweep, 0u, 0u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    or_philox(ctr, key, x);
+}
+/* 53-bit uniform in [0,1) from x1 (32 bits) and the top 21 bits of x2 */
+static double u53(const uint32_t x[4]) {
+    return ((double)x[1] * 2097152.0 + (double)(x[2] >> 11)) * (1.0 / 9007199254740992.0);
+}
+
+/* ------------------------------------------------------------------ */
+/* log generalised Stirling numbers                       */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    double a;
+    int nmax;          /* rows 0..nmax */
+    double *v;         /* row N at offset N(N+1)/2, entries M = 0..N */
+} stable_t;
+
+static double logaddexp(double x, double y) {
+    if (x == -INFINITY) return y;
+    if (y == -INFINITY) return x;
+    double mx = x > y ? x : y, mn = x > y ? y : x;
+    return mx + log1p(exp(mn - mx));
+}
+
+static int stable_build(stable_t *s, double a, int nmax) {
+    size_t sz = (size_t)(nmax + 1) * (size_t)(nmax + 2) / 2;
+    double *v = (double *)malloc(sizeof(double) * sz);
+    if (!v) return -1;
+    v[0] = 0.0; /* S^0_0 = 1 */
+    for (int N = 0; N < nmax; N++) {
+        const double *row = v + (size_t)N * (N + 1) / 2;
+        double *nxt = v + (size_t)(N + 1) * (N + 2) / 2;
+        nxt[0] = -INFINITY; /* S^{N+1}_0 = 0 */
+        for (int M = 1; M <= N + 1; M++) {
+            double left = row[M - 1];                                 /* S^N_{M-1} */
+            double right = (M <= N) ? row[M] : -INFINITY;             /* S^N_M (0 if M > N) */
+            double coef = (double)N - (double)M * a;                  /* (N - M a) */
+            double term = (right == -INFINITY || coef <= 0.0) ? -INFINITY : log(coef) + right;
+            nxt[M] = logaddexp(left, term);
+        }
+    }
+    s->a = a; s->nmax = nmax; s->v = v;
+    return 0;
+}
+
+static double stable_get(const stable_t *s, int N, int M) {
+    if (M < 0 || M > N) return -INFINITY;
+    return s->v[(size_t)N * (N + 1) / 2 + M];
+}
+
+double or_log_stirling(double a, int N, int M) {
+    stable_t s;
+    if (N < 0) return -INFINITY;
+    if (stable_build(&s, a, N) != 0) return NAN;
+    double r = stable_get(&s, N, M);
+    free(s.v);
+    return r;
+}
+
+/* ln (x|y)_n = sum_{j<n} ln(x + j y) */
+static double log_poch(double x, double y, int64_t n) {
+    double s = 0.0;
+    for (int64_t j = 0; j < n; j++) s += log(x + (double)j * y);
+    return s;
+}
+
+/* ------------------------------------------------------------------ */
+/* state                                                               */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int I, V, K;
+    double *alpha;     /* [I*K] */
+    double beta;
+    double *a, *b;     /* [I] */
+    uint64_t seed;
+    uint32_t sweep;    /* next sweep index (RNG counter word 1) */
+
+    int64_t N; int32_t D;
+    int32_t *group, *doc, *word, *pos;   /* canonical token arrays; pos = in-doc position l */
+    int32_t *doclen;                      /* [D] */
+    int32_t *z; uint8_t *r;
+    int32_t *n;        /* [D*K] */
+    int32_t *m, *t;    /* [I*V*K]  (i, w, k) */
+    int64_t *M, *Tt;   /* [I*K]    m_{ik.}, t_{ik.} */
+    int64_t *Q;        /* [K*V]    Q_{kw} = sum_i t_{ikw} */
+    int64_t *T;        /* [K]      T_k = sum_w Q_{kw} */
+    stable_t *tab;     /* [I] (aliased when discounts coincide) */
+    int nmax;
+    int64_t stats[8];  /* last sweep: 0 keeps, 1 moved, 2 clamped cells, 3 forced-differ */
+} ostate;
+
+#define IDX3(s, i, w, k) (((size_t)(i) * (s)->V + (size_t)(w)) * (s)->K + (size_t)(k))
+
+void or_destroy(ostate *s) {
+    if (!s) return;
+    free(s->alpha); free(s->a); free(s->b);
+    free(s->group); free(s->doc); free(s->word); free(s->pos); free(s->doclen);
+    free(s->z); free(s->r); free(s->n); free(s->m); free(s->t);
+    free(s->M); free(s->Tt); free(s->Q); free(s->T);
+    if (s->tab) {
+        for (int i = 0; i < s->I; i++) {
+            int alias = 0;
+            for (int j = 0; j < i; j++) if (s->tab[j].v == s->tab[i].v) alias = 1;
+            if (!alias) free(s->tab[i].v);
+        }
+        free(s->tab);
+    }
+    free(s);
+}
+
+ostate *or_create(int I, int V, int K, const double *alpha_ik, double beta,
+                  const double *a, const double *b, uint64_t seed) {
+    if (I < 1 || V < 1 || K < 1 || !(beta > 0.0)) return NULL;
+    ostate *s = (ostate *)calloc(1, sizeof(ostate));
+    if (!s) return NULL;
+    s->I = I; s->V = V; s->K = K; s->beta = beta; s->seed = seed;
+    s->alpha = (double *)malloc(sizeof(double) * (size_t)I * K);
+    s->a = (double *)malloc(sizeof(double) * (size_t)I);
+    s->b = (double *)malloc(sizeof(double) * (size_t)I);
+    if (!s->alpha || !s->a || !s->b) { or_destroy(s); return NULL; }
+    memcpy(s->alpha, alpha_ik, sizeof(double) * (size_t)I * K);
+    memcpy(s->a, a, sizeof(double) * (size_t)I);
+    memcpy(s->b, b, sizeof(double) * (size_t)I);
+    return s;
+}
+
+/* recompute every derived sum from m and t (plain loops) */
+static void recompute_sums(const ostate *s, const int32_t *m, const int32_t *t,
+                           int64_t *M, int64_t *Tt, int64_t *Q, int64_t *T) {
+    int I = s->I, V = s->V, K = s->K;
+    memset(M, 0, sizeof(int64_t) * (size_t)I * K);
+    memset(Tt, 0, sizeof(int64_t) * (size_t)I * K);
+    memset(Q, 0, sizeof(int64_t) * (size_t)K * V);
+    memset(T, 0, sizeof(int64_t) * (size_t)K);
+    for (int i = 0; i < I; i++)
+        for (int w = 0; w < V; w++)
+            for (int k = 0; k < K; k++) {
+                size_t c = IDX3(s, i, w, k);
+                M[(size_t)i * K + k] += m[c];
+                Tt[(size_t)i * K + k] += t[c];
+                Q[(size_t)k * V + w] += t[c];
+                T[k] += t[c];
+            }
+}
+
+static int ensure_tables(ostate *s, int nmax) {
+    if (s->tab && s->nmax >= nmax) return 0;
+    if (s->tab) {
+        for (int i = 0; i < s->I; i++) {
+            int alias = 0;
+            for (int j = 0; j < i; j++) if (s->tab[j].v == s->tab[i].v) alias = 1;
+            if (!alias) free(s->tab[i].v);
+        }
+        free(s->tab);
+    }
+    s->tab = (stable_t *)calloc((size_t)s->I, sizeof(stable_t));
+    if (!s->tab) return -1;
+    for (int i = 0; i < s->I; i++) {
+        int j;
+        for (j = 0; j < i; j++) if (s->a[j] == s->a[i]) break;
+        if (j < i) { s->tab[i] = s->tab[j]; continue; }
+        if (stable_build(&s->tab[i], s->a[i], nmax) != 0) return -1;
+    }
+    s->nmax = nmax;
+    return 0;
+}
+
+/* t_init (optional, [I*V*K]) overrides the table counts derived from r. */
+int or_load(ostate *s, int64_t N, int32_t D, const int32_t *group, const int32_t *doc,
+            const int32_t *word, const int32_t *z_init, const uint8_t *r_init, const int32_t *t_init) {
+    int I = s->I, V = s->V, K = s->K;
+    if (N < 0 || D < 1) return -1;
+    for (int64_t p = 0; p < N; p++) {
+        if (group[p] < 0 || group[p] >= I || doc[p] < 0 || doc[p] >= D || word[p] < 0 || word[p] >= V) return -1;
+        if (z_init && (z_init[p] < 0 || z_init[p] >= K)) return -1;
+        if (r_init && r_init[p] > 1) return -1;
+    }
+    s->N = N; s->D = D;
+    size_t cells = (size_t)I * V * K;
+    s->group = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    s->doc = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    s->word = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    s->pos = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    s->z = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    s->r = (uint8_t *)malloc((size_t)(N + 1));
+    s->doclen = (int32_t *)calloc((size_t)D, sizeof(int32_t));
+    s->n = (int32_t *)calloc((size_t)D * K, sizeof(int32_t));
+    s->m = (int32_t *)calloc(cells, sizeof(int32_t));
+    s->t = (int32_t *)calloc(cells, sizeof(int32_t));
+    s->M = (int64_t *)calloc((size_t)I * K, sizeof(int64_t));
+    s->Tt = (int64_t *)calloc((size_t)I * K, sizeof(int64_t));
+    s->Q = (int64_t *)calloc((size_t)K * V, sizeof(int64_t));
+    s->T = (int64_t *)calloc((size_t)K, sizeof(int64_t));
+    int32_t *docgroup = (int32_t *)malloc(sizeof(int32_t) * (size_t)D);
+    if (!s->group || !s->doc || !s->word || !s->pos || !s->z || !s->r || !s->doclen || !s->n ||
+        !s->m || !s->t || !s->M || !s->Tt || !s->Q || !s->T || !docgroup) { free(docgroup); return -2; }
+    memcpy(s->group, group, sizeof(int32_t) * (size_t)N);
+    memcpy(s->doc, doc, sizeof(int32_t) * (size_t)N);
+    memcpy(s->word, word, sizeof(int32_t) * (size_t)N);
+    for (int32_t d = 0; d < D; d++) docgroup[d] = -1;
+    for (int64_t p = 0; p < N; p++) {
+        int32_t d = doc[p];
+        if (docgroup[d] >= 0 && docgroup[d] != group[p]) { free(docgroup); return -1; } /* doc spans groups */
+        docgroup[d] = group[p];
+        s->pos[p] = s->doclen[d]++;
+    }
+    free(docgroup);
+    /* z: given, or Philox(seed; tok, 0xFFFFFFFF) -> floor(x0 K / 2^32) */
+    for (int64_t p = 0; p < N; p++) {
+        if (z_init) s->z[p] = z_init[p];
+        else {
+            uint32_t x[4];
+            rng_token(s->seed, (uint32_t)p, 0xFFFFFFFFu, x);
+            s->z[p] = (int32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
+        }
+    }
+    /* counts from z ("Initialize counting variables ... from z") */
+    for (int64_t p = 0; p < N; p++) {
+        s->n[(size_t)doc[p] * K + s->z[p]]++;
+        s->m[IDX3(s, group[p], word[p], s->z[p])]++;
+    }
+    /* r: given, or 1 for the first token of each (i,k,w) cell (reading c12) */
+    for (int64_t p = 0; p < N; p++) {
+        size_t c = IDX3(s, group[p], word[p], s->z[p]);
+        if (r_init) s->r[p] = r_init[p];
+        else s->r[p] = (s->t[c] == 0) ? 1 : 0;
+        s->t[c] += s->r[p];
+    }
+    if (t_init) memcpy(s->t, t_init, sizeof(int32_t) * cells);
+    for (size_t c = 0; c < cells; c++) {
+        if (s->t[c] < 0 || s->t[c] > s->m[c] || ((s->m[c] > 0) != (s->t[c] > 0))) return -1;
+    }
+    recompute_sums(s, s->m, s->t, s->M, s->Tt, s->Q, s->T);
+    int32_t mmax = 0;
+    for (size_t c = 0; c < cells; c++) if (s->m[c] > mmax) mmax = s->m[c];
+    /* every reachable m_{ikw} is bounded by count(i,w); the m of a cell never exceeds it */
+    {
+        int32_t *cnt = (int32_t *)calloc((size_t)I * V, sizeof(int32_t));
+        if (!cnt) return -2;
+        for (int64_t p = 0; p < N; p++) cnt[(size_t)group[p] * V + word[p]]++;
+        for (size_t c = 0; c < (size_t)I * V; c++) if (cnt[c] > mmax) mmax = cnt[c];
+        free(cnt);
+    }
+    if (ensure_tables(s, mmax + 1) != 0) return -2;
+    s->sweep = 0;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* the conditional, Eqs. SPDP-sampling-w-z-r0 / -r1      */
+/* ------------------------------------------------------------------ */
+/* Log weights of the 2K slots for token p against the counts given, with the
+ * token's own contribution removed (Alg.1 lines 3-10): its old
+ * topic k0 loses one customer, and one table when r_rem = 1.
+ * Slot order (Alg.4): j = 2k <-> (k, r=1), j = 2k+1 <-> (k, r=0). */
+static void log_weights(const ostate *s, int64_t p, int r_rem,
+                        const int32_t *n, const int32_t *m, const int32_t *t,
+                        const int64_t *M, const int64_t *Tt, const int64_t *Q, const int64_t *T,
+                        double *lw) {
+    int K = s->K, V = s->V;
+    int i = s->group[p], w = s->word[p], d = s->doc[p], k0 = s->z[p];
+    double a = s->a[i], b = s->b[i], beta = s->beta;
+    const stable_t *S = &s->tab[i];
+    for (int k = 0; k < K; k++) {
+        int own = (k == k0);
+        double n_k = (double)n[(size_t)d * K + k] - own;
+        int64_t m_k = m[IDX3(s, i, w, k)] - own;
+        int64_t t_k = t[IDX3(s, i, w, k)] - own * r_rem;
+        double M_k = (double)M[(size_t)i * K + k] - own;
+        double Tt_k = (double)Tt[(size_t)i * K + k] - own * r_rem;
+        double Q_k = (double)Q[(size_t)k * V + w] - own * r_rem;
+        double T_k = (double)T[k] - own * r_rem;
+        double lS = stable_get(S, (int)m_k, (int)t_k);
+        double base = log(s->alpha[(size_t)i * K + k] + n_k) - log(b + M_k);
+        /* r = 0: (alpha+n)/(b+M) * (m-t+1)/(m+1) * S^{m+1}_t / S^m_t */
+        double l0 = base + log((double)(m_k - t_k + 1)) - log((double)(m_k + 1))
+                    + stable_get(S, (int)m_k + 1, (int)t_k) - lS;
+        /* r = 1: (alpha+n)(b + a T_t)/(b+M) * (t+1)/(m+1) * (beta+Q)/(V beta + T) * S^{m+1}_{t+1} / S^m_t */
+        double l1 = base + log(b + a * Tt_k) + log((double)(t_k + 1)) - log((double)(m_k + 1))
+                    + log(beta + Q_k) - log((double)V * beta + T_k)
+                    + stable_get(S, (int)m_k + 1, (int)t_k + 1) - lS;
+        lw[2 * k] = l1;
+        lw[2 * k + 1] = l0;
+    }
+}
+
+/* Normalised probabilities by max-shifted exponentiation in fp64 (reading c9). */
+static void normalise(int n, const double *lw, double *prob) {
+    double mx = -INFINITY;
+    for (int j = 0; j < n; j++) if (lw[j] > mx) mx = lw[j];
+    double tot = 0.0;
+    for (int j = 0; j < n; j++) { prob[j] = (lw[j] == -INFINITY) ? 0.0 : exp(lw[j] - mx); tot += prob[j]; }
+    for (int j = 0; j < n; j++) prob[j] /= tot;
+}
+
+/* j* = min{ j : cdf_j > u }; if rounding leaves none, the last j with p_j > 0
+ * (reading c10).  *margin = distance of u to the nearest edge of slot j*. */
+static int draw_slot(int n, const double *prob, double u, double *margin) {
+    double c = 0.0, prev = 0.0;
+    for (int j = 0; j < n; j++) {
+        prev = c;
+        c += prob[j];
+        if (c > u && prob[j] > 0.0) {
+            if (margin) { double m1 = u - prev, m2 = c - u; *margin = m1 < m2 ? m1 : m2; }
+            return j;
+        }
+    }
+    for (int j = n - 1; j >= 0; j--) if (prob[j] > 0.0) { if (margin) *margin = 0.0; return j; }
+    return -1;
+}
+
+/* Removal draw r ~ Bernoulli(t/m) (Alg.1 line 3): exact integer test
+ * x0 * m < t * 2^32 (reading c7).  keep: r = 1 with t = 1 < m (reading c5). */
+static int removal(uint32_t x0, int64_t m_c, int64_t t_c, int *keep) {
+    int r = ((uint64_t)x0 * (uint64_t)m_c) < ((uint64_t)t_c << 32);
+    *keep = (r && t_c == 1 && m_c > 1);
+    return r;
+}
+
+/* ------------------------------------------------------------------ */
+/* Mode S: Algorithm 1 as printed + keep rule            */
+/* ------------------------------------------------------------------ */
+int or_sweep_seq(ostate *s, int64_t max_tokens) {
+    int K = s->K, V = s->V;
+    double *lw = (double *)malloc(sizeof(double) * 2 * (size_t)K);
+    double *prob = (double *)malloc(sizeof(double) * 2 * (size_t)K);
+    if (!lw || !prob) { free(lw); free(prob); return -2; }
+    memset(s->stats, 0, sizeof(s->stats));
+    int64_t lim = (max_tokens >= 0 && max_tokens < s->N) ? max_tokens : s->N;
+    for (int64_t p = 0; p < lim; p++) {                     /* ForAll w_{i,d,l} */
+        int i = s->group[p], w = s->word[p], d = s->doc[p], k = s->z[p];   /* line 2 */
+        size_t c = IDX3(s, i, w, k);
+        uint32_t x[4];
+        rng_token(s->seed, (uint32_t)p, s->sweep, x);
+        int keep, r = removal(x[0], s->m[c], s->t[c], &keep);             /* line 3 */
+        if (keep) { s->r[p] = 1; s->stats[0]++; continue; }
+        log_weights(s, p, r, s->n, s->m, s->t, s->M, s->Tt, s->Q, s->T, lw); /* lines 11-16 (removal folded in) */
+        /* lines 4-10: decrement n, m (and t, q when r = 1) */
+        s->n[(size_t)d * K + k]--; s->m[c]--; s->M[(size_t)i * K + k]--;
+        if (r) { s->t[c]--; s->Tt[(size_t)i * K + k]--; s->Q[(size_t)k * V + w]--; s->T[k]--; }
+        normalise(2 * K, lw, prob);
+        int j = draw_slot(2 * K, prob, u53(x), NULL);                     /* line 17 */
+        int kn = j / 2, rn = (j % 2 == 0);
+        size_t cn = IDX3(s, i, w, kn);
+        s->n[(size_t)d * K + kn]++; s->m[cn]++; s->M[(size_t)i * K + kn]++;   /* line 18 */
+        if (rn) { s->t[cn]++; s->Tt[(size_t)i * K + kn]++; s->Q[(size_t)kn * V + w]++; s->T[kn]++; } /* 19-22 */
+        if (kn != k) s->stats[1]++;
+        s->z[p] = kn; s->r[p] = (uint8_t)rn;
+    }
+    s->sweep++;
+    free(lw); free(prob);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* document partition over G shards (reading: SURVEY §8(e))            */
+/* ------------------------------------------------------------------ */
+/* Docs are ordered by the Philox word x0 of (doc, 0xFFFFFFFE) (ties by id),
+ * then split contiguously by cumulative token count:
+ * shard = floor(tokens_before * G / N). */
+typedef struct { uint32_t key; int32_t doc; } dkey_t;
+static int dkey_cmp(const void *x, const void *y) {
+    const dkey_t *p = (const dkey_t *)x, *q = (const dkey_t *)y;
+    if (p->key != q->key) return p->key < q->key ? -1 : 1;
+    return p->doc < q->doc ? -1 : (p->doc > q->doc);
+}
+void or_partition(const ostate *s, int G, int32_t *shard_of_doc) {
+    dkey_t *v = (dkey_t *)malloc(sizeof(dkey_t) * (size_t)s->D);
+    for (int32_t d = 0; d < s->D; d++) {
+        uint32_t x[4];
+        rng_token(s->seed, (uint32_t)d, 0xFFFFFFFEu, x);
+        v[d].key = x[0]; v[d].doc = d;
+    }
+    qsort(v, (size_t)s->D, sizeof(dkey_t), dkey_cmp);
+    int64_t before = 0;
+    for (int32_t j = 0; j < s->D; j++) {
+        int32_t d = v[j].doc;
+        int64_t g = (s->N > 0) ? (before * (int64_t)G) / s->N : 0;
+        if (g >= G) g = G - 1;
+        shard_of_doc[d] = (int32_t)g;
+        before += s->doclen[d];
+    }
+    free(v);
+}
+
+/* clamp t into [min(1,m), m] (reading c14) */
+static int64_t clamp_cells(size_t cells, const int32_t *m, int32_t *t) {
+    int64_t changed = 0;
+    for (size_t c = 0; c < cells; c++) {
+        int32_t v = t[c];
+        if (v > m[c]) v = m[c];
+        if (m[c] > 0 && v < 1) v = 1;
+        if (m[c] == 0) v = 0;
+        if (v != t[c]) { t[c] = v; changed++; }
+    }
+    return changed;
+}
+
+/* ------------------------------------------------------------------ */
+/* Mode P: wave snapshots, G shards, merge (reading c13-c15)           */
+/* ------------------------------------------------------------------ */
+/* W >= 1: wave(token) = l mod W (l = in-doc position).
+ * W == 0: every token is its own wave, in canonical order (= mode S).
+ * force_zr (optional, [N], -1 = none): replace the drawn (z | r<<15) of a
+ * token that is not kept (lock-step replay of another sampler's draws).
+ * margin (optional, [N]): distance of u to the edge of the drawn slot.
+ * max_tokens >= 0 limits the sweep to the first max_tokens tokens of each
+ * shard's canonical order (timing samples only). */
+int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margin, int64_t max_tokens) {
+    int I = s->I, V = s->V, K = s->K;
+    int64_t N = s->N;
+    size_t cells = (size_t)I * V * K;
+    if (W < 0 || G < 1) return -1;
+    memset(s->stats, 0, sizeof(s->stats));
+    int32_t *shard = (int32_t *)malloc(sizeof(int32_t) * (size_t)s->D);
+    int32_t *S0m = (int32_t *)malloc(sizeof(int32_t) * cells), *S0t = (int32_t *)malloc(sizeof(int32_t) * cells);
+    int32_t *Lm = (int32_t *)malloc(sizeof(int32_t) * cells), *Lt = (int32_t *)malloc(sizeof(int32_t) * cells);
+    int64_t *Dm = (int64_t *)calloc(cells, sizeof(int64_t)), *Dt = (int64_t *)calloc(cells, sizeof(int64_t));
+    int64_t *M = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K), *Tt = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K);
+    int64_t *Q = (int64_t *)malloc(sizeof(int64_t) * (size_t)K * V), *T = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
+    int32_t *newz = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    int8_t *newr = (int8_t *)malloc((size_t)(N + 1)), *rrem = (int8_t *)malloc((size_t)(N + 1)), *kept = (int8_t *)malloc((size_t)(N + 1));
+    int64_t *inwave = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N + 1));
+    double *lw = (double *)malloc(sizeof(double) * 2 * (size_t)K), *prob = (double *)malloc(sizeof(double) * 2 * (size_t)K);
+    int rc = -2;
+    if (!shard || !S0m || !S0t || !Lm || !Lt || !Dm || !Dt || !M || !Tt || !Q || !T || !newz || !newr || !rrem ||
+        !kept || !inwave || !lw || !prob) goto out;
+    or_partition(s, G, shard);
+    memcpy(S0m, s->m, sizeof(int32_t) * cells);
+    memcpy(S0t, s->t, sizeof(int32_t) * cells);
+    int32_t maxlen = 0;
+    for (int32_t d = 0; d < s->D; d++) if (s->doclen[d] > maxlen) maxlen = s->doclen[d];
+    int64_t nwaves = (W == 0) ? N : (W < maxlen ? W : maxlen);
+    for (int g = 0; g < G; g++) {
+        /* shard-local replica of the sweep-start global state (Alg.3) */
+        memcpy(Lm, S0m, sizeof(int32_t) * cells);
+        memcpy(Lt, S0t, sizeof(int32_t) * cells);
+        recompute_sums(s, Lm, Lt, M, Tt, Q, T);
+        int64_t seen = 0;
+        for (int64_t wave = 0; wave < nwaves; wave++) {
+            /* tokens of this shard in this wave, canonical order */
+            int64_t cnt = 0;
+            if (W == 0) {
+                if (shard[s->doc[wave]] == g) inwave[cnt++] = wave;
+            } else {
+                for (int64_t p = 0; p < N; p++)
+                    if (shard[s->doc[p]] == g && s->pos[p] % W == wave) inwave[cnt++] = p;
+            }
+            /* (1) every token decides against the wave-start snapshot */
+            for (int64_t q = 0; q < cnt; q++) {
+                int64_t p = inwave[q];
+                if (max_tokens >= 0 && seen >= max_tokens) { kept[p] = 2; continue; } /* not sampled */
+                seen++;
+                int i = s->group[p], w = s->word[p], k0 = s->z[p];
+                size_t c = IDX3(s, i, w, k0);
+                uint32_t x[4];
+                rng_token(s->seed, (uint32_t)p, s->sweep, x);
+                int keep, r = removal(x[0], Lm[c], Lt[c], &keep);
+                rrem[p] = (int8_t)r;
+                kept[p] = (int8_t)keep;
+                if (keep) { newz[p] = k0; newr[p] = 1; continue; }
+                log_weights(s, p, r, s->n, Lm, Lt, M, Tt, Q, T, lw);
+                normalise(2 * K, lw, prob);
+                int j = draw_slot(2 * K, prob, u53(x), margin ? &margin[p] : NULL);
+                newz[p] = j / 2; newr[p] = (j % 2 == 0);
+                if (force_zr && force_zr[p] >= 0) {
+                    int fz = force_zr[p] & 0x7FFF, fr = (force_zr[p] >> 15) & 1;
+                    if (fz != newz[p] || fr != newr[p]) s->stats[3]++;
+                    newz[p] = fz; newr[p] = (int8_t)fr;
+                }
+            }
+            /* (2) apply all deltas of the wave, clamp, recompute sums */
+            for (int64_t q = 0; q < cnt; q++) {
+                int64_t p = inwave[q];
+                if (kept[p] == 2) continue;
+                if (kept[p]) { s->r[p] = 1; s->stats[0]++; continue; }
+                int i = s->group[p], w = s->word[p], d = s->doc[p], k0 = s->z[p], kn = newz[p];
+                size_t c0 = IDX3(s, i, w, k0), cn = IDX3(s, i, w, kn);
+                s->n[(size_t)d * K + k0]--; s->n[(size_t)d * K + kn]++;
+                Lm[c0]--; Lm[cn]++;
+                Lt[c0] -= rrem[p]; Lt[cn] += newr[p];
+                if (kn != k0) s->stats[1]++;
+                s->z[p] = kn; s->r[p] = (uint8_t)newr[p];
+            }
+            if (cnt > 0) {
+                s->stats[2] += clamp_cells(cells, Lm, Lt);
+                recompute_sums(s, Lm, Lt, M, Tt, Q, T);
+            }
+        }
+        /* D_g = L_g - S0 */
+        for (size_t c = 0; c < cells; c++) { Dm[c] += Lm[c] - S0m[c]; Dt[c] += Lt[c] - S0t[c]; }
+    }
+    /* merge (Alg.3; reading c14-c15): S1 = clamp(S0 + sum_g D_g) */
+    for (size_t c = 0; c < cells; c++) {
+        s->m[c] = (int32_t)(S0m[c] + Dm[c]);
+        s->t[c] = (int32_t)(S0t[c] + Dt[c]);
+    }
+    s->stats[2] += clamp_cells(cells, s->m, s->t);
+    recompute_sums(s, s->m, s->t, s->M, s->Tt, s->Q, s->T);
+    s->sweep++;
+    rc = 0;
+out:
+    free(shard); free(S0m); free(S0t); free(Lm); free(Lt); free(Dm); free(Dt);
+    free(M); free(Tt); free(Q); free(T); free(newz); free(newr); free(rrem); free(kept); free(inwave);
+    free(lw); free(prob);
+    return rc;
+}
+
+/* ------------------------------------------------------------------ */
+/* queries                                                             */
+/* ------------------------------------------------------------------ */
+void or_get(const ostate *s, int32_t *z, uint8_t *r, int32_t *n, int32_t *m, int32_t *t, int32_t *Q) {
+    size_t cells = (size_t)s->I * s->V * s->K;
+    if (z) memcpy(z, s->z, sizeof(int32_t) * (size_t)s->N);
+    if (r) memcpy(r, s->r, (size_t)s->N);
+    if (n) memcpy(n, s->n, sizeof(int32_t) * (size_t)s->D * s->K);
+    if (m) memcpy(m, s->m, sizeof(int32_t) * cells);
+    if (t) memcpy(t, s->t, sizeof(int32_t) * cells);
+    if (Q) for (size_t j = 0; j < (size_t)s->K * s->V; j++) Q[j] = (int32_t)s->Q[j];
+}
+uint32_t or_sweep_index(const ostate *s) { return s->sweep; }
+void or_set_sweep_index(ostate *s, uint32_t sweep) { s->sweep = sweep; }
+void or_stats(const ostate *s, int64_t *out) { memcpy(out, s->stats, sizeof(s->stats)); }
+
+/* Normalised 2K-slot conditional of token p at the current state with the
+ * given removal indicator.  Returns -1 if that removal is impossible
+ * (r_rem = 0 with t = m, or r_rem = 1 with t = 1 < m: the keep case). */
+int or_conditional(const ostate *s, int64_t p, int r_rem, double *prob) {
+    size_t c = IDX3(s, s->group[p], s->word[p], s->z[p]);
+    int64_t m = s->m[c], t = s->t[c];
+    if (r_rem == 0 && t == m) return -1;
+    if (r_rem == 1 && t == 1 && m > 1) return -1;
+    double *lw = (double *)malloc(sizeof(double) * 2 * (size_t)s->K);
+    if (!lw) return -2;
+    log_weights(s, p, r_rem, s->n, s->m, s->t, s->M, s->Tt, s->Q, s->T, lw);
+    normalise(2 * s->K, lw, prob);
+    free(lw);
+    return 0;
+}
+
+/* The decision token p would take in sweep `sweep` against the current state
+ * (as wave-snapshot): info = {r_rem, keep, new z, new r}, *u = uniform,
+ * prob = conditional (point mass on slot 2 k0 when kept), *margin as above. */
+int or_debug_token(const ostate *s, int64_t p, uint32_t sweep, double *prob, int32_t *info, double *u, double *margin) {
+    int K = s->K;
+    size_t c = IDX3(s, s->group[p], s->word[p], s->z[p]);
+    uint32_t x[4];
+    rng_token(s->seed, (uint32_t)p, sweep, x);
+    int keep, r = removal(x[0], s->m[c], s->t[c], &keep);
+    info[0] = r; info[1] = keep;
+    *u = u53(x);
+    if (keep) {
+        for (int j = 0; j < 2 * K; j++) prob[j] = 0.0;
+        prob[2 * s->z[p]] = 1.0;
+        info[2] = s->z[p]; info[3] = 1; *margin = 1.0;
+        return 0;
+    }
+    int rc = or_conditional(s, p, r, prob);
+    if (rc) return rc;
+    int j = draw_slot(2 * K, prob, *u, margin);
+    info[2] = j / 2; info[3] = (j % 2 == 0);
+    return 0;
+}
+
+/* Training perplexity, P:1978-2007 with theta~, phi0~ and
+ * phi^i~ (reading c16): exp(-sum_tok log sum_k theta_dk phi^i_kw / N). */
+double or_perplexity(const ostate *s) {
+    int K = s->K, V = s->V;
+    double ll = 0.0;
+    for (int64_t p = 0; p < s->N; p++) {
+        int i = s->group[p], w = s->word[p], d = s->doc[p];
+        double a = s->a[i], b = s->b[i];
+        double asum = 0.0;
+        for (int k = 0; k < K; k++) asum += s->alpha[(size_t)i * K + k];
+        double pw = 0.0;
+        for (int k = 0; k < K; k++) {
+            double theta = ((double)s->n[(size_t)d * K + k] + s->alpha[(size_t)i * K + k]) / ((double)s->doclen[d] + asum);
+            double phi0 = (s->beta + (double)s->Q[(size_t)k * V + w]) / ((double)V * s->beta + (double)s->T[k]);
+            double Mk = (double)s->M[(size_t)i * K + k], Tk = (double)s->Tt[(size_t)i * K + k];
+            size_t c = IDX3(s, i, w, k);
+            double phii = ((double)s->m[c] - a * (double)s->t[c]) / (b + Mk) + (b + a * Tk) / (b + Mk) * phi0;
+            pw += theta * phii;
+        }
+        ll += log(pw);
+    }
+    return exp(-ll / (double)s->N);
+}
+
+/* log p(W, Z, T | alpha, beta, a, b): the blocked-Gibbs joint
+ * with identity P, summed over the prod C(m,t) seatings R per T
+ * (Eq. SPDP-table-to-head):
+ *   sum_{docs} [lnG(sum alpha) - lnG(sum alpha + L_d) + sum_k lnG(alpha+n_dk) - lnG(alpha)]
+ * + sum_{i,k} [ln (b|a)_{t_ik.} - ln (b)_{m_ik.}] + sum_{i,k,w} ln S^{m_ikw}_{t_ikw, a}
+ * + sum_k [lnG(V beta) - lnG(V beta + T_k) + sum_w lnG(beta + Q_kw) - lnG(beta)]. */
+double or_log_joint(const ostate *s) {
+    int I = s->I, V = s->V, K = s->K;
+    double lp = 0.0;
+    int32_t *dg = (int32_t *)malloc(sizeof(int32_t) * (size_t)s->D);
+    for (int32_t d = 0; d < s->D; d++) dg[d] = -1;
+    for (int64_t p = 0; p < s->N; p++) dg[s->doc[p]] = s->group[p];
+    for (int32_t d = 0; d < s->D; d++) {
+        if (dg[d] < 0) continue;
+        int i = dg[d];
+        double asum = 0.0;
+        for (int k = 0; k < K; k++) asum += s->alpha[(size_t)i * K + k];
+        lp += lgamma(asum) - lgamma(asum + (double)s->doclen[d]);
+        for (int k = 0; k < K; k++) {
+            double al = s->alpha[(size_t)i * K + k];
+            lp += lgamma(al + (double)s->n[(size_t)d * K + k]) - lgamma(al);
+        }
+    }
+    free(dg);
+    for (int i = 0; i < I; i++)
+        for (int k = 0; k < K; k++)
+            lp += log_poch(s->b[i], s->a[i], s->Tt[(size_t)i * K + k]) - log_poch(s->b[i], 1.0, s->M[(size_t)i * K + k]);
+    for (int i = 0; i < I; i++)
+        for (int w = 0; w < V; w++)
+            for (int k = 0; k < K; k++) {
+                size_t c = IDX3(s, i, w, k);
+                lp += stable_get(&s->tab[i], s->m[c], s->t[c]);
+            }
+    for (int k = 0; k < K; k++) {
+        lp += lgamma((double)V * s->beta) - lgamma((double)V * s->beta + (double)s->T[k]);
+        for (int w = 0; w < V; w++) lp += lgamma(s->beta + (double)s->Q[(size_t)k * V + w]) - lgamma(s->beta);
+    }
+    return lp;
+}
+
+/* Count invariants (north_star (4); SURVEY §8(c) "counts").  0 = all hold. */
+int or_check_invariants(const ostate *s) {
+    int I = s->I, V = s->V, K = s->K;
+    size_t cells = (size_t)I * V * K;
+    int rc = 0;
+    int32_t *n = (int32_t *)calloc((size_t)s->D * K, sizeof(int32_t));
+    int32_t *m = (int32_t *)calloc(cells, sizeof(int32_t));
+    int64_t *M = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K), *Tt = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K);
+    int64_t *Q = (int64_t *)malloc(sizeof(int64_t) * (size_t)K * V), *T = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
+    if (!n || !m || !M || !Tt || !Q || !T) { rc = -2; goto out; }
+    for (int64_t p = 0; p < s->N; p++) {
+        n[(size_t)s->doc[p] * K + s->z[p]]++;
+        m[IDX3(s, s->group[p], s->word[p], s->z[p])]++;
+    }
+    if (memcmp(n, s->n, sizeof(int32_t) * (size_t)s->D * K)) { rc = 1; goto out; }
+    if (memcmp(m, s->m, sizeof(int32_t) * cells)) { rc = 2; goto out; }
+    int64_t sm = 0;
+    for (size_t c = 0; c < cells; c++) {
+        sm += s->m[c];
+        if (s->t[c] < 0 || s->t[c] > s->m[c]) { rc = 3; goto out; }
+        if ((s->t[c] > 0) != (s->m[c] > 0)) { rc = 4; goto out; }
+    }
+    if (sm != s->N) { rc = 5; goto out; }
+    recompute_sums(s, s->m, s->t, M, Tt, Q, T);
+    if (memcmp(M, s->M, sizeof(int64_t) * (size_t)I * K) || memcmp(Tt, s->Tt, sizeof(int64_t) * (size_t)I * K) ||
+        memcmp(Q, s->Q, sizeof(int64_t) * (size_t)K * V) || memcmp(T, s->T, sizeof(int64_t) * (size_t)K)) { rc = 6; goto out; }
+out:
+    free(n); free(m); free(M); free(Tt); free(Q); free(T);
+    return rc;
+}
+
+/* p(w | doc d) = sum_k theta~_dk phi^i~_kw of the perplexity above (for the
+ * normalisation pin: sum_w p(w|d) = 1). */
+double or_word_prob(const ostate *s, int32_t d, int32_t w) {
+    int K = s->K, V = s->V;
+    int i = -1;
+    for (int64_t p = 0; p < s->N; p++) if (s->doc[p] == d) { i = s->group[p]; break; }
+    if (i < 0) return NAN;
+    double a = s->a[i], b = s->b[i], asum = 0.0, pw = 0.0;
+    for (int k = 0; k < K; k++) asum += s->alpha[(size_t)i * K + k];
+    for (int k = 0; k < K; k++) {
+        double theta = ((double)s->n[(size_t)d * K + k] + s->alpha[(size_t)i * K + k]) / ((double)s->doclen[d] + asum);
+        double phi0 = (s->beta + (double)s->Q[(size_t)k * V + w]) / ((double)V * s->beta + (double)s->T[k]);
+        double Mk = (double)s->M[(size_t)i * K + k], Tk = (double)s->Tt[(size_t)i * K + k];
+        size_t c = IDX3(s, i, w, k);
+        pw += theta * (((double)s->m[c] - a * (double)s->t[c]) / (b + Mk) + (b + a * Tk) / (b + Mk) * phi0);
+    }
+    return pw;
+}
+
+/* Run `nsweeps` sweeps (waves < 0: mode S; else mode P with `waves`, 1 shard)
+ * and record after each sweep a code of the whole (z, t) state:
+ * code = sum_p z_p K^p + K^N * sum_c t_c (tbase)^c over all I*V*K cells.
+ * For tiny corpora only (the caller guarantees no int64 overflow). */
+int or_chain_codes(ostate *s, int64_t nsweeps, int waves, int tbase, int64_t *codes) {
+    size_t cells = (size_t)s->I * s->V * s->K;
+    for (int64_t it = 0; it < nsweeps; it++) {
+        int rc = (waves < 0) ? or_sweep_seq(s, -1) : or_sweep_par(s, waves, 1, NULL, NULL, -1);
+        if (rc) return rc;
+        int64_t code = 0, mul = 1;
+        for (int64_t p = 0; p < s->N; p++) { code += mul * s->z[p]; mul *= s->K; }
+        int64_t tc = 0, tm = 1;
+        for (size_t c = 0; c < cells; c++) { tc += tm * s->t[c]; tm *= tbase; }
+        codes[it] = code + mul * tc;
+    }
+    return 0;
+}

@@ -1,0 +1,127 @@
+"""Seeded synthetic corpora shaped like the paper's multi-group collections.
+
+INPUT GENERATION ONLY: this module holds none of the sampler's arithmetic.
+It is the one module both the oracle tests and the CUDA path may share
+(SURVEY.md §8(d) "Synthetic inputs").  The corpus is drawn from the SPDP
+generative process with identity P (§2.3.4) realised
+with the Pitman–Yor seating rule; see synth/gen.c.
+
+Configs C1..C5 are BASELINE.json's `configs`, with the per-config recipe of
+SURVEY.md §8(d) (groups x docs per group, Poisson mean length, V, K_gen, K,
+generator seed).  Sampler hyper-parameters are the paper's
+alpha = beta = 0.1, a = 0.7, b = 100 (§4.1).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gen.c")
+_LIB = os.path.join(_HERE, "libsynth.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", _SRC, "-o", _LIB, "-lm"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.synth_num_tokens.restype = ctypes.c_int64
+        lib.synth_num_tokens.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint64]
+        lib.synth_spdp_corpus.restype = ctypes.c_int
+        lib.synth_spdp_corpus.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_uint64] + [ctypes.c_void_p] * 4
+        _lib = lib
+    return _lib
+
+
+@dataclass(frozen=True)
+class CorpusConfig:
+    name: str
+    groups: int            # I
+    docs_per_group: int    # D_i
+    mean_len: float        # Poisson lambda of document length
+    vocab: int             # V
+    k_gen: int             # topics of the generating process
+    k: int                 # topics of the sampler
+    gen_seed: int
+    # sampler settings
+    alpha: float = 0.1
+    beta: float = 0.1
+    discount: float = 0.7
+    concentration: float = 100.0
+    seed: int = 7
+    sweeps: int = 20
+    # generator hyper-parameters
+    alpha_gen: float = 0.1
+    beta_gen: float = 0.1
+
+    def with_k(self, k: int) -> "CorpusConfig":
+        return replace(self, k=k, name=f"{self.name}_K{k}")
+
+
+CONFIGS = {
+    "C1": CorpusConfig("C1", 2, 100, 100.0, 1_000, 10, 10, 101, sweeps=20),
+    "C2": CorpusConfig("C2", 3, 3_000, 111.0, 10_000, 50, 50, 102, sweeps=20),
+    "C3": CorpusConfig("C3", 4, 20_000, 125.0, 30_000, 100, 100, 103, sweeps=20),
+    "C4": CorpusConfig("C4", 4, 10_000, 125.0, 30_000, 100, 100, 104, sweeps=10),
+    "C5": CorpusConfig("C5", 16, 200_000, 62.5, 100_000, 200, 200, 105, sweeps=10),
+}
+
+
+@dataclass
+class Corpus:
+    group: np.ndarray   # int32 [N]
+    doc: np.ndarray     # int32 [N], global doc ids in [0, num_docs)
+    word: np.ndarray    # int32 [N]
+    z_gen: np.ndarray   # int32 [N], generating topic (not used by the sampler)
+    num_groups: int
+    num_docs: int
+    vocab: int
+
+    @property
+    def num_tokens(self) -> int:
+        return int(self.word.shape[0])
+
+
+def generate(groups: int, docs_per_group: int, mean_len: float, vocab: int, k_gen: int,
+             seed: int, alpha_gen: float = 0.1, beta_gen: float = 0.1,
+             discount: float = 0.7, concentration: float = 100.0) -> Corpus:
+    lib = _load()
+    n = lib.synth_num_tokens(groups, docs_per_group, mean_len, seed)
+    if n < 0:
+        raise MemoryError("synth_num_tokens failed")
+    g = np.empty(n, np.int32); d = np.empty(n, np.int32); w = np.empty(n, np.int32); z = np.empty(n, np.int32)
+    rc = lib.synth_spdp_corpus(groups, docs_per_group, mean_len, vocab, k_gen, alpha_gen, beta_gen,
+                               discount, concentration, seed,
+                               g.ctypes.data, d.ctypes.data, w.ctypes.data, z.ctypes.data)
+    if rc != 0:
+        raise MemoryError("synth_spdp_corpus failed")
+    return Corpus(g, d, w, z, groups, groups * docs_per_group, vocab)
+
+
+def corpus_for(cfg: CorpusConfig) -> Corpus:
+    return generate(cfg.groups, cfg.docs_per_group, cfg.mean_len, cfg.vocab, cfg.k_gen, cfg.gen_seed,
+                    cfg.alpha_gen, cfg.beta_gen, cfg.discount, cfg.concentration)
+
+
+def tiny_corpus(groups: int, docs: list[list[int]], doc_group: list[int], vocab: int) -> Corpus:
+    """Hand-written corpus: docs[d] = list of word ids, doc_group[d] = its group."""
+    g, d, w = [], [], []
+    for di, words in enumerate(docs):
+        for x in words:
+            g.append(doc_group[di]); d.append(di); w.append(x)
+    a = lambda v: np.asarray(v, np.int32)
+    return Corpus(a(g), a(d), a(w), np.zeros(len(w), np.int32), groups, len(docs), vocab)
