@@ -1,0 +1,194 @@
+/*
+ * spdp.h — C ABI of the B200-native SPDP Gibbs sweep (libspdp.so).
+ *
+ * The library samples the collapsed blocked-Gibbs chain of the Shadow
+ * Poisson–Dirichlet Process topic model with identity transformation
+ * matrices (§3.4), i.e. Algorithm 1 "SPDP Full Gibbs
+ * Sampling" with the conditionals of
+ * Eq. SPDP-sampling-w-z-r0 and
+ * Eq. SPDP-sampling-w-z-r1, parallelised the way §3.3
+ * describes ("minimum local copy", PAPER.md:2289-2299
+ * word-order rearrangement, PAPER.md:2370-2386 document division over
+ * devices, Alg.3/Alg.4) under the deterministic
+ * wave-snapshot reading of DESIGN.md §3 (reading c13).
+ *
+ * Problem statement (§2.3.4):
+ * N tokens, each a triple (group i, document d, word w); K topics; the
+ * Dirichlet alpha on document-topic proportions; the Dirichlet beta on the
+ * shared base phi0 (printed gamma_v in Eq. r1); the PDP discount a_i and
+ * concentration b_i per group.
+ *
+ * Conventions
+ *   - Every function returns spdp_status (0 = SPDP_OK).  Nothing aborts; the
+ *     message of the last failing call is spdp_last_error(ctx).
+ *   - All pointer arguments are HOST pointers owned by the caller.  Inputs are
+ *     copied during the call; outputs are caller-allocated and written before
+ *     the call returns.  The context owns all device memory and the NCCL
+ *     communicator.
+ *   - Call order: spdp_create -> spdp_load_corpus -> {spdp_sweep, spdp_counts,
+ *     spdp_loglik, spdp_set_state, spdp_debug_probs}* -> spdp_destroy.
+ *     Anything else returns SPDP_ESTATE.
+ *   - A context is not thread-safe.  Calls are synchronous with respect to
+ *     the host (they return after the work on the context's stream is done).
+ *   - Determinism: outputs are bit-identical for identical (config, corpus,
+ *     initial state, number of sweeps, world_size).  Different world sizes give
+ *     different (equally valid) chains; the oracle reproduces each.
+ *   - Multi-GPU: one process per GPU.  Every rank passes the whole corpus and
+ *     keeps its document shard.  spdp_sweep, spdp_counts and spdp_loglik are
+ *     collective over the world.
+ */
+#ifndef SPDP_H
+#define SPDP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SPDP_OK = 0,
+    SPDP_EINVAL = -1,      /* invalid argument (ranges, shapes, hyper-parameters) */
+    SPDP_ENOMEM = -2,      /* host or device allocation failed */
+    SPDP_ECUDA = -3,       /* CUDA runtime error or no device; context is poisoned */
+    SPDP_ENCCL = -4,       /* NCCL unavailable or failed */
+    SPDP_ESTATE = -5,      /* wrong call order, or context poisoned by an earlier fault */
+    SPDP_ETABLE = -6,      /* Stirling-ratio table would exceed its size limit */
+    SPDP_EINTEGRITY = -7   /* debug_checks found a violated count invariant */
+} spdp_status;
+
+typedef struct spdp_ctx spdp_ctx;
+
+/* How the per-sweep count deltas of a multi-GPU run are summed across ranks. */
+enum {
+    SPDP_EXCHANGE_NCCL = 0,      /* spdp_sweep calls ncclAllReduce itself (needs nccl_unique_id) */
+    SPDP_EXCHANGE_EXTERNAL = 1   /* caller sums the buffer of spdp_exchange_buffer between
+                                    spdp_sweep_local and spdp_sweep_merge */
+};
+
+typedef struct {
+    uint32_t struct_size;          /* = sizeof(spdp_config); ABI versioning */
+    int32_t num_groups;            /* I >= 1 */
+    int32_t vocab_size;            /* V >= 1 */
+    int32_t num_topics;            /* K, 1 <= K <= 1024 */
+    double alpha;                  /* symmetric Dirichlet on theta, > 0 (paper 0.1) */
+    const double* alpha_ik;        /* optional [I*K] asymmetric alpha_{ik} (row-major i,k); NULL -> alpha */
+    double beta;                   /* symmetric Dirichlet on phi0 (paper gamma_v = 0.1), > 0 */
+    const double* discount;        /* [I] a_i in [0, 1)      (paper 0.7) */
+    const double* concentration;   /* [I] b_i > 0            (paper 100) */
+    uint64_t seed;                 /* Philox4x32-10 key (low word, high word) */
+    int32_t num_waves;             /* W >= 1: token of in-document position l is in wave l mod W */
+    int32_t device;                /* CUDA ordinal used by this rank */
+    int32_t rank, world_size;      /* 0, 1 for a single GPU */
+    int32_t exchange;              /* SPDP_EXCHANGE_* (ignored when world_size == 1) */
+    const void* nccl_unique_id;    /* 128-byte ncclUniqueId (same on every rank) for SPDP_EXCHANGE_NCCL */
+    void* stream;                  /* cudaStream_t to order work on; NULL -> a stream owned by the context */
+    int32_t debug_checks;          /* 1 = verify count invariants after every sweep (slow) */
+} spdp_config;
+
+/* Create a context on cfg->device.  Validates the hyper-parameters
+ * (SPDP_EINVAL), selects the device (SPDP_ECUDA when absent) and, for
+ * world_size > 1 with SPDP_EXCHANGE_NCCL, joins the NCCL communicator
+ * (SPDP_ENCCL).  *out receives the context even when the call fails (so that
+ * spdp_last_error can explain the failure); release it with spdp_destroy. */
+spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out);
+
+/* Load the corpus and the initial state.  Token p = (group[p], doc[p],
+ * word[p]), p in [0, num_tokens), is the canonical token id used by the RNG;
+ * its in-document position l is its rank among the tokens of doc[p] in
+ * canonical order.  Doc ids lie in [0, num_docs); all tokens of a document
+ * share one group.
+ *   z_init [N] in [0, K) or NULL: default z_p = floor(x0 * K / 2^32) with
+ *          x = Philox(seed; counter (p, 0xFFFFFFFF, 0, 0)).
+ *   r_init [N] in {0, 1} or NULL: default r_p = 1 for the first token of each
+ *          (i, k, w) cell in canonical order (t = min(1, m)); table counts are
+ *          t_{ikw} = sum of r over the cell and must satisfy 1 <= t <= m on
+ *          every occupied cell ("Initialize counting
+ *          variables ... from z").
+ * Documents are divided over the world by a seeded permutation and a
+ * token-balanced contiguous split.
+ * Errors: SPDP_EINVAL (ids out of range, doc spanning groups, bad z/r/t),
+ * SPDP_ENOMEM, SPDP_ETABLE, SPDP_ECUDA.  May be called once per context. */
+spdp_status spdp_load_corpus(spdp_ctx* ctx, int64_t num_tokens, int32_t num_docs,
+                             const int32_t* group, const int32_t* doc, const int32_t* word,
+                             const int32_t* z_init, const uint8_t* r_init);
+
+/* Replace the sampler state: z [N] and r [N] as in spdp_load_corpus, and
+ * optionally the table counts tables [I*V*K] (row-major i, w, k) which then
+ * override sum-of-r (checkpoint / resume; parity tests).  Every rank passes
+ * the whole arrays.  The sweep counter is left unchanged. */
+spdp_status spdp_set_state(spdp_ctx* ctx, const int32_t* z, const uint8_t* r, const int32_t* tables);
+
+/* Run num_sweeps >= 0 sweeps.  One sweep visits every token once: for each
+ * wave in order, every token of the wave removes itself from the wave-start
+ * counts (Alg.1 lines 3-10), weighs the 2K (topic, table-indicator) slots
+ * (Eqs. r0/r1) and draws one slot with the Philox uniform of (token, sweep);
+ * the wave's count deltas are then applied and t clamped into
+ * [min(1, m), m].  With world_size > 1 the ranks' net
+ * count changes are all-reduced after the last wave and merged (Alg.3
+ * PAPER.md:2960-2965).  Collective.  SPDP_ESTATE for
+ * SPDP_EXCHANGE_EXTERNAL contexts (use the split calls below). */
+spdp_status spdp_sweep(spdp_ctx* ctx, int32_t num_sweeps);
+
+/* Split sweep for SPDP_EXCHANGE_EXTERNAL: spdp_sweep_local runs every wave
+ * on this rank and leaves the rank's net (customer, table) count changes in
+ * the device buffer returned by spdp_exchange_buffer (int32, *count elements,
+ * device pointer owned by the context); the caller replaces its content by
+ * the element-wise sum over ranks, then calls spdp_sweep_merge. */
+spdp_status spdp_sweep_local(spdp_ctx* ctx);
+spdp_status spdp_exchange_buffer(spdp_ctx* ctx, void** device_ptr, int64_t* count);
+spdp_status spdp_sweep_merge(spdp_ctx* ctx);
+/* Copy the exchange buffer to (to_device = 0) or from (to_device = 1) the
+ * caller's host array of *count int32 (e.g. for a host-side all-reduce). */
+spdp_status spdp_exchange_copy(spdp_ctx* ctx, int32_t* host, int32_t to_device);
+
+/* Read the state.  Every output is optional (NULL = skip):
+ *   z [N] int32, r [N] uint8: canonical token order; r is the indicator drawn
+ *       at the token's last insertion (1 when the keep rule held it).  With
+ *       world_size > 1 and SPDP_EXCHANGE_NCCL the values of every rank are
+ *       gathered; with SPDP_EXCHANGE_EXTERNAL only this rank's tokens are
+ *       written.
+ *   doc_topic [D*K] int32 (n_{idk}); same gathering rule as z.
+ *   customers [I*V*K] int32 (m_{ikw}, row-major i, w, k), tables [I*V*K] int32
+ *       (t_{ikw}), shadow [K*V] int32 (Q_{kw} = sum_i t_{ikw}, row-major k, w):
+ *       replicated, identical on every rank after a sweep. */
+spdp_status spdp_counts(spdp_ctx* ctx, int32_t* z, uint8_t* r, int32_t* doc_topic,
+                        int32_t* customers, int32_t* tables, int32_t* shadow);
+
+/* log_joint = log p(W, Z, T | alpha, beta, a, b) (PAPER.md:1654-1665 summed over
+ * the seatings R of each T, Eq. SPDP-table-to-head);
+ * perplexity = training perplexity exp(-sum_tok log sum_k theta~_dk phi^i~_kw / N)
+ * (PAPER.md:1978-2007 with Eqs.; DESIGN.md readings
+ * c16, c17).  Either pointer may be NULL.  Collective. */
+spdp_status spdp_loglik(spdp_ctx* ctx, double* log_joint, double* perplexity);
+
+/* Diagnostics (parity tests): for n local tokens (canonical ids), the
+ * normalised 2K-slot conditional (slot 2k = (k, r=1), slot 2k+1 = (k, r=0);
+ * Alg.4) that the NEXT sweep would draw from if the
+ * current state were its wave-start snapshot, computed by the sweep's own
+ * device code.  probs [n*2K] fp64; info [n*4] int32 = {r_rem, keep, z_new,
+ * r_new}.  No state change.  SPDP_EINVAL for tokens of other ranks. */
+spdp_status spdp_debug_probs(spdp_ctx* ctx, int64_t n, const int64_t* tok_ids, double* probs, int32_t* info);
+
+/* Counters of the last sweep on this rank: out[0] keeps, out[1] moved
+ * tokens, out[2] clamped cells, out[3] sweeps done, out[4] local tokens,
+ * out[5] local docs, out[6] M_max (largest count(i,w)), out[7] chunks. */
+spdp_status spdp_stats(spdp_ctx* ctx, int64_t* out);
+
+/* Document -> rank assignment used by spdp_load_corpus (host only; no
+ * device needed): shard_of_doc [num_docs]. */
+spdp_status spdp_partition(uint64_t seed, int32_t world_size, int64_t num_tokens, int32_t num_docs,
+                           const int32_t* doc, int32_t* shard_of_doc);
+
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 calls this and broadcasts
+ * the bytes, e.g. with torch.distributed).  SPDP_ENCCL if NCCL is absent. */
+spdp_status spdp_nccl_unique_id(void* out);
+
+void spdp_destroy(spdp_ctx* ctx);                  /* NULL-safe; frees device memory and the communicator */
+const char* spdp_last_error(const spdp_ctx* ctx);  /* message of the last failing call ("" if none) */
+const char* spdp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPDP_H */

@@ -50,7 +50,7 @@ def lib():
         L.or_sweep_seq.restype = C.c_int
         L.or_sweep_seq.argtypes = [P, C.c_int64]
         L.or_sweep_par.restype = C.c_int
-        L.or_sweep_par.argtypes = [P, C.c_int, C.c_int, P, P, C.c_int64]
+        L.or_sweep_par.argtypes = [P, C.c_int, C.c_int, P, P, C.c_int64, P]
         L.or_get.argtypes = [P] + [P] * 6
         L.or_sweep_index.restype = C.c_uint32
         L.or_sweep_index.argtypes = [P]
@@ -136,12 +136,16 @@ class Oracle:
         if lib().or_sweep_seq(self.h, int(max_tokens)) != 0:
             raise RuntimeError("or_sweep_seq failed")
 
-    def sweep_par(self, waves: int = 1, shards: int = 1, force_zr=None, want_margin=False, max_tokens: int = -1):
+    def sweep_par(self, waves: int = 1, shards: int = 1, force_zr=None, want_margin=False, max_tokens: int = -1,
+                  want_own=False):
+        """Mode-P sweep.  Returns margin [N] (or None), and with want_own also the
+        oracle's own draws z | r<<15 [N] (before force_zr replaced them)."""
         f = None if force_zr is None else np.ascontiguousarray(force_zr, np.int32)
         mg = np.full(self.N, np.inf) if want_margin else None
-        if lib().or_sweep_par(self.h, int(waves), int(shards), _ptr(f), _ptr(mg), int(max_tokens)) != 0:
+        own = np.full(self.N, -1, np.int32) if want_own else None
+        if lib().or_sweep_par(self.h, int(waves), int(shards), _ptr(f), _ptr(mg), int(max_tokens), _ptr(own)) != 0:
             raise RuntimeError("or_sweep_par failed")
-        return mg
+        return (mg, own) if want_own else mg
 
     @property
     def sweep_index(self) -> int:

@@ -464,9 +464,11 @@ static int64_t clamp_cells(size_t cells, const int32_t *m, int32_t *t) {
  * force_zr (optional, [N], -1 = none): replace the drawn (z | r<<15) of a
  * token that is not kept (lock-step replay of another sampler's draws).
  * margin (optional, [N]): distance of u to the edge of the drawn slot.
+ * own_zr (optional, [N]): the oracle's own draw (z | r<<15) before forcing.
  * max_tokens >= 0 limits the sweep to the first max_tokens tokens of each
  * shard's canonical order (timing samples only). */
-int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margin, int64_t max_tokens) {
+int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margin, int64_t max_tokens,
+                 int32_t *own_zr) {
     int I = s->I, V = s->V, K = s->K;
     int64_t N = s->N;
     size_t cells = (size_t)I * V * K;
@@ -518,11 +520,12 @@ int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margi
                 int keep, r = removal(x[0], Lm[c], Lt[c], &keep);
                 rrem[p] = (int8_t)r;
                 kept[p] = (int8_t)keep;
-                if (keep) { newz[p] = k0; newr[p] = 1; continue; }
+                if (keep) { newz[p] = k0; newr[p] = 1; if (own_zr) own_zr[p] = k0 | (1 << 15); continue; }
                 log_weights(s, p, r, s->n, Lm, Lt, M, Tt, Q, T, lw);
                 normalise(2 * K, lw, prob);
                 int j = draw_slot(2 * K, prob, u53(x), margin ? &margin[p] : NULL);
                 newz[p] = j / 2; newr[p] = (j % 2 == 0);
+                if (own_zr) own_zr[p] = newz[p] | (newr[p] << 15);
                 if (force_zr && force_zr[p] >= 0) {
                     int fz = force_zr[p] & 0x7FFF, fr = (force_zr[p] >> 15) & 1;
                     if (fz != newz[p] || fr != newr[p]) s->stats[3]++;
@@ -743,7 +746,7 @@ double or_word_prob(const ostate *s, int32_t d, int32_t w) {
 int or_chain_codes(ostate *s, int64_t nsweeps, int waves, int tbase, int64_t *codes) {
     size_t cells = (size_t)s->I * s->V * s->K;
     for (int64_t it = 0; it < nsweeps; it++) {
-        int rc = (waves < 0) ? or_sweep_seq(s, -1) : or_sweep_par(s, waves, 1, NULL, NULL, -1);
+        int rc = (waves < 0) ? or_sweep_seq(s, -1) : or_sweep_par(s, waves, 1, NULL, NULL, -1, NULL);
         if (rc) return rc;
         int64_t code = 0, mul = 1;
         for (int64_t p = 0; p < s->N; p++) { code += mul * s->z[p]; mul *= s->K; }

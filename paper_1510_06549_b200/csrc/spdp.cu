@@ -1,0 +1,1019 @@
+// spdp.cu — host side of libspdp.so: the C ABI of include/spdp.h.
+//
+// Validation, document sharding, the word-major wave
+// plan (PAPER.md:2289-2299 reorder as wave = l mod W), device memory, kernel
+// launches, and the cross-GPU count exchange (Alg.3) over
+// NCCL (dlopen'ed, so the library loads on hosts without NCCL).
+// No CPU fallback exists: every step of the sweep runs in the kernels of
+// spdp_device.cuh.
+#include "../../include/spdp.h"
+#include "spdp_device.cuh"
+#include "spdp_loglik.cuh"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace spdp;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclUid { char b[128]; };
+struct NcclApi {
+    void* lib = nullptr;
+    int (*CommInitRank)(void** comm, int nranks, NcclUid id, int rank) = nullptr;
+    int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*CommDestroy)(void*) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0;
+
+// ------------------------------------------------------------------ host Philox4x32-10
+void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
+    uint32_t x0 = ctr[0], x1 = ctr[1], x2 = ctr[2], x3 = ctr[3];
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * x0, p1 = (uint64_t)0xCD9E8D57u * x2;
+        const uint32_t y0 = (uint32_t)(p1 >> 32) ^ x1 ^ k0, y1 = (uint32_t)p1;
+        const uint32_t y2 = (uint32_t)(p0 >> 32) ^ x3 ^ k1, y3 = (uint32_t)p0;
+        x0 = y0; x1 = y1; x2 = y2; x3 = y3;
+    }
+    out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
+}
+
+int pick_lpt(int K) { return K <= 32 ? 8 : (K <= 64 ? 16 : 32); }
+int pick_kpl(int K) {
+    if (K <= 16) return 2;
+    if (K <= 128) return 4;
+    if (K <= 256) return 8;
+    if (K <= 512) return 16;
+    return 32;
+}
+
+template <typename T>
+T* dalloc(size_t n, cudaError_t& e) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    e = cudaMalloc(&p, n * sizeof(T));
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct spdp_ctx {
+    spdp_config cfg{};
+    std::string err;
+    int I = 0, V = 0, K = 0, Kp = 0, W = 1, rank = 0, G = 1;
+    std::vector<double> alpha_ik, disc, conc;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool loaded = false, poisoned = false;
+    NcclApi nccl;
+    void* comm = nullptr;
+    int LPT = 32, KPL = 4, chunk_tokens = 32;
+
+    // corpus (host)
+    int64_t N = 0;
+    int32_t D = 0;
+    std::vector<int32_t> group, doc, word, pos, doclen, docgroup;
+    std::vector<int32_t> shard_of_doc, local_of_doc, global_of_local;
+    int64_t Nloc = 0;
+    int32_t Dloc = 0;
+    std::vector<uint32_t> sorted_tok;            // canonical id at each sorted position
+    std::vector<int64_t> pos_of_tok;              // canonical id -> sorted position (-1: other rank)
+    std::vector<uint32_t> wave_tok_begin, wave_chunk_begin;
+    std::vector<uint32_t> chunk_start, chunk_seg;
+    int mmax = 0;
+    size_t cells = 0;
+
+    // device
+    uint32_t *d_tok_doc = nullptr, *d_tok_id = nullptr, *d_chunk_start = nullptr, *d_chunk_seg = nullptr,
+             *d_sweep = nullptr;
+    uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
+    int32_t *d_n = nullptr, *d_m = nullptr, *d_t = nullptr, *d_Q = nullptr, *d_M = nullptr, *d_Tt = nullptr,
+            *d_T = nullptr, *d_dm = nullptr, *d_dt = nullptr, *d_D = nullptr, *d_doclen = nullptr,
+            *d_docgroup = nullptr;
+    float *d_alpha = nullptr, *d_disc = nullptr, *d_conc = nullptr, *d_alpha_sum = nullptr;
+    double *d_alpha64 = nullptr, *d_disc64 = nullptr, *d_conc64 = nullptr, *d_alpha_sum64 = nullptr;
+    float2* d_tab = nullptr;
+    uint64_t* d_tab_off = nullptr;
+    std::vector<uint64_t> tab_off_host;
+    unsigned long long* d_stats = nullptr;
+    double *d_partial = nullptr, *d_scalar = nullptr;
+    size_t partial_len = 0;
+    uint32_t sweeps_done = 0;
+    std::vector<void*> allocs;
+};
+
+namespace {
+
+spdp_status fail(spdp_ctx* c, spdp_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (s == SPDP_ECUDA) c->poisoned = true;
+    }
+    return s;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(c, SPDP_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+template <typename T>
+spdp_status alloc(spdp_ctx* c, T*& p, size_t n) {
+    cudaError_t e;
+    p = dalloc<T>(n, e);
+    if (e != cudaSuccess) return fail(c, SPDP_ENOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
+    c->allocs.push_back(p);
+    return SPDP_OK;
+}
+#define ALLOC(p, n)                                   \
+    do {                                              \
+        spdp_status s_ = alloc(c, p, (size_t)(n));    \
+        if (s_ != SPDP_OK) return s_;                 \
+    } while (0)
+
+spdp_status nccl_check(spdp_ctx* c, int r, const char* what) {
+    if (r != 0) return fail(c, SPDP_ENCCL, "%s: %s", what, c->nccl.GetErrorString ? c->nccl.GetErrorString(r) : "error");
+    return SPDP_OK;
+}
+
+// ------------------------------------------------------------------ kernel dispatch
+template <int LPT, int KPL, bool DBG>
+void launch_sample_t(const SweepArgs& a, cudaStream_t s) {
+    const size_t smem = (size_t)kWarps * 6 * LPT * KPL * sizeof(float);
+    const int blocks = (a.nchunks + kWarps - 1) / kWarps;
+    if (blocks > 0) sample_kernel<LPT, KPL, DBG><<<blocks, kWarps * 32, smem, s>>>(a);
+}
+template <int LPT, int KPL>
+void set_attr_t() {
+    const int smem = kWarps * 6 * LPT * KPL * (int)sizeof(float);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int psm = kWarps * LPT * KPL * (int)sizeof(double);
+    cudaFuncSetAttribute(perplexity_kernel<LPT, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+}
+template <int LPT, int KPL>
+void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const float* asum, double* partial, cudaStream_t s) {
+    const size_t smem = (size_t)kWarps * LPT * KPL * sizeof(double);
+    const int blocks = (a.nchunks + kWarps - 1) / kWarps;
+    if (blocks > 0) perplexity_kernel<LPT, KPL><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
+}
+
+#define SPDP_DISPATCH(LPT_, KPL_, CALL)                     \
+    switch (LPT_ * 100 + KPL_) {                            \
+        case 802: CALL(8, 2); break;                        \
+        case 804: CALL(8, 4); break;                        \
+        case 1604: CALL(16, 4); break;                      \
+        case 3204: CALL(32, 4); break;                      \
+        case 3208: CALL(32, 8); break;                      \
+        case 3216: CALL(32, 16); break;                     \
+        case 3232: CALL(32, 32); break;                     \
+        default: break;                                     \
+    }
+
+void launch_sample(spdp_ctx* c, const SweepArgs& a, bool dbg) {
+#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream) : launch_sample_t<L, P, false>(a, c->stream))
+    SPDP_DISPATCH(c->LPT, c->KPL, CALL_S)
+#undef CALL_S
+}
+void set_attrs(spdp_ctx* c) {
+#define CALL_A(L, P) set_attr_t<L, P>()
+    SPDP_DISPATCH(c->LPT, c->KPL, CALL_A)
+#undef CALL_A
+}
+void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
+#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum, partial, c->stream)
+    SPDP_DISPATCH(c->LPT, c->KPL, CALL_P)
+#undef CALL_P
+}
+
+SweepArgs base_args(spdp_ctx* c) {
+    SweepArgs a{};
+    a.tok_doc = c->d_tok_doc; a.tok_id = c->d_tok_id; a.zr = c->d_zr; a.zr_next = c->d_zr_next;
+    a.chunk_start = c->d_chunk_start; a.chunk_seg = c->d_chunk_seg; a.nchunks = 0;
+    a.n = c->d_n; a.m = c->d_m; a.t = c->d_t; a.Q = c->d_Q; a.M = c->d_M; a.Tt = c->d_Tt; a.T = c->d_T;
+    a.dm = c->d_dm; a.dt = c->d_dt;
+    a.alpha = c->d_alpha; a.disc = c->d_disc; a.conc = c->d_conc; a.tab = c->d_tab; a.tab_off = c->d_tab_off;
+    a.beta = (float)c->cfg.beta; a.vbeta = (float)((double)c->V * c->cfg.beta);
+    a.I = c->I; a.K = c->K; a.Kp = c->Kp;
+    a.key0 = (uint32_t)c->cfg.seed; a.key1 = (uint32_t)(c->cfg.seed >> 32);
+    a.sweep = c->d_sweep; a.stats = c->d_stats;
+    return a;
+}
+
+int merge_grid() { return 148 * 4; }
+
+template <typename T>
+struct TempBuf {
+    T* p = nullptr;
+    explicit TempBuf(size_t n) { if (cudaMalloc((void**)&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) p = nullptr; }
+    ~TempBuf() { if (p) cudaFree(p); }
+    TempBuf(const TempBuf&) = delete;
+    TempBuf& operator=(const TempBuf&) = delete;
+};
+
+// rows += (dm, dt), clamp, zero deltas, (D += change), recompute Q and sums
+void launch_merge(spdp_ctx* c, int32_t* dm, int32_t* dt, int32_t* Dm, int32_t* Dt) {
+    cudaMemsetAsync(c->d_M, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
+    cudaMemsetAsync(c->d_Tt, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
+    cudaMemsetAsync(c->d_T, 0, sizeof(int32_t) * (size_t)c->Kp, c->stream);
+    const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
+    const int use_smem = smem <= 48 * 1024;
+    merge_rows_kernel<<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
+        c->d_m, c->d_t, dm, dt, Dm, Dt, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I, c->Kp, use_smem, c->d_stats);
+}
+
+spdp_status check_launch(spdp_ctx* c, const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, SPDP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return SPDP_OK;
+}
+
+spdp_status sync(spdp_ctx* c, const char* what) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, SPDP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+    return SPDP_OK;
+}
+
+spdp_status guard(spdp_ctx* c, bool need_loaded) {
+    if (!c) return SPDP_EINVAL;
+    if (c->poisoned) return fail(c, SPDP_ESTATE, "context poisoned by an earlier CUDA fault: %s", c->err.c_str());
+    if (need_loaded && !c->loaded) return fail(c, SPDP_ESTATE, "spdp_load_corpus has not been called");
+    cudaError_t e = cudaSetDevice(c->cfg.device);
+    if (e != cudaSuccess) return fail(c, SPDP_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+    return SPDP_OK;
+}
+
+// host doc -> rank split: docs ordered by Philox x0 of
+// (doc, 0xFFFFFFFE) (ties by id), then rank = floor(tokens_before * G / N).
+void partition_docs(uint64_t seed, int G, int64_t N, int32_t D, const std::vector<int32_t>& doclen,
+                    std::vector<int32_t>& shard) {
+    std::vector<std::pair<uint32_t, int32_t>> key((size_t)D);
+    for (int32_t d = 0; d < D; ++d) {
+        const uint32_t ctr[4] = {(uint32_t)d, 0xFFFFFFFEu, 0u, 0u};
+        uint32_t x[4];
+        philox_host(ctr, (uint32_t)seed, (uint32_t)(seed >> 32), x);
+        key[(size_t)d] = {x[0], d};
+    }
+    std::sort(key.begin(), key.end());
+    shard.assign((size_t)D, 0);
+    int64_t before = 0;
+    for (int32_t j = 0; j < D; ++j) {
+        const int32_t d = key[(size_t)j].second;
+        int64_t g = N > 0 ? (before * (int64_t)G) / N : 0;
+        if (g >= G) g = G - 1;
+        shard[(size_t)d] = (int32_t)g;
+        before += doclen[(size_t)d];
+    }
+}
+
+// Upload (z, r or tables) as the sampler state: counts from z.
+spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in, const int32_t* tables) {
+    const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
+    const int64_t N = c->N;
+    std::vector<int32_t> z((size_t)N);
+    std::vector<uint8_t> r((size_t)N);
+    for (int64_t p = 0; p < N; ++p) {
+        if (z_in) {
+            if (z_in[p] < 0 || z_in[p] >= K) return fail(c, SPDP_EINVAL, "z[%lld] = %d out of [0, K)", (long long)p, z_in[p]);
+            z[(size_t)p] = z_in[p];
+        } else {
+            const uint32_t ctr[4] = {(uint32_t)p, 0xFFFFFFFFu, 0u, 0u};
+            uint32_t x[4];
+            philox_host(ctr, (uint32_t)c->cfg.seed, (uint32_t)(c->cfg.seed >> 32), x);
+            z[(size_t)p] = (int32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
+        }
+    }
+    // global m, t in device layout [w][i][Kp]
+    std::vector<int32_t> m(c->cells, 0), t(c->cells, 0);
+    for (int64_t p = 0; p < N; ++p) {
+        const size_t cell = ((size_t)c->word[(size_t)p] * I + c->group[(size_t)p]) * Kp + z[(size_t)p];
+        m[cell]++;
+        if (r_in) {
+            if (r_in[p] > 1) return fail(c, SPDP_EINVAL, "r[%lld] = %d not in {0,1}", (long long)p, (int)r_in[p]);
+            r[(size_t)p] = r_in[p];
+        } else {
+            r[(size_t)p] = (t[cell] == 0) ? 1 : 0;     // first token of the cell opens its table
+        }
+        t[cell] += r[(size_t)p];
+    }
+    if (tables) {
+        for (int i = 0; i < I; ++i)
+            for (int w = 0; w < V; ++w)
+                for (int k = 0; k < K; ++k)
+                    t[((size_t)w * I + i) * Kp + k] = tables[((size_t)i * V + w) * K + k];
+    }
+    for (size_t cell = 0; cell < c->cells; ++cell)
+        if (t[cell] < 0 || t[cell] > m[cell] || ((t[cell] > 0) != (m[cell] > 0)))
+            return fail(c, SPDP_EINVAL, "table counts violate 1 <= t <= m on an occupied cell (or t > 0 on an empty one)");
+    // local doc-topic counts and token records
+    std::vector<int32_t> n((size_t)c->Dloc * Kp, 0);
+    std::vector<uint16_t> zr((size_t)c->Nloc);
+    for (int64_t q = 0; q < c->Nloc; ++q) {
+        const uint32_t p = c->sorted_tok[(size_t)q];
+        n[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + z[p]]++;
+        zr[(size_t)q] = (uint16_t)(z[p] | (r[p] << 15));
+    }
+    CU(cudaMemcpyAsync(c->d_m, m.data(), sizeof(int32_t) * c->cells, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_t, t.data(), sizeof(int32_t) * c->cells, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_n, n.data(), sizeof(int32_t) * n.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_zr, zr.data(), sizeof(uint16_t) * zr.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_zr_next, zr.data(), sizeof(uint16_t) * zr.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
+    CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
+    if (c->d_D) CU(cudaMemsetAsync(c->d_D, 0, sizeof(int32_t) * 2 * c->cells, c->stream));
+    launch_merge(c, c->d_dm, c->d_dt, nullptr, nullptr);    // zero deltas: recomputes Q and the sums
+    spdp_status s = check_launch(c, "merge_rows_kernel");
+    if (s) return s;
+    return sync(c, "install_state");
+}
+
+spdp_status run_waves(spdp_ctx* c) {
+    SweepArgs a = base_args(c);
+    CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    int32_t* Dm = c->G > 1 ? c->d_D : nullptr;
+    int32_t* Dt = c->G > 1 ? c->d_D + c->cells : nullptr;
+    for (int w = 0; w < c->W; ++w) {
+        const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
+        if (ce == cb) continue;
+        a.chunk_start = c->d_chunk_start + cb;
+        a.chunk_seg = c->d_chunk_seg + cb;
+        a.nchunks = (int)(ce - cb);
+        launch_sample(c, a, false);
+        const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
+        const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
+        apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n,
+                                                                         c->Kp, tb, te);
+        launch_merge(c, c->d_dm, c->d_dt, Dm, Dt);
+    }
+    return check_launch(c, "sweep waves");
+}
+
+spdp_status finish_sweep(spdp_ctx* c) {
+    inc_sweep_kernel<<<1, 1, 0, c->stream>>>(c->d_sweep);
+    c->sweeps_done++;
+    return check_launch(c, "inc_sweep");
+}
+
+spdp_status debug_verify(spdp_ctx* c);
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* spdp_version(void) { return "spdp-b200 0.1 (sm_100a)"; }
+
+const char* spdp_last_error(const spdp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+spdp_status spdp_partition(uint64_t seed, int32_t world_size, int64_t num_tokens, int32_t num_docs, const int32_t* doc,
+                           int32_t* shard_of_doc) {
+    if (world_size < 1 || num_tokens < 0 || num_docs < 1 || (!doc && num_tokens) || !shard_of_doc) return SPDP_EINVAL;
+    std::vector<int32_t> len((size_t)num_docs, 0);
+    for (int64_t p = 0; p < num_tokens; ++p) {
+        if (doc[p] < 0 || doc[p] >= num_docs) return SPDP_EINVAL;
+        len[(size_t)doc[p]]++;
+    }
+    std::vector<int32_t> sh;
+    partition_docs(seed, world_size, num_tokens, num_docs, len, sh);
+    std::memcpy(shard_of_doc, sh.data(), sizeof(int32_t) * (size_t)num_docs);
+    return SPDP_OK;
+}
+
+spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
+    if (!out) return SPDP_EINVAL;
+    *out = nullptr;
+    if (!cfg || cfg->struct_size != sizeof(spdp_config)) return SPDP_EINVAL;
+    spdp_ctx* c = new (std::nothrow) spdp_ctx();
+    if (!c) return SPDP_ENOMEM;
+    c->cfg = *cfg;
+    auto bad = [&](const char* msg) { fail(c, SPDP_EINVAL, "%s", msg); *out = c; return SPDP_EINVAL; };
+    if (cfg->num_groups < 1 || cfg->vocab_size < 1) return bad("num_groups and vocab_size must be >= 1");
+    if (cfg->num_topics < 1 || cfg->num_topics > 1024) return bad("num_topics must be in [1, 1024]");
+    if (!(cfg->beta > 0.0)) return bad("beta must be > 0");
+    if (!cfg->discount || !cfg->concentration) return bad("discount and concentration arrays are required");
+    if (cfg->num_waves < 1) return bad("num_waves must be >= 1");
+    if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return bad("rank / world_size out of range");
+    c->I = cfg->num_groups; c->V = cfg->vocab_size; c->K = cfg->num_topics;
+    c->Kp = (c->K + 3) & ~3; c->W = cfg->num_waves; c->rank = cfg->rank; c->G = cfg->world_size;
+    c->alpha_ik.resize((size_t)c->I * c->K);
+    for (size_t j = 0; j < c->alpha_ik.size(); ++j) {
+        c->alpha_ik[j] = cfg->alpha_ik ? cfg->alpha_ik[j] : cfg->alpha;
+        if (!(c->alpha_ik[j] > 0.0)) return bad("alpha must be > 0");
+    }
+    c->disc.assign(cfg->discount, cfg->discount + c->I);
+    c->conc.assign(cfg->concentration, cfg->concentration + c->I);
+    for (int i = 0; i < c->I; ++i) {
+        if (!(c->disc[(size_t)i] >= 0.0 && c->disc[(size_t)i] < 1.0)) return bad("discount must be in [0, 1)");
+        if (!(c->conc[(size_t)i] > 0.0)) return bad("concentration must be > 0");
+    }
+    c->cfg.alpha_ik = nullptr; c->cfg.discount = nullptr; c->cfg.concentration = nullptr; c->cfg.nccl_unique_id = nullptr;
+    c->LPT = pick_lpt(c->K);
+    c->KPL = pick_kpl(c->K);
+    if (c->LPT * c->KPL < c->K) return bad("internal: no kernel configuration for K");
+    int steps = 32;
+    if (const char* e = getenv("SPDP_CHUNK_STEPS")) steps = std::max(1, atoi(e));
+    c->chunk_tokens = steps * (32 / c->LPT);
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        fail(c, SPDP_ECUDA, "no CUDA device: %s", e != cudaSuccess ? cudaGetErrorString(e) : "0 devices");
+        *out = c;
+        return SPDP_ECUDA;
+    }
+    if (cfg->device < 0 || cfg->device >= ndev) return bad("device ordinal out of range");
+    if ((e = cudaSetDevice(cfg->device)) != cudaSuccess) {
+        fail(c, SPDP_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+        *out = c;
+        return SPDP_ECUDA;
+    }
+    if (cfg->stream) c->stream = (cudaStream_t)cfg->stream;
+    else {
+        if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            fail(c, SPDP_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+            *out = c;
+            return SPDP_ECUDA;
+        }
+        c->own_stream = true;
+    }
+    set_attrs(c);
+    if (c->G > 1 && cfg->exchange == SPDP_EXCHANGE_NCCL) {
+        if (!cfg->nccl_unique_id) return bad("nccl_unique_id is required for SPDP_EXCHANGE_NCCL with world_size > 1");
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* nm : names)
+            if ((c->nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!c->nccl.lib) {
+            fail(c, SPDP_ENCCL, "cannot dlopen libnccl.so.2");
+            *out = c;
+            return SPDP_ENCCL;
+        }
+        c->nccl.CommInitRank = (decltype(c->nccl.CommInitRank))dlsym(c->nccl.lib, "ncclCommInitRank");
+        c->nccl.AllReduce = (decltype(c->nccl.AllReduce))dlsym(c->nccl.lib, "ncclAllReduce");
+        c->nccl.CommDestroy = (decltype(c->nccl.CommDestroy))dlsym(c->nccl.lib, "ncclCommDestroy");
+        c->nccl.GetErrorString = (decltype(c->nccl.GetErrorString))dlsym(c->nccl.lib, "ncclGetErrorString");
+        if (!c->nccl.CommInitRank || !c->nccl.AllReduce || !c->nccl.CommDestroy) {
+            fail(c, SPDP_ENCCL, "libnccl lacks the required symbols");
+            *out = c;
+            return SPDP_ENCCL;
+        }
+        NcclUid uid;
+        std::memcpy(uid.b, cfg->nccl_unique_id, 128);
+        int r = c->nccl.CommInitRank(&c->comm, c->G, uid, c->rank);
+        if (r != 0) {
+            fail(c, SPDP_ENCCL, "ncclCommInitRank: %s", c->nccl.GetErrorString ? c->nccl.GetErrorString(r) : "error");
+            *out = c;
+            return SPDP_ENCCL;
+        }
+    }
+    *out = c;
+    return SPDP_OK;
+}
+
+spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, const int32_t* group, const int32_t* doc,
+                             const int32_t* word, const int32_t* z_init, const uint8_t* r_init) {
+    spdp_status s = guard(c, false);
+    if (s) return s;
+    if (c->loaded) return fail(c, SPDP_ESTATE, "spdp_load_corpus may be called once per context");
+    if (num_tokens < 1 || num_docs < 1 || !group || !doc || !word)
+        return fail(c, SPDP_EINVAL, "need num_tokens >= 1, num_docs >= 1 and the three token arrays");
+    if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
+    const int I = c->I, V = c->V, Kp = c->Kp, W = c->W;
+    c->N = num_tokens; c->D = num_docs;
+    c->group.assign(group, group + num_tokens);
+    c->doc.assign(doc, doc + num_tokens);
+    c->word.assign(word, word + num_tokens);
+    c->pos.resize((size_t)num_tokens);
+    c->doclen.assign((size_t)num_docs, 0);
+    c->docgroup.assign((size_t)num_docs, -1);
+    for (int64_t p = 0; p < num_tokens; ++p) {
+        const int32_t g = group[p], d = doc[p], w = word[p];
+        if (g < 0 || g >= I || d < 0 || d >= num_docs || w < 0 || w >= V)
+            return fail(c, SPDP_EINVAL, "token %lld = (%d, %d, %d) out of range", (long long)p, g, d, w);
+        if (c->docgroup[(size_t)d] >= 0 && c->docgroup[(size_t)d] != g)
+            return fail(c, SPDP_EINVAL, "document %d spans groups %d and %d", d, c->docgroup[(size_t)d], g);
+        c->docgroup[(size_t)d] = g;
+        c->pos[(size_t)p] = c->doclen[(size_t)d]++;
+    }
+    // M_max = largest count(i, w): bounds every m_{ikw} the chain can reach
+    {
+        std::vector<int32_t> cnt((size_t)I * V, 0);
+        for (int64_t p = 0; p < num_tokens; ++p) cnt[(size_t)group[p] * V + word[p]]++;
+        c->mmax = *std::max_element(cnt.begin(), cnt.end());
+        if ((double)c->mmax * (c->mmax + 1) / 2 * sizeof(float2) > 16e9)
+            return fail(c, SPDP_ETABLE, "Stirling-ratio table for M_max = %d exceeds 16 GB", c->mmax);
+    }
+    // documents -> ranks
+    if (c->G > 1) partition_docs(c->cfg.seed, c->G, num_tokens, num_docs, c->doclen, c->shard_of_doc);
+    else c->shard_of_doc.assign((size_t)num_docs, 0);
+    c->local_of_doc.assign((size_t)num_docs, -1);
+    c->global_of_local.clear();
+    for (int32_t d = 0; d < num_docs; ++d)
+        if (c->shard_of_doc[(size_t)d] == c->rank) {
+            c->local_of_doc[(size_t)d] = (int32_t)c->global_of_local.size();
+            c->global_of_local.push_back(d);
+        }
+    c->Dloc = (int32_t)c->global_of_local.size();
+    // wave plan: stable counting sort of local tokens by seg = w*I + i, then by wave = l mod W
+    std::vector<uint32_t> local;
+    local.reserve((size_t)num_tokens / c->G + 16);
+    for (int64_t p = 0; p < num_tokens; ++p)
+        if (c->shard_of_doc[(size_t)doc[p]] == c->rank) local.push_back((uint32_t)p);
+    c->Nloc = (int64_t)local.size();
+    {
+        const size_t S = (size_t)V * I;
+        std::vector<uint32_t> off(S + 1, 0), tmp(local.size());
+        for (uint32_t p : local) off[(size_t)word[p] * I + group[p] + 1]++;
+        for (size_t j = 0; j < S; ++j) off[j + 1] += off[j];
+        for (uint32_t p : local) tmp[off[(size_t)word[p] * I + group[p]]++] = p;
+        std::vector<uint32_t> woff((size_t)W + 1, 0);
+        for (uint32_t p : tmp) woff[(size_t)(c->pos[p] % W) + 1]++;
+        for (int w = 0; w < W; ++w) woff[(size_t)w + 1] += woff[(size_t)w];
+        c->wave_tok_begin.assign(woff.begin(), woff.end());
+        c->sorted_tok.assign(local.size(), 0);
+        for (uint32_t p : tmp) c->sorted_tok[woff[(size_t)(c->pos[p] % W)]++] = p;
+    }
+    c->pos_of_tok.assign((size_t)num_tokens, -1);
+    for (size_t q = 0; q < c->sorted_tok.size(); ++q) c->pos_of_tok[c->sorted_tok[q]] = (int64_t)q;
+    // chunks: split each wave's (w, i) segments into runs of <= chunk_tokens tokens
+    c->chunk_start.clear(); c->chunk_seg.clear();
+    c->wave_chunk_begin.assign((size_t)W + 1, 0);
+    for (int w = 0; w < W; ++w) {
+        c->wave_chunk_begin[(size_t)w] = (uint32_t)c->chunk_seg.size();
+        uint32_t q = c->wave_tok_begin[(size_t)w];
+        const uint32_t qe = c->wave_tok_begin[(size_t)w + 1];
+        while (q < qe) {
+            const uint32_t p = c->sorted_tok[q];
+            const uint32_t seg = (uint32_t)word[p] * (uint32_t)I + (uint32_t)group[p];
+            uint32_t r = q, len = 0;
+            while (r < qe && len < (uint32_t)c->chunk_tokens) {
+                const uint32_t pr = c->sorted_tok[r];
+                if ((uint32_t)word[pr] * (uint32_t)I + (uint32_t)group[pr] != seg) break;
+                ++r; ++len;
+            }
+            c->chunk_start.push_back(q);
+            c->chunk_seg.push_back(seg);
+            q = r;
+        }
+    }
+    c->wave_chunk_begin[(size_t)W] = (uint32_t)c->chunk_seg.size();
+    c->chunk_start.push_back((uint32_t)c->Nloc);
+    const size_t nch = c->chunk_seg.size();
+    c->cells = (size_t)V * I * Kp;
+
+    // device allocations
+    ALLOC(c->d_tok_doc, c->Nloc); ALLOC(c->d_tok_id, c->Nloc);
+    ALLOC(c->d_zr, c->Nloc); ALLOC(c->d_zr_next, c->Nloc);
+    ALLOC(c->d_chunk_start, nch + 1); ALLOC(c->d_chunk_seg, nch);
+    ALLOC(c->d_sweep, 1);
+    ALLOC(c->d_n, (size_t)c->Dloc * Kp);
+    ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
+    ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);
+    if (c->G > 1) ALLOC(c->d_D, 2 * c->cells);
+    ALLOC(c->d_Q, (size_t)V * Kp);
+    ALLOC(c->d_M, (size_t)I * Kp); ALLOC(c->d_Tt, (size_t)I * Kp); ALLOC(c->d_T, (size_t)Kp);
+    ALLOC(c->d_doclen, std::max<int32_t>(c->Dloc, 1)); ALLOC(c->d_docgroup, std::max<int32_t>(c->Dloc, 1));
+    ALLOC(c->d_alpha, (size_t)I * Kp); ALLOC(c->d_alpha64, (size_t)I * Kp);
+    ALLOC(c->d_disc, I); ALLOC(c->d_conc, I); ALLOC(c->d_disc64, I); ALLOC(c->d_conc64, I);
+    ALLOC(c->d_alpha_sum, I); ALLOC(c->d_alpha_sum64, I);
+    ALLOC(c->d_stats, 8);
+    c->partial_len = std::max<size_t>(nch, 4096);
+    ALLOC(c->d_partial, c->partial_len);
+    ALLOC(c->d_scalar, 8);
+    {
+        std::vector<uint32_t> tdoc((size_t)c->Nloc), tid((size_t)c->Nloc);
+        for (int64_t q = 0; q < c->Nloc; ++q) {
+            const uint32_t p = c->sorted_tok[(size_t)q];
+            tdoc[(size_t)q] = (uint32_t)c->local_of_doc[(size_t)doc[p]];
+            tid[(size_t)q] = p;
+        }
+        std::vector<int32_t> dl((size_t)std::max<int32_t>(c->Dloc, 1), 0), dg((size_t)std::max<int32_t>(c->Dloc, 1), 0);
+        for (int32_t j = 0; j < c->Dloc; ++j) {
+            dl[(size_t)j] = c->doclen[(size_t)c->global_of_local[(size_t)j]];
+            dg[(size_t)j] = std::max(c->docgroup[(size_t)c->global_of_local[(size_t)j]], 0);   // empty docs: any group
+        }
+        std::vector<float> al((size_t)I * Kp, 0.f), disc((size_t)I), conc((size_t)I), asum((size_t)I);
+        std::vector<double> al64((size_t)I * Kp, 0.0), asum64((size_t)I, 0.0);
+        for (int i = 0; i < I; ++i) {
+            for (int k = 0; k < c->K; ++k) {
+                al[(size_t)i * Kp + k] = (float)c->alpha_ik[(size_t)i * c->K + k];
+                al64[(size_t)i * Kp + k] = c->alpha_ik[(size_t)i * c->K + k];
+                asum64[(size_t)i] += c->alpha_ik[(size_t)i * c->K + k];
+            }
+            asum[(size_t)i] = (float)asum64[(size_t)i];
+            disc[(size_t)i] = (float)c->disc[(size_t)i];
+            conc[(size_t)i] = (float)c->conc[(size_t)i];
+        }
+        CU(cudaMemcpy(c->d_tok_doc, tdoc.data(), sizeof(uint32_t) * tdoc.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_tok_id, tid.data(), sizeof(uint32_t) * tid.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_chunk_start, c->chunk_start.data(), sizeof(uint32_t) * c->chunk_start.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_chunk_seg, c->chunk_seg.data(), sizeof(uint32_t) * std::max<size_t>(nch, 0), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_doclen, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_docgroup, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_alpha, al.data(), sizeof(float) * al.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_alpha64, al64.data(), sizeof(double) * al64.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_disc, disc.data(), sizeof(float) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_conc, conc.data(), sizeof(float) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_disc64, c->disc.data(), sizeof(double) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_conc64, c->conc.data(), sizeof(double) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_alpha_sum, asum.data(), sizeof(float) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_alpha_sum64, asum64.data(), sizeof(double) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemset(c->d_sweep, 0, sizeof(uint32_t)));
+        CU(cudaMemset(c->d_stats, 0, sizeof(unsigned long long) * 8));
+    }
+    // Stirling-ratio tables, one per distinct discount (M_max rows)
+    {
+        std::vector<double> distinct;
+        std::vector<int> which((size_t)I);
+        for (int i = 0; i < I; ++i) {
+            size_t j = 0;
+            while (j < distinct.size() && distinct[j] != c->disc[(size_t)i]) ++j;
+            if (j == distinct.size()) distinct.push_back(c->disc[(size_t)i]);
+            which[(size_t)i] = (int)j;
+        }
+        const uint64_t per = (uint64_t)(c->mmax + 1) * (uint64_t)(c->mmax + 2) / 2;
+        ALLOC(c->d_tab, per * distinct.size());
+        ALLOC(c->d_tab_off, I);
+        c->tab_off_host.resize((size_t)I);
+        for (int i = 0; i < I; ++i) c->tab_off_host[(size_t)i] = per * (uint64_t)which[(size_t)i];
+        CU(cudaMemcpy(c->d_tab_off, c->tab_off_host.data(), sizeof(uint64_t) * I, cudaMemcpyHostToDevice));
+        double* scratch = nullptr;
+        ALLOC(scratch, 2 * (size_t)(c->mmax + 2));
+        for (size_t j = 0; j < distinct.size(); ++j)
+            build_ratio_table<<<1, 1024, 0, c->stream>>>(c->d_tab + per * j, scratch, c->mmax, distinct[j]);
+        s = check_launch(c, "build_ratio_table");
+        if (s) return s;
+        s = sync(c, "build_ratio_table");
+        if (s) return s;
+    }
+    s = install_state(c, z_init, r_init, nullptr);
+    if (s) return s;
+    c->loaded = true;
+    return SPDP_OK;
+}
+
+spdp_status spdp_set_state(spdp_ctx* c, const int32_t* z, const uint8_t* r, const int32_t* tables) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!z || (!r && !tables)) return fail(c, SPDP_EINVAL, "spdp_set_state needs z and (r or tables)");
+    std::vector<uint8_t> ones;
+    if (!r) { ones.assign((size_t)c->N, 1); r = ones.data(); }
+    return install_state(c, z, r, tables);
+}
+
+spdp_status spdp_sweep_local(spdp_ctx* c) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if ((s = run_waves(c))) return s;
+    if (c->G > 1) {
+        unapply_net_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_D, c->d_D + c->cells, c->cells);
+        if ((s = check_launch(c, "unapply_net_kernel"))) return s;
+    }
+    return sync(c, "spdp_sweep_local");
+}
+
+spdp_status spdp_exchange_buffer(spdp_ctx* c, void** ptr, int64_t* count) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!ptr || !count) return fail(c, SPDP_EINVAL, "null output");
+    if (c->G == 1) return fail(c, SPDP_ESTATE, "world_size == 1 has no exchange buffer");
+    *ptr = c->d_D;
+    *count = (int64_t)(2 * c->cells);
+    return SPDP_OK;
+}
+
+spdp_status spdp_exchange_copy(spdp_ctx* c, int32_t* host, int32_t to_device) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!host) return fail(c, SPDP_EINVAL, "null host buffer");
+    if (c->G == 1) return fail(c, SPDP_ESTATE, "world_size == 1 has no exchange buffer");
+    const size_t bytes = sizeof(int32_t) * 2 * c->cells;
+    if (to_device) CU(cudaMemcpyAsync(c->d_D, host, bytes, cudaMemcpyHostToDevice, c->stream));
+    else CU(cudaMemcpyAsync(host, c->d_D, bytes, cudaMemcpyDeviceToHost, c->stream));
+    return sync(c, "spdp_exchange_copy");
+}
+
+spdp_status spdp_sweep_merge(spdp_ctx* c) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (c->G > 1) {
+        launch_merge(c, c->d_D, c->d_D + c->cells, nullptr, nullptr);
+        if ((s = check_launch(c, "merge (exchange)"))) return s;
+    }
+    if ((s = finish_sweep(c))) return s;
+    if ((s = sync(c, "spdp_sweep_merge"))) return s;
+    if (c->cfg.debug_checks) return debug_verify(c);
+    return SPDP_OK;
+}
+
+spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (num_sweeps < 0) return fail(c, SPDP_EINVAL, "num_sweeps must be >= 0");
+    if (c->G > 1 && c->cfg.exchange != SPDP_EXCHANGE_NCCL)
+        return fail(c, SPDP_ESTATE, "SPDP_EXCHANGE_EXTERNAL: use spdp_sweep_local / spdp_sweep_merge");
+    for (int it = 0; it < num_sweeps; ++it) {
+        if ((s = run_waves(c))) return s;
+        if (c->G > 1) {
+            unapply_net_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_D, c->d_D + c->cells, c->cells);
+            if ((s = nccl_check(c, c->nccl.AllReduce(c->d_D, c->d_D, 2 * c->cells, kNcclInt32, kNcclSum, c->comm, c->stream),
+                                "ncclAllReduce(deltas)")))
+                return s;
+            launch_merge(c, c->d_D, c->d_D + c->cells, nullptr, nullptr);
+        }
+        if ((s = finish_sweep(c))) return s;
+        if (c->cfg.debug_checks) {
+            if ((s = sync(c, "spdp_sweep"))) return s;
+            if ((s = debug_verify(c))) return s;
+        }
+    }
+    return sync(c, "spdp_sweep");
+}
+
+spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic, int32_t* customers, int32_t* tables,
+                        int32_t* shadow) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
+    const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
+    if (z || r) {
+        std::vector<uint16_t> zr((size_t)c->Nloc);
+        CU(cudaMemcpyAsync(zr.data(), c->d_zr, sizeof(uint16_t) * zr.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "counts(z)"))) return s;
+        std::vector<int32_t> all;
+        if (gather) {
+            all.assign((size_t)c->N, 0);
+            for (int64_t q = 0; q < c->Nloc; ++q) all[c->sorted_tok[(size_t)q]] = (int32_t)zr[(size_t)q] + 1;
+            TempBuf<int32_t> tb(c->N);
+            if (!tb.p) return fail(c, SPDP_ENOMEM, "gather buffer");
+            int32_t* dbuf = tb.p;
+            CU(cudaMemcpyAsync(dbuf, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice, c->stream));
+            if ((s = nccl_check(c, c->nccl.AllReduce(dbuf, dbuf, (size_t)c->N, kNcclInt32, kNcclSum, c->comm, c->stream), "allreduce z")))
+                return s;
+            CU(cudaMemcpyAsync(all.data(), dbuf, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost, c->stream));
+            if ((s = sync(c, "counts(z gather)"))) return s;
+            for (int64_t p = 0; p < c->N; ++p) {
+                const uint32_t v = (uint32_t)(all[(size_t)p] - 1);
+                if (z) z[p] = (int32_t)(v & 0x7FFFu);
+                if (r) r[p] = (uint8_t)((v >> 15) & 1u);
+            }
+        } else {
+            for (int64_t q = 0; q < c->Nloc; ++q) {
+                const uint32_t p = c->sorted_tok[(size_t)q];
+                if (z) z[p] = (int32_t)(zr[(size_t)q] & 0x7FFFu);
+                if (r) r[p] = (uint8_t)((zr[(size_t)q] >> 15) & 1u);
+            }
+        }
+    }
+    if (doc_topic) {
+        std::vector<int32_t> n((size_t)c->Dloc * Kp);
+        CU(cudaMemcpyAsync(n.data(), c->d_n, sizeof(int32_t) * n.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "counts(n)"))) return s;
+        std::vector<int32_t> full;
+        if (gather) full.assign((size_t)c->D * K, 0);
+        int32_t* dst = gather ? full.data() : doc_topic;
+        for (int32_t j = 0; j < c->Dloc; ++j)
+            std::memcpy(dst + (size_t)c->global_of_local[(size_t)j] * K, n.data() + (size_t)j * Kp, sizeof(int32_t) * K);
+        if (gather) {
+            TempBuf<int32_t> tb(full.size());
+            if (!tb.p) return fail(c, SPDP_ENOMEM, "gather buffer");
+            int32_t* dbuf = tb.p;
+            CU(cudaMemcpyAsync(dbuf, full.data(), sizeof(int32_t) * full.size(), cudaMemcpyHostToDevice, c->stream));
+            if ((s = nccl_check(c, c->nccl.AllReduce(dbuf, dbuf, full.size(), kNcclInt32, kNcclSum, c->comm, c->stream), "allreduce n")))
+                return s;
+            CU(cudaMemcpyAsync(doc_topic, dbuf, sizeof(int32_t) * full.size(), cudaMemcpyDeviceToHost, c->stream));
+            if ((s = sync(c, "counts(n gather)"))) return s;
+        }
+    }
+    if (customers || tables) {
+        std::vector<int32_t> buf(c->cells);
+        for (int which = 0; which < 2; ++which) {
+            int32_t* out = which ? tables : customers;
+            if (!out) continue;
+            CU(cudaMemcpyAsync(buf.data(), which ? c->d_t : c->d_m, sizeof(int32_t) * c->cells, cudaMemcpyDeviceToHost, c->stream));
+            if ((s = sync(c, "counts(m,t)"))) return s;
+            for (int w = 0; w < V; ++w)
+                for (int i = 0; i < I; ++i)
+                    for (int k = 0; k < K; ++k)
+                        out[((size_t)i * V + w) * K + k] = buf[((size_t)w * I + i) * Kp + k];
+        }
+    }
+    if (shadow) {
+        std::vector<int32_t> q((size_t)V * Kp);
+        CU(cudaMemcpyAsync(q.data(), c->d_Q, sizeof(int32_t) * q.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "counts(Q)"))) return s;
+        for (int w = 0; w < V; ++w)
+            for (int k = 0; k < K; ++k) shadow[(size_t)k * V + w] = q[(size_t)w * Kp + k];
+    }
+    return SPDP_OK;
+}
+
+spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
+    if (perplexity) {
+        SweepArgs a = base_args(c);
+        a.nchunks = (int)c->chunk_seg.size();
+        launch_ppl(c, a, c->d_partial);
+        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(c->d_partial, c->chunk_seg.size(), c->d_scalar);
+        if ((s = check_launch(c, "perplexity_kernel"))) return s;
+        if (gather && (s = nccl_check(c, c->nccl.AllReduce(c->d_scalar, c->d_scalar, 1, kNcclFloat64, kNcclSum, c->comm, c->stream), "allreduce ppl")))
+            return s;
+        double ll = 0.0;
+        CU(cudaMemcpyAsync(&ll, c->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "perplexity"))) return s;
+        *perplexity = std::exp(-ll / (double)(gather ? c->N : c->Nloc));
+    }
+    if (log_joint) {
+        const uint64_t per = (uint64_t)(c->mmax + 1) * (uint64_t)(c->mmax + 2) / 2;
+        std::vector<double> distinct;
+        std::vector<uint64_t> off((size_t)c->I);
+        for (int i = 0; i < c->I; ++i) {
+            size_t j = 0;
+            while (j < distinct.size() && distinct[j] != c->disc[(size_t)i]) ++j;
+            if (j == distinct.size()) distinct.push_back(c->disc[(size_t)i]);
+            off[(size_t)i] = per * j;
+        }
+        double* ls = nullptr;
+        uint64_t* d_off = nullptr;
+        cudaError_t e;
+        ls = dalloc<double>(per * distinct.size(), e);
+        if (e != cudaSuccess) return fail(c, SPDP_ENOMEM, "log-Stirling table: %s", cudaGetErrorString(e));
+        d_off = dalloc<uint64_t>((size_t)c->I, e);
+        if (e != cudaSuccess) { cudaFree(ls); return fail(c, SPDP_ENOMEM, "log-Stirling offsets"); }
+        cudaMemcpyAsync(d_off, off.data(), sizeof(uint64_t) * off.size(), cudaMemcpyHostToDevice, c->stream);
+        for (size_t j = 0; j < distinct.size(); ++j)
+            build_log_stirling<<<1, 1024, 0, c->stream>>>(ls + per * j, c->mmax, distinct[j]);
+        const int grid = 296;
+        double* part = c->d_partial;       // [0, grid) words, [grid, 2 grid) docs
+        loglik_words_kernel<<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_Q, ls, d_off, c->V, c->I, c->K, c->Kp,
+                                                        c->cfg.beta, part);
+        loglik_docs_kernel<<<grid, 256, 0, c->stream>>>(c->d_n, c->d_doclen, c->d_docgroup, c->d_alpha64, c->d_alpha_sum64,
+                                                       c->Dloc, c->K, c->Kp, part + grid);
+        loglik_small_kernel<<<1, 1024, 0, c->stream>>>(c->d_M, c->d_Tt, c->d_T, c->d_disc64, c->d_conc64, c->I, c->K, c->Kp,
+                                                      (double)c->V * c->cfg.beta, part + 2 * grid);
+        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(part, 2 * grid + 1, c->d_scalar + 1);   // words + docs + small
+        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(part + grid, grid, c->d_scalar + 2);    // docs only
+        if ((s = check_launch(c, "loglik kernels"))) { cudaFree(ls); cudaFree(d_off); return s; }
+        double v[2] = {0, 0};
+        CU(cudaMemcpyAsync(v, c->d_scalar + 1, sizeof(double) * 2, cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "log_joint"))) { cudaFree(ls); cudaFree(d_off); return s; }
+        cudaFree(ls);
+        cudaFree(d_off);
+        double total = v[0];
+        if (gather) {
+            // replicated terms once (rank 0), doc terms from every rank
+            double mine = (c->rank == 0) ? v[0] : v[1];
+            CU(cudaMemcpyAsync(c->d_scalar + 3, &mine, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            if ((s = nccl_check(c, c->nccl.AllReduce(c->d_scalar + 3, c->d_scalar + 3, 1, kNcclFloat64, kNcclSum, c->comm, c->stream), "allreduce lj")))
+                return s;
+            CU(cudaMemcpyAsync(&total, c->d_scalar + 3, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            if ((s = sync(c, "log_joint gather"))) return s;
+        }
+        *log_joint = total;
+    }
+    return SPDP_OK;
+}
+
+spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, double* probs, int32_t* info) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (n < 0 || (n > 0 && (!tok_ids || !probs))) return fail(c, SPDP_EINVAL, "bad debug_probs arguments");
+    if (n == 0) return SPDP_OK;
+    const int I = c->I, K = c->K;
+    std::vector<uint32_t> tdoc((size_t)n), tid((size_t)n), cs((size_t)n + 1), seg((size_t)n);
+    std::vector<uint16_t> zr((size_t)n);
+    std::vector<uint16_t> allzr((size_t)c->Nloc);
+    CU(cudaMemcpyAsync(allzr.data(), c->d_zr, sizeof(uint16_t) * allzr.size(), cudaMemcpyDeviceToHost, c->stream));
+    if ((s = sync(c, "debug zr"))) return s;
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t p = tok_ids[j];
+        if (p < 0 || p >= c->N || c->pos_of_tok[(size_t)p] < 0) return fail(c, SPDP_EINVAL, "token %lld is not on this rank", (long long)p);
+        tdoc[(size_t)j] = (uint32_t)c->local_of_doc[(size_t)c->doc[(size_t)p]];
+        tid[(size_t)j] = (uint32_t)p;
+        zr[(size_t)j] = allzr[(size_t)c->pos_of_tok[(size_t)p]];
+        cs[(size_t)j] = (uint32_t)j;
+        seg[(size_t)j] = (uint32_t)c->word[(size_t)p] * (uint32_t)I + (uint32_t)c->group[(size_t)p];
+    }
+    cs[(size_t)n] = (uint32_t)n;
+    uint32_t *d_doc = nullptr, *d_id = nullptr, *d_cs = nullptr, *d_seg = nullptr;
+    uint16_t* d_zr = nullptr;
+    double* d_w = nullptr;
+    int32_t* d_info = nullptr;
+    ALLOC(d_doc, n); ALLOC(d_id, n); ALLOC(d_cs, n + 1); ALLOC(d_seg, n); ALLOC(d_zr, n);
+    ALLOC(d_w, (size_t)n * 2 * K); ALLOC(d_info, (size_t)n * 4);
+    CU(cudaMemcpyAsync(d_doc, tdoc.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(d_id, tid.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(d_cs, cs.data(), 4 * ((size_t)n + 1), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(d_seg, seg.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(d_zr, zr.data(), 2 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+    SweepArgs a = base_args(c);
+    a.tok_doc = d_doc; a.tok_id = d_id; a.zr = d_zr; a.zr_next = nullptr;
+    a.chunk_start = d_cs; a.chunk_seg = d_seg; a.nchunks = (int)n;
+    a.dbg_w = d_w; a.dbg_info = d_info;
+    launch_sample(c, a, true);
+    normalise_rows_kernel<<<(int)((n + 127) / 128), 128, 0, c->stream>>>(d_w, (int)n, 2 * K);
+    if ((s = check_launch(c, "debug sample_kernel"))) return s;
+    CU(cudaMemcpyAsync(probs, d_w, sizeof(double) * (size_t)n * 2 * K, cudaMemcpyDeviceToHost, c->stream));
+    if (info) CU(cudaMemcpyAsync(info, d_info, sizeof(int32_t) * (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
+    s = sync(c, "debug_probs");
+    for (void* p : {(void*)d_doc, (void*)d_id, (void*)d_cs, (void*)d_seg, (void*)d_zr, (void*)d_w, (void*)d_info}) {
+        cudaFree(p);
+        c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
+    }
+    // keep-rule tokens: the conditional is the point mass on (k0, r=1)
+    if (!s && info)
+        for (int64_t j = 0; j < n; ++j)
+            if (info[4 * j + 1]) {
+                for (int q = 0; q < 2 * K; ++q) probs[(size_t)j * 2 * K + q] = 0.0;
+                probs[(size_t)j * 2 * K + 2 * (zr[(size_t)j] & 0x7FFF)] = 1.0;
+            }
+    return s;
+}
+
+spdp_status spdp_nccl_unique_id(void* out) {
+    if (!out) return SPDP_EINVAL;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return SPDP_ENCCL;
+    auto fn = (int (*)(NcclUid*))dlsym(lib, "ncclGetUniqueId");
+    if (!fn) return SPDP_ENCCL;
+    NcclUid uid;
+    if (fn(&uid) != 0) return SPDP_ENCCL;
+    std::memcpy(out, uid.b, 128);
+    return SPDP_OK;
+}
+
+spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    unsigned long long st[8] = {0};
+    CU(cudaMemcpyAsync(st, c->d_stats, sizeof st, cudaMemcpyDeviceToHost, c->stream));
+    if ((s = sync(c, "stats"))) return s;
+    out[0] = (int64_t)st[0]; out[1] = (int64_t)st[1]; out[2] = (int64_t)st[2];
+    out[3] = c->sweeps_done; out[4] = c->Nloc; out[5] = c->Dloc; out[6] = c->mmax; out[7] = (int64_t)c->chunk_seg.size();
+    return SPDP_OK;
+}
+
+void spdp_destroy(spdp_ctx* c) {
+    if (!c) return;
+    if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->comm && c->nccl.CommDestroy) c->nccl.CommDestroy(c->comm);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // extern "C"
+
+namespace {
+// debug_checks: recount n and m from z, check 0 <= t <= m, t > 0 iff m > 0, Q = sum_i t.
+spdp_status debug_verify(spdp_ctx* c) {
+    const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
+    std::vector<uint16_t> zr((size_t)c->Nloc);
+    std::vector<int32_t> n((size_t)c->Dloc * Kp), m(c->cells), t(c->cells), Q((size_t)V * Kp);
+    CU(cudaMemcpy(zr.data(), c->d_zr, 2 * zr.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(n.data(), c->d_n, 4 * n.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(m.data(), c->d_m, 4 * m.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(t.data(), c->d_t, 4 * t.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(Q.data(), c->d_Q, 4 * Q.size(), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> n2((size_t)c->Dloc * Kp, 0);
+    for (int64_t q = 0; q < c->Nloc; ++q) {
+        const uint32_t p = c->sorted_tok[(size_t)q];
+        n2[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + (zr[(size_t)q] & 0x7FFF)]++;
+    }
+    if (n2 != n) return fail(c, SPDP_EINTEGRITY, "doc-topic counts differ from a recount of z");
+    int64_t sm = 0;
+    for (int w = 0; w < V; ++w)
+        for (int k = 0; k < K; ++k) {
+            int64_t q = 0;
+            for (int i = 0; i < I; ++i) {
+                const size_t cell = ((size_t)w * I + i) * Kp + k;
+                if (t[cell] < 0 || t[cell] > m[cell] || ((t[cell] > 0) != (m[cell] > 0)))
+                    return fail(c, SPDP_EINTEGRITY, "t out of [min(1,m), m] at (i=%d, w=%d, k=%d)", i, w, k);
+                q += t[cell];
+                sm += m[cell];
+            }
+            if (q != Q[(size_t)w * Kp + k]) return fail(c, SPDP_EINTEGRITY, "Q != sum_i t at (w=%d, k=%d)", w, k);
+        }
+    if (c->G == 1 && sm != c->N) return fail(c, SPDP_EINTEGRITY, "sum m = %lld != N", (long long)sm);
+    return SPDP_OK;
+}
+}  // namespace

@@ -1,0 +1,524 @@
+// spdp_device.cuh — sm_100a kernels of the SPDP Gibbs sweep.
+//
+// Notation follows PAPER.md §2.4.5: z topic, r table indicator, n_{dk}
+// doc-topic counts, m_{ikw} customers and t_{ikw} tables of dish w in
+// restaurant (group i, topic k), Q_{kw} = sum_i t_{ikw} shadow counts (identity
+// P), M_{ik} = m_{ik.}, Tt_{ik} = t_{ik.}, T_k = sum_w Q_{kw}.
+//
+// Layout in HBM: every count row is padded to Kp = round_up(K, 4)
+// int32 so rows are 16-byte aligned for vector loads.
+//   n  [D_local][Kp]      doc-topic, this rank's documents
+//   m,t[V][I][Kp]          word-major: the rows of one (w, i) segment are adjacent
+//   Q  [V][Kp]             shadow counts, word-major
+//   M,Tt [I][Kp], T [Kp]   marginal sums
+//   tokens, sorted by (wave, w, i, doc): doc (u32 local), id (u32 canonical), zr (u16 z | r<<15)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace spdp {
+
+constexpr int kWarps = 4;          // warps per block of the sample kernel
+constexpr uint32_t kRBit = 0x8000u;
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Counter-based RNG (Salmon et al. 2011), keyed by the seed, counter
+// (token, sweep, 0, 0) — DESIGN.md reading c11.
+__device__ __forceinline__ uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+// 53-bit uniform in [0,1): x1 * 2^21 + (x2 >> 11), exact in fp64.
+__device__ __forceinline__ double u53(uint4 x) {
+    return fma((double)x.y, 2097152.0, (double)(x.z >> 11)) * (1.0 / 9007199254740992.0);
+}
+// Removal indicator r ~ Bernoulli(t/m) (Alg.1 line 3), exact in integers.
+__device__ __forceinline__ int removal_draw(uint32_t x0, int m, int t) {
+    return ((uint64_t)x0 * (uint64_t)(uint32_t)m) < ((uint64_t)(uint32_t)t << 32);
+}
+
+__device__ __forceinline__ uint64_t tri(int m) { return (uint64_t)m * (uint64_t)(m + 1) / 2; }
+
+// ---------------------------------------------------------------- Stirling ratio table
+// A0(m,t) = (m-t+1)/(m+1) * S^{m+1}_t / S^m_t      (Eq. r0)
+// A1(m,t) = (t+1)/(m+1)   * S^{m+1}_{t+1} / S^m_t  (Eq. r1)
+// for 0 <= t <= m <= mmax, stored as float2 at tri(m) + t.  Built row by row
+// in fp64 from q_N(M) = S^N_{M+1} / S^N_M (1 <= M <= N, q_N(N) = 0), which the
+// recursion S^{N+1}_M = S^N_{M-1} + (N - M a) S^N_M turns into
+//   q_{N+1}(M) = (1 + (N - (M+1) a) q_N(M)) / (1/q_N(M-1) + N - M a),  2 <= M <= N
+//   q_{N+1}(1) = (1 + (N - 2a) q_N(1)) / (N - a)
+// and then A0(m,t) = (m-t+1)/(m+1) * (1/q_m(t-1) + m - t a) (t >= 2),
+// A0(m,1) = (m - a) m/(m+1), A1(m,t) = (t+1)/(m+1) * (1 + (m - (t+1) a) q_m(t)).
+// No logarithms and no overflow: every quantity is a bounded ratio.
+// One block per distinct discount; q rows ping-pong in global scratch.
+__global__ void build_ratio_table(float2* __restrict__ tab, double* __restrict__ scratch, int mmax, double a) {
+    double* q0 = scratch;                  // row N
+    double* q1 = scratch + (mmax + 2);     // row N+1
+    // row m = 0: A0(0,0) = 0, A1(0,0) = 1
+    if (threadIdx.x == 0) {
+        tab[0] = make_float2(0.f, 1.f);
+        q0[1] = 0.0;                        // q_1(1) = 0 (S^1_2 = 0)
+    }
+    __syncthreads();
+    for (int N = 1; N <= mmax; ++N) {
+        // emit row m = N from q_N
+        const double inv = 1.0 / (double)(N + 1);
+        for (int t = threadIdx.x; t <= N; t += blockDim.x) {
+            float A0, A1;
+            if (t == 0) { A0 = 0.f; A1 = 0.f; }   // t = 0 < m is not a valid state
+            else {
+                const double s0 = (t == 1) ? ((double)N - a) : (1.0 / q0[t - 1] + (double)N - (double)t * a);
+                A0 = (float)((double)(N - t + 1) * inv * s0);
+                A1 = (float)((double)(t + 1) * inv * (1.0 + ((double)N - (double)(t + 1) * a) * q0[t]));
+            }
+            tab[tri(N) + t] = make_float2(A0, A1);
+        }
+        if (N == mmax) break;
+        // q_{N+1} from q_N
+        for (int M = threadIdx.x + 1; M <= N + 1; M += blockDim.x) {
+            double v;
+            if (M == N + 1) v = 0.0;
+            else if (M == 1) v = (1.0 + ((double)N - 2.0 * a) * q0[1]) / ((double)N - a);
+            else v = (1.0 + ((double)N - (double)(M + 1) * a) * q0[M]) / (1.0 / q0[M - 1] + (double)N - (double)M * a);
+            q1[M] = v;
+        }
+        __syncthreads();
+        double* tmp = q0; q0 = q1; q1 = tmp;
+    }
+}
+
+// ---------------------------------------------------------------- shared weight factor
+// Per (group i, topic k, word w) factor of the 2K weights, with the doc term
+// (alpha_ik + n_dk) left out:
+//   F0 = A0(m,t) / (b + M)                                         (Eq. r0)
+//   F1 = A1(m,t) (b + a Tt) / (b + M) * (beta + Q) / (V beta + T)  (Eq. r1)
+__device__ __forceinline__ void slot_factors(int M, int Tt, int Qv, int Tk, float2 A, float a, float b,
+                                             float beta, float vbeta, float& F0, float& F1) {
+    const float C0 = 1.0f / (b + (float)M);
+    F0 = A.x * C0;
+    F1 = A.y * ((b + a * (float)Tt) * C0) * ((beta + (float)Qv) / (vbeta + (float)Tk));
+}
+
+struct SweepArgs {
+    // tokens of this rank, sorted by (wave, w, i, doc)
+    const uint32_t* tok_doc;
+    const uint32_t* tok_id;
+    uint16_t* zr;
+    uint16_t* zr_next;
+    // chunks (warp work units) of the launched wave
+    const uint32_t* chunk_start;   // [nchunks + 1] absolute token offsets
+    const uint32_t* chunk_seg;     // [nchunks] segment = w * I + i
+    int nchunks;
+    // counts
+    int32_t* n;
+    int32_t* m;
+    int32_t* t;
+    int32_t* Q;
+    int32_t* M;
+    int32_t* Tt;
+    int32_t* T;
+    int32_t* dm;                   // raw wave deltas [V][I][Kp]
+    int32_t* dt;
+    const float* alpha;            // [I][Kp] (0 on padding)
+    const float* disc;             // [I]
+    const float* conc;             // [I]
+    const float2* tab;             // concatenated ratio tables
+    const uint64_t* tab_off;       // [I] offset of group i's table
+    float beta, vbeta;
+    int I, K, Kp;
+    uint32_t key0, key1;
+    const uint32_t* sweep;         // device counter (RNG counter word 1)
+    unsigned long long* stats;     // [8]
+    // debug_probs
+    double* dbg_w;                 // [ntok][2K] unnormalised weights, or null
+    int32_t* dbg_info;             // [ntok][4]
+};
+
+// ---------------------------------------------------------------- the sample kernel
+// One warp per chunk of one (w, i) segment; LPT lanes per token (TPW = 32/LPT
+// tokens in flight per warp), each lane owning KPL consecutive topics.
+// Steps per token:
+//   a2 Philox(seed; id, sweep)  a3 removal against the wave-start snapshot
+//   a4/a5 weights (alpha+n_dk) F_k with the own-removal correction at k0
+//   a6 fp64 prefix (lane-local, then a group scan), first slot whose prefix
+//      exceeds u*total, slots in the paper's order j = 2k (r=1), 2k+1 (r=0)
+//   a7 zr_next, and the segment's (delta m, delta t) accumulated in smem,
+//      flushed once per chunk with integer atomics (deterministic).
+template <int LPT, int KPL, bool DEBUG>
+__global__ void __launch_bounds__(kWarps * 32)
+sample_kernel(SweepArgs A) {
+    constexpr int TPW = 32 / LPT;
+    constexpr int KSPAN = LPT * KPL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWarps + wid;
+    if (c >= A.nchunks) return;                      // warp-uniform
+
+    float* sF0 = reinterpret_cast<float*>(smem_raw) + (size_t)wid * KSPAN * 6;
+    float* sF1 = sF0 + KSPAN;
+    int* sm = reinterpret_cast<int*>(sF1 + KSPAN);
+    int* st = sm + KSPAN;
+    int* sdm = st + KSPAN;
+    int* sdt = sdm + KSPAN;
+
+    const uint32_t seg = A.chunk_seg[c];
+    const int I = A.I, K = A.K, Kp = A.Kp;
+    const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
+    const size_t row = (size_t)seg * Kp;
+    const float a = A.disc[i], b = A.conc[i];
+    const float2* __restrict__ tab = A.tab + A.tab_off[i];
+    const int32_t* __restrict__ Mi = A.M + (size_t)i * Kp;
+    const int32_t* __restrict__ Tti = A.Tt + (size_t)i * Kp;
+    const int32_t* __restrict__ Qw = A.Q + (size_t)w * Kp;
+
+    // prologue: the segment's slot factors F0_k, F1_k (wave-start snapshot)
+    for (int k = lane; k < KSPAN; k += 32) {
+        float F0 = 0.f, F1 = 0.f;
+        int mv = 0, tv = 0;
+        if (k < K) {
+            mv = A.m[row + k];
+            tv = A.t[row + k];
+            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+        }
+        sF0[k] = F0; sF1[k] = F1; sm[k] = mv; st[k] = tv; sdm[k] = 0; sdt[k] = 0;
+    }
+    __syncwarp();
+
+    const int g = lane / LPT, gl = lane % LPT;
+    const int kb = gl * KPL;                          // first topic of this lane
+    const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
+    float F0[KPL], F1[KPL], al[KPL];
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+        F0[j] = sF0[kb + j];
+        F1[j] = sF1[kb + j];
+        al[j] = (kb + j < K) ? A.alpha[(size_t)i * Kp + kb + j] : 0.f;
+    }
+    const uint32_t sweep = *A.sweep;
+    const uint32_t start = A.chunk_start[c], end = A.chunk_start[c + 1];
+    unsigned keeps = 0, moved = 0;
+
+    for (uint32_t base = start; base < end; base += TPW) {
+        const uint32_t tok = base + g;
+        const bool valid = tok < end;
+        uint32_t doc = 0, id = 0, zr0 = 0;
+        if (valid) { doc = A.tok_doc[tok]; id = A.tok_id[tok]; zr0 = A.zr[tok]; }
+        const uint4 x = philox(make_uint4(id, sweep, 0u, 0u), A.key0, A.key1);       // a2
+        const int k0 = (int)(zr0 & 0x7FFFu);
+        const int m0 = sm[k0], t0 = st[k0];
+        const int rrem = removal_draw(x.x, m0, t0);                                   // a3
+        const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
+
+        // own-removal factors of topic k0 (Alg.1 lines 4-10)
+        float F0k0, F1k0;
+        {
+            const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
+            slot_factors(Mi[k0] - 1, Tti[k0] - rrem, Qw[k0] - rrem, A.T[k0] - rrem,
+                         tab[tri(mm) + tt], a, b, A.beta, A.vbeta, F0k0, F1k0);
+        }
+        // a4: doc-topic row (vectorised, predicated per 4-topic block)
+        int nv[KPL];
+        const int32_t* nrow = A.n + (size_t)doc * Kp + kb;
+        if constexpr (KPL % 4 == 0) {
+#pragma unroll
+            for (int q = 0; q < KPL / 4; ++q) {
+                int4 v = make_int4(0, 0, 0, 0);
+                if (kb + 4 * q < K) v = __ldg(reinterpret_cast<const int4*>(nrow) + q);
+                nv[4 * q] = v.x; nv[4 * q + 1] = v.y; nv[4 * q + 2] = v.z; nv[4 * q + 3] = v.w;
+            }
+        } else if constexpr (KPL == 2) {
+            int2 v = make_int2(0, 0);
+            if (kb < K) v = __ldg(reinterpret_cast<const int2*>(nrow));
+            nv[0] = v.x; nv[1] = v.y;
+        } else {
+            nv[0] = (kb < K) ? __ldg(nrow) : 0;
+        }
+        // a5: slot masses w1 = (alpha+n) F1, w0 = (alpha+n) F0 in fp32; a6: fp64 prefix in slot order
+        float w1v[KPL], w0v[KPL];
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j) {
+            const bool own = (kb + j == k0);
+            const float base = al[j] + (float)(nv[j] - (own ? 1 : 0));
+            w1v[j] = base * (own ? F1k0 : F1[j]);
+            w0v[j] = base * (own ? F0k0 : F0[j]);
+            acc += (double)w1v[j];
+            acc += (double)w0v[j];
+        }
+        double incl = acc;
+#pragma unroll
+        for (int off = 1; off < LPT; off <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
+            if (gl >= off) incl += y;
+        }
+        double excl = __shfl_up_sync(0xffffffffu, incl, 1, LPT);
+        if (gl == 0) excl = 0.0;
+        const double total = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
+        const double target = u53(x) * total;
+        const unsigned hit = __ballot_sync(0xffffffffu, incl > target) & gmask;
+        const unsigned pos = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
+        const bool fb = (hit == 0u);
+        const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
+        int slot = -1, last = 0;
+        if (lane == winner) {
+            // j* = min{ j : prefix_j > u * total } over this lane's slots (reading c10)
+            double run = excl;
+#pragma unroll
+            for (int j = 0; j < KPL; ++j) {
+                const double r1 = run + (double)w1v[j];
+                const double r0 = r1 + (double)w0v[j];
+                if (slot < 0) {
+                    if (r1 > target) slot = 2 * (kb + j);
+                    else if (r0 > target) slot = 2 * (kb + j) + 1;
+                }
+                if (w1v[j] > 0.f) last = 2 * (kb + j);
+                if (w0v[j] > 0.f) last = 2 * (kb + j) + 1;
+                run = r0;
+            }
+            if (fb || slot < 0) slot = last;   // rounding: the last slot with positive mass
+        }
+        slot = __shfl_sync(0xffffffffu, slot, winner);
+        int ks = slot >> 1, rs = (slot & 1) ? 0 : 1;
+        if (keep) { ks = k0; rs = 1; }
+
+        if constexpr (DEBUG) {
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < KPL; ++j) {
+                    const int k = kb + j;
+                    if (k < K) {
+                        A.dbg_w[(size_t)tok * 2 * K + 2 * k] = (double)w1v[j];
+                        A.dbg_w[(size_t)tok * 2 * K + 2 * k + 1] = (double)w0v[j];
+                    }
+                }
+                if (gl == 0) {
+                    int32_t* inf = A.dbg_info + (size_t)tok * 4;
+                    inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
+                }
+            }
+        } else {
+            if (valid && gl == 0) {                                                   // a7
+                A.zr_next[tok] = (uint16_t)(ks | (rs << 15));
+                if (keep) ++keeps;
+                else {
+                    atomicAdd(&sdm[k0], -1); atomicAdd(&sdt[k0], -rrem);
+                    atomicAdd(&sdm[ks], 1); atomicAdd(&sdt[ks], rs);
+                    moved += (ks != k0);
+                }
+            }
+        }
+    }
+    if constexpr (!DEBUG) {
+        __syncwarp();
+        for (int k = lane; k < K; k += 32) {
+            const int dmv = sdm[k], dtv = sdt[k];
+            if (dmv) atomicAdd(A.dm + row + k, dmv);
+            if (dtv) atomicAdd(A.dt + row + k, dtv);
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            keeps += __shfl_xor_sync(0xffffffffu, keeps, off);
+            moved += __shfl_xor_sync(0xffffffffu, moved, off);
+        }
+        if (lane == 0 && (keeps | moved)) {
+            atomicAdd(A.stats + 0, (unsigned long long)keeps);
+            atomicAdd(A.stats + 1, (unsigned long long)moved);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- end of wave: n and z
+// n_{d k0} -= 1, n_{d k*} += 1 for every token of the wave that moved; zr <- zr_next.
+__global__ void apply_tokens_kernel(const uint32_t* __restrict__ tok_doc, uint16_t* __restrict__ zr,
+                                    const uint16_t* __restrict__ zr_next, int32_t* __restrict__ n,
+                                    int Kp, uint32_t begin, uint32_t end) {
+    for (uint32_t p = begin + blockIdx.x * blockDim.x + threadIdx.x; p < end; p += gridDim.x * blockDim.x) {
+        const uint32_t zo = zr[p], zn = zr_next[p];
+        const uint32_t ko = zo & 0x7FFFu, kn = zn & 0x7FFFu;
+        if (ko != kn) {
+            int32_t* nr = n + (size_t)tok_doc[p] * Kp;
+            atomicSub(nr + ko, 1);
+            atomicAdd(nr + kn, 1);
+        }
+        zr[p] = (uint16_t)zn;
+    }
+}
+
+// ---------------------------------------------------------------- end of wave: rows, clamp, sums
+// For every (w, i) row: m += dm, t = clamp(t + dt) into [min(1,m), m]
+// (PAPER.md:2411-2419 correction; reading c14), dm = dt = 0; with a
+// net-change buffer (multi-GPU) D += (new - old).  Then Q_w = sum_i t, and the
+// marginal sums M, Tt, T are accumulated into zeroed buffers.
+// One warp per word; int4 over topics.
+__global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t,
+                                  int32_t* __restrict__ dm, int32_t* __restrict__ dt,
+                                  int32_t* __restrict__ Dm, int32_t* __restrict__ Dt,
+                                  int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
+                                  int32_t* __restrict__ T, int V, int I, int Kp, int use_smem_sums,
+                                  unsigned long long* __restrict__ stats) {
+    extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
+    int* sM = ssum;
+    int* sT = ssum + (size_t)I * Kp;
+    int* sK = ssum + (size_t)2 * I * Kp;
+    if (use_smem_sums) {
+        for (int j = threadIdx.x; j < (2 * I + 1) * Kp; j += blockDim.x) ssum[j] = 0;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    unsigned clamped = 0;
+    for (int w = blockIdx.x * wpb + (threadIdx.x >> 5); w < V; w += gridDim.x * wpb) {
+        for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
+            int4 q = make_int4(0, 0, 0, 0);
+            for (int i = 0; i < I; ++i) {
+                const size_t off = ((size_t)w * I + i) * Kp + k4;
+                int4 vm = *reinterpret_cast<const int4*>(m + off);
+                int4 vt = *reinterpret_cast<const int4*>(t + off);
+                const int4 a = *reinterpret_cast<const int4*>(dm + off);
+                const int4 d = *reinterpret_cast<const int4*>(dt + off);
+                if ((a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) != 0) {
+                    const int4 om = vm, ot = vt;
+                    int* pm = &vm.x; int* pt = &vt.x;
+                    const int* pa = &a.x; const int* pd = &d.x;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int mv = pm[e] + pa[e];
+                        const int raw = pt[e] + pd[e];
+                        int tv = min(raw, mv);
+                        tv = (mv > 0) ? max(tv, 1) : 0;
+                        clamped += (tv != raw);
+                        pm[e] = mv; pt[e] = tv;
+                    }
+                    *reinterpret_cast<int4*>(m + off) = vm;
+                    *reinterpret_cast<int4*>(t + off) = vt;
+                    *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
+                    *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
+                    if (Dm) {
+                        int4 x = *reinterpret_cast<int4*>(Dm + off), y = *reinterpret_cast<int4*>(Dt + off);
+                        x.x += vm.x - om.x; x.y += vm.y - om.y; x.z += vm.z - om.z; x.w += vm.w - om.w;
+                        y.x += vt.x - ot.x; y.y += vt.y - ot.y; y.z += vt.z - ot.z; y.w += vt.w - ot.w;
+                        *reinterpret_cast<int4*>(Dm + off) = x;
+                        *reinterpret_cast<int4*>(Dt + off) = y;
+                    }
+                }
+                q.x += vt.x; q.y += vt.y; q.z += vt.z; q.w += vt.w;
+                const int* pm = &vm.x; const int* pt = &vt.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (pm[e]) {
+                        if (use_smem_sums) { atomicAdd(sM + (size_t)i * Kp + k4 + e, pm[e]); atomicAdd(sT + (size_t)i * Kp + k4 + e, pt[e]); }
+                        else { atomicAdd(M + (size_t)i * Kp + k4 + e, pm[e]); atomicAdd(Tt + (size_t)i * Kp + k4 + e, pt[e]); }
+                    }
+                }
+            }
+            *reinterpret_cast<int4*>(Q + (size_t)w * Kp + k4) = q;
+            const int* pq = &q.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (pq[e]) { if (use_smem_sums) atomicAdd(sK + k4 + e, pq[e]); else atomicAdd(T + k4 + e, pq[e]); }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) clamped += __shfl_xor_sync(0xffffffffu, clamped, off);
+    if (lane == 0 && clamped) atomicAdd(stats + 2, (unsigned long long)clamped);
+    if (use_smem_sums) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < I * Kp; j += blockDim.x) {
+            if (sM[j]) atomicAdd(M + j, sM[j]);
+            if (sT[j]) atomicAdd(Tt + j, sT[j]);
+        }
+        for (int j = threadIdx.x; j < Kp; j += blockDim.x) if (sK[j]) atomicAdd(T + j, sK[j]);
+    }
+}
+
+// Multi-GPU merge (Alg.3): restore the sweep-start state
+// S0 = L - D before the exchange ...
+__global__ void unapply_net_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t,
+                                   const int32_t* __restrict__ Dm, const int32_t* __restrict__ Dt, size_t cells) {
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < cells; j += (size_t)gridDim.x * blockDim.x) {
+        m[j] -= Dm[j];
+        t[j] -= Dt[j];
+    }
+}
+// ... and after it: m = S0 + sum_g D_g, t likewise, through merge_rows_kernel
+// with (dm, dt) = the all-reduced D.
+
+__global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
+
+// ---------------------------------------------------------------- training perplexity
+// One warp per chunk (all waves): phi^i_kw = (m - a t)/(b + M) + (b + a Tt)/(b + M) phi0_kw,
+// phi0_kw = (beta + Q)/(V beta + T) (reading c16);
+// per token log sum_k (n_dk + alpha_ik) phi^i_kw / (L_d + sum_k alpha_ik).
+// Per-chunk fp64 partials (fixed order) -> deterministic final reduction.
+template <int LPT, int KPL>
+__global__ void __launch_bounds__(kWarps * 32)
+perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const float* __restrict__ alpha_sum,
+                  double* __restrict__ partial) {
+    constexpr int TPW = 32 / LPT;
+    constexpr int KSPAN = LPT * KPL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int c = blockIdx.x * kWarps + wid;
+    if (c >= A.nchunks) return;
+    double* sphi = reinterpret_cast<double*>(smem_raw) + (size_t)wid * KSPAN;
+    const uint32_t seg = A.chunk_seg[c];
+    const int I = A.I, K = A.K, Kp = A.Kp;
+    const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
+    const size_t row = (size_t)seg * Kp;
+    const double a = A.disc[i], b = A.conc[i];
+    for (int k = lane; k < KSPAN; k += 32) {
+        double phi = 0.0;
+        if (k < K) {
+            const double Mk = A.M[(size_t)i * Kp + k], Tk = A.Tt[(size_t)i * Kp + k];
+            const double phi0 = ((double)A.beta + (double)A.Q[(size_t)w * Kp + k]) / ((double)A.vbeta + (double)A.T[k]);
+            phi = ((double)A.m[row + k] - a * (double)A.t[row + k]) / (b + Mk) + (b + a * Tk) / (b + Mk) * phi0;
+        }
+        sphi[k] = phi;
+    }
+    __syncwarp();
+    const int g = lane / LPT, gl = lane % LPT, kb = gl * KPL;
+    double al[KPL];
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) al[j] = (kb + j < K) ? (double)A.alpha[(size_t)i * Kp + kb + j] : 0.0;
+    const double asum = (double)alpha_sum[i];
+    double ll = 0.0;
+    const uint32_t start = A.chunk_start[c], end = A.chunk_start[c + 1];
+    for (uint32_t base = start; base < end; base += TPW) {
+        const uint32_t tok = base + g;
+        const bool valid = tok < end;
+        const uint32_t doc = valid ? A.tok_doc[tok] : 0u;
+        const int32_t* nrow = A.n + (size_t)doc * Kp + kb;
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < KPL; ++j)
+            if (kb + j < K) s += ((double)__ldg(nrow + j) + al[j]) * sphi[kb + j];
+#pragma unroll
+        for (int off = LPT / 2; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, LPT);
+        if (valid && gl == 0) ll += log(s / ((double)doclen[doc] + asum));
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, off);
+    if (lane == 0) partial[c] = ll;
+}
+
+// Fixed-order reduction of n doubles by one block (deterministic).
+__global__ void reduce_fixed_kernel(const double* __restrict__ x, size_t n, double* __restrict__ out) {
+    __shared__ double s[1024];
+    double acc = 0.0;
+    for (size_t j = threadIdx.x; j < n; j += blockDim.x) acc += x[j];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h; h >>= 1) {
+        if ((int)threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = s[0];
+}
+
+}  // namespace spdp

@@ -1,0 +1,161 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+north_star (5): conditional probabilities within 1e-5 relative error; draw
+mismatches <= 1e-4 of tokens and only where the uniform lies within 1e-6 of
+a CDF boundary; count tables bit-exact whenever the draws agree.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1510_06549_b200 as spdp
+import synth
+from gpu_util import (HYPER, assert_counts_equal, assert_draw_parity, corpus, lockstep_sweep, pack, pair,
+                      require_gpu)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    require_gpu()
+
+
+def _probs_parity(g, o, toks, sweep):
+    gp, info = g.debug_probs(toks)
+    for j, p in enumerate(toks):
+        d = o.debug_token(int(p), sweep)
+        assert (info[j, 0], info[j, 1]) == (d["r_rem"], d["keep"]), (p, info[j], d)
+        op = d["prob"]
+        big = op >= 1e-30
+        rel = np.abs(gp[j][big] - op[big]) / op[big]
+        assert rel.max() <= 1e-5, (p, rel.max())
+        assert np.abs(gp[j][~big] - op[~big]).max(initial=0.0) <= 1e-12
+        if d["margin"] > 1e-6:
+            assert (info[j, 2], info[j, 3]) == (d["z"], d["r"]), (p, info[j], d)
+
+
+@pytest.mark.parametrize("name,K", [("C1", 10), ("C2", 50)])
+def test_conditionals_match_oracle(name, K):
+    c = corpus(name)
+    g, o = pair(c, K)
+    rng = np.random.default_rng(0)
+    toks = rng.choice(c.num_tokens, size=min(c.num_tokens, 3000), replace=False)
+    _probs_parity(g, o, toks, 0)
+    # after a few lock-step sweeps (non-trivial t, clamps)
+    for _ in range(3):
+        rep, gc = lockstep_sweep(g, o)
+        assert_draw_parity(rep)
+    _probs_parity(g, o, toks, o.sweep_index)
+
+
+@pytest.mark.parametrize("name,K,waves", [("C1", 10, 1), ("C1", 10, 4), ("C1", 10, 200), ("C2", 50, 1),
+                                          ("C2", 50, 3)])
+def test_one_sweep_from_identical_state(name, K, waves):
+    c = corpus(name)
+    g, o = pair(c, K, waves=waves)
+    rep, gc = lockstep_sweep(g, o, waves=waves)
+    assert_draw_parity(rep)
+    assert_counts_equal(gc, o.state())
+
+
+def test_twenty_lockstep_sweeps_c1():
+    c = corpus("C1")
+    g, o = pair(c, 10, waves=1)
+    for s in range(20):
+        rep, gc = lockstep_sweep(g, o)
+        assert_draw_parity(rep)
+        assert_counts_equal(gc, o.state())
+    st = g.stats()
+    assert st["sweeps"] == 20
+
+
+@pytest.mark.parametrize("K", [1, 3, 16, 17, 33, 100, 130, 300, 700, 1024])
+def test_topic_counts_edge_cases(K):
+    """Every kernel configuration (lanes-per-token x topics-per-lane), ragged K."""
+    c = synth.generate(2, 30, 40.0, 300, 8, seed=K)
+    g, o = pair(c, K, waves=2)
+    for _ in range(2):
+        rep, gc = lockstep_sweep(g, o, waves=2)
+        assert_draw_parity(rep)
+        assert_counts_equal(gc, o.state())
+
+
+def test_tiny_and_degenerate_corpora():
+    # single-token docs, a doc with one repeated word, unused words and groups
+    c = synth.tiny_corpus(3, [[0], [1, 1, 1, 1], [2, 0, 2], [5]], [0, 0, 1, 1], vocab=7)
+    g, o = pair(c, 2, waves=1)
+    for _ in range(5):
+        rep, gc = lockstep_sweep(g, o)
+        assert_draw_parity(rep)
+        assert_counts_equal(gc, o.state())
+
+
+def test_loglik_matches_oracle():
+    c = corpus("C1")
+    g, o = pair(c, 10)
+    for _ in range(3):
+        rep, gc = lockstep_sweep(g, o)
+    lj, ppl = g.loglik()
+    assert ppl == pytest.approx(o.perplexity(), rel=1e-9)
+    assert lj == pytest.approx(o.log_joint(), rel=1e-9)
+
+
+def test_determinism_and_invariants():
+    c = corpus("C1")
+    a = spdp.sampler_for(c, 10, seed=3, debug_checks=True, **HYPER)
+    b = spdp.sampler_for(c, 10, seed=3, **HYPER)
+    a.sweep(4); b.sweep(4)
+    ca, cb = a.counts(), b.counts()
+    for k in ca:
+        np.testing.assert_array_equal(ca[k], cb[k])
+    assert ca["m"].sum() == c.num_tokens
+    assert (ca["t"] <= ca["m"]).all() and ((ca["t"] > 0) == (ca["m"] > 0)).all()
+    np.testing.assert_array_equal(ca["Q"], ca["t"].sum(axis=0).T)
+
+
+def test_set_state_roundtrip_with_tables():
+    c = corpus("C1")
+    g, o = pair(c, 10)
+    for _ in range(2):
+        lockstep_sweep(g, o)
+    st = o.state()
+    h = spdp.sampler_for(c, 10, **HYPER)
+    h.set_state(st["z"], st["r"], st["t"])
+    hc = h.counts()
+    assert_counts_equal(hc, st, keys=("z", "n", "m", "t", "Q"))
+
+
+@pytest.mark.parametrize("G,waves", [(2, 1), (3, 2), (8, 1)])
+def test_multi_rank_exchange_matches_oracle_shards(G, waves):
+    """G ranks as G contexts on one GPU with the external exchange (host sum):
+    bit-exact against the oracle's G-shard simulation (reading c13-c15)."""
+    c = corpus("C1")
+    ranks = [spdp.sampler_for(c, 10, num_waves=waves, rank=r, world_size=G,
+                              exchange=spdp.SPDP_EXCHANGE_EXTERNAL, **HYPER) for r in range(G)]
+    o = oracle.from_corpus(c, 10, **HYPER)
+    for s in range(3):
+        for r in ranks:
+            r.sweep_local()
+        tot = sum(r.exchange_get().astype(np.int64) for r in ranks).astype(np.int32)
+        for r in ranks:
+            r.exchange_put(tot)
+            r.sweep_merge()
+        # gather the per-rank token state (each rank writes only its own tokens)
+        z = np.full(c.num_tokens, -1, np.int32); rr = np.zeros(c.num_tokens, np.uint8)
+        n = np.zeros((c.num_docs, 10), np.int32)
+        for r in ranks:
+            cr = r.counts()
+            own = np.asarray(spdp.spdp_partition(7, G, c.doc, c.num_docs))[c.doc] == ranks.index(r)
+            z[own] = cr["z"][own]; rr[own] = cr["r"][own]
+            owndoc = np.asarray(spdp.spdp_partition(7, G, c.doc, c.num_docs)) == ranks.index(r)
+            n[owndoc] = cr["n"][owndoc]
+        gc = ranks[0].counts()
+        gc.update(z=z, r=rr, n=n)
+        for r in ranks[1:]:
+            cr = r.counts()
+            for k in ("m", "t", "Q"):
+                np.testing.assert_array_equal(cr[k], gc[k])
+        rep, _ = lockstep_sweep(None, o, waves=waves, shards=G, gpu_counts=gc)
+        assert_draw_parity(rep)
+        assert_counts_equal(gc, o.state())
