@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""bench.py — sampled tokens/sec of the SPDP Gibbs sweep on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--waves 1] [--impl reference]
+
+One step = one full sweep (every token of the corpus sampled once) on a
+synthetic SPDP corpus shaped like the paper's multi-group collections
+(synth/).  N > 1 is launched with torch.distributed.run; the
+corpus (fixed total) is sharded by document over the ranks (strong scaling)
+and the count deltas are all-reduced over NCCL inside the library.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--topics", type=int, default=0, help="override K (C4's K sweep)")
+    ap.add_argument("--waves", type=int, default=1)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy b.copy_(a))"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 9:
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def alg_bytes(plan, K):
+    """Algorithmic HBM bytes of one sample-kernel pass:
+    per token 12 B of token record (doc, id, zr in; zr out) + 4K B doc-topic row;
+    per (w, i) segment 28K B (m, t, Q rows, A0/A1 table row in; dm, dt rows out)."""
+    return plan["tokens"] * (12 + 4 * K) + plan["segments"] * 28 * K
+
+
+def plan_stats(corpus, shard_docs, waves):
+    """Distinct (wave, w, i) segments and tokens of this rank (from the wave plan)."""
+    mask = np.isin(corpus.doc, shard_docs) if shard_docs is not None else np.ones(corpus.num_tokens, bool)
+    doc = corpus.doc[mask]
+    # in-document position l
+    order = np.argsort(corpus.doc, kind="stable")
+    pos = np.empty(corpus.num_tokens, np.int64)
+    d_sorted = corpus.doc[order]
+    starts = np.r_[0, np.nonzero(np.diff(d_sorted))[0] + 1]
+    run = np.arange(corpus.num_tokens) - np.repeat(starts, np.diff(np.r_[starts, corpus.num_tokens]))
+    pos[order] = run
+    key = ((pos[mask] % waves) * corpus.vocab + corpus.word[mask]).astype(np.int64) * corpus.num_groups + corpus.group[mask]
+    return {"tokens": int(doc.shape[0]), "segments": int(np.unique(key).shape[0])}
+
+
+def load_traffic(cfg_name, K):
+    p = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}_K{K}_sample.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+def cpu_baseline(corpus, cfg, K, waves, sample_tokens):
+    """The oracle as it stands, single thread, on a bounded sample of the same
+    workload: the first `sample_tokens` tokens of one mode-P sweep."""
+    import oracle
+    o = oracle.from_corpus(corpus, K, cfg.alpha, cfg.beta, cfg.discount, cfg.concentration, cfg.seed)
+    t0 = time.perf_counter()
+    o.sweep_par(waves=waves, shards=1, max_tokens=sample_tokens)
+    dt = time.perf_counter() - t0
+    return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {sample_tokens} tokens of one mode-P (W={waves}) sweep of {cfg.name} "
+                      f"(N={corpus.num_tokens}, K={K}); plain C oracle, fp64 log space, 1 thread; "
+                      f"{dt:.1f} s incl. the sweep's fixed per-wave passes"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    K = args.topics or cfg.k
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    workload = f"{cfg.name}: I={cfg.groups} groups x {cfg.docs_per_group} docs, mean len {cfg.mean_len}, " \
+               f"V={cfg.vocab}, K={K}, W={args.waves}"
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, K, world, rank, workload)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1510_06549_b200 as spdp
+
+    spdp.build()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local_rank))
+    corpus = synth.corpus_for(cfg)
+    N = corpus.num_tokens
+    uid = None
+    if world > 1:
+        t = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            t = torch.tensor(list(spdp.spdp_nccl_unique_id()), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        uid = bytes(t.tolist())
+    stream = torch.cuda.current_stream()
+    kw = dict(alpha=cfg.alpha, beta=cfg.beta, discount=cfg.discount, concentration=cfg.concentration,
+              seed=cfg.seed, num_waves=args.waves, device=local_rank, rank=rank, world_size=world,
+              nccl_unique_id=uid, stream=stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- device-resident throughput (value) ----------------
+    g = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
+    g.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs)
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        g.sweep(1)
+    g.profile(True)
+    torch.cuda.synchronize(); barrier()
+    evs = []
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize(); barrier()
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)                      # evict L2 between timed sweeps (outside the events)
+            s = torch.cuda.Event(enable_timing=True); e = torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            g.sweep(1)
+            e.record(stream)
+            evs.append((s, e))
+        torch.cuda.synchronize(); barrier()
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    tm = g.timings()
+    g.profile(False)
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = N / (ms / 1e3)
+    stats = g.stats()
+    _, ppl = g.loglik(log_joint=False)
+    g.close()
+
+    # roofline of the dominant kernel (sample_kernel), from this run's CUDA events
+    shard_docs = None
+    if world > 1:
+        part = spdp.spdp_partition(cfg.seed, world, corpus.doc, corpus.num_docs)
+        shard_docs = np.nonzero(part == rank)[0]
+    plan = plan_stats(corpus, shard_docs, args.waves)
+    peak, peak_src = measured_peaks()
+    sample_ms = tm["sample_ms"] / max(tm["sample_launches"], 1) * args.waves   # per sweep (all waves)
+    bytes_sweep = alg_bytes(plan, K)
+    achieved = bytes_sweep / (sample_ms / 1e3) / 1e9
+    traffic = load_traffic(cfg.name, K)
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "sample_kernel",
+            "alg_bytes_per_launch": int(bytes_sweep / max(args.waves, 1)), "peak_source": peak_src,
+            "sample_ms_per_sweep": round(sample_ms, 4), "share_of_step": round(sample_ms / ms, 3)}
+
+    # ---------------- end to end through the C ABI with host buffers ----------------
+    torch.cuda.synchronize(); barrier()
+    e2e_steps = args.steps
+    t0 = time.perf_counter()
+    h = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
+    h.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs)     # H2D of the job's inputs
+    for _ in range(e2e_steps):
+        h.sweep(1)
+        out = h.counts(doc_topic=False, customers=False, tables=False, shadow=False)   # D2H of z, r
+    torch.cuda.synchronize(); barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    h.close()
+    e2e = {"value": N * e2e_steps / e2e_s, "unit": "tokens/s",
+           "h2d_bytes_per_step": int(N * 12 / e2e_steps), "d2h_bytes_per_step": int(plan["tokens"] * 2),
+           "includes": "spdp_create + spdp_load_corpus (host token arrays) + per step spdp_sweep(1) + "
+                       "spdp_counts(z, r) to host; wall clock, max over ranks"}
+
+    line = {
+        "metric": "sampled tokens/sec per sweep", "value": round(value, 1), "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32 weights / fp64 CDF / int32 counts",
+        "data": "synthetic SPDP-generated corpus (synth/, seeded)",
+        "config": {"workload": workload, "tokens": N, "groups": cfg.groups, "docs": corpus.num_docs,
+                   "vocab": cfg.vocab, "topics": K, "waves": args.waves, "parallelism": f"doc-shard x{world}",
+                   "l2": "flushed between timed sweeps (256 MiB write outside the events)" if flush is not None else "not flushed",
+                   "sweep_ms": [round(x, 4) for x in step_ms]},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": int(tm["launches"]),
+        "clocks": clk.summary(),
+        "perplexity_after": round(ppl, 4),
+        "stats": stats,
+        "timings_ms": {k: round(v, 4) for k, v in tm.items()},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        st = args.cpu_sample_tokens or min(N, 400_000 if K <= 100 else 100_000)
+        line["cpu_baseline"] = cpu_baseline(corpus, cfg, K, args.waves, st)
+        line["cpu_baseline"]["cpu"] = cpu_model()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, cfg, K, world, rank, workload):
+    """--impl reference: the oracle as it stands on the host cores (the paper ships
+    no code; the CPU oracle is this tier's reference arm).  Rank 0 only."""
+    if rank != 0:
+        return
+    import synth
+    corpus = synth.corpus_for(cfg)
+    sample = args.cpu_sample_tokens or min(corpus.num_tokens, 60_000 if K <= 100 else 20_000)
+    import oracle
+    o = oracle.from_corpus(corpus, K, cfg.alpha, cfg.beta, cfg.discount, cfg.concentration, cfg.seed)
+    for _ in range(args.warmup):
+        o.sweep_par(waves=args.waves, max_tokens=sample)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.sweep_par(waves=args.waves, max_tokens=sample)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = sample / (ms / 1e3)
+    cb = {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+          "sample": f"first {sample} tokens of a mode-P (W={args.waves}) sweep of {cfg.name} per step"}
+    line = {"impl": "reference", "metric": "sampled tokens/sec per sweep", "value": round(value, 1),
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic SPDP-generated corpus (synth/, seeded)",
+            "config": {"workload": workload, "tokens": corpus.num_tokens, "topics": K, "waves": args.waves},
+            "cpu_baseline": cb,
+            "e2e": {"value": round(value, 1), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

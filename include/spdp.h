@@ -175,6 +175,16 @@ spdp_status spdp_debug_probs(spdp_ctx* ctx, int64_t n, const int64_t* tok_ids, d
  * out[5] local docs, out[6] M_max (largest count(i,w)), out[7] chunks. */
 spdp_status spdp_stats(spdp_ctx* ctx, int64_t* out);
 
+/* Phase timing with CUDA events recorded on the context's stream around each
+ * launch of the sweep (enable = 1 resets the accumulators and starts;
+ * 0 stops).  spdp_timings fills out[8] with totals since the reset:
+ * out[0] sample-kernel ms, out[1] token-apply ms, out[2] row-merge ms,
+ * out[3] exchange ms (unapply + all-reduce + merge), out[4] whole-sweep ms,
+ * out[5] sample-kernel launches, out[6] kernel launches of all kinds,
+ * out[7] sweeps timed. */
+spdp_status spdp_profile(spdp_ctx* ctx, int32_t enable);
+spdp_status spdp_timings(spdp_ctx* ctx, double* out);
+
 /* Document -> rank assignment used by spdp_load_corpus (host only; no
  * device needed): shard_of_doc [num_docs]. */
 spdp_status spdp_partition(uint64_t seed, int32_t world_size, int64_t num_tokens, int32_t num_docs,

@@ -33,7 +33,7 @@ _NAMES = {0: "SPDP_OK", -1: "SPDP_EINVAL", -2: "SPDP_ENOMEM", -3: "SPDP_ECUDA", 
 # every symbol include/spdp.h declares
 EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "spdp_sweep_local",
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
-           "spdp_stats", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
+           "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
            "spdp_version"]
 
 
@@ -80,6 +80,7 @@ def lib():
             "spdp_set_state": [P, P, P, P], "spdp_sweep": [P, I32], "spdp_sweep_local": [P],
             "spdp_exchange_buffer": [P, P, P], "spdp_exchange_copy": [P, P, I32], "spdp_sweep_merge": [P], "spdp_counts": [P, P, P, P, P, P, P],
             "spdp_loglik": [P, P, P], "spdp_debug_probs": [P, I64, P, P, P], "spdp_stats": [P, P],
+            "spdp_profile": [P, I32], "spdp_timings": [P, P],
             "spdp_partition": [C.c_uint64, I32, I64, I32, P, P], "spdp_nccl_unique_id": [P],
         }
         for name, args in sig.items():
@@ -220,6 +221,17 @@ def spdp_stats(ctx):
     return dict(zip(keys, (int(x) for x in out)))
 
 
+def spdp_profile(ctx, enable=True):
+    _check(lib().spdp_profile(ctx, int(bool(enable))), ctx)
+
+
+def spdp_timings(ctx):
+    out = np.zeros(8)
+    _check(lib().spdp_timings(ctx, _p(out)), ctx)
+    keys = ["sample_ms", "apply_ms", "merge_ms", "exchange_ms", "sweep_ms", "sample_launches", "launches", "sweeps"]
+    return dict(zip(keys, (float(x) for x in out)))
+
+
 def spdp_destroy(ctx):
     if ctx:
         lib().spdp_destroy(ctx)
@@ -278,6 +290,12 @@ class Sampler:
 
     def stats(self):
         return spdp_stats(self.ctx)
+
+    def profile(self, enable=True):
+        spdp_profile(self.ctx, enable)
+
+    def timings(self):
+        return spdp_timings(self.ctx)
 
     def close(self):
         if self.ctx:

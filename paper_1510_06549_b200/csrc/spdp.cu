@@ -110,6 +110,11 @@ struct spdp_ctx {
     size_t partial_len = 0;
     uint32_t sweeps_done = 0;
     std::vector<void*> allocs;
+    // profiling (spdp_profile)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev;          // 4 per wave + 2 for the exchange
+    double acc[8] = {0};
+    int64_t launches = 0;
 };
 
 namespace {
@@ -168,7 +173,7 @@ void set_attr_t() {
     cudaFuncSetAttribute(perplexity_kernel<LPT, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
 }
 template <int LPT, int KPL>
-void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const float* asum, double* partial, cudaStream_t s) {
+void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum, double* partial, cudaStream_t s) {
     const size_t smem = (size_t)kWarps * LPT * KPL * sizeof(double);
     const int blocks = (a.nchunks + kWarps - 1) / kWarps;
     if (blocks > 0) perplexity_kernel<LPT, KPL><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
@@ -197,7 +202,7 @@ void set_attrs(spdp_ctx* c) {
 #undef CALL_A
 }
 void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
-#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum, partial, c->stream)
+#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream)
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_P)
 #undef CALL_P
 }
@@ -210,6 +215,8 @@ SweepArgs base_args(spdp_ctx* c) {
     a.dm = c->d_dm; a.dt = c->d_dt;
     a.alpha = c->d_alpha; a.disc = c->d_disc; a.conc = c->d_conc; a.tab = c->d_tab; a.tab_off = c->d_tab_off;
     a.beta = (float)c->cfg.beta; a.vbeta = (float)((double)c->V * c->cfg.beta);
+    a.alpha64 = c->d_alpha64; a.disc64 = c->d_disc64; a.conc64 = c->d_conc64;
+    a.beta64 = c->cfg.beta; a.vbeta64 = (double)c->V * c->cfg.beta;
     a.I = c->I; a.K = c->K; a.Kp = c->Kp;
     a.key0 = (uint32_t)c->cfg.seed; a.key1 = (uint32_t)(c->cfg.seed >> 32);
     a.sweep = c->d_sweep; a.stats = c->d_stats;
@@ -343,29 +350,67 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     return sync(c, "install_state");
 }
 
+spdp_status ensure_events(spdp_ctx* c) {
+    const size_t need = 4 * (size_t)c->W + 2;
+    while (c->ev.size() < need) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        c->ev.push_back(e);
+    }
+    return SPDP_OK;
+}
+inline void rec(spdp_ctx* c, size_t j) {
+    if (c->profiling) cudaEventRecord(c->ev[j], c->stream);
+}
+
 spdp_status run_waves(spdp_ctx* c) {
     SweepArgs a = base_args(c);
     CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    if (c->profiling) { spdp_status s = ensure_events(c); if (s) return s; }
     int32_t* Dm = c->G > 1 ? c->d_D : nullptr;
     int32_t* Dt = c->G > 1 ? c->d_D + c->cells : nullptr;
     for (int w = 0; w < c->W; ++w) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
-        if (ce == cb) continue;
+        rec(c, 4 * (size_t)w);
+        if (ce == cb) { rec(c, 4 * (size_t)w + 1); rec(c, 4 * (size_t)w + 2); rec(c, 4 * (size_t)w + 3); continue; }
         a.chunk_start = c->d_chunk_start + cb;
         a.chunk_seg = c->d_chunk_seg + cb;
         a.nchunks = (int)(ce - cb);
         launch_sample(c, a, false);
+        rec(c, 4 * (size_t)w + 1);
         const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
         const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
         apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n,
                                                                          c->Kp, tb, te);
+        rec(c, 4 * (size_t)w + 2);
         launch_merge(c, c->d_dm, c->d_dt, Dm, Dt);
+        rec(c, 4 * (size_t)w + 3);
+        c->launches += 3;
+        c->acc[5] += 1;
     }
     return check_launch(c, "sweep waves");
 }
 
+// after the stream is synchronised: accumulate this sweep's phase times
+void collect_times(spdp_ctx* c, bool exchanged) {
+    if (!c->profiling) return;
+    float ms;
+    for (int w = 0; w < c->W; ++w) {
+        const size_t b = 4 * (size_t)w;
+        if (cudaEventElapsedTime(&ms, c->ev[b], c->ev[b + 1]) == cudaSuccess) c->acc[0] += ms;
+        if (cudaEventElapsedTime(&ms, c->ev[b + 1], c->ev[b + 2]) == cudaSuccess) c->acc[1] += ms;
+        if (cudaEventElapsedTime(&ms, c->ev[b + 2], c->ev[b + 3]) == cudaSuccess) c->acc[2] += ms;
+    }
+    const size_t x = 4 * (size_t)c->W;
+    if (exchanged && cudaEventElapsedTime(&ms, c->ev[x], c->ev[x + 1]) == cudaSuccess) c->acc[3] += ms;
+    const size_t last = exchanged ? x + 1 : 4 * (size_t)(c->W - 1) + 3;
+    if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[last]) == cudaSuccess) c->acc[4] += ms;
+    c->acc[7] += 1;
+}
+
 spdp_status finish_sweep(spdp_ctx* c) {
     inc_sweep_kernel<<<1, 1, 0, c->stream>>>(c->d_sweep);
+    c->launches += 1;
     c->sweeps_done++;
     return check_launch(c, "inc_sweep");
 }
@@ -730,13 +775,20 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
     for (int it = 0; it < num_sweeps; ++it) {
         if ((s = run_waves(c))) return s;
         if (c->G > 1) {
+            rec(c, 4 * (size_t)c->W);
             unapply_net_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_D, c->d_D + c->cells, c->cells);
             if ((s = nccl_check(c, c->nccl.AllReduce(c->d_D, c->d_D, 2 * c->cells, kNcclInt32, kNcclSum, c->comm, c->stream),
                                 "ncclAllReduce(deltas)")))
                 return s;
             launch_merge(c, c->d_D, c->d_D + c->cells, nullptr, nullptr);
+            rec(c, 4 * (size_t)c->W + 1);
+            c->launches += 2;
         }
         if ((s = finish_sweep(c))) return s;
+        if (c->profiling) {
+            if ((s = sync(c, "spdp_sweep"))) return s;
+            collect_times(c, c->G > 1);
+        }
         if (c->cfg.debug_checks) {
             if ((s = sync(c, "spdp_sweep"))) return s;
             if ((s = debug_verify(c))) return s;
@@ -960,6 +1012,23 @@ spdp_status spdp_nccl_unique_id(void* out) {
     return SPDP_OK;
 }
 
+spdp_status spdp_profile(spdp_ctx* c, int32_t enable) {
+    spdp_status s = guard(c, false);
+    if (s) return s;
+    c->profiling = enable != 0;
+    for (double& v : c->acc) v = 0.0;
+    c->launches = 0;
+    if (c->profiling && c->loaded) return ensure_events(c);
+    return SPDP_OK;
+}
+
+spdp_status spdp_timings(spdp_ctx* c, double* out) {
+    if (!c || !out) return SPDP_EINVAL;
+    for (int j = 0; j < 8; ++j) out[j] = c->acc[j];
+    out[6] = (double)c->launches;
+    return SPDP_OK;
+}
+
 spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
     spdp_status s = guard(c, true);
     if (s) return s;
@@ -976,6 +1045,7 @@ void spdp_destroy(spdp_ctx* c) {
     if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : c->allocs) cudaFree(p);
+    for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->comm && c->nccl.CommDestroy) c->nccl.CommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;

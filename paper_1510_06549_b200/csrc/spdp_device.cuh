@@ -131,6 +131,11 @@ struct SweepArgs {
     const float2* tab;             // concatenated ratio tables
     const uint64_t* tab_off;       // [I] offset of group i's table
     float beta, vbeta;
+    // fp64 copies for the estimators (perplexity)
+    const double* alpha64;         // [I][Kp]
+    const double* disc64;
+    const double* conc64;
+    double beta64, vbeta64;
     int I, K, Kp;
     uint32_t key0, key1;
     const uint32_t* sweep;         // device counter (RNG counter word 1)
@@ -458,7 +463,7 @@ __global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
 // Per-chunk fp64 partials (fixed order) -> deterministic final reduction.
 template <int LPT, int KPL>
 __global__ void __launch_bounds__(kWarps * 32)
-perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const float* __restrict__ alpha_sum,
+perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const double* __restrict__ alpha_sum,
                   double* __restrict__ partial) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
@@ -471,12 +476,12 @@ perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const float* 
     const int I = A.I, K = A.K, Kp = A.Kp;
     const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
     const size_t row = (size_t)seg * Kp;
-    const double a = A.disc[i], b = A.conc[i];
+    const double a = A.disc64[i], b = A.conc64[i];
     for (int k = lane; k < KSPAN; k += 32) {
         double phi = 0.0;
         if (k < K) {
             const double Mk = A.M[(size_t)i * Kp + k], Tk = A.Tt[(size_t)i * Kp + k];
-            const double phi0 = ((double)A.beta + (double)A.Q[(size_t)w * Kp + k]) / ((double)A.vbeta + (double)A.T[k]);
+            const double phi0 = (A.beta64 + (double)A.Q[(size_t)w * Kp + k]) / (A.vbeta64 + (double)A.T[k]);
             phi = ((double)A.m[row + k] - a * (double)A.t[row + k]) / (b + Mk) + (b + a * Tk) / (b + Mk) * phi0;
         }
         sphi[k] = phi;
@@ -485,8 +490,8 @@ perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const float* 
     const int g = lane / LPT, gl = lane % LPT, kb = gl * KPL;
     double al[KPL];
 #pragma unroll
-    for (int j = 0; j < KPL; ++j) al[j] = (kb + j < K) ? (double)A.alpha[(size_t)i * Kp + kb + j] : 0.0;
-    const double asum = (double)alpha_sum[i];
+    for (int j = 0; j < KPL; ++j) al[j] = (kb + j < K) ? A.alpha64[(size_t)i * Kp + kb + j] : 0.0;
+    const double asum = alpha_sum[i];
     double ll = 0.0;
     const uint32_t start = A.chunk_start[c], end = A.chunk_start[c + 1];
     for (uint32_t base = start; base < end; base += TPW) {
