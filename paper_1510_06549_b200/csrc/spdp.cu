@@ -48,11 +48,12 @@ void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4
     out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
 }
 
-int pick_lpt(int K) { return K <= 32 ? 8 : (K <= 64 ? 16 : 32); }
+// (lanes per token, topics per lane) by K: few lanes per token so the
+// per-token fixed work (removal, scan, search) is shared by 32/LPT tokens.
+int pick_lpt(int K) { return K <= 32 ? 4 : (K <= 128 ? 8 : (K <= 256 ? 16 : 32)); }
 int pick_kpl(int K) {
-    if (K <= 16) return 2;
-    if (K <= 128) return 4;
-    if (K <= 256) return 8;
+    if (K <= 16) return 4;
+    if (K <= 64) return 8;
     if (K <= 512) return 16;
     return 32;
 }
@@ -160,13 +161,13 @@ spdp_status nccl_check(spdp_ctx* c, int r, const char* what) {
 // ------------------------------------------------------------------ kernel dispatch
 template <int LPT, int KPL, bool DBG>
 void launch_sample_t(const SweepArgs& a, cudaStream_t s) {
-    const size_t smem = (size_t)kWarps * 6 * LPT * KPL * sizeof(float);
+    const size_t smem = sample_smem_bytes<LPT, KPL>();
     const int blocks = (a.nchunks + kWarps - 1) / kWarps;
     if (blocks > 0) sample_kernel<LPT, KPL, DBG><<<blocks, kWarps * 32, smem, s>>>(a);
 }
 template <int LPT, int KPL>
 void set_attr_t() {
-    const int smem = kWarps * 6 * LPT * KPL * (int)sizeof(float);
+    const int smem = (int)sample_smem_bytes<LPT, KPL>();
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int psm = kWarps * LPT * KPL * (int)sizeof(double);
@@ -181,11 +182,11 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
 
 #define SPDP_DISPATCH(LPT_, KPL_, CALL)                     \
     switch (LPT_ * 100 + KPL_) {                            \
-        case 802: CALL(8, 2); break;                        \
-        case 804: CALL(8, 4); break;                        \
-        case 1604: CALL(16, 4); break;                      \
-        case 3204: CALL(32, 4); break;                      \
-        case 3208: CALL(32, 8); break;                      \
+        case 404: CALL(4, 4); break;                        \
+        case 408: CALL(4, 8); break;                        \
+        case 808: CALL(8, 8); break;                        \
+        case 816: CALL(8, 16); break;                       \
+        case 1616: CALL(16, 16); break;                     \
         case 3216: CALL(32, 16); break;                     \
         case 3232: CALL(32, 32); break;                     \
         default: break;                                     \
@@ -471,9 +472,9 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     c->LPT = pick_lpt(c->K);
     c->KPL = pick_kpl(c->K);
     if (c->LPT * c->KPL < c->K) return bad("internal: no kernel configuration for K");
-    int steps = 32;
-    if (const char* e = getenv("SPDP_CHUNK_STEPS")) steps = std::max(1, atoi(e));
-    c->chunk_tokens = steps * (32 / c->LPT);
+    int chunk = 256;
+    if (const char* e = getenv("SPDP_CHUNK_TOKENS")) chunk = std::max(1, atoi(e));
+    c->chunk_tokens = chunk;
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);

@@ -100,9 +100,9 @@ __global__ void build_ratio_table(float2* __restrict__ tab, double* __restrict__
 //   F1 = A1(m,t) (b + a Tt) / (b + M) * (beta + Q) / (V beta + T)  (Eq. r1)
 __device__ __forceinline__ void slot_factors(int M, int Tt, int Qv, int Tk, float2 A, float a, float b,
                                              float beta, float vbeta, float& F0, float& F1) {
-    const float C0 = 1.0f / (b + (float)M);
+    const float C0 = __frcp_rn(b + (float)M);
     F0 = A.x * C0;
-    F1 = A.y * ((b + a * (float)Tt) * C0) * ((beta + (float)Qv) / (vbeta + (float)Tk));
+    F1 = A.y * ((b + a * (float)Tt) * C0) * __fdividef(beta + (float)Qv, vbeta + (float)Tk);
 }
 
 struct SweepArgs {
@@ -146,31 +146,45 @@ struct SweepArgs {
 };
 
 // ---------------------------------------------------------------- the sample kernel
-// One warp per chunk of one (w, i) segment; LPT lanes per token (TPW = 32/LPT
-// tokens in flight per warp), each lane owning KPL consecutive topics.
-// Steps per token:
-//   a2 Philox(seed; id, sweep)  a3 removal against the wave-start snapshot
-//   a4/a5 weights (alpha+n_dk) F_k with the own-removal correction at k0
-//   a6 fp64 prefix (lane-local, then a group scan), first slot whose prefix
-//      exceeds u*total, slots in the paper's order j = 2k (r=1), 2k+1 (r=0)
-//   a7 zr_next, and the segment's (delta m, delta t) accumulated in smem,
-//      flushed once per chunk with integer atomics (deterministic).
+// Per-warp shared memory layout (floats / ints, KSPAN entries each).
+template <int KSPAN>
+struct WarpSmem {
+    float F[KSPAN];      // F0 + F1 at the snapshot counts
+    float F1[KSPAN];     // F1 at the snapshot counts
+    float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
+    float F1r[2][KSPAN];
+    int m[KSPAN];
+    int t[KSPAN];
+    int dm[KSPAN];       // the chunk's delta m, delta t
+    int dt[KSPAN];
+};
+
+// One warp per chunk of one (w, i) segment.  LPT lanes per token (TPW = 32/LPT
+// tokens in flight per warp-step), each lane owning KPL consecutive topics.
+//   prologue (once per chunk): the segment's factors F_k, F1_k at the snapshot,
+//     and the own-removal variants for both removal draws (Alg.1 lines 4-10),
+//     so a token's removal costs two shared-memory loads;
+//   per 32 tokens: lane l loads token l's record and runs its Philox
+//     (a2), the groups receive them by shuffles;
+//   per token (a3-a7): removal draw against the snapshot; topic masses
+//     w_k = (alpha_ik + n_dk) F_k (one FFMA each) summed per 4-topic block in
+//     fp32 and across blocks/lanes in fp64; the own-removal correction of
+//     topic k0 added by its owner lane; group scan; first slot whose fp64
+//     prefix exceeds u * total, in the paper's slot order j = 2k (r = 1),
+//     2k+1 (r = 0) — the r split uses w1 = (alpha + n) F1 exactly; smem deltas.
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 2 : 4)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
+    constexpr int NB = KPL / 4;                      // 4-topic blocks per lane
+    static_assert(KPL % 4 == 0, "KPL must be a multiple of 4");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int c = blockIdx.x * kWarps + wid;
     if (c >= A.nchunks) return;                      // warp-uniform
-
-    float* sF0 = reinterpret_cast<float*>(smem_raw) + (size_t)wid * KSPAN * 6;
-    float* sF1 = sF0 + KSPAN;
-    int* sm = reinterpret_cast<int*>(sF1 + KSPAN);
-    int* st = sm + KSPAN;
-    int* sdm = st + KSPAN;
-    int* sdt = sdm + KSPAN;
+    WarpSmem<KSPAN>& S = reinterpret_cast<WarpSmem<KSPAN>*>(smem_raw)[wid];
+    float* scratch = reinterpret_cast<float*>(smem_raw + sizeof(WarpSmem<KSPAN>) * kWarps) + (size_t)wid * 32 * KPL;
 
     const uint32_t seg = A.chunk_seg[c];
     const int I = A.I, K = A.K, Kp = A.Kp;
@@ -181,140 +195,201 @@ sample_kernel(SweepArgs A) {
     const int32_t* __restrict__ Mi = A.M + (size_t)i * Kp;
     const int32_t* __restrict__ Tti = A.Tt + (size_t)i * Kp;
     const int32_t* __restrict__ Qw = A.Q + (size_t)w * Kp;
+    const float* __restrict__ alpha_i = A.alpha + (size_t)i * Kp;
 
-    // prologue: the segment's slot factors F0_k, F1_k (wave-start snapshot)
+    // ---- prologue: slot factors at the snapshot and with the own removal
     for (int k = lane; k < KSPAN; k += 32) {
-        float F0 = 0.f, F1 = 0.f;
+        float F0 = 0.f, F1 = 0.f, R0 = 0.f, R1 = 0.f, R10 = 0.f, R11 = 0.f;
         int mv = 0, tv = 0;
         if (k < K) {
             mv = A.m[row + k];
             tv = A.t[row + k];
-            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+            const int Mv = Mi[k], Ttv = Tti[k], Qv = Qw[k], Tv = A.T[k];
+            slot_factors(Mv, Ttv, Qv, Tv, tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+            if (mv > 0) {
+                const int mm = mv - 1;
+                float x0, x1;
+                slot_factors(Mv - 1, Ttv, Qv, Tv, tab[tri(mm) + min(tv, mm)], a, b, A.beta, A.vbeta, x0, x1);
+                R0 = x0 + x1; R10 = x1;                                   // r_rem = 0: (m-1, t)
+                slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, tab[tri(mm) + max(tv - 1, 0)], a, b, A.beta, A.vbeta, x0, x1);
+                R1 = x0 + x1; R11 = x1;                                   // r_rem = 1: (m-1, t-1)
+            }
         }
-        sF0[k] = F0; sF1[k] = F1; sm[k] = mv; st[k] = tv; sdm[k] = 0; sdt[k] = 0;
+        S.F[k] = F0 + F1; S.F1[k] = F1;
+        S.Fr[0][k] = R0; S.Fr[1][k] = R1; S.F1r[0][k] = R10; S.F1r[1][k] = R11;
+        S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
     }
     __syncwarp();
 
     const int g = lane / LPT, gl = lane % LPT;
     const int kb = gl * KPL;                          // first topic of this lane
     const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
-    float F0[KPL], F1[KPL], al[KPL];
+    float F[KPL], aF[KPL];
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
-        F0[j] = sF0[kb + j];
-        F1[j] = sF1[kb + j];
-        al[j] = (kb + j < K) ? A.alpha[(size_t)i * Kp + kb + j] : 0.f;
+        F[j] = S.F[kb + j];
+        aF[j] = __fmul_rn((kb + j < K) ? alpha_i[kb + j] : 0.f, F[j]);
     }
+    float* myscr = scratch + lane * KPL;
     const uint32_t sweep = *A.sweep;
     const uint32_t start = A.chunk_start[c], end = A.chunk_start[c + 1];
     unsigned keeps = 0, moved = 0;
 
-    for (uint32_t base = start; base < end; base += TPW) {
-        const uint32_t tok = base + g;
-        const bool valid = tok < end;
-        uint32_t doc = 0, id = 0, zr0 = 0;
-        if (valid) { doc = A.tok_doc[tok]; id = A.tok_id[tok]; zr0 = A.zr[tok]; }
-        const uint4 x = philox(make_uint4(id, sweep, 0u, 0u), A.key0, A.key1);       // a2
-        const int k0 = (int)(zr0 & 0x7FFFu);
-        const int m0 = sm[k0], t0 = st[k0];
-        const int rrem = removal_draw(x.x, m0, t0);                                   // a3
-        const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
-
-        // own-removal factors of topic k0 (Alg.1 lines 4-10)
-        float F0k0, F1k0;
-        {
-            const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
-            slot_factors(Mi[k0] - 1, Tti[k0] - rrem, Qw[k0] - rrem, A.T[k0] - rrem,
-                         tab[tri(mm) + tt], a, b, A.beta, A.vbeta, F0k0, F1k0);
+    for (uint32_t b0 = start; b0 < end; b0 += 32) {
+        // ---- a2: this lane's token of the batch: record + Philox
+        const uint32_t nb = min(32u, end - b0);
+        uint32_t t_doc = 0, t_zr = 0, t_x0 = 0;
+        double t_u = 0.0;
+        if ((uint32_t)lane < nb) {
+            const uint32_t p = b0 + lane;
+            t_doc = A.tok_doc[p];
+            t_zr = A.zr[p];
+            const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);
+            t_x0 = x.x;
+            t_u = u53(x);
         }
-        // a4: doc-topic row (vectorised, predicated per 4-topic block)
-        int nv[KPL];
-        const int32_t* nrow = A.n + (size_t)doc * Kp + kb;
-        if constexpr (KPL % 4 == 0) {
+        for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
+            const uint32_t src = s0 + g;
+            const bool valid = src < nb;
+            const uint32_t doc = __shfl_sync(0xffffffffu, t_doc, src & 31);
+            const uint32_t zr0 = __shfl_sync(0xffffffffu, t_zr, src & 31);
+            const uint32_t x0 = __shfl_sync(0xffffffffu, t_x0, src & 31);
+            const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
+            const uint32_t tok = b0 + src;
+
+            // ---- a3: removal against the wave-start snapshot
+            const int k0 = (int)(zr0 & 0x7FFFu);
+            const int m0 = S.m[k0], t0 = S.t[k0];
+            const int rrem = removal_draw(x0, m0, t0);
+            const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
+            const float Fk0 = S.Fr[rrem][k0], F1k0 = S.F1r[rrem][k0];
+
+            // ---- a4/a5: doc-topic row and topic masses
+            const int32_t* nrow = A.n + (size_t)doc * Kp;
+            double bp[NB];
+            double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < KPL / 4; ++q) {
+            for (int q = 0; q < NB; ++q) {
                 int4 v = make_int4(0, 0, 0, 0);
-                if (kb + 4 * q < K) v = __ldg(reinterpret_cast<const int4*>(nrow) + q);
-                nv[4 * q] = v.x; nv[4 * q + 1] = v.y; nv[4 * q + 2] = v.z; nv[4 * q + 3] = v.w;
+                if (kb + 4 * q < K) v = __ldg(reinterpret_cast<const int4*>(nrow + kb) + q);
+                const float w0 = __fmaf_rn((float)v.x, F[4 * q + 0], aF[4 * q + 0]);
+                const float w1 = __fmaf_rn((float)v.y, F[4 * q + 1], aF[4 * q + 1]);
+                const float w2 = __fmaf_rn((float)v.z, F[4 * q + 2], aF[4 * q + 2]);
+                const float w3 = __fmaf_rn((float)v.w, F[4 * q + 3], aF[4 * q + 3]);
+                *reinterpret_cast<float4*>(myscr + 4 * q) = make_float4(w0, w1, w2, w3);
+                acc += (double)((w0 + w1) + (w2 + w3));
+                bp[q] = acc;
             }
-        } else if constexpr (KPL == 2) {
-            int2 v = make_int2(0, 0);
-            if (kb < K) v = __ldg(reinterpret_cast<const int2*>(nrow));
-            nv[0] = v.x; nv[1] = v.y;
-        } else {
-            nv[0] = (kb < K) ? __ldg(nrow) : 0;
-        }
-        // a5: slot masses w1 = (alpha+n) F1, w0 = (alpha+n) F0 in fp32; a6: fp64 prefix in slot order
-        float w1v[KPL], w0v[KPL];
-        double acc = 0.0;
+            // own-removal correction of topic k0 by its owner lane
+            {
+                const int n0 = __ldg(nrow + k0);
+                const float al0 = alpha_i[k0];
+                const float Fo = S.F[k0];
+                const float wold = __fmaf_rn((float)n0, Fo, __fmul_rn(al0, Fo));
+                const float wnew = __fmaf_rn((float)(n0 - 1), Fk0, __fmul_rn(al0, Fk0));
+                const double delta = (double)wnew - (double)wold;
+                const int jo = k0 - kb;
+                if (jo >= 0 && jo < KPL) {
+                    acc += delta;
 #pragma unroll
-        for (int j = 0; j < KPL; ++j) {
-            const bool own = (kb + j == k0);
-            const float base = al[j] + (float)(nv[j] - (own ? 1 : 0));
-            w1v[j] = base * (own ? F1k0 : F1[j]);
-            w0v[j] = base * (own ? F0k0 : F0[j]);
-            acc += (double)w1v[j];
-            acc += (double)w0v[j];
-        }
-        double incl = acc;
-#pragma unroll
-        for (int off = 1; off < LPT; off <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
-            if (gl >= off) incl += y;
-        }
-        double excl = __shfl_up_sync(0xffffffffu, incl, 1, LPT);
-        if (gl == 0) excl = 0.0;
-        const double total = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
-        const double target = u53(x) * total;
-        const unsigned hit = __ballot_sync(0xffffffffu, incl > target) & gmask;
-        const unsigned pos = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
-        const bool fb = (hit == 0u);
-        const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
-        int slot = -1, last = 0;
-        if (lane == winner) {
-            // j* = min{ j : prefix_j > u * total } over this lane's slots (reading c10)
-            double run = excl;
-#pragma unroll
-            for (int j = 0; j < KPL; ++j) {
-                const double r1 = run + (double)w1v[j];
-                const double r0 = r1 + (double)w0v[j];
-                if (slot < 0) {
-                    if (r1 > target) slot = 2 * (kb + j);
-                    else if (r0 > target) slot = 2 * (kb + j) + 1;
+                    for (int q = 0; q < NB; ++q) if (4 * q + 3 >= jo) bp[q] += delta;
+                    myscr[jo] = wnew;
                 }
-                if (w1v[j] > 0.f) last = 2 * (kb + j);
-                if (w0v[j] > 0.f) last = 2 * (kb + j) + 1;
-                run = r0;
             }
-            if (fb || slot < 0) slot = last;   // rounding: the last slot with positive mass
-        }
-        slot = __shfl_sync(0xffffffffu, slot, winner);
-        int ks = slot >> 1, rs = (slot & 1) ? 0 : 1;
-        if (keep) { ks = k0; rs = 1; }
-
-        if constexpr (DEBUG) {
-            if (valid) {
+            // ---- a6: group scan, draw
+            double incl = acc;
 #pragma unroll
-                for (int j = 0; j < KPL; ++j) {
-                    const int k = kb + j;
-                    if (k < K) {
-                        A.dbg_w[(size_t)tok * 2 * K + 2 * k] = (double)w1v[j];
-                        A.dbg_w[(size_t)tok * 2 * K + 2 * k + 1] = (double)w0v[j];
+            for (int off = 1; off < LPT; off <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
+                if (gl >= off) incl += y;
+            }
+            double excl = __shfl_up_sync(0xffffffffu, incl, 1, LPT);
+            if (gl == 0) excl = 0.0;
+            const double total = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
+            const double target = u * total;
+            const unsigned hit = __ballot_sync(0xffffffffu, incl > target) & gmask;
+            const unsigned pos = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
+            const bool fb = (hit == 0u);
+            const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
+            int slot = 0;
+            if (lane == winner) {
+                // block, then topic within the block (fp64 prefix of fp32 masses)
+                int qs = NB - 1;
+                double prev = excl, before = excl;
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    const double cur = excl + bp[q];
+                    if (!found && cur > target) { qs = q; before = prev; found = true; }
+                    prev = cur;
+                }
+                if (!found) before = prev - (bp[NB - 1] - (NB > 1 ? bp[NB > 1 ? NB - 2 : 0] : 0.0));
+                const float4 w4 = *reinterpret_cast<const float4*>(myscr + 4 * qs);
+                const float wq[4] = {w4.x, w4.y, w4.z, w4.w};
+                int es = -1, elast = 0;
+                double run = before, bes = before, blast = before;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double nxt = run + (double)wq[e];
+                    if (es < 0 && nxt > target) { es = e; bes = run; }
+                    if (wq[e] > 0.f) { elast = e; blast = run; }
+                    run = nxt;
+                }
+                if (es < 0 || fb) {                  // rounding: last positive topic of the block
+                    es = elast;
+                    bes = blast;                     // only used for the r split below
+                }
+                const int ks = kb + 4 * qs + es;
+                const bool own = (ks == k0);
+                const int nks = __ldg(nrow + ks) - (own ? 1 : 0);
+                const float f1 = own ? F1k0 : S.F1[ks];
+                const float w1 = __fmaf_rn((float)nks, f1, __fmul_rn(alpha_i[ks], f1));
+                int rs;
+                if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
+                else rs = ((own ? m0 - 1 : S.m[ks]) > 0) ? 0 : 1;  // last positive slot
+                slot = ks | (rs << 15);
+            }
+            slot = __shfl_sync(0xffffffffu, slot, winner);
+            int ks = slot & 0x7FFF, rs = slot >> 15;
+            if (keep) { ks = k0; rs = 1; }
+
+            if constexpr (DEBUG) {
+                // exact slot masses w1 = (alpha + n) F1, w0 = (alpha + n) F0 of every topic
+                if (valid) {
+#pragma unroll
+                    for (int j = 0; j < KPL; ++j) {
+                        const int k = kb + j;
+                        if (k < K) {
+                            const bool own = (k == k0);
+                            const int nk = __ldg(nrow + k) - (own ? 1 : 0);
+                            float f0, f1;
+                            if (own) {
+                                const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
+                                slot_factors(Mi[k] - 1, Tti[k] - rrem, Qw[k] - rrem, A.T[k] - rrem, tab[tri(mm) + tt],
+                                             a, b, A.beta, A.vbeta, f0, f1);
+                            } else {
+                                slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(S.m[k]) + S.t[k]], a, b, A.beta,
+                                             A.vbeta, f0, f1);
+                            }
+                            const double base = (double)alpha_i[k] + (double)nk;
+                            A.dbg_w[(size_t)tok * 2 * K + 2 * k] = base * (double)f1;
+                            A.dbg_w[(size_t)tok * 2 * K + 2 * k + 1] = base * (double)f0;
+                        }
+                    }
+                    if (gl == 0) {
+                        int32_t* inf = A.dbg_info + (size_t)tok * 4;
+                        inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
                     }
                 }
-                if (gl == 0) {
-                    int32_t* inf = A.dbg_info + (size_t)tok * 4;
-                    inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
-                }
-            }
-        } else {
-            if (valid && gl == 0) {                                                   // a7
-                A.zr_next[tok] = (uint16_t)(ks | (rs << 15));
-                if (keep) ++keeps;
-                else {
-                    atomicAdd(&sdm[k0], -1); atomicAdd(&sdt[k0], -rrem);
-                    atomicAdd(&sdm[ks], 1); atomicAdd(&sdt[ks], rs);
-                    moved += (ks != k0);
+            } else {
+                if (valid && gl == 0) {                                            // a7
+                    A.zr_next[tok] = (uint16_t)(ks | (rs << 15));
+                    if (keep) ++keeps;
+                    else {
+                        atomicAdd(&S.dm[k0], -1); atomicAdd(&S.dt[k0], -rrem);
+                        atomicAdd(&S.dm[ks], 1); atomicAdd(&S.dt[ks], rs);
+                        moved += (ks != k0);
+                    }
                 }
             }
         }
@@ -322,7 +397,7 @@ sample_kernel(SweepArgs A) {
     if constexpr (!DEBUG) {
         __syncwarp();
         for (int k = lane; k < K; k += 32) {
-            const int dmv = sdm[k], dtv = sdt[k];
+            const int dmv = S.dm[k], dtv = S.dt[k];
             if (dmv) atomicAdd(A.dm + row + k, dmv);
             if (dtv) atomicAdd(A.dt + row + k, dtv);
         }
@@ -336,6 +411,11 @@ sample_kernel(SweepArgs A) {
             atomicAdd(A.stats + 1, (unsigned long long)moved);
         }
     }
+}
+
+template <int LPT, int KPL>
+constexpr size_t sample_smem_bytes() {
+    return kWarps * (sizeof(WarpSmem<LPT * KPL>) + 32 * KPL * sizeof(float));
 }
 
 // ---------------------------------------------------------------- end of wave: n and z
