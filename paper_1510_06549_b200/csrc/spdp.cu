@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -90,15 +91,19 @@ struct spdp_ctx {
     std::vector<uint32_t> sorted_tok;            // canonical id at each sorted position
     std::vector<int64_t> pos_of_tok;              // canonical id -> sorted position (-1: other rank)
     std::vector<uint32_t> wave_tok_begin, wave_chunk_begin;
-    std::vector<uint32_t> chunk_start, chunk_seg;
+    std::vector<uint32_t> chunk_start, chunk_end, chunk_seg;
     int mmax = 0;
     size_t cells = 0;
 
     // device
-    uint32_t *d_tok_doc = nullptr, *d_tok_id = nullptr, *d_chunk_start = nullptr, *d_chunk_seg = nullptr,
+    uint32_t *d_tok_doc = nullptr, *d_tok_id = nullptr, *d_chunk_start = nullptr, *d_chunk_end = nullptr,
+             *d_chunk_seg = nullptr,
              *d_sweep = nullptr;
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
-    int32_t *d_n = nullptr, *d_m = nullptr, *d_t = nullptr, *d_Q = nullptr, *d_M = nullptr, *d_Tt = nullptr,
+    float* d_n = nullptr;                         // n_dk as exact integers in fp32
+    uint32_t* d_work = nullptr;                   // [W + 1] persistent-warp counters
+    int sample_grid = 0;
+    int32_t *d_m = nullptr, *d_t = nullptr, *d_Q = nullptr, *d_M = nullptr, *d_Tt = nullptr,
             *d_T = nullptr, *d_dm = nullptr, *d_dt = nullptr, *d_D = nullptr, *d_doclen = nullptr,
             *d_docgroup = nullptr;
     float *d_alpha = nullptr, *d_disc = nullptr, *d_conc = nullptr, *d_alpha_sum = nullptr;
@@ -160,10 +165,19 @@ spdp_status nccl_check(spdp_ctx* c, int r, const char* what) {
 
 // ------------------------------------------------------------------ kernel dispatch
 template <int LPT, int KPL, bool DBG>
-void launch_sample_t(const SweepArgs& a, cudaStream_t s) {
+void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks) {
     const size_t smem = sample_smem_bytes<LPT, KPL>();
-    const int blocks = (a.nchunks + kWarps - 1) / kWarps;
+    const int blocks = std::min((a.nchunks + kWarps - 1) / kWarps, max_blocks);
     if (blocks > 0) sample_kernel<LPT, KPL, DBG><<<blocks, kWarps * 32, smem, s>>>(a);
+}
+template <int LPT, int KPL>
+int resident_blocks_t() {
+    int nb = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sample_kernel<LPT, KPL, false>, kWarps * 32,
+                                                  sample_smem_bytes<LPT, KPL>());
+    return std::max(nb, 1) * std::max(sms, 1);
 }
 template <int LPT, int KPL>
 void set_attr_t() {
@@ -193,7 +207,7 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
     }
 
 void launch_sample(spdp_ctx* c, const SweepArgs& a, bool dbg) {
-#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream) : launch_sample_t<L, P, false>(a, c->stream))
+#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid))
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_S)
 #undef CALL_S
 }
@@ -201,6 +215,9 @@ void set_attrs(spdp_ctx* c) {
 #define CALL_A(L, P) set_attr_t<L, P>()
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_A)
 #undef CALL_A
+#define CALL_R(L, P) c->sample_grid = resident_blocks_t<L, P>()
+    SPDP_DISPATCH(c->LPT, c->KPL, CALL_R)
+#undef CALL_R
 }
 void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
 #define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream)
@@ -211,7 +228,7 @@ void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
 SweepArgs base_args(spdp_ctx* c) {
     SweepArgs a{};
     a.tok_doc = c->d_tok_doc; a.tok_id = c->d_tok_id; a.zr = c->d_zr; a.zr_next = c->d_zr_next;
-    a.chunk_start = c->d_chunk_start; a.chunk_seg = c->d_chunk_seg; a.nchunks = 0;
+    a.chunk_start = c->d_chunk_start; a.chunk_end = c->d_chunk_end; a.chunk_seg = c->d_chunk_seg; a.nchunks = 0;
     a.n = c->d_n; a.m = c->d_m; a.t = c->d_t; a.Q = c->d_Q; a.M = c->d_M; a.Tt = c->d_Tt; a.T = c->d_T;
     a.dm = c->d_dm; a.dt = c->d_dt;
     a.alpha = c->d_alpha; a.disc = c->d_disc; a.conc = c->d_conc; a.tab = c->d_tab; a.tab_off = c->d_tab_off;
@@ -330,16 +347,16 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
         if (t[cell] < 0 || t[cell] > m[cell] || ((t[cell] > 0) != (m[cell] > 0)))
             return fail(c, SPDP_EINVAL, "table counts violate 1 <= t <= m on an occupied cell (or t > 0 on an empty one)");
     // local doc-topic counts and token records
-    std::vector<int32_t> n((size_t)c->Dloc * Kp, 0);
+    std::vector<float> n((size_t)c->Dloc * Kp, 0.f);
     std::vector<uint16_t> zr((size_t)c->Nloc);
     for (int64_t q = 0; q < c->Nloc; ++q) {
         const uint32_t p = c->sorted_tok[(size_t)q];
-        n[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + z[p]]++;
+        n[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + z[p]] += 1.f;
         zr[(size_t)q] = (uint16_t)(z[p] | (r[p] << 15));
     }
     CU(cudaMemcpyAsync(c->d_m, m.data(), sizeof(int32_t) * c->cells, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(c->d_t, t.data(), sizeof(int32_t) * c->cells, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->d_n, n.data(), sizeof(int32_t) * n.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_n, n.data(), sizeof(float) * n.size(), cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(c->d_zr, zr.data(), sizeof(uint16_t) * zr.size(), cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(c->d_zr_next, zr.data(), sizeof(uint16_t) * zr.size(), cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
@@ -367,6 +384,7 @@ inline void rec(spdp_ctx* c, size_t j) {
 spdp_status run_waves(spdp_ctx* c) {
     SweepArgs a = base_args(c);
     CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    CU(cudaMemsetAsync(c->d_work, 0, sizeof(uint32_t) * ((size_t)c->W + 2), c->stream));
     if (c->profiling) { spdp_status s = ensure_events(c); if (s) return s; }
     int32_t* Dm = c->G > 1 ? c->d_D : nullptr;
     int32_t* Dt = c->G > 1 ? c->d_D + c->cells : nullptr;
@@ -375,8 +393,10 @@ spdp_status run_waves(spdp_ctx* c) {
         rec(c, 4 * (size_t)w);
         if (ce == cb) { rec(c, 4 * (size_t)w + 1); rec(c, 4 * (size_t)w + 2); rec(c, 4 * (size_t)w + 3); continue; }
         a.chunk_start = c->d_chunk_start + cb;
+        a.chunk_end = c->d_chunk_end + cb;
         a.chunk_seg = c->d_chunk_seg + cb;
         a.nchunks = (int)(ce - cb);
+        a.work = c->d_work + w;
         launch_sample(c, a, false);
         rec(c, 4 * (size_t)w + 1);
         const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
@@ -596,11 +616,13 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     }
     c->pos_of_tok.assign((size_t)num_tokens, -1);
     for (size_t q = 0; q < c->sorted_tok.size(); ++q) c->pos_of_tok[c->sorted_tok[q]] = (int64_t)q;
-    // chunks: split each wave's (w, i) segments into runs of <= chunk_tokens tokens
-    c->chunk_start.clear(); c->chunk_seg.clear();
+    // chunks: split each wave's (w, i) segments into runs of <= chunk_tokens tokens;
+    // within a wave, longest first (the persistent warps take them in order)
+    c->chunk_start.clear(); c->chunk_end.clear(); c->chunk_seg.clear();
     c->wave_chunk_begin.assign((size_t)W + 1, 0);
     for (int w = 0; w < W; ++w) {
         c->wave_chunk_begin[(size_t)w] = (uint32_t)c->chunk_seg.size();
+        std::vector<std::array<uint32_t, 3>> wc;
         uint32_t q = c->wave_tok_begin[(size_t)w];
         const uint32_t qe = c->wave_tok_begin[(size_t)w + 1];
         while (q < qe) {
@@ -612,22 +634,29 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
                 if ((uint32_t)word[pr] * (uint32_t)I + (uint32_t)group[pr] != seg) break;
                 ++r; ++len;
             }
-            c->chunk_start.push_back(q);
-            c->chunk_seg.push_back(seg);
+            wc.push_back({q, r, seg});
             q = r;
+        }
+        std::stable_sort(wc.begin(), wc.end(), [](const std::array<uint32_t, 3>& x, const std::array<uint32_t, 3>& y) {
+            return (x[1] - x[0]) > (y[1] - y[0]);
+        });
+        for (const auto& ch : wc) {
+            c->chunk_start.push_back(ch[0]);
+            c->chunk_end.push_back(ch[1]);
+            c->chunk_seg.push_back(ch[2]);
         }
     }
     c->wave_chunk_begin[(size_t)W] = (uint32_t)c->chunk_seg.size();
-    c->chunk_start.push_back((uint32_t)c->Nloc);
     const size_t nch = c->chunk_seg.size();
     c->cells = (size_t)V * I * Kp;
 
     // device allocations
     ALLOC(c->d_tok_doc, c->Nloc); ALLOC(c->d_tok_id, c->Nloc);
     ALLOC(c->d_zr, c->Nloc); ALLOC(c->d_zr_next, c->Nloc);
-    ALLOC(c->d_chunk_start, nch + 1); ALLOC(c->d_chunk_seg, nch);
+    ALLOC(c->d_chunk_start, nch); ALLOC(c->d_chunk_end, nch); ALLOC(c->d_chunk_seg, nch);
     ALLOC(c->d_sweep, 1);
     ALLOC(c->d_n, (size_t)c->Dloc * Kp);
+    ALLOC(c->d_work, (size_t)W + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
     ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);
     if (c->G > 1) ALLOC(c->d_D, 2 * c->cells);
@@ -667,7 +696,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
         CU(cudaMemcpy(c->d_tok_doc, tdoc.data(), sizeof(uint32_t) * tdoc.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_tok_id, tid.data(), sizeof(uint32_t) * tid.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_chunk_start, c->chunk_start.data(), sizeof(uint32_t) * c->chunk_start.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_chunk_start, c->chunk_start.data(), sizeof(uint32_t) * nch, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_chunk_end, c->chunk_end.data(), sizeof(uint32_t) * nch, cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_chunk_seg, c->chunk_seg.data(), sizeof(uint32_t) * std::max<size_t>(nch, 0), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_doclen, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_docgroup, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice));
@@ -834,14 +864,15 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
         }
     }
     if (doc_topic) {
-        std::vector<int32_t> n((size_t)c->Dloc * Kp);
-        CU(cudaMemcpyAsync(n.data(), c->d_n, sizeof(int32_t) * n.size(), cudaMemcpyDeviceToHost, c->stream));
+        std::vector<float> nf((size_t)c->Dloc * Kp);
+        CU(cudaMemcpyAsync(nf.data(), c->d_n, sizeof(float) * nf.size(), cudaMemcpyDeviceToHost, c->stream));
         if ((s = sync(c, "counts(n)"))) return s;
         std::vector<int32_t> full;
         if (gather) full.assign((size_t)c->D * K, 0);
         int32_t* dst = gather ? full.data() : doc_topic;
         for (int32_t j = 0; j < c->Dloc; ++j)
-            std::memcpy(dst + (size_t)c->global_of_local[(size_t)j] * K, n.data() + (size_t)j * Kp, sizeof(int32_t) * K);
+            for (int k = 0; k < K; ++k)
+                dst[(size_t)c->global_of_local[(size_t)j] * K + k] = (int32_t)nf[(size_t)j * Kp + k];
         if (gather) {
             TempBuf<int32_t> tb(full.size());
             if (!tb.p) return fail(c, SPDP_ENOMEM, "gather buffer");
@@ -950,7 +981,7 @@ spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, dou
     if (n < 0 || (n > 0 && (!tok_ids || !probs))) return fail(c, SPDP_EINVAL, "bad debug_probs arguments");
     if (n == 0) return SPDP_OK;
     const int I = c->I, K = c->K;
-    std::vector<uint32_t> tdoc((size_t)n), tid((size_t)n), cs((size_t)n + 1), seg((size_t)n);
+    std::vector<uint32_t> tdoc((size_t)n), tid((size_t)n), cs((size_t)n + 1), ce((size_t)n), seg((size_t)n);
     std::vector<uint16_t> zr((size_t)n);
     std::vector<uint16_t> allzr((size_t)c->Nloc);
     CU(cudaMemcpyAsync(allzr.data(), c->d_zr, sizeof(uint16_t) * allzr.size(), cudaMemcpyDeviceToHost, c->stream));
@@ -962,23 +993,27 @@ spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, dou
         tid[(size_t)j] = (uint32_t)p;
         zr[(size_t)j] = allzr[(size_t)c->pos_of_tok[(size_t)p]];
         cs[(size_t)j] = (uint32_t)j;
+        ce[(size_t)j] = (uint32_t)j + 1;
         seg[(size_t)j] = (uint32_t)c->word[(size_t)p] * (uint32_t)I + (uint32_t)c->group[(size_t)p];
     }
     cs[(size_t)n] = (uint32_t)n;
-    uint32_t *d_doc = nullptr, *d_id = nullptr, *d_cs = nullptr, *d_seg = nullptr;
+    uint32_t *d_doc = nullptr, *d_id = nullptr, *d_cs = nullptr, *d_ce = nullptr, *d_seg = nullptr;
     uint16_t* d_zr = nullptr;
     double* d_w = nullptr;
     int32_t* d_info = nullptr;
-    ALLOC(d_doc, n); ALLOC(d_id, n); ALLOC(d_cs, n + 1); ALLOC(d_seg, n); ALLOC(d_zr, n);
+    ALLOC(d_doc, n); ALLOC(d_id, n); ALLOC(d_cs, n + 1); ALLOC(d_ce, n); ALLOC(d_seg, n); ALLOC(d_zr, n);
     ALLOC(d_w, (size_t)n * 2 * K); ALLOC(d_info, (size_t)n * 4);
     CU(cudaMemcpyAsync(d_doc, tdoc.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(d_id, tid.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(d_cs, cs.data(), 4 * ((size_t)n + 1), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(d_ce, ce.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(d_seg, seg.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(d_zr, zr.data(), 2 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     SweepArgs a = base_args(c);
     a.tok_doc = d_doc; a.tok_id = d_id; a.zr = d_zr; a.zr_next = nullptr;
-    a.chunk_start = d_cs; a.chunk_seg = d_seg; a.nchunks = (int)n;
+    a.chunk_start = d_cs; a.chunk_end = d_ce; a.chunk_seg = d_seg; a.nchunks = (int)n;
+    a.work = c->d_work + c->W + 1;
+    CU(cudaMemsetAsync(a.work, 0, sizeof(uint32_t), c->stream));
     a.dbg_w = d_w; a.dbg_info = d_info;
     launch_sample(c, a, true);
     normalise_rows_kernel<<<(int)((n + 127) / 128), 128, 0, c->stream>>>(d_w, (int)n, 2 * K);
@@ -986,7 +1021,7 @@ spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, dou
     CU(cudaMemcpyAsync(probs, d_w, sizeof(double) * (size_t)n * 2 * K, cudaMemcpyDeviceToHost, c->stream));
     if (info) CU(cudaMemcpyAsync(info, d_info, sizeof(int32_t) * (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream));
     s = sync(c, "debug_probs");
-    for (void* p : {(void*)d_doc, (void*)d_id, (void*)d_cs, (void*)d_seg, (void*)d_zr, (void*)d_w, (void*)d_info}) {
+    for (void* p : {(void*)d_doc, (void*)d_id, (void*)d_cs, (void*)d_ce, (void*)d_seg, (void*)d_zr, (void*)d_w, (void*)d_info}) {
         cudaFree(p);
         c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), p), c->allocs.end());
     }
@@ -1059,9 +1094,11 @@ namespace {
 spdp_status debug_verify(spdp_ctx* c) {
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     std::vector<uint16_t> zr((size_t)c->Nloc);
+    std::vector<float> nf((size_t)c->Dloc * Kp);
     std::vector<int32_t> n((size_t)c->Dloc * Kp), m(c->cells), t(c->cells), Q((size_t)V * Kp);
     CU(cudaMemcpy(zr.data(), c->d_zr, 2 * zr.size(), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(n.data(), c->d_n, 4 * n.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(nf.data(), c->d_n, 4 * nf.size(), cudaMemcpyDeviceToHost));
+    for (size_t j = 0; j < nf.size(); ++j) n[j] = (int32_t)nf[j];
     CU(cudaMemcpy(m.data(), c->d_m, 4 * m.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(t.data(), c->d_t, 4 * t.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(Q.data(), c->d_Q, 4 * Q.size(), cudaMemcpyDeviceToHost));

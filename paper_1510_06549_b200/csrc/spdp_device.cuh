@@ -112,11 +112,13 @@ struct SweepArgs {
     uint16_t* zr;
     uint16_t* zr_next;
     // chunks (warp work units) of the launched wave
-    const uint32_t* chunk_start;   // [nchunks + 1] absolute token offsets
+    const uint32_t* chunk_start;   // [nchunks] first token of the chunk
+    const uint32_t* chunk_end;     // [nchunks] one past its last token
     const uint32_t* chunk_seg;     // [nchunks] segment = w * I + i
     int nchunks;
+    uint32_t* work;                // persistent-warp chunk counter (zeroed before each launch)
     // counts
-    int32_t* n;
+    float* n;                      // doc-topic counts n_dk as exact integers in fp32
     int32_t* m;
     int32_t* t;
     int32_t* Q;
@@ -181,13 +183,22 @@ sample_kernel(SweepArgs A) {
     static_assert(KPL % 4 == 0, "KPL must be a multiple of 4");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int c = blockIdx.x * kWarps + wid;
-    if (c >= A.nchunks) return;                      // warp-uniform
     WarpSmem<KSPAN>& S = reinterpret_cast<WarpSmem<KSPAN>*>(smem_raw)[wid];
-    float* scratch = reinterpret_cast<float*>(smem_raw + sizeof(WarpSmem<KSPAN>) * kWarps) + (size_t)wid * 32 * KPL;
-
-    const uint32_t seg = A.chunk_seg[c];
+    // per-lane scratch: the token's topic masses (KPL floats) and counts (KPL floats)
+    float* scratch = reinterpret_cast<float*>(smem_raw + sizeof(WarpSmem<KSPAN>) * kWarps) + (size_t)wid * 64 * KPL;
+    float* myw = scratch + lane * KPL;
+    float* myn = scratch + 32 * KPL + lane * KPL;
     const int I = A.I, K = A.K, Kp = A.Kp;
+    unsigned keeps = 0, moved = 0;
+
+  // persistent warps: grab chunks (sorted longest first on the host) from a counter
+  for (;;) {
+    uint32_t cc = 0;
+    if (lane == 0) cc = atomicAdd(A.work, 1u);
+    const int c = (int)__shfl_sync(0xffffffffu, cc, 0);
+    if (c >= A.nchunks) break;                       // warp-uniform
+    __syncwarp();
+    const uint32_t seg = A.chunk_seg[c];
     const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
     const size_t row = (size_t)seg * Kp;
     const float a = A.disc[i], b = A.conc[i];
@@ -230,10 +241,8 @@ sample_kernel(SweepArgs A) {
         F[j] = S.F[kb + j];
         aF[j] = __fmul_rn((kb + j < K) ? alpha_i[kb + j] : 0.f, F[j]);
     }
-    float* myscr = scratch + lane * KPL;
     const uint32_t sweep = *A.sweep;
-    const uint32_t start = A.chunk_start[c], end = A.chunk_start[c + 1];
-    unsigned keeps = 0, moved = 0;
+    const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
 
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
         // ---- a2: this lane's token of the batch: record + Philox
@@ -265,36 +274,34 @@ sample_kernel(SweepArgs A) {
             const float Fk0 = S.Fr[rrem][k0], F1k0 = S.F1r[rrem][k0];
 
             // ---- a4/a5: doc-topic row and topic masses
-            const int32_t* nrow = A.n + (size_t)doc * Kp;
+            const float* nrow = A.n + (size_t)doc * Kp;
             double bp[NB];
             double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
-                int4 v = make_int4(0, 0, 0, 0);
-                if (kb + 4 * q < K) v = __ldg(reinterpret_cast<const int4*>(nrow + kb) + q);
-                const float w0 = __fmaf_rn((float)v.x, F[4 * q + 0], aF[4 * q + 0]);
-                const float w1 = __fmaf_rn((float)v.y, F[4 * q + 1], aF[4 * q + 1]);
-                const float w2 = __fmaf_rn((float)v.z, F[4 * q + 2], aF[4 * q + 2]);
-                const float w3 = __fmaf_rn((float)v.w, F[4 * q + 3], aF[4 * q + 3]);
-                *reinterpret_cast<float4*>(myscr + 4 * q) = make_float4(w0, w1, w2, w3);
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (kb + 4 * q < K) v = __ldg(reinterpret_cast<const float4*>(nrow + kb) + q);
+                const float w0 = __fmaf_rn(v.x, F[4 * q + 0], aF[4 * q + 0]);
+                const float w1 = __fmaf_rn(v.y, F[4 * q + 1], aF[4 * q + 1]);
+                const float w2 = __fmaf_rn(v.z, F[4 * q + 2], aF[4 * q + 2]);
+                const float w3 = __fmaf_rn(v.w, F[4 * q + 3], aF[4 * q + 3]);
+                *reinterpret_cast<float4*>(myw + 4 * q) = make_float4(w0, w1, w2, w3);
+                *reinterpret_cast<float4*>(myn + 4 * q) = v;
                 acc += (double)((w0 + w1) + (w2 + w3));
                 bp[q] = acc;
             }
             // own-removal correction of topic k0 by its owner lane
-            {
-                const int n0 = __ldg(nrow + k0);
+            const int jo = k0 - kb;
+            if (jo >= 0 && jo < KPL) {
+                const float n0 = myn[jo];
                 const float al0 = alpha_i[k0];
-                const float Fo = S.F[k0];
-                const float wold = __fmaf_rn((float)n0, Fo, __fmul_rn(al0, Fo));
-                const float wnew = __fmaf_rn((float)(n0 - 1), Fk0, __fmul_rn(al0, Fk0));
+                const float wold = myw[jo];
+                const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
                 const double delta = (double)wnew - (double)wold;
-                const int jo = k0 - kb;
-                if (jo >= 0 && jo < KPL) {
-                    acc += delta;
+                acc += delta;
 #pragma unroll
-                    for (int q = 0; q < NB; ++q) if (4 * q + 3 >= jo) bp[q] += delta;
-                    myscr[jo] = wnew;
-                }
+                for (int q = 0; q < NB; ++q) if (4 * q + 3 >= jo) bp[q] += delta;
+                myw[jo] = wnew;
             }
             // ---- a6: group scan, draw
             double incl = acc;
@@ -324,7 +331,7 @@ sample_kernel(SweepArgs A) {
                     prev = cur;
                 }
                 if (!found) before = prev - (bp[NB - 1] - (NB > 1 ? bp[NB > 1 ? NB - 2 : 0] : 0.0));
-                const float4 w4 = *reinterpret_cast<const float4*>(myscr + 4 * qs);
+                const float4 w4 = *reinterpret_cast<const float4*>(myw + 4 * qs);
                 const float wq[4] = {w4.x, w4.y, w4.z, w4.w};
                 int es = -1, elast = 0;
                 double run = before, bes = before, blast = before;
@@ -341,9 +348,9 @@ sample_kernel(SweepArgs A) {
                 }
                 const int ks = kb + 4 * qs + es;
                 const bool own = (ks == k0);
-                const int nks = __ldg(nrow + ks) - (own ? 1 : 0);
+                const float nks = myn[4 * qs + es] - (own ? 1.f : 0.f);
                 const float f1 = own ? F1k0 : S.F1[ks];
-                const float w1 = __fmaf_rn((float)nks, f1, __fmul_rn(alpha_i[ks], f1));
+                const float w1 = __fmaf_rn(nks, f1, __fmul_rn(alpha_i[ks], f1));
                 int rs;
                 if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
                 else rs = ((own ? m0 - 1 : S.m[ks]) > 0) ? 0 : 1;  // last positive slot
@@ -361,7 +368,7 @@ sample_kernel(SweepArgs A) {
                         const int k = kb + j;
                         if (k < K) {
                             const bool own = (k == k0);
-                            const int nk = __ldg(nrow + k) - (own ? 1 : 0);
+                            const float nk = nrow[k] - (own ? 1.f : 0.f);
                             float f0, f1;
                             if (own) {
                                 const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
@@ -401,6 +408,10 @@ sample_kernel(SweepArgs A) {
             if (dmv) atomicAdd(A.dm + row + k, dmv);
             if (dtv) atomicAdd(A.dt + row + k, dtv);
         }
+    }
+    __syncwarp();
+  }  // chunk loop
+    if constexpr (!DEBUG) {
 #pragma unroll
         for (int off = 16; off; off >>= 1) {
             keeps += __shfl_xor_sync(0xffffffffu, keeps, off);
@@ -415,21 +426,21 @@ sample_kernel(SweepArgs A) {
 
 template <int LPT, int KPL>
 constexpr size_t sample_smem_bytes() {
-    return kWarps * (sizeof(WarpSmem<LPT * KPL>) + 32 * KPL * sizeof(float));
+    return kWarps * (sizeof(WarpSmem<LPT * KPL>) + 64 * KPL * sizeof(float));
 }
 
 // ---------------------------------------------------------------- end of wave: n and z
 // n_{d k0} -= 1, n_{d k*} += 1 for every token of the wave that moved; zr <- zr_next.
 __global__ void apply_tokens_kernel(const uint32_t* __restrict__ tok_doc, uint16_t* __restrict__ zr,
-                                    const uint16_t* __restrict__ zr_next, int32_t* __restrict__ n,
+                                    const uint16_t* __restrict__ zr_next, float* __restrict__ n,
                                     int Kp, uint32_t begin, uint32_t end) {
     for (uint32_t p = begin + blockIdx.x * blockDim.x + threadIdx.x; p < end; p += gridDim.x * blockDim.x) {
         const uint32_t zo = zr[p], zn = zr_next[p];
         const uint32_t ko = zo & 0x7FFFu, kn = zn & 0x7FFFu;
         if (ko != kn) {
-            int32_t* nr = n + (size_t)tok_doc[p] * Kp;
-            atomicSub(nr + ko, 1);
-            atomicAdd(nr + kn, 1);
+            float* nr = n + (size_t)tok_doc[p] * Kp;
+            atomicAdd(nr + ko, -1.0f);      // exact: integer-valued fp32 (< 2^24)
+            atomicAdd(nr + kn, 1.0f);
         }
         zr[p] = (uint16_t)zn;
     }
@@ -573,12 +584,12 @@ perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const double*
     for (int j = 0; j < KPL; ++j) al[j] = (kb + j < K) ? A.alpha64[(size_t)i * Kp + kb + j] : 0.0;
     const double asum = alpha_sum[i];
     double ll = 0.0;
-    const uint32_t start = A.chunk_start[c], end = A.chunk_start[c + 1];
+    const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
     for (uint32_t base = start; base < end; base += TPW) {
         const uint32_t tok = base + g;
         const bool valid = tok < end;
         const uint32_t doc = valid ? A.tok_doc[tok] : 0u;
-        const int32_t* nrow = A.n + (size_t)doc * Kp + kb;
+        const float* nrow = A.n + (size_t)doc * Kp + kb;
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < KPL; ++j)
