@@ -175,7 +175,7 @@ struct WarpSmem {
 //     prefix exceeds u * total, in the paper's slot order j = 2k (r = 1),
 //     2k+1 (r = 0) — the r split uses w1 = (alpha + n) F1 exactly; smem deltas.
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 2 : 4)
+__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 2 : 5)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
@@ -184,10 +184,6 @@ sample_kernel(SweepArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN>& S = reinterpret_cast<WarpSmem<KSPAN>*>(smem_raw)[wid];
-    // per-lane scratch: the token's topic masses (KPL floats) and counts (KPL floats)
-    float* scratch = reinterpret_cast<float*>(smem_raw + sizeof(WarpSmem<KSPAN>) * kWarps) + (size_t)wid * 64 * KPL;
-    float* myw = scratch + lane * KPL;
-    float* myn = scratch + 32 * KPL + lane * KPL;
     const int I = A.I, K = A.K, Kp = A.Kp;
     unsigned keeps = 0, moved = 0;
 
@@ -285,23 +281,23 @@ sample_kernel(SweepArgs A) {
                 const float w1 = __fmaf_rn(v.y, F[4 * q + 1], aF[4 * q + 1]);
                 const float w2 = __fmaf_rn(v.z, F[4 * q + 2], aF[4 * q + 2]);
                 const float w3 = __fmaf_rn(v.w, F[4 * q + 3], aF[4 * q + 3]);
-                *reinterpret_cast<float4*>(myw + 4 * q) = make_float4(w0, w1, w2, w3);
-                *reinterpret_cast<float4*>(myn + 4 * q) = v;
                 acc += (double)((w0 + w1) + (w2 + w3));
                 bp[q] = acc;
             }
             // own-removal correction of topic k0 by its owner lane
             const int jo = k0 - kb;
-            if (jo >= 0 && jo < KPL) {
-                const float n0 = myn[jo];
+            const bool owner = (jo >= 0 && jo < KPL);
+            float wnew = 0.f;
+            if (owner) {
+                const float n0 = __ldg(nrow + k0);
                 const float al0 = alpha_i[k0];
-                const float wold = myw[jo];
-                const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
+                const float Fo = S.F[k0];
+                const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));   // == the main loop's mass
+                wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
                 const double delta = (double)wnew - (double)wold;
                 acc += delta;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) if (4 * q + 3 >= jo) bp[q] += delta;
-                myw[jo] = wnew;
             }
             // ---- a6: group scan, draw
             double incl = acc;
@@ -331,26 +327,38 @@ sample_kernel(SweepArgs A) {
                     prev = cur;
                 }
                 if (!found) before = prev - (bp[NB - 1] - (NB > 1 ? bp[NB > 1 ? NB - 2 : 0] : 0.0));
-                const float4 w4 = *reinterpret_cast<const float4*>(myw + 4 * qs);
-                const float wq[4] = {w4.x, w4.y, w4.z, w4.w};
+                // recompute the block's 4 masses exactly as the main loop did
+                const int kq = kb + 4 * qs;
+                float4 n4 = make_float4(0.f, 0.f, 0.f, 0.f), F4 = n4, al4 = n4;
+                if (kq < K) {
+                    n4 = __ldg(reinterpret_cast<const float4*>(nrow + kq));
+                    F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
+                    al4 = __ldg(reinterpret_cast<const float4*>(alpha_i + kq));
+                }
+                const float nq[4] = {n4.x, n4.y, n4.z, n4.w};
+                float wq[4] = {__fmaf_rn(n4.x, F4.x, __fmul_rn(al4.x, F4.x)), __fmaf_rn(n4.y, F4.y, __fmul_rn(al4.y, F4.y)),
+                               __fmaf_rn(n4.z, F4.z, __fmul_rn(al4.z, F4.z)), __fmaf_rn(n4.w, F4.w, __fmul_rn(al4.w, F4.w))};
+                const float alq[4] = {al4.x, al4.y, al4.z, al4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) if (kq + e == k0) wq[e] = wnew;
                 int es = -1, elast = 0;
                 double run = before, bes = before, blast = before;
+                float nsel = 0.f, nlast = 0.f, asel = 0.f, alast = 0.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const double nxt = run + (double)wq[e];
-                    if (es < 0 && nxt > target) { es = e; bes = run; }
-                    if (wq[e] > 0.f) { elast = e; blast = run; }
+                    if (es < 0 && nxt > target) { es = e; bes = run; nsel = nq[e]; asel = alq[e]; }
+                    if (wq[e] > 0.f) { elast = e; blast = run; nlast = nq[e]; alast = alq[e]; }
                     run = nxt;
                 }
                 if (es < 0 || fb) {                  // rounding: last positive topic of the block
-                    es = elast;
-                    bes = blast;                     // only used for the r split below
+                    es = elast; bes = blast; nsel = nlast; asel = alast;
                 }
-                const int ks = kb + 4 * qs + es;
+                const int ks = kq + es;
                 const bool own = (ks == k0);
-                const float nks = myn[4 * qs + es] - (own ? 1.f : 0.f);
+                const float nks = nsel - (own ? 1.f : 0.f);
                 const float f1 = own ? F1k0 : S.F1[ks];
-                const float w1 = __fmaf_rn(nks, f1, __fmul_rn(alpha_i[ks], f1));
+                const float w1 = __fmaf_rn(nks, f1, __fmul_rn(asel, f1));
                 int rs;
                 if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
                 else rs = ((own ? m0 - 1 : S.m[ks]) > 0) ? 0 : 1;  // last positive slot
@@ -426,7 +434,7 @@ sample_kernel(SweepArgs A) {
 
 template <int LPT, int KPL>
 constexpr size_t sample_smem_bytes() {
-    return kWarps * (sizeof(WarpSmem<LPT * KPL>) + 64 * KPL * sizeof(float));
+    return kWarps * sizeof(WarpSmem<LPT * KPL>);
 }
 
 // ---------------------------------------------------------------- end of wave: n and z
