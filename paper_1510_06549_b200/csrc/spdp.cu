@@ -51,11 +51,11 @@ void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4
 
 // (lanes per token, topics per lane) by K: few lanes per token so the
 // per-token fixed work (removal, scan, search) is shared by 32/LPT tokens.
-int pick_lpt(int K) { return K <= 32 ? 4 : (K <= 128 ? 8 : (K <= 256 ? 16 : 32)); }
+int pick_lpt(int K) { return K <= 128 ? 4 : (K <= 256 ? 8 : (K <= 512 ? 16 : 32)); }
 int pick_kpl(int K) {
     if (K <= 16) return 4;
-    if (K <= 64) return 8;
-    if (K <= 512) return 16;
+    if (K <= 32) return 8;
+    if (K <= 64) return 16;
     return 32;
 }
 
@@ -198,10 +198,12 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
     switch (LPT_ * 100 + KPL_) {                            \
         case 404: CALL(4, 4); break;                        \
         case 408: CALL(4, 8); break;                        \
-        case 808: CALL(8, 8); break;                        \
+        case 416: CALL(4, 16); break;                       \
+        case 432: CALL(4, 32); break;                       \
         case 816: CALL(8, 16); break;                       \
         case 1616: CALL(16, 16); break;                     \
-        case 3216: CALL(32, 16); break;                     \
+        case 832: CALL(8, 32); break;                       \
+        case 1632: CALL(16, 32); break;                     \
         case 3232: CALL(32, 32); break;                     \
         default: break;                                     \
     }
@@ -491,6 +493,10 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     c->cfg.alpha_ik = nullptr; c->cfg.discount = nullptr; c->cfg.concentration = nullptr; c->cfg.nccl_unique_id = nullptr;
     c->LPT = pick_lpt(c->K);
     c->KPL = pick_kpl(c->K);
+    if (const char* e = getenv("SPDP_KERNEL_CFG")) {       // tuning override "LPTxKPL", e.g. "8x16"
+        int l = 0, p = 0;
+        if (sscanf(e, "%dx%d", &l, &p) == 2 && l * p >= c->K) { c->LPT = l; c->KPL = p; }
+    }
     if (c->LPT * c->KPL < c->K) return bad("internal: no kernel configuration for K");
     int chunk = 256;
     if (const char* e = getenv("SPDP_CHUNK_TOKENS")) chunk = std::max(1, atoi(e));

@@ -155,6 +155,7 @@ struct WarpSmem {
     float F1[KSPAN];     // F1 at the snapshot counts
     float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
     float F1r[2][KSPAN];
+    float al[KSPAN];     // alpha_ik (0 on padding)
     int m[KSPAN];
     int t[KSPAN];
     int dm[KSPAN];       // the chunk's delta m, delta t
@@ -175,7 +176,7 @@ struct WarpSmem {
 //     prefix exceeds u * total, in the paper's slot order j = 2k (r = 1),
 //     2k+1 (r = 0) — the r split uses w1 = (alpha + n) F1 exactly; smem deltas.
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 2 : 5)
+__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 4 : 5)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
@@ -224,6 +225,7 @@ sample_kernel(SweepArgs A) {
         }
         S.F[k] = F0 + F1; S.F1[k] = F1;
         S.Fr[0][k] = R0; S.Fr[1][k] = R1; S.F1r[0][k] = R10; S.F1r[1][k] = R11;
+        S.al[k] = (k < K) ? alpha_i[k] : 0.f;
         S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
     }
     __syncwarp();
@@ -235,7 +237,7 @@ sample_kernel(SweepArgs A) {
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
         F[j] = S.F[kb + j];
-        aF[j] = __fmul_rn((kb + j < K) ? alpha_i[kb + j] : 0.f, F[j]);
+        aF[j] = __fmul_rn(S.al[kb + j], F[j]);
     }
     const uint32_t sweep = *A.sweep;
     const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
@@ -243,11 +245,11 @@ sample_kernel(SweepArgs A) {
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
         // ---- a2: this lane's token of the batch: record + Philox
         const uint32_t nb = min(32u, end - b0);
-        uint32_t t_doc = 0, t_zr = 0, t_x0 = 0;
+        uint32_t t_noff = 0, t_zr = 0, t_x0 = 0;
         double t_u = 0.0;
         if ((uint32_t)lane < nb) {
             const uint32_t p = b0 + lane;
-            t_doc = A.tok_doc[p];
+            t_noff = A.tok_doc[p] * (uint32_t)Kp;          // doc-topic row offset (fits 32 bits)
             t_zr = A.zr[p];
             const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);
             t_x0 = x.x;
@@ -256,7 +258,7 @@ sample_kernel(SweepArgs A) {
         for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
             const uint32_t src = s0 + g;
             const bool valid = src < nb;
-            const uint32_t doc = __shfl_sync(0xffffffffu, t_doc, src & 31);
+            const uint32_t noff = __shfl_sync(0xffffffffu, t_noff, src & 31);
             const uint32_t zr0 = __shfl_sync(0xffffffffu, t_zr, src & 31);
             const uint32_t x0 = __shfl_sync(0xffffffffu, t_x0, src & 31);
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
@@ -270,7 +272,13 @@ sample_kernel(SweepArgs A) {
             const float Fk0 = S.Fr[rrem][k0], F1k0 = S.F1r[rrem][k0];
 
             // ---- a4/a5: doc-topic row and topic masses
-            const float* nrow = A.n + (size_t)doc * Kp;
+            const float* nrow = A.n + noff;
+            // the owner lane of k0 fetches what its correction needs before the main loop
+            const int jo = k0 - kb;
+            const bool owner = (jo >= 0 && jo < KPL);
+            const float n0 = owner ? __ldg(nrow + k0) : 0.f;
+            const float al0 = S.al[k0];
+            const float Fo = S.F[k0];
             double bp[NB];
             double acc = 0.0;
 #pragma unroll
@@ -285,13 +293,8 @@ sample_kernel(SweepArgs A) {
                 bp[q] = acc;
             }
             // own-removal correction of topic k0 by its owner lane
-            const int jo = k0 - kb;
-            const bool owner = (jo >= 0 && jo < KPL);
             float wnew = 0.f;
             if (owner) {
-                const float n0 = __ldg(nrow + k0);
-                const float al0 = alpha_i[k0];
-                const float Fo = S.F[k0];
                 const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));   // == the main loop's mass
                 wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
                 const double delta = (double)wnew - (double)wold;
@@ -333,7 +336,7 @@ sample_kernel(SweepArgs A) {
                 if (kq < K) {
                     n4 = __ldg(reinterpret_cast<const float4*>(nrow + kq));
                     F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
-                    al4 = __ldg(reinterpret_cast<const float4*>(alpha_i + kq));
+                    al4 = *reinterpret_cast<const float4*>(&S.al[kq]);
                 }
                 const float nq[4] = {n4.x, n4.y, n4.z, n4.w};
                 float wq[4] = {__fmaf_rn(n4.x, F4.x, __fmul_rn(al4.x, F4.x)), __fmaf_rn(n4.y, F4.y, __fmul_rn(al4.y, F4.y)),
@@ -377,6 +380,7 @@ sample_kernel(SweepArgs A) {
                         if (k < K) {
                             const bool own = (k == k0);
                             const float nk = nrow[k] - (own ? 1.f : 0.f);
+                            const uint32_t doc = noff / (uint32_t)Kp; (void)doc;
                             float f0, f1;
                             if (own) {
                                 const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
