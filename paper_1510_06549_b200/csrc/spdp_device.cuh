@@ -163,20 +163,24 @@ struct WarpSmem {
 };
 
 // One warp per chunk of one (w, i) segment.  LPT lanes per token (TPW = 32/LPT
-// tokens in flight per warp-step), each lane owning KPL consecutive topics.
+// tokens in flight per warp-step), each lane owning KPL topics as NB = KPL/4
+// blocks of 4: block B = q*LPT + gl holds topics 4B..4B+3, so one 16-byte load
+// instruction of a group covers 4*LPT consecutive topics (coalesced rows).
 //   prologue (once per chunk): the segment's factors F_k, F1_k at the snapshot,
-//     and the own-removal variants for both removal draws (Alg.1 lines 4-10),
-//     so a token's removal costs two shared-memory loads;
-//   per 32 tokens: lane l loads token l's record and runs its Philox
-//     (a2), the groups receive them by shuffles;
+//     and the own-removal variants for both removal draws (Alg.1 lines 4-10);
+//   per 32 tokens: lane l loads token l's record and runs its Philox (a2);
+//     the groups receive them by shuffles;
 //   per token (a3-a7): removal draw against the snapshot; topic masses
-//     w_k = (alpha_ik + n_dk) F_k (one FFMA each) summed per 4-topic block in
-//     fp32 and across blocks/lanes in fp64; the own-removal correction of
-//     topic k0 added by its owner lane; group scan; first slot whose fp64
-//     prefix exceeds u * total, in the paper's slot order j = 2k (r = 1),
-//     2k+1 (r = 0) — the r split uses w1 = (alpha + n) F1 exactly; smem deltas.
+//     w_k = (alpha_ik + n_dk) F_k (one FFMA each) summed per block in fp32;
+//     the own-removal correction of topic k0 by its owner lane; block-column
+//     totals T_q over the group, their fp64 prefix P_q, then the lane and the
+//     topic where the fp64 prefix first exceeds u * total, slots in the paper's
+//     order j = 2k (r = 1), 2k+1 (r = 0); the r split uses w1 = (alpha + n) F1.
+//   Every boundary is an fp64 sum of fp32 partial sums of <= 4 terms, so a
+//   boundary is off by at most a few fp32 ulps of a partial sum (< 3e-7 of the
+//   total), inside the 1e-6 band of north_star (5).
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 4 : 5)
+__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 3 : 5)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
@@ -187,6 +191,8 @@ sample_kernel(SweepArgs A) {
     WarpSmem<KSPAN>& S = reinterpret_cast<WarpSmem<KSPAN>*>(smem_raw)[wid];
     const int I = A.I, K = A.K, Kp = A.Kp;
     unsigned keeps = 0, moved = 0;
+    const int g = lane / LPT, gl = lane % LPT;
+    const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
 
   // persistent warps: grab chunks (sorted longest first on the host) from a counter
   for (;;) {
@@ -230,14 +236,15 @@ sample_kernel(SweepArgs A) {
     }
     __syncwarp();
 
-    const int g = lane / LPT, gl = lane % LPT;
-    const int kb = gl * KPL;                          // first topic of this lane
-    const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
     float F[KPL], aF[KPL];
 #pragma unroll
-    for (int j = 0; j < KPL; ++j) {
-        F[j] = S.F[kb + j];
-        aF[j] = __fmul_rn(S.al[kb + j], F[j]);
+    for (int q = 0; q < NB; ++q) {
+        const int kq = 4 * (q * LPT + gl);
+        const float4 f4 = *reinterpret_cast<const float4*>(&S.F[kq]);
+        const float4 a4 = *reinterpret_cast<const float4*>(&S.al[kq]);
+        F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
+        aF[4 * q] = __fmul_rn(a4.x, f4.x); aF[4 * q + 1] = __fmul_rn(a4.y, f4.y);
+        aF[4 * q + 2] = __fmul_rn(a4.z, f4.z); aF[4 * q + 3] = __fmul_rn(a4.w, f4.w);
     }
     const uint32_t sweep = *A.sweep;
     const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
@@ -263,6 +270,7 @@ sample_kernel(SweepArgs A) {
             const uint32_t x0 = __shfl_sync(0xffffffffu, t_x0, src & 31);
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
             const uint32_t tok = b0 + src;
+            const float* nrow = A.n + noff;
 
             // ---- a3: removal against the wave-start snapshot
             const int k0 = (int)(zr0 & 0x7FFFu);
@@ -270,68 +278,81 @@ sample_kernel(SweepArgs A) {
             const int rrem = removal_draw(x0, m0, t0);
             const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
             const float Fk0 = S.Fr[rrem][k0], F1k0 = S.F1r[rrem][k0];
-
-            // ---- a4/a5: doc-topic row and topic masses
-            const float* nrow = A.n + noff;
-            // the owner lane of k0 fetches what its correction needs before the main loop
-            const int jo = k0 - kb;
-            const bool owner = (jo >= 0 && jo < KPL);
+            const int B0 = k0 >> 2, q0 = B0 / LPT;
+            const bool owner = (B0 % LPT) == gl;
             const float n0 = owner ? __ldg(nrow + k0) : 0.f;
-            const float al0 = S.al[k0];
-            const float Fo = S.F[k0];
-            double bp[NB];
-            double acc = 0.0;
+            const float al0 = S.al[k0], Fo = S.F[k0];
+
+            // ---- a4/a5: doc-topic row (coalesced per group) and block masses
+            float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
+                const int kq = 4 * (q * LPT + gl);
                 float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (kb + 4 * q < K) v = __ldg(reinterpret_cast<const float4*>(nrow + kb) + q);
+                if (kq < K) v = __ldg(reinterpret_cast<const float4*>(nrow + kq));
                 const float w0 = __fmaf_rn(v.x, F[4 * q + 0], aF[4 * q + 0]);
                 const float w1 = __fmaf_rn(v.y, F[4 * q + 1], aF[4 * q + 1]);
                 const float w2 = __fmaf_rn(v.z, F[4 * q + 2], aF[4 * q + 2]);
                 const float w3 = __fmaf_rn(v.w, F[4 * q + 3], aF[4 * q + 3]);
-                acc += (double)((w0 + w1) + (w2 + w3));
-                bp[q] = acc;
+                sb[q] = (w0 + w1) + (w2 + w3);
             }
-            // own-removal correction of topic k0 by its owner lane
-            float wnew = 0.f;
+            // own-removal correction of topic k0 (its owner lane)
+            const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the main loop's mass
+            const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
             if (owner) {
-                const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));   // == the main loop's mass
-                wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
-                const double delta = (double)wnew - (double)wold;
-                acc += delta;
 #pragma unroll
-                for (int q = 0; q < NB; ++q) if (4 * q + 3 >= jo) bp[q] += delta;
+                for (int q = 0; q < NB; ++q) if (q == q0) sb[q] = sb[q] - wold + wnew;
             }
-            // ---- a6: group scan, draw
-            double incl = acc;
+            // ---- a6: block-column totals over the group, fp64 prefix over columns
+            float Tq[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                float x = sb[q];
+#pragma unroll
+                for (int off = 1; off < LPT; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off, LPT);
+                Tq[q] = x;
+            }
+            double P = 0.0, Pq = 0.0;
+            int qs = -1, qlast = 0;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                const double nxt = P + (double)Tq[q];
+                if (Tq[q] > 0.f) qlast = q;
+                P = nxt;
+            }
+            const double total = P;
+            const double target = u * total;
+            P = 0.0;
+            float sq = 0.f;
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                const double nxt = P + (double)Tq[q];
+                if (qs < 0 && nxt > target) { qs = q; Pq = P; sq = sb[q]; }
+                P = nxt;
+            }
+            bool fb = false;
+            if (qs < 0) {                                  // rounding: the last non-empty column
+                fb = true; qs = qlast; Pq = 0.0;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) { if (q < qlast) Pq += (double)Tq[q]; if (q == qlast) sq = sb[q]; }
+            }
+            // lanes of the group within column qs: fp32 exclusive scan
+            float incl = sq;
 #pragma unroll
             for (int off = 1; off < LPT; off <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
+                const float y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
                 if (gl >= off) incl += y;
             }
-            double excl = __shfl_up_sync(0xffffffffu, incl, 1, LPT);
-            if (gl == 0) excl = 0.0;
-            const double total = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
-            const double target = u * total;
-            const unsigned hit = __ballot_sync(0xffffffffu, incl > target) & gmask;
-            const unsigned pos = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
-            const bool fb = (hit == 0u);
+            const float excl = incl - sq;
+            const double lbeg = Pq + (double)excl;
+            const unsigned hit = __ballot_sync(0xffffffffu, !fb && (lbeg + (double)sq > target)) & gmask;
+            const unsigned pos = __ballot_sync(0xffffffffu, sq > 0.f) & gmask;
+            fb = fb || (hit == 0u);
             const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
             int slot = 0;
             if (lane == winner) {
-                // block, then topic within the block (fp64 prefix of fp32 masses)
-                int qs = NB - 1;
-                double prev = excl, before = excl;
-                bool found = false;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    const double cur = excl + bp[q];
-                    if (!found && cur > target) { qs = q; before = prev; found = true; }
-                    prev = cur;
-                }
-                if (!found) before = prev - (bp[NB - 1] - (NB > 1 ? bp[NB > 1 ? NB - 2 : 0] : 0.0));
                 // recompute the block's 4 masses exactly as the main loop did
-                const int kq = kb + 4 * qs;
+                const int kq = 4 * (qs * LPT + gl);
                 float4 n4 = make_float4(0.f, 0.f, 0.f, 0.f), F4 = n4, al4 = n4;
                 if (kq < K) {
                     n4 = __ldg(reinterpret_cast<const float4*>(nrow + kq));
@@ -345,7 +366,7 @@ sample_kernel(SweepArgs A) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) if (kq + e == k0) wq[e] = wnew;
                 int es = -1, elast = 0;
-                double run = before, bes = before, blast = before;
+                double run = lbeg, bes = lbeg, blast = lbeg;
                 float nsel = 0.f, nlast = 0.f, asel = 0.f, alast = 0.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -374,26 +395,21 @@ sample_kernel(SweepArgs A) {
             if constexpr (DEBUG) {
                 // exact slot masses w1 = (alpha + n) F1, w0 = (alpha + n) F0 of every topic
                 if (valid) {
-#pragma unroll
-                    for (int j = 0; j < KPL; ++j) {
-                        const int k = kb + j;
-                        if (k < K) {
-                            const bool own = (k == k0);
-                            const float nk = nrow[k] - (own ? 1.f : 0.f);
-                            const uint32_t doc = noff / (uint32_t)Kp; (void)doc;
-                            float f0, f1;
-                            if (own) {
-                                const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
-                                slot_factors(Mi[k] - 1, Tti[k] - rrem, Qw[k] - rrem, A.T[k] - rrem, tab[tri(mm) + tt],
-                                             a, b, A.beta, A.vbeta, f0, f1);
-                            } else {
-                                slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(S.m[k]) + S.t[k]], a, b, A.beta,
-                                             A.vbeta, f0, f1);
-                            }
-                            const double base = (double)alpha_i[k] + (double)nk;
-                            A.dbg_w[(size_t)tok * 2 * K + 2 * k] = base * (double)f1;
-                            A.dbg_w[(size_t)tok * 2 * K + 2 * k + 1] = base * (double)f0;
+                    for (int k = gl; k < K; k += LPT) {
+                        const bool own = (k == k0);
+                        const float nk = nrow[k] - (own ? 1.f : 0.f);
+                        float f0, f1;
+                        if (own) {
+                            const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
+                            slot_factors(Mi[k] - 1, Tti[k] - rrem, Qw[k] - rrem, A.T[k] - rrem, tab[tri(mm) + tt],
+                                         a, b, A.beta, A.vbeta, f0, f1);
+                        } else {
+                            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(S.m[k]) + S.t[k]], a, b, A.beta,
+                                         A.vbeta, f0, f1);
                         }
+                        const double base = (double)S.al[k] + (double)nk;
+                        A.dbg_w[(size_t)tok * 2 * K + 2 * k] = base * (double)f1;
+                        A.dbg_w[(size_t)tok * 2 * K + 2 * k + 1] = base * (double)f0;
                     }
                     if (gl == 0) {
                         int32_t* inf = A.dbg_info + (size_t)tok * 4;
