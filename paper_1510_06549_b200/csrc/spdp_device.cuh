@@ -180,7 +180,7 @@ struct WarpSmem {
 //   boundary is off by at most a few fp32 ulps of a partial sum (< 3e-7 of the
 //   total), inside the 1e-6 band of north_star (5).
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 3 : 5)
+__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 3 : 4)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
@@ -262,6 +262,17 @@ sample_kernel(SweepArgs A) {
             t_x0 = x.x;
             t_u = u53(x);
         }
+        // software pipeline: the doc-topic row of step s+1 is loaded during step s
+        float4 vn[NB];
+        {
+            const uint32_t noff1 = __shfl_sync(0xffffffffu, t_noff, (uint32_t)g & 31);
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                const int kq = 4 * (q * LPT + gl);
+                vn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (kq < K && (uint32_t)g < nb) vn[q] = __ldg(reinterpret_cast<const float4*>(A.n + noff1 + kq));
+            }
+        }
         for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
             const uint32_t src = s0 + g;
             const bool valid = src < nb;
@@ -269,8 +280,19 @@ sample_kernel(SweepArgs A) {
             const uint32_t zr0 = __shfl_sync(0xffffffffu, t_zr, src & 31);
             const uint32_t x0 = __shfl_sync(0xffffffffu, t_x0, src & 31);
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
+            const uint32_t nxt_src = src + TPW;
+            const uint32_t noff_n = __shfl_sync(0xffffffffu, t_noff, nxt_src & 31);
             const uint32_t tok = b0 + src;
             const float* nrow = A.n + noff;
+            float4 v[NB];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) v[q] = vn[q];
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                const int kq = 4 * (q * LPT + gl);
+                vn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (kq < K && nxt_src < nb) vn[q] = __ldg(reinterpret_cast<const float4*>(A.n + noff_n + kq));
+            }
 
             // ---- a3: removal against the wave-start snapshot
             const int k0 = (int)(zr0 & 0x7FFFu);
@@ -283,17 +305,14 @@ sample_kernel(SweepArgs A) {
             const float n0 = owner ? __ldg(nrow + k0) : 0.f;
             const float al0 = S.al[k0], Fo = S.F[k0];
 
-            // ---- a4/a5: doc-topic row (coalesced per group) and block masses
+            // ---- a4/a5: block masses from the (prefetched) doc-topic row
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
-                const int kq = 4 * (q * LPT + gl);
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (kq < K) v = __ldg(reinterpret_cast<const float4*>(nrow + kq));
-                const float w0 = __fmaf_rn(v.x, F[4 * q + 0], aF[4 * q + 0]);
-                const float w1 = __fmaf_rn(v.y, F[4 * q + 1], aF[4 * q + 1]);
-                const float w2 = __fmaf_rn(v.z, F[4 * q + 2], aF[4 * q + 2]);
-                const float w3 = __fmaf_rn(v.w, F[4 * q + 3], aF[4 * q + 3]);
+                const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], aF[4 * q + 0]);
+                const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], aF[4 * q + 1]);
+                const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], aF[4 * q + 2]);
+                const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], aF[4 * q + 3]);
                 sb[q] = (w0 + w1) + (w2 + w3);
             }
             // own-removal correction of topic k0 (its owner lane)
