@@ -302,7 +302,7 @@ sample_kernel(SweepArgs A) {
             const float Fk0 = S.Fr[rrem][k0], F1k0 = S.F1r[rrem][k0];
             const int B0 = k0 >> 2, q0 = B0 / LPT;
             const bool owner = (B0 % LPT) == gl;
-            const float n0 = owner ? __ldg(nrow + k0) : 0.f;
+            const float n0 = __ldg(nrow + k0);
             const float al0 = S.al[k0], Fo = S.F[k0];
 
             // ---- a4/a5: block masses from the (prefetched) doc-topic row
@@ -331,83 +331,64 @@ sample_kernel(SweepArgs A) {
                 for (int off = 1; off < LPT; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off, LPT);
                 Tq[q] = x;
             }
-            double P = 0.0, Pq = 0.0;
-            int qs = -1, qlast = 0;
+            double total = 0.0;
 #pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                const double nxt = P + (double)Tq[q];
-                if (Tq[q] > 0.f) qlast = q;
-                P = nxt;
-            }
-            const double total = P;
+            for (int q = 0; q < NB; ++q) total += (double)Tq[q];
             const double target = u * total;
-            P = 0.0;
-            float sq = 0.f;
+            int qs = -1, qlast = 0;
+            double P = 0.0, Pq = 0.0, Plast = 0.0;
+            float sq = 0.f, slast = 0.f;
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
                 const double nxt = P + (double)Tq[q];
                 if (qs < 0 && nxt > target) { qs = q; Pq = P; sq = sb[q]; }
+                if (Tq[q] > 0.f) { qlast = q; Plast = P; slast = sb[q]; }
                 P = nxt;
             }
-            bool fb = false;
-            if (qs < 0) {                                  // rounding: the last non-empty column
-                fb = true; qs = qlast; Pq = 0.0;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) { if (q < qlast) Pq += (double)Tq[q]; if (q == qlast) sq = sb[q]; }
-            }
-            // lanes of the group within column qs: fp32 exclusive scan
+            bool fb = (qs < 0);
+            if (fb) { qs = qlast; Pq = Plast; sq = slast; }   // rounding: the last non-empty column
+            // lanes of the group within column qs: fp32 inclusive scan, ballot for the lane
             float incl = sq;
 #pragma unroll
             for (int off = 1; off < LPT; off <<= 1) {
                 const float y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
                 if (gl >= off) incl += y;
             }
-            const float excl = incl - sq;
-            const double lbeg = Pq + (double)excl;
-            const unsigned hit = __ballot_sync(0xffffffffu, !fb && (lbeg + (double)sq > target)) & gmask;
+            const double lbeg = Pq + (double)(incl - sq);
+            const unsigned hit = __ballot_sync(0xffffffffu, !fb && (Pq + (double)incl > target)) & gmask;
             const unsigned pos = __ballot_sync(0xffffffffu, sq > 0.f) & gmask;
             fb = fb || (hit == 0u);
             const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
-            int slot = 0;
-            if (lane == winner) {
-                // recompute the block's 4 masses exactly as the main loop did
-                const int kq = 4 * (qs * LPT + gl);
-                float4 n4 = make_float4(0.f, 0.f, 0.f, 0.f), F4 = n4, al4 = n4;
-                if (kq < K) {
-                    n4 = __ldg(reinterpret_cast<const float4*>(nrow + kq));
-                    F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
-                    al4 = *reinterpret_cast<const float4*>(&S.al[kq]);
-                }
-                const float nq[4] = {n4.x, n4.y, n4.z, n4.w};
-                float wq[4] = {__fmaf_rn(n4.x, F4.x, __fmul_rn(al4.x, F4.x)), __fmaf_rn(n4.y, F4.y, __fmul_rn(al4.y, F4.y)),
-                               __fmaf_rn(n4.z, F4.z, __fmul_rn(al4.z, F4.z)), __fmaf_rn(n4.w, F4.w, __fmul_rn(al4.w, F4.w))};
-                const float alq[4] = {al4.x, al4.y, al4.z, al4.w};
+            // ---- the winning block's 4 topics, one per lane gl < 4 of the group
+            const double wbeg = __shfl_sync(0xffffffffu, lbeg, winner);
+            const int kq = 4 * (qs * LPT + (winner % LPT));
+            const int kk = kq + (gl & 3);
+            const bool act = (gl < 4) && (kk < K);
+            float ne = 0.f, Fe = 0.f, ale = 0.f;
+            if (act) { ne = __ldg(nrow + kk); Fe = S.F[kk]; ale = S.al[kk]; }
+            const bool own = act && (kk == k0);
+            float we = __fmaf_rn(ne, Fe, __fmul_rn(ale, Fe));
+            if (own) we = wnew;
+            float ie = we;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) if (kq + e == k0) wq[e] = wnew;
-                int es = -1, elast = 0;
-                double run = lbeg, bes = lbeg, blast = lbeg;
-                float nsel = 0.f, nlast = 0.f, asel = 0.f, alast = 0.f;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const double nxt = run + (double)wq[e];
-                    if (es < 0 && nxt > target) { es = e; bes = run; nsel = nq[e]; asel = alq[e]; }
-                    if (wq[e] > 0.f) { elast = e; blast = run; nlast = nq[e]; alast = alq[e]; }
-                    run = nxt;
-                }
-                if (es < 0 || fb) {                  // rounding: last positive topic of the block
-                    es = elast; bes = blast; nsel = nlast; asel = alast;
-                }
-                const int ks = kq + es;
-                const bool own = (ks == k0);
-                const float nks = nsel - (own ? 1.f : 0.f);
-                const float f1 = own ? F1k0 : S.F1[ks];
-                const float w1 = __fmaf_rn(nks, f1, __fmul_rn(asel, f1));
-                int rs;
-                if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
-                else rs = ((own ? m0 - 1 : S.m[ks]) > 0) ? 0 : 1;  // last positive slot
-                slot = ks | (rs << 15);
+            for (int off = 1; off < 4; off <<= 1) {
+                const float y = __shfl_up_sync(0xffffffffu, ie, off, LPT);
+                if (gl >= off) ie += y;
             }
-            slot = __shfl_sync(0xffffffffu, slot, winner);
+            const unsigned ehit = __ballot_sync(0xffffffffu, act && !fb && (wbeg + (double)ie > target)) & gmask;
+            const unsigned epos = __ballot_sync(0xffffffffu, act && we > 0.f) & gmask;
+            const int es = ehit ? (__ffs(ehit) - 1) : (epos ? 31 - __clz(epos) : g * LPT);
+            const bool efb = fb || (ehit == 0u);
+            int slot = 0;
+            if (lane == es) {
+                const float f1 = own ? F1k0 : S.F1[kk];
+                const float w1 = __fmaf_rn(ne - (own ? 1.f : 0.f), f1, __fmul_rn(ale, f1));
+                int rs;
+                if (!efb) rs = (wbeg + (double)(ie - we) + (double)w1 > target) ? 1 : 0;
+                else rs = ((own ? m0 - 1 : S.m[kk]) > 0) ? 0 : 1;   // last positive slot
+                slot = kk | (rs << 15);
+            }
+            slot = __shfl_sync(0xffffffffu, slot, es);
             int ks = slot & 0x7FFF, rs = slot >> 15;
             if (keep) { ks = k0; rs = 1; }
 
