@@ -661,7 +661,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_zr, c->Nloc); ALLOC(c->d_zr_next, c->Nloc);
     ALLOC(c->d_chunk_start, nch); ALLOC(c->d_chunk_end, nch); ALLOC(c->d_chunk_seg, nch);
     ALLOC(c->d_sweep, 1);
-    ALLOC(c->d_n, (size_t)c->Dloc * Kp);
+    ALLOC(c->d_n, (size_t)c->Dloc * Kp + 1024);      // +1024: the sample kernel reads whole topic spans
+    CU(cudaMemset(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024)));
     ALLOC(c->d_work, (size_t)W + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
     ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);

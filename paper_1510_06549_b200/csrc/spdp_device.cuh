@@ -149,12 +149,13 @@ struct SweepArgs {
 
 // ---------------------------------------------------------------- the sample kernel
 // Per-warp shared memory layout (floats / ints, KSPAN entries each).
-template <int KSPAN>
+template <int KSPAN, int KPL>
 struct WarpSmem {
+    float w[32 * KPL];   // each lane's topic masses of the current token (final search)
     float F[KSPAN];      // F0 + F1 at the snapshot counts
-    float F1[KSPAN];     // F1 at the snapshot counts
+    float R1[KSPAN];     // F1 / (F0 + F1): the r = 1 share of the topic mass
     float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
-    float F1r[2][KSPAN];
+    float R1r[2][KSPAN];
     float al[KSPAN];     // alpha_ik (0 on padding)
     int m[KSPAN];
     int t[KSPAN];
@@ -188,7 +189,7 @@ sample_kernel(SweepArgs A) {
     static_assert(KPL % 4 == 0, "KPL must be a multiple of 4");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpSmem<KSPAN>& S = reinterpret_cast<WarpSmem<KSPAN>*>(smem_raw)[wid];
+    WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
     const int I = A.I, K = A.K, Kp = A.Kp;
     unsigned keeps = 0, moved = 0;
     const int g = lane / LPT, gl = lane % LPT;
@@ -229,8 +230,10 @@ sample_kernel(SweepArgs A) {
                 R1 = x0 + x1; R11 = x1;                                   // r_rem = 1: (m-1, t-1)
             }
         }
-        S.F[k] = F0 + F1; S.F1[k] = F1;
-        S.Fr[0][k] = R0; S.Fr[1][k] = R1; S.F1r[0][k] = R10; S.F1r[1][k] = R11;
+        S.F[k] = F0 + F1; S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, F0 + F1) : 0.f;
+        S.Fr[0][k] = R0; S.Fr[1][k] = R1;
+        S.R1r[0][k] = (R10 > 0.f) ? __fdiv_rn(R10, R0) : 0.f;
+        S.R1r[1][k] = (R11 > 0.f) ? __fdiv_rn(R11, R1) : 0.f;
         S.al[k] = (k < K) ? alpha_i[k] : 0.f;
         S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
     }
@@ -262,17 +265,6 @@ sample_kernel(SweepArgs A) {
             t_x0 = x.x;
             t_u = u53(x);
         }
-        // software pipeline: the doc-topic row of step s+1 is loaded during step s
-        float4 vn[NB];
-        {
-            const uint32_t noff1 = __shfl_sync(0xffffffffu, t_noff, (uint32_t)g & 31);
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                const int kq = 4 * (q * LPT + gl);
-                vn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (kq < K && (uint32_t)g < nb) vn[q] = __ldg(reinterpret_cast<const float4*>(A.n + noff1 + kq));
-            }
-        }
         for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
             const uint32_t src = s0 + g;
             const bool valid = src < nb;
@@ -280,32 +272,31 @@ sample_kernel(SweepArgs A) {
             const uint32_t zr0 = __shfl_sync(0xffffffffu, t_zr, src & 31);
             const uint32_t x0 = __shfl_sync(0xffffffffu, t_x0, src & 31);
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
-            const uint32_t nxt_src = src + TPW;
-            const uint32_t noff_n = __shfl_sync(0xffffffffu, t_noff, nxt_src & 31);
             const uint32_t tok = b0 + src;
-            const float* nrow = A.n + noff;
+            const float* __restrict__ nrow = A.n + noff;
+            // a4: the doc-topic row, one 16-byte load per block (coalesced over the group);
+            // rows are padded so that blocks past K read harmless values (F = 0 there)
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = vn[q];
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                const int kq = 4 * (q * LPT + gl);
-                vn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (kq < K && nxt_src < nb) vn[q] = __ldg(reinterpret_cast<const float4*>(A.n + noff_n + kq));
-            }
+            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nrow + 4 * (q * LPT + gl)));
 
             // ---- a3: removal against the wave-start snapshot
             const int k0 = (int)(zr0 & 0x7FFFu);
             const int m0 = S.m[k0], t0 = S.t[k0];
             const int rrem = removal_draw(x0, m0, t0);
             const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
-            const float Fk0 = S.Fr[rrem][k0], F1k0 = S.F1r[rrem][k0];
+            const float Fk0 = S.Fr[rrem][k0];
             const int B0 = k0 >> 2, q0 = B0 / LPT;
             const bool owner = (B0 % LPT) == gl;
             const float n0 = __ldg(nrow + k0);
             const float al0 = S.al[k0], Fo = S.F[k0];
+            // own-removal correction of topic k0 (same value on every lane of the group)
+            const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the main loop's mass
+            const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
+            const float dlt = wnew - wold;
 
-            // ---- a4/a5: block masses from the (prefetched) doc-topic row
+            // ---- a5: topic masses w = (alpha + n) F, kept in smem for the final search
+            float* myw = S.w + lane * KPL;
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -313,15 +304,11 @@ sample_kernel(SweepArgs A) {
                 const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], aF[4 * q + 1]);
                 const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], aF[4 * q + 2]);
                 const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], aF[4 * q + 3]);
+                *reinterpret_cast<float4*>(myw + 4 * q) = make_float4(w0, w1, w2, w3);
                 sb[q] = (w0 + w1) + (w2 + w3);
+                if (owner && q == q0) sb[q] += dlt;
             }
-            // own-removal correction of topic k0 (its owner lane)
-            const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the main loop's mass
-            const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
-            if (owner) {
-#pragma unroll
-                for (int q = 0; q < NB; ++q) if (q == q0) sb[q] = sb[q] - wold + wnew;
-            }
+            if (owner) myw[4 * q0 + (k0 & 3)] = wnew;
             // ---- a6: block-column totals over the group, fp64 prefix over columns
             float Tq[NB];
 #pragma unroll
@@ -359,16 +346,14 @@ sample_kernel(SweepArgs A) {
             const unsigned pos = __ballot_sync(0xffffffffu, sq > 0.f) & gmask;
             fb = fb || (hit == 0u);
             const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
+            __syncwarp();
             // ---- the winning block's 4 topics, one per lane gl < 4 of the group
             const double wbeg = __shfl_sync(0xffffffffu, lbeg, winner);
             const int kq = 4 * (qs * LPT + (winner % LPT));
-            const int kk = kq + (gl & 3);
+            const int e = gl & 3;
+            const int kk = kq + e;
             const bool act = (gl < 4) && (kk < K);
-            float ne = 0.f, Fe = 0.f, ale = 0.f;
-            if (act) { ne = __ldg(nrow + kk); Fe = S.F[kk]; ale = S.al[kk]; }
-            const bool own = act && (kk == k0);
-            float we = __fmaf_rn(ne, Fe, __fmul_rn(ale, Fe));
-            if (own) we = wnew;
+            const float we = act ? S.w[winner * KPL + 4 * qs + e] : 0.f;
             float ie = we;
 #pragma unroll
             for (int off = 1; off < 4; off <<= 1) {
@@ -381,8 +366,8 @@ sample_kernel(SweepArgs A) {
             const bool efb = fb || (ehit == 0u);
             int slot = 0;
             if (lane == es) {
-                const float f1 = own ? F1k0 : S.F1[kk];
-                const float w1 = __fmaf_rn(ne - (own ? 1.f : 0.f), f1, __fmul_rn(ale, f1));
+                const bool own = (kk == k0);
+                const float w1 = we * (own ? S.R1r[rrem][k0] : S.R1[kk]);
                 int rs;
                 if (!efb) rs = (wbeg + (double)(ie - we) + (double)w1 > target) ? 1 : 0;
                 else rs = ((own ? m0 - 1 : S.m[kk]) > 0) ? 0 : 1;   // last positive slot
@@ -391,6 +376,7 @@ sample_kernel(SweepArgs A) {
             slot = __shfl_sync(0xffffffffu, slot, es);
             int ks = slot & 0x7FFF, rs = slot >> 15;
             if (keep) { ks = k0; rs = 1; }
+            __syncwarp();
 
             if constexpr (DEBUG) {
                 // exact slot masses w1 = (alpha + n) F1, w0 = (alpha + n) F0 of every topic
@@ -454,7 +440,7 @@ sample_kernel(SweepArgs A) {
 
 template <int LPT, int KPL>
 constexpr size_t sample_smem_bytes() {
-    return kWarps * sizeof(WarpSmem<LPT * KPL>);
+    return kWarps * sizeof(WarpSmem<LPT * KPL, KPL>);
 }
 
 // ---------------------------------------------------------------- end of wave: n and z
