@@ -151,7 +151,7 @@ struct SweepArgs {
 // Per-warp shared memory layout (floats / ints, KSPAN entries each).
 template <int KSPAN, int KPL>
 struct WarpSmem {
-    float w[32 * KPL];   // each lane's topic masses of the current token (final search)
+    float w[32 * KPL];   // topic masses of the current token, [q][lane][4] (conflict-free float4 stores)
     float F[KSPAN];      // F0 + F1 at the snapshot counts
     float R1[KSPAN];     // F1 / (F0 + F1): the r = 1 share of the topic mass
     float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
@@ -296,7 +296,6 @@ sample_kernel(SweepArgs A) {
             const float dlt = wnew - wold;
 
             // ---- a5: topic masses w = (alpha + n) F, kept in smem for the final search
-            float* myw = S.w + lane * KPL;
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -304,11 +303,11 @@ sample_kernel(SweepArgs A) {
                 const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], aF[4 * q + 1]);
                 const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], aF[4 * q + 2]);
                 const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], aF[4 * q + 3]);
-                *reinterpret_cast<float4*>(myw + 4 * q) = make_float4(w0, w1, w2, w3);
+                *reinterpret_cast<float4*>(S.w + (q * 32 + lane) * 4) = make_float4(w0, w1, w2, w3);
                 sb[q] = (w0 + w1) + (w2 + w3);
                 if (owner && q == q0) sb[q] += dlt;
             }
-            if (owner) myw[4 * q0 + (k0 & 3)] = wnew;
+            if (owner) S.w[(q0 * 32 + lane) * 4 + (k0 & 3)] = wnew;
             // ---- a6: block-column totals over the group, fp64 prefix over columns
             float Tq[NB];
 #pragma unroll
@@ -353,7 +352,7 @@ sample_kernel(SweepArgs A) {
             const int e = gl & 3;
             const int kk = kq + e;
             const bool act = (gl < 4) && (kk < K);
-            const float we = act ? S.w[winner * KPL + 4 * qs + e] : 0.f;
+            const float we = act ? S.w[(qs * 32 + winner) * 4 + e] : 0.f;
             float ie = we;
 #pragma unroll
             for (int off = 1; off < 4; off <<= 1) {
