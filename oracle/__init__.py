@@ -67,6 +67,10 @@ def lib():
         L.or_check_invariants.restype = C.c_int
         L.or_check_invariants.argtypes = [P]
         L.or_partition.argtypes = [P, C.c_int, P]
+        L.or_sweep_shard.restype = C.c_int
+        L.or_sweep_shard.argtypes = [P, C.c_int, C.c_int, C.c_int, P, P]
+        L.or_merge.restype = C.c_int
+        L.or_merge.argtypes = [P, P, P]
         L.or_word_prob.restype = C.c_double
         L.or_word_prob.argtypes = [P, C.c_int32, C.c_int32]
         L.or_chain_codes.restype = C.c_int
@@ -146,6 +150,19 @@ class Oracle:
         if lib().or_sweep_par(self.h, int(waves), int(shards), _ptr(f), _ptr(mg), int(max_tokens), _ptr(own)) != 0:
             raise RuntimeError("or_sweep_par failed")
         return (mg, own) if want_own else mg
+
+    def sweep_shard(self, waves: int, shards: int, shard: int):
+        """One shard's part of a distributed mode-P sweep: returns its net changes
+        (Dm, Dt) as int32 [I*V*K]; the global counts are left untouched."""
+        cells = self.I * self.V * self.K
+        Dm = np.zeros(cells, np.int32); Dt = np.zeros(cells, np.int32)
+        if lib().or_sweep_shard(self.h, int(waves), int(shards), int(shard), _ptr(Dm), _ptr(Dt)) != 0:
+            raise RuntimeError("or_sweep_shard failed")
+        return Dm, Dt
+
+    def merge(self, Dm_sum, Dt_sum):
+        Dm = np.ascontiguousarray(Dm_sum, np.int32); Dt = np.ascontiguousarray(Dt_sum, np.int32)
+        lib().or_merge(self.h, _ptr(Dm), _ptr(Dt))
 
     @property
     def sweep_index(self) -> int:

@@ -467,8 +467,8 @@ static int64_t clamp_cells(size_t cells, const int32_t *m, int32_t *t) {
  * own_zr (optional, [N]): the oracle's own draw (z | r<<15) before forcing.
  * max_tokens >= 0 limits the sweep to the first max_tokens tokens of each
  * shard's canonical order (timing samples only). */
-int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margin, int64_t max_tokens,
-                 int32_t *own_zr) {
+static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *force_zr, double *margin,
+                          int64_t max_tokens, int32_t *own_zr, int32_t *Dout_m, int32_t *Dout_t) {
     int I = s->I, V = s->V, K = s->K;
     int64_t N = s->N;
     size_t cells = (size_t)I * V * K;
@@ -494,6 +494,7 @@ int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margi
     for (int32_t d = 0; d < s->D; d++) if (s->doclen[d] > maxlen) maxlen = s->doclen[d];
     int64_t nwaves = (W == 0) ? N : (W < maxlen ? W : maxlen);
     for (int g = 0; g < G; g++) {
+        if (only >= 0 && g != only) continue;
         /* shard-local replica of the sweep-start global state (Alg.3) */
         memcpy(Lm, S0m, sizeof(int32_t) * cells);
         memcpy(Lt, S0t, sizeof(int32_t) * cells);
@@ -553,6 +554,11 @@ int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margi
         /* D_g = L_g - S0 */
         for (size_t c = 0; c < cells; c++) { Dm[c] += Lm[c] - S0m[c]; Dt[c] += Lt[c] - S0t[c]; }
     }
+    if (only >= 0) {           /* one shard of a distributed sweep: hand out D_g, no merge */
+        for (size_t c = 0; c < cells; c++) { Dout_m[c] = (int32_t)Dm[c]; Dout_t[c] = (int32_t)Dt[c]; }
+        rc = 0;
+        goto out;
+    }
     /* merge (Alg.3; reading c14-c15): S1 = clamp(S0 + sum_g D_g) */
     for (size_t c = 0; c < cells; c++) {
         s->m[c] = (int32_t)(S0m[c] + Dm[c]);
@@ -567,6 +573,27 @@ out:
     free(M); free(Tt); free(Q); free(T); free(newz); free(newr); free(rrem); free(kept); free(inwave);
     free(lw); free(prob);
     return rc;
+}
+
+int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margin, int64_t max_tokens,
+                 int32_t *own_zr) {
+    return sweep_par_impl(s, W, G, -1, force_zr, margin, max_tokens, own_zr, NULL, NULL);
+}
+
+/* Distributed form of the same sweep: shard g runs its waves and returns its
+ * net changes D_g (int32, [I*V*K]) without touching the global m, t ... */
+int or_sweep_shard(ostate *s, int W, int G, int g, int32_t *Dm, int32_t *Dt) {
+    if (g < 0 || g >= G || !Dm || !Dt) return -1;
+    return sweep_par_impl(s, W, G, g, NULL, NULL, -1, NULL, Dm, Dt);
+}
+/* ... and, once every rank holds sum_g D_g, the merge S1 = clamp(S0 + sum D). */
+int or_merge(ostate *s, const int32_t *Dm, const int32_t *Dt) {
+    size_t cells = (size_t)s->I * s->V * s->K;
+    for (size_t c = 0; c < cells; c++) { s->m[c] += Dm[c]; s->t[c] += Dt[c]; }
+    s->stats[2] += clamp_cells(cells, s->m, s->t);
+    recompute_sums(s, s->m, s->t, s->M, s->Tt, s->Q, s->T);
+    s->sweep++;
+    return 0;
 }
 
 /* ------------------------------------------------------------------ */

@@ -38,7 +38,8 @@ def lockstep_sweep(g, o, waves=1, shards=1, gpu_counts=None):
     within 1e-6 of a CDF boundary; counts bit-exact once the draws agree."""
     if gpu_counts is None:
         g.sweep(1)
-        gpu_counts = g.counts()
+        gpu_counts = g.counts(customers=False, tables=False, shadow=False, doc_topic=False)
+        gpu_counts.update(g.counts(z=False, r=False))
     forced = pack(gpu_counts["z"], gpu_counts["r"])
     margin, own = o.sweep_par(waves=waves, shards=shards, force_zr=forced, want_margin=True, want_own=True)
     mism = np.nonzero(own != forced)[0]

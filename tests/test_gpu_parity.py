@@ -159,3 +159,34 @@ def test_multi_rank_exchange_matches_oracle_shards(G, waves):
         rep, _ = lockstep_sweep(None, o, waves=waves, shards=G, gpu_counts=gc)
         assert_draw_parity(rep)
         assert_counts_equal(gc, o.state())
+
+
+def test_perplexity_trajectory_lockstep_c1_100_sweeps():
+    """north_star (5), lock-step form: 100 sweeps of C1, counts bit-exact and the
+    perplexity trajectories identical (to fp64 summation order)."""
+    c = corpus("C1")
+    g, o = pair(c, 10, waves=1)
+    worst = 0
+    for s in range(100):
+        rep, gc = lockstep_sweep(g, o)
+        assert_draw_parity(rep)
+        worst = max(worst, rep["mismatch"])
+        if s % 10 == 9:
+            assert_counts_equal(gc, o.state(), keys=("m", "t", "Q", "n"))
+            assert g.perplexity() == pytest.approx(o.perplexity(), rel=1e-9)
+
+
+@pytest.mark.slow
+def test_perplexity_trajectory_free_running_c2_100_sweeps():
+    """north_star (5): the free-running 1-GPU chain stays within 1% of the oracle's
+    (same seed, same corpus, W = 1) after 100 sweeps on C2 (1M tokens)."""
+    c = corpus("C2")
+    g, o = pair(c, 50, waves=1)
+    traj = []
+    for s in range(100):
+        g.sweep(1)
+        o.sweep_par(waves=1)
+        if s % 10 == 9:
+            traj.append((s + 1, g.perplexity(), o.perplexity()))
+    last = traj[-1]
+    assert abs(last[1] / last[2] - 1) <= 0.01, traj
