@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -92,15 +93,18 @@ struct spdp_ctx {
     std::vector<int64_t> pos_of_tok;              // canonical id -> sorted position (-1: other rank)
     std::vector<uint32_t> wave_tok_begin, wave_chunk_begin;
     std::vector<uint32_t> chunk_start, chunk_end, chunk_seg;
+    std::vector<uint32_t> wave_seg_begin, wave_segs;   // distinct (w, i) segments of each wave
     int mmax = 0;
     size_t cells = 0;
 
     // device
     uint32_t *d_tok_doc = nullptr, *d_tok_id = nullptr, *d_chunk_start = nullptr, *d_chunk_end = nullptr,
-             *d_chunk_seg = nullptr,
+             *d_chunk_seg = nullptr, *d_wave_segs = nullptr,
              *d_sweep = nullptr;
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
     float* d_n = nullptr;                         // n_dk as exact integers in fp32
+    uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
+    uint16_t* h_zr_canon = nullptr;               // pinned host copy
     uint32_t* d_work = nullptr;                   // [W + 1] persistent-warp counters
     int sample_grid = 0;
     int32_t *d_m = nullptr, *d_t = nullptr, *d_Q = nullptr, *d_M = nullptr, *d_Tt = nullptr,
@@ -265,6 +269,18 @@ void launch_merge(spdp_ctx* c, int32_t* dm, int32_t* dt, int32_t* Dm, int32_t* D
         c->d_m, c->d_t, dm, dt, Dm, Dt, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I, c->Kp, use_smem, c->d_stats);
 }
 
+// SPDP_VERBOSE=1: phase times of spdp_load_corpus on stderr
+struct LoadTimer {
+    bool on = getenv("SPDP_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[spdp] load %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
+
 spdp_status check_launch(spdp_ctx* c, const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(c, SPDP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -406,7 +422,15 @@ spdp_status run_waves(spdp_ctx* c) {
         apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n,
                                                                          c->Kp, tb, te);
         rec(c, 4 * (size_t)w + 2);
-        launch_merge(c, c->d_dm, c->d_dt, Dm, Dt);
+        {
+            const uint32_t sb = c->wave_seg_begin[(size_t)w], se = c->wave_seg_begin[(size_t)w + 1];
+            const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
+            const int use_smem = smem <= 48 * 1024;
+            const int blocks = (int)std::min<uint32_t>((se - sb + 7) / 8, 148u * 4u);
+            merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, c->stream>>>(
+                c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dm, Dt, c->d_Q, c->d_M,
+                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats);
+        }
         rec(c, 4 * (size_t)w + 3);
         c->launches += 3;
         c->acc[5] += 1;
@@ -559,6 +583,7 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
 
 spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, const int32_t* group, const int32_t* doc,
                              const int32_t* word, const int32_t* z_init, const uint8_t* r_init) {
+    LoadTimer lt;
     spdp_status s = guard(c, false);
     if (s) return s;
     if (c->loaded) return fail(c, SPDP_ESTATE, "spdp_load_corpus may be called once per context");
@@ -582,6 +607,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         c->docgroup[(size_t)d] = g;
         c->pos[(size_t)p] = c->doclen[(size_t)d]++;
     }
+    lt.mark("validate + positions");
     // M_max = largest count(i, w): bounds every m_{ikw} the chain can reach
     {
         std::vector<int32_t> cnt((size_t)I * V, 0);
@@ -601,6 +627,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             c->global_of_local.push_back(d);
         }
     c->Dloc = (int32_t)c->global_of_local.size();
+    lt.mark("M_max + partition");
     // wave plan: stable counting sort of local tokens by seg = w*I + i, then by wave = l mod W
     std::vector<uint32_t> local;
     local.reserve((size_t)num_tokens / c->G + 16);
@@ -653,6 +680,19 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
     }
     c->wave_chunk_begin[(size_t)W] = (uint32_t)c->chunk_seg.size();
+    // distinct segments per wave (the rows the wave's merge touches), ascending
+    c->wave_seg_begin.assign((size_t)W + 1, 0);
+    c->wave_segs.clear();
+    for (int w = 0; w < W; ++w) {
+        c->wave_seg_begin[(size_t)w] = (uint32_t)c->wave_segs.size();
+        std::vector<uint32_t> ss(c->chunk_seg.begin() + c->wave_chunk_begin[(size_t)w],
+                                 c->chunk_seg.begin() + c->wave_chunk_begin[(size_t)w + 1]);
+        std::sort(ss.begin(), ss.end());
+        ss.erase(std::unique(ss.begin(), ss.end()), ss.end());
+        c->wave_segs.insert(c->wave_segs.end(), ss.begin(), ss.end());
+    }
+    c->wave_seg_begin[(size_t)W] = (uint32_t)c->wave_segs.size();
+    lt.mark("wave plan + chunks");
     const size_t nch = c->chunk_seg.size();
     c->cells = (size_t)V * I * Kp;
 
@@ -660,6 +700,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_tok_doc, c->Nloc); ALLOC(c->d_tok_id, c->Nloc);
     ALLOC(c->d_zr, c->Nloc); ALLOC(c->d_zr_next, c->Nloc);
     ALLOC(c->d_chunk_start, nch); ALLOC(c->d_chunk_end, nch); ALLOC(c->d_chunk_seg, nch);
+    ALLOC(c->d_wave_segs, c->wave_segs.size());
     ALLOC(c->d_sweep, 1);
     ALLOC(c->d_n, (size_t)c->Dloc * Kp + 1024);      // +1024: the sample kernel reads whole topic spans
     CU(cudaMemset(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024)));
@@ -705,6 +746,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         CU(cudaMemcpy(c->d_tok_id, tid.data(), sizeof(uint32_t) * tid.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_chunk_start, c->chunk_start.data(), sizeof(uint32_t) * nch, cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_chunk_end, c->chunk_end.data(), sizeof(uint32_t) * nch, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_wave_segs, c->wave_segs.data(), sizeof(uint32_t) * c->wave_segs.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_chunk_seg, c->chunk_seg.data(), sizeof(uint32_t) * std::max<size_t>(nch, 0), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_doclen, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_docgroup, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice));
@@ -719,6 +761,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         CU(cudaMemset(c->d_sweep, 0, sizeof(uint32_t)));
         CU(cudaMemset(c->d_stats, 0, sizeof(unsigned long long) * 8));
     }
+    lt.mark("device alloc + upload");
     // Stirling-ratio tables, one per distinct discount (M_max rows)
     {
         std::vector<double> distinct;
@@ -744,8 +787,10 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         s = sync(c, "build_ratio_table");
         if (s) return s;
     }
+    lt.mark("Stirling-ratio tables");
     s = install_state(c, z_init, r_init, nullptr);
     if (s) return s;
+    lt.mark("initial state (counts)");
     c->loaded = true;
     return SPDP_OK;
 }
@@ -842,13 +887,20 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
     if (z || r) {
-        std::vector<uint16_t> zr((size_t)c->Nloc);
-        CU(cudaMemcpyAsync(zr.data(), c->d_zr, sizeof(uint16_t) * zr.size(), cudaMemcpyDeviceToHost, c->stream));
+        // canonical order on the device (z | r<<15, +1 so that 0 marks other ranks' tokens)
+        if (!c->d_zr_canon) ALLOC(c->d_zr_canon, c->N);
+        CU(cudaMemsetAsync(c->d_zr_canon, 0, sizeof(uint16_t) * (size_t)c->N, c->stream));
+        if (c->Nloc > 0)
+            scatter_zr_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_tok_id, c->d_zr, (uint32_t)c->Nloc, c->d_zr_canon);
+        if ((s = check_launch(c, "scatter_zr_kernel"))) return s;
+        if (!c->h_zr_canon) CU(cudaMallocHost((void**)&c->h_zr_canon, sizeof(uint16_t) * (size_t)c->N));
+        CU(cudaMemcpyAsync(c->h_zr_canon, c->d_zr_canon, sizeof(uint16_t) * (size_t)c->N, cudaMemcpyDeviceToHost,
+                           c->stream));
         if ((s = sync(c, "counts(z)"))) return s;
         std::vector<int32_t> all;
         if (gather) {
             all.assign((size_t)c->N, 0);
-            for (int64_t q = 0; q < c->Nloc; ++q) all[c->sorted_tok[(size_t)q]] = (int32_t)zr[(size_t)q] + 1;
+            for (int64_t p = 0; p < c->N; ++p) all[(size_t)p] = c->h_zr_canon[(size_t)p];
             TempBuf<int32_t> tb(c->N);
             if (!tb.p) return fail(c, SPDP_ENOMEM, "gather buffer");
             int32_t* dbuf = tb.p;
@@ -857,17 +909,14 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
                 return s;
             CU(cudaMemcpyAsync(all.data(), dbuf, sizeof(int32_t) * all.size(), cudaMemcpyDeviceToHost, c->stream));
             if ((s = sync(c, "counts(z gather)"))) return s;
-            for (int64_t p = 0; p < c->N; ++p) {
-                const uint32_t v = (uint32_t)(all[(size_t)p] - 1);
-                if (z) z[p] = (int32_t)(v & 0x7FFFu);
-                if (r) r[p] = (uint8_t)((v >> 15) & 1u);
-            }
-        } else {
-            for (int64_t q = 0; q < c->Nloc; ++q) {
-                const uint32_t p = c->sorted_tok[(size_t)q];
-                if (z) z[p] = (int32_t)(zr[(size_t)q] & 0x7FFFu);
-                if (r) r[p] = (uint8_t)((zr[(size_t)q] >> 15) & 1u);
-            }
+            for (int64_t p = 0; p < c->N; ++p) c->h_zr_canon[(size_t)p] = (uint16_t)all[(size_t)p];
+        }
+        const uint16_t* h = c->h_zr_canon;
+        for (int64_t p = 0; p < c->N; ++p) {
+            const uint32_t v = h[p];
+            if (!v) continue;                                   // another rank's token
+            if (z) z[p] = (int32_t)((v - 1u) & 0x7FFFu);
+            if (r) r[p] = (uint8_t)(((v - 1u) >> 15) & 1u);
         }
     }
     if (doc_topic) {
@@ -1090,6 +1139,7 @@ void spdp_destroy(spdp_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : c->allocs) cudaFree(p);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+    if (c->h_zr_canon) cudaFreeHost(c->h_zr_canon);
     if (c->comm && c->nccl.CommDestroy) c->nccl.CommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;

@@ -546,6 +546,92 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
     }
 }
 
+// ---------------------------------------------------------------- end of wave: touched rows only
+// One warp per (w, i) segment the wave touched: m += dm, t = clamp(t + dt) into
+// [min(1,m), m], dm = dt = 0; the changes are added to Q_w (int atomics) and to
+// the marginal sums M, Tt, T (block-reduced in smem, then int atomics), and to
+// the net-change buffer D when there is one (multi-GPU).  Integer arithmetic:
+// the result does not depend on the order of the atomics.
+__global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nseg,
+                                      int32_t* __restrict__ m, int32_t* __restrict__ t,
+                                      int32_t* __restrict__ dm, int32_t* __restrict__ dt,
+                                      int32_t* __restrict__ Dm, int32_t* __restrict__ Dt,
+                                      int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
+                                      int32_t* __restrict__ T, int I, int Kp, int use_smem_sums,
+                                      unsigned long long* __restrict__ stats) {
+    extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
+    int* sM = ssum;
+    int* sT = ssum + (size_t)I * Kp;
+    int* sK = ssum + (size_t)2 * I * Kp;
+    if (use_smem_sums) {
+        for (int j = threadIdx.x; j < (2 * I + 1) * Kp; j += blockDim.x) ssum[j] = 0;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    unsigned clamped = 0;
+    for (int j = blockIdx.x * wpb + (threadIdx.x >> 5); j < nseg; j += gridDim.x * wpb) {
+        const uint32_t seg = segs[j];
+        const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
+        for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
+            const size_t off = (size_t)seg * Kp + k4;
+            const int4 a = *reinterpret_cast<const int4*>(dm + off);
+            const int4 d = *reinterpret_cast<const int4*>(dt + off);
+            if ((a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) == 0) continue;
+            int4 vm = *reinterpret_cast<const int4*>(m + off);
+            int4 vt = *reinterpret_cast<const int4*>(t + off);
+            const int4 om = vm, ot = vt;
+            int* pm = &vm.x; int* pt = &vt.x;
+            const int* pa = &a.x; const int* pd = &d.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int mv = pm[e] + pa[e];
+                const int raw = pt[e] + pd[e];
+                int tv = min(raw, mv);
+                tv = (mv > 0) ? max(tv, 1) : 0;
+                clamped += (tv != raw);
+                pm[e] = mv; pt[e] = tv;
+            }
+            *reinterpret_cast<int4*>(m + off) = vm;
+            *reinterpret_cast<int4*>(t + off) = vt;
+            *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
+            *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
+            const int cm[4] = {vm.x - om.x, vm.y - om.y, vm.z - om.z, vm.w - om.w};
+            const int ct[4] = {vt.x - ot.x, vt.y - ot.y, vt.z - ot.z, vt.w - ot.w};
+            if (Dm) {
+                int4 x = *reinterpret_cast<int4*>(Dm + off), y = *reinterpret_cast<int4*>(Dt + off);
+                x.x += cm[0]; x.y += cm[1]; x.z += cm[2]; x.w += cm[3];
+                y.x += ct[0]; y.y += ct[1]; y.z += ct[2]; y.w += ct[3];
+                *reinterpret_cast<int4*>(Dm + off) = x;
+                *reinterpret_cast<int4*>(Dt + off) = y;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (ct[e]) {
+                    atomicAdd(Q + (size_t)w * Kp + k4 + e, ct[e]);
+                    if (use_smem_sums) { atomicAdd(sT + (size_t)i * Kp + k4 + e, ct[e]); atomicAdd(sK + k4 + e, ct[e]); }
+                    else { atomicAdd(Tt + (size_t)i * Kp + k4 + e, ct[e]); atomicAdd(T + k4 + e, ct[e]); }
+                }
+                if (cm[e]) {
+                    if (use_smem_sums) atomicAdd(sM + (size_t)i * Kp + k4 + e, cm[e]);
+                    else atomicAdd(M + (size_t)i * Kp + k4 + e, cm[e]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) clamped += __shfl_xor_sync(0xffffffffu, clamped, off);
+    if (lane == 0 && clamped) atomicAdd(stats + 2, (unsigned long long)clamped);
+    if (use_smem_sums) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < I * Kp; j += blockDim.x) {
+            if (sM[j]) atomicAdd(M + j, sM[j]);
+            if (sT[j]) atomicAdd(Tt + j, sT[j]);
+        }
+        for (int j = threadIdx.x; j < Kp; j += blockDim.x) if (sK[j]) atomicAdd(T + j, sK[j]);
+    }
+}
+
 // Multi-GPU merge (Alg.3): restore the sweep-start state
 // S0 = L - D before the exchange ...
 __global__ void unapply_net_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t,
@@ -559,6 +645,13 @@ __global__ void unapply_net_kernel(int32_t* __restrict__ m, int32_t* __restrict_
 // with (dm, dt) = the all-reduced D.
 
 __global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
+
+// zr in canonical token order (for spdp_counts): out[id[p]] = zr[p] + 1 (0 = other rank)
+__global__ void scatter_zr_kernel(const uint32_t* __restrict__ id, const uint16_t* __restrict__ zr, uint32_t n,
+                                  uint16_t* __restrict__ out) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
+        out[id[p]] = (uint16_t)(zr[p] + 1u);
+}
 
 // ---------------------------------------------------------------- training perplexity
 // One warp per chunk (all waves): phi^i_kw = (m - a t)/(b + M) + (b + a Tt)/(b + M) phi0_kw,
