@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     stale = force or not os.path.exists(LIB_PATH) or any(
         os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in _SOURCES)
     if stale:
-        cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_HERE, "csrc", "spdp.cu"), "-o", LIB_PATH, "-ldl"]
+        cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_HERE, "csrc", "spdp.cu"), "-o", LIB_PATH, "-ldl", "-lpthread"]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)

@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
+#include <thread>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -326,62 +328,84 @@ void partition_docs(uint64_t seed, int G, int64_t N, int32_t D, const std::vecto
 }
 
 // Upload (z, r or tables) as the sampler state: counts from z.
+// run fn(begin, end) over [0, n) on the host cores
+template <typename Fn>
+void parallel_for(int64_t n, Fn fn) {
+    int nt = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 32u);
+    if (n < 1 << 16) nt = 1;
+    std::vector<std::thread> th;
+    const int64_t step = (n + nt - 1) / nt;
+    for (int j = 0; j < nt; ++j) {
+        const int64_t b = j * step, e = std::min(n, b + step);
+        if (b < e) th.emplace_back(fn, b, e);
+    }
+    for (auto& x : th) x.join();
+}
+
+// Upload (z, r or tables) as the sampler state; counts from z
+// are built on the device.
 spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in, const int32_t* tables) {
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     const int64_t N = c->N;
     std::vector<int32_t> z((size_t)N);
-    std::vector<uint8_t> r((size_t)N);
-    for (int64_t p = 0; p < N; ++p) {
-        if (z_in) {
-            if (z_in[p] < 0 || z_in[p] >= K) return fail(c, SPDP_EINVAL, "z[%lld] = %d out of [0, K)", (long long)p, z_in[p]);
-            z[(size_t)p] = z_in[p];
-        } else {
-            const uint32_t ctr[4] = {(uint32_t)p, 0xFFFFFFFFu, 0u, 0u};
-            uint32_t x[4];
-            philox_host(ctr, (uint32_t)c->cfg.seed, (uint32_t)(c->cfg.seed >> 32), x);
-            z[(size_t)p] = (int32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
+    std::atomic<int64_t> badz{-1}, badr{-1};
+    parallel_for(N, [&](int64_t b, int64_t e) {
+        for (int64_t p = b; p < e; ++p) {
+            if (z_in) {
+                if (z_in[p] < 0 || z_in[p] >= K) badz = p;
+                z[(size_t)p] = z_in[p];
+            } else {
+                const uint32_t ctr[4] = {(uint32_t)p, 0xFFFFFFFFu, 0u, 0u};
+                uint32_t x[4];
+                philox_host(ctr, (uint32_t)c->cfg.seed, (uint32_t)(c->cfg.seed >> 32), x);
+                z[(size_t)p] = (int32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
+            }
+            if (r_in && r_in[p] > 1) badr = p;
         }
-    }
-    // global m, t in device layout [w][i][Kp]
-    std::vector<int32_t> m(c->cells, 0), t(c->cells, 0);
-    for (int64_t p = 0; p < N; ++p) {
-        const size_t cell = ((size_t)c->word[(size_t)p] * I + c->group[(size_t)p]) * Kp + z[(size_t)p];
-        m[cell]++;
-        if (r_in) {
-            if (r_in[p] > 1) return fail(c, SPDP_EINVAL, "r[%lld] = %d not in {0,1}", (long long)p, (int)r_in[p]);
-            r[(size_t)p] = r_in[p];
-        } else {
-            r[(size_t)p] = (t[cell] == 0) ? 1 : 0;     // first token of the cell opens its table
-        }
-        t[cell] += r[(size_t)p];
-    }
+    });
+    if (badz >= 0) return fail(c, SPDP_EINVAL, "z[%lld] out of [0, K)", (long long)badz.load());
+    if (badr >= 0) return fail(c, SPDP_EINVAL, "r[%lld] not in {0,1}", (long long)badr.load());
+    TempBuf<int32_t> dz(N), dg(N), dw(N);
+    TempBuf<uint8_t> dr(N);
+    TempBuf<uint32_t> dfirst(r_in ? 1 : c->cells);
+    TempBuf<unsigned long long> dbad(1);
+    if (!dz.p || !dg.p || !dw.p || !dr.p || !dfirst.p || !dbad.p) return fail(c, SPDP_ENOMEM, "install_state buffers");
+    CU(cudaMemcpyAsync(dz.p, z.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(dg.p, c->group.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(dw.p, c->word.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
+    if (r_in) CU(cudaMemcpyAsync(dr.p, r_in, (size_t)N, cudaMemcpyHostToDevice, c->stream));
+    else CU(cudaMemsetAsync(dfirst.p, 0xFF, sizeof(uint32_t) * c->cells, c->stream));
+    CU(cudaMemsetAsync(c->d_m, 0, sizeof(int32_t) * c->cells, c->stream));
+    CU(cudaMemsetAsync(c->d_t, 0, sizeof(int32_t) * c->cells, c->stream));
+    CU(cudaMemsetAsync(dbad.p, 0, sizeof(unsigned long long), c->stream));
+    const int grid = 148 * 8;
+    init_cells_kernel<<<grid, 256, 0, c->stream>>>(dg.p, dw.p, dz.p, r_in ? dr.p : nullptr, (uint32_t)N, I, Kp, c->d_m,
+                                                   c->d_t, dfirst.p);
+    if (!r_in)
+        init_first_table_kernel<<<grid, 256, 0, c->stream>>>(dg.p, dw.p, dz.p, (uint32_t)N, I, Kp, dfirst.p, dr.p, c->d_t);
     if (tables) {
-        for (int i = 0; i < I; ++i)
-            for (int w = 0; w < V; ++w)
-                for (int k = 0; k < K; ++k)
-                    t[((size_t)w * I + i) * Kp + k] = tables[((size_t)i * V + w) * K + k];
+        TempBuf<int32_t> dt_in((size_t)I * V * K);
+        if (!dt_in.p) return fail(c, SPDP_ENOMEM, "tables buffer");
+        CU(cudaMemcpyAsync(dt_in.p, tables, sizeof(int32_t) * (size_t)I * V * K, cudaMemcpyHostToDevice, c->stream));
+        load_tables_kernel<<<grid, 256, 0, c->stream>>>(dt_in.p, I, V, K, Kp, c->d_t);
+        spdp_status s0 = sync(c, "load tables");
+        if (s0) return s0;
     }
-    for (size_t cell = 0; cell < c->cells; ++cell)
-        if (t[cell] < 0 || t[cell] > m[cell] || ((t[cell] > 0) != (m[cell] > 0)))
-            return fail(c, SPDP_EINVAL, "table counts violate 1 <= t <= m on an occupied cell (or t > 0 on an empty one)");
-    // local doc-topic counts and token records
-    std::vector<float> n((size_t)c->Dloc * Kp, 0.f);
-    std::vector<uint16_t> zr((size_t)c->Nloc);
-    for (int64_t q = 0; q < c->Nloc; ++q) {
-        const uint32_t p = c->sorted_tok[(size_t)q];
-        n[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + z[p]] += 1.f;
-        zr[(size_t)q] = (uint16_t)(z[p] | (r[p] << 15));
-    }
-    CU(cudaMemcpyAsync(c->d_m, m.data(), sizeof(int32_t) * c->cells, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->d_t, t.data(), sizeof(int32_t) * c->cells, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->d_n, n.data(), sizeof(float) * n.size(), cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->d_zr, zr.data(), sizeof(uint16_t) * zr.size(), cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(c->d_zr_next, zr.data(), sizeof(uint16_t) * zr.size(), cudaMemcpyHostToDevice, c->stream));
+    check_cells_kernel<<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->cells, dbad.p);
+    unsigned long long nbad = 0;
+    CU(cudaMemcpyAsync(&nbad, dbad.p, sizeof(nbad), cudaMemcpyDeviceToHost, c->stream));
+    spdp_status s = sync(c, "install_state cells");
+    if (s) return s;
+    if (nbad) return fail(c, SPDP_EINVAL, "table counts violate 1 <= t <= m on %llu occupied cell(s) (or t > 0 on an empty one)", nbad);
+    CU(cudaMemsetAsync(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024), c->stream));
+    if (c->Nloc > 0)
+        init_local_kernel<<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc, Kp,
+                                                       c->d_zr, c->d_zr_next, c->d_n);
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
     if (c->d_D) CU(cudaMemsetAsync(c->d_D, 0, sizeof(int32_t) * 2 * c->cells, c->stream));
     launch_merge(c, c->d_dm, c->d_dt, nullptr, nullptr);    // zero deltas: recomputes Q and the sums
-    spdp_status s = check_launch(c, "merge_rows_kernel");
+    s = check_launch(c, "install_state kernels");
     if (s) return s;
     return sync(c, "install_state");
 }
@@ -635,20 +659,48 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         if (c->shard_of_doc[(size_t)doc[p]] == c->rank) local.push_back((uint32_t)p);
     c->Nloc = (int64_t)local.size();
     {
-        const size_t S = (size_t)V * I;
-        std::vector<uint32_t> off(S + 1, 0), tmp(local.size());
-        for (uint32_t p : local) off[(size_t)word[p] * I + group[p] + 1]++;
-        for (size_t j = 0; j < S; ++j) off[j + 1] += off[j];
-        for (uint32_t p : local) tmp[off[(size_t)word[p] * I + group[p]]++] = p;
+        // stable parallel counting sort: per-thread histograms over contiguous ranges
+        const size_t S = (size_t)V * I, n = local.size();
+        auto counting_sort = [&](const std::vector<uint32_t>& in, std::vector<uint32_t>& out, size_t nbuckets,
+                                 auto key) {
+            const int nt = (int)std::min<size_t>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())),
+                                                 std::max<size_t>(1, n >> 16));
+            const size_t step = (n + nt - 1) / nt;
+            std::vector<std::vector<uint32_t>> hist((size_t)nt, std::vector<uint32_t>(nbuckets, 0));
+            std::vector<std::thread> th;
+            for (int j = 0; j < nt; ++j)
+                th.emplace_back([&, j] {
+                    for (size_t q = j * step; q < std::min(n, (j + 1) * step); ++q) hist[(size_t)j][key(in[q])]++;
+                });
+            for (auto& x : th) x.join();
+            th.clear();
+            uint64_t run = 0;
+            for (size_t bk = 0; bk < nbuckets; ++bk)
+                for (int j = 0; j < nt; ++j) {
+                    const uint32_t v = hist[(size_t)j][bk];
+                    hist[(size_t)j][bk] = (uint32_t)run;
+                    run += v;
+                }
+            out.assign(n, 0);
+            for (int j = 0; j < nt; ++j)
+                th.emplace_back([&, j] {
+                    std::vector<uint32_t>& h = hist[(size_t)j];
+                    for (size_t q = j * step; q < std::min(n, (j + 1) * step); ++q) out[h[key(in[q])]++] = in[q];
+                });
+            for (auto& x : th) x.join();
+        };
+        std::vector<uint32_t> tmp;
+        counting_sort(local, tmp, S, [&](uint32_t p) { return (size_t)word[p] * I + group[p]; });
+        counting_sort(tmp, c->sorted_tok, (size_t)W, [&](uint32_t p) { return (size_t)(c->pos[p] % W); });
         std::vector<uint32_t> woff((size_t)W + 1, 0);
-        for (uint32_t p : tmp) woff[(size_t)(c->pos[p] % W) + 1]++;
+        for (uint32_t p : local) woff[(size_t)(c->pos[p] % W) + 1]++;
         for (int w = 0; w < W; ++w) woff[(size_t)w + 1] += woff[(size_t)w];
         c->wave_tok_begin.assign(woff.begin(), woff.end());
-        c->sorted_tok.assign(local.size(), 0);
-        for (uint32_t p : tmp) c->sorted_tok[woff[(size_t)(c->pos[p] % W)]++] = p;
     }
     c->pos_of_tok.assign((size_t)num_tokens, -1);
-    for (size_t q = 0; q < c->sorted_tok.size(); ++q) c->pos_of_tok[c->sorted_tok[q]] = (int64_t)q;
+    parallel_for((int64_t)c->sorted_tok.size(), [&](int64_t b, int64_t e) {
+        for (int64_t q = b; q < e; ++q) c->pos_of_tok[c->sorted_tok[(size_t)q]] = q;
+    });
     // chunks: split each wave's (w, i) segments into runs of <= chunk_tokens tokens;
     // within a wave, longest first (the persistent warps take them in order)
     c->chunk_start.clear(); c->chunk_end.clear(); c->chunk_seg.clear();
@@ -912,12 +964,14 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
             for (int64_t p = 0; p < c->N; ++p) c->h_zr_canon[(size_t)p] = (uint16_t)all[(size_t)p];
         }
         const uint16_t* h = c->h_zr_canon;
-        for (int64_t p = 0; p < c->N; ++p) {
-            const uint32_t v = h[p];
-            if (!v) continue;                                   // another rank's token
-            if (z) z[p] = (int32_t)((v - 1u) & 0x7FFFu);
-            if (r) r[p] = (uint8_t)(((v - 1u) >> 15) & 1u);
-        }
+        parallel_for(c->N, [&](int64_t b, int64_t e) {
+            for (int64_t p = b; p < e; ++p) {
+                const uint32_t v = h[p];
+                if (!v) continue;                                   // another rank's token
+                if (z) z[p] = (int32_t)((v - 1u) & 0x7FFFu);
+                if (r) r[p] = (uint8_t)(((v - 1u) >> 15) & 1u);
+            }
+        });
     }
     if (doc_topic) {
         std::vector<float> nf((size_t)c->Dloc * Kp);

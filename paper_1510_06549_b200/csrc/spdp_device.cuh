@@ -105,6 +105,22 @@ __device__ __forceinline__ void slot_factors(int M, int Tt, int Qv, int Tk, floa
     F1 = A.y * ((b + a * (float)Tt) * C0) * __fdividef(beta + (float)Qv, vbeta + (float)Tk);
 }
 
+// Topic k0's factors after the token's own removal (Alg.1 lines 4-10): the
+// customer leaves (m-1, M-1) and, when r_rem = 1, its table too (t-1, Tt-1, Q-1, T-1).
+// Returns F = F0 + F1 and the r = 1 share F1 / F.
+__device__ __forceinline__ void removal_factors(int rrem, int mv, int tv, int Mv, int Ttv, int Qv, int Tv,
+                                                const float2* __restrict__ tab, float a, float b, float beta,
+                                                float vbeta, float& Fsum, float& R1) {
+    float x0 = 0.f, x1 = 0.f;
+    if (mv > 0) {
+        const int mm = mv - 1;
+        if (rrem) slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, tab[tri(mm) + max(tv - 1, 0)], a, b, beta, vbeta, x0, x1);
+        else slot_factors(Mv - 1, Ttv, Qv, Tv, tab[tri(mm) + min(tv, mm)], a, b, beta, vbeta, x0, x1);
+    }
+    Fsum = x0 + x1;
+    R1 = (x1 > 0.f) ? __fdiv_rn(x1, Fsum) : 0.f;
+}
+
 struct SweepArgs {
     // tokens of this rank, sorted by (wave, w, i, doc)
     const uint32_t* tok_doc;
@@ -212,6 +228,9 @@ sample_kernel(SweepArgs A) {
     const int32_t* __restrict__ Qw = A.Q + (size_t)w * Kp;
     const float* __restrict__ alpha_i = A.alpha + (size_t)i * Kp;
 
+    const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
+    // short chunks compute their tokens' own-removal factors per token instead
+    const bool pre = (end - start) >= 16u;
     // ---- prologue: slot factors at the snapshot and with the own removal
     for (int k = lane; k < KSPAN; k += 32) {
         float F0 = 0.f, F1 = 0.f, R0 = 0.f, R1 = 0.f, R10 = 0.f, R11 = 0.f;
@@ -221,19 +240,15 @@ sample_kernel(SweepArgs A) {
             tv = A.t[row + k];
             const int Mv = Mi[k], Ttv = Tti[k], Qv = Qw[k], Tv = A.T[k];
             slot_factors(Mv, Ttv, Qv, Tv, tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
-            if (mv > 0) {
-                const int mm = mv - 1;
-                float x0, x1;
-                slot_factors(Mv - 1, Ttv, Qv, Tv, tab[tri(mm) + min(tv, mm)], a, b, A.beta, A.vbeta, x0, x1);
-                R0 = x0 + x1; R10 = x1;                                   // r_rem = 0: (m-1, t)
-                slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, tab[tri(mm) + max(tv - 1, 0)], a, b, A.beta, A.vbeta, x0, x1);
-                R1 = x0 + x1; R11 = x1;                                   // r_rem = 1: (m-1, t-1)
+            if (pre) {                                  // own-removal variants, long chunks only
+                removal_factors(0, mv, tv, Mv, Ttv, Qv, Tv, tab, a, b, A.beta, A.vbeta, R0, R10);
+                removal_factors(1, mv, tv, Mv, Ttv, Qv, Tv, tab, a, b, A.beta, A.vbeta, R1, R11);
             }
         }
         S.F[k] = F0 + F1; S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, F0 + F1) : 0.f;
         S.Fr[0][k] = R0; S.Fr[1][k] = R1;
-        S.R1r[0][k] = (R10 > 0.f) ? __fdiv_rn(R10, R0) : 0.f;
-        S.R1r[1][k] = (R11 > 0.f) ? __fdiv_rn(R11, R1) : 0.f;
+        S.R1r[0][k] = R10;
+        S.R1r[1][k] = R11;
         S.al[k] = (k < K) ? alpha_i[k] : 0.f;
         S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
     }
@@ -250,7 +265,6 @@ sample_kernel(SweepArgs A) {
         aF[4 * q + 2] = __fmul_rn(a4.z, f4.z); aF[4 * q + 3] = __fmul_rn(a4.w, f4.w);
     }
     const uint32_t sweep = *A.sweep;
-    const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
 
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
         // ---- a2: this lane's token of the batch: record + Philox
@@ -285,7 +299,9 @@ sample_kernel(SweepArgs A) {
             const int m0 = S.m[k0], t0 = S.t[k0];
             const int rrem = removal_draw(x0, m0, t0);
             const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
-            const float Fk0 = S.Fr[rrem][k0];
+            float Fk0, R1k0;
+            if (pre) { Fk0 = S.Fr[rrem][k0]; R1k0 = S.R1r[rrem][k0]; }
+            else removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
             const int B0 = k0 >> 2, q0 = B0 / LPT;
             const bool owner = (B0 % LPT) == gl;
             const float n0 = __ldg(nrow + k0);
@@ -366,7 +382,7 @@ sample_kernel(SweepArgs A) {
             int slot = 0;
             if (lane == es) {
                 const bool own = (kk == k0);
-                const float w1 = we * (own ? S.R1r[rrem][k0] : S.R1[kk]);
+                const float w1 = we * (own ? R1k0 : S.R1[kk]);
                 int rs;
                 if (!efb) rs = (wbeg + (double)(ie - we) + (double)w1 > target) ? 1 : 0;
                 else rs = ((own ? m0 - 1 : S.m[kk]) > 0) ? 0 : 1;   // last positive slot
@@ -645,6 +661,60 @@ __global__ void unapply_net_kernel(int32_t* __restrict__ m, int32_t* __restrict_
 // with (dm, dt) = the all-reduced D.
 
 __global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
+
+// ---------------------------------------------------------------- state installation
+// counts from z: m_{ikw} and, with given r, t_{ikw} = sum r
+__global__ void init_cells_kernel(const int32_t* __restrict__ group, const int32_t* __restrict__ word,
+                                  const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t n, int I,
+                                  int Kp, int32_t* __restrict__ m, int32_t* __restrict__ t, uint32_t* __restrict__ first) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const size_t cell = ((size_t)word[p] * I + group[p]) * Kp + z[p];
+        atomicAdd(m + cell, 1);
+        if (r) { if (r[p]) atomicAdd(t + cell, 1); }
+        else atomicMin(first + cell, p);
+    }
+}
+// default r: the first token (canonical order) of each cell opens its table (reading c12)
+__global__ void init_first_table_kernel(const int32_t* __restrict__ group, const int32_t* __restrict__ word,
+                                        const int32_t* __restrict__ z, uint32_t n, int I, int Kp,
+                                        const uint32_t* __restrict__ first, uint8_t* __restrict__ r,
+                                        int32_t* __restrict__ t) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const size_t cell = ((size_t)word[p] * I + group[p]) * Kp + z[p];
+        const bool f = first[cell] == p;
+        r[p] = f ? 1 : 0;
+        if (f) t[cell] = 1;
+    }
+}
+// tables given as [I][V][K] (spdp_set_state): transpose into [V][I][Kp]
+__global__ void load_tables_kernel(const int32_t* __restrict__ tin, int I, int V, int K, int Kp, int32_t* __restrict__ t) {
+    const size_t total = (size_t)I * V * K;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < total; j += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(j % K);
+        const size_t iw = j / K;
+        const int w = (int)(iw % V), i = (int)(iw / V);
+        t[((size_t)w * I + i) * Kp + k] = tin[j];
+    }
+}
+// count cells violating 0 <= t <= m, t > 0 iff m > 0
+__global__ void check_cells_kernel(const int32_t* __restrict__ m, const int32_t* __restrict__ t, size_t cells,
+                                   unsigned long long* __restrict__ bad) {
+    unsigned long long nb = 0;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < cells; j += (size_t)gridDim.x * blockDim.x)
+        nb += (t[j] < 0 || t[j] > m[j] || ((t[j] > 0) != (m[j] > 0)));
+    if (nb) atomicAdd(bad, nb);
+}
+// this rank's token records (sorted order) and doc-topic counts
+__global__ void init_local_kernel(const uint32_t* __restrict__ tok_id, const uint32_t* __restrict__ tok_doc,
+                                  const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t nloc, int Kp,
+                                  uint16_t* __restrict__ zr, uint16_t* __restrict__ zr_next, float* __restrict__ n) {
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += gridDim.x * blockDim.x) {
+        const uint32_t p = tok_id[q];
+        const uint16_t v = (uint16_t)(z[p] | (r[p] << 15));
+        zr[q] = v; zr_next[q] = v;
+        atomicAdd(n + (size_t)tok_doc[q] * Kp + z[p], 1.0f);
+    }
+}
 
 // zr in canonical token order (for spdp_counts): out[id[p]] = zr[p] + 1 (0 = other rank)
 __global__ void scatter_zr_kernel(const uint32_t* __restrict__ id, const uint16_t* __restrict__ zr, uint32_t n,
