@@ -54,11 +54,11 @@ void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4
 
 // (lanes per token, topics per lane) by K: few lanes per token so the
 // per-token fixed work (removal, scan, search) is shared by 32/LPT tokens.
-int pick_lpt(int K) { return K <= 64 ? 4 : (K <= 128 ? 8 : (K <= 256 ? 16 : 32)); }
+int pick_lpt(int K) { return K <= 128 ? 4 : (K <= 256 ? 8 : (K <= 512 ? 16 : 32)); }
 int pick_kpl(int K) {
     if (K <= 16) return 4;
     if (K <= 32) return 8;
-    if (K <= 256) return 16;
+    if (K <= 64) return 16;
     return 32;
 }
 

@@ -169,6 +169,7 @@ template <int KSPAN, int KPL>
 struct WarpSmem {
     float w[32 * KPL];   // topic masses of the current token, [q][lane][4] (conflict-free float4 stores)
     float F[KSPAN];      // F0 + F1 at the snapshot counts
+    float aF[KSPAN];     // alpha_ik * F (the n-independent part of the topic mass)
     float R1[KSPAN];     // F1 / (F0 + F1): the r = 1 share of the topic mass
     float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
     float R1r[2][KSPAN];
@@ -197,7 +198,7 @@ struct WarpSmem {
 //   boundary is off by at most a few fp32 ulps of a partial sum (< 3e-7 of the
 //   total), inside the 1e-6 band of north_star (5).
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32, (KPL >= 32) ? 3 : 4)
+__global__ void __launch_bounds__(kWarps * 32, 4)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
@@ -250,19 +251,17 @@ sample_kernel(SweepArgs A) {
         S.R1r[0][k] = R10;
         S.R1r[1][k] = R11;
         S.al[k] = (k < K) ? alpha_i[k] : 0.f;
+        S.aF[k] = __fmul_rn(S.al[k], F0 + F1);
         S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
     }
     __syncwarp();
 
-    float F[KPL], aF[KPL];
+    float F[KPL];                                    // aF stays in smem (broadcast loads)
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
         const int kq = 4 * (q * LPT + gl);
         const float4 f4 = *reinterpret_cast<const float4*>(&S.F[kq]);
-        const float4 a4 = *reinterpret_cast<const float4*>(&S.al[kq]);
         F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
-        aF[4 * q] = __fmul_rn(a4.x, f4.x); aF[4 * q + 1] = __fmul_rn(a4.y, f4.y);
-        aF[4 * q + 2] = __fmul_rn(a4.z, f4.z); aF[4 * q + 3] = __fmul_rn(a4.w, f4.w);
     }
     const uint32_t sweep = *A.sweep;
 
@@ -315,10 +314,11 @@ sample_kernel(SweepArgs A) {
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
-                const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], aF[4 * q + 0]);
-                const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], aF[4 * q + 1]);
-                const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], aF[4 * q + 2]);
-                const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], aF[4 * q + 3]);
+                const float4 af = *reinterpret_cast<const float4*>(&S.aF[4 * (q * LPT + gl)]);
+                const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], af.x);
+                const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], af.y);
+                const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
+                const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
                 *reinterpret_cast<float4*>(S.w + (q * 32 + lane) * 4) = make_float4(w0, w1, w2, w3);
                 sb[q] = (w0 + w1) + (w2 + w3);
                 if (owner && q == q0) sb[q] += dlt;
