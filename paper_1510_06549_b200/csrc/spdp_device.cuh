@@ -287,6 +287,14 @@ sample_kernel(SweepArgs A) {
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
             const uint32_t tok = b0 + src;
             const float* __restrict__ nrow = A.n + noff;
+            {   // warm L1 with the next step's doc-topic rows (one 128-byte line per lane)
+                const uint32_t nsrc = src + TPW;
+                const uint32_t noff_n = __shfl_sync(0xffffffffu, t_noff, nsrc & 31);
+                constexpr int LINES = KSPAN / 32;
+#pragma unroll
+                for (int l = gl; l < LINES; l += LPT)
+                    if (nsrc < nb) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.n + noff_n + 32 * l));
+            }
             // a4: the doc-topic row, one 16-byte load per block (coalesced over the group);
             // rows are padded so that blocks past K read harmless values (F = 0 there)
             float4 v[NB];
