@@ -18,7 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "libspdp.so")
+LIB_PATH = os.environ.get("SPDP_LIB") or os.path.join(_HERE, "libspdp.so")   # SPDP_LIB: tuning variants
 _SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("spdp.cu", "spdp_device.cuh", "spdp_loglik.cuh")] + [
     os.path.join(_ROOT, "include", "spdp.h")]
 

@@ -19,6 +19,9 @@
 namespace spdp {
 
 constexpr int kWarps = 4;          // warps per block of the sample kernel
+#ifndef SPDP_MINB
+#define SPDP_MINB 4                // resident blocks per SM the sample kernel is compiled for
+#endif
 constexpr uint32_t kRBit = 0x8000u;
 
 // ---------------------------------------------------------------- Philox4x32-10
@@ -198,7 +201,7 @@ struct WarpSmem {
 //   boundary is off by at most a few fp32 ulps of a partial sum (< 3e-7 of the
 //   total), inside the 1e-6 band of north_star (5).
 template <int LPT, int KPL, bool DEBUG>
-__global__ void __launch_bounds__(kWarps * 32, 4)
+__global__ void __launch_bounds__(kWarps * 32, SPDP_MINB)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
