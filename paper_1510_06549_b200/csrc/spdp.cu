@@ -104,7 +104,10 @@ struct spdp_ctx {
              *d_chunk_seg = nullptr, *d_wave_segs = nullptr,
              *d_sweep = nullptr;
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
-    float* d_n = nullptr;                         // n_dk as exact integers in fp32
+    float* d_n = nullptr;                         // n_dk as exact integers in fp32, rows in sigma order
+    int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
+    std::vector<int> sigma;
+    int colstart[8] = {0};
     uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
     uint16_t* h_zr_canon = nullptr;               // pinned host copy
     uint32_t* d_work = nullptr;                   // [W + 1] persistent-warp counters
@@ -237,7 +240,9 @@ SweepArgs base_args(spdp_ctx* c) {
     SweepArgs a{};
     a.tok_doc = c->d_tok_doc; a.tok_id = c->d_tok_id; a.zr = c->d_zr; a.zr_next = c->d_zr_next;
     a.chunk_start = c->d_chunk_start; a.chunk_end = c->d_chunk_end; a.chunk_seg = c->d_chunk_seg; a.nchunks = 0;
-    a.n = c->d_n; a.m = c->d_m; a.t = c->d_t; a.Q = c->d_Q; a.M = c->d_M; a.Tt = c->d_Tt; a.T = c->d_T;
+    a.n = c->d_n; a.sigma = c->d_sigma;
+    for (int q = 0; q < 8; ++q) a.colstart[q] = c->colstart[q];
+    a.m = c->d_m; a.t = c->d_t; a.Q = c->d_Q; a.M = c->d_M; a.Tt = c->d_Tt; a.T = c->d_T;
     a.dm = c->d_dm; a.dt = c->d_dt;
     a.alpha = c->d_alpha; a.disc = c->d_disc; a.conc = c->d_conc; a.tab = c->d_tab; a.tab_off = c->d_tab_off;
     a.beta = (float)c->cfg.beta; a.vbeta = (float)((double)c->V * c->cfg.beta);
@@ -400,7 +405,7 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     CU(cudaMemsetAsync(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024), c->stream));
     if (c->Nloc > 0)
         init_local_kernel<<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc, Kp,
-                                                       c->d_zr, c->d_zr_next, c->d_n);
+                                                       c->d_sigma, c->d_zr, c->d_zr_next, c->d_n);
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
     if (c->d_D) CU(cudaMemsetAsync(c->d_D, 0, sizeof(int32_t) * 2 * c->cells, c->stream));
@@ -443,7 +448,7 @@ spdp_status run_waves(spdp_ctx* c) {
         rec(c, 4 * (size_t)w + 1);
         const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
         const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
-        apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n,
+        apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n, c->d_sigma,
                                                                          c->Kp, tb, te);
         rec(c, 4 * (size_t)w + 2);
         {
@@ -747,6 +752,22 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     lt.mark("wave plan + chunks");
     const size_t nch = c->chunk_seg.size();
     c->cells = (size_t)V * I * Kp;
+    // doc-topic row layout (sigma order, see spdp_device.cuh): lane gl owns canonical
+    // blocks [gl*NB, gl*NB + NB); block q of each lane is stored column-major over lanes
+    {
+        const int NBLK = Kp / 4, NB = c->KPL / 4;
+        int run = 0;
+        for (int q = 0; q < 8; ++q) {
+            c->colstart[q] = run;
+            if (q < NB)
+                for (int gl = 0; gl < c->LPT; ++gl) run += (gl * NB + q < NBLK) ? 1 : 0;
+        }
+        c->sigma.assign((size_t)Kp, 0);
+        for (int k = 0; k < Kp; ++k) {
+            const int B = k / 4, gl = B / NB, q = B % NB;
+            c->sigma[(size_t)k] = 4 * (c->colstart[q] + gl) + (k & 3);
+        }
+    }
 
     // device allocations
     ALLOC(c->d_tok_doc, c->Nloc); ALLOC(c->d_tok_id, c->Nloc);
@@ -754,6 +775,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_chunk_start, nch); ALLOC(c->d_chunk_end, nch); ALLOC(c->d_chunk_seg, nch);
     ALLOC(c->d_wave_segs, c->wave_segs.size());
     ALLOC(c->d_sweep, 1);
+    ALLOC(c->d_sigma, Kp);
+    CU(cudaMemcpy(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice));
     ALLOC(c->d_n, (size_t)c->Dloc * Kp + 1024);      // +1024: the sample kernel reads whole topic spans
     CU(cudaMemset(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024)));
     ALLOC(c->d_work, (size_t)W + 2);
@@ -982,7 +1005,7 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
         int32_t* dst = gather ? full.data() : doc_topic;
         for (int32_t j = 0; j < c->Dloc; ++j)
             for (int k = 0; k < K; ++k)
-                dst[(size_t)c->global_of_local[(size_t)j] * K + k] = (int32_t)nf[(size_t)j * Kp + k];
+                dst[(size_t)c->global_of_local[(size_t)j] * K + k] = (int32_t)nf[(size_t)j * Kp + c->sigma[(size_t)k]];
         if (gather) {
             TempBuf<int32_t> tb(full.size());
             if (!tb.p) return fail(c, SPDP_ENOMEM, "gather buffer");
@@ -1058,7 +1081,7 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
         double* part = c->d_partial;       // [0, grid) words, [grid, 2 grid) docs
         loglik_words_kernel<<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_Q, ls, d_off, c->V, c->I, c->K, c->Kp,
                                                         c->cfg.beta, part);
-        loglik_docs_kernel<<<grid, 256, 0, c->stream>>>(c->d_n, c->d_doclen, c->d_docgroup, c->d_alpha64, c->d_alpha_sum64,
+        loglik_docs_kernel<<<grid, 256, 0, c->stream>>>(c->d_n, c->d_sigma, c->d_doclen, c->d_docgroup, c->d_alpha64, c->d_alpha_sum64,
                                                        c->Dloc, c->K, c->Kp, part + grid);
         loglik_small_kernel<<<1, 1024, 0, c->stream>>>(c->d_M, c->d_Tt, c->d_T, c->d_disc64, c->d_conc64, c->I, c->K, c->Kp,
                                                       (double)c->V * c->cfg.beta, part + 2 * grid);
@@ -1210,7 +1233,8 @@ spdp_status debug_verify(spdp_ctx* c) {
     std::vector<int32_t> n((size_t)c->Dloc * Kp), m(c->cells), t(c->cells), Q((size_t)V * Kp);
     CU(cudaMemcpy(zr.data(), c->d_zr, 2 * zr.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(nf.data(), c->d_n, 4 * nf.size(), cudaMemcpyDeviceToHost));
-    for (size_t j = 0; j < nf.size(); ++j) n[j] = (int32_t)nf[j];
+    for (int32_t j = 0; j < c->Dloc; ++j)
+        for (int k = 0; k < Kp; ++k) n[(size_t)j * Kp + k] = (int32_t)nf[(size_t)j * Kp + c->sigma[(size_t)k]];
     CU(cudaMemcpy(m.data(), c->d_m, 4 * m.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(t.data(), c->d_t, 4 * t.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(Q.data(), c->d_Q, 4 * Q.size(), cudaMemcpyDeviceToHost));

@@ -137,7 +137,9 @@ struct SweepArgs {
     int nchunks;
     uint32_t* work;                // persistent-warp chunk counter (zeroed before each launch)
     // counts
-    float* n;                      // doc-topic counts n_dk as exact integers in fp32
+    float* n;                      // doc-topic counts n_dk as exact integers in fp32, rows in sigma order
+    const int* sigma;              // [Kp] in-row position of topic k
+    int colstart[8];               // first block of column q in the sigma order
     int32_t* m;
     int32_t* t;
     int32_t* Q;
@@ -167,12 +169,21 @@ struct SweepArgs {
 };
 
 // ---------------------------------------------------------------- the sample kernel
-// Per-warp shared memory layout (floats / ints, KSPAN entries each).
+// Doc-topic row layout ("sigma order").  A token is handled by LPT lanes; lane
+// gl owns the canonical topics [gl*KPL, gl*KPL + KPL) as NB = KPL/4 blocks of 4.
+// In memory the blocks are stored column-major over the lanes: block q of
+// lane gl sits at position colstart[q] + gl (colstart = prefix of the number of
+// lanes that have a block q), so one 16-byte load instruction of the group reads
+// consecutive bytes, rows keep length Kp, and each lane's topics are contiguous
+// in the canonical order — the CDF is one scan over lanes.  sigma[k] is the
+// in-row position of topic k (host table); every kernel touching n uses it.
+
+// Per-warp shared memory (KSPAN entries each unless noted).
 template <int KSPAN, int KPL>
 struct WarpSmem {
     float w[32 * KPL];   // topic masses of the current token, [q][lane][4] (conflict-free float4 stores)
     float F[KSPAN];      // F0 + F1 at the snapshot counts
-    float aF[KSPAN];     // alpha_ik * F (the n-independent part of the topic mass)
+    float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
     float R1[KSPAN];     // F1 / (F0 + F1): the r = 1 share of the topic mass
     float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
     float R1r[2][KSPAN];
@@ -182,38 +193,39 @@ struct WarpSmem {
     int dm[KSPAN];       // the chunk's delta m, delta t
     int dt[KSPAN];
 };
+template <int KPL>
+__device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
 
-// One warp per chunk of one (w, i) segment.  LPT lanes per token (TPW = 32/LPT
-// tokens in flight per warp-step), each lane owning KPL topics as NB = KPL/4
-// blocks of 4: block B = q*LPT + gl holds topics 4B..4B+3, so one 16-byte load
-// instruction of a group covers 4*LPT consecutive topics (coalesced rows).
-//   prologue (once per chunk): the segment's factors F_k, F1_k at the snapshot,
-//     and the own-removal variants for both removal draws (Alg.1 lines 4-10);
+// One warp per chunk of one (w, i) segment; TPW = 32/LPT tokens per warp-step.
+//   prologue (once per chunk): the segment's factors F_k, F1_k/F_k at the
+//     snapshot and (long chunks) the own-removal variants (Alg.1 lines 4-10);
 //   per 32 tokens: lane l loads token l's record and runs its Philox (a2);
-//     the groups receive them by shuffles;
 //   per token (a3-a7): removal draw against the snapshot; topic masses
-//     w_k = (alpha_ik + n_dk) F_k (one FFMA each) summed per block in fp32;
-//     the own-removal correction of topic k0 by its owner lane; block-column
-//     totals T_q over the group, their fp64 prefix P_q, then the lane and the
-//     topic where the fp64 prefix first exceeds u * total, slots in the paper's
-//     order j = 2k (r = 1), 2k+1 (r = 0); the r split uses w1 = (alpha + n) F1.
-//   Every boundary is an fp64 sum of fp32 partial sums of <= 4 terms, so a
-//   boundary is off by at most a few fp32 ulps of a partial sum (< 3e-7 of the
-//   total), inside the 1e-6 band of north_star (5).
+//     w_k = (alpha_ik + n_dk) F_k (one FFMA each); 4-topic block sums in fp32;
+//     the own-removal correction of topic k0 by its owner lane; lane totals
+//     in fp64 and one fp64 scan over the group's lanes; the first lane, block
+//     and topic whose prefix exceeds u * total, slots in the paper's order
+//     j = 2k (r = 1), 2k+1 (r = 0); the r split by the exact r = 1 share.
+//   Every CDF boundary is an fp64 sum of fp32 partial sums of <= 4 terms
+//   (< 3e-7 of the total off), inside the 1e-6 band of north_star (5).
 template <int LPT, int KPL, bool DEBUG>
 __global__ void __launch_bounds__(kWarps * 32, SPDP_MINB)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
     constexpr int KSPAN = LPT * KPL;
     constexpr int NB = KPL / 4;                      // 4-topic blocks per lane
-    static_assert(KPL % 4 == 0, "KPL must be a multiple of 4");
+    static_assert(KPL % 4 == 0 && NB <= 8, "KPL must be a multiple of 4, at most 32");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
     const int I = A.I, K = A.K, Kp = A.Kp;
     unsigned keeps = 0, moved = 0;
     const int g = lane / LPT, gl = lane % LPT;
+    const int kb = gl * KPL;                         // this lane's first canonical topic
     const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
+    int pos[NB];                                     // in-row float offsets of this lane's blocks
+#pragma unroll
+    for (int q = 0; q < NB; ++q) pos[q] = 4 * (A.colstart[q] + gl);
 
   // persistent warps: grab chunks (sorted longest first on the host) from a counter
   for (;;) {
@@ -237,11 +249,12 @@ sample_kernel(SweepArgs A) {
     const bool pre = (end - start) >= 16u;
     // ---- prologue: slot factors at the snapshot and with the own removal
     for (int k = lane; k < KSPAN; k += 32) {
-        float F0 = 0.f, F1 = 0.f, R0 = 0.f, R1 = 0.f, R10 = 0.f, R11 = 0.f;
+        float F0 = 0.f, F1 = 0.f, R0 = 0.f, R1 = 0.f, R10 = 0.f, R11 = 0.f, al = 0.f;
         int mv = 0, tv = 0;
         if (k < K) {
             mv = A.m[row + k];
             tv = A.t[row + k];
+            al = alpha_i[k];
             const int Mv = Mi[k], Ttv = Tti[k], Qv = Qw[k], Tv = A.T[k];
             slot_factors(Mv, Ttv, Qv, Tv, tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
             if (pre) {                                  // own-removal variants, long chunks only
@@ -249,23 +262,24 @@ sample_kernel(SweepArgs A) {
                 removal_factors(1, mv, tv, Mv, Ttv, Qv, Tv, tab, a, b, A.beta, A.vbeta, R1, R11);
             }
         }
-        S.F[k] = F0 + F1; S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, F0 + F1) : 0.f;
+        const float Fk = F0 + F1;
+        S.F[k] = Fk; S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
         S.Fr[0][k] = R0; S.Fr[1][k] = R1;
         S.R1r[0][k] = R10;
         S.R1r[1][k] = R11;
-        S.al[k] = (k < K) ? alpha_i[k] : 0.f;
-        S.aF[k] = __fmul_rn(S.al[k], F0 + F1);
+        S.al[k] = al;
+        S.aF[skew<KPL>(k)] = __fmul_rn(al, Fk);
         S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
     }
     __syncwarp();
 
-    float F[KPL];                                    // aF stays in smem (broadcast loads)
+    float F[KPL];                                    // aF stays in smem (conflict-free broadcast loads)
 #pragma unroll
     for (int q = 0; q < NB; ++q) {
-        const int kq = 4 * (q * LPT + gl);
-        const float4 f4 = *reinterpret_cast<const float4*>(&S.F[kq]);
+        const float4 f4 = *reinterpret_cast<const float4*>(&S.F[kb + 4 * q]);
         F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
     }
+    const float* aFl = &S.aF[skew<KPL>(kb)];
     const uint32_t sweep = *A.sweep;
 
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
@@ -290,19 +304,11 @@ sample_kernel(SweepArgs A) {
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
             const uint32_t tok = b0 + src;
             const float* __restrict__ nrow = A.n + noff;
-            {   // warm L1 with the next step's doc-topic rows (one 128-byte line per lane)
-                const uint32_t nsrc = src + TPW;
-                const uint32_t noff_n = __shfl_sync(0xffffffffu, t_noff, nsrc & 31);
-                constexpr int LINES = KSPAN / 32;
-#pragma unroll
-                for (int l = gl; l < LINES; l += LPT)
-                    if (nsrc < nb) asm volatile("prefetch.global.L1 [%0];" ::"l"(A.n + noff_n + 32 * l));
-            }
-            // a4: the doc-topic row, one 16-byte load per block (coalesced over the group);
-            // rows are padded so that blocks past K read harmless values (F = 0 there)
+            // a4: the doc-topic row, one coalesced 16-byte load per block; blocks
+            // past K read finite values of the row or the padding (F = aF = 0 there)
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nrow + 4 * (q * LPT + gl)));
+            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nrow + pos[q]));
 
             // ---- a3: removal against the wave-start snapshot
             const int k0 = (int)(zr0 & 0x7FFFu);
@@ -312,72 +318,71 @@ sample_kernel(SweepArgs A) {
             float Fk0, R1k0;
             if (pre) { Fk0 = S.Fr[rrem][k0]; R1k0 = S.R1r[rrem][k0]; }
             else removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
-            const int B0 = k0 >> 2, q0 = B0 / LPT;
-            const bool owner = (B0 % LPT) == gl;
-            const float n0 = __ldg(nrow + k0);
+            const int q0 = (k0 - kb) >> 2;                 // block of k0 if this lane owns it
+            const bool owner = (k0 >= kb) && (k0 < kb + KPL);
+            const float n0 = __ldg(nrow + A.sigma[k0]);
             const float al0 = S.al[k0], Fo = S.F[k0];
             // own-removal correction of topic k0 (same value on every lane of the group)
             const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the main loop's mass
             const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
             const float dlt = wnew - wold;
 
-            // ---- a5: topic masses w = (alpha + n) F, kept in smem for the final search
+            // ---- a5: topic masses w = (alpha + n) F, block sums, lane total (fp64)
             float sb[NB];
+            double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
-                const float4 af = *reinterpret_cast<const float4*>(&S.aF[4 * (q * LPT + gl)]);
+                const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
                 const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], af.x);
                 const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], af.y);
                 const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
                 const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
                 *reinterpret_cast<float4*>(S.w + (q * 32 + lane) * 4) = make_float4(w0, w1, w2, w3);
-                sb[q] = (w0 + w1) + (w2 + w3);
-                if (owner && q == q0) sb[q] += dlt;
+                float sq = (w0 + w1) + (w2 + w3);
+                if (owner && q == q0) sq += dlt;
+                sb[q] = sq;
+                acc += (double)sq;
             }
             if (owner) S.w[(q0 * 32 + lane) * 4 + (k0 & 3)] = wnew;
-            // ---- a6: block-column totals over the group, fp64 prefix over columns
-            float Tq[NB];
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                float x = sb[q];
-#pragma unroll
-                for (int off = 1; off < LPT; off <<= 1) x += __shfl_xor_sync(0xffffffffu, x, off, LPT);
-                Tq[q] = x;
-            }
-            double total = 0.0;
-#pragma unroll
-            for (int q = 0; q < NB; ++q) total += (double)Tq[q];
-            const double target = u * total;
-            int qs = -1, qlast = 0;
-            double P = 0.0, Pq = 0.0, Plast = 0.0;
-            float sq = 0.f, slast = 0.f;
-#pragma unroll
-            for (int q = 0; q < NB; ++q) {
-                const double nxt = P + (double)Tq[q];
-                if (qs < 0 && nxt > target) { qs = q; Pq = P; sq = sb[q]; }
-                if (Tq[q] > 0.f) { qlast = q; Plast = P; slast = sb[q]; }
-                P = nxt;
-            }
-            bool fb = (qs < 0);
-            if (fb) { qs = qlast; Pq = Plast; sq = slast; }   // rounding: the last non-empty column
-            // lanes of the group within column qs: fp32 inclusive scan, ballot for the lane
-            float incl = sq;
+            // ---- a6: one fp64 scan over the group's lanes (canonical topic order)
+            double incl = acc;
 #pragma unroll
             for (int off = 1; off < LPT; off <<= 1) {
-                const float y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
+                const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
                 if (gl >= off) incl += y;
             }
-            const double lbeg = Pq + (double)(incl - sq);
-            const unsigned hit = __ballot_sync(0xffffffffu, !fb && (Pq + (double)incl > target)) & gmask;
-            const unsigned pos = __ballot_sync(0xffffffffu, sq > 0.f) & gmask;
-            fb = fb || (hit == 0u);
-            const int winner = !fb ? (__ffs(hit) - 1) : (pos ? 31 - __clz(pos) : g * LPT);
-            __syncwarp();
+            const double excl = incl - acc;
+            const double total = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
+            const double target = u * total;
+            const unsigned hit = __ballot_sync(0xffffffffu, incl > target) & gmask;
+            const unsigned pos_l = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
+            bool fb = (hit == 0u);                         // rounding: fall back to the last positive slot
+            const int winner = !fb ? (__ffs(hit) - 1) : (pos_l ? 31 - __clz(pos_l) : g * LPT);
+            // the winner lane finds its block: fp64 running prefix from its lane start
+            int qs = 0;
+            double bbeg = excl;
+            if (lane == winner) {
+                double run = excl;
+                int qlast = 0;
+                double blast = excl;
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) {
+                    const double nxt = run + (double)sb[q];
+                    if (!found && nxt > target) { found = true; qs = q; bbeg = run; }
+                    if (sb[q] > 0.f) { qlast = q; blast = run; }
+                    run = nxt;
+                }
+                if (!found || fb) { qs = qlast; bbeg = blast; }
+                if (!found) fb = true;
+            }
+            qs = __shfl_sync(0xffffffffu, qs, winner);
+            const double wbeg = __shfl_sync(0xffffffffu, bbeg, winner);
+            fb = __shfl_sync(0xffffffffu, (int)fb, winner) != 0;
             // ---- the winning block's 4 topics, one per lane gl < 4 of the group
-            const double wbeg = __shfl_sync(0xffffffffu, lbeg, winner);
-            const int kq = 4 * (qs * LPT + (winner % LPT));
+            const int wgl = winner % LPT;
             const int e = gl & 3;
-            const int kk = kq + e;
+            const int kk = wgl * KPL + 4 * qs + e;
             const bool act = (gl < 4) && (kk < K);
             const float we = act ? S.w[(qs * 32 + winner) * 4 + e] : 0.f;
             float ie = we;
@@ -409,7 +414,7 @@ sample_kernel(SweepArgs A) {
                 if (valid) {
                     for (int k = gl; k < K; k += LPT) {
                         const bool own = (k == k0);
-                        const float nk = nrow[k] - (own ? 1.f : 0.f);
+                        const float nk = nrow[A.sigma[k]] - (own ? 1.f : 0.f);
                         float f0, f1;
                         if (own) {
                             const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
@@ -473,14 +478,15 @@ constexpr size_t sample_smem_bytes() {
 // n_{d k0} -= 1, n_{d k*} += 1 for every token of the wave that moved; zr <- zr_next.
 __global__ void apply_tokens_kernel(const uint32_t* __restrict__ tok_doc, uint16_t* __restrict__ zr,
                                     const uint16_t* __restrict__ zr_next, float* __restrict__ n,
+                                    const int* __restrict__ sigma,
                                     int Kp, uint32_t begin, uint32_t end) {
     for (uint32_t p = begin + blockIdx.x * blockDim.x + threadIdx.x; p < end; p += gridDim.x * blockDim.x) {
         const uint32_t zo = zr[p], zn = zr_next[p];
         const uint32_t ko = zo & 0x7FFFu, kn = zn & 0x7FFFu;
         if (ko != kn) {
             float* nr = n + (size_t)tok_doc[p] * Kp;
-            atomicAdd(nr + ko, -1.0f);      // exact: integer-valued fp32 (< 2^24)
-            atomicAdd(nr + kn, 1.0f);
+            atomicAdd(nr + sigma[ko], -1.0f);      // exact: integer-valued fp32 (< 2^24)
+            atomicAdd(nr + sigma[kn], 1.0f);
         }
         zr[p] = (uint16_t)zn;
     }
@@ -718,12 +724,13 @@ __global__ void check_cells_kernel(const int32_t* __restrict__ m, const int32_t*
 // this rank's token records (sorted order) and doc-topic counts
 __global__ void init_local_kernel(const uint32_t* __restrict__ tok_id, const uint32_t* __restrict__ tok_doc,
                                   const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t nloc, int Kp,
+                                  const int* __restrict__ sigma,
                                   uint16_t* __restrict__ zr, uint16_t* __restrict__ zr_next, float* __restrict__ n) {
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += gridDim.x * blockDim.x) {
         const uint32_t p = tok_id[q];
         const uint16_t v = (uint16_t)(z[p] | (r[p] << 15));
         zr[q] = v; zr_next[q] = v;
-        atomicAdd(n + (size_t)tok_doc[q] * Kp + z[p], 1.0f);
+        atomicAdd(n + (size_t)tok_doc[q] * Kp + sigma[z[p]], 1.0f);
     }
 }
 
@@ -776,11 +783,11 @@ perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const double*
         const uint32_t tok = base + g;
         const bool valid = tok < end;
         const uint32_t doc = valid ? A.tok_doc[tok] : 0u;
-        const float* nrow = A.n + (size_t)doc * Kp + kb;
+        const float* nrow = A.n + (size_t)doc * Kp;
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < KPL; ++j)
-            if (kb + j < K) s += ((double)__ldg(nrow + j) + al[j]) * sphi[kb + j];
+            if (kb + j < K) s += ((double)__ldg(nrow + A.sigma[kb + j]) + al[j]) * sphi[kb + j];
 #pragma unroll
         for (int off = LPT / 2; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, LPT);
         if (valid && gl == 0) ll += log(s / ((double)doclen[doc] + asum));
