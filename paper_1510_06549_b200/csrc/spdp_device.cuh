@@ -304,11 +304,13 @@ sample_kernel(SweepArgs A) {
             const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
             const uint32_t tok = b0 + src;
             const float* __restrict__ nrow = A.n + noff;
-            // a4: the doc-topic row, one coalesced 16-byte load per block; blocks
-            // past K read finite values of the row or the padding (F = aF = 0 there)
+            const float* __restrict__ nlane = nrow + 4 * gl;
+            // a4: the doc-topic row, one coalesced 16-byte load per block (column
+            // offsets are kernel parameters, i.e. uniform); blocks past K read finite
+            // values of the row or the padding (F = aF = 0 there)
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nrow + pos[q]));
+            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nlane + 4 * A.colstart[q]));
 
             // ---- a3: removal against the wave-start snapshot
             const int k0 = (int)(zr0 & 0x7FFFu);
@@ -327,9 +329,8 @@ sample_kernel(SweepArgs A) {
             const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
             const float dlt = wnew - wold;
 
-            // ---- a5: topic masses w = (alpha + n) F, block sums, lane total (fp64)
+            // ---- a5: topic masses w = (alpha + n) F, fp32 block sums and lane total
             float sb[NB];
-            double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
                 const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
@@ -338,12 +339,21 @@ sample_kernel(SweepArgs A) {
                 const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
                 const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
                 *reinterpret_cast<float4*>(S.w + (q * 32 + lane) * 4) = make_float4(w0, w1, w2, w3);
-                float sq = (w0 + w1) + (w2 + w3);
-                if (owner && q == q0) sq += dlt;
-                sb[q] = sq;
-                acc += (double)sq;
+                sb[q] = (w0 + w1) + (w2 + w3);
             }
             if (owner) S.w[(q0 * 32 + lane) * 4 + (k0 & 3)] = wnew;
+            float lt32;                                     // tree sum of the block sums
+            {
+                float t8[NB];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) t8[q] = sb[q];
+#pragma unroll
+                for (int h = 1; h < NB; h <<= 1)
+#pragma unroll
+                    for (int q = 0; q + h < NB; q += 2 * h) t8[q] += t8[q + h];
+                lt32 = t8[0];
+            }
+            const double acc = (double)lt32 + (owner ? (double)dlt : 0.0);
             // ---- a6: one fp64 scan over the group's lanes (canonical topic order)
             double incl = acc;
 #pragma unroll
@@ -358,26 +368,31 @@ sample_kernel(SweepArgs A) {
             const unsigned pos_l = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
             bool fb = (hit == 0u);                         // rounding: fall back to the last positive slot
             const int winner = !fb ? (__ffs(hit) - 1) : (pos_l ? 31 - __clz(pos_l) : g * LPT);
-            // the winner lane finds its block: fp64 running prefix from its lane start
+            // the winner lane finds its block: count the blocks whose (corrected)
+            // fp32 prefix, relative to the lane start, does not exceed the target
             int qs = 0;
-            double bbeg = excl;
+            float pre32 = 0.f;
             if (lane == winner) {
-                double run = excl;
-                int qlast = 0;
-                double blast = excl;
-                bool found = false;
+                const float rel = (float)(target - excl);
+                float run = 0.f;
+                int cnt = 0;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) {
-                    const double nxt = run + (double)sb[q];
-                    if (!found && nxt > target) { found = true; qs = q; bbeg = run; }
-                    if (sb[q] > 0.f) { qlast = q; blast = run; }
-                    run = nxt;
+                    run += sb[q] + ((owner && q == q0) ? dlt : 0.f);
+                    cnt += (run <= rel) ? 1 : 0;
                 }
-                if (!found || fb) { qs = qlast; bbeg = blast; }
-                if (!found) fb = true;
+                qs = cnt;
+                if (qs >= NB || fb) {                      // rounding: the last positive block
+                    fb = true;
+                    qs = 0;
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) if (sb[q] + ((owner && q == q0) ? dlt : 0.f) > 0.f) qs = q;
+                }
+#pragma unroll
+                for (int q = 0; q < NB; ++q) if (q < qs) pre32 += sb[q] + ((owner && q == q0) ? dlt : 0.f);
             }
             qs = __shfl_sync(0xffffffffu, qs, winner);
-            const double wbeg = __shfl_sync(0xffffffffu, bbeg, winner);
+            const double wbeg = __shfl_sync(0xffffffffu, excl, winner) + (double)__shfl_sync(0xffffffffu, pre32, winner);
             fb = __shfl_sync(0xffffffffu, (int)fb, winner) != 0;
             // ---- the winning block's 4 topics, one per lane gl < 4 of the group
             const int wgl = winner % LPT;
