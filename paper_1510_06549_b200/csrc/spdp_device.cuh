@@ -169,9 +169,9 @@ struct SweepArgs {
 };
 
 // ---------------------------------------------------------------- the sample kernel
-// Doc-topic row layout ("sigma order").  A token is handled by LPT lanes; lane
-// gl owns the canonical topics [gl*KPL, gl*KPL + KPL) as NB = KPL/4 blocks of 4.
-// In memory the blocks are stored column-major over the lanes: block q of
+// Doc-topic row layout ("sigma order").  A token's dense pass uses LPT lanes;
+// lane gl owns the canonical topics [gl*KPL, gl*KPL + KPL) as NB = KPL/4 blocks
+// of 4.  In memory the blocks are stored column-major over the lanes: block q of
 // lane gl sits at position colstart[q] + gl (colstart = prefix of the number of
 // lanes that have a block q), so one 16-byte load instruction of the group reads
 // consecutive bytes, rows keep length Kp, and each lane's topics are contiguous
@@ -181,7 +181,6 @@ struct SweepArgs {
 // Per-warp shared memory (KSPAN entries each unless noted).
 template <int KSPAN, int KPL>
 struct WarpSmem {
-    float w[32 * KPL];   // topic masses of the current token, [q][lane][4] (conflict-free float4 stores)
     float F[KSPAN];      // F0 + F1 at the snapshot counts
     float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
     float R1[KSPAN];     // F1 / (F0 + F1): the r = 1 share of the topic mass
@@ -192,22 +191,29 @@ struct WarpSmem {
     int t[KSPAN];
     int dm[KSPAN];       // the chunk's delta m, delta t
     int dt[KSPAN];
+    // hand-over from the dense pass to the per-token search (one entry per token of the batch)
+    float bs[KPL / 4][32];   // the winning lane's block sums (without the own-removal fix)
+    double lbeg[32];         // prefix before the winning lane
+    double target[32];       // u * total
+    int wgl[32];             // winning lane within the group (-1: fall back to the last positive slot)
 };
 template <int KPL>
 __device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
 
-// One warp per chunk of one (w, i) segment; TPW = 32/LPT tokens per warp-step.
-//   prologue (once per chunk): the segment's factors F_k, F1_k/F_k at the
-//     snapshot and (long chunks) the own-removal variants (Alg.1 lines 4-10);
-//   per 32 tokens: lane l loads token l's record and runs its Philox (a2);
-//   per token (a3-a7): removal draw against the snapshot; topic masses
-//     w_k = (alpha_ik + n_dk) F_k (one FFMA each); 4-topic block sums in fp32;
-//     the own-removal correction of topic k0 by its owner lane; lane totals
-//     in fp64 and one fp64 scan over the group's lanes; the first lane, block
-//     and topic whose prefix exceeds u * total, slots in the paper's order
-//     j = 2k (r = 1), 2k+1 (r = 0); the r split by the exact r = 1 share.
-//   Every CDF boundary is an fp64 sum of fp32 partial sums of <= 4 terms
-//   (< 3e-7 of the total off), inside the 1e-6 band of north_star (5).
+// One warp per chunk of one (w, i) segment.  Per chunk, the segment's factors
+// F_k and F1_k/F_k at the snapshot (and, for long chunks, the own-removal
+// variants, Alg.1 lines 4-10) go to shared memory.  Per batch of 32 tokens:
+//   phase 1 (lane = token): record, Philox (a2), removal draw against the
+//     snapshot and the own-removal correction of topic k0 (a3);
+//   phase 2 (LPT lanes per token, 32/LPT tokens per step): the doc-topic row
+//     (a4), topic masses w_k = (alpha_ik + n_dk) F_k (one FFMA each), fp32
+//     4-topic block sums and lane totals, one fp64 scan over the group's lanes,
+//     target = u * total, the lane holding it (a5, a6);
+//   phase 3 (lane = token): the block and the topic where the prefix first
+//     exceeds the target, slots in the paper's order j = 2k (r = 1), 2k+1 (r = 0),
+//     the r split by the exact r = 1 share; outputs and count deltas (a7).
+//   Every CDF boundary is an fp64 sum of fp32 partial sums of few terms
+//   (a few fp32 ulps of the total), inside the 1e-6 band of north_star (5).
 template <int LPT, int KPL, bool DEBUG>
 __global__ void __launch_bounds__(kWarps * 32, SPDP_MINB)
 sample_kernel(SweepArgs A) {
@@ -221,11 +227,8 @@ sample_kernel(SweepArgs A) {
     const int I = A.I, K = A.K, Kp = A.Kp;
     unsigned keeps = 0, moved = 0;
     const int g = lane / LPT, gl = lane % LPT;
-    const int kb = gl * KPL;                         // this lane's first canonical topic
+    const int kb = gl * KPL;                         // this lane's first canonical topic (phase 2)
     const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
-    int pos[NB];                                     // in-row float offsets of this lane's blocks
-#pragma unroll
-    for (int q = 0; q < NB; ++q) pos[q] = 4 * (A.colstart[q] + gl);
 
   // persistent warps: grab chunks (sorted longest first on the host) from a counter
   for (;;) {
@@ -283,53 +286,44 @@ sample_kernel(SweepArgs A) {
     const uint32_t sweep = *A.sweep;
 
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
-        // ---- a2: this lane's token of the batch: record + Philox
         const uint32_t nb = min(32u, end - b0);
-        uint32_t t_noff = 0, t_zr = 0, t_x0 = 0;
-        double t_u = 0.0;
-        if ((uint32_t)lane < nb) {
-            const uint32_t p = b0 + lane;
-            t_noff = A.tok_doc[p] * (uint32_t)Kp;          // doc-topic row offset (fits 32 bits)
-            t_zr = A.zr[p];
-            const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);
-            t_x0 = x.x;
-            t_u = u53(x);
+        // ======== phase 1: lane = token
+        const bool mine = (uint32_t)lane < nb;
+        const uint32_t p = b0 + lane;
+        uint32_t noff = 0, zr0 = 0, x0 = 0;
+        double u = 0.0;
+        if (mine) {
+            noff = A.tok_doc[p] * (uint32_t)Kp;            // doc-topic row offset (fits 32 bits)
+            zr0 = A.zr[p];
+            const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);   // a2
+            x0 = x.x;
+            u = u53(x);
         }
+        const float* __restrict__ nrow = A.n + noff;
+        const int k0 = (int)(zr0 & 0x7FFFu);
+        const int m0 = S.m[k0], t0 = S.t[k0];
+        const int rrem = removal_draw(x0, m0, t0);                                            // a3
+        const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
+        float Fk0, R1k0;
+        if (pre) { Fk0 = S.Fr[rrem][k0]; R1k0 = S.R1r[rrem][k0]; }
+        else removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        const float n0 = mine ? __ldg(nrow + A.sigma[k0]) : 0.f;
+        const float al0 = S.al[k0], Fo = S.F[k0];
+        const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the dense pass's mass
+        const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
+        const float dlt = wnew - wold;
+
+        // ======== phase 2: LPT lanes per token
         for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
-            const uint32_t src = s0 + g;
-            const bool valid = src < nb;
-            const uint32_t noff = __shfl_sync(0xffffffffu, t_noff, src & 31);
-            const uint32_t zr0 = __shfl_sync(0xffffffffu, t_zr, src & 31);
-            const uint32_t x0 = __shfl_sync(0xffffffffu, t_x0, src & 31);
-            const double u = __shfl_sync(0xffffffffu, t_u, src & 31);
-            const uint32_t tok = b0 + src;
-            const float* __restrict__ nrow = A.n + noff;
-            const float* __restrict__ nlane = nrow + 4 * gl;
-            // a4: the doc-topic row, one coalesced 16-byte load per block (column
-            // offsets are kernel parameters, i.e. uniform); blocks past K read finite
-            // values of the row or the padding (F = aF = 0 there)
+            const uint32_t src = (s0 + g) & 31;
+            const uint32_t snoff = __shfl_sync(0xffffffffu, noff, src);
+            const int sk0 = __shfl_sync(0xffffffffu, k0, src);
+            const float sdlt = __shfl_sync(0xffffffffu, dlt, src);
+            const double su = __shfl_sync(0xffffffffu, u, src);
+            const float* __restrict__ nl = A.n + snoff + 4 * gl;
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nlane + 4 * A.colstart[q]));
-
-            // ---- a3: removal against the wave-start snapshot
-            const int k0 = (int)(zr0 & 0x7FFFu);
-            const int m0 = S.m[k0], t0 = S.t[k0];
-            const int rrem = removal_draw(x0, m0, t0);
-            const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
-            float Fk0, R1k0;
-            if (pre) { Fk0 = S.Fr[rrem][k0]; R1k0 = S.R1r[rrem][k0]; }
-            else removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
-            const int q0 = (k0 - kb) >> 2;                 // block of k0 if this lane owns it
-            const bool owner = (k0 >= kb) && (k0 < kb + KPL);
-            const float n0 = __ldg(nrow + A.sigma[k0]);
-            const float al0 = S.al[k0], Fo = S.F[k0];
-            // own-removal correction of topic k0 (same value on every lane of the group)
-            const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the main loop's mass
-            const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
-            const float dlt = wnew - wold;
-
-            // ---- a5: topic masses w = (alpha + n) F, fp32 block sums and lane total
+            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nl + 4 * A.colstart[q]));
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -338,11 +332,9 @@ sample_kernel(SweepArgs A) {
                 const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], af.y);
                 const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
                 const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
-                *reinterpret_cast<float4*>(S.w + (q * 32 + lane) * 4) = make_float4(w0, w1, w2, w3);
                 sb[q] = (w0 + w1) + (w2 + w3);
             }
-            if (owner) S.w[(q0 * 32 + lane) * 4 + (k0 & 3)] = wnew;
-            float lt32;                                     // tree sum of the block sums
+            float lt32;                                    // tree sum of the block sums
             {
                 float t8[NB];
 #pragma unroll
@@ -353,113 +345,118 @@ sample_kernel(SweepArgs A) {
                     for (int q = 0; q + h < NB; q += 2 * h) t8[q] += t8[q + h];
                 lt32 = t8[0];
             }
-            const double acc = (double)lt32 + (owner ? (double)dlt : 0.0);
-            // ---- a6: one fp64 scan over the group's lanes (canonical topic order)
+            const bool owner = (sk0 >= kb) && (sk0 < kb + KPL);
+            const double acc = (double)lt32 + (owner ? (double)sdlt : 0.0);
             double incl = acc;
 #pragma unroll
             for (int off = 1; off < LPT; off <<= 1) {
                 const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
                 if (gl >= off) incl += y;
             }
-            const double excl = incl - acc;
             const double total = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
-            const double target = u * total;
+            const double target = su * total;
             const unsigned hit = __ballot_sync(0xffffffffu, incl > target) & gmask;
-            const unsigned pos_l = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
-            bool fb = (hit == 0u);                         // rounding: fall back to the last positive slot
-            const int winner = !fb ? (__ffs(hit) - 1) : (pos_l ? 31 - __clz(pos_l) : g * LPT);
-            // the winner lane finds its block: count the blocks whose (corrected)
-            // fp32 prefix, relative to the lane start, does not exceed the target
-            int qs = 0;
-            float pre32 = 0.f;
-            if (lane == winner) {
-                const float rel = (float)(target - excl);
-                float run = 0.f;
-                int cnt = 0;
+            const unsigned posl = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
+            const int winner = hit ? (__ffs(hit) - 1) : (posl ? 31 - __clz(posl) : g * LPT);
+            if (lane == winner && s0 + g < nb) {
 #pragma unroll
-                for (int q = 0; q < NB; ++q) {
-                    run += sb[q] + ((owner && q == q0) ? dlt : 0.f);
-                    cnt += (run <= rel) ? 1 : 0;
-                }
-                qs = cnt;
-                if (qs >= NB || fb) {                      // rounding: the last positive block
-                    fb = true;
-                    qs = 0;
-#pragma unroll
-                    for (int q = 0; q < NB; ++q) if (sb[q] + ((owner && q == q0) ? dlt : 0.f) > 0.f) qs = q;
-                }
-#pragma unroll
-                for (int q = 0; q < NB; ++q) if (q < qs) pre32 += sb[q] + ((owner && q == q0) ? dlt : 0.f);
+                for (int q = 0; q < NB; ++q) S.bs[q][src] = sb[q];
+                S.lbeg[src] = incl - acc;
+                S.target[src] = target;
+                S.wgl[src] = hit ? gl : -1 - gl;
             }
-            qs = __shfl_sync(0xffffffffu, qs, winner);
-            const double wbeg = __shfl_sync(0xffffffffu, excl, winner) + (double)__shfl_sync(0xffffffffu, pre32, winner);
-            fb = __shfl_sync(0xffffffffu, (int)fb, winner) != 0;
-            // ---- the winning block's 4 topics, one per lane gl < 4 of the group
-            const int wgl = winner % LPT;
-            const int e = gl & 3;
-            const int kk = wgl * KPL + 4 * qs + e;
-            const bool act = (gl < 4) && (kk < K);
-            const float we = act ? S.w[(qs * 32 + winner) * 4 + e] : 0.f;
-            float ie = we;
-#pragma unroll
-            for (int off = 1; off < 4; off <<= 1) {
-                const float y = __shfl_up_sync(0xffffffffu, ie, off, LPT);
-                if (gl >= off) ie += y;
-            }
-            const unsigned ehit = __ballot_sync(0xffffffffu, act && !fb && (wbeg + (double)ie > target)) & gmask;
-            const unsigned epos = __ballot_sync(0xffffffffu, act && we > 0.f) & gmask;
-            const int es = ehit ? (__ffs(ehit) - 1) : (epos ? 31 - __clz(epos) : g * LPT);
-            const bool efb = fb || (ehit == 0u);
-            int slot = 0;
-            if (lane == es) {
-                const bool own = (kk == k0);
-                const float w1 = we * (own ? R1k0 : S.R1[kk]);
-                int rs;
-                if (!efb) rs = (wbeg + (double)(ie - we) + (double)w1 > target) ? 1 : 0;
-                else rs = ((own ? m0 - 1 : S.m[kk]) > 0) ? 0 : 1;   // last positive slot
-                slot = kk | (rs << 15);
-            }
-            slot = __shfl_sync(0xffffffffu, slot, es);
-            int ks = slot & 0x7FFF, rs = slot >> 15;
-            if (keep) { ks = k0; rs = 1; }
-            __syncwarp();
+        }
+        __syncwarp();
 
+        // ======== phase 3: lane = token
+        if (mine) {
+            int ks = k0, rs = 1;
+            if (!keep) {
+                const double target = S.target[lane];
+                const double lbeg = S.lbeg[lane];
+                const int wv = S.wgl[lane];
+                bool fb = wv < 0;
+                const int wg = fb ? -1 - wv : wv;
+                const int own_q = (k0 >= wg * KPL && k0 < wg * KPL + KPL) ? ((k0 - wg * KPL) >> 2) : -1;
+                float bsv[NB];
+#pragma unroll
+                for (int q = 0; q < NB; ++q) bsv[q] = S.bs[q][lane] + ((q == own_q) ? dlt : 0.f);
+                // block: count the blocks whose fp32 prefix does not exceed the target
+                const float rel = (float)(target - lbeg);
+                float run = 0.f;
+                int qs = 0;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) { run += bsv[q]; qs += (run <= rel) ? 1 : 0; }
+                if (fb || qs >= NB) {                      // rounding: the last positive block
+                    fb = true; qs = 0;
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) if (bsv[q] > 0.f) qs = q;
+                }
+                float pre32 = 0.f;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) if (q < qs) pre32 += bsv[q];
+                // the block's 4 topic masses, recomputed exactly as the dense pass did
+                const int kq = wg * KPL + 4 * qs;
+                int cs = 0;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) if (q == qs) cs = A.colstart[q];
+                const float4 n4 = __ldg(reinterpret_cast<const float4*>(nrow + 4 * (cs + wg)));
+                const float4 F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
+                const float4 a4 = *reinterpret_cast<const float4*>(&S.aF[skew<KPL>(kq)]);
+                float wq[4] = {__fmaf_rn(n4.x, F4.x, a4.x), __fmaf_rn(n4.y, F4.y, a4.y),
+                               __fmaf_rn(n4.z, F4.z, a4.z), __fmaf_rn(n4.w, F4.w, a4.w)};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) if (kq + e == k0) wq[e] = wnew;
+                double run2 = lbeg + (double)pre32, bes = run2, blast = run2;
+                int es = -1, elast = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double nxt = run2 + (double)wq[e];
+                    if (es < 0 && !fb && nxt > target) { es = e; bes = run2; }
+                    if (wq[e] > 0.f) { elast = e; blast = run2; }
+                    run2 = nxt;
+                }
+                if (es < 0) { fb = true; es = elast; bes = blast; }   // rounding: last positive topic
+                float wsel = 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) if (e == es) wsel = wq[e];
+                ks = kq + es;
+                const bool own = (ks == k0);
+                const float w1 = wsel * (own ? R1k0 : S.R1[ks]);
+                if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
+                else rs = ((own ? m0 - 1 : S.m[ks]) > 0) ? 0 : 1;   // last positive slot
+            }
             if constexpr (DEBUG) {
                 // exact slot masses w1 = (alpha + n) F1, w0 = (alpha + n) F0 of every topic
-                if (valid) {
-                    for (int k = gl; k < K; k += LPT) {
-                        const bool own = (k == k0);
-                        const float nk = nrow[A.sigma[k]] - (own ? 1.f : 0.f);
-                        float f0, f1;
-                        if (own) {
-                            const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
-                            slot_factors(Mi[k] - 1, Tti[k] - rrem, Qw[k] - rrem, A.T[k] - rrem, tab[tri(mm) + tt],
-                                         a, b, A.beta, A.vbeta, f0, f1);
-                        } else {
-                            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(S.m[k]) + S.t[k]], a, b, A.beta,
-                                         A.vbeta, f0, f1);
-                        }
-                        const double base = (double)S.al[k] + (double)nk;
-                        A.dbg_w[(size_t)tok * 2 * K + 2 * k] = base * (double)f1;
-                        A.dbg_w[(size_t)tok * 2 * K + 2 * k + 1] = base * (double)f0;
+                for (int k = 0; k < K; ++k) {
+                    const bool own = (k == k0);
+                    const float nk = nrow[A.sigma[k]] - (own ? 1.f : 0.f);
+                    float f0, f1;
+                    if (own) {
+                        const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
+                        slot_factors(Mi[k] - 1, Tti[k] - rrem, Qw[k] - rrem, A.T[k] - rrem, tab[tri(mm) + tt],
+                                     a, b, A.beta, A.vbeta, f0, f1);
+                    } else {
+                        slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(S.m[k]) + S.t[k]], a, b, A.beta,
+                                     A.vbeta, f0, f1);
                     }
-                    if (gl == 0) {
-                        int32_t* inf = A.dbg_info + (size_t)tok * 4;
-                        inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
-                    }
+                    const double base = (double)S.al[k] + (double)nk;
+                    A.dbg_w[(size_t)p * 2 * K + 2 * k] = base * (double)f1;
+                    A.dbg_w[(size_t)p * 2 * K + 2 * k + 1] = base * (double)f0;
                 }
+                int32_t* inf = A.dbg_info + (size_t)p * 4;
+                inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
             } else {
-                if (valid && gl == 0) {                                            // a7
-                    A.zr_next[tok] = (uint16_t)(ks | (rs << 15));
-                    if (keep) ++keeps;
-                    else {
-                        atomicAdd(&S.dm[k0], -1); atomicAdd(&S.dt[k0], -rrem);
-                        atomicAdd(&S.dm[ks], 1); atomicAdd(&S.dt[ks], rs);
-                        moved += (ks != k0);
-                    }
+                A.zr_next[p] = (uint16_t)(ks | (rs << 15));                                   // a7
+                if (keep) ++keeps;
+                else {
+                    atomicAdd(&S.dm[k0], -1); atomicAdd(&S.dt[k0], -rrem);
+                    atomicAdd(&S.dm[ks], 1); atomicAdd(&S.dt[ks], rs);
+                    moved += (ks != k0);
                 }
             }
         }
+        __syncwarp();
     }
     if constexpr (!DEBUG) {
         __syncwarp();
