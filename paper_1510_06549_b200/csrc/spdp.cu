@@ -104,6 +104,7 @@ struct spdp_ctx {
              *d_chunk_seg = nullptr, *d_wave_segs = nullptr,
              *d_sweep = nullptr;
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
+    uint32_t *d_doc_ptr = nullptr, *d_doc_pos = nullptr;   // CSR: sorted-token positions of each local doc
     float* d_n = nullptr;                         // n_dk as exact integers in fp32, rows in sigma order
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
@@ -447,9 +448,17 @@ spdp_status run_waves(spdp_ctx* c) {
         launch_sample(c, a, false);
         rec(c, 4 * (size_t)w + 1);
         const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
-        const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
-        apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n, c->d_sigma,
-                                                                         c->Kp, tb, te);
+        if (c->W == 1) {
+            // every token moved to zr_next: rebuild the doc-topic rows, then swap
+            const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
+            recount_docs_kernel<<<148 * 8, 256, smem, c->stream>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
+                                                                  c->Dloc, c->Kp, c->d_n);
+            std::swap(c->d_zr, c->d_zr_next);
+        } else {
+            const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
+            apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n,
+                                                                             c->d_sigma, c->Kp, tb, te);
+        }
         rec(c, 4 * (size_t)w + 2);
         {
             const uint32_t sb = c->wave_seg_begin[(size_t)w], se = c->wave_seg_begin[(size_t)w + 1];
@@ -800,6 +809,18 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             tdoc[(size_t)q] = (uint32_t)c->local_of_doc[(size_t)doc[p]];
             tid[(size_t)q] = p;
         }
+        // doc -> sorted-token positions (CSR), for the W = 1 recount of the doc-topic rows
+        std::vector<uint32_t> dptr((size_t)c->Dloc + 1, 0), dpos((size_t)c->Nloc);
+        for (int64_t q = 0; q < c->Nloc; ++q) dptr[(size_t)tdoc[(size_t)q] + 1]++;
+        for (int32_t j = 0; j < c->Dloc; ++j) dptr[(size_t)j + 1] += dptr[(size_t)j];
+        {
+            std::vector<uint32_t> fill(dptr.begin(), dptr.end() - 1);
+            for (int64_t q = 0; q < c->Nloc; ++q) dpos[fill[(size_t)tdoc[(size_t)q]]++] = (uint32_t)q;
+        }
+        ALLOC(c->d_doc_ptr, (size_t)c->Dloc + 1);
+        ALLOC(c->d_doc_pos, std::max<int64_t>(c->Nloc, 1));
+        CU(cudaMemcpy(c->d_doc_ptr, dptr.data(), sizeof(uint32_t) * dptr.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(c->d_doc_pos, dpos.data(), sizeof(uint32_t) * dpos.size(), cudaMemcpyHostToDevice));
         std::vector<int32_t> dl((size_t)std::max<int32_t>(c->Dloc, 1), 0), dg((size_t)std::max<int32_t>(c->Dloc, 1), 0);
         for (int32_t j = 0; j < c->Dloc; ++j) {
             dl[(size_t)j] = c->doclen[(size_t)c->global_of_local[(size_t)j]];

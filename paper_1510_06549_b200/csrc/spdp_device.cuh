@@ -591,6 +591,30 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
     }
 }
 
+// ---------------------------------------------------------------- end of sweep (W = 1): recount n
+// With one wave every token has a new z in zr_next, so the doc-topic rows are
+// rebuilt from it (n, m "can be re-generated from topic
+// assignments") instead of two scattered atomics per moved token: one warp per
+// document, a shared-memory histogram over the document's tokens (CSR index in
+// sorted-token positions), one coalesced row write in sigma order.
+__global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const uint32_t* __restrict__ doc_pos,
+                                    const uint16_t* __restrict__ zr, const int* __restrict__ sigma, int D, int Kp,
+                                    float* __restrict__ n) {
+    extern __shared__ int hist[];                    // [warps][Kp]
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    int* h = hist + (size_t)(threadIdx.x >> 5) * Kp;
+    for (int d = blockIdx.x * wpb + (threadIdx.x >> 5); d < D; d += gridDim.x * wpb) {
+        for (int j = lane; j < Kp; j += 32) h[j] = 0;
+        __syncwarp();
+        const uint32_t e = doc_ptr[d + 1];
+        for (uint32_t t = doc_ptr[d] + lane; t < e; t += 32) atomicAdd(&h[sigma[zr[doc_pos[t]] & 0x7FFFu]], 1);
+        __syncwarp();
+        float* row = n + (size_t)d * Kp;
+        for (int j = lane; j < Kp; j += 32) row[j] = (float)h[j];
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------- end of wave: touched rows only
 // One warp per (w, i) segment the wave touched: m += dm, t = clamp(t + dt) into
 // [min(1,m), m], dm = dt = 0; the changes are added to Q_w (int atomics) and to
