@@ -300,6 +300,9 @@ sample_kernel(SweepArgs A) {
             u = u53(x);
         }
         const float* __restrict__ nrow = A.n + noff;
+        if (mine) {   // pull this token's doc-topic row towards L2 for the dense pass
+            for (int l = 0; l * 32 < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + 32 * l));
+        }
         const int k0 = (int)(zr0 & 0x7FFFu);
         const int m0 = S.m[k0], t0 = S.t[k0];
         const int rrem = removal_draw(x0, m0, t0);                                            // a3
