@@ -109,6 +109,7 @@ struct spdp_ctx {
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
     int colstart[8] = {0};
+    int prefetch_rows = 0;
     uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
     uint16_t* h_zr_canon = nullptr;               // pinned host copy
     uint32_t* d_work = nullptr;                   // [W + 1] persistent-warp counters
@@ -243,6 +244,7 @@ SweepArgs base_args(spdp_ctx* c) {
     a.chunk_start = c->d_chunk_start; a.chunk_end = c->d_chunk_end; a.chunk_seg = c->d_chunk_seg; a.nchunks = 0;
     a.n = c->d_n; a.sigma = c->d_sigma;
     for (int q = 0; q < 8; ++q) a.colstart[q] = c->colstart[q];
+    a.prefetch_rows = c->prefetch_rows;
     a.m = c->d_m; a.t = c->d_t; a.Q = c->d_Q; a.M = c->d_M; a.Tt = c->d_Tt; a.T = c->d_T;
     a.dm = c->d_dm; a.dt = c->d_dt;
     a.alpha = c->d_alpha; a.disc = c->d_disc; a.conc = c->d_conc; a.tab = c->d_tab; a.tab_off = c->d_tab_off;
@@ -784,6 +786,13 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_chunk_start, nch); ALLOC(c->d_chunk_end, nch); ALLOC(c->d_chunk_seg, nch);
     ALLOC(c->d_wave_segs, c->wave_segs.size());
     ALLOC(c->d_sweep, 1);
+    {   // prefetch doc-topic rows into L2 only when the array does not live there anyway
+        int dev = 0, l2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        c->prefetch_rows = ((double)c->Dloc * Kp * sizeof(float) > 0.5 * (double)l2) ? 1 : 0;
+        if (const char* e = getenv("SPDP_PREFETCH_ROWS")) c->prefetch_rows = atoi(e);
+    }
     ALLOC(c->d_sigma, Kp);
     CU(cudaMemcpy(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice));
     ALLOC(c->d_n, (size_t)c->Dloc * Kp + 1024);      // +1024: the sample kernel reads whole topic spans

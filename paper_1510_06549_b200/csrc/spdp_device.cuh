@@ -140,6 +140,7 @@ struct SweepArgs {
     float* n;                      // doc-topic counts n_dk as exact integers in fp32, rows in sigma order
     const int* sigma;              // [Kp] in-row position of topic k
     int colstart[8];               // first block of column q in the sigma order
+    int prefetch_rows;             // the doc-topic array exceeds L2: prefetch rows in phase 1
     int32_t* m;
     int32_t* t;
     int32_t* Q;
@@ -300,7 +301,7 @@ sample_kernel(SweepArgs A) {
             u = u53(x);
         }
         const float* __restrict__ nrow = A.n + noff;
-        if (mine) {   // pull this token's doc-topic row towards L2 for the dense pass
+        if (mine && A.prefetch_rows) {   // rows not L2-resident: pull this token's row towards L2
             for (int l = 0; l * 32 < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + 32 * l));
         }
         const int k0 = (int)(zr0 & 0x7FFFu);
