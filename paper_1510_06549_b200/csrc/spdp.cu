@@ -563,7 +563,7 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     }
     if (c->LPT * c->KPL < c->K) return bad("internal: no kernel configuration for K");
     int chunk = 256;
-    if (const char* e = getenv("SPDP_CHUNK_TOKENS")) chunk = std::max(1, atoi(e));
+    if (const char* e = getenv("SPDP_CHUNK_TOKENS")) chunk = std::min(std::max(1, atoi(e)), 16384);
     c->chunk_tokens = chunk;
 
     int ndev = 0;
@@ -653,6 +653,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         std::vector<int32_t> cnt((size_t)I * V, 0);
         for (int64_t p = 0; p < num_tokens; ++p) cnt[(size_t)group[p] * V + word[p]]++;
         c->mmax = *std::max_element(cnt.begin(), cnt.end());
+        if (c->mmax >= 65536)
+            return fail(c, SPDP_ETABLE, "M_max = %d: cells are packed in 16 bits (M_max < 65536)", c->mmax);
         if ((double)c->mmax * (c->mmax + 1) / 2 * sizeof(float2) > 16e9)
             return fail(c, SPDP_ETABLE, "Stirling-ratio table for M_max = %d exceeds 16 GB", c->mmax);
     }

@@ -184,19 +184,13 @@ template <int KSPAN, int KPL>
 struct WarpSmem {
     float F[KSPAN];      // F0 + F1 at the snapshot counts
     float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
-    float R1[KSPAN];     // F1 / (F0 + F1): the r = 1 share of the topic mass
-    float Fr[2][KSPAN];  // F0 + F1 with the own removal at this topic, r_rem = 0 / 1
-    float R1r[2][KSPAN];
-    float al[KSPAN];     // alpha_ik (0 on padding)
-    int m[KSPAN];
-    int t[KSPAN];
-    int dm[KSPAN];       // the chunk's delta m, delta t
-    int dt[KSPAN];
+    uint32_t mt[KSPAN];  // snapshot m << 16 | t of the segment's cells (M_max < 2^16)
+    int dmt[KSPAN];      // the chunk's delta m * 2^16 + delta t (|delta| <= chunk length)
     // hand-over from the dense pass to the per-token search (one entry per token of the batch)
     float bs[KPL / 4][32];   // the winning lane's block sums (without the own-removal fix)
     double lbeg[32];         // prefix before the winning lane
     double target[32];       // u * total
-    int wgl[32];             // winning lane within the group (-1: fall back to the last positive slot)
+    int wgl[32];             // winning lane within the group (negative: fall back to the last positive slot)
 };
 template <int KPL>
 __device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
@@ -249,31 +243,21 @@ sample_kernel(SweepArgs A) {
     const float* __restrict__ alpha_i = A.alpha + (size_t)i * Kp;
 
     const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
-    // short chunks compute their tokens' own-removal factors per token instead
-    const bool pre = (end - start) >= 16u;
-    // ---- prologue: slot factors at the snapshot and with the own removal
+    // ---- prologue: the segment's slot factors at the wave-start snapshot
     for (int k = lane; k < KSPAN; k += 32) {
-        float F0 = 0.f, F1 = 0.f, R0 = 0.f, R1 = 0.f, R10 = 0.f, R11 = 0.f, al = 0.f;
+        float F0 = 0.f, F1 = 0.f, al = 0.f;
         int mv = 0, tv = 0;
         if (k < K) {
             mv = A.m[row + k];
             tv = A.t[row + k];
             al = alpha_i[k];
-            const int Mv = Mi[k], Ttv = Tti[k], Qv = Qw[k], Tv = A.T[k];
-            slot_factors(Mv, Ttv, Qv, Tv, tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
-            if (pre) {                                  // own-removal variants, long chunks only
-                removal_factors(0, mv, tv, Mv, Ttv, Qv, Tv, tab, a, b, A.beta, A.vbeta, R0, R10);
-                removal_factors(1, mv, tv, Mv, Ttv, Qv, Tv, tab, a, b, A.beta, A.vbeta, R1, R11);
-            }
+            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
         }
         const float Fk = F0 + F1;
-        S.F[k] = Fk; S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
-        S.Fr[0][k] = R0; S.Fr[1][k] = R1;
-        S.R1r[0][k] = R10;
-        S.R1r[1][k] = R11;
-        S.al[k] = al;
+        S.F[k] = Fk;
         S.aF[skew<KPL>(k)] = __fmul_rn(al, Fk);
-        S.m[k] = mv; S.t[k] = tv; S.dm[k] = 0; S.dt[k] = 0;
+        S.mt[k] = ((uint32_t)mv << 16) | (uint32_t)tv;
+        S.dmt[k] = 0;
     }
     __syncwarp();
 
@@ -305,15 +289,15 @@ sample_kernel(SweepArgs A) {
             for (int l = 0; l * 32 < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + 32 * l));
         }
         const int k0 = (int)(zr0 & 0x7FFFu);
-        const int m0 = S.m[k0], t0 = S.t[k0];
+        const uint32_t mt0 = S.mt[k0];
+        const int m0 = (int)(mt0 >> 16), t0 = (int)(mt0 & 0xFFFFu);
         const int rrem = removal_draw(x0, m0, t0);                                            // a3
         const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
-        float Fk0, R1k0;
-        if (pre) { Fk0 = S.Fr[rrem][k0]; R1k0 = S.R1r[rrem][k0]; }
-        else removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        float Fk0 = 0.f, R1k0 = 0.f;                    // topic k0's factors after the own removal
+        if (mine) removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
         const float n0 = mine ? __ldg(nrow + A.sigma[k0]) : 0.f;
-        const float al0 = S.al[k0], Fo = S.F[k0];
-        const float wold = __fmaf_rn(n0, Fo, __fmul_rn(al0, Fo));     // == the dense pass's mass
+        const float al0 = alpha_i[k0];
+        const float wold = __fmaf_rn(n0, S.F[k0], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
         const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
         const float dlt = wnew - wold;
 
@@ -426,9 +410,17 @@ sample_kernel(SweepArgs A) {
                 for (int e = 0; e < 4; ++e) if (e == es) wsel = wq[e];
                 ks = kq + es;
                 const bool own = (ks == k0);
-                const float w1 = wsel * (own ? R1k0 : S.R1[ks]);
+                const uint32_t mts = S.mt[ks];
+                float R1s = R1k0;
+                if (!own) {                                // r = 1 share of topic ks at the snapshot
+                    float f0, f1;
+                    slot_factors(Mi[ks], Tti[ks], Qw[ks], A.T[ks], tab[tri((int)(mts >> 16)) + (mts & 0xFFFFu)], a, b,
+                                 A.beta, A.vbeta, f0, f1);
+                    R1s = (f1 > 0.f) ? __fdiv_rn(f1, f0 + f1) : 0.f;
+                }
+                const float w1 = wsel * R1s;
                 if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
-                else rs = ((own ? m0 - 1 : S.m[ks]) > 0) ? 0 : 1;   // last positive slot
+                else rs = ((own ? m0 - 1 : (int)(mts >> 16)) > 0) ? 0 : 1;   // last positive slot
             }
             if constexpr (DEBUG) {
                 // exact slot masses w1 = (alpha + n) F1, w0 = (alpha + n) F0 of every topic
@@ -441,10 +433,10 @@ sample_kernel(SweepArgs A) {
                         slot_factors(Mi[k] - 1, Tti[k] - rrem, Qw[k] - rrem, A.T[k] - rrem, tab[tri(mm) + tt],
                                      a, b, A.beta, A.vbeta, f0, f1);
                     } else {
-                        slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(S.m[k]) + S.t[k]], a, b, A.beta,
-                                     A.vbeta, f0, f1);
+                        slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri((int)(S.mt[k] >> 16)) + (S.mt[k] & 0xFFFFu)],
+                                     a, b, A.beta, A.vbeta, f0, f1);
                     }
-                    const double base = (double)S.al[k] + (double)nk;
+                    const double base = (double)alpha_i[k] + (double)nk;
                     A.dbg_w[(size_t)p * 2 * K + 2 * k] = base * (double)f1;
                     A.dbg_w[(size_t)p * 2 * K + 2 * k + 1] = base * (double)f0;
                 }
@@ -454,8 +446,8 @@ sample_kernel(SweepArgs A) {
                 A.zr_next[p] = (uint16_t)(ks | (rs << 15));                                   // a7
                 if (keep) ++keeps;
                 else {
-                    atomicAdd(&S.dm[k0], -1); atomicAdd(&S.dt[k0], -rrem);
-                    atomicAdd(&S.dm[ks], 1); atomicAdd(&S.dt[ks], rs);
+                    atomicAdd(&S.dmt[k0], -65536 - rrem);
+                    atomicAdd(&S.dmt[ks], 65536 + rs);
                     moved += (ks != k0);
                 }
             }
@@ -465,9 +457,13 @@ sample_kernel(SweepArgs A) {
     if constexpr (!DEBUG) {
         __syncwarp();
         for (int k = lane; k < K; k += 32) {
-            const int dmv = S.dm[k], dtv = S.dt[k];
-            if (dmv) atomicAdd(A.dm + row + k, dmv);
-            if (dtv) atomicAdd(A.dt + row + k, dtv);
+            const int x = S.dmt[k];
+            if (x) {
+                const int dtv = (int)(short)(x & 0xFFFF);   // low half, sign-extended
+                const int dmv = (x - dtv) >> 16;
+                if (dmv) atomicAdd(A.dm + row + k, dmv);
+                if (dtv) atomicAdd(A.dt + row + k, dtv);
+            }
         }
     }
     __syncwarp();
