@@ -105,7 +105,8 @@ struct spdp_ctx {
              *d_sweep = nullptr;
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
     uint32_t *d_doc_ptr = nullptr, *d_doc_pos = nullptr;   // CSR: sorted-token positions of each local doc
-    float* d_n = nullptr;                         // n_dk as exact integers in fp32, rows in sigma order
+    void* d_n = nullptr;                          // n_dk rows in sigma order: fp32 or uint16 (row16)
+    bool row16 = false;                           // uint16 doc-topic rows (HBM-resident arrays)
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
     int colstart[8] = {0};
@@ -176,33 +177,41 @@ spdp_status nccl_check(spdp_ctx* c, int r, const char* what) {
 
 // ------------------------------------------------------------------ kernel dispatch
 template <int LPT, int KPL, bool DBG>
-void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks) {
+void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks, bool row16) {
     const size_t smem = sample_smem_bytes<LPT, KPL>();
     const int blocks = std::min((a.nchunks + kWarps - 1) / kWarps, max_blocks);
-    if (blocks > 0) sample_kernel<LPT, KPL, DBG><<<blocks, kWarps * 32, smem, s>>>(a);
+    if (blocks <= 0) return;
+    if (row16) sample_kernel<LPT, KPL, DBG, uint16_t><<<blocks, kWarps * 32, smem, s>>>(a);
+    else sample_kernel<LPT, KPL, DBG, float><<<blocks, kWarps * 32, smem, s>>>(a);
 }
 template <int LPT, int KPL>
 int resident_blocks_t() {
     int nb = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sample_kernel<LPT, KPL, false>, kWarps * 32,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sample_kernel<LPT, KPL, false, float>, kWarps * 32,
                                                   sample_smem_bytes<LPT, KPL>());
     return std::max(nb, 1) * std::max(sms, 1);
 }
 template <int LPT, int KPL>
 void set_attr_t() {
     const int smem = (int)sample_smem_bytes<LPT, KPL>();
-    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(sample_kernel<LPT, KPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, true, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, true, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int psm = kWarps * LPT * KPL * (int)sizeof(double);
-    cudaFuncSetAttribute(perplexity_kernel<LPT, KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+    cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+    cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
 }
 template <int LPT, int KPL>
-void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum, double* partial, cudaStream_t s) {
+void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum, double* partial, cudaStream_t s,
+                  bool row16) {
     const size_t smem = (size_t)kWarps * LPT * KPL * sizeof(double);
     const int blocks = (a.nchunks + kWarps - 1) / kWarps;
-    if (blocks > 0) perplexity_kernel<LPT, KPL><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
+    if (blocks <= 0) return;
+    if (row16) perplexity_kernel<LPT, KPL, uint16_t><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
+    else perplexity_kernel<LPT, KPL, float><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
 }
 
 #define SPDP_DISPATCH(LPT_, KPL_, CALL)                     \
@@ -220,7 +229,7 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
     }
 
 void launch_sample(spdp_ctx* c, const SweepArgs& a, bool dbg) {
-#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid))
+#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid, c->row16) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid, c->row16))
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_S)
 #undef CALL_S
 }
@@ -233,7 +242,7 @@ void set_attrs(spdp_ctx* c) {
 #undef CALL_R
 }
 void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
-#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream)
+#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream, c->row16)
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_P)
 #undef CALL_P
 }
@@ -336,6 +345,27 @@ void partition_docs(uint64_t seed, int G, int64_t N, int32_t D, const std::vecto
 }
 
 // Upload (z, r or tables) as the sampler state: counts from z.
+size_t row_bytes(const spdp_ctx* c) {
+    return ((size_t)c->Dloc * c->Kp + 1024) * (c->row16 ? sizeof(uint16_t) : sizeof(float));
+}
+
+// doc-topic rows to the host as floats (sigma order, [Dloc][Kp])
+spdp_status read_rows(spdp_ctx* c, std::vector<float>& out) {
+    const size_t n = (size_t)c->Dloc * c->Kp;
+    out.assign(n, 0.f);
+    if (c->row16) {
+        std::vector<uint16_t> tmp(n);
+        CU(cudaMemcpyAsync(tmp.data(), c->d_n, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        spdp_status s = sync(c, "read rows");
+        if (s) return s;
+        for (size_t j = 0; j < n; ++j) out[j] = (float)tmp[j];
+    } else {
+        CU(cudaMemcpyAsync(out.data(), c->d_n, sizeof(float) * n, cudaMemcpyDeviceToHost, c->stream));
+        return sync(c, "read rows");
+    }
+    return SPDP_OK;
+}
+
 // run fn(begin, end) over [0, n) on the host cores
 template <typename Fn>
 void parallel_for(int64_t n, Fn fn) {
@@ -405,10 +435,16 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     spdp_status s = sync(c, "install_state cells");
     if (s) return s;
     if (nbad) return fail(c, SPDP_EINVAL, "table counts violate 1 <= t <= m on %llu occupied cell(s) (or t > 0 on an empty one)", nbad);
-    CU(cudaMemsetAsync(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024), c->stream));
-    if (c->Nloc > 0)
-        init_local_kernel<<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc, Kp,
-                                                       c->d_sigma, c->d_zr, c->d_zr_next, c->d_n);
+    CU(cudaMemsetAsync(c->d_n, 0, row_bytes(c), c->stream));
+    if (c->Nloc > 0) {
+        if (c->row16)
+            init_local_kernel<uint16_t><<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc,
+                                                                     Kp, c->d_sigma, c->d_zr, c->d_zr_next,
+                                                                     (uint16_t*)c->d_n);
+        else
+            init_local_kernel<float><<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc,
+                                                                  Kp, c->d_sigma, c->d_zr, c->d_zr_next, (float*)c->d_n);
+    }
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
     if (c->d_D) CU(cudaMemsetAsync(c->d_D, 0, sizeof(int32_t) * 2 * c->cells, c->stream));
@@ -453,13 +489,21 @@ spdp_status run_waves(spdp_ctx* c) {
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
-            recount_docs_kernel<<<148 * 8, 256, smem, c->stream>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
-                                                                  c->Dloc, c->Kp, c->d_n);
+            if (c->row16)
+                recount_docs_kernel<uint16_t><<<148 * 8, 256, smem, c->stream>>>(
+                    c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (uint16_t*)c->d_n);
+            else
+                recount_docs_kernel<float><<<148 * 8, 256, smem, c->stream>>>(
+                    c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (float*)c->d_n);
             std::swap(c->d_zr, c->d_zr_next);
         } else {
             const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
-            apply_tokens_kernel<<<std::max(tblocks, 1), 256, 0, c->stream>>>(c->d_tok_doc, c->d_zr, c->d_zr_next, c->d_n,
-                                                                             c->d_sigma, c->Kp, tb, te);
+            if (c->row16)
+                apply_tokens_kernel<uint16_t><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
+                    c->d_tok_doc, c->d_zr, c->d_zr_next, (uint16_t*)c->d_n, c->d_sigma, c->Kp, tb, te);
+            else
+                apply_tokens_kernel<float><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
+                    c->d_tok_doc, c->d_zr, c->d_zr_next, (float*)c->d_n, c->d_sigma, c->Kp, tb, te);
         }
         rec(c, 4 * (size_t)w + 2);
         {
@@ -794,11 +838,20 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         c->prefetch_rows = ((double)c->Dloc * Kp * sizeof(float) > 0.5 * (double)l2) ? 1 : 0;
         if (const char* e = getenv("SPDP_PREFETCH_ROWS")) c->prefetch_rows = atoi(e);
+        c->row16 = c->prefetch_rows != 0;                // HBM-resident rows: half the bytes
+        if (const char* e = getenv("SPDP_ROW16")) c->row16 = atoi(e) != 0;
+        int32_t maxlen = 0;
+        for (int32_t dl : c->doclen) maxlen = std::max(maxlen, dl);
+        if (maxlen >= 65536) c->row16 = false;           // uint16 needs L_d < 2^16
     }
     ALLOC(c->d_sigma, Kp);
     CU(cudaMemcpy(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice));
-    ALLOC(c->d_n, (size_t)c->Dloc * Kp + 1024);      // +1024: the sample kernel reads whole topic spans
-    CU(cudaMemset(c->d_n, 0, sizeof(float) * ((size_t)c->Dloc * Kp + 1024)));
+    {   // +1024 elements: the sample kernel reads whole topic spans
+        uint8_t* nb = nullptr;
+        ALLOC(nb, row_bytes(c));
+        c->d_n = nb;
+        CU(cudaMemset(c->d_n, 0, row_bytes(c)));
+    }
     ALLOC(c->d_work, (size_t)W + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
     ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);
@@ -1029,9 +1082,8 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
         });
     }
     if (doc_topic) {
-        std::vector<float> nf((size_t)c->Dloc * Kp);
-        CU(cudaMemcpyAsync(nf.data(), c->d_n, sizeof(float) * nf.size(), cudaMemcpyDeviceToHost, c->stream));
-        if ((s = sync(c, "counts(n)"))) return s;
+        std::vector<float> nf;
+        if ((s = read_rows(c, nf))) return s;
         std::vector<int32_t> full;
         if (gather) full.assign((size_t)c->D * K, 0);
         int32_t* dst = gather ? full.data() : doc_topic;
@@ -1113,8 +1165,14 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
         double* part = c->d_partial;       // [0, grid) words, [grid, 2 grid) docs
         loglik_words_kernel<<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_Q, ls, d_off, c->V, c->I, c->K, c->Kp,
                                                         c->cfg.beta, part);
-        loglik_docs_kernel<<<grid, 256, 0, c->stream>>>(c->d_n, c->d_sigma, c->d_doclen, c->d_docgroup, c->d_alpha64, c->d_alpha_sum64,
-                                                       c->Dloc, c->K, c->Kp, part + grid);
+        if (c->row16)
+            loglik_docs_kernel<uint16_t><<<grid, 256, 0, c->stream>>>((const uint16_t*)c->d_n, c->d_sigma, c->d_doclen,
+                                                                      c->d_docgroup, c->d_alpha64, c->d_alpha_sum64, c->Dloc,
+                                                                      c->K, c->Kp, part + grid);
+        else
+            loglik_docs_kernel<float><<<grid, 256, 0, c->stream>>>((const float*)c->d_n, c->d_sigma, c->d_doclen,
+                                                                   c->d_docgroup, c->d_alpha64, c->d_alpha_sum64, c->Dloc,
+                                                                   c->K, c->Kp, part + grid);
         loglik_small_kernel<<<1, 1024, 0, c->stream>>>(c->d_M, c->d_Tt, c->d_T, c->d_disc64, c->d_conc64, c->I, c->K, c->Kp,
                                                       (double)c->V * c->cfg.beta, part + 2 * grid);
         reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(part, 2 * grid + 1, c->d_scalar + 1);   // words + docs + small
@@ -1261,10 +1319,13 @@ namespace {
 spdp_status debug_verify(spdp_ctx* c) {
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     std::vector<uint16_t> zr((size_t)c->Nloc);
-    std::vector<float> nf((size_t)c->Dloc * Kp);
+    std::vector<float> nf;
     std::vector<int32_t> n((size_t)c->Dloc * Kp), m(c->cells), t(c->cells), Q((size_t)V * Kp);
     CU(cudaMemcpy(zr.data(), c->d_zr, 2 * zr.size(), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(nf.data(), c->d_n, 4 * nf.size(), cudaMemcpyDeviceToHost));
+    {
+        spdp_status s0 = read_rows(c, nf);
+        if (s0) return s0;
+    }
     for (int32_t j = 0; j < c->Dloc; ++j)
         for (int k = 0; k < Kp; ++k) n[(size_t)j * Kp + k] = (int32_t)nf[(size_t)j * Kp + c->sigma[(size_t)k]];
     CU(cudaMemcpy(m.data(), c->d_m, 4 * m.size(), cudaMemcpyDeviceToHost));

@@ -124,6 +124,36 @@ __device__ __forceinline__ void removal_factors(int rrem, int mv, int tv, int Mv
     R1 = (x1 > 0.f) ? __fdiv_rn(x1, Fsum) : 0.f;
 }
 
+// ---------------------------------------------------------------- doc-topic row element
+// Doc-topic counts are stored either as exact-integer fp32 (rows that live in
+// L2) or as uint16 (half the bytes when the rows stream from HBM; n_dk <= L_d < 2^16).
+template <typename NT>
+struct Row;
+template <>
+struct Row<float> {
+    __device__ __forceinline__ static float4 load4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+    __device__ __forceinline__ static float load1(const float* p) { return __ldg(p); }
+    __device__ __forceinline__ static void add(float* base, size_t idx, int d) { atomicAdd(base + idx, (float)d); }
+    __device__ __forceinline__ static void store(float* p, int v) { *p = (float)v; }
+    __device__ __forceinline__ static int get(const float* p) { return (int)*p; }
+};
+__device__ __forceinline__ float u16lo(uint32_t x) { return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7610)) - 8388608.f; }
+__device__ __forceinline__ float u16hi(uint32_t x) { return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7632)) - 8388608.f; }
+template <>
+struct Row<uint16_t> {
+    __device__ __forceinline__ static float4 load4(const uint16_t* p) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+        return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y));
+    }
+    __device__ __forceinline__ static float load1(const uint16_t* p) { return (float)__ldg(p); }
+    // +-1 on one half of the containing 32-bit word (a half never leaves [0, L_d], no carry)
+    __device__ __forceinline__ static void add(uint16_t* base, size_t idx, int d) {
+        atomicAdd(reinterpret_cast<unsigned int*>(base) + (idx >> 1), (unsigned int)d << ((idx & 1) * 16));
+    }
+    __device__ __forceinline__ static void store(uint16_t* p, int v) { *p = (uint16_t)v; }
+    __device__ __forceinline__ static int get(const uint16_t* p) { return (int)*p; }
+};
+
 struct SweepArgs {
     // tokens of this rank, sorted by (wave, w, i, doc)
     const uint32_t* tok_doc;
@@ -137,7 +167,7 @@ struct SweepArgs {
     int nchunks;
     uint32_t* work;                // persistent-warp chunk counter (zeroed before each launch)
     // counts
-    float* n;                      // doc-topic counts n_dk as exact integers in fp32, rows in sigma order
+    void* n;                       // doc-topic counts n_dk (Row<NT>), rows in sigma order
     const int* sigma;              // [Kp] in-row position of topic k
     int colstart[8];               // first block of column q in the sigma order
     int prefetch_rows;             // the doc-topic array exceeds L2: prefetch rows in phase 1
@@ -209,7 +239,7 @@ __device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
 //     the r split by the exact r = 1 share; outputs and count deltas (a7).
 //   Every CDF boundary is an fp64 sum of fp32 partial sums of few terms
 //   (a few fp32 ulps of the total), inside the 1e-6 band of north_star (5).
-template <int LPT, int KPL, bool DEBUG>
+template <int LPT, int KPL, bool DEBUG, typename NT>
 __global__ void __launch_bounds__(kWarps * 32, SPDP_MINB)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
@@ -284,9 +314,10 @@ sample_kernel(SweepArgs A) {
             x0 = x.x;
             u = u53(x);
         }
-        const float* __restrict__ nrow = A.n + noff;
+        const NT* __restrict__ nrow = reinterpret_cast<const NT*>(A.n) + noff;
         if (mine && A.prefetch_rows) {   // rows not L2-resident: pull this token's row towards L2
-            for (int l = 0; l * 32 < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + 32 * l));
+            constexpr int PER_LINE = 128 / (int)sizeof(NT);
+            for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
         }
         const int k0 = (int)(zr0 & 0x7FFFu);
         const uint32_t mt0 = S.mt[k0];
@@ -295,7 +326,7 @@ sample_kernel(SweepArgs A) {
         const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
         float Fk0 = 0.f, R1k0 = 0.f;                    // topic k0's factors after the own removal
         if (mine) removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
-        const float n0 = mine ? __ldg(nrow + A.sigma[k0]) : 0.f;
+        const float n0 = mine ? Row<NT>::load1(nrow + A.sigma[k0]) : 0.f;
         const float al0 = alpha_i[k0];
         const float wold = __fmaf_rn(n0, S.F[k0], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
         const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
@@ -308,10 +339,10 @@ sample_kernel(SweepArgs A) {
             const int sk0 = __shfl_sync(0xffffffffu, k0, src);
             const float sdlt = __shfl_sync(0xffffffffu, dlt, src);
             const double su = __shfl_sync(0xffffffffu, u, src);
-            const float* __restrict__ nl = A.n + snoff + 4 * gl;
+            const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + snoff + 4 * gl;
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = __ldg(reinterpret_cast<const float4*>(nl + 4 * A.colstart[q]));
+            for (int q = 0; q < NB; ++q) v[q] = Row<NT>::load4(nl + 4 * A.colstart[q]);
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -388,7 +419,7 @@ sample_kernel(SweepArgs A) {
                 int cs = 0;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) if (q == qs) cs = A.colstart[q];
-                const float4 n4 = __ldg(reinterpret_cast<const float4*>(nrow + 4 * (cs + wg)));
+                const float4 n4 = Row<NT>::load4(nrow + 4 * (cs + wg));
                 const float4 F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
                 const float4 a4 = *reinterpret_cast<const float4*>(&S.aF[skew<KPL>(kq)]);
                 float wq[4] = {__fmaf_rn(n4.x, F4.x, a4.x), __fmaf_rn(n4.y, F4.y, a4.y),
@@ -426,7 +457,7 @@ sample_kernel(SweepArgs A) {
                 // exact slot masses w1 = (alpha + n) F1, w0 = (alpha + n) F0 of every topic
                 for (int k = 0; k < K; ++k) {
                     const bool own = (k == k0);
-                    const float nk = nrow[A.sigma[k]] - (own ? 1.f : 0.f);
+                    const float nk = (float)Row<NT>::get(nrow + A.sigma[k]) - (own ? 1.f : 0.f);
                     float f0, f1;
                     if (own) {
                         const int mm = max(m0 - 1, 0), tt = min(max(t0 - rrem, 0), mm);
@@ -482,23 +513,24 @@ sample_kernel(SweepArgs A) {
 }
 
 template <int LPT, int KPL>
-constexpr size_t sample_smem_bytes() {
+constexpr size_t sample_smem_bytes() {  // (independent of the row element type)
     return kWarps * sizeof(WarpSmem<LPT * KPL, KPL>);
 }
 
 // ---------------------------------------------------------------- end of wave: n and z
 // n_{d k0} -= 1, n_{d k*} += 1 for every token of the wave that moved; zr <- zr_next.
+template <typename NT>
 __global__ void apply_tokens_kernel(const uint32_t* __restrict__ tok_doc, uint16_t* __restrict__ zr,
-                                    const uint16_t* __restrict__ zr_next, float* __restrict__ n,
+                                    const uint16_t* __restrict__ zr_next, NT* __restrict__ n,
                                     const int* __restrict__ sigma,
                                     int Kp, uint32_t begin, uint32_t end) {
     for (uint32_t p = begin + blockIdx.x * blockDim.x + threadIdx.x; p < end; p += gridDim.x * blockDim.x) {
         const uint32_t zo = zr[p], zn = zr_next[p];
         const uint32_t ko = zo & 0x7FFFu, kn = zn & 0x7FFFu;
         if (ko != kn) {
-            float* nr = n + (size_t)tok_doc[p] * Kp;
-            atomicAdd(nr + sigma[ko], -1.0f);      // exact: integer-valued fp32 (< 2^24)
-            atomicAdd(nr + sigma[kn], 1.0f);
+            const size_t r0 = (size_t)tok_doc[p] * Kp;
+            Row<NT>::add(n, r0 + sigma[ko], -1);   // exact integer arithmetic
+            Row<NT>::add(n, r0 + sigma[kn], 1);
         }
         zr[p] = (uint16_t)zn;
     }
@@ -597,9 +629,10 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
 // assignments") instead of two scattered atomics per moved token: one warp per
 // document, a shared-memory histogram over the document's tokens (CSR index in
 // sorted-token positions), one coalesced row write in sigma order.
+template <typename NT>
 __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const uint32_t* __restrict__ doc_pos,
                                     const uint16_t* __restrict__ zr, const int* __restrict__ sigma, int D, int Kp,
-                                    float* __restrict__ n) {
+                                    NT* __restrict__ n) {
     extern __shared__ int hist[];                    // [warps][Kp]
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     int* h = hist + (size_t)(threadIdx.x >> 5) * Kp;
@@ -609,8 +642,8 @@ __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const 
         const uint32_t e = doc_ptr[d + 1];
         for (uint32_t t = doc_ptr[d] + lane; t < e; t += 32) atomicAdd(&h[sigma[zr[doc_pos[t]] & 0x7FFFu]], 1);
         __syncwarp();
-        float* row = n + (size_t)d * Kp;
-        for (int j = lane; j < Kp; j += 32) row[j] = (float)h[j];
+        NT* row = n + (size_t)d * Kp;
+        for (int j = lane; j < Kp; j += 32) Row<NT>::store(row + j, h[j]);
         __syncwarp();
     }
 }
@@ -758,15 +791,16 @@ __global__ void check_cells_kernel(const int32_t* __restrict__ m, const int32_t*
     if (nb) atomicAdd(bad, nb);
 }
 // this rank's token records (sorted order) and doc-topic counts
+template <typename NT>
 __global__ void init_local_kernel(const uint32_t* __restrict__ tok_id, const uint32_t* __restrict__ tok_doc,
                                   const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t nloc, int Kp,
                                   const int* __restrict__ sigma,
-                                  uint16_t* __restrict__ zr, uint16_t* __restrict__ zr_next, float* __restrict__ n) {
+                                  uint16_t* __restrict__ zr, uint16_t* __restrict__ zr_next, NT* __restrict__ n) {
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += gridDim.x * blockDim.x) {
         const uint32_t p = tok_id[q];
         const uint16_t v = (uint16_t)(z[p] | (r[p] << 15));
         zr[q] = v; zr_next[q] = v;
-        atomicAdd(n + (size_t)tok_doc[q] * Kp + sigma[z[p]], 1.0f);
+        Row<NT>::add(n, (size_t)tok_doc[q] * Kp + sigma[z[p]], 1);
     }
 }
 
@@ -782,7 +816,7 @@ __global__ void scatter_zr_kernel(const uint32_t* __restrict__ id, const uint16_
 // phi0_kw = (beta + Q)/(V beta + T) (reading c16);
 // per token log sum_k (n_dk + alpha_ik) phi^i_kw / (L_d + sum_k alpha_ik).
 // Per-chunk fp64 partials (fixed order) -> deterministic final reduction.
-template <int LPT, int KPL>
+template <int LPT, int KPL, typename NT>
 __global__ void __launch_bounds__(kWarps * 32)
 perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const double* __restrict__ alpha_sum,
                   double* __restrict__ partial) {
@@ -819,11 +853,11 @@ perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const double*
         const uint32_t tok = base + g;
         const bool valid = tok < end;
         const uint32_t doc = valid ? A.tok_doc[tok] : 0u;
-        const float* nrow = A.n + (size_t)doc * Kp;
+        const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * Kp;
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < KPL; ++j)
-            if (kb + j < K) s += ((double)__ldg(nrow + A.sigma[kb + j]) + al[j]) * sphi[kb + j];
+            if (kb + j < K) s += ((double)Row<NT>::load1(nrow + A.sigma[kb + j]) + al[j]) * sphi[kb + j];
 #pragma unroll
         for (int off = LPT / 2; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, LPT);
         if (valid && gl == 0) ll += log(s / ((double)doclen[doc] + asum));

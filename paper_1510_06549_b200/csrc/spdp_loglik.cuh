@@ -76,7 +76,8 @@ __global__ void loglik_words_kernel(const int32_t* __restrict__ m, const int32_t
 }
 
 // document terms, one warp per local document.
-__global__ void loglik_docs_kernel(const float* __restrict__ n, const int* __restrict__ sigma,
+template <typename NT>
+__global__ void loglik_docs_kernel(const NT* __restrict__ n, const int* __restrict__ sigma,
                                    const int32_t* __restrict__ doclen,
                                    const int32_t* __restrict__ docgroup, const double* __restrict__ alpha,
                                    const double* __restrict__ alpha_sum, int D, int K, int Kp,
@@ -88,7 +89,7 @@ __global__ void loglik_docs_kernel(const float* __restrict__ n, const int* __res
         const int i = docgroup[d];
         if (doclen[d] == 0) continue;      // empty document: p(z_d) = 1
         for (int k = lane; k < K; k += 32) {
-            const int nv = (int)n[(size_t)d * Kp + sigma[k]];
+            const int nv = Row<NT>::get(n + (size_t)d * Kp + sigma[k]);
             if (nv) {
                 const double al = alpha[(size_t)i * Kp + k];
                 acc += lgamma(al + (double)nv) - lgamma(al);
