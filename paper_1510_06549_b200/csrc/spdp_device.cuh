@@ -137,8 +137,8 @@ struct Row<float> {
     __device__ __forceinline__ static void store(float* p, int v) { *p = (float)v; }
     __device__ __forceinline__ static int get(const float* p) { return (int)*p; }
 };
-__device__ __forceinline__ float u16lo(uint32_t x) { return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7610)) - 8388608.f; }
-__device__ __forceinline__ float u16hi(uint32_t x) { return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7632)) - 8388608.f; }
+__device__ __forceinline__ float u16lo(uint32_t x) { return __uint2float_rn(x & 0xFFFFu); }   // I2F.U16
+__device__ __forceinline__ float u16hi(uint32_t x) { return __uint2float_rn(x >> 16); }       // I2F.U16 .H1
 template <>
 struct Row<uint16_t> {
     __device__ __forceinline__ static float4 load4(const uint16_t* p) {
@@ -315,9 +315,15 @@ sample_kernel(SweepArgs A) {
             u = u53(x);
         }
         const NT* __restrict__ nrow = reinterpret_cast<const NT*>(A.n) + noff;
-        if (mine && A.prefetch_rows) {   // rows not L2-resident: pull this token's row towards L2
+        if (A.prefetch_rows) {   // rows not L2-resident: pull rows of this batch (first) and the next towards L2
             constexpr int PER_LINE = 128 / (int)sizeof(NT);
-            for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
+            if (mine && b0 == start)
+                for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
+            const uint32_t pn = p + 32;
+            if (pn < end) {
+                const NT* nn = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp;
+                for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
+            }
         }
         const int k0 = (int)(zr0 & 0x7FFFu);
         const uint32_t mt0 = S.mt[k0];
