@@ -19,6 +19,9 @@
 namespace spdp {
 
 constexpr int kWarps = 4;          // warps per block of the sample kernel
+#ifndef SPDP_PREFETCH_NEXT
+#define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
+#endif
 #ifndef SPDP_MINB
 #define SPDP_MINB 4                // resident blocks per SM the sample kernel is compiled for
 #endif
@@ -137,8 +140,14 @@ struct Row<float> {
     __device__ __forceinline__ static void store(float* p, int v) { *p = (float)v; }
     __device__ __forceinline__ static int get(const float* p) { return (int)*p; }
 };
+#ifdef SPDP_CVT_I2F
 __device__ __forceinline__ float u16lo(uint32_t x) { return __uint2float_rn(x & 0xFFFFu); }   // I2F.U16
 __device__ __forceinline__ float u16hi(uint32_t x) { return __uint2float_rn(x >> 16); }       // I2F.U16 .H1
+#else
+// exact u16 -> f32 on the full-rate pipes: 2^23 + x as a bit pattern, minus 2^23
+__device__ __forceinline__ float u16lo(uint32_t x) { return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7610)) - 8388608.f; }
+__device__ __forceinline__ float u16hi(uint32_t x) { return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7632)) - 8388608.f; }
+#endif
 template <>
 struct Row<uint16_t> {
     __device__ __forceinline__ static float4 load4(const uint16_t* p) {
@@ -317,10 +326,10 @@ sample_kernel(SweepArgs A) {
         const NT* __restrict__ nrow = reinterpret_cast<const NT*>(A.n) + noff;
         if (A.prefetch_rows) {   // rows not L2-resident: pull rows of this batch (first) and the next towards L2
             constexpr int PER_LINE = 128 / (int)sizeof(NT);
-            if (mine && b0 == start)
+            if (mine && (b0 == start || !SPDP_PREFETCH_NEXT))
                 for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
             const uint32_t pn = p + 32;
-            if (pn < end) {
+            if (SPDP_PREFETCH_NEXT && pn < end) {
                 const NT* nn = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp;
                 for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
             }
