@@ -75,6 +75,20 @@ def lib():
         L.or_word_prob.argtypes = [P, C.c_int32, C.c_int32]
         L.or_chain_codes.restype = C.c_int
         L.or_chain_codes.argtypes = [P, C.c_int64, C.c_int, C.c_int, P]
+        L.or_phi0.argtypes = [P, C.c_int, C.c_int]
+        L.or_phi0.restype = C.c_double
+        L.or_phi.argtypes = [P, C.c_int, C.c_int, C.c_int]
+        L.or_phi.restype = C.c_double
+        L.or_topics.argtypes = [P, P, P]
+        L.or_topics.restype = None
+        L.or_foldin.argtypes = [P, C.c_int64, C.c_int32, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.c_int, P, P, P]
+        L.or_heldout_perplexity.argtypes = [P, C.c_int64, C.c_int32, P, P, P, P, P]
+        L.or_heldout_perplexity.restype = C.c_double
+        L.or_hellinger.argtypes = [C.c_int64, P, P]
+        L.or_hellinger.restype = C.c_double
+        L.or_greedy_match.argtypes = [C.c_int, P, P]
+        L.or_greedy_match.restype = None
+        L.or_topic_align.argtypes = [P, P, P, P]
         _lib = L
     return _lib
 
@@ -217,10 +231,60 @@ class Oracle:
     def check_invariants(self) -> int:
         return int(lib().or_check_invariants(self.h))
 
+    # ---------------- NEXT-1: held-out evaluation ----------------
+    def topics(self):
+        """(phi0 [K,V], phi [I,K,V]): Eqs. P:1753-1754 of the current state."""
+        p0 = np.zeros((self.K, self.V)); p = np.zeros((self.I, self.K, self.V))
+        lib().or_topics(self.h, _ptr(p0), _ptr(p))
+        return p0, p
+
+    def foldin(self, group, doc, word, num_docs, seed, iterations, first_iteration=0, z=None,
+               force_z=None, want_margin=False):
+        """Fold-in (reading c21).  z None: Philox initial topics.  Returns z (and margins)."""
+        g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
+        w = np.ascontiguousarray(word, np.int32)
+        init = z is None
+        zz = np.full(len(g), -1, np.int32) if init else np.array(z, np.int32, copy=True)
+        fz = None if force_z is None else np.ascontiguousarray(force_z, np.int32)
+        mg = np.zeros(len(g)) if want_margin else None
+        rc = lib().or_foldin(self.h, len(g), int(num_docs), _ptr(g), _ptr(d), _ptr(w), int(seed) & (2**64 - 1),
+                             int(first_iteration), int(iterations), int(init), _ptr(zz), _ptr(fz), _ptr(mg))
+        if rc != 0:
+            raise RuntimeError(f"or_foldin failed ({rc})")
+        return (zz, mg) if want_margin else zz
+
+    def heldout_perplexity(self, group, doc, word, num_docs, z, want_theta=False):
+        g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
+        w = np.ascontiguousarray(word, np.int32); zz = np.ascontiguousarray(z, np.int32)
+        th = np.zeros((int(num_docs), self.K)) if want_theta else None
+        ppl = float(lib().or_heldout_perplexity(self.h, len(g), int(num_docs), _ptr(g), _ptr(d), _ptr(w), _ptr(zz),
+                                                _ptr(th)))
+        return (ppl, th) if want_theta else ppl
+
+    def topic_align(self, other):
+        """(dist [K,K] Hellinger on phi0~, perm [K]) against another oracle state."""
+        dist = np.zeros((self.K, self.K)); perm = np.zeros(self.K, np.int32)
+        if lib().or_topic_align(self.h, other.h, _ptr(dist), _ptr(perm)) != 0:
+            raise RuntimeError("or_topic_align: K or V mismatch")
+        return dist, perm
+
     def partition(self, shards: int):
         out = np.zeros(self.D, np.int32)
         lib().or_partition(self.h, int(shards), _ptr(out))
         return out
+
+
+def hellinger(p, q) -> float:
+    p = np.ascontiguousarray(p, np.float64); q = np.ascontiguousarray(q, np.float64)
+    assert p.shape == q.shape
+    return float(lib().or_hellinger(p.size, _ptr(p), _ptr(q)))
+
+
+def greedy_match(dist):
+    d = np.ascontiguousarray(dist, np.float64); K = d.shape[0]
+    perm = np.zeros(K, np.int32)
+    lib().or_greedy_match(K, _ptr(d), _ptr(perm))
+    return perm
 
 
 def from_corpus(corpus, num_topics, alpha=0.1, beta=0.1, discount=0.7, concentration=100.0, seed=7,

@@ -32,6 +32,11 @@
  *      C(m,t) factor of Eq. SPDP-table-to-head summed out
  *      = or_log_joint (reading c1, c2).
  *  - Philox4x32-10 counter-based RNG (reading c11; Salmon et al. 2011).
+ *  - NEXT-1 held-out evaluation: topic estimates or_phi0 / or_phi / or_topics
+ *      (P:1753-1754); fold-in of held-out documents or_foldin (reading c21);
+ *      held-out perplexity or_heldout_perplexity; Hellinger
+ *      distance and greedy topic alignment or_hellinger / or_topic_align
+ *      (§4.2.6, reading c22).
  */
 #include <math.h>
 #include <stdint.h>
@@ -782,4 +787,172 @@ int or_chain_codes(ostate *s, int64_t nsweeps, int waves, int tbase, int64_t *co
         codes[it] = code + mul * tc;
     }
     return 0;
+}
+
+/* ================================================================== */
+/* NEXT-1: held-out evaluation                    */
+/* ================================================================== */
+/* Topic-word estimates of the current state (after convergence):
+ *   phi0~_kw  = (beta + Q_kw) / (V beta + T_k)                  Eq. spdp-word-topic-estimate,
+ *               identity P: sum_i sum_w q_{ikwv} = Q_kv;
+ *   phi~^i_kw = (m_ikw - a_i t_ikw)/(b_i + m_ik.) + (b_i + a_i t_ik.)/(b_i + m_ik.) phi0~_kw
+ *               Eq. spdp-group-word-topic-estimate, mixing weight of reading c16,
+ *               identity P: sum_v p_{w,v} phi0~_kv = phi0~_kw. */
+double or_phi0(const ostate *s, int k, int w) {
+    return (s->beta + (double)s->Q[(size_t)k * s->V + w]) / ((double)s->V * s->beta + (double)s->T[k]);
+}
+double or_phi(const ostate *s, int i, int k, int w) {
+    double a = s->a[i], b = s->b[i];
+    double Mk = (double)s->M[(size_t)i * s->K + k], Tk = (double)s->Tt[(size_t)i * s->K + k];
+    size_t c = IDX3(s, i, w, k);
+    return ((double)s->m[c] - a * (double)s->t[c]) / (b + Mk) + (b + a * Tk) / (b + Mk) * or_phi0(s, k, w);
+}
+
+/* Fold-in of held-out documents (reading c21; the paper does not say how the
+ * theta~ of a test document is obtained): collapsed Gibbs over
+ * the held-out tokens' topics z only, with the trained phi~^i frozen as the
+ * word likelihoods.  The held-out documents are independent given phi~, and
+ * within a document the tokens are visited sequentially in canonical order:
+ *   p(z_p = k | rest) ∝ (alpha_ik + n_dk^{-p}) phi~^i_{k w_p}      (LDA fold-in with phi~^i of P:1754).
+ * Randomness: u = u53(Philox(seed; p, it, 1, 0)) for token p in iteration it;
+ * the draw is k* = min{k : cdf_k > u} (reading c10 with K slots).
+ * Initial z (z in/out holds -1 entries or a state): when init != 0,
+ * z_p = floor(x0 K / 2^32) of Philox(seed; p, 0xFFFFFFFF, 1, 0).
+ * force_z / margin: lock-step testing as in or_sweep_par. */
+int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
+              const int32_t *word, uint64_t seed, int32_t first_iter, int32_t iters, int init, int32_t *z,
+              const int32_t *force_z, double *margin) {
+    int K = s->K;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int64_t p = 0; p < Nh; p++) {
+        if (group[p] < 0 || group[p] >= s->I || word[p] < 0 || word[p] >= s->V || doc[p] < 0 || doc[p] >= Dh) return -1;
+        if (init) {
+            uint32_t ctr[4] = {(uint32_t)p, 0xFFFFFFFFu, 1u, 0u}, x[4];
+            or_philox(ctr, key, x);
+            z[p] = (int32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
+        }
+        if (z[p] < 0 || z[p] >= K) return -1;
+    }
+    int32_t *n = (int32_t *)calloc((size_t)Dh * K, sizeof(int32_t));
+    double *w = (double *)malloc(sizeof(double) * (size_t)K), *prob = (double *)malloc(sizeof(double) * (size_t)K);
+    if (!n || !w || !prob) { free(n); free(w); free(prob); return -2; }
+    for (int64_t p = 0; p < Nh; p++) n[(size_t)doc[p] * K + z[p]]++;
+    for (int32_t it = first_iter; it < first_iter + iters; it++) {
+        for (int64_t p = 0; p < Nh; p++) {
+            int i = group[p], d = doc[p];
+            n[(size_t)d * K + z[p]]--;
+            double tot = 0.0;
+            for (int k = 0; k < K; k++) {
+                w[k] = (s->alpha[(size_t)i * K + k] + (double)n[(size_t)d * K + k]) * or_phi(s, i, k, word[p]);
+                tot += w[k];
+            }
+            for (int k = 0; k < K; k++) prob[k] = w[k] / tot;
+            uint32_t ctr[4] = {(uint32_t)p, (uint32_t)it, 1u, 0u}, x[4];
+            or_philox(ctr, key, x);
+            double mg = 0.0;
+            int k_new = draw_slot(K, prob, u53(x), &mg);
+            if (margin) margin[p] = mg;
+            if (force_z) k_new = force_z[p];
+            z[p] = k_new;
+            n[(size_t)d * K + k_new]++;
+        }
+    }
+    free(n); free(w); free(prob);
+    return 0;
+}
+
+/* Held-out perplexity (§3.2.2, reading c17 for the exponent):
+ *   exp(- sum_p log sum_k theta~_dk phi~^i_{k w_p} / Nh),
+ * theta~_dk = (n_dk + alpha_ik) / sum_k (n_dk + alpha_ik)   Eq. spdp-topic-doc-estimate
+ * with n_dk counted from the held-out z.  theta (optional) receives [Dh*K]. */
+double or_heldout_perplexity(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
+                             const int32_t *word, const int32_t *z, double *theta) {
+    int K = s->K;
+    int32_t *n = (int32_t *)calloc((size_t)Dh * K, sizeof(int32_t));
+    int32_t *len = (int32_t *)calloc((size_t)Dh, sizeof(int32_t));
+    int32_t *dg = (int32_t *)malloc(sizeof(int32_t) * (size_t)Dh);
+    if (!n || !len || !dg) { free(n); free(len); free(dg); return NAN; }
+    for (int32_t d = 0; d < Dh; d++) dg[d] = 0;
+    for (int64_t p = 0; p < Nh; p++) { n[(size_t)doc[p] * K + z[p]]++; len[doc[p]]++; dg[doc[p]] = group[p]; }
+    if (theta)
+        for (int32_t d = 0; d < Dh; d++) {
+            int i = dg[d];
+            double asum = 0.0;
+            for (int k = 0; k < K; k++) asum += s->alpha[(size_t)i * K + k];
+            for (int k = 0; k < K; k++)
+                theta[(size_t)d * K + k] = ((double)n[(size_t)d * K + k] + s->alpha[(size_t)i * K + k]) / ((double)len[d] + asum);
+        }
+    double ll = 0.0;
+    for (int64_t p = 0; p < Nh; p++) {
+        int i = group[p], d = doc[p];
+        double asum = 0.0;
+        for (int k = 0; k < K; k++) asum += s->alpha[(size_t)i * K + k];
+        double pw = 0.0;
+        for (int k = 0; k < K; k++) {
+            double th = ((double)n[(size_t)d * K + k] + s->alpha[(size_t)i * K + k]) / ((double)len[d] + asum);
+            pw += th * or_phi(s, i, k, word[p]);
+        }
+        ll += log(pw);
+    }
+    free(n); free(len); free(dg);
+    return exp(-ll / (double)Nh);
+}
+
+/* Hellinger distance between two discrete distributions (§4.2.6
+ * compares topic models with it; the formula is not printed — reading c22:
+ * the standard H(p,q) = sqrt(1 - sum_v sqrt(p_v q_v)), clamped into [0,1]). */
+double or_hellinger(int64_t V, const double *p, const double *q) {
+    double bc = 0.0;
+    for (int64_t v = 0; v < V; v++) bc += sqrt(p[v] * q[v]);
+    double h2 = 1.0 - bc;
+    if (h2 < 0.0) h2 = 0.0;
+    if (h2 > 1.0) h2 = 1.0;
+    return sqrt(h2);
+}
+
+/* Topic alignment of two models on their base distributions phi0~ (reading c22):
+ * dist[k*K + k'] = H(phi0~_A[k], phi0~_B[k']); greedy minimum-distance
+ * matching: repeatedly take the smallest remaining distance (ties: smaller k,
+ * then smaller k') whose row and column are both free; perm[k] = k'. */
+typedef struct { double d; int k, kp; } pair_t;
+static int pair_cmp(const void *x, const void *y) {
+    const pair_t *a = (const pair_t *)x, *b = (const pair_t *)y;
+    if (a->d != b->d) return a->d < b->d ? -1 : 1;
+    if (a->k != b->k) return a->k < b->k ? -1 : 1;
+    return (a->kp > b->kp) - (a->kp < b->kp);
+}
+void or_greedy_match(int K, const double *dist, int32_t *perm) {
+    pair_t *pr = (pair_t *)malloc(sizeof(pair_t) * (size_t)K * K);
+    char *ur = (char *)calloc((size_t)K, 1), *uc = (char *)calloc((size_t)K, 1);
+    for (int k = 0; k < K; k++)
+        for (int kp = 0; kp < K; kp++) { pr[(size_t)k * K + kp].d = dist[(size_t)k * K + kp]; pr[(size_t)k * K + kp].k = k; pr[(size_t)k * K + kp].kp = kp; }
+    qsort(pr, (size_t)K * K, sizeof(pair_t), pair_cmp);
+    for (size_t j = 0; j < (size_t)K * K; j++)
+        if (!ur[pr[j].k] && !uc[pr[j].kp]) { ur[pr[j].k] = 1; uc[pr[j].kp] = 1; perm[pr[j].k] = pr[j].kp; }
+    free(pr); free(ur); free(uc);
+}
+int or_topic_align(const ostate *A, const ostate *B, double *dist, int32_t *perm) {
+    if (A->K != B->K || A->V != B->V) return -1;
+    int K = A->K, V = A->V;
+    double *pa = (double *)malloc(sizeof(double) * (size_t)V), *pb = (double *)malloc(sizeof(double) * (size_t)V);
+    for (int k = 0; k < K; k++) {
+        for (int w = 0; w < V; w++) pa[w] = or_phi0(A, k, w);
+        for (int kp = 0; kp < K; kp++) {
+            for (int w = 0; w < V; w++) pb[w] = or_phi0(B, kp, w);
+            dist[(size_t)k * K + kp] = or_hellinger(V, pa, pb);
+        }
+    }
+    free(pa); free(pb);
+    or_greedy_match(K, dist, perm);
+    return 0;
+}
+
+/* phi0 [K*V] and phi [I*K*V] (either may be NULL) of the current state. */
+void or_topics(const ostate *s, double *phi0, double *phi) {
+    for (int k = 0; k < s->K; k++)
+        for (int w = 0; w < s->V; w++) {
+            if (phi0) phi0[(size_t)k * s->V + w] = or_phi0(s, k, w);
+            if (phi)
+                for (int i = 0; i < s->I; i++) phi[((size_t)i * s->K + k) * s->V + w] = or_phi(s, i, k, w);
+        }
 }

@@ -125,3 +125,30 @@ def tiny_corpus(groups: int, docs: list[list[int]], doc_group: list[int], vocab:
             g.append(doc_group[di]); d.append(di); w.append(x)
     a = lambda v: np.asarray(v, np.int32)
     return Corpus(a(g), a(d), a(w), np.zeros(len(w), np.int32), groups, len(docs), vocab)
+
+
+def holdout_split(corpus: Corpus, fraction: float = 0.1, seed: int = 0) -> tuple[Corpus, Corpus]:
+    """(train, test): hold out ``fraction`` of the documents of every group
+    (§4.1: "For each group, 10% of the data is held out
+    from training for computing the perplexity").  Seeded choice of
+    round(fraction * D_i) documents per group; doc ids renumbered densely in
+    each part, token order kept (canonical: group, doc, position)."""
+    rng = np.random.default_rng(seed)
+    doc_group = np.full(corpus.num_docs, -1, np.int64)
+    doc_group[corpus.doc] = corpus.group
+    test_doc = np.zeros(corpus.num_docs, bool)
+    for i in range(corpus.num_groups):
+        ids = np.nonzero(doc_group == i)[0]
+        k = int(round(fraction * len(ids)))
+        if k:
+            test_doc[rng.choice(ids, size=k, replace=False)] = True
+
+    def part(mask_doc):
+        keep = mask_doc[corpus.doc]
+        old = np.nonzero(mask_doc)[0]
+        new_id = np.full(corpus.num_docs, -1, np.int64)
+        new_id[old] = np.arange(len(old))
+        return Corpus(corpus.group[keep].copy(), new_id[corpus.doc[keep]].astype(np.int32), corpus.word[keep].copy(),
+                      corpus.z_gen[keep].copy(), corpus.num_groups, int(len(old)), corpus.vocab)
+
+    return part(~test_doc), part(test_doc)
