@@ -131,16 +131,24 @@ spdp_status spdp_set_state(spdp_ctx* ctx, const int32_t* z, const uint8_t* r, co
 spdp_status spdp_sweep(spdp_ctx* ctx, int32_t num_sweeps);
 
 /* Split sweep for SPDP_EXCHANGE_EXTERNAL: spdp_sweep_local runs every wave
- * on this rank and leaves the rank's net (customer, table) count changes in
- * the device buffer returned by spdp_exchange_buffer (int32, *count elements,
- * device pointer owned by the context); the caller replaces its content by
- * the element-wise sum over ranks, then calls spdp_sweep_merge. */
+ * on this rank and leaves the rank's net (customer, table) count change of
+ * every cell since the sweep start in the device buffer returned by
+ * spdp_exchange_buffer (*count elements of *elem_bytes bytes, device pointer
+ * owned by the context).  Each element packs both changes of one cell as
+ * dm * 2^B + dt in two's complement, B = 16 for 4-byte elements (chosen when
+ * max_{i,w} count(i,w) < 2^15, which bounds |sum over ranks| of either half)
+ * and B = 32 for 8-byte elements, so the plain integer sum of the packed
+ * elements over ranks (wrapping) is the packed sum of dm and dt.  The caller
+ * replaces the buffer's content by that element-wise sum over ranks, then
+ * calls spdp_sweep_merge (Alg.3: rows = sweep-start
+ * state + summed changes, t clamped, Q and the sums recomputed). */
 spdp_status spdp_sweep_local(spdp_ctx* ctx);
-spdp_status spdp_exchange_buffer(spdp_ctx* ctx, void** device_ptr, int64_t* count);
+spdp_status spdp_exchange_buffer(spdp_ctx* ctx, void** device_ptr, int64_t* count, int32_t* elem_bytes);
 spdp_status spdp_sweep_merge(spdp_ctx* ctx);
 /* Copy the exchange buffer to (to_device = 0) or from (to_device = 1) the
- * caller's host array of *count int32 (e.g. for a host-side all-reduce). */
-spdp_status spdp_exchange_copy(spdp_ctx* ctx, int32_t* host, int32_t to_device);
+ * caller's host array of *count elements of *elem_bytes bytes
+ * (e.g. for a host-side all-reduce). */
+spdp_status spdp_exchange_copy(spdp_ctx* ctx, void* host, int32_t to_device);
 
 /* Read the state.  Every output is optional (NULL = skip):
  *   z [N] int32, r [N] uint8: canonical token order; r is the indicator drawn
@@ -161,6 +169,54 @@ spdp_status spdp_counts(spdp_ctx* ctx, int32_t* z, uint8_t* r, int32_t* doc_topi
  * (PAPER.md:1978-2007 with Eqs.; DESIGN.md readings
  * c16, c17).  Either pointer may be NULL.  Collective. */
 spdp_status spdp_loglik(spdp_ctx* ctx, double* log_joint, double* perplexity);
+
+/* ---- Held-out evaluation ---------------------
+ *
+ * spdp_topics: the topic-word estimates of the current state, computed on
+ * the device in fp64 (identity P):
+ *   phi0 [K*V] (row-major k, w): phi0~_kw = (beta + Q_kw) / (V beta + T_k)   Eq. P:1753;
+ *   phi [I*K*V] (row-major i, k, w): phi~^i_kw = (m_ikw - a_i t_ikw)/(b_i + m_ik.)
+ *        + (b_i + a_i t_ik.)/(b_i + m_ik.) phi0~_kw   Eq. P:1754 (reading c16).
+ * Either output may be NULL; host buffers owned by the caller.  Not
+ * collective: the word-topic state is replicated, so every rank returns the
+ * same values after a sweep.  Errors: SPDP_ESTATE before spdp_load_corpus,
+ * SPDP_ENOMEM, SPDP_ECUDA. */
+spdp_status spdp_topics(spdp_ctx* ctx, double* phi0, double* phi);
+
+/* spdp_heldout: fold-in of held-out documents and the held-out perplexity of
+ * PAPER.md:1978-2007 ("test documents are documents held out in each group
+ * during training"; 10% per group in §4.1).
+ *   Tokens: num_tokens triples (group, doc, word) in canonical order, doc ids
+ *   in [0, num_docs), every document inside one group (SPDP_EINVAL otherwise).
+ *   Fold-in (reading c21; the paper does not say how theta~ of a
+ *   test document is obtained): `iterations` sweeps of collapsed Gibbs over
+ *   the held-out topics only, phi~^i frozen, p(z_p = k) ∝ (alpha_ik + n_dk^{-p})
+ *   phi~^i_{k w_p}, tokens of a document visited sequentially in canonical
+ *   order (documents are independent given phi~: exact, no staleness).
+ *   Randomness: Philox4x32-10 with key `seed`, counter (p, iteration, 1, 0)
+ *   for held-out token p; iterations are numbered from first_iteration.
+ *   z_init [num_tokens] in [0,K), or NULL: z_p = floor(x0 K / 2^32) of counter
+ *   (p, 0xFFFFFFFF, 1, 0).  z_out [num_tokens] (optional): topics after the
+ *   last iteration.  theta [num_docs*K] (optional): theta~_dk =
+ *   (n_dk + alpha_ik) / (L_d + sum_k alpha_ik) (Eq. P:1736-1740).
+ *   perplexity (optional): exp(-sum_p log sum_k theta~_dk phi~^i_{k w_p} / num_tokens)
+ *   (reading c17).  Host buffers owned by the caller.  Not collective; the
+ *   trained state is not modified.  Errors: SPDP_EINVAL, SPDP_ESTATE,
+ *   SPDP_ENOMEM, SPDP_ECUDA. */
+spdp_status spdp_heldout(spdp_ctx* ctx, int64_t num_tokens, int32_t num_docs, const int32_t* group,
+                         const int32_t* doc, const int32_t* word, uint64_t seed, int32_t first_iteration,
+                         int32_t iterations, const int32_t* z_init, int32_t* z_out, double* theta,
+                         double* perplexity);
+
+/* spdp_topic_hellinger: compare two models' topics (§4.2.6 PAPER.md:4377-4411,
+ * "re-ordered to align with the topics"; reading c22).
+ * dist [K*K] (optional): dist[k*K + k'] = H(phi0~_a[k], phi0~_b[k']) with
+ * H(p, q) = sqrt(1 - sum_w sqrt(p_w q_w)) clamped into [0, 1], fp64.
+ * perm [K] (optional): greedy minimum-distance matching (ascending distance,
+ * ties by smaller k then k'), perm[k] = matched topic of model b.
+ * Both contexts must be loaded, share K and V and live on the same device
+ * (SPDP_EINVAL otherwise).  Not collective. */
+spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t* perm);
 
 /* Diagnostics (parity tests): for n local tokens (canonical ids), the
  * normalised 2K-slot conditional (slot 2k = (k, r=1), slot 2k+1 = (k, r=0);

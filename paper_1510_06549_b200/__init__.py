@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("SPDP_LIB") or os.path.join(_HERE, "libspdp.so")   # SPDP_LIB: tuning variants
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("spdp.cu", "spdp_device.cuh", "spdp_loglik.cuh")] + [
+_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("spdp.cu", "spdp_device.cuh", "spdp_loglik.cuh", "spdp_eval.cuh")] + [
     os.path.join(_ROOT, "include", "spdp.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -34,7 +34,7 @@ _NAMES = {0: "SPDP_OK", -1: "SPDP_EINVAL", -2: "SPDP_ENOMEM", -3: "SPDP_ECUDA", 
 EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "spdp_sweep_local",
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
-           "spdp_version"]
+           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -78,10 +78,13 @@ def lib():
         sig = {
             "spdp_create": [P, P], "spdp_load_corpus": [P, I64, I32, P, P, P, P, P],
             "spdp_set_state": [P, P, P, P], "spdp_sweep": [P, I32], "spdp_sweep_local": [P],
-            "spdp_exchange_buffer": [P, P, P], "spdp_exchange_copy": [P, P, I32], "spdp_sweep_merge": [P], "spdp_counts": [P, P, P, P, P, P, P],
+            "spdp_exchange_buffer": [P, P, P, P], "spdp_exchange_copy": [P, P, I32], "spdp_sweep_merge": [P], "spdp_counts": [P, P, P, P, P, P, P],
             "spdp_loglik": [P, P, P], "spdp_debug_probs": [P, I64, P, P, P], "spdp_stats": [P, P],
             "spdp_profile": [P, I32], "spdp_timings": [P, P],
             "spdp_partition": [C.c_uint64, I32, I64, I32, P, P], "spdp_nccl_unique_id": [P],
+            "spdp_topics": [P, P, P],
+            "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
+            "spdp_topic_hellinger": [P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -172,14 +175,15 @@ def spdp_sweep_local(ctx):
 
 
 def spdp_exchange_buffer(ctx):
-    ptr, cnt = C.c_void_p(), C.c_int64()
-    _check(lib().spdp_exchange_buffer(ctx, C.byref(ptr), C.byref(cnt)), ctx)
-    return ptr.value, cnt.value
+    """(device pointer, element count, element bytes): packed dm*2^B + dt per cell (B = 16 or 32)."""
+    ptr, cnt, eb = C.c_void_p(), C.c_int64(), C.c_int32()
+    _check(lib().spdp_exchange_buffer(ctx, C.byref(ptr), C.byref(cnt), C.byref(eb)), ctx)
+    return ptr.value, cnt.value, eb.value
 
 
 def spdp_exchange_copy(ctx, host, to_device):
-    """host: contiguous int32 numpy array of spdp_exchange_buffer()[1] elements."""
-    assert host.dtype == np.int32 and host.flags["C_CONTIGUOUS"]
+    """host: contiguous int32 (4-byte elements) or int64 numpy array of spdp_exchange_buffer()[1] elements."""
+    assert host.dtype in (np.int32, np.int64) and host.flags["C_CONTIGUOUS"]
     _check(lib().spdp_exchange_copy(ctx, _p(host), int(bool(to_device))), ctx)
     return host
 
@@ -205,6 +209,35 @@ def spdp_loglik(ctx, log_joint=True, perplexity=True):
     lj, pp = C.c_double(np.nan), C.c_double(np.nan)
     _check(lib().spdp_loglik(ctx, C.byref(lj) if log_joint else None, C.byref(pp) if perplexity else None), ctx)
     return (lj.value if log_joint else None), (pp.value if perplexity else None)
+
+
+def spdp_topics(ctx, I, V, K, phi0=True, phi=True):
+    """(phi0 [K,V], phi [I,K,V]) fp64 estimates, or None for a skipped one."""
+    p0 = np.zeros((K, V)) if phi0 else None
+    p = np.zeros((I, K, V)) if phi else None
+    _check(lib().spdp_topics(ctx, _p(p0), _p(p)), ctx)
+    return p0, p
+
+
+def spdp_heldout(ctx, K, group, doc, word, num_docs, seed, iterations, first_iteration=0, z_init=None,
+                 want_z=True, want_theta=False):
+    """Fold-in + held-out perplexity (NEXT-1).  Returns dict(perplexity, z, theta)."""
+    g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
+    w = np.ascontiguousarray(word, np.int32)
+    zi = None if z_init is None else np.ascontiguousarray(z_init, np.int32)
+    zo = np.zeros(len(w), np.int32) if want_z else None
+    th = np.zeros((int(num_docs), K)) if want_theta else None
+    ppl = C.c_double(np.nan)
+    _check(lib().spdp_heldout(ctx, len(w), int(num_docs), _p(g), _p(d), _p(w), int(seed) & (2**64 - 1),
+                              int(first_iteration), int(iterations), _p(zi), _p(zo), _p(th), C.byref(ppl)), ctx)
+    return {"perplexity": ppl.value, "z": zo, "theta": th}
+
+
+def spdp_topic_hellinger(ctx_a, ctx_b, K):
+    """(dist [K,K], perm [K]): Hellinger distances of phi0~ rows and the greedy alignment."""
+    dist = np.zeros((K, K)); perm = np.zeros(K, np.int32)
+    _check(lib().spdp_topic_hellinger(ctx_a, ctx_b, _p(dist), _p(perm)), ctx_a)
+    return dist, perm
 
 
 def spdp_debug_probs(ctx, tok_ids, K):
@@ -265,11 +298,12 @@ class Sampler:
         return spdp_exchange_buffer(self.ctx)
 
     def exchange_get(self):
-        _, n = spdp_exchange_buffer(self.ctx)
-        return spdp_exchange_copy(self.ctx, np.zeros(n, np.int32), False)
+        _, n, eb = spdp_exchange_buffer(self.ctx)
+        return spdp_exchange_copy(self.ctx, np.zeros(n, np.int32 if eb == 4 else np.int64), False)
 
     def exchange_put(self, host):
-        spdp_exchange_copy(self.ctx, np.ascontiguousarray(host, np.int32), True)
+        _, n, eb = spdp_exchange_buffer(self.ctx)
+        spdp_exchange_copy(self.ctx, np.ascontiguousarray(host, np.int32 if eb == 4 else np.int64), True)
 
     def sweep_merge(self):
         spdp_sweep_merge(self.ctx)
@@ -288,6 +322,16 @@ class Sampler:
 
     def debug_probs(self, tok_ids):
         return spdp_debug_probs(self.ctx, tok_ids, self.K)
+
+    def topics(self, phi0=True, phi=True):
+        return spdp_topics(self.ctx, self.I, self.V, self.K, phi0, phi)
+
+    def heldout(self, corpus, seed, iterations, first_iteration=0, z_init=None, want_z=True, want_theta=False):
+        return spdp_heldout(self.ctx, self.K, corpus.group, corpus.doc, corpus.word, corpus.num_docs, seed,
+                            iterations, first_iteration, z_init, want_z, want_theta)
+
+    def topic_hellinger(self, other):
+        return spdp_topic_hellinger(self.ctx, other.ctx, self.K)
 
     def stats(self):
         return spdp_stats(self.ctx)

@@ -9,6 +9,7 @@
 #include "../../include/spdp.h"
 #include "spdp_device.cuh"
 #include "spdp_loglik.cuh"
+#include "spdp_eval.cuh"
 
 #include <dlfcn.h>
 
@@ -37,7 +38,7 @@ struct NcclApi {
     int (*CommDestroy)(void*) = nullptr;
     const char* (*GetErrorString)(int) = nullptr;
 };
-constexpr int kNcclInt32 = 2, kNcclFloat64 = 8, kNcclSum = 0;
+constexpr int kNcclInt32 = 2, kNcclInt64 = 4, kNcclFloat64 = 8, kNcclSum = 0;
 
 // ------------------------------------------------------------------ host Philox4x32-10
 void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
@@ -98,6 +99,10 @@ struct spdp_ctx {
     std::vector<uint32_t> wave_seg_begin, wave_segs;   // distinct (w, i) segments of each wave
     int mmax = 0;
     size_t cells = 0;
+    // multi-GPU net change since the sweep start, packed dm*2^B + dt (B = 16: int32, else int64)
+    void *d_Dloc = nullptr, *d_Dsum = nullptr;
+    bool pack32 = true;
+    size_t dbytes() const { return cells * (pack32 ? 4 : 8); }
 
     // device
     uint32_t *d_tok_doc = nullptr, *d_tok_id = nullptr, *d_chunk_start = nullptr, *d_chunk_end = nullptr,
@@ -116,7 +121,7 @@ struct spdp_ctx {
     uint32_t* d_work = nullptr;                   // [W + 1] persistent-warp counters
     int sample_grid = 0;
     int32_t *d_m = nullptr, *d_t = nullptr, *d_Q = nullptr, *d_M = nullptr, *d_Tt = nullptr,
-            *d_T = nullptr, *d_dm = nullptr, *d_dt = nullptr, *d_D = nullptr, *d_doclen = nullptr,
+            *d_T = nullptr, *d_dm = nullptr, *d_dt = nullptr, *d_doclen = nullptr,
             *d_docgroup = nullptr;
     float *d_alpha = nullptr, *d_disc = nullptr, *d_conc = nullptr, *d_alpha_sum = nullptr;
     double *d_alpha64 = nullptr, *d_disc64 = nullptr, *d_conc64 = nullptr, *d_alpha_sum64 = nullptr;
@@ -278,14 +283,31 @@ struct TempBuf {
 };
 
 // rows += (dm, dt), clamp, zero deltas, (D += change), recompute Q and sums
-void launch_merge(spdp_ctx* c, int32_t* dm, int32_t* dt, int32_t* Dm, int32_t* Dt) {
+void launch_merge(spdp_ctx* c, int32_t* dm, int32_t* dt) {
     cudaMemsetAsync(c->d_M, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
     cudaMemsetAsync(c->d_Tt, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
     cudaMemsetAsync(c->d_T, 0, sizeof(int32_t) * (size_t)c->Kp, c->stream);
     const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
     const int use_smem = smem <= 48 * 1024;
     merge_rows_kernel<<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
-        c->d_m, c->d_t, dm, dt, Dm, Dt, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I, c->Kp, use_smem, c->d_stats);
+        c->d_m, c->d_t, dm, dt, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I, c->Kp, use_smem, c->d_stats);
+}
+
+// after the all-reduce Dloc -> Dsum: rows = S0 + sum of D, clamp, Dloc = 0, Q and sums
+void launch_exchange_merge(spdp_ctx* c) {
+    cudaMemsetAsync(c->d_M, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
+    cudaMemsetAsync(c->d_Tt, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
+    cudaMemsetAsync(c->d_T, 0, sizeof(int32_t) * (size_t)c->Kp, c->stream);
+    const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
+    const int use_smem = smem <= 48 * 1024;
+    if (c->pack32)
+        exchange_merge_kernel<int32_t><<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
+            c->d_m, c->d_t, (int32_t*)c->d_Dloc, (const int32_t*)c->d_Dsum, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I,
+            c->Kp, use_smem, c->d_stats);
+    else
+        exchange_merge_kernel<long long><<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
+            c->d_m, c->d_t, (long long*)c->d_Dloc, (const long long*)c->d_Dsum, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V,
+            c->I, c->Kp, use_smem, c->d_stats);
 }
 
 // SPDP_VERBOSE=1: phase times of spdp_load_corpus on stderr
@@ -447,8 +469,8 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     }
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
-    if (c->d_D) CU(cudaMemsetAsync(c->d_D, 0, sizeof(int32_t) * 2 * c->cells, c->stream));
-    launch_merge(c, c->d_dm, c->d_dt, nullptr, nullptr);    // zero deltas: recomputes Q and the sums
+    if (c->d_Dloc) CU(cudaMemsetAsync(c->d_Dloc, 0, c->dbytes(), c->stream));
+    launch_merge(c, c->d_dm, c->d_dt);    // zero deltas: recomputes Q and the sums
     s = check_launch(c, "install_state kernels");
     if (s) return s;
     return sync(c, "install_state");
@@ -472,8 +494,7 @@ spdp_status run_waves(spdp_ctx* c) {
     CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
     CU(cudaMemsetAsync(c->d_work, 0, sizeof(uint32_t) * ((size_t)c->W + 2), c->stream));
     if (c->profiling) { spdp_status s = ensure_events(c); if (s) return s; }
-    int32_t* Dm = c->G > 1 ? c->d_D : nullptr;
-    int32_t* Dt = c->G > 1 ? c->d_D + c->cells : nullptr;
+    void* Dnet = c->G > 1 ? c->d_Dloc : nullptr;
     for (int w = 0; w < c->W; ++w) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
         rec(c, 4 * (size_t)w);
@@ -512,7 +533,7 @@ spdp_status run_waves(spdp_ctx* c) {
             const int use_smem = smem <= 48 * 1024;
             const int blocks = (int)std::min<uint32_t>((se - sb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, c->stream>>>(
-                c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dm, Dt, c->d_Q, c->d_M,
+                c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q, c->d_M,
                 c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats);
         }
         rec(c, 4 * (size_t)w + 3);
@@ -855,7 +876,14 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_work, (size_t)W + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
     ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);
-    if (c->G > 1) ALLOC(c->d_D, 2 * c->cells);
+    if (c->G > 1) {
+        // |sum over ranks of dt| <= count(i,w) <= M_max, so 16-bit halves suffice below 2^15
+        c->pack32 = c->mmax < 32768 && !getenv("SPDP_EXCHANGE_PACK64");
+        const size_t words = c->cells * (c->pack32 ? 1 : 2);
+        int32_t *dl = nullptr, *ds = nullptr;
+        ALLOC(dl, words); ALLOC(ds, words);
+        c->d_Dloc = dl; c->d_Dsum = ds;
+    }
     ALLOC(c->d_Q, (size_t)V * Kp);
     ALLOC(c->d_M, (size_t)I * Kp); ALLOC(c->d_Tt, (size_t)I * Kp); ALLOC(c->d_T, (size_t)Kp);
     ALLOC(c->d_doclen, std::max<int32_t>(c->Dloc, 1)); ALLOC(c->d_docgroup, std::max<int32_t>(c->Dloc, 1));
@@ -968,31 +996,29 @@ spdp_status spdp_sweep_local(spdp_ctx* c) {
     spdp_status s = guard(c, true);
     if (s) return s;
     if ((s = run_waves(c))) return s;
-    if (c->G > 1) {
-        unapply_net_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_D, c->d_D + c->cells, c->cells);
-        if ((s = check_launch(c, "unapply_net_kernel"))) return s;
-    }
+    if (c->G > 1) CU(cudaMemcpyAsync(c->d_Dsum, c->d_Dloc, c->dbytes(), cudaMemcpyDeviceToDevice, c->stream));
     return sync(c, "spdp_sweep_local");
 }
 
-spdp_status spdp_exchange_buffer(spdp_ctx* c, void** ptr, int64_t* count) {
+spdp_status spdp_exchange_buffer(spdp_ctx* c, void** ptr, int64_t* count, int32_t* elem_bytes) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    if (!ptr || !count) return fail(c, SPDP_EINVAL, "null output");
+    if (!ptr || !count || !elem_bytes) return fail(c, SPDP_EINVAL, "null output");
     if (c->G == 1) return fail(c, SPDP_ESTATE, "world_size == 1 has no exchange buffer");
-    *ptr = c->d_D;
-    *count = (int64_t)(2 * c->cells);
+    *ptr = c->d_Dsum;
+    *count = (int64_t)c->cells;
+    *elem_bytes = c->pack32 ? 4 : 8;
     return SPDP_OK;
 }
 
-spdp_status spdp_exchange_copy(spdp_ctx* c, int32_t* host, int32_t to_device) {
+spdp_status spdp_exchange_copy(spdp_ctx* c, void* host, int32_t to_device) {
     spdp_status s = guard(c, true);
     if (s) return s;
     if (!host) return fail(c, SPDP_EINVAL, "null host buffer");
     if (c->G == 1) return fail(c, SPDP_ESTATE, "world_size == 1 has no exchange buffer");
-    const size_t bytes = sizeof(int32_t) * 2 * c->cells;
-    if (to_device) CU(cudaMemcpyAsync(c->d_D, host, bytes, cudaMemcpyHostToDevice, c->stream));
-    else CU(cudaMemcpyAsync(host, c->d_D, bytes, cudaMemcpyDeviceToHost, c->stream));
+    const size_t bytes = c->dbytes();
+    if (to_device) CU(cudaMemcpyAsync(c->d_Dsum, host, bytes, cudaMemcpyHostToDevice, c->stream));
+    else CU(cudaMemcpyAsync(host, c->d_Dsum, bytes, cudaMemcpyDeviceToHost, c->stream));
     return sync(c, "spdp_exchange_copy");
 }
 
@@ -1000,7 +1026,7 @@ spdp_status spdp_sweep_merge(spdp_ctx* c) {
     spdp_status s = guard(c, true);
     if (s) return s;
     if (c->G > 1) {
-        launch_merge(c, c->d_D, c->d_D + c->cells, nullptr, nullptr);
+        launch_exchange_merge(c);
         if ((s = check_launch(c, "merge (exchange)"))) return s;
     }
     if ((s = finish_sweep(c))) return s;
@@ -1019,13 +1045,13 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
         if ((s = run_waves(c))) return s;
         if (c->G > 1) {
             rec(c, 4 * (size_t)c->W);
-            unapply_net_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_D, c->d_D + c->cells, c->cells);
-            if ((s = nccl_check(c, c->nccl.AllReduce(c->d_D, c->d_D, 2 * c->cells, kNcclInt32, kNcclSum, c->comm, c->stream),
-                                "ncclAllReduce(deltas)")))
+            if ((s = nccl_check(c, c->nccl.AllReduce(c->d_Dloc, c->d_Dsum, c->cells, c->pack32 ? kNcclInt32 : kNcclInt64,
+                                                     kNcclSum, c->comm, c->stream),
+                                "ncclAllReduce(packed deltas)")))
                 return s;
-            launch_merge(c, c->d_D, c->d_D + c->cells, nullptr, nullptr);
+            launch_exchange_merge(c);
             rec(c, 4 * (size_t)c->W + 1);
-            c->launches += 2;
+            c->launches += 1;
         }
         if ((s = finish_sweep(c))) return s;
         if (c->profiling) {
@@ -1194,6 +1220,159 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
             if ((s = sync(c, "log_joint gather"))) return s;
         }
         *log_joint = total;
+    }
+    return SPDP_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-1: held-out evaluation
+namespace {
+spdp_status launch_phi_table(spdp_ctx* c, double* phi, double* phi0) {
+    const size_t cells = c->cells;
+    const int grid = (int)std::min<size_t>((cells + 255) / 256, 148u * 16u);
+    phi_table_kernel<<<std::max(grid, 1), 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T,
+                                                              c->d_disc64, c->d_conc64, c->cfg.beta,
+                                                              (double)c->V * c->cfg.beta, c->V, c->I, c->K, c->Kp,
+                                                              phi, phi0);
+    c->launches += 1;
+    return check_launch(c, "phi_table_kernel");
+}
+}  // namespace
+
+spdp_status spdp_topics(spdp_ctx* c, double* phi0, double* phi) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
+    TempBuf<double> dphi(c->cells), dphi0((size_t)K * V);
+    if (!dphi.p || !dphi0.p) return fail(c, SPDP_ENOMEM, "spdp_topics buffers");
+    if ((s = launch_phi_table(c, dphi.p, dphi0.p))) return s;
+    if (phi0) CU(cudaMemcpyAsync(phi0, dphi0.p, sizeof(double) * (size_t)K * V, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> rows;
+    if (phi) {
+        rows.resize(c->cells);
+        CU(cudaMemcpyAsync(rows.data(), dphi.p, sizeof(double) * c->cells, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if ((s = sync(c, "spdp_topics"))) return s;
+    if (phi)
+        parallel_for(V, [&](int64_t b, int64_t e) {
+            for (int64_t w = b; w < e; ++w)
+                for (int i = 0; i < I; ++i)
+                    for (int k = 0; k < K; ++k)
+                        phi[((size_t)i * K + k) * V + (size_t)w] = rows[((size_t)w * I + i) * Kp + k];
+        });
+    return SPDP_OK;
+}
+
+spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, const int32_t* group, const int32_t* doc,
+                         const int32_t* word, uint64_t seed, int32_t first_iteration, int32_t iterations,
+                         const int32_t* z_init, int32_t* z_out, double* theta, double* perplexity) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
+    if (num_tokens < 0 || num_tokens > (int64_t)UINT32_MAX || num_docs < 1 || iterations < 0 || first_iteration < 0 ||
+        (num_tokens > 0 && (!group || !doc || !word)))
+        return fail(c, SPDP_EINVAL, "spdp_heldout: bad sizes or null token arrays");
+    // group tokens by document (stable: canonical order inside each document)
+    std::vector<uint32_t> ptr((size_t)num_docs + 1, 0);
+    std::vector<int32_t> dgroup((size_t)num_docs, -1);
+    for (int64_t p = 0; p < num_tokens; ++p) {
+        const int32_t d = doc[p], g = group[p], w = word[p];
+        if (d < 0 || d >= num_docs || g < 0 || g >= I || w < 0 || w >= V)
+            return fail(c, SPDP_EINVAL, "spdp_heldout: token %lld out of range", (long long)p);
+        if (z_init && (z_init[p] < 0 || z_init[p] >= K)) return fail(c, SPDP_EINVAL, "spdp_heldout: z_init out of range");
+        if (dgroup[(size_t)d] >= 0 && dgroup[(size_t)d] != g)
+            return fail(c, SPDP_EINVAL, "spdp_heldout: document %d spans groups", d);
+        dgroup[(size_t)d] = g;
+        ptr[(size_t)d + 1]++;
+    }
+    for (int32_t d = 0; d < num_docs; ++d) {
+        ptr[(size_t)d + 1] += ptr[(size_t)d];
+        if (dgroup[(size_t)d] < 0) dgroup[(size_t)d] = 0;
+    }
+    std::vector<uint32_t> fill(ptr.begin(), ptr.end() - 1), id((size_t)num_tokens);
+    std::vector<int32_t> wsorted((size_t)num_tokens), zsorted((size_t)num_tokens, 0);
+    for (int64_t p = 0; p < num_tokens; ++p) {
+        const uint32_t q = fill[(size_t)doc[p]]++;
+        id[q] = (uint32_t)p;
+        wsorted[q] = word[p];
+        if (z_init) zsorted[q] = z_init[p];
+    }
+    const size_t nh = (size_t)std::max<int64_t>(num_tokens, 1);
+    TempBuf<double> dphi(c->cells), dpart((size_t)num_docs), dscal(1);
+    TempBuf<int32_t> dword(nh), dz(nh), dgrp((size_t)num_docs);
+    TempBuf<uint32_t> did(nh), dptr((size_t)num_docs + 1);
+    TempBuf<double> dtheta(theta ? (size_t)num_docs * K : 1);
+    if (!dphi.p || !dpart.p || !dscal.p || !dword.p || !dz.p || !dgrp.p || !did.p || !dptr.p || !dtheta.p)
+        return fail(c, SPDP_ENOMEM, "spdp_heldout buffers");
+    if ((s = launch_phi_table(c, dphi.p, nullptr))) return s;
+    CU(cudaMemcpyAsync(dword.p, wsorted.data(), sizeof(int32_t) * (size_t)num_tokens, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(dz.p, zsorted.data(), sizeof(int32_t) * (size_t)num_tokens, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(did.p, id.data(), sizeof(uint32_t) * (size_t)num_tokens, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(dptr.p, ptr.data(), sizeof(uint32_t) * ptr.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(dgrp.p, dgroup.data(), sizeof(int32_t) * dgroup.size(), cudaMemcpyHostToDevice, c->stream));
+    FoldinArgs a;
+    a.word = dword.p; a.id = did.p; a.doc_ptr = dptr.p; a.doc_group = dgrp.p; a.z = dz.p; a.phi = dphi.p;
+    a.alpha = c->d_alpha64; a.alpha_sum = c->d_alpha_sum64; a.theta = theta ? dtheta.p : nullptr; a.partial = dpart.p;
+    a.Dh = num_docs; a.I = I; a.K = K; a.Kp = Kp;
+    a.key0 = (uint32_t)seed; a.key1 = (uint32_t)(seed >> 32);
+    a.first_iter = first_iteration; a.iters = iterations; a.init = z_init ? 0 : 1;
+    const int warps = 8;
+    const size_t smem = sizeof(int) * (size_t)warps * Kp;
+    const int grid = (int)std::min<int64_t>((num_docs + warps - 1) / warps, 148 * 8);
+    const int kb = (K + 31) / 32;
+#define SPDP_FOLDIN(KB) foldin_kernel<KB><<<grid, warps * 32, smem, c->stream>>>(a)
+    if (kb <= 1) SPDP_FOLDIN(1);
+    else if (kb <= 2) SPDP_FOLDIN(2);
+    else if (kb <= 4) SPDP_FOLDIN(4);
+    else if (kb <= 8) SPDP_FOLDIN(8);
+    else if (kb <= 16) SPDP_FOLDIN(16);
+    else SPDP_FOLDIN(32);
+#undef SPDP_FOLDIN
+    reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(dpart.p, (size_t)num_docs, dscal.p);
+    c->launches += 2;
+    if ((s = check_launch(c, "foldin_kernel"))) return s;
+    double ll = 0.0;
+    CU(cudaMemcpyAsync(&ll, dscal.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (z_out) CU(cudaMemcpyAsync(zsorted.data(), dz.p, sizeof(int32_t) * (size_t)num_tokens, cudaMemcpyDeviceToHost, c->stream));
+    if (theta) CU(cudaMemcpyAsync(theta, dtheta.p, sizeof(double) * (size_t)num_docs * K, cudaMemcpyDeviceToHost, c->stream));
+    if ((s = sync(c, "spdp_heldout"))) return s;
+    if (z_out)
+        for (size_t q = 0; q < (size_t)num_tokens; ++q) z_out[id[q]] = zsorted[q];
+    if (perplexity) *perplexity = num_tokens > 0 ? std::exp(-ll / (double)num_tokens) : 1.0;
+    return SPDP_OK;
+}
+
+spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t* perm) {
+    spdp_status s = guard(a, true);
+    if (s) return s;
+    if ((s = guard(b, true))) return fail(a, s, "spdp_topic_hellinger: second context: %s", b ? b->err.c_str() : "null");
+    spdp_ctx* c = a;
+    if (a->K != b->K || a->V != b->V) return fail(c, SPDP_EINVAL, "spdp_topic_hellinger: K or V differ");
+    if (a->cfg.device != b->cfg.device) return fail(c, SPDP_EINVAL, "spdp_topic_hellinger: contexts on different devices");
+    if (!dist && !perm) return SPDP_OK;
+    const int K = a->K, V = a->V;
+    CU(cudaStreamSynchronize(b->stream));
+    TempBuf<double> sa((size_t)K * V), sb((size_t)K * V), dd((size_t)K * K);
+    if (!sa.p || !sb.p || !dd.p) return fail(c, SPDP_ENOMEM, "spdp_topic_hellinger buffers");
+    const int grid = (int)std::min<size_t>(((size_t)K * V + 255) / 256, 148u * 16u);
+    sqrt_phi0_kernel<<<grid, 256, 0, c->stream>>>(a->d_Q, a->d_T, a->cfg.beta, (double)V * a->cfg.beta, V, K, a->Kp, sa.p);
+    sqrt_phi0_kernel<<<grid, 256, 0, c->stream>>>(b->d_Q, b->d_T, b->cfg.beta, (double)V * b->cfg.beta, V, K, b->Kp, sb.p);
+    hellinger_kernel<<<dim3((K + 31) / 32, (K + 31) / 32), 256, 0, c->stream>>>(sa.p, sb.p, K, V, dd.p);
+    c->launches += 3;
+    if ((s = check_launch(c, "hellinger kernels"))) return s;
+    std::vector<double> h((size_t)K * K);
+    CU(cudaMemcpyAsync(h.data(), dd.p, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    if ((s = sync(c, "spdp_topic_hellinger"))) return s;
+    if (dist) std::memcpy(dist, h.data(), sizeof(double) * h.size());
+    if (perm) {
+        // greedy minimum-distance matching (reading c22): ascending (distance, k, k'), both ends free
+        std::vector<uint32_t> order((size_t)K * K);
+        for (size_t j = 0; j < order.size(); ++j) order[j] = (uint32_t)j;
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return h[x] < h[y]; });
+        std::vector<char> ur((size_t)K, 0), uc((size_t)K, 0);
+        for (uint32_t j : order) {
+            const int k = (int)(j / (uint32_t)K), kp = (int)(j % (uint32_t)K);
+            if (!ur[(size_t)k] && !uc[(size_t)kp]) { ur[(size_t)k] = uc[(size_t)kp] = 1; perm[k] = kp; }
+        }
     }
     return SPDP_OK;
 }

@@ -553,13 +553,11 @@ __global__ void apply_tokens_kernel(const uint32_t* __restrict__ tok_doc, uint16
 
 // ---------------------------------------------------------------- end of wave: rows, clamp, sums
 // For every (w, i) row: m += dm, t = clamp(t + dt) into [min(1,m), m]
-// (PAPER.md:2411-2419 correction; reading c14), dm = dt = 0; with a
-// net-change buffer (multi-GPU) D += (new - old).  Then Q_w = sum_i t, and the
+// (PAPER.md:2411-2419 correction; reading c14), dm = dt = 0.  Then Q_w = sum_i t, and the
 // marginal sums M, Tt, T are accumulated into zeroed buffers.
 // One warp per word; int4 over topics.
 __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t,
                                   int32_t* __restrict__ dm, int32_t* __restrict__ dt,
-                                  int32_t* __restrict__ Dm, int32_t* __restrict__ Dt,
                                   int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
                                   int32_t* __restrict__ T, int V, int I, int Kp, int use_smem_sums,
                                   unsigned long long* __restrict__ stats) {
@@ -584,7 +582,6 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
                 const int4 a = *reinterpret_cast<const int4*>(dm + off);
                 const int4 d = *reinterpret_cast<const int4*>(dt + off);
                 if ((a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) != 0) {
-                    const int4 om = vm, ot = vt;
                     int* pm = &vm.x; int* pt = &vt.x;
                     const int* pa = &a.x; const int* pd = &d.x;
 #pragma unroll
@@ -600,13 +597,6 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
                     *reinterpret_cast<int4*>(t + off) = vt;
                     *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
                     *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
-                    if (Dm) {
-                        int4 x = *reinterpret_cast<int4*>(Dm + off), y = *reinterpret_cast<int4*>(Dt + off);
-                        x.x += vm.x - om.x; x.y += vm.y - om.y; x.z += vm.z - om.z; x.w += vm.w - om.w;
-                        y.x += vt.x - ot.x; y.y += vt.y - ot.y; y.z += vt.z - ot.z; y.w += vt.w - ot.w;
-                        *reinterpret_cast<int4*>(Dm + off) = x;
-                        *reinterpret_cast<int4*>(Dt + off) = y;
-                    }
                 }
                 q.x += vt.x; q.y += vt.y; q.z += vt.z; q.w += vt.w;
                 const int* pm = &vm.x; const int* pt = &vt.x;
@@ -663,6 +653,69 @@ __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const 
     }
 }
 
+// Multi-GPU merge (Alg.3; reading c14/c15).
+// Each rank's net change of a cell since the sweep start, D = (dm, dt), is
+// carried as ONE integer: dm * 2^B + dt with B = 16 (int32, valid when every
+// |sum of D over ranks| < 2^15, i.e. max_{i,w} count(i,w) < 2^15) or B = 32
+// (int64).  Integer addition of packed words is the packed addition of both
+// halves (two's complement wraps cancel), so one all-reduce of the packed
+// buffer sums dm and dt at once: half the NVLink bytes of two int32 arrays.
+template <typename P> struct Packed;
+template <> struct Packed<int32_t> {
+    __device__ static void add4(int32_t* p, const int* cm, const int* ct) {
+        int4 x = *reinterpret_cast<int4*>(p);
+        x.x = (int)((unsigned)x.x + ((unsigned)cm[0] << 16) + (unsigned)ct[0]);
+        x.y = (int)((unsigned)x.y + ((unsigned)cm[1] << 16) + (unsigned)ct[1]);
+        x.z = (int)((unsigned)x.z + ((unsigned)cm[2] << 16) + (unsigned)ct[2]);
+        x.w = (int)((unsigned)x.w + ((unsigned)cm[3] << 16) + (unsigned)ct[3]);
+        *reinterpret_cast<int4*>(p) = x;
+    }
+    __device__ static void load4(const int32_t* p, int* dm, int* dt) {
+        const int4 x = *reinterpret_cast<const int4*>(p);
+        const int v[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            dt[e] = (int)(short)(v[e] & 0xFFFF);
+            dm[e] = (int)((unsigned)v[e] - (unsigned)dt[e]) >> 16;
+        }
+    }
+    __device__ static bool zero4(const int32_t* p) {
+        const int4 x = *reinterpret_cast<const int4*>(p);
+        return (x.x | x.y | x.z | x.w) == 0;
+    }
+    __device__ static void clear4(int32_t* p) { *reinterpret_cast<int4*>(p) = make_int4(0, 0, 0, 0); }
+};
+template <> struct Packed<long long> {
+    __device__ static void add4(long long* p, const int* cm, const int* ct) {
+        longlong2* q = reinterpret_cast<longlong2*>(p);
+        longlong2 a = q[0], b = q[1];
+        a.x = (long long)((unsigned long long)a.x + ((unsigned long long)(long long)cm[0] << 32) + (unsigned long long)(long long)ct[0]);
+        a.y = (long long)((unsigned long long)a.y + ((unsigned long long)(long long)cm[1] << 32) + (unsigned long long)(long long)ct[1]);
+        b.x = (long long)((unsigned long long)b.x + ((unsigned long long)(long long)cm[2] << 32) + (unsigned long long)(long long)ct[2]);
+        b.y = (long long)((unsigned long long)b.y + ((unsigned long long)(long long)cm[3] << 32) + (unsigned long long)(long long)ct[3]);
+        q[0] = a; q[1] = b;
+    }
+    __device__ static void load4(const long long* p, int* dm, int* dt) {
+        const longlong2* q = reinterpret_cast<const longlong2*>(p);
+        const longlong2 a = q[0], b = q[1];
+        const long long v[4] = {a.x, a.y, b.x, b.y};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            dt[e] = (int)(v[e] & 0xFFFFFFFFll);
+            dm[e] = (int)((long long)((unsigned long long)v[e] - (unsigned long long)(long long)dt[e]) >> 32);
+        }
+    }
+    __device__ static bool zero4(const long long* p) {
+        const longlong2* q = reinterpret_cast<const longlong2*>(p);
+        const longlong2 a = q[0], b = q[1];
+        return (a.x | a.y | b.x | b.y) == 0;
+    }
+    __device__ static void clear4(long long* p) {
+        longlong2* q = reinterpret_cast<longlong2*>(p);
+        q[0] = make_longlong2(0, 0); q[1] = make_longlong2(0, 0);
+    }
+};
+
 // ---------------------------------------------------------------- end of wave: touched rows only
 // One warp per (w, i) segment the wave touched: m += dm, t = clamp(t + dt) into
 // [min(1,m), m], dm = dt = 0; the changes are added to Q_w (int atomics) and to
@@ -672,7 +725,7 @@ __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const 
 __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nseg,
                                       int32_t* __restrict__ m, int32_t* __restrict__ t,
                                       int32_t* __restrict__ dm, int32_t* __restrict__ dt,
-                                      int32_t* __restrict__ Dm, int32_t* __restrict__ Dt,
+                                      void* __restrict__ D, int pack32,
                                       int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
                                       int32_t* __restrict__ T, int I, int Kp, int use_smem_sums,
                                       unsigned long long* __restrict__ stats) {
@@ -715,12 +768,9 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
             *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
             const int cm[4] = {vm.x - om.x, vm.y - om.y, vm.z - om.z, vm.w - om.w};
             const int ct[4] = {vt.x - ot.x, vt.y - ot.y, vt.z - ot.z, vt.w - ot.w};
-            if (Dm) {
-                int4 x = *reinterpret_cast<int4*>(Dm + off), y = *reinterpret_cast<int4*>(Dt + off);
-                x.x += cm[0]; x.y += cm[1]; x.z += cm[2]; x.w += cm[3];
-                y.x += ct[0]; y.y += ct[1]; y.z += ct[2]; y.w += ct[3];
-                *reinterpret_cast<int4*>(Dm + off) = x;
-                *reinterpret_cast<int4*>(Dt + off) = y;
+            if (D) {
+                if (pack32) Packed<int32_t>::add4(reinterpret_cast<int32_t*>(D) + off, cm, ct);
+                else Packed<long long>::add4(reinterpret_cast<long long*>(D) + off, cm, ct);
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -749,17 +799,81 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
     }
 }
 
-// Multi-GPU merge (Alg.3): restore the sweep-start state
-// S0 = L - D before the exchange ...
-__global__ void unapply_net_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t,
-                                   const int32_t* __restrict__ Dm, const int32_t* __restrict__ Dt, size_t cells) {
-    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < cells; j += (size_t)gridDim.x * blockDim.x) {
-        m[j] -= Dm[j];
-        t[j] -= Dt[j];
+// After the all-reduce (out of place: Dloc = this rank's D, Dsum = sum over
+// ranks): m = (m - dm_loc) + dm_sum, t = clamp((t - dt_loc) + dt_sum) into
+// [min(1,m), m]; Dloc = 0; Q_w = sum_i t and the marginal sums M, Tt, T into
+// zeroed buffers.  One pass over the rows; one warp per word.
+template <typename P>
+__global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t, P* __restrict__ Dloc,
+                                      const P* __restrict__ Dsum, int32_t* __restrict__ Q, int32_t* __restrict__ M,
+                                      int32_t* __restrict__ Tt, int32_t* __restrict__ T, int V, int I, int Kp,
+                                      int use_smem_sums, unsigned long long* __restrict__ stats) {
+    extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
+    int* sM = ssum;
+    int* sT = ssum + (size_t)I * Kp;
+    int* sK = ssum + (size_t)2 * I * Kp;
+    if (use_smem_sums) {
+        for (int j = threadIdx.x; j < (2 * I + 1) * Kp; j += blockDim.x) ssum[j] = 0;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    unsigned clamped = 0;
+    for (int w = blockIdx.x * wpb + (threadIdx.x >> 5); w < V; w += gridDim.x * wpb) {
+        for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
+            int4 q = make_int4(0, 0, 0, 0);
+            for (int i = 0; i < I; ++i) {
+                const size_t off = ((size_t)w * I + i) * Kp + k4;
+                int4 vm = *reinterpret_cast<const int4*>(m + off);
+                int4 vt = *reinterpret_cast<const int4*>(t + off);
+                const bool lz = Packed<P>::zero4(Dloc + off), sz = Packed<P>::zero4(Dsum + off);
+                if (!(lz && sz)) {
+                    int lm[4], lt[4], gm[4], gt[4];
+                    Packed<P>::load4(Dloc + off, lm, lt);
+                    Packed<P>::load4(Dsum + off, gm, gt);
+                    int* pm = &vm.x; int* pt = &vt.x;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int mv = pm[e] - lm[e] + gm[e];
+                        const int raw = pt[e] - lt[e] + gt[e];
+                        int tv = min(raw, mv);
+                        tv = (mv > 0) ? max(tv, 1) : 0;
+                        clamped += (tv != raw);
+                        pm[e] = mv; pt[e] = tv;
+                    }
+                    *reinterpret_cast<int4*>(m + off) = vm;
+                    *reinterpret_cast<int4*>(t + off) = vt;
+                    if (!lz) Packed<P>::clear4(Dloc + off);
+                }
+                q.x += vt.x; q.y += vt.y; q.z += vt.z; q.w += vt.w;
+                const int* pm = &vm.x; const int* pt = &vt.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (pm[e]) {
+                        if (use_smem_sums) { atomicAdd(sM + (size_t)i * Kp + k4 + e, pm[e]); atomicAdd(sT + (size_t)i * Kp + k4 + e, pt[e]); }
+                        else { atomicAdd(M + (size_t)i * Kp + k4 + e, pm[e]); atomicAdd(Tt + (size_t)i * Kp + k4 + e, pt[e]); }
+                    }
+                }
+            }
+            *reinterpret_cast<int4*>(Q + (size_t)w * Kp + k4) = q;
+            const int* pq = &q.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (pq[e]) { if (use_smem_sums) atomicAdd(sK + k4 + e, pq[e]); else atomicAdd(T + k4 + e, pq[e]); }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) clamped += __shfl_xor_sync(0xffffffffu, clamped, off);
+    if (lane == 0 && clamped) atomicAdd(stats + 2, (unsigned long long)clamped);
+    if (use_smem_sums) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < I * Kp; j += blockDim.x) {
+            if (sM[j]) atomicAdd(M + j, sM[j]);
+            if (sT[j]) atomicAdd(Tt + j, sT[j]);
+        }
+        for (int j = threadIdx.x; j < Kp; j += blockDim.x) if (sK[j]) atomicAdd(T + j, sK[j]);
     }
 }
-// ... and after it: m = S0 + sum_g D_g, t likewise, through merge_rows_kernel
-// with (dm, dt) = the all-reduced D.
 
 __global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
 

@@ -126,10 +126,13 @@ def test_set_state_roundtrip_with_tables():
     assert_counts_equal(hc, st, keys=("z", "n", "m", "t", "Q"))
 
 
-@pytest.mark.parametrize("G,waves", [(2, 1), (3, 2), (8, 1)])
-def test_multi_rank_exchange_matches_oracle_shards(G, waves):
-    """G ranks as G contexts on one GPU with the external exchange (host sum):
-    bit-exact against the oracle's G-shard simulation (reading c13-c15)."""
+@pytest.mark.parametrize("G,waves,pack", [(2, 1, 32), (3, 2, 32), (8, 1, 32), (2, 1, 64), (3, 2, 64)])
+def test_multi_rank_exchange_matches_oracle_shards(G, waves, pack, monkeypatch):
+    """G ranks as G contexts on one GPU with the external exchange (host sum of
+    the packed dm*2^B + dt buffers, B = 16 and 32): bit-exact against the
+    oracle's G-shard simulation (reading c13-c15)."""
+    if pack == 64:
+        monkeypatch.setenv("SPDP_EXCHANGE_PACK64", "1")
     c = corpus("C1")
     ranks = [spdp.sampler_for(c, 10, num_waves=waves, rank=r, world_size=G,
                               exchange=spdp.SPDP_EXCHANGE_EXTERNAL, **HYPER) for r in range(G)]
@@ -137,7 +140,10 @@ def test_multi_rank_exchange_matches_oracle_shards(G, waves):
     for s in range(3):
         for r in ranks:
             r.sweep_local()
-        tot = sum(r.exchange_get().astype(np.int64) for r in ranks).astype(np.int32)
+        bufs = [r.exchange_get() for r in ranks]
+        assert bufs[0].dtype == (np.int32 if pack == 32 else np.int64)
+        with np.errstate(over="ignore"):
+            tot = sum(b.astype(np.int64) for b in bufs).astype(bufs[0].dtype)   # wrapping integer sum
         for r in ranks:
             r.exchange_put(tot)
             r.sweep_merge()
