@@ -40,6 +40,10 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=0)
+    ap.add_argument("--mode", default="sweep", choices=["sweep", "heldout"],
+                    help="heldout: NEXT-1 fold-in + held-out perplexity of the 10%% hold-out (separate line)")
+    ap.add_argument("--foldin-iters", type=int, default=20)
+    ap.add_argument("--train-sweeps", type=int, default=20)
     return ap.parse_args()
 
 
@@ -123,11 +127,15 @@ def plan_stats(corpus, shard_docs, waves):
     return {"tokens": int(doc.shape[0]), "segments": int(np.unique(key).shape[0])}
 
 
-def load_traffic(cfg_name, K):
-    p = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}_K{K}_sample.json")
-    if os.path.exists(p):
-        with open(p) as f:
+def load_traffic(cfg_name, K, kernel="sample"):
+    """DRAM bytes per launch from the latest round's committed ncu --set full summary."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{cfg_name}_K{K}_{kernel}.json")))
+    if paths:
+        with open(paths[-1]) as f:
             d = json.load(f)
+        if isinstance(d, list):
+            d = d[0]
         return d.get("dram_bytes_per_launch")
     return None
 
@@ -170,6 +178,8 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, cfg, K, world, rank, workload)
+    if args.mode == "heldout":
+        return run_heldout(args, cfg, K, workload)
 
     import torch
     import torch.distributed as dist
@@ -292,6 +302,64 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_heldout(args, cfg, K, workload):
+    """NEXT-1 measurement (one GPU): train on 90% of the corpus, then time
+    spdp_heldout (fold-in of the held-out 10% per group + held-out perplexity,
+    DESIGN.md §11) per step; the fold-in kernel's own CUDA-event time gives the
+    roofline (fp64 phi~ row of 8K bytes + 16 B of token record per
+    token-iteration, plus one 8K-byte row per token for the likelihood pass)."""
+    import torch
+    import paper_1510_06549_b200 as spdp
+    import synth
+    spdp.build()
+    torch.cuda.set_device(0)
+    train, test = synth.holdout_split(synth.corpus_for(cfg), 0.1, seed=1)
+    stream = torch.cuda.current_stream()
+    g = spdp.Sampler(cfg.groups, cfg.vocab, K, alpha=cfg.alpha, beta=cfg.beta, discount=cfg.discount,
+                     concentration=cfg.concentration, seed=cfg.seed, num_waves=args.waves, stream=stream.cuda_stream)
+    g.load_corpus(train.group, train.doc, train.word, train.num_docs)
+    g.sweep(args.train_sweeps)
+    F = args.foldin_iters
+    for s_ in range(args.warmup):
+        g.heldout(test, 1000 + s_, F, want_z=False)
+    g.profile(True)
+    torch.cuda.synchronize()
+    ms, ppl = [], []
+    with ClockSampler(0) as clk:
+        for s_ in range(args.steps):
+            t0 = time.perf_counter()
+            r = g.heldout(test, s_, F, want_z=False)          # host prep + H2D + phi table + fold-in + D2H
+            ms.append((time.perf_counter() - t0) * 1e3)
+            ppl.append(r["perplexity"])
+    tm = g.timings()
+    _, train_ppl = g.loglik(log_joint=False)
+    g.close()
+    Nh = test.num_tokens
+    units = Nh * F
+    kern_ms = tm["foldin_ms"] / max(args.steps, 1)
+    alg = Nh * F * (8 * K + 16) + Nh * (8 * K + 8)
+    peak, src = measured_peaks()
+    line = {
+        "metric": "held-out fold-in token-iterations/sec", "value": round(units / (float(np.mean(ms)) / 1e3), 1),
+        "unit": "token-iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(float(np.mean(ms)), 4), "higher_is_better": True, "scaling": "none",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic SPDP-generated corpus (synth/, seeded), 10% per group held out",
+        "config": {"workload": f"{workload} | train {train.num_tokens} tokens x {args.train_sweeps} sweeps, "
+                               f"held-out {Nh} tokens / {test.num_docs} docs x {F} fold-in iterations",
+                   "timing": "wall clock per spdp_heldout call (host prep, H2D, phi table, fold-in, reduce, D2H)"},
+        "kernel_ms_per_step": round(kern_ms, 4),
+        "kernel_value": round(units / (kern_ms / 1e3), 1) if kern_ms > 0 else None,
+        "roofline": {"bound": "hbm", "achieved": round(alg / (kern_ms / 1e3) / 1e9, 1) if kern_ms > 0 else None,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": round(alg / (kern_ms / 1e3) / 1e9 / peak, 4) if kern_ms > 0 else None,
+                     "traffic": load_traffic(cfg.name, K, "foldin"), "kernel": "foldin_kernel",
+                     "alg_bytes_per_launch": int(alg), "peak_source": src},
+        "heldout_perplexity": round(float(np.mean(ppl)), 4), "train_perplexity": round(train_ppl, 4),
+        "clocks": clk.summary(), "gpu_launches": int(tm["launches"]),
+    }
+    print(json.dumps(line), flush=True)
 
 
 def run_reference(args, cfg, K, world, rank, workload):

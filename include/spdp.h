@@ -235,11 +235,12 @@ spdp_status spdp_stats(spdp_ctx* ctx, int64_t* out);
 
 /* Phase timing with CUDA events recorded on the context's stream around each
  * launch of the sweep (enable = 1 resets the accumulators and starts;
- * 0 stops).  spdp_timings fills out[8] with totals since the reset:
- * out[0] sample-kernel ms, out[1] token-apply ms, out[2] row-merge ms,
- * out[3] exchange ms (unapply + all-reduce + merge), out[4] whole-sweep ms,
- * out[5] sample-kernel launches, out[6] kernel launches of all kinds,
- * out[7] sweeps timed. */
+ * 0 stops).  spdp_timings fills out[10] with totals since the reset:
+ * out[0] sample-kernel ms, out[1] token-apply / doc-recount ms, out[2]
+ * row-merge ms, out[3] exchange ms (all-reduce + merge), out[4] whole-sweep
+ * ms, out[5] sample-kernel launches, out[6] kernel launches of all kinds,
+ * out[7] sweeps timed, out[8] fold-in kernel ms (spdp_heldout), out[9]
+ * fold-in token-iterations. */
 spdp_status spdp_profile(spdp_ctx* ctx, int32_t enable);
 spdp_status spdp_timings(spdp_ctx* ctx, double* out);
 

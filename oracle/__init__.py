@@ -81,7 +81,7 @@ def lib():
         L.or_phi.restype = C.c_double
         L.or_topics.argtypes = [P, P, P]
         L.or_topics.restype = None
-        L.or_foldin.argtypes = [P, C.c_int64, C.c_int32, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.c_int, P, P, P]
+        L.or_foldin.argtypes = [P, C.c_int64, C.c_int32, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.c_int, P, P, P, P]
         L.or_heldout_perplexity.argtypes = [P, C.c_int64, C.c_int32, P, P, P, P, P]
         L.or_heldout_perplexity.restype = C.c_double
         L.or_hellinger.argtypes = [C.c_int64, P, P]
@@ -240,18 +240,21 @@ class Oracle:
 
     def foldin(self, group, doc, word, num_docs, seed, iterations, first_iteration=0, z=None,
                force_z=None, want_margin=False):
-        """Fold-in (reading c21).  z None: Philox initial topics.  Returns z (and margins)."""
+        """Fold-in (reading c21).  z None: Philox initial topics.  Returns z, or with
+        want_margin (z, margins, own draws before forcing)."""
         g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
         w = np.ascontiguousarray(word, np.int32)
         init = z is None
         zz = np.full(len(g), -1, np.int32) if init else np.array(z, np.int32, copy=True)
         fz = None if force_z is None else np.ascontiguousarray(force_z, np.int32)
         mg = np.zeros(len(g)) if want_margin else None
+        own = np.zeros(len(g), np.int32) if want_margin else None
         rc = lib().or_foldin(self.h, len(g), int(num_docs), _ptr(g), _ptr(d), _ptr(w), int(seed) & (2**64 - 1),
-                             int(first_iteration), int(iterations), int(init), _ptr(zz), _ptr(fz), _ptr(mg))
+                             int(first_iteration), int(iterations), int(init), _ptr(zz), _ptr(fz), _ptr(mg),
+                             _ptr(own))
         if rc != 0:
             raise RuntimeError(f"or_foldin failed ({rc})")
-        return (zz, mg) if want_margin else zz
+        return (zz, mg, own) if want_margin else zz
 
     def heldout_perplexity(self, group, doc, word, num_docs, z, want_theta=False):
         g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)

@@ -818,10 +818,11 @@ double or_phi(const ostate *s, int i, int k, int w) {
  * the draw is k* = min{k : cdf_k > u} (reading c10 with K slots).
  * Initial z (z in/out holds -1 entries or a state): when init != 0,
  * z_p = floor(x0 K / 2^32) of Philox(seed; p, 0xFFFFFFFF, 1, 0).
- * force_z / margin: lock-step testing as in or_sweep_par. */
+ * force_z / margin / own: lock-step testing as in or_sweep_par (own = the
+ * oracle's draw before it is replaced by force_z). */
 int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
               const int32_t *word, uint64_t seed, int32_t first_iter, int32_t iters, int init, int32_t *z,
-              const int32_t *force_z, double *margin) {
+              const int32_t *force_z, double *margin, int32_t *own) {
     int K = s->K;
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     for (int64_t p = 0; p < Nh; p++) {
@@ -852,6 +853,7 @@ int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, con
             double mg = 0.0;
             int k_new = draw_slot(K, prob, u53(x), &mg);
             if (margin) margin[p] = mg;
+            if (own) own[p] = k_new;
             if (force_z) k_new = force_z[p];
             z[p] = k_new;
             n[(size_t)d * K + k_new]++;

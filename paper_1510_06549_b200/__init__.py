@@ -260,9 +260,10 @@ def spdp_profile(ctx, enable=True):
 
 
 def spdp_timings(ctx):
-    out = np.zeros(8)
+    out = np.zeros(10)
     _check(lib().spdp_timings(ctx, _p(out)), ctx)
-    keys = ["sample_ms", "apply_ms", "merge_ms", "exchange_ms", "sweep_ms", "sample_launches", "launches", "sweeps"]
+    keys = ["sample_ms", "apply_ms", "merge_ms", "exchange_ms", "sweep_ms", "sample_launches", "launches", "sweeps",
+            "foldin_ms", "foldin_token_iters"]
     return dict(zip(keys, (float(x) for x in out)))
 
 

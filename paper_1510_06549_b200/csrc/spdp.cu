@@ -136,7 +136,7 @@ struct spdp_ctx {
     // profiling (spdp_profile)
     bool profiling = false;
     std::vector<cudaEvent_t> ev;          // 4 per wave + 2 for the exchange
-    double acc[8] = {0};
+    double acc[10] = {0};
     int64_t launches = 0;
 };
 
@@ -1319,6 +1319,11 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
     const size_t smem = sizeof(int) * (size_t)warps * Kp;
     const int grid = (int)std::min<int64_t>((num_docs + warps - 1) / warps, 148 * 8);
     const int kb = (K + 31) / 32;
+    cudaEvent_t fe[2] = {nullptr, nullptr};
+    if (c->profiling) {
+        CU(cudaEventCreate(&fe[0])); CU(cudaEventCreate(&fe[1]));
+        CU(cudaEventRecord(fe[0], c->stream));
+    }
 #define SPDP_FOLDIN(KB) foldin_kernel<KB><<<grid, warps * 32, smem, c->stream>>>(a)
     if (kb <= 1) SPDP_FOLDIN(1);
     else if (kb <= 2) SPDP_FOLDIN(2);
@@ -1327,6 +1332,7 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
     else if (kb <= 16) SPDP_FOLDIN(16);
     else SPDP_FOLDIN(32);
 #undef SPDP_FOLDIN
+    if (c->profiling) CU(cudaEventRecord(fe[1], c->stream));
     reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(dpart.p, (size_t)num_docs, dscal.p);
     c->launches += 2;
     if ((s = check_launch(c, "foldin_kernel"))) return s;
@@ -1335,6 +1341,12 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
     if (z_out) CU(cudaMemcpyAsync(zsorted.data(), dz.p, sizeof(int32_t) * (size_t)num_tokens, cudaMemcpyDeviceToHost, c->stream));
     if (theta) CU(cudaMemcpyAsync(theta, dtheta.p, sizeof(double) * (size_t)num_docs * K, cudaMemcpyDeviceToHost, c->stream));
     if ((s = sync(c, "spdp_heldout"))) return s;
+    if (c->profiling) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, fe[0], fe[1]) == cudaSuccess) c->acc[8] += ms;
+        c->acc[9] += (double)num_tokens * iterations;
+        cudaEventDestroy(fe[0]); cudaEventDestroy(fe[1]);
+    }
     if (z_out)
         for (size_t q = 0; q < (size_t)num_tokens; ++q) z_out[id[q]] = zsorted[q];
     if (perplexity) *perplexity = num_tokens > 0 ? std::exp(-ll / (double)num_tokens) : 1.0;
@@ -1462,7 +1474,7 @@ spdp_status spdp_profile(spdp_ctx* c, int32_t enable) {
 
 spdp_status spdp_timings(spdp_ctx* c, double* out) {
     if (!c || !out) return SPDP_EINVAL;
-    for (int j = 0; j < 8; ++j) out[j] = c->acc[j];
+    for (int j = 0; j < 10; ++j) out[j] = c->acc[j];
     out[6] = (double)c->launches;
     return SPDP_OK;
 }
