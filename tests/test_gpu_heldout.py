@@ -105,7 +105,8 @@ def test_topic_hellinger_matches_oracle(name, K):
     o2 = oracle.Oracle(train.num_groups, train.vocab, K, **HYPER, seed=8)
     o2.load(train.group, train.doc, train.word, train.num_docs, z_init=gc2["z"], t_init=gc2["t"])
     d_self, p_self = g.topic_hellinger(g)
-    assert np.abs(np.diag(d_self)).max() <= 2e-8 and list(p_self) == list(range(K))
+    # H = sqrt(1 - BC) turns the ~1e-15 rounding of BC = 1 into ~1e-7
+    assert np.abs(np.diag(d_self)).max() <= 1e-6 and list(p_self) == list(range(K))
     d, p = g.topic_hellinger(g2)
     od, op = o.topic_align(o2)
     np.testing.assert_allclose(d ** 2, od ** 2, atol=1e-12)
