@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--mode", default="sweep", choices=["sweep", "heldout"],
                     help="heldout: NEXT-1 fold-in + held-out perplexity of the 10%% hold-out (separate line)")
     ap.add_argument("--foldin-iters", type=int, default=20)
+    ap.add_argument("--update", default="wave", choices=["wave", "async"],
+                    help="async: NEXT-2, the paper's immediate-update in-GPU scheme (nondeterministic)")
     ap.add_argument("--train-sweeps", type=int, default=20)
     return ap.parse_args()
 
@@ -174,7 +176,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     workload = f"{cfg.name}: I={cfg.groups} groups x {cfg.docs_per_group} docs, mean len {cfg.mean_len}, " \
-               f"V={cfg.vocab}, K={K}, W={args.waves}"
+               f"V={cfg.vocab}, K={K}, W={args.waves}" + (", async updates (NEXT-2)" if args.update == "async" else "")
 
     if args.impl == "reference":
         return run_reference(args, cfg, K, world, rank, workload)
@@ -201,7 +203,8 @@ def main():
     stream = torch.cuda.current_stream()
     kw = dict(alpha=cfg.alpha, beta=cfg.beta, discount=cfg.discount, concentration=cfg.concentration,
               seed=cfg.seed, num_waves=args.waves, device=local_rank, rank=rank, world_size=world,
-              nccl_unique_id=uid, stream=stream.cuda_stream)
+              nccl_unique_id=uid, stream=stream.cuda_stream,
+              update_mode=spdp.SPDP_UPDATE_ASYNC if args.update == "async" else spdp.SPDP_UPDATE_WAVE)
 
     def barrier():
         if world > 1:

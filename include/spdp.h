@@ -66,6 +66,17 @@ enum {
                                     spdp_sweep_local and spdp_sweep_merge */
 };
 
+/* How a sweep updates the counts (DESIGN.md §3 reading c13, §12). */
+enum {
+    SPDP_UPDATE_WAVE = 0,   /* deterministic wave snapshots: every token of a wave decides against the
+                               wave-start counts, the wave's deltas are applied after it (default) */
+    SPDP_UPDATE_ASYNC = 1   /* the paper's in-GPU scheme (Alg.4 PAPER.md:2973-3012;
+                               SURVEY.md §8(f) NEXT-2): live counts copied per work unit, updates applied
+                               to the global counts at once with atomics, t corrected into its valid range
+                               and the sums recomputed at the end of the sweep.  Nondeterministic;
+                               needs num_waves == 1 */
+};
+
 typedef struct {
     uint32_t struct_size;          /* = sizeof(spdp_config); ABI versioning */
     int32_t num_groups;            /* I >= 1 */
@@ -84,6 +95,7 @@ typedef struct {
     const void* nccl_unique_id;    /* 128-byte ncclUniqueId (same on every rank) for SPDP_EXCHANGE_NCCL */
     void* stream;                  /* cudaStream_t to order work on; NULL -> a stream owned by the context */
     int32_t debug_checks;          /* 1 = verify count invariants after every sweep (slow) */
+    int32_t update_mode;           /* SPDP_UPDATE_* */
 } spdp_config;
 
 /* Create a context on cfg->device.  Validates the hyper-parameters

@@ -27,6 +27,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 SPDP_OK, SPDP_EINVAL, SPDP_ENOMEM, SPDP_ECUDA, SPDP_ENCCL, SPDP_ESTATE, SPDP_ETABLE, SPDP_EINTEGRITY = 0, -1, -2, -3, -4, -5, -6, -7
 SPDP_EXCHANGE_NCCL, SPDP_EXCHANGE_EXTERNAL = 0, 1
+SPDP_UPDATE_WAVE, SPDP_UPDATE_ASYNC = 0, 1
 _NAMES = {0: "SPDP_OK", -1: "SPDP_EINVAL", -2: "SPDP_ENOMEM", -3: "SPDP_ECUDA", -4: "SPDP_ENCCL",
           -5: "SPDP_ESTATE", -6: "SPDP_ETABLE", -7: "SPDP_EINTEGRITY"}
 
@@ -61,7 +62,7 @@ class spdp_config(C.Structure):
                 ("discount", C.c_void_p), ("concentration", C.c_void_p), ("seed", C.c_uint64),
                 ("num_waves", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("exchange", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
-                ("debug_checks", C.c_int32)]
+                ("debug_checks", C.c_int32), ("update_mode", C.c_int32)]
 
 
 _lib = None
@@ -130,7 +131,7 @@ def spdp_nccl_unique_id() -> bytes:
 
 def spdp_create(num_groups, vocab_size, num_topics, alpha=0.1, beta=0.1, discount=0.7, concentration=100.0,
                 seed=7, num_waves=1, device=0, rank=0, world_size=1, exchange=SPDP_EXCHANGE_NCCL,
-                nccl_unique_id=None, stream=None, debug_checks=False, alpha_ik=None):
+                nccl_unique_id=None, stream=None, debug_checks=False, alpha_ik=None, update_mode=SPDP_UPDATE_WAVE):
     """Returns (ctx handle, keep-alive tuple)."""
     I, K = int(num_groups), int(num_topics)
     disc = np.ascontiguousarray(np.broadcast_to(np.asarray(discount, np.float64), (I,)))
@@ -140,7 +141,7 @@ def spdp_create(num_groups, vocab_size, num_topics, alpha=0.1, beta=0.1, discoun
     cfg = spdp_config(C.sizeof(spdp_config), I, int(vocab_size), K, float(alpha), _p(aik), float(beta),
                       _p(disc), _p(conc), int(seed) & (2**64 - 1), int(num_waves), int(device), int(rank),
                       int(world_size), int(exchange), C.cast(uid, C.c_void_p) if uid is not None else None,
-                      stream, int(bool(debug_checks)))
+                      stream, int(bool(debug_checks)), int(update_mode))
     h = C.c_void_p()
     code = lib().spdp_create(C.byref(cfg), C.byref(h))
     if code != SPDP_OK:

@@ -112,6 +112,7 @@ struct spdp_ctx {
     uint32_t *d_doc_ptr = nullptr, *d_doc_pos = nullptr;   // CSR: sorted-token positions of each local doc
     void* d_n = nullptr;                          // n_dk rows in sigma order: fp32 or uint16 (row16)
     bool row16 = false;                           // uint16 doc-topic rows (HBM-resident arrays)
+    bool async = false;                           // SPDP_UPDATE_ASYNC (NEXT-2): immediate count updates
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
     int colstart[8] = {0};
@@ -182,10 +183,17 @@ spdp_status nccl_check(spdp_ctx* c, int r, const char* what) {
 
 // ------------------------------------------------------------------ kernel dispatch
 template <int LPT, int KPL, bool DBG>
-void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks, bool row16) {
+void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks, bool row16, bool async) {
     const size_t smem = sample_smem_bytes<LPT, KPL>();
     const int blocks = std::min((a.nchunks + kWarps - 1) / kWarps, max_blocks);
     if (blocks <= 0) return;
+    if constexpr (!DBG) {
+        if (async) {
+            if (row16) sample_kernel<LPT, KPL, false, uint16_t, true><<<blocks, kWarps * 32, smem, s>>>(a);
+            else sample_kernel<LPT, KPL, false, float, true><<<blocks, kWarps * 32, smem, s>>>(a);
+            return;
+        }
+    }
     if (row16) sample_kernel<LPT, KPL, DBG, uint16_t><<<blocks, kWarps * 32, smem, s>>>(a);
     else sample_kernel<LPT, KPL, DBG, float><<<blocks, kWarps * 32, smem, s>>>(a);
 }
@@ -205,6 +213,8 @@ void set_attr_t() {
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, true, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, true, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int psm = kWarps * LPT * KPL * (int)sizeof(double);
     cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
     cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
@@ -234,7 +244,7 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
     }
 
 void launch_sample(spdp_ctx* c, const SweepArgs& a, bool dbg) {
-#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid, c->row16) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid, c->row16))
+#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid, c->row16, false) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid, c->row16, c->async))
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_S)
 #undef CALL_S
 }
@@ -290,7 +300,8 @@ void launch_merge(spdp_ctx* c, int32_t* dm, int32_t* dt) {
     const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
     const int use_smem = smem <= 48 * 1024;
     merge_rows_kernel<<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
-        c->d_m, c->d_t, dm, dt, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I, c->Kp, use_smem, c->d_stats);
+        c->d_m, c->d_t, dm, dt, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I, c->Kp, use_smem, c->d_stats,
+        dm == nullptr);
 }
 
 // after the all-reduce Dloc -> Dsum: rows = S0 + sum of D, clamp, Dloc = 0, Q and sums
@@ -495,6 +506,36 @@ spdp_status run_waves(spdp_ctx* c) {
     CU(cudaMemsetAsync(c->d_work, 0, sizeof(uint32_t) * ((size_t)c->W + 2), c->stream));
     if (c->profiling) { spdp_status s = ensure_events(c); if (s) return s; }
     void* Dnet = c->G > 1 ? c->d_Dloc : nullptr;
+    if (c->async) {
+        // NEXT-2: one launch with immediate updates, then the end-of-sweep correction
+        // (t into its valid range, Q and the sums recomputed: Alg.4)
+        if (c->G > 1) {                                  // sweep-start copy for the net change
+            CU(cudaMemcpyAsync(c->d_dm, c->d_m, sizeof(int32_t) * c->cells, cudaMemcpyDeviceToDevice, c->stream));
+            CU(cudaMemcpyAsync(c->d_dt, c->d_t, sizeof(int32_t) * c->cells, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        rec(c, 0);
+        a.nchunks = (int)c->chunk_seg.size();
+        a.work = c->d_work;
+        launch_sample(c, a, false);
+        rec(c, 1);
+        std::swap(c->d_zr, c->d_zr_next);
+        rec(c, 2);
+        launch_merge(c, nullptr, nullptr);
+        if (c->G > 1) {
+            const int grid = 148 * 8;
+            if (c->pack32)
+                net_change_kernel<int32_t><<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_dm, c->d_dt,
+                                                                        (int32_t*)c->d_Dloc, c->cells);
+            else
+                net_change_kernel<long long><<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_dm, c->d_dt,
+                                                                          (long long*)c->d_Dloc, c->cells);
+            c->launches += 1;
+        }
+        rec(c, 3);
+        c->launches += 2;
+        c->acc[5] += 1;
+        return check_launch(c, "async sweep");
+    }
     for (int w = 0; w < c->W; ++w) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
         rec(c, 4 * (size_t)w);
@@ -605,6 +646,9 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     if (!(cfg->beta > 0.0)) return bad("beta must be > 0");
     if (!cfg->discount || !cfg->concentration) return bad("discount and concentration arrays are required");
     if (cfg->num_waves < 1) return bad("num_waves must be >= 1");
+    if (cfg->update_mode != SPDP_UPDATE_WAVE && cfg->update_mode != SPDP_UPDATE_ASYNC) return bad("unknown update_mode");
+    if (cfg->update_mode == SPDP_UPDATE_ASYNC && cfg->num_waves != 1) return bad("SPDP_UPDATE_ASYNC needs num_waves == 1");
+    c->async = cfg->update_mode == SPDP_UPDATE_ASYNC;
     if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return bad("rank / world_size out of range");
     c->I = cfg->num_groups; c->V = cfg->vocab_size; c->K = cfg->num_topics;
     c->Kp = (c->K + 3) & ~3; c->W = cfg->num_waves; c->rank = cfg->rank; c->G = cfg->world_size;

@@ -132,9 +132,45 @@ __device__ __forceinline__ void removal_factors(int rrem, int mv, int tv, int Mv
 // L2) or as uint16 (half the bytes when the rows stream from HBM; n_dk <= L_d < 2^16).
 template <typename NT>
 struct Row;
+// Coherent loads for the async mode (NEXT-2): the counts change while the
+// kernel runs, so they are read with ld.relaxed.gpu (L2, never the
+// non-coherent path of __ldg).
+__device__ __forceinline__ int ld_relaxed(const int32_t* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float4 ld_relaxed_f4(const float* p) {
+    float4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_relaxed_f(const float* p) {
+    float v;
+    asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_relaxed_u2(const void* p) {
+    uint2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ unsigned short ld_relaxed_u16(const uint16_t* p) {
+    unsigned short v;
+    asm volatile("ld.relaxed.gpu.global.b16 %0, [%1];" : "=h"(v) : "l"(p));
+    return v;
+}
+template <bool AS>
+__device__ __forceinline__ int ldc(const int32_t* p) {   // count read: snapshot (wave mode) or live (async)
+    if constexpr (AS) return ld_relaxed(p);
+    else return *p;
+}
+
 template <>
 struct Row<float> {
     __device__ __forceinline__ static float4 load4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+    __device__ __forceinline__ static float4 load4_live(const float* p) { return ld_relaxed_f4(p); }
+    __device__ __forceinline__ static float load1_live(const float* p) { return ld_relaxed_f(p); }
     __device__ __forceinline__ static float load1(const float* p) { return __ldg(p); }
     __device__ __forceinline__ static void add(float* base, size_t idx, int d) { atomicAdd(base + idx, (float)d); }
     __device__ __forceinline__ static void store(float* p, int v) { *p = (float)v; }
@@ -154,6 +190,11 @@ struct Row<uint16_t> {
         const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
         return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y));
     }
+    __device__ __forceinline__ static float4 load4_live(const uint16_t* p) {
+        const uint2 v = ld_relaxed_u2(p);
+        return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y));
+    }
+    __device__ __forceinline__ static float load1_live(const uint16_t* p) { return (float)ld_relaxed_u16(p); }
     __device__ __forceinline__ static float load1(const uint16_t* p) { return (float)__ldg(p); }
     // +-1 on one half of the containing 32-bit word (a half never leaves [0, L_d], no carry)
     __device__ __forceinline__ static void add(uint16_t* base, size_t idx, int d) {
@@ -248,7 +289,25 @@ __device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
 //     the r split by the exact r = 1 share; outputs and count deltas (a7).
 //   Every CDF boundary is an fp64 sum of fp32 partial sums of few terms
 //   (a few fp32 ulps of the total), inside the 1e-6 band of north_star (5).
-template <int LPT, int KPL, bool DEBUG, typename NT>
+template <typename NT, bool AS>
+__device__ __forceinline__ float4 row_load4(const NT* p) {
+    if constexpr (AS) return Row<NT>::load4_live(p);
+    else return Row<NT>::load4(p);
+}
+template <typename NT, bool AS>
+__device__ __forceinline__ float row_load1(const NT* p) {
+    if constexpr (AS) return Row<NT>::load1_live(p);
+    else return Row<NT>::load1(p);
+}
+
+// ASYNC (the paper's in-GPU scheme P:2210-2233 / Alg.4
+// P:2973-3012): no wave snapshot.  A chunk copies the live counts of its
+// segment when it starts ("local copy ... at the beginning of each thread"),
+// corrects the copy into the valid range (Alg.4 "correct local counts copied
+// ... to ensure they are in valid range"), reads doc-topic rows live, and
+// applies its updates to the global counts at once: n per token (atomics),
+// m, t, Q and the sums per chunk (atomics).  Nondeterministic by design.
+template <int LPT, int KPL, bool DEBUG, typename NT, bool ASYNC = false>
 __global__ void __launch_bounds__(kWarps * 32, SPDP_MINB)
 sample_kernel(SweepArgs A) {
     constexpr int TPW = 32 / LPT;
@@ -287,10 +346,15 @@ sample_kernel(SweepArgs A) {
         float F0 = 0.f, F1 = 0.f, al = 0.f;
         int mv = 0, tv = 0;
         if (k < K) {
-            mv = A.m[row + k];
-            tv = A.t[row + k];
+            mv = ldc<ASYNC>(A.m + row + k);
+            tv = ldc<ASYNC>(A.t + row + k);
+            if constexpr (ASYNC) {                    // valid range of the local copy (reading c14)
+                mv = max(mv, 0);
+                tv = mv > 0 ? min(max(tv, 1), mv) : 0;
+            }
             al = alpha_i[k];
-            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+            slot_factors(ldc<ASYNC>(Mi + k), ldc<ASYNC>(Tti + k), ldc<ASYNC>(Qw + k), ldc<ASYNC>(A.T + k),
+                         tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
         }
         const float Fk = F0 + F1;
         S.F[k] = Fk;
@@ -340,8 +404,10 @@ sample_kernel(SweepArgs A) {
         const int rrem = removal_draw(x0, m0, t0);                                            // a3
         const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
         float Fk0 = 0.f, R1k0 = 0.f;                    // topic k0's factors after the own removal
-        if (mine) removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
-        const float n0 = mine ? Row<NT>::load1(nrow + A.sigma[k0]) : 0.f;
+        if (mine) removal_factors(rrem, m0, t0, ldc<ASYNC>(Mi + k0), ldc<ASYNC>(Tti + k0), ldc<ASYNC>(Qw + k0),
+                                  ldc<ASYNC>(A.T + k0), tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        float n0 = mine ? row_load1<NT, ASYNC>(nrow + A.sigma[k0]) : 0.f;
+        if constexpr (ASYNC) n0 = fmaxf(n0, 1.f);    // the token itself is counted in its row
         const float al0 = alpha_i[k0];
         const float wold = __fmaf_rn(n0, S.F[k0], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
         const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
@@ -357,7 +423,7 @@ sample_kernel(SweepArgs A) {
             const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + snoff + 4 * gl;
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = Row<NT>::load4(nl + 4 * A.colstart[q]);
+            for (int q = 0; q < NB; ++q) v[q] = row_load4<NT, ASYNC>(nl + 4 * A.colstart[q]);
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -434,7 +500,7 @@ sample_kernel(SweepArgs A) {
                 int cs = 0;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) if (q == qs) cs = A.colstart[q];
-                const float4 n4 = Row<NT>::load4(nrow + 4 * (cs + wg));
+                const float4 n4 = row_load4<NT, ASYNC>(nrow + 4 * (cs + wg));
                 const float4 F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
                 const float4 a4 = *reinterpret_cast<const float4*>(&S.aF[skew<KPL>(kq)]);
                 float wq[4] = {__fmaf_rn(n4.x, F4.x, a4.x), __fmaf_rn(n4.y, F4.y, a4.y),
@@ -460,8 +526,8 @@ sample_kernel(SweepArgs A) {
                 float R1s = R1k0;
                 if (!own) {                                // r = 1 share of topic ks at the snapshot
                     float f0, f1;
-                    slot_factors(Mi[ks], Tti[ks], Qw[ks], A.T[ks], tab[tri((int)(mts >> 16)) + (mts & 0xFFFFu)], a, b,
-                                 A.beta, A.vbeta, f0, f1);
+                    slot_factors(ldc<ASYNC>(Mi + ks), ldc<ASYNC>(Tti + ks), ldc<ASYNC>(Qw + ks), ldc<ASYNC>(A.T + ks),
+                                 tab[tri((int)(mts >> 16)) + (mts & 0xFFFFu)], a, b, A.beta, A.vbeta, f0, f1);
                     R1s = (f1 > 0.f) ? __fdiv_rn(f1, f0 + f1) : 0.f;
                 }
                 const float w1 = wsel * R1s;
@@ -495,6 +561,13 @@ sample_kernel(SweepArgs A) {
                     atomicAdd(&S.dmt[k0], -65536 - rrem);
                     atomicAdd(&S.dmt[ks], 65536 + rs);
                     moved += (ks != k0);
+                    if constexpr (ASYNC) {                 // doc-topic row updated at once (Alg.4 "atomically")
+                        if (ks != k0) {
+                            NT* nw = reinterpret_cast<NT*>(A.n);
+                            Row<NT>::add(nw, (size_t)noff + A.sigma[k0], -1);
+                            Row<NT>::add(nw, (size_t)noff + A.sigma[ks], 1);
+                        }
+                    }
                 }
             }
         }
@@ -507,8 +580,16 @@ sample_kernel(SweepArgs A) {
             if (x) {
                 const int dtv = (int)(short)(x & 0xFFFF);   // low half, sign-extended
                 const int dmv = (x - dtv) >> 16;
-                if (dmv) atomicAdd(A.dm + row + k, dmv);
-                if (dtv) atomicAdd(A.dt + row + k, dtv);
+                if constexpr (ASYNC) {                     // global counts and sums updated at once
+                    if (dmv) { atomicAdd(A.m + row + k, dmv); atomicAdd(A.M + (size_t)i * Kp + k, dmv); }
+                    if (dtv) {
+                        atomicAdd(A.t + row + k, dtv); atomicAdd(A.Q + (size_t)w * Kp + k, dtv);
+                        atomicAdd(A.Tt + (size_t)i * Kp + k, dtv); atomicAdd(A.T + k, dtv);
+                    }
+                } else {
+                    if (dmv) atomicAdd(A.dm + row + k, dmv);
+                    if (dtv) atomicAdd(A.dt + row + k, dtv);
+                }
             }
         }
     }
@@ -560,7 +641,7 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
                                   int32_t* __restrict__ dm, int32_t* __restrict__ dt,
                                   int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
                                   int32_t* __restrict__ T, int V, int I, int Kp, int use_smem_sums,
-                                  unsigned long long* __restrict__ stats) {
+                                  unsigned long long* __restrict__ stats, int clamp_all) {
     extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
     int* sM = ssum;
     int* sT = ssum + (size_t)I * Kp;
@@ -579,9 +660,9 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
                 const size_t off = ((size_t)w * I + i) * Kp + k4;
                 int4 vm = *reinterpret_cast<const int4*>(m + off);
                 int4 vt = *reinterpret_cast<const int4*>(t + off);
-                const int4 a = *reinterpret_cast<const int4*>(dm + off);
-                const int4 d = *reinterpret_cast<const int4*>(dt + off);
-                if ((a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) != 0) {
+                const int4 a = dm ? *reinterpret_cast<const int4*>(dm + off) : make_int4(0, 0, 0, 0);
+                const int4 d = dt ? *reinterpret_cast<const int4*>(dt + off) : make_int4(0, 0, 0, 0);
+                if (clamp_all || (a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) != 0) {
                     int* pm = &vm.x; int* pt = &vt.x;
                     const int* pa = &a.x; const int* pd = &d.x;
 #pragma unroll
@@ -595,8 +676,8 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
                     }
                     *reinterpret_cast<int4*>(m + off) = vm;
                     *reinterpret_cast<int4*>(t + off) = vt;
-                    *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
-                    *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
+                    if (dm) *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
+                    if (dt) *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
                 }
                 q.x += vt.x; q.y += vt.y; q.z += vt.z; q.w += vt.w;
                 const int* pm = &vm.x; const int* pt = &vt.x;
@@ -796,6 +877,23 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
             if (sT[j]) atomicAdd(Tt + j, sT[j]);
         }
         for (int j = threadIdx.x; j < Kp; j += blockDim.x) if (sK[j]) atomicAdd(T + j, sK[j]);
+    }
+}
+
+// Async mode with several ranks: D = (m - m0, t - t0) packed, from the sweep-start
+// copy (m0, t0) kept in the otherwise unused wave-delta buffers, which are zeroed.
+template <typename P>
+__global__ void net_change_kernel(const int32_t* __restrict__ m, const int32_t* __restrict__ t,
+                                  int32_t* __restrict__ m0, int32_t* __restrict__ t0, P* __restrict__ D, size_t cells) {
+    for (size_t j = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 4; j < cells; j += (size_t)gridDim.x * blockDim.x * 4) {
+        const int4 a = *reinterpret_cast<const int4*>(m + j), b = *reinterpret_cast<const int4*>(t + j);
+        const int4 a0 = *reinterpret_cast<const int4*>(m0 + j), b0 = *reinterpret_cast<const int4*>(t0 + j);
+        const int cm[4] = {a.x - a0.x, a.y - a0.y, a.z - a0.z, a.w - a0.w};
+        const int ct[4] = {b.x - b0.x, b.y - b0.y, b.z - b0.z, b.w - b0.w};
+        Packed<P>::clear4(D + j);
+        Packed<P>::add4(D + j, cm, ct);
+        *reinterpret_cast<int4*>(m0 + j) = make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(t0 + j) = make_int4(0, 0, 0, 0);
     }
 }
 
