@@ -310,7 +310,7 @@ def main():
 def run_heldout(args, cfg, K, workload):
     """NEXT-1 measurement (one GPU): train on 90% of the corpus, then time
     spdp_heldout (fold-in of the held-out 10% per group + held-out perplexity,
-    DESIGN.md §11) per step; the fold-in kernel's own CUDA-event time gives the
+    DESIGN.md §10) per step; the fold-in kernel's own CUDA-event time gives the
     roofline (fp64 phi~ row of 8K bytes + 16 B of token record per
     token-iteration, plus one 8K-byte row per token for the likelihood pass)."""
     import torch

@@ -66,7 +66,7 @@ enum {
                                     spdp_sweep_local and spdp_sweep_merge */
 };
 
-/* How a sweep updates the counts (DESIGN.md §3 reading c13, §12). */
+/* How a sweep updates the counts (DESIGN.md §3 reading c13, §11). */
 enum {
     SPDP_UPDATE_WAVE = 0,   /* deterministic wave snapshots: every token of a wave decides against the
                                wave-start counts, the wave's deltas are applied after it (default) */
