@@ -265,9 +265,10 @@ def main():
     t0 = time.perf_counter()
     h = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
     h.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs)     # H2D of the job's inputs
+    out = {"z": np.empty(N, np.int32), "r": np.empty(N, np.uint8)}               # caller-owned, reused
     for _ in range(e2e_steps):
         h.sweep(1)
-        out = h.counts(doc_topic=False, customers=False, tables=False, shadow=False)   # D2H of z, r
+        h.counts(out=out, doc_topic=False, customers=False, tables=False, shadow=False)   # D2H of z, r
     torch.cuda.synchronize(); barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:

@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("SPDP_LIB") or os.path.join(_HERE, "libspdp.so")   # SPDP_LIB: tuning variants
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("spdp.cu", "spdp_device.cuh", "spdp_loglik.cuh", "spdp_eval.cuh")] + [
+_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("spdp.cu", "spdp_device.cuh", "spdp_loglik.cuh", "spdp_eval.cuh", "spdp_plan.cuh")] + [
     os.path.join(_ROOT, "include", "spdp.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -193,14 +193,19 @@ def spdp_sweep_merge(ctx):
     _check(lib().spdp_sweep_merge(ctx), ctx)
 
 
-def spdp_counts(ctx, N, D, I, V, K, z=True, r=True, doc_topic=True, customers=True, tables=True, shadow=True):
-    out = {}
-    if z: out["z"] = np.zeros(N, np.int32)
-    if r: out["r"] = np.zeros(N, np.uint8)
-    if doc_topic: out["n"] = np.zeros((D, K), np.int32)
-    if customers: out["m"] = np.zeros((I, V, K), np.int32)
-    if tables: out["t"] = np.zeros((I, V, K), np.int32)
-    if shadow: out["Q"] = np.zeros((K, V), np.int32)
+def spdp_counts(ctx, N, D, I, V, K, z=True, r=True, doc_topic=True, customers=True, tables=True, shadow=True,
+                out=None):
+    """State read-out.  out: optional dict of caller-owned arrays to fill (reused across calls)."""
+    out = {} if out is None else out
+    shapes = {"z": ((N,), np.int32, z), "r": ((N,), np.uint8, r), "n": ((D, K), np.int32, doc_topic),
+              "m": ((I, V, K), np.int32, customers), "t": ((I, V, K), np.int32, tables), "Q": ((K, V), np.int32, shadow)}
+    for k, (shape, dt, want) in shapes.items():
+        if not want:
+            out.pop(k, None)
+        elif k not in out:
+            out[k] = np.zeros(shape, dt)
+        else:
+            assert out[k].shape == shape and out[k].dtype == dt and out[k].flags["C_CONTIGUOUS"], k
     _check(lib().spdp_counts(ctx, _p(out.get("z")), _p(out.get("r")), _p(out.get("n")), _p(out.get("m")),
                              _p(out.get("t")), _p(out.get("Q"))), ctx)
     return out
@@ -310,8 +315,8 @@ class Sampler:
     def sweep_merge(self):
         spdp_sweep_merge(self.ctx)
 
-    def counts(self, **which):
-        return spdp_counts(self.ctx, self.N, self.D, self.I, self.V, self.K, **which)
+    def counts(self, out=None, **which):
+        return spdp_counts(self.ctx, self.N, self.D, self.I, self.V, self.K, out=out, **which)
 
     def loglik(self, log_joint=True, perplexity=True):
         return spdp_loglik(self.ctx, log_joint, perplexity)

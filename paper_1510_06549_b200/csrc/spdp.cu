@@ -10,6 +10,7 @@
 #include "spdp_device.cuh"
 #include "spdp_loglik.cuh"
 #include "spdp_eval.cuh"
+#include "spdp_plan.cuh"
 
 #include <dlfcn.h>
 
@@ -88,15 +89,15 @@ struct spdp_ctx {
     // corpus (host)
     int64_t N = 0;
     int32_t D = 0;
-    std::vector<int32_t> group, doc, word, pos, doclen, docgroup;
+    std::vector<int32_t> group, doc, word, doclen, docgroup;
     std::vector<int32_t> shard_of_doc, local_of_doc, global_of_local;
     int64_t Nloc = 0;
     int32_t Dloc = 0;
-    std::vector<uint32_t> sorted_tok;            // canonical id at each sorted position
-    std::vector<int64_t> pos_of_tok;              // canonical id -> sorted position (-1: other rank)
+    std::vector<uint32_t> sorted_tok;            // canonical id at each sorted position (lazy host copy)
+    std::vector<int64_t> pos_of_tok;              // canonical id -> sorted position (-1: other rank; lazy)
     std::vector<uint32_t> wave_tok_begin, wave_chunk_begin;
-    std::vector<uint32_t> chunk_start, chunk_end, chunk_seg;
-    std::vector<uint32_t> wave_seg_begin, wave_segs;   // distinct (w, i) segments of each wave
+    std::vector<uint32_t> wave_seg_begin;          // distinct (w, i) segments of each wave (d_wave_segs)
+    uint32_t nchunks = 0, nsegs = 0;
     int mmax = 0;
     size_t cells = 0;
     // multi-GPU net change since the sweep start, packed dm*2^B + dt (B = 16: int32, else int64)
@@ -109,6 +110,7 @@ struct spdp_ctx {
              *d_chunk_seg = nullptr, *d_wave_segs = nullptr,
              *d_sweep = nullptr;
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
+    int32_t *d_group = nullptr, *d_doc = nullptr, *d_word = nullptr;   // canonical token triples (all ranks' tokens)
     uint32_t *d_doc_ptr = nullptr, *d_doc_pos = nullptr;   // CSR: sorted-token positions of each local doc
     void* d_n = nullptr;                          // n_dk rows in sigma order: fp32 or uint16 (row16)
     bool row16 = false;                           // uint16 doc-topic rows (HBM-resident arrays)
@@ -413,47 +415,61 @@ void parallel_for(int64_t n, Fn fn) {
     for (auto& x : th) x.join();
 }
 
+// Host copy of the plan's token order (diagnostics only: debug_probs, debug_verify).
+spdp_status ensure_host_plan(spdp_ctx* c) {
+    if ((int64_t)c->sorted_tok.size() == c->Nloc && (int64_t)c->pos_of_tok.size() == c->N &&
+        (int64_t)c->doc.size() == c->N)
+        return SPDP_OK;
+    c->sorted_tok.resize((size_t)c->Nloc);
+    if (c->Nloc > 0)
+        CU(cudaMemcpy(c->sorted_tok.data(), c->d_tok_id, sizeof(uint32_t) * (size_t)c->Nloc, cudaMemcpyDeviceToHost));
+    c->group.resize((size_t)c->N); c->doc.resize((size_t)c->N); c->word.resize((size_t)c->N);
+    CU(cudaMemcpy(c->group.data(), c->d_group, sizeof(int32_t) * (size_t)c->N, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(c->doc.data(), c->d_doc, sizeof(int32_t) * (size_t)c->N, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(c->word.data(), c->d_word, sizeof(int32_t) * (size_t)c->N, cudaMemcpyDeviceToHost));
+    c->pos_of_tok.assign((size_t)c->N, -1);
+    parallel_for(c->Nloc, [&](int64_t b, int64_t e) {
+        for (int64_t q = b; q < e; ++q) c->pos_of_tok[c->sorted_tok[(size_t)q]] = q;
+    });
+    return SPDP_OK;
+}
+
 // Upload (z, r or tables) as the sampler state; counts from z
 // are built on the device.
 spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in, const int32_t* tables) {
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     const int64_t N = c->N;
-    std::vector<int32_t> z((size_t)N);
-    std::atomic<int64_t> badz{-1}, badr{-1};
-    parallel_for(N, [&](int64_t b, int64_t e) {
-        for (int64_t p = b; p < e; ++p) {
-            if (z_in) {
-                if (z_in[p] < 0 || z_in[p] >= K) badz = p;
-                z[(size_t)p] = z_in[p];
-            } else {
-                const uint32_t ctr[4] = {(uint32_t)p, 0xFFFFFFFFu, 0u, 0u};
-                uint32_t x[4];
-                philox_host(ctr, (uint32_t)c->cfg.seed, (uint32_t)(c->cfg.seed >> 32), x);
-                z[(size_t)p] = (int32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
-            }
-            if (r_in && r_in[p] > 1) badr = p;
-        }
-    });
-    if (badz >= 0) return fail(c, SPDP_EINVAL, "z[%lld] out of [0, K)", (long long)badz.load());
-    if (badr >= 0) return fail(c, SPDP_EINVAL, "r[%lld] not in {0,1}", (long long)badr.load());
-    TempBuf<int32_t> dz(N), dg(N), dw(N);
+    TempBuf<int32_t> dz(N);
     TempBuf<uint8_t> dr(N);
     TempBuf<uint32_t> dfirst(r_in ? 1 : c->cells);
-    TempBuf<unsigned long long> dbad(1);
-    if (!dz.p || !dg.p || !dw.p || !dr.p || !dfirst.p || !dbad.p) return fail(c, SPDP_ENOMEM, "install_state buffers");
-    CU(cudaMemcpyAsync(dz.p, z.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(dg.p, c->group.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
-    CU(cudaMemcpyAsync(dw.p, c->word.data(), sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
+    TempBuf<unsigned long long> dbad(1), dbadzr(2);
+    if (!dz.p || !dr.p || !dfirst.p || !dbad.p || !dbadzr.p) return fail(c, SPDP_ENOMEM, "install_state buffers");
+    int32_t* dg = c->d_group;
+    int32_t* dw = c->d_word;
+    // z: the caller's, or the Philox initial topics z_p = floor(x0 K / 2^32), counter (p, 0xFFFFFFFF) (reading c11)
+    if (z_in) CU(cudaMemcpyAsync(dz.p, z_in, sizeof(int32_t) * (size_t)N, cudaMemcpyHostToDevice, c->stream));
+    else init_z_kernel<<<148 * 8, 256, 0, c->stream>>>(dz.p, (uint32_t)N, K, (uint32_t)c->cfg.seed,
+                                                       (uint32_t)(c->cfg.seed >> 32));
     if (r_in) CU(cudaMemcpyAsync(dr.p, r_in, (size_t)N, cudaMemcpyHostToDevice, c->stream));
-    else CU(cudaMemsetAsync(dfirst.p, 0xFF, sizeof(uint32_t) * c->cells, c->stream));
+    CU(cudaMemsetAsync(dbadzr.p, 0xFF, sizeof(unsigned long long) * 2, c->stream));
+    check_zr_kernel<<<148 * 8, 256, 0, c->stream>>>(dz.p, r_in ? dr.p : nullptr, (uint32_t)N, K, dbadzr.p);
+    {
+        unsigned long long bz[2];
+        CU(cudaMemcpyAsync(bz, dbadzr.p, sizeof(bz), cudaMemcpyDeviceToHost, c->stream));
+        spdp_status s0 = sync(c, "install_state check");
+        if (s0) return s0;
+        if (bz[0] != ~0ull) return fail(c, SPDP_EINVAL, "z[%llu] out of [0, K)", bz[0]);
+        if (bz[1] != ~0ull) return fail(c, SPDP_EINVAL, "r[%llu] not in {0,1}", bz[1]);
+    }
+    if (!r_in) CU(cudaMemsetAsync(dfirst.p, 0xFF, sizeof(uint32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_m, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_t, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(dbad.p, 0, sizeof(unsigned long long), c->stream));
     const int grid = 148 * 8;
-    init_cells_kernel<<<grid, 256, 0, c->stream>>>(dg.p, dw.p, dz.p, r_in ? dr.p : nullptr, (uint32_t)N, I, Kp, c->d_m,
+    init_cells_kernel<<<grid, 256, 0, c->stream>>>(dg, dw, dz.p, r_in ? dr.p : nullptr, (uint32_t)N, I, Kp, c->d_m,
                                                    c->d_t, dfirst.p);
     if (!r_in)
-        init_first_table_kernel<<<grid, 256, 0, c->stream>>>(dg.p, dw.p, dz.p, (uint32_t)N, I, Kp, dfirst.p, dr.p, c->d_t);
+        init_first_table_kernel<<<grid, 256, 0, c->stream>>>(dg, dw, dz.p, (uint32_t)N, I, Kp, dfirst.p, dr.p, c->d_t);
     if (tables) {
         TempBuf<int32_t> dt_in((size_t)I * V * K);
         if (!dt_in.p) return fail(c, SPDP_ENOMEM, "tables buffer");
@@ -514,7 +530,7 @@ spdp_status run_waves(spdp_ctx* c) {
             CU(cudaMemcpyAsync(c->d_dt, c->d_t, sizeof(int32_t) * c->cells, cudaMemcpyDeviceToDevice, c->stream));
         }
         rec(c, 0);
-        a.nchunks = (int)c->chunk_seg.size();
+        a.nchunks = (int)c->nchunks;
         a.work = c->d_work;
         launch_sample(c, a, false);
         rec(c, 1);
@@ -741,27 +757,77 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
     const int I = c->I, V = c->V, Kp = c->Kp, W = c->W;
     c->N = num_tokens; c->D = num_docs;
-    c->group.assign(group, group + num_tokens);
-    c->doc.assign(doc, doc + num_tokens);
-    c->word.assign(word, word + num_tokens);
-    c->pos.resize((size_t)num_tokens);
-    c->doclen.assign((size_t)num_docs, 0);
-    c->docgroup.assign((size_t)num_docs, -1);
-    for (int64_t p = 0; p < num_tokens; ++p) {
-        const int32_t g = group[p], d = doc[p], w = word[p];
-        if (g < 0 || g >= I || d < 0 || d >= num_docs || w < 0 || w >= V)
-            return fail(c, SPDP_EINVAL, "token %lld = (%d, %d, %d) out of range", (long long)p, g, d, w);
-        if (c->docgroup[(size_t)d] >= 0 && c->docgroup[(size_t)d] != g)
-            return fail(c, SPDP_EINVAL, "document %d spans groups %d and %d", d, c->docgroup[(size_t)d], g);
-        c->docgroup[(size_t)d] = g;
-        c->pos[(size_t)p] = c->doclen[(size_t)d]++;
+    // the token triples stay on the device (state installation); host copies only on demand (diagnostics)
+    c->group.clear(); c->doc.clear(); c->word.clear();
+    const uint32_t n = (uint32_t)num_tokens;
+    const int grid = 148 * 8;
+    cudaStream_t st = c->stream;
+    auto bits = [](uint64_t x) { int b = 1; while (b < 64 && (x >> b)) ++b; return b; };
+    ALLOC(c->d_group, n); ALLOC(c->d_doc, n); ALLOC(c->d_word, n);
+    struct { int32_t* p; } dgrp{c->d_group}, ddoc{c->d_doc}, dwrd{c->d_word};
+    TempBuf<int32_t> dpos(n), ddg((size_t)num_docs), ddl((size_t)num_docs);
+    TempBuf<uint32_t> diota(n), dbydoc(n), dstart((size_t)num_docs);
+    TempBuf<int32_t> dkeyd(n);
+    TempBuf<unsigned long long> derr(2);
+    if (!dpos.p || !ddg.p || !ddl.p || !diota.p || !dbydoc.p || !dstart.p ||
+        !dkeyd.p || !derr.p)
+        return fail(c, SPDP_ENOMEM, "load planning buffers");
+    CU(cudaMemcpyAsync(dgrp.p, group, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(ddoc.p, doc, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dwrd.p, word, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    CU(cudaMemsetAsync(ddg.p, 0xFF, sizeof(int32_t) * (size_t)num_docs, st));
+    CU(cudaMemsetAsync(ddl.p, 0, sizeof(int32_t) * (size_t)num_docs, st));
+    CU(cudaMemsetAsync(derr.p, 0xFF, sizeof(unsigned long long) * 2, st));
+    validate_tokens_kernel<<<grid, 256, 0, st>>>(dgrp.p, ddoc.p, dwrd.p, n, I, V, num_docs, ddg.p, ddl.p, derr.p);
+    unsigned long long herr[2];
+    CU(cudaMemcpyAsync(herr, derr.p, sizeof(herr), cudaMemcpyDeviceToHost, st));
+    c->doclen.resize((size_t)num_docs);
+    c->docgroup.resize((size_t)num_docs);
+    CU(cudaMemcpyAsync(c->doclen.data(), ddl.p, sizeof(int32_t) * (size_t)num_docs, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(c->docgroup.data(), ddg.p, sizeof(int32_t) * (size_t)num_docs, cudaMemcpyDeviceToHost, st));
+    if ((s = sync(c, "validate tokens"))) return s;
+    if (herr[0] != ~0ull) {
+        const size_t q = (size_t)herr[0];
+        return fail(c, SPDP_EINVAL, "token %lld = (%d, %d, %d) out of range", (long long)q, group[q], doc[q], word[q]);
     }
+    if (herr[1] != ~0ull) {
+        const size_t q = (size_t)herr[1];
+        return fail(c, SPDP_EINVAL, "document %d spans groups (%d and %d)", doc[q], c->docgroup[(size_t)doc[q]], group[q]);
+    }
+    // in-document positions: stable sort of the tokens by document (ties keep canonical order)
+    auto cub_run = [&](auto f, const char* what) -> spdp_status {
+        size_t bytes = 0;
+        cudaError_t e = f((void*)nullptr, bytes);
+        if (e == cudaSuccess) {
+            TempBuf<uint8_t> tmp(bytes);
+            if (!tmp.p) return fail(c, SPDP_ENOMEM, "%s: temporary storage", what);
+            e = f((void*)tmp.p, bytes);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        }
+        if (e != cudaSuccess) return fail(c, SPDP_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+        return SPDP_OK;
+    };
+    iota_kernel<<<grid, 256, 0, st>>>(diota.p, n);
+    if ((s = cub_run([&](void* t, size_t& b) {
+             return cub::DeviceRadixSort::SortPairs(t, b, ddoc.p, dkeyd.p, diota.p, dbydoc.p, (int)n, 0, bits((uint64_t)num_docs), st);
+         }, "sort by document")))
+        return s;
+    if ((s = cub_run([&](void* t, size_t& b) {
+             return cub::DeviceScan::ExclusiveSum(t, b, reinterpret_cast<const uint32_t*>(ddl.p), dstart.p, num_docs, st);
+         }, "document offsets")))
+        return s;
+    positions_kernel<<<grid, 256, 0, st>>>(dbydoc.p, ddoc.p, dstart.p, n, dpos.p);
     lt.mark("validate + positions");
     // M_max = largest count(i, w): bounds every m_{ikw} the chain can reach
     {
-        std::vector<int32_t> cnt((size_t)I * V, 0);
-        for (int64_t p = 0; p < num_tokens; ++p) cnt[(size_t)group[p] * V + word[p]]++;
-        c->mmax = *std::max_element(cnt.begin(), cnt.end());
+        TempBuf<int32_t> dcnt((size_t)I * V), dmx(1);
+        if (!dcnt.p || !dmx.p) return fail(c, SPDP_ENOMEM, "count(i,w) buffer");
+        CU(cudaMemsetAsync(dcnt.p, 0, sizeof(int32_t) * (size_t)I * V, st));
+        cell_count_kernel<<<grid, 256, 0, st>>>(dgrp.p, dwrd.p, n, V, dcnt.p);
+        if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, dcnt.p, dmx.p, I * V, st); },
+                         "M_max")))
+            return s;
+        CU(cudaMemcpyAsync(&c->mmax, dmx.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
         if (c->mmax >= 65536)
             return fail(c, SPDP_ETABLE, "M_max = %d: cells are packed in 16 bits (M_max < 65536)", c->mmax);
         if ((double)c->mmax * (c->mmax + 1) / 2 * sizeof(float2) > 16e9)
@@ -779,100 +845,120 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
     c->Dloc = (int32_t)c->global_of_local.size();
     lt.mark("M_max + partition");
-    // wave plan: stable counting sort of local tokens by seg = w*I + i, then by wave = l mod W
-    std::vector<uint32_t> local;
-    local.reserve((size_t)num_tokens / c->G + 16);
-    for (int64_t p = 0; p < num_tokens; ++p)
-        if (c->shard_of_doc[(size_t)doc[p]] == c->rank) local.push_back((uint32_t)p);
-    c->Nloc = (int64_t)local.size();
+    // this rank's tokens, canonical order
+    TempBuf<uint32_t> dlocal(n);
+    TempBuf<int32_t> dlod(c->G > 1 ? (size_t)num_docs : 1);
+    if (!dlocal.p || !dlod.p) return fail(c, SPDP_ENOMEM, "local token buffer");
+    uint32_t nloc = n;
+    if (c->G > 1) {
+        TempBuf<int32_t> dshard((size_t)num_docs);
+        TempBuf<uint8_t> dflag(n);
+        TempBuf<uint32_t> dnsel(1);
+        if (!dshard.p || !dflag.p || !dnsel.p) return fail(c, SPDP_ENOMEM, "shard buffers");
+        CU(cudaMemcpyAsync(dshard.p, c->shard_of_doc.data(), sizeof(int32_t) * (size_t)num_docs, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(dlod.p, c->local_of_doc.data(), sizeof(int32_t) * (size_t)num_docs, cudaMemcpyHostToDevice, st));
+        local_flags_kernel<<<grid, 256, 0, st>>>(ddoc.p, dshard.p, c->rank, n, dflag.p);
+        if ((s = cub_run([&](void* t, size_t& b) {
+                 return cub::DeviceSelect::Flagged(t, b, diota.p, dflag.p, dlocal.p, dnsel.p, (int)n, st);
+             }, "select local tokens")))
+            return s;
+        CU(cudaMemcpyAsync(&nloc, dnsel.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+    } else {
+        CU(cudaMemcpyAsync(dlocal.p, diota.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
+    }
+    c->Nloc = nloc;
+    // wave plan: stable sort of the local tokens by (wave = l mod W, w * I + i)
+    const uint64_t S = (uint64_t)V * I;
+    const uint32_t chunk = (uint32_t)c->chunk_tokens;
+    uint32_t R = 0, nch = 0;
     {
-        // stable parallel counting sort: per-thread histograms over contiguous ranges
-        const size_t S = (size_t)V * I, n = local.size();
-        auto counting_sort = [&](const std::vector<uint32_t>& in, std::vector<uint32_t>& out, size_t nbuckets,
-                                 auto key) {
-            const int nt = (int)std::min<size_t>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())),
-                                                 std::max<size_t>(1, n >> 16));
-            const size_t step = (n + nt - 1) / nt;
-            std::vector<std::vector<uint32_t>> hist((size_t)nt, std::vector<uint32_t>(nbuckets, 0));
-            std::vector<std::thread> th;
-            for (int j = 0; j < nt; ++j)
-                th.emplace_back([&, j] {
-                    for (size_t q = j * step; q < std::min(n, (j + 1) * step); ++q) hist[(size_t)j][key(in[q])]++;
-                });
-            for (auto& x : th) x.join();
-            th.clear();
-            uint64_t run = 0;
-            for (size_t bk = 0; bk < nbuckets; ++bk)
-                for (int j = 0; j < nt; ++j) {
-                    const uint32_t v = hist[(size_t)j][bk];
-                    hist[(size_t)j][bk] = (uint32_t)run;
-                    run += v;
-                }
-            out.assign(n, 0);
-            for (int j = 0; j < nt; ++j)
-                th.emplace_back([&, j] {
-                    std::vector<uint32_t>& h = hist[(size_t)j];
-                    for (size_t q = j * step; q < std::min(n, (j + 1) * step); ++q) out[h[key(in[q])]++] = in[q];
-                });
-            for (auto& x : th) x.join();
-        };
-        std::vector<uint32_t> tmp;
-        counting_sort(local, tmp, S, [&](uint32_t p) { return (size_t)word[p] * I + group[p]; });
-        counting_sort(tmp, c->sorted_tok, (size_t)W, [&](uint32_t p) { return (size_t)(c->pos[p] % W); });
-        std::vector<uint32_t> woff((size_t)W + 1, 0);
-        for (uint32_t p : local) woff[(size_t)(c->pos[p] % W) + 1]++;
-        for (int w = 0; w < W; ++w) woff[(size_t)w + 1] += woff[(size_t)w];
-        c->wave_tok_begin.assign(woff.begin(), woff.end());
-    }
-    c->pos_of_tok.assign((size_t)num_tokens, -1);
-    parallel_for((int64_t)c->sorted_tok.size(), [&](int64_t b, int64_t e) {
-        for (int64_t q = b; q < e; ++q) c->pos_of_tok[c->sorted_tok[(size_t)q]] = q;
-    });
-    // chunks: split each wave's (w, i) segments into runs of <= chunk_tokens tokens;
-    // within a wave, longest first (the persistent warps take them in order)
-    c->chunk_start.clear(); c->chunk_end.clear(); c->chunk_seg.clear();
-    c->wave_chunk_begin.assign((size_t)W + 1, 0);
-    for (int w = 0; w < W; ++w) {
-        c->wave_chunk_begin[(size_t)w] = (uint32_t)c->chunk_seg.size();
-        std::vector<std::array<uint32_t, 3>> wc;
-        uint32_t q = c->wave_tok_begin[(size_t)w];
-        const uint32_t qe = c->wave_tok_begin[(size_t)w + 1];
-        while (q < qe) {
-            const uint32_t p = c->sorted_tok[q];
-            const uint32_t seg = (uint32_t)word[p] * (uint32_t)I + (uint32_t)group[p];
-            uint32_t r = q, len = 0;
-            while (r < qe && len < (uint32_t)c->chunk_tokens) {
-                const uint32_t pr = c->sorted_tok[r];
-                if ((uint32_t)word[pr] * (uint32_t)I + (uint32_t)group[pr] != seg) break;
-                ++r; ++len;
-            }
-            wc.push_back({q, r, seg});
-            q = r;
+        const size_t nl = std::max<uint32_t>(nloc, 1);
+        TempBuf<uint64_t> dkey(nl), dkey2(nl), drkey(nl);
+        TempBuf<uint32_t> drlen(nl), droff(nl), dnch(nl), dchoff(nl), dR(1), dwb((size_t)W + 1);
+        if (!dkey.p || !dkey2.p || !drkey.p || !drlen.p || !droff.p || !dnch.p || !dchoff.p || !dR.p || !dwb.p)
+            return fail(c, SPDP_ENOMEM, "wave plan buffers");
+        ALLOC(c->d_tok_id, nl);
+        plan_keys_kernel<<<grid, 256, 0, st>>>(dlocal.p, nloc, dgrp.p, dwrd.p, dpos.p, I, W, S, dkey.p);
+        if ((s = cub_run([&](void* t, size_t& b) {
+                 return cub::DeviceRadixSort::SortPairs(t, b, dkey.p, dkey2.p, dlocal.p, c->d_tok_id, (int)nloc, 0,
+                                                        bits((uint64_t)W * S), st);
+             }, "sort by (wave, word, group)")))
+            return s;
+        bounds_kernel<<<grid, 256, 0, st>>>(WaveOfKey{dkey2.p, S}, nloc, (uint32_t)W, dwb.p);
+        c->wave_tok_begin.resize((size_t)W + 1);
+        CU(cudaMemcpyAsync(c->wave_tok_begin.data(), dwb.p, sizeof(uint32_t) * ((size_t)W + 1), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+        // segments of each wave = runs of equal keys
+        if ((s = cub_run([&](void* t, size_t& b) {
+                 return cub::DeviceRunLengthEncode::Encode(t, b, dkey2.p, drkey.p, drlen.p, dR.p, (int)nloc, st);
+             }, "segments")))
+            return s;
+        CU(cudaMemcpyAsync(&R, dR.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+        if (nloc == 0) R = 0;
+        ALLOC(c->d_wave_segs, std::max<uint32_t>(R, 1));
+        c->wave_seg_begin.assign((size_t)W + 1, 0);
+        c->wave_chunk_begin.assign((size_t)W + 1, 0);
+        if (R > 0) {
+            seg_of_key_kernel<<<grid, 256, 0, st>>>(drkey.p, R, S, c->d_wave_segs);
+            bounds_kernel<<<grid, 256, 0, st>>>(WaveOfKey{drkey.p, S}, R, (uint32_t)W, dwb.p);
+            CU(cudaMemcpyAsync(c->wave_seg_begin.data(), dwb.p, sizeof(uint32_t) * ((size_t)W + 1), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+            // chunks of <= chunk_tokens tokens; within a wave longest first (stable)
+            if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, drlen.p, droff.p, (int)R, st); },
+                             "segment offsets")))
+                return s;
+            chunk_count_kernel<<<grid, 256, 0, st>>>(drlen.p, R, chunk, dnch.p);
+            if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, dnch.p, dchoff.p, (int)R, st); },
+                             "chunk offsets")))
+                return s;
+            uint32_t last[2];
+            CU(cudaMemcpyAsync(&last[0], dchoff.p + (R - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+            CU(cudaMemcpyAsync(&last[1], dnch.p + (R - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+            nch = last[0] + last[1];
         }
-        std::stable_sort(wc.begin(), wc.end(), [](const std::array<uint32_t, 3>& x, const std::array<uint32_t, 3>& y) {
-            return (x[1] - x[0]) > (y[1] - y[0]);
-        });
-        for (const auto& ch : wc) {
-            c->chunk_start.push_back(ch[0]);
-            c->chunk_end.push_back(ch[1]);
-            c->chunk_seg.push_back(ch[2]);
+        const size_t nc = std::max<uint32_t>(nch, 1);
+        ALLOC(c->d_chunk_start, nc); ALLOC(c->d_chunk_end, nc); ALLOC(c->d_chunk_seg, nc);
+        if (nch > 0) {
+            TempBuf<uint32_t> cs(nc), ce(nc), cg(nc), ci(nc), ci2(nc);
+            TempBuf<uint64_t> ck(nc), ck2(nc);
+            if (!cs.p || !ce.p || !cg.p || !ci.p || !ci2.p || !ck.p || !ck2.p) return fail(c, SPDP_ENOMEM, "chunk buffers");
+            chunk_emit_kernel<<<grid, 256, 0, st>>>(drkey.p, drlen.p, droff.p, dchoff.p, R, chunk, S, cs.p, ce.p, cg.p,
+                                                    ck.p, ci.p);
+            if ((s = cub_run([&](void* t, size_t& b) {
+                     return cub::DeviceRadixSort::SortPairs(t, b, ck.p, ck2.p, ci.p, ci2.p, (int)nch, 0,
+                                                            bits((uint64_t)W * (chunk + 1)), st);
+                 }, "chunk order")))
+                return s;
+            gather3_kernel<<<grid, 256, 0, st>>>(ci2.p, nch, cs.p, ce.p, cg.p, c->d_chunk_start, c->d_chunk_end,
+                                                 c->d_chunk_seg);
+            bounds_kernel<<<grid, 256, 0, st>>>(WaveOfChunkKey{ck2.p, (uint64_t)chunk + 1}, nch, (uint32_t)W, dwb.p);
+            CU(cudaMemcpyAsync(c->wave_chunk_begin.data(), dwb.p, sizeof(uint32_t) * ((size_t)W + 1), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
         }
     }
-    c->wave_chunk_begin[(size_t)W] = (uint32_t)c->chunk_seg.size();
-    // distinct segments per wave (the rows the wave's merge touches), ascending
-    c->wave_seg_begin.assign((size_t)W + 1, 0);
-    c->wave_segs.clear();
-    for (int w = 0; w < W; ++w) {
-        c->wave_seg_begin[(size_t)w] = (uint32_t)c->wave_segs.size();
-        std::vector<uint32_t> ss(c->chunk_seg.begin() + c->wave_chunk_begin[(size_t)w],
-                                 c->chunk_seg.begin() + c->wave_chunk_begin[(size_t)w + 1]);
-        std::sort(ss.begin(), ss.end());
-        ss.erase(std::unique(ss.begin(), ss.end()), ss.end());
-        c->wave_segs.insert(c->wave_segs.end(), ss.begin(), ss.end());
+    c->nchunks = nch;
+    c->nsegs = R;
+    // doc of every sorted position, and the doc -> sorted-positions CSR (W = 1 recount)
+    {
+        const size_t nl = std::max<uint32_t>(nloc, 1);
+        ALLOC(c->d_tok_doc, nl);
+        ALLOC(c->d_doc_pos, nl);
+        ALLOC(c->d_doc_ptr, (size_t)c->Dloc + 1);
+        TempBuf<uint32_t> dq(nl), dk2(nl);
+        if (!dq.p || !dk2.p) return fail(c, SPDP_ENOMEM, "CSR buffers");
+        tdoc_kernel<<<grid, 256, 0, st>>>(c->d_tok_id, nloc, ddoc.p, c->G > 1 ? dlod.p : nullptr, c->d_tok_doc, dq.p);
+        if (nloc > 0 && (s = cub_run([&](void* t, size_t& b) {
+                             return cub::DeviceRadixSort::SortPairs(t, b, c->d_tok_doc, dk2.p, dq.p, c->d_doc_pos, (int)nloc,
+                                                                    0, bits((uint64_t)std::max(c->Dloc, 1)), st);
+                         }, "CSR")))
+            return s;
+        std::vector<uint32_t> dptr((size_t)c->Dloc + 1, 0);
+        for (int32_t j = 0; j < c->Dloc; ++j)
+            dptr[(size_t)j + 1] = dptr[(size_t)j] + (uint32_t)c->doclen[(size_t)c->global_of_local[(size_t)j]];
+        CU(cudaMemcpyAsync(c->d_doc_ptr, dptr.data(), sizeof(uint32_t) * dptr.size(), cudaMemcpyHostToDevice, st));
     }
-    c->wave_seg_begin[(size_t)W] = (uint32_t)c->wave_segs.size();
-    lt.mark("wave plan + chunks");
-    const size_t nch = c->chunk_seg.size();
+    if ((s = check_launch(c, "load planning kernels"))) return s;
+    if ((s = sync(c, "load planning"))) return s;
+    c->sorted_tok.clear();
+    c->pos_of_tok.clear();
+    lt.mark("wave plan + chunks (device)");
     c->cells = (size_t)V * I * Kp;
     // doc-topic row layout (sigma order, see spdp_device.cuh): lane gl owns canonical
     // blocks [gl*NB, gl*NB + NB); block q of each lane is stored column-major over lanes
@@ -892,10 +978,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     }
 
     // device allocations
-    ALLOC(c->d_tok_doc, c->Nloc); ALLOC(c->d_tok_id, c->Nloc);
-    ALLOC(c->d_zr, c->Nloc); ALLOC(c->d_zr_next, c->Nloc);
-    ALLOC(c->d_chunk_start, nch); ALLOC(c->d_chunk_end, nch); ALLOC(c->d_chunk_seg, nch);
-    ALLOC(c->d_wave_segs, c->wave_segs.size());
+    ALLOC(c->d_zr, std::max<int64_t>(c->Nloc, 1)); ALLOC(c->d_zr_next, std::max<int64_t>(c->Nloc, 1));
     ALLOC(c->d_sweep, 1);
     {   // prefetch doc-topic rows into L2 only when the array does not live there anyway
         int dev = 0, l2 = 0;
@@ -939,24 +1022,6 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_partial, c->partial_len);
     ALLOC(c->d_scalar, 8);
     {
-        std::vector<uint32_t> tdoc((size_t)c->Nloc), tid((size_t)c->Nloc);
-        for (int64_t q = 0; q < c->Nloc; ++q) {
-            const uint32_t p = c->sorted_tok[(size_t)q];
-            tdoc[(size_t)q] = (uint32_t)c->local_of_doc[(size_t)doc[p]];
-            tid[(size_t)q] = p;
-        }
-        // doc -> sorted-token positions (CSR), for the W = 1 recount of the doc-topic rows
-        std::vector<uint32_t> dptr((size_t)c->Dloc + 1, 0), dpos((size_t)c->Nloc);
-        for (int64_t q = 0; q < c->Nloc; ++q) dptr[(size_t)tdoc[(size_t)q] + 1]++;
-        for (int32_t j = 0; j < c->Dloc; ++j) dptr[(size_t)j + 1] += dptr[(size_t)j];
-        {
-            std::vector<uint32_t> fill(dptr.begin(), dptr.end() - 1);
-            for (int64_t q = 0; q < c->Nloc; ++q) dpos[fill[(size_t)tdoc[(size_t)q]]++] = (uint32_t)q;
-        }
-        ALLOC(c->d_doc_ptr, (size_t)c->Dloc + 1);
-        ALLOC(c->d_doc_pos, std::max<int64_t>(c->Nloc, 1));
-        CU(cudaMemcpy(c->d_doc_ptr, dptr.data(), sizeof(uint32_t) * dptr.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_doc_pos, dpos.data(), sizeof(uint32_t) * dpos.size(), cudaMemcpyHostToDevice));
         std::vector<int32_t> dl((size_t)std::max<int32_t>(c->Dloc, 1), 0), dg((size_t)std::max<int32_t>(c->Dloc, 1), 0);
         for (int32_t j = 0; j < c->Dloc; ++j) {
             dl[(size_t)j] = c->doclen[(size_t)c->global_of_local[(size_t)j]];
@@ -974,12 +1039,6 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             disc[(size_t)i] = (float)c->disc[(size_t)i];
             conc[(size_t)i] = (float)c->conc[(size_t)i];
         }
-        CU(cudaMemcpy(c->d_tok_doc, tdoc.data(), sizeof(uint32_t) * tdoc.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_tok_id, tid.data(), sizeof(uint32_t) * tid.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_chunk_start, c->chunk_start.data(), sizeof(uint32_t) * nch, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_chunk_end, c->chunk_end.data(), sizeof(uint32_t) * nch, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_wave_segs, c->wave_segs.data(), sizeof(uint32_t) * c->wave_segs.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_chunk_seg, c->chunk_seg.data(), sizeof(uint32_t) * std::max<size_t>(nch, 0), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_doclen, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_docgroup, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice));
         CU(cudaMemcpy(c->d_alpha, al.data(), sizeof(float) * al.size(), cudaMemcpyHostToDevice));
@@ -1200,9 +1259,9 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
     const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
     if (perplexity) {
         SweepArgs a = base_args(c);
-        a.nchunks = (int)c->chunk_seg.size();
+        a.nchunks = (int)c->nchunks;
         launch_ppl(c, a, c->d_partial);
-        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(c->d_partial, c->chunk_seg.size(), c->d_scalar);
+        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(c->d_partial, (size_t)c->nchunks, c->d_scalar);
         if ((s = check_launch(c, "perplexity_kernel"))) return s;
         if (gather && (s = nccl_check(c, c->nccl.AllReduce(c->d_scalar, c->d_scalar, 1, kNcclFloat64, kNcclSum, c->comm, c->stream), "allreduce ppl")))
             return s;
@@ -1441,6 +1500,7 @@ spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, dou
     const int I = c->I, K = c->K;
     std::vector<uint32_t> tdoc((size_t)n), tid((size_t)n), cs((size_t)n + 1), ce((size_t)n), seg((size_t)n);
     std::vector<uint16_t> zr((size_t)n);
+    if ((s = ensure_host_plan(c))) return s;
     std::vector<uint16_t> allzr((size_t)c->Nloc);
     CU(cudaMemcpyAsync(allzr.data(), c->d_zr, sizeof(uint16_t) * allzr.size(), cudaMemcpyDeviceToHost, c->stream));
     if ((s = sync(c, "debug zr"))) return s;
@@ -1530,7 +1590,7 @@ spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
     CU(cudaMemcpyAsync(st, c->d_stats, sizeof st, cudaMemcpyDeviceToHost, c->stream));
     if ((s = sync(c, "stats"))) return s;
     out[0] = (int64_t)st[0]; out[1] = (int64_t)st[1]; out[2] = (int64_t)st[2];
-    out[3] = c->sweeps_done; out[4] = c->Nloc; out[5] = c->Dloc; out[6] = c->mmax; out[7] = (int64_t)c->chunk_seg.size();
+    out[3] = c->sweeps_done; out[4] = c->Nloc; out[5] = c->Dloc; out[6] = c->mmax; out[7] = (int64_t)(size_t)c->nchunks;
     out[8] = c->LPT; out[9] = c->KPL; out[10] = c->chunk_tokens; out[11] = c->sample_grid;
     return SPDP_OK;
 }
@@ -1556,6 +1616,10 @@ spdp_status debug_verify(spdp_ctx* c) {
     std::vector<uint16_t> zr((size_t)c->Nloc);
     std::vector<float> nf;
     std::vector<int32_t> n((size_t)c->Dloc * Kp), m(c->cells), t(c->cells), Q((size_t)V * Kp);
+    {
+        spdp_status s0 = ensure_host_plan(c);
+        if (s0) return s0;
+    }
     CU(cudaMemcpy(zr.data(), c->d_zr, 2 * zr.size(), cudaMemcpyDeviceToHost));
     {
         spdp_status s0 = read_rows(c, nf);

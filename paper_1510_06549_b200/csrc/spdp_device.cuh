@@ -976,6 +976,22 @@ __global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restri
 __global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
 
 // ---------------------------------------------------------------- state installation
+// initial topics z_p = floor(x0 K / 2^32) of Philox(seed; p, 0xFFFFFFFF, 0, 0) (reading c11)
+__global__ void init_z_kernel(int32_t* __restrict__ z, uint32_t n, int K, uint32_t k0, uint32_t k1) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const uint4 x = philox(make_uint4(p, 0xFFFFFFFFu, 0u, 0u), k0, k1);
+        z[p] = (int32_t)(((uint64_t)x.x * (uint64_t)K) >> 32);
+    }
+}
+// first invalid z (err[0]) and r (err[1]) index
+__global__ void check_zr_kernel(const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t n, int K,
+                                unsigned long long* __restrict__ err) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        if (z[p] < 0 || z[p] >= K) atomicMin(err, (unsigned long long)p);
+        if (r && r[p] > 1) atomicMin(err + 1, (unsigned long long)p);
+    }
+}
+
 // counts from z: m_{ikw} and, with given r, t_{ikw} = sum r
 __global__ void init_cells_kernel(const int32_t* __restrict__ group, const int32_t* __restrict__ word,
                                   const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t n, int I,
