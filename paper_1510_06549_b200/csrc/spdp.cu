@@ -11,6 +11,7 @@
 #include "spdp_loglik.cuh"
 #include "spdp_eval.cuh"
 #include "spdp_plan.cuh"
+#include "spdp_token.cuh"
 
 #include <dlfcn.h>
 
@@ -115,6 +116,9 @@ struct spdp_ctx {
     void* d_n = nullptr;                          // n_dk rows in sigma order: fp32 or uint16 (row16)
     bool row16 = false;                           // uint16 doc-topic rows (HBM-resident arrays)
     bool async = false;                           // SPDP_UPDATE_ASYNC (NEXT-2): immediate count updates
+    bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
+    uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
+    float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
     int colstart[8] = {0};
@@ -233,6 +237,10 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
 
 #define SPDP_DISPATCH(LPT_, KPL_, CALL)                     \
     switch (LPT_ * 100 + KPL_) {                            \
+        case 116: CALL(1, 16); break;                       \
+        case 132: CALL(1, 32); break;                       \
+        case 216: CALL(2, 16); break;                       \
+        case 232: CALL(2, 32); break;                       \
         case 404: CALL(4, 4); break;                        \
         case 408: CALL(4, 8); break;                        \
         case 416: CALL(4, 16); break;                       \
@@ -262,6 +270,43 @@ void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
 #define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream, c->row16)
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_P)
 #undef CALL_P
+}
+
+// K <= 64: factor table of the wave's segments, then one lane per token (spdp_token.cuh)
+void launch_token(spdp_ctx* c, int w) {
+    const uint32_t r0 = c->wave_seg_begin[(size_t)w], r1 = c->wave_seg_begin[(size_t)w + 1];
+    const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
+    const size_t nf = (size_t)(r1 - r0) * c->Kp;
+    const int fgrid = (int)std::min<size_t>((nf + 255) / 256, 148u * 16u);
+    factor_kernel<<<std::max(fgrid, 1), 256, 0, c->stream>>>(
+        c->d_wave_segs, r0, r1, c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->d_disc, c->d_conc, c->d_tab,
+        c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F);
+    TokenArgs t{};
+    t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
+    t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.F = c->d_F; t.n = c->d_n;
+    t.sigma = c->d_sigma;
+    for (int B = 0; B < 16; ++B) {
+        const int nbl = c->KPL / 4;
+        t.bpos[B] = (B < c->Kp / 4) ? c->colstart[B % nbl] + B / nbl : 0;
+    }
+    t.m = c->d_m; t.t = c->d_t; t.Q = c->d_Q; t.M = c->d_M; t.Tt = c->d_Tt; t.T = c->d_T; t.dmt = c->d_dm;
+    t.alpha = c->d_alpha; t.disc = c->d_disc; t.conc = c->d_conc; t.tab = c->d_tab; t.tab_off = c->d_tab_off;
+    t.beta = (float)c->cfg.beta; t.vbeta = (float)((double)c->V * c->cfg.beta);
+    t.I = c->I; t.K = c->K; t.Kp = c->Kp;
+    t.key0 = (uint32_t)c->cfg.seed; t.key1 = (uint32_t)(c->cfg.seed >> 32);
+    t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats;
+    const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
+    const int nbk = (c->K + 3) / 4;
+#define SPDP_TOK(NBK)                                                                                   \
+    do {                                                                                                \
+        if (c->row16) token_kernel<NBK, uint16_t><<<std::max(grid, 1), 256, 0, c->stream>>>(t);         \
+        else token_kernel<NBK, float><<<std::max(grid, 1), 256, 0, c->stream>>>(t);                     \
+    } while (0)
+    if (nbk <= 4) SPDP_TOK(4);
+    else if (nbk <= 8) SPDP_TOK(8);
+    else SPDP_TOK(16);
+#undef SPDP_TOK
+    c->launches += 1;
 }
 
 SweepArgs base_args(spdp_ctx* c) {
@@ -556,14 +601,18 @@ spdp_status run_waves(spdp_ctx* c) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
         rec(c, 4 * (size_t)w);
         if (ce == cb) { rec(c, 4 * (size_t)w + 1); rec(c, 4 * (size_t)w + 2); rec(c, 4 * (size_t)w + 3); continue; }
-        a.chunk_start = c->d_chunk_start + cb;
-        a.chunk_end = c->d_chunk_end + cb;
-        a.chunk_seg = c->d_chunk_seg + cb;
-        a.nchunks = (int)(ce - cb);
-        a.work = c->d_work + w;
-        launch_sample(c, a, false);
-        rec(c, 4 * (size_t)w + 1);
         const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
+        if (c->token_kernel) {
+            launch_token(c, w);
+        } else {
+            a.chunk_start = c->d_chunk_start + cb;
+            a.chunk_end = c->d_chunk_end + cb;
+            a.chunk_seg = c->d_chunk_seg + cb;
+            a.nchunks = (int)(ce - cb);
+            a.work = c->d_work + w;
+            launch_sample(c, a, false);
+        }
+        rec(c, 4 * (size_t)w + 1);
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
@@ -591,7 +640,7 @@ spdp_status run_waves(spdp_ctx* c) {
             const int blocks = (int)std::min<uint32_t>((se - sb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, c->stream>>>(
                 c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q, c->d_M,
-                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats);
+                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats, (int)c->token_kernel);
         }
         rec(c, 4 * (size_t)w + 3);
         c->launches += 3;
@@ -833,6 +882,9 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         if ((double)c->mmax * (c->mmax + 1) / 2 * sizeof(float2) > 16e9)
             return fail(c, SPDP_ETABLE, "Stirling-ratio table for M_max = %d exceeds 16 GB", c->mmax);
     }
+    // small K: the token kernel (packed per-wave deltas need |delta| <= count(i,w) < 2^15)
+    c->token_kernel = !c->async && c->K <= 64 && c->mmax < 32768;
+    if (const char* e = getenv("SPDP_TOKEN_KERNEL")) c->token_kernel = c->token_kernel && atoi(e) != 0;
     // documents -> ranks
     if (c->G > 1) partition_docs(c->cfg.seed, c->G, num_tokens, num_docs, c->doclen, c->shard_of_doc);
     else c->shard_of_doc.assign((size_t)num_docs, 0);
@@ -905,6 +957,11 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, drlen.p, droff.p, (int)R, st); },
                              "segment offsets")))
                 return s;
+            if (c->token_kernel) {
+                ALLOC(c->d_tok_run, nl);
+                ALLOC(c->d_F, (size_t)R * Kp);
+                token_run_kernel<<<grid, 256, 0, st>>>(droff.p, drlen.p, R, c->d_tok_run);
+            }
             chunk_count_kernel<<<grid, 256, 0, st>>>(drlen.p, R, chunk, dnch.p);
             if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, dnch.p, dchoff.p, (int)R, st); },
                              "chunk offsets")))

@@ -22,6 +22,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_PREFETCH_NEXT
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
+#ifndef SPDP_SKIP_PAD_BLOCKS
+#define SPDP_SKIP_PAD_BLOCKS 1     // sample kernel: no row loads for 4-topic blocks past K
+#endif
 #ifndef SPDP_MINB
 #define SPDP_MINB 4                // resident blocks per SM the sample kernel is compiled for
 #endif
@@ -314,6 +317,9 @@ sample_kernel(SweepArgs A) {
     constexpr int KSPAN = LPT * KPL;
     constexpr int NB = KPL / 4;                      // 4-topic blocks per lane
     static_assert(KPL % 4 == 0 && NB <= 8, "KPL must be a multiple of 4, at most 32");
+    // skipping the loads of blocks past K saves bytes but changes register allocation and
+    // scheduling; measured (B200): a gain at 4x32 and 16x32, a loss at 8x32 (C5) and 32x32 (K = 1000)
+    constexpr bool kSkipPad = SPDP_SKIP_PAD_BLOCKS && (LPT == 4 || LPT == 16);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
@@ -423,7 +429,9 @@ sample_kernel(SweepArgs A) {
             const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + snoff + 4 * gl;
             float4 v[NB];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) v[q] = row_load4<NT, ASYNC>(nl + 4 * A.colstart[q]);
+            for (int q = 0; q < NB; ++q)   // blocks past K hold no topic (zero mass): optionally no load
+                v[q] = (!kSkipPad || kb + 4 * q < K) ? row_load4<NT, ASYNC>(nl + 4 * A.colstart[q])
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -809,7 +817,7 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
                                       void* __restrict__ D, int pack32,
                                       int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
                                       int32_t* __restrict__ T, int I, int Kp, int use_smem_sums,
-                                      unsigned long long* __restrict__ stats) {
+                                      unsigned long long* __restrict__ stats, int packed_deltas) {
     extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
     int* sM = ssum;
     int* sT = ssum + (size_t)I * Kp;
@@ -826,9 +834,18 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
         const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
         for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
             const size_t off = (size_t)seg * Kp + k4;
-            const int4 a = *reinterpret_cast<const int4*>(dm + off);
-            const int4 d = *reinterpret_cast<const int4*>(dt + off);
+            int4 a = *reinterpret_cast<const int4*>(dm + off);
+            int4 d = packed_deltas ? make_int4(0, 0, 0, 0) : *reinterpret_cast<const int4*>(dt + off);
             if ((a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) == 0) continue;
+            if (packed_deltas) {                             // dm * 2^16 + dt (token kernel)
+                int* pa = &a.x; int* pd = &d.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int x = pa[e];
+                    pd[e] = (int)(short)(x & 0xFFFF);
+                    pa[e] = (int)((unsigned)x - (unsigned)pd[e]) >> 16;
+                }
+            }
             int4 vm = *reinterpret_cast<const int4*>(m + off);
             int4 vt = *reinterpret_cast<const int4*>(t + off);
             const int4 om = vm, ot = vt;
@@ -846,7 +863,7 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
             *reinterpret_cast<int4*>(m + off) = vm;
             *reinterpret_cast<int4*>(t + off) = vt;
             *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
-            *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
+            if (!packed_deltas) *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
             const int cm[4] = {vm.x - om.x, vm.y - om.y, vm.z - om.z, vm.w - om.w};
             const int ct[4] = {vt.x - ot.x, vt.y - ot.y, vt.z - ot.z, vt.w - ot.w};
             if (D) {
