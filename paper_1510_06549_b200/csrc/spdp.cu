@@ -104,6 +104,16 @@ struct spdp_ctx {
     // multi-GPU net change since the sweep start, packed dm*2^B + dt (B = 16: int32, else int64)
     void *d_Dloc = nullptr, *d_Dsum = nullptr;
     bool pack32 = true;
+    // exchange pipelining (W = 1): the sweep runs in P word-range parts; part p's rows are
+    // all-reduced and merged on comm_stream while part p+1 samples
+    int P = 1;
+    bool overlap = false;
+    std::vector<uint32_t> part_word, part_run, part_tok, part_chunk;   // [P + 1] boundaries
+    cudaStream_t comm_stream = nullptr;
+    std::vector<cudaEvent_t> part_ev;
+    cudaEvent_t comm_done = nullptr;
+    int32_t *d_Mn = nullptr, *d_Ttn = nullptr, *d_Tn = nullptr;    // deferred local sums (sampling reads the snapshot)
+    int32_t *d_Mf = nullptr, *d_Ttf = nullptr, *d_Tf = nullptr;    // sums after the pipelined exchange
     size_t dbytes() const { return cells * (pack32 ? 4 : 8); }
 
     // device
@@ -273,9 +283,7 @@ void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
 }
 
 // K <= 64: factor table of the wave's segments, then one lane per token (spdp_token.cuh)
-void launch_token(spdp_ctx* c, int w) {
-    const uint32_t r0 = c->wave_seg_begin[(size_t)w], r1 = c->wave_seg_begin[(size_t)w + 1];
-    const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
+void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t te) {
     const size_t nf = (size_t)(r1 - r0) * c->Kp;
     const int fgrid = (int)std::min<size_t>((nf + 255) / 256, 148u * 16u);
     factor_kernel<<<std::max(fgrid, 1), 256, 0, c->stream>>>(
@@ -351,21 +359,27 @@ void launch_merge(spdp_ctx* c, int32_t* dm, int32_t* dt) {
         dm == nullptr);
 }
 
-// after the all-reduce Dloc -> Dsum: rows = S0 + sum of D, clamp, Dloc = 0, Q and sums
+// after the all-reduce Dloc -> Dsum: rows of words [w0, w1) = S0 + sum of D, clamp, Dloc = 0,
+// Q rows, and the rows' contributions to the sums added into (M, Tt, T)
+void launch_exchange_merge_range(spdp_ctx* c, int w0, int w1, int32_t* M, int32_t* Tt, int32_t* T, cudaStream_t st) {
+    const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
+    const int use_smem = smem <= 48 * 1024;
+    if (w1 <= w0) return;
+    const int grid = std::min(merge_grid(), (w1 - w0 + 7) / 8);
+    if (c->pack32)
+        exchange_merge_kernel<int32_t><<<grid, 256, use_smem ? smem : 0, st>>>(
+            c->d_m, c->d_t, (int32_t*)c->d_Dloc, (const int32_t*)c->d_Dsum, c->d_Q, M, Tt, T, w0, w1, c->I, c->Kp,
+            use_smem, c->d_stats);
+    else
+        exchange_merge_kernel<long long><<<grid, 256, use_smem ? smem : 0, st>>>(
+            c->d_m, c->d_t, (long long*)c->d_Dloc, (const long long*)c->d_Dsum, c->d_Q, M, Tt, T, w0, w1, c->I, c->Kp,
+            use_smem, c->d_stats);
+}
 void launch_exchange_merge(spdp_ctx* c) {
     cudaMemsetAsync(c->d_M, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
     cudaMemsetAsync(c->d_Tt, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
     cudaMemsetAsync(c->d_T, 0, sizeof(int32_t) * (size_t)c->Kp, c->stream);
-    const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
-    const int use_smem = smem <= 48 * 1024;
-    if (c->pack32)
-        exchange_merge_kernel<int32_t><<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
-            c->d_m, c->d_t, (int32_t*)c->d_Dloc, (const int32_t*)c->d_Dsum, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V, c->I,
-            c->Kp, use_smem, c->d_stats);
-    else
-        exchange_merge_kernel<long long><<<merge_grid(), 256, use_smem ? smem : 0, c->stream>>>(
-            c->d_m, c->d_t, (long long*)c->d_Dloc, (const long long*)c->d_Dsum, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->V,
-            c->I, c->Kp, use_smem, c->d_stats);
+    launch_exchange_merge_range(c, 0, c->V, c->d_M, c->d_Tt, c->d_T, c->stream);
 }
 
 // SPDP_VERBOSE=1: phase times of spdp_load_corpus on stderr
@@ -561,10 +575,99 @@ inline void rec(spdp_ctx* c, size_t j) {
     if (c->profiling) cudaEventRecord(c->ev[j], c->stream);
 }
 
+// W = 1 in P word-range parts (DESIGN.md §5 "exchange pipelining").  Semantics are those of the
+// single wave: every token decides against the sweep-start snapshot.  Rows of part p are only read
+// by part p's tokens, so they may be merged (and, with several ranks, all-reduced and merged again)
+// while later parts sample; the sums M, Tt, T are read by every token and are updated only after
+// the last part (deferred into d_Mn...; with the pipelined exchange rebuilt into d_Mf...).
+spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
+    const size_t isz = sizeof(int32_t) * (size_t)c->I * c->Kp, ksz = sizeof(int32_t) * (size_t)c->Kp;
+    cudaStream_t st = c->stream;
+    CU(cudaMemcpyAsync(c->d_Mn, c->d_M, isz, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(c->d_Ttn, c->d_Tt, isz, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(c->d_Tn, c->d_T, ksz, cudaMemcpyDeviceToDevice, st));
+    if (c->overlap) {
+        // comm_stream starts after the main stream's previous read of d_Mf... (and everything before)
+        CU(cudaEventRecord(c->part_ev[0], st));
+        CU(cudaStreamWaitEvent(c->comm_stream, c->part_ev[0], 0));
+        CU(cudaMemsetAsync(c->d_Mf, 0, isz, c->comm_stream));
+        CU(cudaMemsetAsync(c->d_Ttf, 0, isz, c->comm_stream));
+        CU(cudaMemsetAsync(c->d_Tf, 0, ksz, c->comm_stream));
+    }
+    void* Dnet = c->G > 1 ? c->d_Dloc : nullptr;
+    const size_t smem = sizeof(int) * (size_t)(2 * c->I + 1) * c->Kp;
+    const int use_smem = smem <= 48 * 1024;
+    const size_t row_cells = (size_t)c->I * c->Kp;          // cells per word
+    const size_t esz = c->pack32 ? 4 : 8;
+    rec(c, 0);
+    for (int p = 0; p < c->P; ++p) {
+        const uint32_t cb = c->part_chunk[(size_t)p], ce = c->part_chunk[(size_t)p + 1];
+        const uint32_t rb = c->part_run[(size_t)p], re = c->part_run[(size_t)p + 1];
+        const uint32_t tb = c->part_tok[(size_t)p], te = c->part_tok[(size_t)p + 1];
+        if (te > tb) {
+            if (c->token_kernel) {
+                launch_token(c, rb, re, tb, te);
+            } else {
+                a.chunk_start = c->d_chunk_start + cb;
+                a.chunk_end = c->d_chunk_end + cb;
+                a.chunk_seg = c->d_chunk_seg + cb;
+                a.nchunks = (int)(ce - cb);
+                a.work = c->d_work + p;
+                launch_sample(c, a, false);
+            }
+            const int blocks = (int)std::min<uint32_t>((re - rb + 7) / 8, 148u * 4u);
+            merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, st>>>(
+                c->d_wave_segs + rb, (int)(re - rb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q,
+                c->d_Mn, c->d_Ttn, c->d_Tn, c->I, c->Kp, use_smem, c->d_stats, (int)c->token_kernel);
+            c->launches += 2;
+        }
+        if (c->overlap) {                                   // rows of part p: all-reduce + merge on comm_stream
+            const int w0 = (int)c->part_word[(size_t)p], w1 = (int)c->part_word[(size_t)p + 1];
+            CU(cudaEventRecord(c->part_ev[(size_t)p], st));
+            CU(cudaStreamWaitEvent(c->comm_stream, c->part_ev[(size_t)p], 0));
+            if (w1 > w0) {
+                const size_t off = (size_t)w0 * row_cells, cnt = (size_t)(w1 - w0) * row_cells;
+                char* dl = (char*)c->d_Dloc + off * esz;
+                char* ds = (char*)c->d_Dsum + off * esz;
+                spdp_status s = nccl_check(c, c->nccl.AllReduce(dl, ds, cnt, c->pack32 ? kNcclInt32 : kNcclInt64, kNcclSum,
+                                                                c->comm, c->comm_stream), "ncclAllReduce(part)");
+                if (s) return s;
+                launch_exchange_merge_range(c, w0, w1, c->d_Mf, c->d_Ttf, c->d_Tf, c->comm_stream);
+                c->launches += 1;
+            }
+        }
+    }
+    rec(c, 1);
+    const size_t rsm = sizeof(int) * 8 * (size_t)c->Kp;      // every token moved to zr_next: rebuild n, swap
+    if (c->row16)
+        recount_docs_kernel<uint16_t><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
+                                                                c->Dloc, c->Kp, (uint16_t*)c->d_n);
+    else
+        recount_docs_kernel<float><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
+                                                             c->Dloc, c->Kp, (float*)c->d_n);
+    std::swap(c->d_zr, c->d_zr_next);
+    rec(c, 2);
+    if (c->overlap) {
+        CU(cudaEventRecord(c->comm_done, c->comm_stream));
+        CU(cudaStreamWaitEvent(st, c->comm_done, 0));
+        CU(cudaMemcpyAsync(c->d_M, c->d_Mf, isz, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(c->d_Tt, c->d_Ttf, isz, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(c->d_T, c->d_Tf, ksz, cudaMemcpyDeviceToDevice, st));
+    } else {
+        CU(cudaMemcpyAsync(c->d_M, c->d_Mn, isz, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(c->d_Tt, c->d_Ttn, isz, cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(c->d_T, c->d_Tn, ksz, cudaMemcpyDeviceToDevice, st));
+    }
+    rec(c, 3);
+    c->launches += 1;
+    c->acc[5] += 1;
+    return check_launch(c, "sweep parts");
+}
+
 spdp_status run_waves(spdp_ctx* c) {
     SweepArgs a = base_args(c);
     CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
-    CU(cudaMemsetAsync(c->d_work, 0, sizeof(uint32_t) * ((size_t)c->W + 2), c->stream));
+    CU(cudaMemsetAsync(c->d_work, 0, sizeof(uint32_t) * ((size_t)std::max(c->W, c->P) + 2), c->stream));
     if (c->profiling) { spdp_status s = ensure_events(c); if (s) return s; }
     void* Dnet = c->G > 1 ? c->d_Dloc : nullptr;
     if (c->async) {
@@ -597,13 +700,14 @@ spdp_status run_waves(spdp_ctx* c) {
         c->acc[5] += 1;
         return check_launch(c, "async sweep");
     }
+    if (c->P > 1) return run_parts(c, a);
     for (int w = 0; w < c->W; ++w) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
         rec(c, 4 * (size_t)w);
         if (ce == cb) { rec(c, 4 * (size_t)w + 1); rec(c, 4 * (size_t)w + 2); rec(c, 4 * (size_t)w + 3); continue; }
         const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
         if (c->token_kernel) {
-            launch_token(c, w);
+            launch_token(c, c->wave_seg_begin[(size_t)w], c->wave_seg_begin[(size_t)w + 1], tb, te);
         } else {
             a.chunk_start = c->d_chunk_start + cb;
             a.chunk_end = c->d_chunk_end + cb;
@@ -881,6 +985,27 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             return fail(c, SPDP_ETABLE, "M_max = %d: cells are packed in 16 bits (M_max < 65536)", c->mmax);
         if ((double)c->mmax * (c->mmax + 1) / 2 * sizeof(float2) > 16e9)
             return fail(c, SPDP_ETABLE, "Stirling-ratio table for M_max = %d exceeds 16 GB", c->mmax);
+        // word-range parts of the sweep (W = 1 only): balanced by the corpus' token counts, so that
+        // every rank cuts at the same words (the all-reduce slices must match)
+        // (each part costs a launch tail: pipelining pays when a rank samples many tokens, measured
+        // +11% (C3) and +40% (C2) sampling time for 4 parts on one GPU)
+        c->P = (W == 1 && c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL && !c->async &&
+                num_tokens / c->G >= (int64_t)8000000) ? 4 : 1;
+        if (const char* e = getenv("SPDP_EXCHANGE_PARTS")) c->P = std::min(std::max(atoi(e), 1), 16);
+        if (W != 1 || c->async) c->P = 1;
+        c->part_word.assign((size_t)c->P + 1, (uint32_t)V);
+        c->part_word[0] = 0;
+        if (c->P > 1) {
+            std::vector<int32_t> cnt((size_t)I * V);
+            CU(cudaMemcpyAsync(cnt.data(), dcnt.p, sizeof(int32_t) * cnt.size(), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            int64_t run = 0;
+            int p = 1;
+            for (int w = 0; w < V && p < c->P; ++w) {
+                for (int i = 0; i < I; ++i) run += cnt[(size_t)i * V + w];
+                while (p < c->P && run * c->P >= (int64_t)p * num_tokens) c->part_word[(size_t)p++] = (uint32_t)(w + 1);
+            }
+        }
     }
     // small K: the token kernel (packed per-wave deltas need |delta| <= count(i,w) < 2^15)
     c->token_kernel = !c->async && c->K <= 64 && c->mmax < 32768;
@@ -922,11 +1047,23 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     // wave plan: stable sort of the local tokens by (wave = l mod W, w * I + i)
     const uint64_t S = (uint64_t)V * I;
     const uint32_t chunk = (uint32_t)c->chunk_tokens;
+    const int Pp = c->P;
     uint32_t R = 0, nch = 0;
+    TempBuf<uint32_t> dpartseg((size_t)Pp + 1);
+    if (!dpartseg.p) return fail(c, SPDP_ENOMEM, "part buffer");
+    {
+        std::vector<uint32_t> ps((size_t)Pp + 1);
+        for (int p = 0; p <= Pp; ++p) ps[(size_t)p] = c->part_word[(size_t)p] * (uint32_t)I;
+        CU(cudaMemcpyAsync(dpartseg.p, ps.data(), sizeof(uint32_t) * ps.size(), cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    c->part_chunk.assign((size_t)Pp + 1, 0);
+    c->part_run.assign((size_t)Pp + 1, 0);
+    c->part_tok.assign((size_t)Pp + 1, 0);
     {
         const size_t nl = std::max<uint32_t>(nloc, 1);
         TempBuf<uint64_t> dkey(nl), dkey2(nl), drkey(nl);
-        TempBuf<uint32_t> drlen(nl), droff(nl), dnch(nl), dchoff(nl), dR(1), dwb((size_t)W + 1);
+        TempBuf<uint32_t> drlen(nl), droff(nl), dnch(nl), dchoff(nl), dR(1), dwb((size_t)std::max(W, Pp) + 1);
         if (!dkey.p || !dkey2.p || !drkey.p || !drlen.p || !droff.p || !dnch.p || !dchoff.p || !dR.p || !dwb.p)
             return fail(c, SPDP_ENOMEM, "wave plan buffers");
         ALLOC(c->d_tok_id, nl);
@@ -977,21 +1114,45 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             TempBuf<uint32_t> cs(nc), ce(nc), cg(nc), ci(nc), ci2(nc);
             TempBuf<uint64_t> ck(nc), ck2(nc);
             if (!cs.p || !ce.p || !cg.p || !ci.p || !ci2.p || !ck.p || !ck2.p) return fail(c, SPDP_ENOMEM, "chunk buffers");
-            chunk_emit_kernel<<<grid, 256, 0, st>>>(drkey.p, drlen.p, droff.p, dchoff.p, R, chunk, S, cs.p, ce.p, cg.p,
-                                                    ck.p, ci.p);
+            chunk_emit_kernel<<<grid, 256, 0, st>>>(drkey.p, drlen.p, droff.p, dchoff.p, R, chunk, S, dpartseg.p, Pp,
+                                                    cs.p, ce.p, cg.p, ck.p, ci.p);
             if ((s = cub_run([&](void* t, size_t& b) {
                      return cub::DeviceRadixSort::SortPairs(t, b, ck.p, ck2.p, ci.p, ci2.p, (int)nch, 0,
-                                                            bits((uint64_t)W * (chunk + 1)), st);
+                                                            bits((uint64_t)W * Pp * (chunk + 1)), st);
                  }, "chunk order")))
                 return s;
             gather3_kernel<<<grid, 256, 0, st>>>(ci2.p, nch, cs.p, ce.p, cg.p, c->d_chunk_start, c->d_chunk_end,
                                                  c->d_chunk_seg);
-            bounds_kernel<<<grid, 256, 0, st>>>(WaveOfChunkKey{ck2.p, (uint64_t)chunk + 1}, nch, (uint32_t)W, dwb.p);
+            bounds_kernel<<<grid, 256, 0, st>>>(WaveOfChunkKey{ck2.p, (uint64_t)(chunk + 1) * Pp}, nch, (uint32_t)W, dwb.p);
             CU(cudaMemcpyAsync(c->wave_chunk_begin.data(), dwb.p, sizeof(uint32_t) * ((size_t)W + 1), cudaMemcpyDeviceToHost, st)); CU(cudaStreamSynchronize(st));
+            if (Pp > 1) {                                  // W = 1: chunk ranges of the parts
+                bounds_kernel<<<grid, 256, 0, st>>>(WaveOfChunkKey{ck2.p, (uint64_t)chunk + 1}, nch, (uint32_t)Pp, dwb.p);
+                CU(cudaMemcpyAsync(c->part_chunk.data(), dwb.p, sizeof(uint32_t) * ((size_t)Pp + 1), cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+            }
+        }
+        if (Pp > 1) {                                      // run and token ranges of the parts
+            std::vector<uint32_t> rs(R), ro(R);
+            if (R > 0) {
+                CU(cudaMemcpyAsync(rs.data(), c->d_wave_segs, sizeof(uint32_t) * R, cudaMemcpyDeviceToHost, st));
+                CU(cudaMemcpyAsync(ro.data(), droff.p, sizeof(uint32_t) * R, cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+            }
+            for (int p = 0; p <= Pp; ++p) {
+                const uint32_t sfirst = c->part_word[(size_t)p] * (uint32_t)I;
+                const uint32_t r = (uint32_t)(std::lower_bound(rs.begin(), rs.end(), sfirst) - rs.begin());
+                c->part_run[(size_t)p] = r;
+                c->part_tok[(size_t)p] = r < R ? ro[r] : nloc;
+            }
         }
     }
     c->nchunks = nch;
     c->nsegs = R;
+    if (c->P == 1) {
+        c->part_chunk = {0u, nch};
+        c->part_run = {0u, R};
+        c->part_tok = {0u, nloc};
+    }
     // doc of every sorted position, and the doc -> sorted-positions CSR (W = 1 recount)
     {
         const size_t nl = std::max<uint32_t>(nloc, 1);
@@ -1057,7 +1218,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         c->d_n = nb;
         CU(cudaMemset(c->d_n, 0, row_bytes(c)));
     }
-    ALLOC(c->d_work, (size_t)W + 2);
+    ALLOC(c->d_work, (size_t)std::max(W, c->P) + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
     ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);
     if (c->G > 1) {
@@ -1070,6 +1231,17 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     }
     ALLOC(c->d_Q, (size_t)V * Kp);
     ALLOC(c->d_M, (size_t)I * Kp); ALLOC(c->d_Tt, (size_t)I * Kp); ALLOC(c->d_T, (size_t)Kp);
+    if (c->P > 1) {
+        ALLOC(c->d_Mn, (size_t)I * Kp); ALLOC(c->d_Ttn, (size_t)I * Kp); ALLOC(c->d_Tn, (size_t)Kp);
+        c->overlap = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
+        if (c->overlap) {
+            ALLOC(c->d_Mf, (size_t)I * Kp); ALLOC(c->d_Ttf, (size_t)I * Kp); ALLOC(c->d_Tf, (size_t)Kp);
+            CU(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+            c->part_ev.resize((size_t)c->P, nullptr);
+            for (auto& e : c->part_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming));
+        }
+    }
     ALLOC(c->d_doclen, std::max<int32_t>(c->Dloc, 1)); ALLOC(c->d_docgroup, std::max<int32_t>(c->Dloc, 1));
     ALLOC(c->d_alpha, (size_t)I * Kp); ALLOC(c->d_alpha64, (size_t)I * Kp);
     ALLOC(c->d_disc, I); ALLOC(c->d_conc, I); ALLOC(c->d_disc64, I); ALLOC(c->d_conc64, I);
@@ -1203,7 +1375,7 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
         return fail(c, SPDP_ESTATE, "SPDP_EXCHANGE_EXTERNAL: use spdp_sweep_local / spdp_sweep_merge");
     for (int it = 0; it < num_sweeps; ++it) {
         if ((s = run_waves(c))) return s;
-        if (c->G > 1) {
+        if (c->G > 1 && !c->overlap) {
             rec(c, 4 * (size_t)c->W);
             if ((s = nccl_check(c, c->nccl.AllReduce(c->d_Dloc, c->d_Dsum, c->cells, c->pack32 ? kNcclInt32 : kNcclInt64,
                                                      kNcclSum, c->comm, c->stream),
@@ -1216,7 +1388,7 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
         if ((s = finish_sweep(c))) return s;
         if (c->profiling) {
             if ((s = sync(c, "spdp_sweep"))) return s;
-            collect_times(c, c->G > 1);
+            collect_times(c, c->G > 1 && !c->overlap);
         }
         if (c->cfg.debug_checks) {
             if ((s = sync(c, "spdp_sweep"))) return s;
@@ -1660,6 +1832,9 @@ void spdp_destroy(spdp_ctx* c) {
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->h_zr_canon) cudaFreeHost(c->h_zr_canon);
     if (c->comm && c->nccl.CommDestroy) c->nccl.CommDestroy(c->comm);
+    if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
+    for (cudaEvent_t e : c->part_ev) cudaEventDestroy(e);
+    if (c->comm_done) cudaEventDestroy(c->comm_done);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -916,12 +916,13 @@ __global__ void net_change_kernel(const int32_t* __restrict__ m, const int32_t* 
 
 // After the all-reduce (out of place: Dloc = this rank's D, Dsum = sum over
 // ranks): m = (m - dm_loc) + dm_sum, t = clamp((t - dt_loc) + dt_sum) into
-// [min(1,m), m]; Dloc = 0; Q_w = sum_i t and the marginal sums M, Tt, T into
-// zeroed buffers.  One pass over the rows; one warp per word.
+// [min(1,m), m]; Dloc = 0; Q_w = sum_i t and the rows' contributions to the
+// marginal sums M, Tt, T (added into the given buffers).  Words [w0, w1): one
+// pass over their rows, one warp per word.
 template <typename P>
 __global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t, P* __restrict__ Dloc,
                                       const P* __restrict__ Dsum, int32_t* __restrict__ Q, int32_t* __restrict__ M,
-                                      int32_t* __restrict__ Tt, int32_t* __restrict__ T, int V, int I, int Kp,
+                                      int32_t* __restrict__ Tt, int32_t* __restrict__ T, int w0, int w1, int I, int Kp,
                                       int use_smem_sums, unsigned long long* __restrict__ stats) {
     extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
     int* sM = ssum;
@@ -934,7 +935,7 @@ __global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restri
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     unsigned clamped = 0;
-    for (int w = blockIdx.x * wpb + (threadIdx.x >> 5); w < V; w += gridDim.x * wpb) {
+    for (int w = w0 + blockIdx.x * wpb + (threadIdx.x >> 5); w < w1; w += gridDim.x * wpb) {
         for (int k4 = lane * 4; k4 < Kp; k4 += 128) {
             int4 q = make_int4(0, 0, 0, 0);
             for (int i = 0; i < I; ++i) {

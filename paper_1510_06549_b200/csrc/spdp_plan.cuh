@@ -99,13 +99,17 @@ __global__ void chunk_count_kernel(const uint32_t* __restrict__ run_len, uint32_
 // chunks of each run (segment of a wave), in segment order; sort key (wave, longest first)
 __global__ void chunk_emit_kernel(const uint64_t* __restrict__ run_key, const uint32_t* __restrict__ run_len,
                                   const uint32_t* __restrict__ run_off, const uint32_t* __restrict__ chunk_off,
-                                  uint32_t R, uint32_t chunk, uint64_t S, uint32_t* __restrict__ cstart,
+                                  uint32_t R, uint32_t chunk, uint64_t S, const uint32_t* __restrict__ part_seg,
+                                  int P, uint32_t* __restrict__ cstart,
                                   uint32_t* __restrict__ cend, uint32_t* __restrict__ cseg, uint64_t* __restrict__ ckey,
                                   uint32_t* __restrict__ cidx) {
     for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
         const uint64_t key = run_key[r];
-        const uint64_t wave = key / S;
         const uint32_t seg = (uint32_t)(key % S);
+        // word-range part of the segment (exchange pipelining, W = 1): part_seg[j] = first segment of part j
+        int part = 0;
+        for (int j = 1; j < P; ++j) part += (seg >= part_seg[j]) ? 1 : 0;
+        const uint64_t wave = (key / S) * (uint64_t)P + (uint64_t)part;
         const uint32_t off = run_off[r], len = run_len[r];
         uint32_t c = chunk_off[r];
         for (uint32_t s = 0; s < len; s += chunk, ++c) {

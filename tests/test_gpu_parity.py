@@ -196,3 +196,54 @@ def test_perplexity_trajectory_free_running_c2_100_sweeps():
             traj.append((s + 1, g.perplexity(), o.perplexity()))
     last = traj[-1]
     assert abs(last[1] / last[2] - 1) <= 0.01, traj
+
+
+@pytest.mark.parametrize("name,K", [("C1", 10), ("C1", 100), ("C2", 50)])
+def test_word_range_parts_equal_single_wave(name, K, monkeypatch):
+    """The sweep in P word-range parts (the exchange pipeline's schedule)
+    is the same W = 1 sweep: identical state after 3 sweeps, for the token kernel
+    (K <= 64) and the chunk kernel."""
+    c = corpus(name)
+    ref = spdp.sampler_for(c, K, **HYPER)
+    ref.sweep(3)
+    want = ref.counts()
+    monkeypatch.setenv("SPDP_EXCHANGE_PARTS", "4")
+    g = spdp.sampler_for(c, K, **HYPER)
+    g.sweep(3)
+    got = g.counts()
+    for k in ("z", "r", "n", "m", "t", "Q"):
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    assert g.perplexity() == pytest.approx(ref.perplexity(), rel=1e-12)   # per-chunk partials in another order
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_multi_rank_parts_match_oracle_shards(G, monkeypatch):
+    """G ranks (external exchange) sampling in word-range parts: still the oracle's
+    G-shard sweep, bit for bit."""
+    monkeypatch.setenv("SPDP_EXCHANGE_PARTS", "3")
+    c = corpus("C1")
+    ranks = [spdp.sampler_for(c, 10, rank=r, world_size=G, exchange=spdp.SPDP_EXCHANGE_EXTERNAL, **HYPER)
+             for r in range(G)]
+    o = oracle.from_corpus(c, 10, **HYPER)
+    for s in range(2):
+        for r in ranks:
+            r.sweep_local()
+        bufs = [r.exchange_get() for r in ranks]
+        with np.errstate(over="ignore"):
+            tot = sum(b.astype(np.int64) for b in bufs).astype(bufs[0].dtype)
+        for r in ranks:
+            r.exchange_put(tot)
+            r.sweep_merge()
+        z = np.full(c.num_tokens, -1, np.int32)
+        for r in ranks:
+            cr = r.counts()
+            own = np.asarray(spdp.spdp_partition(7, G, c.doc, c.num_docs))[c.doc] == ranks.index(r)
+            z[own] = cr["z"][own]
+        forced = np.full(c.num_tokens, -1, np.int32)
+        o.sweep_par(waves=1, shards=G)
+        oc = o.state()
+        mism = np.count_nonzero(z != oc["z"])
+        assert mism <= max(1, 1e-4 * c.num_tokens), mism
+        if mism == 0:
+            for k in ("m", "t", "Q"):
+                np.testing.assert_array_equal(ranks[0].counts()[k], oc[k], err_msg=k)
