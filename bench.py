@@ -253,9 +253,10 @@ def main():
     sample_ms = tm["sample_ms"] / max(tm["sample_launches"], 1) * args.waves   # per sweep (all waves)
     bytes_sweep = alg_bytes(plan, K)
     achieved = bytes_sweep / (sample_ms / 1e3) / 1e9
-    traffic = load_traffic(cfg.name, K)
+    kname = "token_kernel" if stats.get("token_kernel") else "sample_kernel"
+    traffic = load_traffic(cfg.name, K, kname.split("_")[0])
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "sample_kernel",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
             "alg_bytes_per_launch": int(bytes_sweep / max(args.waves, 1)), "peak_source": peak_src,
             "sample_ms_per_sweep": round(sample_ms, 4), "share_of_step": round(sample_ms / ms, 3)}
 

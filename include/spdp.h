@@ -242,7 +242,10 @@ spdp_status spdp_debug_probs(spdp_ctx* ctx, int64_t n, const int64_t* tok_ids, d
  * tokens, out[2] clamped cells, out[3] sweeps done, out[4] local tokens,
  * out[5] local docs, out[6] M_max (largest count(i,w)), out[7] chunks,
  * out[8] lanes per token, out[9] topics per lane, out[10] tokens per chunk,
- * out[11] resident sample-kernel blocks (persistent grid).  out has 12 slots. */
+ * out[11] resident sample-kernel blocks (persistent grid), out[12] 1 if the
+ * token kernel samples (K <= 64), out[13] word-range parts of the sweep
+ * (exchange pipelining), out[14] 1 if doc-topic rows are uint16, out[15] 1
+ * for SPDP_UPDATE_ASYNC.  out has 16 slots. */
 spdp_status spdp_stats(spdp_ctx* ctx, int64_t* out);
 
 /* Phase timing with CUDA events recorded on the context's stream around each

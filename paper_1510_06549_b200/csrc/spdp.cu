@@ -1821,6 +1821,7 @@ spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
     out[0] = (int64_t)st[0]; out[1] = (int64_t)st[1]; out[2] = (int64_t)st[2];
     out[3] = c->sweeps_done; out[4] = c->Nloc; out[5] = c->Dloc; out[6] = c->mmax; out[7] = (int64_t)(size_t)c->nchunks;
     out[8] = c->LPT; out[9] = c->KPL; out[10] = c->chunk_tokens; out[11] = c->sample_grid;
+    out[12] = c->token_kernel ? 1 : 0; out[13] = c->P; out[14] = c->row16 ? 1 : 0; out[15] = c->async ? 1 : 0;
     return SPDP_OK;
 }
 

@@ -25,6 +25,7 @@ KEYS = {
     "smsp__average_warp_latency_per_inst_issued.ratio": "cycles_per_issue",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
          "second": 1e3}
 
 
