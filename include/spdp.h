@@ -96,6 +96,9 @@ typedef struct {
     void* stream;                  /* cudaStream_t to order work on; NULL -> a stream owned by the context */
     int32_t debug_checks;          /* 1 = verify count invariants after every sweep (slow) */
     int32_t update_mode;           /* SPDP_UPDATE_* */
+    int32_t merge_every;           /* world_size > 1: exchange the ranks' count changes after every
+                                      merge_every waves (bounded staleness, SURVEY.md §8(f) NEXT-3;
+                                      PAPER.md:2427-2434); 0 = once per sweep (Alg.3) */
 } spdp_config;
 
 /* Create a context on cfg->device.  Validates the hyper-parameters
@@ -155,6 +158,10 @@ spdp_status spdp_sweep(spdp_ctx* ctx, int32_t num_sweeps);
  * calls spdp_sweep_merge (Alg.3: rows = sweep-start
  * state + summed changes, t clamped, Q and the sums recomputed). */
 spdp_status spdp_sweep_local(spdp_ctx* ctx);
+/* Exchange blocks per sweep (merge_every): the caller repeats
+ * {spdp_sweep_local, sum over ranks, spdp_sweep_merge} *nblocks times per
+ * sweep; each spdp_sweep_local runs the next merge_every waves. */
+spdp_status spdp_exchange_blocks(spdp_ctx* ctx, int32_t* nblocks);
 spdp_status spdp_exchange_buffer(spdp_ctx* ctx, void** device_ptr, int64_t* count, int32_t* elem_bytes);
 spdp_status spdp_sweep_merge(spdp_ctx* ctx);
 /* Copy the exchange buffer to (to_device = 0) or from (to_device = 1) the

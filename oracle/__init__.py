@@ -51,6 +51,8 @@ def lib():
         L.or_sweep_seq.argtypes = [P, C.c_int64]
         L.or_sweep_par.restype = C.c_int
         L.or_sweep_par.argtypes = [P, C.c_int, C.c_int, P, P, C.c_int64, P]
+        L.or_sweep_par_e.restype = C.c_int
+        L.or_sweep_par_e.argtypes = [P, C.c_int, C.c_int, C.c_int, P, P, C.c_int64, P]
         L.or_get.argtypes = [P] + [P] * 6
         L.or_sweep_index.restype = C.c_uint32
         L.or_sweep_index.argtypes = [P]
@@ -155,13 +157,16 @@ class Oracle:
             raise RuntimeError("or_sweep_seq failed")
 
     def sweep_par(self, waves: int = 1, shards: int = 1, force_zr=None, want_margin=False, max_tokens: int = -1,
-                  want_own=False):
+                  want_own=False, merge_every: int = 0):
         """Mode-P sweep.  Returns margin [N] (or None), and with want_own also the
-        oracle's own draws z | r<<15 [N] (before force_zr replaced them)."""
+        oracle's own draws z | r<<15 [N] (before force_zr replaced them).
+        merge_every E >= 1: the shards exchange after every E waves (NEXT-3)."""
         f = None if force_zr is None else np.ascontiguousarray(force_zr, np.int32)
         mg = np.full(self.N, np.inf) if want_margin else None
         own = np.full(self.N, -1, np.int32) if want_own else None
-        if lib().or_sweep_par(self.h, int(waves), int(shards), _ptr(f), _ptr(mg), int(max_tokens), _ptr(own)) != 0:
+        rc = lib().or_sweep_par_e(self.h, int(waves), int(shards), int(merge_every), _ptr(f), _ptr(mg),
+                                  int(max_tokens), _ptr(own))
+        if rc != 0:
             raise RuntimeError("or_sweep_par failed")
         return (mg, own) if want_own else mg
 

@@ -472,8 +472,13 @@ static int64_t clamp_cells(size_t cells, const int32_t *m, int32_t *t) {
  * own_zr (optional, [N]): the oracle's own draw (z | r<<15) before forcing.
  * max_tokens >= 0 limits the sweep to the first max_tokens tokens of each
  * shard's canonical order (timing samples only). */
+/* E >= 1: the shards exchange (merge) after every E waves instead of once per
+ * sweep (bounded staleness; P:2427-2434 relies on
+ * "implicit synchronization ... as long as the delay can be tolerated"): each
+ * block of E waves starts from the merged state of the previous block.
+ * E <= 0 (or E >= the number of waves): one exchange per sweep. */
 static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *force_zr, double *margin,
-                          int64_t max_tokens, int32_t *own_zr, int32_t *Dout_m, int32_t *Dout_t) {
+                          int64_t max_tokens, int32_t *own_zr, int32_t *Dout_m, int32_t *Dout_t, int E) {
     int I = s->I, V = s->V, K = s->K;
     int64_t N = s->N;
     size_t cells = (size_t)I * V * K;
@@ -488,24 +493,30 @@ static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *forc
     int32_t *newz = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
     int8_t *newr = (int8_t *)malloc((size_t)(N + 1)), *rrem = (int8_t *)malloc((size_t)(N + 1)), *kept = (int8_t *)malloc((size_t)(N + 1));
     int64_t *inwave = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N + 1));
+    int64_t *seen = (int64_t *)calloc((size_t)G, sizeof(int64_t));
     double *lw = (double *)malloc(sizeof(double) * 2 * (size_t)K), *prob = (double *)malloc(sizeof(double) * 2 * (size_t)K);
     int rc = -2;
     if (!shard || !S0m || !S0t || !Lm || !Lt || !Dm || !Dt || !M || !Tt || !Q || !T || !newz || !newr || !rrem ||
-        !kept || !inwave || !lw || !prob) goto out;
+        !kept || !inwave || !lw || !prob || !seen) goto out;
     or_partition(s, G, shard);
-    memcpy(S0m, s->m, sizeof(int32_t) * cells);
-    memcpy(S0t, s->t, sizeof(int32_t) * cells);
     int32_t maxlen = 0;
     for (int32_t d = 0; d < s->D; d++) if (s->doclen[d] > maxlen) maxlen = s->doclen[d];
     int64_t nwaves = (W == 0) ? N : (W < maxlen ? W : maxlen);
+    int64_t block = (E <= 0 || E >= nwaves) ? nwaves : E;
+    if (only >= 0 && block < nwaves) goto out;   /* the distributed form exchanges once per sweep */
+    for (int64_t b0 = 0; b0 < nwaves || (nwaves == 0 && b0 == 0); b0 += (block > 0 ? block : 1)) {
+    int64_t b1 = b0 + block < nwaves ? b0 + block : nwaves;
+    memcpy(S0m, s->m, sizeof(int32_t) * cells);
+    memcpy(S0t, s->t, sizeof(int32_t) * cells);
+    memset(Dm, 0, sizeof(int64_t) * cells);
+    memset(Dt, 0, sizeof(int64_t) * cells);
     for (int g = 0; g < G; g++) {
         if (only >= 0 && g != only) continue;
-        /* shard-local replica of the sweep-start global state (Alg.3) */
+        /* shard-local replica of the block-start global state (Alg.3) */
         memcpy(Lm, S0m, sizeof(int32_t) * cells);
         memcpy(Lt, S0t, sizeof(int32_t) * cells);
         recompute_sums(s, Lm, Lt, M, Tt, Q, T);
-        int64_t seen = 0;
-        for (int64_t wave = 0; wave < nwaves; wave++) {
+        for (int64_t wave = b0; wave < b1; wave++) {
             /* tokens of this shard in this wave, canonical order */
             int64_t cnt = 0;
             if (W == 0) {
@@ -517,8 +528,8 @@ static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *forc
             /* (1) every token decides against the wave-start snapshot */
             for (int64_t q = 0; q < cnt; q++) {
                 int64_t p = inwave[q];
-                if (max_tokens >= 0 && seen >= max_tokens) { kept[p] = 2; continue; } /* not sampled */
-                seen++;
+                if (max_tokens >= 0 && seen[g] >= max_tokens) { kept[p] = 2; continue; } /* not sampled */
+                seen[g]++;
                 int i = s->group[p], w = s->word[p], k0 = s->z[p];
                 size_t c = IDX3(s, i, w, k0);
                 uint32_t x[4];
@@ -571,25 +582,32 @@ static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *forc
     }
     s->stats[2] += clamp_cells(cells, s->m, s->t);
     recompute_sums(s, s->m, s->t, s->M, s->Tt, s->Q, s->T);
+    if (nwaves == 0) break;
+    }   /* blocks */
     s->sweep++;
     rc = 0;
 out:
     free(shard); free(S0m); free(S0t); free(Lm); free(Lt); free(Dm); free(Dt);
-    free(M); free(Tt); free(Q); free(T); free(newz); free(newr); free(rrem); free(kept); free(inwave);
+    free(M); free(Tt); free(Q); free(T); free(newz); free(newr); free(rrem); free(kept); free(inwave); free(seen);
     free(lw); free(prob);
     return rc;
 }
 
 int or_sweep_par(ostate *s, int W, int G, const int32_t *force_zr, double *margin, int64_t max_tokens,
                  int32_t *own_zr) {
-    return sweep_par_impl(s, W, G, -1, force_zr, margin, max_tokens, own_zr, NULL, NULL);
+    return sweep_par_impl(s, W, G, -1, force_zr, margin, max_tokens, own_zr, NULL, NULL, 0);
+}
+/* the same with an exchange every E waves (NEXT-3 bounded staleness) */
+int or_sweep_par_e(ostate *s, int W, int G, int E, const int32_t *force_zr, double *margin, int64_t max_tokens,
+                   int32_t *own_zr) {
+    return sweep_par_impl(s, W, G, -1, force_zr, margin, max_tokens, own_zr, NULL, NULL, E);
 }
 
 /* Distributed form of the same sweep: shard g runs its waves and returns its
  * net changes D_g (int32, [I*V*K]) without touching the global m, t ... */
 int or_sweep_shard(ostate *s, int W, int G, int g, int32_t *Dm, int32_t *Dt) {
     if (g < 0 || g >= G || !Dm || !Dt) return -1;
-    return sweep_par_impl(s, W, G, g, NULL, NULL, -1, NULL, Dm, Dt);
+    return sweep_par_impl(s, W, G, g, NULL, NULL, -1, NULL, Dm, Dt, 0);
 }
 /* ... and, once every rank holds sum_g D_g, the merge S1 = clamp(S0 + sum D). */
 int or_merge(ostate *s, const int32_t *Dm, const int32_t *Dt) {

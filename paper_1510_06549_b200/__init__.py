@@ -35,7 +35,7 @@ _NAMES = {0: "SPDP_OK", -1: "SPDP_EINVAL", -2: "SPDP_ENOMEM", -3: "SPDP_ECUDA", 
 EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "spdp_sweep_local",
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
-           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger"]
+           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -62,7 +62,7 @@ class spdp_config(C.Structure):
                 ("discount", C.c_void_p), ("concentration", C.c_void_p), ("seed", C.c_uint64),
                 ("num_waves", C.c_int32), ("device", C.c_int32), ("rank", C.c_int32), ("world_size", C.c_int32),
                 ("exchange", C.c_int32), ("nccl_unique_id", C.c_void_p), ("stream", C.c_void_p),
-                ("debug_checks", C.c_int32), ("update_mode", C.c_int32)]
+                ("debug_checks", C.c_int32), ("update_mode", C.c_int32), ("merge_every", C.c_int32)]
 
 
 _lib = None
@@ -85,7 +85,7 @@ def lib():
             "spdp_partition": [C.c_uint64, I32, I64, I32, P, P], "spdp_nccl_unique_id": [P],
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
-            "spdp_topic_hellinger": [P, P, P, P],
+            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -131,7 +131,8 @@ def spdp_nccl_unique_id() -> bytes:
 
 def spdp_create(num_groups, vocab_size, num_topics, alpha=0.1, beta=0.1, discount=0.7, concentration=100.0,
                 seed=7, num_waves=1, device=0, rank=0, world_size=1, exchange=SPDP_EXCHANGE_NCCL,
-                nccl_unique_id=None, stream=None, debug_checks=False, alpha_ik=None, update_mode=SPDP_UPDATE_WAVE):
+                nccl_unique_id=None, stream=None, debug_checks=False, alpha_ik=None, update_mode=SPDP_UPDATE_WAVE,
+                merge_every=0):
     """Returns (ctx handle, keep-alive tuple)."""
     I, K = int(num_groups), int(num_topics)
     disc = np.ascontiguousarray(np.broadcast_to(np.asarray(discount, np.float64), (I,)))
@@ -141,7 +142,7 @@ def spdp_create(num_groups, vocab_size, num_topics, alpha=0.1, beta=0.1, discoun
     cfg = spdp_config(C.sizeof(spdp_config), I, int(vocab_size), K, float(alpha), _p(aik), float(beta),
                       _p(disc), _p(conc), int(seed) & (2**64 - 1), int(num_waves), int(device), int(rank),
                       int(world_size), int(exchange), C.cast(uid, C.c_void_p) if uid is not None else None,
-                      stream, int(bool(debug_checks)), int(update_mode))
+                      stream, int(bool(debug_checks)), int(update_mode), int(merge_every))
     h = C.c_void_p()
     code = lib().spdp_create(C.byref(cfg), C.byref(h))
     if code != SPDP_OK:
@@ -301,6 +302,11 @@ class Sampler:
 
     def sweep_local(self):
         spdp_sweep_local(self.ctx)
+
+    def exchange_blocks(self):
+        n = C.c_int32()
+        _check(lib().spdp_exchange_blocks(self.ctx, C.byref(n)), self.ctx)
+        return n.value
 
     def exchange_buffer(self):
         return spdp_exchange_buffer(self.ctx)

@@ -108,6 +108,8 @@ struct spdp_ctx {
     // all-reduced and merged on comm_stream while part p+1 samples
     int P = 1;
     bool overlap = false;
+    // bounded staleness (NEXT-3): exchange after every E waves; the sweep is nblocks exchange blocks
+    int E = 1, nblocks = 1, block = 0, nwaves_eff = 1;
     std::vector<uint32_t> part_word, part_run, part_tok, part_chunk;   // [P + 1] boundaries
     cudaStream_t comm_stream = nullptr;
     std::vector<cudaEvent_t> part_ev;
@@ -664,9 +666,10 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
     return check_launch(c, "sweep parts");
 }
 
-spdp_status run_waves(spdp_ctx* c) {
+// waves [w0, w1) of the sweep (one exchange block); first: the sweep's first block
+spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
     SweepArgs a = base_args(c);
-    CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    if (first) CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
     CU(cudaMemsetAsync(c->d_work, 0, sizeof(uint32_t) * ((size_t)std::max(c->W, c->P) + 2), c->stream));
     if (c->profiling) { spdp_status s = ensure_events(c); if (s) return s; }
     void* Dnet = c->G > 1 ? c->d_Dloc : nullptr;
@@ -701,7 +704,7 @@ spdp_status run_waves(spdp_ctx* c) {
         return check_launch(c, "async sweep");
     }
     if (c->P > 1) return run_parts(c, a);
-    for (int w = 0; w < c->W; ++w) {
+    for (int w = w0; w < w1; ++w) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
         rec(c, 4 * (size_t)w);
         if (ce == cb) { rec(c, 4 * (size_t)w + 1); rec(c, 4 * (size_t)w + 2); rec(c, 4 * (size_t)w + 3); continue; }
@@ -752,6 +755,10 @@ spdp_status run_waves(spdp_ctx* c) {
     }
     return check_launch(c, "sweep waves");
 }
+
+// waves of exchange block b (the last block also covers the empty waves past the longest document)
+inline int block_w0(const spdp_ctx* c, int b) { return b * c->E; }
+inline int block_w1(const spdp_ctx* c, int b) { return b + 1 >= c->nblocks ? c->W : std::min((b + 1) * c->E, c->W); }
 
 // after the stream is synchronised: accumulate this sweep's phase times
 void collect_times(spdp_ctx* c, bool exchanged) {
@@ -815,6 +822,7 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     if (!(cfg->beta > 0.0)) return bad("beta must be > 0");
     if (!cfg->discount || !cfg->concentration) return bad("discount and concentration arrays are required");
     if (cfg->num_waves < 1) return bad("num_waves must be >= 1");
+    if (cfg->merge_every < 0) return bad("merge_every must be >= 0");
     if (cfg->update_mode != SPDP_UPDATE_WAVE && cfg->update_mode != SPDP_UPDATE_ASYNC) return bad("unknown update_mode");
     if (cfg->update_mode == SPDP_UPDATE_ASYNC && cfg->num_waves != 1) return bad("SPDP_UPDATE_ASYNC needs num_waves == 1");
     c->async = cfg->update_mode == SPDP_UPDATE_ASYNC;
@@ -1148,6 +1156,15 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     }
     c->nchunks = nch;
     c->nsegs = R;
+    {   // exchange blocks (NEXT-3): waves that can hold tokens = min(W, longest document)
+        int32_t maxlen = 1;
+        for (int32_t dl : c->doclen) maxlen = std::max(maxlen, dl);
+        c->nwaves_eff = std::max(1, std::min(W, maxlen));
+        const int e = c->cfg.merge_every;
+        c->E = (e <= 0 || c->G == 1 || c->async) ? c->nwaves_eff : std::min(e, c->nwaves_eff);
+        c->nblocks = (c->nwaves_eff + c->E - 1) / c->E;
+        c->block = 0;
+    }
     if (c->P == 1) {
         c->part_chunk = {0u, nch};
         c->part_run = {0u, R};
@@ -1327,9 +1344,17 @@ spdp_status spdp_set_state(spdp_ctx* c, const int32_t* z, const uint8_t* r, cons
 spdp_status spdp_sweep_local(spdp_ctx* c) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    if ((s = run_waves(c))) return s;
+    if ((s = run_waves(c, block_w0(c, c->block), block_w1(c, c->block), c->block == 0))) return s;
     if (c->G > 1) CU(cudaMemcpyAsync(c->d_Dsum, c->d_Dloc, c->dbytes(), cudaMemcpyDeviceToDevice, c->stream));
     return sync(c, "spdp_sweep_local");
+}
+
+spdp_status spdp_exchange_blocks(spdp_ctx* c, int32_t* nblocks) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!nblocks) return fail(c, SPDP_EINVAL, "null output");
+    *nblocks = c->nblocks;
+    return SPDP_OK;
 }
 
 spdp_status spdp_exchange_buffer(spdp_ctx* c, void** ptr, int64_t* count, int32_t* elem_bytes) {
@@ -1361,6 +1386,8 @@ spdp_status spdp_sweep_merge(spdp_ctx* c) {
         launch_exchange_merge(c);
         if ((s = check_launch(c, "merge (exchange)"))) return s;
     }
+    if (++c->block < c->nblocks) return sync(c, "spdp_sweep_merge");   // more exchange blocks in this sweep
+    c->block = 0;
     if ((s = finish_sweep(c))) return s;
     if ((s = sync(c, "spdp_sweep_merge"))) return s;
     if (c->cfg.debug_checks) return debug_verify(c);
@@ -1374,7 +1401,8 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
     if (c->G > 1 && c->cfg.exchange != SPDP_EXCHANGE_NCCL)
         return fail(c, SPDP_ESTATE, "SPDP_EXCHANGE_EXTERNAL: use spdp_sweep_local / spdp_sweep_merge");
     for (int it = 0; it < num_sweeps; ++it) {
-        if ((s = run_waves(c))) return s;
+      for (int b = 0; b < c->nblocks; ++b) {
+        if ((s = run_waves(c, block_w0(c, b), block_w1(c, b), b == 0))) return s;
         if (c->G > 1 && !c->overlap) {
             rec(c, 4 * (size_t)c->W);
             if ((s = nccl_check(c, c->nccl.AllReduce(c->d_Dloc, c->d_Dsum, c->cells, c->pack32 ? kNcclInt32 : kNcclInt64,
@@ -1385,6 +1413,7 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
             rec(c, 4 * (size_t)c->W + 1);
             c->launches += 1;
         }
+      }
         if ((s = finish_sweep(c))) return s;
         if (c->profiling) {
             if ((s = sync(c, "spdp_sweep"))) return s;

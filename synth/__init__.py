@@ -152,3 +152,19 @@ def holdout_split(corpus: Corpus, fraction: float = 0.1, seed: int = 0) -> tuple
                       corpus.z_gen[keep].copy(), corpus.num_groups, int(len(old)), corpus.vocab)
 
     return part(~test_doc), part(test_doc)
+
+
+def duplicate(corpus: Corpus, copies: int) -> Corpus:
+    """Training-data duplication (§3.3):
+    the corpus followed by `copies` more copies of every document, as new
+    documents (copy j of doc d is doc j*D + d; its tokens follow all tokens of
+    copy j-1, so canonical token j*N + p is copy j of token p).  With several
+    ranks the copies of a document usually land on different ranks (the
+    partition keys on the doc id), which is what averages out their errors."""
+    if copies < 0:
+        raise ValueError("copies must be >= 0")
+    n = copies + 1
+    rep = lambda a: np.tile(a, n)
+    doc = np.concatenate([corpus.doc + j * corpus.num_docs for j in range(n)]).astype(np.int32)
+    return Corpus(rep(corpus.group).astype(np.int32), doc, rep(corpus.word).astype(np.int32),
+                  rep(corpus.z_gen).astype(np.int32), corpus.num_groups, corpus.num_docs * n, corpus.vocab)

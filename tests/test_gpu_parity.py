@@ -247,3 +247,48 @@ def test_multi_rank_parts_match_oracle_shards(G, monkeypatch):
         if mism == 0:
             for k in ("m", "t", "Q"):
                 np.testing.assert_array_equal(ranks[0].counts()[k], oc[k], err_msg=k)
+
+
+@pytest.mark.parametrize("G,waves,E", [(2, 4, 1), (3, 4, 2), (2, 3, 1)])
+def test_bounded_staleness_exchange_matches_oracle(G, waves, E):
+    """NEXT-3: ranks exchanging after every E waves (external exchange, G contexts on
+    one GPU) follow the oracle's G-shard sweep with the same cadence."""
+    c = corpus("C1")
+    ranks = [spdp.sampler_for(c, 10, num_waves=waves, rank=r, world_size=G, merge_every=E,
+                              exchange=spdp.SPDP_EXCHANGE_EXTERNAL, **HYPER) for r in range(G)]
+    nb = ranks[0].exchange_blocks()
+    assert nb == -(-waves // E)
+    o = oracle.from_corpus(c, 10, **HYPER)
+    part = np.asarray(spdp.spdp_partition(7, G, c.doc, c.num_docs))[c.doc]
+    for s in range(2):
+        for b in range(nb):
+            for r in ranks:
+                r.sweep_local()
+            bufs = [r.exchange_get() for r in ranks]
+            with np.errstate(over="ignore"):
+                tot = sum(x.astype(np.int64) for x in bufs).astype(bufs[0].dtype)
+            for r in ranks:
+                r.exchange_put(tot)
+                r.sweep_merge()
+        o.sweep_par(waves=waves, shards=G, merge_every=E)
+        oc = o.state()
+        z = np.full(c.num_tokens, -1, np.int32)
+        for j, r in enumerate(ranks):
+            z[part == j] = r.counts()["z"][part == j]
+        mism = np.count_nonzero(z != oc["z"])
+        assert mism <= max(1, 1e-4 * c.num_tokens), mism
+        if mism == 0:
+            got = ranks[0].counts()
+            for k in ("m", "t", "Q"):
+                np.testing.assert_array_equal(got[k], oc[k], err_msg=k)
+
+
+def test_duplicated_corpus_parity():
+    """NEXT-3 duplication: the duplicated corpus is an ordinary input; one lock-step
+    sweep against the oracle on it."""
+    c = synth.duplicate(corpus("C1"), 1)
+    assert c.num_tokens == 2 * corpus("C1").num_tokens
+    g, o = pair(c, 10)
+    rep, gc = lockstep_sweep(g, o)
+    assert_draw_parity(rep)
+    assert_counts_equal(gc, o.state())

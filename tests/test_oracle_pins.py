@@ -405,3 +405,43 @@ def test_perplexity_degenerate_cases():
     o = oracle.Oracle(2, 17, 3, 1e12, 1e12, 0.7, 1e15, 1)
     o.load(c.group, c.doc, c.word, c.num_docs)
     assert o.perplexity() == pytest.approx(17.0, rel=1e-9)
+
+
+# --------------------------------------------------------------------------
+# NEXT-3: exchanges every E waves (bounded staleness) and training-data duplication
+# --------------------------------------------------------------------------
+def test_per_wave_exchange_with_one_token_waves_is_algorithm1():
+    """G shards exchanging after every one-token wave see every earlier decision:
+    exactly the sequential sampler (Alg.1, pinned against exact enumeration)."""
+    import synth
+    c = synth.generate(2, 6, 12.0, 40, 4, seed=5)
+    a = oracle.from_corpus(c, 4)
+    b = oracle.from_corpus(c, 4)
+    for _ in range(4):
+        a.sweep_seq()
+        b.sweep_par(waves=0, shards=3, merge_every=1)
+        sa, sb = a.state(), b.state()
+        for k in ("z", "r", "n", "m", "t", "Q"):
+            assert np.array_equal(sa[k], sb[k]), k
+    assert b.stats()["clamped"] == 0
+
+
+@pytest.mark.parametrize("E", [1, 2, 3])
+def test_exchange_cadence_single_shard_and_invariants(E):
+    import synth
+    c = synth.generate(2, 10, 15.0, 30, 4, seed=9)
+    a = oracle.from_corpus(c, 4)
+    b = oracle.from_corpus(c, 4)
+    for _ in range(3):                       # one shard: the exchange cadence changes nothing
+        a.sweep_par(waves=4)
+        b.sweep_par(waves=4, merge_every=E)
+    assert all(np.array_equal(a.state()[k], b.state()[k]) for k in ("z", "r", "n", "m", "t", "Q"))
+    d = oracle.from_corpus(c, 4)
+    for _ in range(3):                       # several shards: a valid state after every sweep
+        d.sweep_par(waves=4, shards=3, merge_every=E)
+        assert d.check_invariants() == 0
+    e = oracle.from_corpus(c, 4)
+    f = oracle.from_corpus(c, 4)
+    e.sweep_par(waves=4, shards=3, merge_every=99)
+    f.sweep_par(waves=4, shards=3)
+    assert all(np.array_equal(e.state()[k], f.state()[k]) for k in ("z", "r", "n", "m", "t", "Q"))
