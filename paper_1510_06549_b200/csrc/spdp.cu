@@ -41,6 +41,14 @@ struct NcclApi {
     const char* (*GetErrorString)(int) = nullptr;
 };
 constexpr int kNcclInt32 = 2, kNcclInt64 = 4, kNcclFloat64 = 8, kNcclSum = 0;
+// SPDP_NCCL_LIB: another implementation of the same symbols (tests/nccl_shim.c lets several
+// processes share one GPU, which NCCL itself refuses)
+void* open_nccl() {
+    if (const char* e = getenv("SPDP_NCCL_LIB")) return dlopen(e, RTLD_NOW | RTLD_LOCAL);
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    return lib;
+}
 
 // ------------------------------------------------------------------ host Philox4x32-10
 void philox_host(const uint32_t ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4]) {
@@ -877,9 +885,7 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     set_attrs(c);
     if (c->G > 1 && cfg->exchange == SPDP_EXCHANGE_NCCL) {
         if (!cfg->nccl_unique_id) return bad("nccl_unique_id is required for SPDP_EXCHANGE_NCCL with world_size > 1");
-        const char* names[] = {"libnccl.so.2", "libnccl.so"};
-        for (const char* nm : names)
-            if ((c->nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+        c->nccl.lib = open_nccl();
         if (!c->nccl.lib) {
             fail(c, SPDP_ENCCL, "cannot dlopen libnccl.so.2");
             *out = c;
@@ -1813,8 +1819,7 @@ spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, dou
 
 spdp_status spdp_nccl_unique_id(void* out) {
     if (!out) return SPDP_EINVAL;
-    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    void* lib = open_nccl();
     if (!lib) return SPDP_ENCCL;
     auto fn = (int (*)(NcclUid*))dlsym(lib, "ncclGetUniqueId");
     if (!fn) return SPDP_ENCCL;
