@@ -1304,6 +1304,9 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         CU(cudaMemset(c->d_sweep, 0, sizeof(uint32_t)));
         CU(cudaMemset(c->d_stats, 0, sizeof(unsigned long long) * 8));
     }
+    // pageable cudaMemcpy may return before its DMA lands; the context stream does not
+    // order after the legacy stream, so settle every upload before the stream reads them
+    CU(cudaDeviceSynchronize());
     lt.mark("device alloc + upload");
     // Stirling-ratio tables, one per distinct discount (M_max rows)
     {
@@ -1320,7 +1323,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         ALLOC(c->d_tab_off, I);
         c->tab_off_host.resize((size_t)I);
         for (int i = 0; i < I; ++i) c->tab_off_host[(size_t)i] = per * (uint64_t)which[(size_t)i];
-        CU(cudaMemcpy(c->d_tab_off, c->tab_off_host.data(), sizeof(uint64_t) * I, cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(c->d_tab_off, c->tab_off_host.data(), sizeof(uint64_t) * I, cudaMemcpyHostToDevice, c->stream));
         double* scratch = nullptr;
         ALLOC(scratch, 2 * (size_t)(c->mmax + 2));
         for (size_t j = 0; j < distinct.size(); ++j)

@@ -88,7 +88,8 @@ int ncclAllReduce(const void *send, void *recv, size_t count, int dtype, int op,
         size_t n = count - off < per ? count - off : per;
         if (count == 0) n = 0;
         char *mine = c->slots + (size_t)c->rank * SLOT;
-        if (n && cudaMemcpy(mine, (const char *)send + off * es, n * es, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+        if (n && (cudaMemcpyAsync(mine, (const char *)send + off * es, n * es, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                  cudaStreamSynchronize(st) != cudaSuccess)) return 1;
         barrier(c);
         memset(tmp, 0, n * es);
         for (int r = 0; r < c->nranks; r++) {      /* fixed rank order: deterministic sums */
@@ -100,7 +101,9 @@ int ncclAllReduce(const void *send, void *recv, size_t count, int dtype, int op,
             }
         }
         barrier(c);                                  /* every rank has read every slot */
-        if (n && cudaMemcpy((char *)recv + off * es, tmp, n * es, cudaMemcpyHostToDevice) != cudaSuccess) return 1;
+        /* on the caller's stream, complete before returning (a pageable cudaMemcpy may still be in flight) */
+        if (n && (cudaMemcpyAsync((char *)recv + off * es, tmp, n * es, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                  cudaStreamSynchronize(st) != cudaSuccess)) return 1;
         if (count == 0) break;
     }
     free(tmp);
