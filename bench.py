@@ -188,9 +188,17 @@ def main():
     import paper_1510_06549_b200 as spdp
 
     spdp.build()
+    # SPDP_BENCH_SHARE_GPU=1 (functional test only, with SPDP_NCCL_LIB=tests/libnccl_shim.so): every rank on
+    # GPU 0, torch.distributed over gloo; the numbers of such a run are not measurements
+    share = os.environ.get("SPDP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local_rank))
     corpus = synth.corpus_for(cfg)
     N = corpus.num_tokens
     uid = None
