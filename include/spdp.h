@@ -182,6 +182,13 @@ spdp_status spdp_exchange_copy(spdp_ctx* ctx, void* host, int32_t to_device);
 spdp_status spdp_counts(spdp_ctx* ctx, int32_t* z, uint8_t* r, int32_t* doc_topic,
                         int32_t* customers, int32_t* tables, int32_t* shadow);
 
+/* The assignments packed: zr [N] uint16 = z | r << 15 in canonical token order
+ * (2 bytes per token, no host-side unpacking; pass pinned memory for a
+ * full-speed copy).  Tokens of other ranks read 0xFFFF with
+ * SPDP_EXCHANGE_EXTERNAL; gathered from every rank (collective) with
+ * SPDP_EXCHANGE_NCCL.  Caller-owned host buffer. */
+spdp_status spdp_zr(spdp_ctx* ctx, uint16_t* zr);
+
 /* log_joint = log p(W, Z, T | alpha, beta, a, b) (PAPER.md:1654-1665 summed over
  * the seatings R of each T, Eq. SPDP-table-to-head);
  * perplexity = training perplexity exp(-sum_tok log sum_k theta~_dk phi^i~_kw / N)

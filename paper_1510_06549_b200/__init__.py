@@ -35,7 +35,7 @@ _NAMES = {0: "SPDP_OK", -1: "SPDP_EINVAL", -2: "SPDP_ENOMEM", -3: "SPDP_ECUDA", 
 EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "spdp_sweep_local",
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
-           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks"]
+           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -85,7 +85,7 @@ def lib():
             "spdp_partition": [C.c_uint64, I32, I64, I32, P, P], "spdp_nccl_unique_id": [P],
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
-            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P],
+            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -212,6 +212,14 @@ def spdp_counts(ctx, N, D, I, V, K, z=True, r=True, doc_topic=True, customers=Tr
     return out
 
 
+def spdp_zr(ctx, N, out=None):
+    """Packed assignments z | r << 15 [N] uint16 (out: caller-owned, e.g. pinned, reused)."""
+    out = np.empty(N, np.uint16) if out is None else out
+    assert out.dtype == np.uint16 and out.shape == (N,) and out.flags["C_CONTIGUOUS"]
+    _check(lib().spdp_zr(ctx, _p(out)), ctx)
+    return out
+
+
 def spdp_loglik(ctx, log_joint=True, perplexity=True):
     lj, pp = C.c_double(np.nan), C.c_double(np.nan)
     _check(lib().spdp_loglik(ctx, C.byref(lj) if log_joint else None, C.byref(pp) if perplexity else None), ctx)
@@ -324,6 +332,9 @@ class Sampler:
 
     def counts(self, out=None, **which):
         return spdp_counts(self.ctx, self.N, self.D, self.I, self.V, self.K, out=out, **which)
+
+    def zr(self, out=None):
+        return spdp_zr(self.ctx, self.N, out)
 
     def loglik(self, log_joint=True, perplexity=True):
         return spdp_loglik(self.ctx, log_joint, perplexity)

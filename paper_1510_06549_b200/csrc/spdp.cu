@@ -1520,6 +1520,29 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
     return SPDP_OK;
 }
 
+spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!zr) return fail(c, SPDP_EINVAL, "null output");
+    const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
+    if (gather) {                                   // the gathered path of spdp_counts, then packed
+        std::vector<int32_t> z((size_t)c->N);
+        std::vector<uint8_t> r((size_t)c->N);
+        if ((s = spdp_counts(c, z.data(), r.data(), nullptr, nullptr, nullptr, nullptr))) return s;
+        for (int64_t p = 0; p < c->N; ++p) zr[p] = (uint16_t)(z[(size_t)p] | (r[(size_t)p] << 15));
+        return SPDP_OK;
+    }
+    if (!c->d_zr_canon) ALLOC(c->d_zr_canon, c->N);
+    if (c->Nloc < c->N) CU(cudaMemsetAsync(c->d_zr_canon, 0xFF, sizeof(uint16_t) * (size_t)c->N, c->stream));
+    if (c->Nloc > 0)
+        scatter_zr_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_tok_id, c->d_zr, (uint32_t)c->Nloc, c->d_zr_canon, 0u);
+    if ((s = check_launch(c, "scatter_zr_kernel"))) return s;
+    c->launches += 1;
+    // straight into the caller's buffer (pinned memory makes this a full-speed DMA)
+    CU(cudaMemcpyAsync(zr, c->d_zr_canon, sizeof(uint16_t) * (size_t)c->N, cudaMemcpyDeviceToHost, c->stream));
+    return sync(c, "spdp_zr");
+}
+
 spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;

@@ -1067,9 +1067,9 @@ __global__ void init_local_kernel(const uint32_t* __restrict__ tok_id, const uin
 
 // zr in canonical token order (for spdp_counts): out[id[p]] = zr[p] + 1 (0 = other rank)
 __global__ void scatter_zr_kernel(const uint32_t* __restrict__ id, const uint16_t* __restrict__ zr, uint32_t n,
-                                  uint16_t* __restrict__ out) {
+                                  uint16_t* __restrict__ out, uint32_t add = 1u) {
     for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x)
-        out[id[p]] = (uint16_t)(zr[p] + 1u);
+        out[id[p]] = (uint16_t)(zr[p] + add);
 }
 
 // ---------------------------------------------------------------- training perplexity

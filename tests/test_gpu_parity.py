@@ -292,3 +292,13 @@ def test_duplicated_corpus_parity():
     rep, gc = lockstep_sweep(g, o)
     assert_draw_parity(rep)
     assert_counts_equal(gc, o.state())
+
+
+def test_packed_assignments_match_counts():
+    c = corpus("C1")
+    g = spdp.sampler_for(c, 10, **HYPER)
+    g.sweep(2)
+    cnt = g.counts(doc_topic=False, customers=False, tables=False, shadow=False)
+    zr = g.zr()
+    np.testing.assert_array_equal(zr & 0x7FFF, cnt["z"])
+    np.testing.assert_array_equal(zr >> 15, cnt["r"])
