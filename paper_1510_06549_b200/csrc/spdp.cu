@@ -139,6 +139,7 @@ struct spdp_ctx {
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
+    float* d_R1 = nullptr;                        // token kernel: r = 1 shares [run][Kp]
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
     int colstart[8] = {0};
@@ -298,10 +299,10 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     const int fgrid = (int)std::min<size_t>((nf + 255) / 256, 148u * 16u);
     factor_kernel<<<std::max(fgrid, 1), 256, 0, c->stream>>>(
         c->d_wave_segs, r0, r1, c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->d_disc, c->d_conc, c->d_tab,
-        c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F);
+        c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F, c->d_R1);
     TokenArgs t{};
     t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
-    t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.F = c->d_F; t.n = c->d_n;
+    t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.F = c->d_F; t.R1 = c->d_R1; t.n = c->d_n;
     t.sigma = c->d_sigma;
     for (int B = 0; B < 16; ++B) {
         const int nbl = c->KPL / 4;
@@ -1111,6 +1112,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             if (c->token_kernel) {
                 ALLOC(c->d_tok_run, nl);
                 ALLOC(c->d_F, (size_t)R * Kp);
+                ALLOC(c->d_R1, (size_t)R * Kp);
                 token_run_kernel<<<grid, 256, 0, st>>>(droff.p, drlen.p, R, c->d_tok_run);
             }
             chunk_count_kernel<<<grid, 256, 0, st>>>(drlen.p, R, chunk, dnch.p);

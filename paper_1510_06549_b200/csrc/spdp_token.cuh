@@ -34,12 +34,12 @@ __global__ void factor_kernel(const uint32_t* __restrict__ run_seg, uint32_t r0,
                               const int32_t* __restrict__ Tt, const int32_t* __restrict__ T,
                               const float* __restrict__ disc, const float* __restrict__ conc,
                               const float2* __restrict__ tab, const uint64_t* __restrict__ tab_off, float beta,
-                              float vbeta, int I, int K, int Kp, float* __restrict__ F) {
+                              float vbeta, int I, int K, int Kp, float* __restrict__ F, float* __restrict__ R1) {
     const size_t n = (size_t)(r1 - r0) * Kp;
     for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
         const uint32_t r = r0 + (uint32_t)(j / Kp);
         const int k = (int)(j % Kp);
-        float Fk = 0.f;
+        float Fk = 0.f, Rk = 0.f;
         if (k < K) {
             const uint32_t seg = run_seg[r];
             const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
@@ -49,8 +49,10 @@ __global__ void factor_kernel(const uint32_t* __restrict__ run_seg, uint32_t r0,
             slot_factors(M[(size_t)i * Kp + k], Tt[(size_t)i * Kp + k], Q[(size_t)w * Kp + k], T[k],
                          tab[tab_off[i] + tri(mv) + tv], disc[i], conc[i], beta, vbeta, F0, F1);
             Fk = F0 + F1;
+            Rk = (F1 > 0.f) ? __fdiv_rn(F1, F0 + F1) : 0.f;     // exact r = 1 share of the slot pair
         }
         F[(size_t)r * Kp + k] = Fk;
+        R1[(size_t)r * Kp + k] = Rk;
     }
 }
 
@@ -62,6 +64,7 @@ struct TokenArgs {
     const uint16_t* zr;
     uint16_t* zr_next;
     const float* F;                // [run][Kp]
+    const float* R1;               // [run][Kp] r = 1 share F1 / F at the snapshot
     const void* n;                 // doc-topic rows (sigma layout of the chunk kernel)
     const int* sigma;              // [Kp] in-row position of topic k
     int bpos[16];                  // in-row position (float4 units) of 4-topic block B
@@ -173,19 +176,13 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
             for (int e = 0; e < 4; ++e) if (e == es) wsel = wq[e];
             ks = 4 * qs + es;
             const bool own = (ks == k0);
-            float R1s = R1k0;
-            int ms = m0 - 1;
-            if (!own) {                                                             // r = 1 share of ks at the snapshot
-                const size_t cs_ = (size_t)seg * Kp + ks;
-                const int mv = A.m[cs_], tv = A.t[cs_];
-                ms = mv;
-                float f0, f1;
-                slot_factors(Mi[ks], Tti[ks], Qw[ks], A.T[ks], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, f0, f1);
-                R1s = (f1 > 0.f) ? __fdiv_rn(f1, f0 + f1) : 0.f;
-            }
+            const float R1s = own ? R1k0 : A.R1[(size_t)run * Kp + ks];           // r = 1 share of ks
             const float w1 = wsel * R1s;
             if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
-            else rs = (ms > 0) ? 0 : 1;                                             // last positive slot
+            else {                                                                  // last positive slot
+                const int ms = own ? m0 - 1 : A.m[(size_t)seg * Kp + ks];
+                rs = (ms > 0) ? 0 : 1;
+            }
             // a7: packed deltas (dm * 2^16 + dt) of the two cells
             atomicAdd(A.dmt + cell0, -65536 - rrem);
             atomicAdd(A.dmt + (size_t)seg * Kp + ks, 65536 + rs);
