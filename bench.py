@@ -129,8 +129,8 @@ def plan_stats(corpus, shard_docs, waves):
     return {"tokens": int(doc.shape[0]), "segments": int(np.unique(key).shape[0])}
 
 
-def load_traffic(cfg_name, K, kernel="sample"):
-    """DRAM bytes per launch from the latest round's committed ncu --set full summary."""
+def ncu_summary(cfg_name, K, kernel="sample"):
+    """The latest round's committed ncu --set full summary of the kernel (profiles/), or {}."""
     import glob
     paths = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{cfg_name}_K{K}_{kernel}.json")))
     if paths:
@@ -138,8 +138,14 @@ def load_traffic(cfg_name, K, kernel="sample"):
             d = json.load(f)
         if isinstance(d, list):
             d = d[0]
-        return d.get("dram_bytes_per_launch")
-    return None
+        d["file"] = os.path.relpath(paths[-1], ROOT)
+        return d
+    return {}
+
+
+def load_traffic(cfg_name, K, kernel="sample"):
+    """DRAM bytes per launch from the latest round's committed ncu --set full summary."""
+    return ncu_summary(cfg_name, K, kernel).get("dram_bytes_per_launch")
 
 
 def cpu_baseline(corpus, cfg, K, waves, sample_tokens):
@@ -267,6 +273,10 @@ def main():
             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
             "alg_bytes_per_launch": int(bytes_sweep / max(args.waves, 1)), "peak_source": peak_src,
             "sample_ms_per_sweep": round(sample_ms, 4), "share_of_step": round(sample_ms / ms, 3)}
+    nc = ncu_summary(cfg.name, K, kname.split("_")[0])
+    if nc:   # what actually limits the kernel (from the committed ncu capture, not this run)
+        roof["ncu"] = {k: nc.get(k) for k in ("file", "l2_hit_pct", "l1_pct_of_peak", "issue_active_pct",
+                                               "achieved_occupancy_pct", "warp_instructions", "duration_ms")}
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     torch.cuda.synchronize(); barrier()
