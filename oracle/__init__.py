@@ -91,6 +91,18 @@ def lib():
         L.or_greedy_match.argtypes = [C.c_int, P, P]
         L.or_greedy_match.restype = None
         L.or_topic_align.argtypes = [P, P, P, P]
+        # NEXT-4 (sparse P^i)
+        L.or_sp_create.restype = P
+        L.or_sp_create.argtypes = [P, P, P, P]
+        L.or_sp_destroy.argtypes = [P]
+        L.or_sp_destroy.restype = None
+        L.or_sp_sweep_seq.argtypes = [P]
+        L.or_sp_sweep_par.argtypes = [P, C.c_int, P, P, P]
+        L.or_sp_get.argtypes = [P, P, P]
+        L.or_sp_get.restype = None
+        L.or_sp_set_q.argtypes = [P, P]
+        L.or_sp_conditional.argtypes = [P, C.c_int64, C.c_int, C.c_int32, P]
+        L.or_sp_chain_codes.argtypes = [P, C.c_int64, C.c_int, C.c_int, P]
         _lib = L
     return _lib
 
@@ -151,6 +163,7 @@ class Oracle:
         if rc != 0:
             raise ValueError(f"or_load failed ({rc})")
         self.N, self.D = len(w), int(num_docs)
+        self._tok = (g, d, w)
 
     def sweep_seq(self, max_tokens: int = -1):
         if lib().or_sweep_seq(self.h, int(max_tokens)) != 0:
@@ -279,6 +292,69 @@ class Oracle:
     def partition(self, shards: int):
         out = np.zeros(self.D, np.int32)
         lib().or_partition(self.h, int(shards), _ptr(out))
+        return out
+
+
+class SparseOracle:
+    """NEXT-4: the sampler with sparse transformation matrices P^i (spdp_oracle.c
+    "NEXT-4").  P as CSR rows over (i, w): pptr [I*V+1], pv [E] source words,
+    pp [E] weights (columns of each P^i sum to 1).  Wraps a loaded Oracle."""
+
+    def __init__(self, base: "Oracle", pptr, pv, pp):
+        self.base = base
+        self._keep = (np.ascontiguousarray(pptr, np.int32), np.ascontiguousarray(pv, np.int32),
+                      np.ascontiguousarray(pp, np.float64))
+        self.E = int(self._keep[0][-1])
+        self.h = lib().or_sp_create(base.h, *(_ptr(a) for a in self._keep))
+        if not self.h:
+            raise ValueError("invalid P (rows need a source, columns must sum to 1)")
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().or_sp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sweep_seq(self):
+        if lib().or_sp_sweep_seq(self.h) != 0:
+            raise RuntimeError("or_sp_sweep_seq failed")
+
+    def sweep_par(self, waves=1, force=None, want_margin=False, want_own=False):
+        f = None if force is None else np.ascontiguousarray(force, np.int32)
+        mg = np.full(self.base.N, np.inf) if want_margin else None
+        own = np.full(self.base.N, -1, np.int32) if want_own else None
+        if lib().or_sp_sweep_par(self.h, int(waves), _ptr(f), _ptr(mg), _ptr(own)) != 0:
+            raise RuntimeError("or_sp_sweep_par failed")
+        return mg, own
+
+    def state(self):
+        st = self.base.state()
+        q = np.zeros((self.E, self.base.K), np.int32); Qs = np.zeros((self.base.K, self.base.V), np.int64)
+        lib().or_sp_get(self.h, _ptr(q), _ptr(Qs))
+        st["q"], st["Qs"] = q, Qs
+        return st
+
+    def set_q(self, q):
+        q = np.ascontiguousarray(q, np.int32)
+        lib().or_sp_set_q(self.h, _ptr(q))
+
+    def conditional(self, tok, r_rem, e_rem):
+        i, w = int(self.base._tok[0][tok]), int(self.base._tok[2][tok])
+        r = i * self.base.V + w
+        S = int(self._keep[0][r + 1] - self._keep[0][r])
+        out = np.zeros(self.base.K * (S + 1))
+        rc = lib().or_sp_conditional(self.h, int(tok), int(r_rem), int(e_rem), _ptr(out))
+        return None if rc != 0 else out
+
+    def chain_codes(self, nsweeps, waves=-1, qbase=5):
+        out = np.zeros(int(nsweeps), np.int64)
+        if lib().or_sp_chain_codes(self.h, int(nsweeps), int(waves), int(qbase), _ptr(out)) != 0:
+            raise RuntimeError("or_sp_chain_codes failed")
         return out
 
 

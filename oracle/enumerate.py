@@ -158,3 +158,118 @@ class TinyCorpus:
                 out.append(self.joint_WZR_per_T(tuple(z2), t2) if ok else Fraction(0))
         tot = sum(out)
         return [v / tot for v in out]
+
+
+def multinomial(n, parts):
+    out = Fraction(1)
+    rest = n
+    for x in parts:
+        out *= comb(rest, x)
+        rest -= x
+    return out
+
+
+class TinyCorpusP(TinyCorpus):
+    """NEXT-4: the same brute force with a transformation matrix P^i per group
+    (PAPER.md:985-1014): a table of restaurant (i,k) serving word w takes its
+    dish through a source word v with probability p_{i,w,v} phi0_{k,v}
+    (P^i phi0 is the base of the group's PDP).  Expanding
+    H(w)^{t_w} = (sum_v p_wv phi0_v)^{t_w} over the tables' sources gives, for
+    source counts q (sum_v q_v = t_w), multinomial(t_w; q) prod_v (p_wv phi0_v)^{q_v};
+    phi0 is integrated exactly as before with Q_kv = sum_{i,w} q_{ikwv}.
+    P: {(i, w): [(v, p), ...]} (entries in the sampler's order)."""
+
+    def __init__(self, *args, P=None, **kw):
+        super().__init__(*args, **kw)
+        self.P = {key: [(v, Fraction(p)) for v, p in ent] for key, ent in P.items()}
+
+    def states_q(self):
+        """Every valid (z, t, q): q[(i,w,k)] a tuple of per-entry source counts summing to t."""
+        for z, t in self.states():
+            keys = sorted(t)
+            splits = []
+            for c in keys:
+                i, w, k = c
+                S = len(self.P[(i, w)])
+                splits.append([q for q in itertools.product(range(t[c] + 1), repeat=S) if sum(q) == t[c]])
+            for qs in itertools.product(*splits):
+                yield z, t, dict(zip(keys, qs))
+
+    def joint_WZTQ(self, z, t, q):
+        K, V = self.K, self.V
+        p = Fraction(1)
+        for d in range(self.D):
+            toks = [x for x in range(self.N) if self.doc[x] == d]
+            if not toks:
+                continue
+            for k in range(K):
+                p *= rising(self.alpha, sum(1 for x in toks if z[x] == k))
+            p /= rising(K * self.alpha, len(toks))
+        Q = defaultdict(int)
+        for i in range(self.I):
+            for k in range(K):
+                words = [self.word[x] for x in range(self.N) if self.group[x] == i and z[x] == k]
+                if not words:
+                    continue
+                tw = {w: t[(i, w, k)] for w in set(words)}
+                p *= self._restaurant_coef(words, tw)
+                for w in set(words):
+                    qc = q[(i, w, k)]
+                    p *= multinomial(t[(i, w, k)], qc)
+                    for (v, pv), qv in zip(self.P[(i, w)], qc):
+                        p *= pv ** qv
+                        Q[(k, v)] += qv
+        for k in range(K):
+            Tk = 0
+            for v in range(V):
+                p *= rising(self.beta, Q[(k, v)])
+                Tk += Q[(k, v)]
+            p /= rising(V * self.beta, Tk)
+        return p
+
+    def joint_WZRV(self, z, t, q):
+        """p(W, Z, R, V) for any table-creator and per-table source assignment consistent
+        with (T, Q): p(W, Z, T, Q) / prod_cells C(m, t) multinomial(t; q)."""
+        m = self.cells(z)
+        den = Fraction(1)
+        for c, mv in m.items():
+            den *= comb(mv, t[c]) * multinomial(t[c], q[c])
+        return self.joint_WZTQ(z, t, q) / den
+
+    def posterior_q(self):
+        w = {}
+        for z, t, q in self.states_q():
+            w[(z, tuple(sorted(q.items())))] = self.joint_WZTQ(z, t, q)
+        tot = sum(w.values())
+        return {s: v / tot for s, v in w.items()}
+
+    def exact_conditional_q(self, z, t, q, p, r_rem, e_rem):
+        """Exact normalised conditional of (z_p, r_p, source) after removing token p
+        (its table with source entry e_rem when r_rem): slots k (S+1) + e (r = 1, entry e),
+        k (S+1) + S (r = 0), as ratios of p(W, Z, R, V)."""
+        i, w, k0 = self.group[p], self.word[p], z[p]
+        S = len(self.P[(i, w)])
+        tm, qm = dict(t), dict(q)
+        if r_rem:
+            tm[(i, w, k0)] -= 1
+            qq = list(qm[(i, w, k0)]); qq[e_rem] -= 1; qm[(i, w, k0)] = tuple(qq)
+        out = []
+        for k in range(self.K):
+            for slot in range(S + 1):
+                r = slot < S
+                z2 = list(z); z2[p] = k
+                t2, q2 = dict(tm), dict(qm)
+                c = (i, w, k)
+                if c not in q2:
+                    q2[c] = (0,) * S
+                    t2[c] = 0
+                if r:
+                    t2[c] += 1
+                    qq = list(q2[c]); qq[slot] += 1; q2[c] = tuple(qq)
+                m2 = self.cells(z2)
+                t2 = {cc: v for cc, v in t2.items() if cc in m2}
+                q2 = {cc: v for cc, v in q2.items() if cc in m2}
+                ok = all(1 <= t2.get(cc, 0) <= m2[cc] for cc in m2) and all(min(v) >= 0 for v in q2.values())
+                out.append(self.joint_WZRV(tuple(z2), t2, q2) if ok else Fraction(0))
+        tot = sum(out)
+        return [v / tot for v in out]

@@ -976,3 +976,349 @@ void or_topics(const ostate *s, double *phi0, double *phi) {
                 for (int i = 0; i < s->I; i++) phi[((size_t)i * s->K + k) * s->V + w] = or_phi(s, i, k, w);
         }
 }
+
+/* ================================================================== */
+/* NEXT-4: sparse non-identity transformation matrices P^i             */
+/* ================================================================== */
+/* The full SPDP of §2.4.6/§3.1: group
+ * i's word distribution for topic k is PDP(a, b, P^i phi0_k), so a table of
+ * restaurant (i,k) serving word w draws a *source* word v with probability
+ * p_{i,w,v} phi0_{k,v}.  State: z, r per token; q_{i,k,w,v} = tables of
+ * (i,k,w) whose source is v; t_{ikw} = sum_v q_{ikwv};
+ * Q_{k,v} = sum_{i,w} q_{ikwv} (the shadow counts of Eq. r1);
+ * T_k = sum_v Q_{kv}.  P^i is given per group as sparse rows: entries
+ * e in [pptr[i*V+w], pptr[i*V+w+1]) with source pv[e] and weight pp[e];
+ * the columns must sum to 1 (P^i phi0 is a distribution).
+ *
+ * Conditional (Alg.1 P:1698-1727 with Eq. r1's p_{i,w,v}): per topic k the
+ * slots (k, r=1, e) for the row's entries e in order, then (k, r=0):
+ *   r=0:   (alpha+n)/(b+M) (m-t+1)/(m+1) S^{m+1}_t/S^m_t
+ *   r=1,e: p_e (alpha+n)(b+a Tt)/(b+M) (t+1)/(m+1) (beta+Q_{k,v_e})/(V beta+T_k) S^{m+1}_{t+1}/S^m_t
+ * Removal (Alg.1 lines 3-9): r ~ Bernoulli(t/m) (reading c7); if r = 1 the
+ * removed table is uniform among the cell's t tables, i.e. its source entry
+ * e is the one where the integer j = floor(x3 t / 2^32) falls in the
+ * cumulative q counts of the cell (reading c26); keep rule c5 unchanged.
+ * Initial sources (reading c25): every table of a cell starts on the row's
+ * entry of largest p (first on ties).
+ * Wave merges (reading c24, the "error correction ... for q"): after a wave's
+ * deltas, q_e <- max(q_e, 0); if m = 0 all q_e = 0; else if sum q = 0 the
+ * largest-p entry gets one table; while sum q > m the largest q (first on
+ * ties) loses one.  With P^i = identity all of this is the identity-P sampler
+ * above, bit for bit (pinned). */
+typedef struct {
+    ostate *o;
+    int32_t E;
+    int32_t *pptr, *pv;
+    double *pp;
+    int32_t *q;          /* [E*K] */
+    int64_t *Qs;         /* [K*V] */
+    int32_t *best;       /* [I*V] entry of largest p in each row */
+} spstate;
+
+void or_sp_destroy(spstate *sp) {
+    if (!sp) return;
+    free(sp->pptr); free(sp->pv); free(sp->pp); free(sp->q); free(sp->Qs); free(sp->best);
+    free(sp);
+}
+
+static void sp_recompute(spstate *sp) {
+    ostate *s = sp->o;
+    int I = s->I, V = s->V, K = s->K;
+    memset(sp->Qs, 0, sizeof(int64_t) * (size_t)K * V);
+    memset(s->M, 0, sizeof(int64_t) * (size_t)I * K);
+    memset(s->Tt, 0, sizeof(int64_t) * (size_t)I * K);
+    memset(s->T, 0, sizeof(int64_t) * (size_t)K);
+    for (int i = 0; i < I; i++)
+        for (int w = 0; w < V; w++)
+            for (int k = 0; k < K; k++) {
+                size_t c = IDX3(s, i, w, k);
+                int32_t t = 0;
+                for (int32_t e = sp->pptr[i * V + w]; e < sp->pptr[i * V + w + 1]; e++) {
+                    int32_t qv = sp->q[(size_t)e * K + k];
+                    t += qv;
+                    sp->Qs[(size_t)k * V + sp->pv[e]] += qv;
+                }
+                s->t[c] = t;
+                s->M[(size_t)i * K + k] += s->m[c];
+                s->Tt[(size_t)i * K + k] += t;
+                s->T[k] += t;
+            }
+}
+
+/* o: a loaded oracle state (z, r, counts from or_load); its t become the q of
+ * the rows' largest-p entries.  Returns NULL on invalid P. */
+spstate *or_sp_create(ostate *o, const int32_t *pptr, const int32_t *pv, const double *pp) {
+    int I = o->I, V = o->V, K = o->K;
+    int32_t E = pptr[I * V];
+    if (pptr[0] != 0 || E < I * V) return NULL;
+    double *col = (double *)calloc((size_t)I * V, sizeof(double));
+    for (int r = 0; r < I * V; r++) {
+        if (pptr[r + 1] <= pptr[r]) { free(col); return NULL; }        /* every row needs a source */
+        for (int32_t e = pptr[r]; e < pptr[r + 1]; e++) {
+            if (pv[e] < 0 || pv[e] >= V || !(pp[e] > 0.0)) { free(col); return NULL; }
+            col[(size_t)(r / V) * V + pv[e]] += pp[e];
+        }
+    }
+    for (size_t c = 0; c < (size_t)I * V; c++)
+        if (fabs(col[c] - 1.0) > 1e-9) { free(col); return NULL; }       /* columns sum to 1 */
+    free(col);
+    spstate *sp = (spstate *)calloc(1, sizeof(spstate));
+    sp->o = o; sp->E = E;
+    sp->pptr = (int32_t *)malloc(sizeof(int32_t) * (size_t)(I * V + 1));
+    sp->pv = (int32_t *)malloc(sizeof(int32_t) * (size_t)E);
+    sp->pp = (double *)malloc(sizeof(double) * (size_t)E);
+    sp->q = (int32_t *)calloc((size_t)E * K, sizeof(int32_t));
+    sp->Qs = (int64_t *)calloc((size_t)K * V, sizeof(int64_t));
+    sp->best = (int32_t *)malloc(sizeof(int32_t) * (size_t)I * V);
+    memcpy(sp->pptr, pptr, sizeof(int32_t) * (size_t)(I * V + 1));
+    memcpy(sp->pv, pv, sizeof(int32_t) * (size_t)E);
+    memcpy(sp->pp, pp, sizeof(double) * (size_t)E);
+    for (int r = 0; r < I * V; r++) {
+        int32_t b = pptr[r];
+        for (int32_t e = pptr[r]; e < pptr[r + 1]; e++) if (pp[e] > pp[b]) b = e;
+        sp->best[r] = b;
+    }
+    for (int i = 0; i < I; i++)                                       /* reading c25 */
+        for (int w = 0; w < V; w++)
+            for (int k = 0; k < K; k++) sp->q[(size_t)sp->best[i * V + w] * K + k] = o->t[IDX3(o, i, w, k)];
+    sp_recompute(sp);
+    return sp;
+}
+
+/* log weights of the K (S+1) slots of token p (S = its row's entries), own
+ * contribution removed: one customer of k0 and, when r_rem, the table whose
+ * source entry is e_rem.  Slot of (k, r=1, e-th entry) = k(S+1) + e, (k, r=0) = k(S+1) + S. */
+static void sp_log_weights(const spstate *sp, int64_t p, int r_rem, int32_t e_rem, const int32_t *n, const int32_t *m,
+                           const int32_t *t, const int64_t *M, const int64_t *Tt, const int64_t *Qs, const int64_t *T,
+                           double *lw) {
+    const ostate *s = sp->o;
+    int K = s->K, V = s->V;
+    int i = s->group[p], w = s->word[p], d = s->doc[p], k0 = s->z[p];
+    int32_t e0 = sp->pptr[i * V + w], S = sp->pptr[i * V + w + 1] - e0;
+    double a = s->a[i], b = s->b[i], beta = s->beta;
+    const stable_t *St = &s->tab[i];
+    for (int k = 0; k < K; k++) {
+        int own = (k == k0);
+        double n_k = (double)n[(size_t)d * K + k] - own;
+        int64_t m_k = m[IDX3(s, i, w, k)] - own;
+        int64_t t_k = t[IDX3(s, i, w, k)] - own * r_rem;
+        double M_k = (double)M[(size_t)i * K + k] - own;
+        double Tt_k = (double)Tt[(size_t)i * K + k] - own * r_rem;
+        double T_k = (double)T[k] - own * r_rem;
+        double lS = stable_get(St, (int)m_k, (int)t_k);
+        double base = log(s->alpha[(size_t)i * K + k] + n_k) - log(b + M_k);
+        lw[(size_t)k * (S + 1) + S] = base + log((double)(m_k - t_k + 1)) - log((double)(m_k + 1))
+                                      + stable_get(St, (int)m_k + 1, (int)t_k) - lS;
+        double l1 = base + log(b + a * Tt_k) + log((double)(t_k + 1)) - log((double)(m_k + 1))
+                    - log((double)V * beta + T_k) + stable_get(St, (int)m_k + 1, (int)t_k + 1) - lS;
+        for (int32_t j = 0; j < S; j++) {
+            int32_t e = e0 + j, v = sp->pv[e];
+            double Q_kv = (double)Qs[(size_t)k * V + v] - ((own && r_rem && sp->pv[e_rem] == v) ? 1.0 : 0.0);
+            lw[(size_t)k * (S + 1) + j] = l1 + log(sp->pp[e]) + log(beta + Q_kv);
+        }
+    }
+}
+
+/* source entry of the removed table: j = floor(x3 t / 2^32) in the cumulative q of the cell (reading c26) */
+static int32_t sp_removed_entry(const spstate *sp, int i, int w, int k, uint32_t x3, int32_t t) {
+    int K = sp->o->K, V = sp->o->V;
+    int64_t j = (int64_t)(((uint64_t)x3 * (uint64_t)t) >> 32), cum = 0;
+    for (int32_t e = sp->pptr[i * V + w]; e < sp->pptr[i * V + w + 1]; e++) {
+        cum += sp->q[(size_t)e * K + k];
+        if (cum > j) return e;
+    }
+    return sp->pptr[i * V + w + 1] - 1;
+}
+
+static int32_t sp_max_row(const spstate *sp) {
+    int32_t mx = 1;
+    for (int r = 0; r < sp->o->I * sp->o->V; r++)
+        if (sp->pptr[r + 1] - sp->pptr[r] > mx) mx = sp->pptr[r + 1] - sp->pptr[r];
+    return mx;
+}
+
+/* Mode S: Alg.1 with the source variables (sequential, exact). */
+int or_sp_sweep_seq(spstate *sp) {
+    ostate *s = sp->o;
+    int K = s->K, V = s->V;
+    int32_t Smax = sp_max_row(sp);
+    double *lw = (double *)malloc(sizeof(double) * (size_t)K * (Smax + 1));
+    double *prob = (double *)malloc(sizeof(double) * (size_t)K * (Smax + 1));
+    if (!lw || !prob) { free(lw); free(prob); return -2; }
+    memset(s->stats, 0, sizeof(s->stats));
+    for (int64_t p = 0; p < s->N; p++) {
+        int i = s->group[p], w = s->word[p], d = s->doc[p], k = s->z[p];
+        int32_t e0 = sp->pptr[i * V + w], S = sp->pptr[i * V + w + 1] - e0;
+        size_t c = IDX3(s, i, w, k);
+        uint32_t x[4];
+        rng_token(s->seed, (uint32_t)p, s->sweep, x);
+        int keep, r = removal(x[0], s->m[c], s->t[c], &keep);
+        if (keep) { s->r[p] = 1; s->stats[0]++; continue; }
+        int32_t er = r ? sp_removed_entry(sp, i, w, k, x[3], s->t[c]) : e0;
+        sp_log_weights(sp, p, r, er, s->n, s->m, s->t, s->M, s->Tt, sp->Qs, s->T, lw);
+        s->n[(size_t)d * K + k]--; s->m[c]--; s->M[(size_t)i * K + k]--;
+        if (r) {
+            s->t[c]--; s->Tt[(size_t)i * K + k]--; s->T[k]--;
+            sp->q[(size_t)er * K + k]--; sp->Qs[(size_t)k * V + sp->pv[er]]--;
+        }
+        int ns = K * (S + 1);
+        normalise(ns, lw, prob);
+        int j = draw_slot(ns, prob, u53(x), NULL);
+        int kn = j / (S + 1), within = j % (S + 1), rn = within < S;
+        size_t cn = IDX3(s, i, w, kn);
+        s->n[(size_t)d * K + kn]++; s->m[cn]++; s->M[(size_t)i * K + kn]++;
+        if (rn) {
+            int32_t e = e0 + within;
+            s->t[cn]++; s->Tt[(size_t)i * K + kn]++; s->T[kn]++;
+            sp->q[(size_t)e * K + kn]++; sp->Qs[(size_t)kn * V + sp->pv[e]]++;
+        }
+        if (kn != k) s->stats[1]++;
+        s->z[p] = kn; s->r[p] = (uint8_t)rn;
+    }
+    s->sweep++;
+    free(lw); free(prob);
+    return 0;
+}
+
+/* Mode P on one shard: waves against the wave-start snapshot, then the
+ * wave's deltas and the q correction (reading c24).  force (optional, [N]):
+ * lock-step replay of another sampler's draws, as slot index
+ * (k (S+1) + within); own/margin as in or_sweep_par. */
+int or_sp_sweep_par(spstate *sp, int W, const int32_t *force, double *margin, int32_t *own) {
+    ostate *s = sp->o;
+    int I = s->I, V = s->V, K = s->K;
+    int64_t N = s->N;
+    size_t cells = (size_t)I * V * K;
+    int32_t Smax = sp_max_row(sp);
+    if (W < 1) return -1;
+    memset(s->stats, 0, sizeof(s->stats));
+    int32_t *m0 = (int32_t *)malloc(sizeof(int32_t) * cells), *t0 = (int32_t *)malloc(sizeof(int32_t) * cells);
+    int64_t *M0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K), *Tt0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K);
+    int64_t *Q0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)K * V), *T0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
+    int32_t *dq = (int32_t *)calloc((size_t)sp->E * K, sizeof(int32_t));
+    int32_t *dm = (int32_t *)calloc(cells, sizeof(int32_t));
+    int32_t *slot = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1)), *erem = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    int8_t *rr = (int8_t *)malloc((size_t)(N + 1)), *kept = (int8_t *)malloc((size_t)(N + 1));
+    double *lw = (double *)malloc(sizeof(double) * (size_t)K * (Smax + 1)), *prob = (double *)malloc(sizeof(double) * (size_t)K * (Smax + 1));
+    int rc = -2;
+    if (!m0 || !t0 || !M0 || !Tt0 || !Q0 || !T0 || !dq || !dm || !slot || !erem || !rr || !kept || !lw || !prob) goto out;
+    int32_t maxlen = 0;
+    for (int32_t d = 0; d < s->D; d++) if (s->doclen[d] > maxlen) maxlen = s->doclen[d];
+    int64_t nwaves = W < maxlen ? W : maxlen;
+    for (int64_t wave = 0; wave < nwaves; wave++) {
+        memcpy(m0, s->m, sizeof(int32_t) * cells); memcpy(t0, s->t, sizeof(int32_t) * cells);
+        memcpy(M0, s->M, sizeof(int64_t) * (size_t)I * K); memcpy(Tt0, s->Tt, sizeof(int64_t) * (size_t)I * K);
+        memcpy(Q0, sp->Qs, sizeof(int64_t) * (size_t)K * V); memcpy(T0, s->T, sizeof(int64_t) * (size_t)K);
+        /* (1) every token of the wave decides against the wave-start snapshot */
+        for (int64_t p = 0; p < N; p++) {
+            if (s->pos[p] % W != wave) continue;
+            int i = s->group[p], w = s->word[p], k0 = s->z[p];
+            int32_t e0 = sp->pptr[i * V + w], S = sp->pptr[i * V + w + 1] - e0;
+            size_t c = IDX3(s, i, w, k0);
+            uint32_t x[4];
+            rng_token(s->seed, (uint32_t)p, s->sweep, x);
+            int keep, r = removal(x[0], m0[c], t0[c], &keep);
+            rr[p] = (int8_t)r; kept[p] = (int8_t)keep;
+            if (keep) { slot[p] = -1; if (own) own[p] = -1; continue; }
+            /* the removed table's source from the snapshot's q (dq holds only this wave's deltas: still 0 here) */
+            erem[p] = r ? sp_removed_entry(sp, i, w, k0, x[3], t0[c]) : e0;
+            sp_log_weights(sp, p, r, erem[p], s->n, m0, t0, M0, Tt0, Q0, T0, lw);
+            int ns = K * (S + 1);
+            normalise(ns, lw, prob);
+            int j = draw_slot(ns, prob, u53(x), margin ? &margin[p] : NULL);
+            if (own) own[p] = j;
+            if (force && force[p] >= 0) { if (force[p] != j) s->stats[3]++; j = force[p]; }
+            slot[p] = j;
+        }
+        /* (2) apply the wave's deltas, correct q (reading c24), recompute t and the sums */
+        for (int64_t p = 0; p < N; p++) {
+            if (s->pos[p] % W != wave) continue;
+            if (kept[p]) { s->r[p] = 1; s->stats[0]++; continue; }
+            int i = s->group[p], w = s->word[p], d = s->doc[p], k0 = s->z[p];
+            int32_t e0 = sp->pptr[i * V + w], S = sp->pptr[i * V + w + 1] - e0;
+            int kn = slot[p] / (S + 1), within = slot[p] % (S + 1), rn = within < S;
+            s->n[(size_t)d * K + k0]--; s->n[(size_t)d * K + kn]++;
+            dm[IDX3(s, i, w, k0)]--; dm[IDX3(s, i, w, kn)]++;
+            if (rr[p]) dq[(size_t)erem[p] * K + k0]--;
+            if (rn) dq[(size_t)(e0 + within) * K + kn]++;
+            if (kn != k0) s->stats[1]++;
+            s->z[p] = kn; s->r[p] = (uint8_t)rn;
+        }
+        for (int i = 0; i < I; i++)
+            for (int w = 0; w < V; w++)
+                for (int k = 0; k < K; k++) {
+                    size_t c = IDX3(s, i, w, k);
+                    int32_t eb = sp->pptr[i * V + w], ee = sp->pptr[i * V + w + 1];
+                    int changed = 0, any = dm[c] != 0;
+                    for (int32_t e = eb; e < ee; e++) any |= dq[(size_t)e * K + k] != 0;
+                    if (!any) continue;
+                    s->m[c] += dm[c]; dm[c] = 0;
+                    int32_t t = 0;
+                    for (int32_t e = eb; e < ee; e++) {
+                        int32_t *qe = &sp->q[(size_t)e * K + k];
+                        *qe += dq[(size_t)e * K + k]; dq[(size_t)e * K + k] = 0;
+                        if (*qe < 0) { *qe = 0; changed = 1; }
+                        t += *qe;
+                    }
+                    if (s->m[c] == 0) {
+                        for (int32_t e = eb; e < ee; e++) if (sp->q[(size_t)e * K + k]) { sp->q[(size_t)e * K + k] = 0; changed = 1; }
+                    } else if (t == 0) {
+                        sp->q[(size_t)sp->best[i * V + w] * K + k] = 1; changed = 1;
+                    } else {
+                        while (t > s->m[c]) {
+                            int32_t eb2 = eb;
+                            for (int32_t e = eb; e < ee; e++) if (sp->q[(size_t)e * K + k] > sp->q[(size_t)eb2 * K + k]) eb2 = e;
+                            sp->q[(size_t)eb2 * K + k]--; t--; changed = 1;
+                        }
+                    }
+                    s->stats[2] += changed;
+                }
+        sp_recompute(sp);
+    }
+    s->sweep++;
+    rc = 0;
+out:
+    free(m0); free(t0); free(M0); free(Tt0); free(Q0); free(T0); free(dq); free(dm); free(slot); free(erem); free(rr);
+    free(kept); free(lw); free(prob);
+    return rc;
+}
+
+/* state read-out: q [E*K], Qs [K*V] (t, m, n, z, r through or_get on sp->o) */
+void or_sp_get(const spstate *sp, int32_t *q, int64_t *Qs) {
+    if (q) memcpy(q, sp->q, sizeof(int32_t) * (size_t)sp->E * sp->o->K);
+    if (Qs) memcpy(Qs, sp->Qs, sizeof(int64_t) * (size_t)sp->o->K * sp->o->V);
+}
+/* set the sources (q) of the current state (tests: enumeration of (z, t, q) states) */
+int or_sp_set_q(spstate *sp, const int32_t *q) {
+    memcpy(sp->q, q, sizeof(int32_t) * (size_t)sp->E * sp->o->K);
+    sp_recompute(sp);
+    return 0;
+}
+/* normalised conditional of token p after removing it with (r_rem, e_rem) (tests) */
+int or_sp_conditional(const spstate *sp, int64_t p, int r_rem, int32_t e_rem, double *prob) {
+    const ostate *s = sp->o;
+    int i = s->group[p], w = s->word[p], k0 = s->z[p];
+    size_t c = IDX3(s, i, w, k0);
+    int32_t e0 = sp->pptr[i * s->V + w], S = sp->pptr[i * s->V + w + 1] - e0;
+    if (r_rem && (s->t[c] < 1 || sp->q[(size_t)e_rem * s->K + k0] < 1 || (s->t[c] == 1 && s->m[c] > 1))) return -1;
+    if (!r_rem && s->t[c] == s->m[c]) return -1;
+    double *lw = (double *)malloc(sizeof(double) * (size_t)s->K * (S + 1));
+    sp_log_weights(sp, p, r_rem, r_rem ? e_rem : e0, s->n, s->m, s->t, s->M, s->Tt, sp->Qs, s->T, lw);
+    normalise(s->K * (S + 1), lw, prob);
+    free(lw);
+    return 0;
+}
+/* (z, q) code after each of nsweeps sequential (W < 0) or wave (W >= 1) sweeps (tests; tiny corpora) */
+int or_sp_chain_codes(spstate *sp, int64_t nsweeps, int W, int qbase, int64_t *codes) {
+    ostate *s = sp->o;
+    for (int64_t it = 0; it < nsweeps; it++) {
+        int rc = (W < 0) ? or_sp_sweep_seq(sp) : or_sp_sweep_par(sp, W, NULL, NULL, NULL);
+        if (rc) return rc;
+        int64_t code = 0, mul = 1;
+        for (int64_t p = 0; p < s->N; p++) { code += mul * s->z[p]; mul *= s->K; }
+        int64_t qc = 0, qm = 1;
+        for (int64_t j = 0; j < (int64_t)sp->E * s->K; j++) { qc += qm * sp->q[j]; qm *= qbase; }
+        codes[it] = code + mul * qc;
+    }
+    return 0;
+}
