@@ -244,6 +244,29 @@ spdp_status spdp_heldout(spdp_ctx* ctx, int64_t num_tokens, int32_t num_docs, co
  * (SPDP_EINVAL otherwise).  Not collective. */
 spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t* perm);
 
+/* ---- Sparse transformation matrices -------------
+ *
+ * spdp_set_transform: the full SPDP of PAPER.md:985-1014 — group i's base for
+ * topic k is P^i phi0_k, so every table of (i, k, w) has a source word v drawn
+ * with probability p_{i,w,v} phi0_{k,v} (Eq. r1 P:1688-1693 carries p_{i,w,v};
+ * Alg.1 lines 6-9 and 19-21 remove / add the table's source).  P^i as sparse
+ * rows over r = i * V + w: entries [pptr[r], pptr[r+1]) with source word pv[e]
+ * in [0, V) and weight pp[e] > 0; every row needs >= 1 entry (<= 32767) and
+ * every column of every P^i must sum to 1 (±1e-9; P^i phi0 is a distribution,
+ * P:990-993).  Host arrays, copied.  Call after spdp_create and before
+ * spdp_load_corpus.  This version: world_size == 1, SPDP_UPDATE_WAVE; the
+ * likelihood / held-out / diagnostics calls return SPDP_ESTATE.  Readings:
+ * DESIGN.md §13 (c24 wave correction of the sources, c25 initial sources,
+ * c26 the removed table's source).  Errors: SPDP_EINVAL, SPDP_ESTATE.
+ *
+ * spdp_sparse_state: q [E*K] int32 (tables of (i, k, w) per source entry, in
+ * the caller's entry order, row-major e, k), shadow [K*V] int32
+ * (Q_{k,v} = sum_{i,w} q_{i,k,w,v}), src [N] int16 (the source entry, within
+ * its row, chosen at each token's last draw; -1 for r = 0 and kept tokens).
+ * Any output may be NULL. */
+spdp_status spdp_set_transform(spdp_ctx* ctx, const int32_t* pptr, const int32_t* pv, const double* pp);
+spdp_status spdp_sparse_state(spdp_ctx* ctx, int32_t* q, int32_t* shadow, int16_t* src);
+
 /* Diagnostics (parity tests): for n local tokens (canonical ids), the
  * normalised 2K-slot conditional (slot 2k = (k, r=1), slot 2k+1 = (k, r=0);
  * Alg.4) that the NEXT sweep would draw from if the

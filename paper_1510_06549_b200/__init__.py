@@ -35,7 +35,8 @@ _NAMES = {0: "SPDP_OK", -1: "SPDP_EINVAL", -2: "SPDP_ENOMEM", -3: "SPDP_ECUDA", 
 EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "spdp_sweep_local",
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
-           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr"]
+           "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr",
+           "spdp_set_transform", "spdp_sparse_state"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -85,7 +86,7 @@ def lib():
             "spdp_partition": [C.c_uint64, I32, I64, I32, P, P], "spdp_nccl_unique_id": [P],
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
-            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P],
+            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -333,6 +334,20 @@ class Sampler:
     def counts(self, out=None, **which):
         return spdp_counts(self.ctx, self.N, self.D, self.I, self.V, self.K, out=out, **which)
 
+    def set_transform(self, pptr, pv, pp):
+        """NEXT-4: sparse P^i rows over r = i * V + w (before load_corpus)."""
+        self._P = (np.ascontiguousarray(pptr, np.int32), np.ascontiguousarray(pv, np.int32),
+                   np.ascontiguousarray(pp, np.float64))
+        _check(lib().spdp_set_transform(self.ctx, *(_p(a) for a in self._P)), self.ctx)
+        return self
+
+    def sparse_state(self):
+        E = int(self._P[0][-1])
+        q = np.zeros((E, self.K), np.int32); Q = np.zeros((self.K, self.V), np.int32)
+        src = np.zeros(self.N, np.int16)
+        _check(lib().spdp_sparse_state(self.ctx, _p(q), _p(Q), _p(src)), self.ctx)
+        return {"q": q, "Qs": Q, "src": src}
+
     def zr(self, out=None):
         return spdp_zr(self.ctx, self.N, out)
 
@@ -386,7 +401,9 @@ class Sampler:
 
 
 def sampler_for(corpus, num_topics, alpha=0.1, beta=0.1, discount=0.7, concentration=100.0, seed=7,
-                num_waves=1, z_init=None, r_init=None, **kw) -> Sampler:
+                num_waves=1, z_init=None, r_init=None, transform=None, **kw) -> Sampler:
     s = Sampler(corpus.num_groups, corpus.vocab, num_topics, alpha=alpha, beta=beta, discount=discount,
                 concentration=concentration, seed=seed, num_waves=num_waves, **kw)
+    if transform is not None:
+        s.set_transform(*transform)
     return s.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs, z_init, r_init)

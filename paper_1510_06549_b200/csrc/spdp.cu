@@ -12,6 +12,7 @@
 #include "spdp_eval.cuh"
 #include "spdp_plan.cuh"
 #include "spdp_token.cuh"
+#include "spdp_sparse.cuh"
 
 #include <dlfcn.h>
 
@@ -140,6 +141,17 @@ struct spdp_ctx {
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
     float* d_R1 = nullptr;                        // token kernel: r = 1 shares [run][Kp]
+    // NEXT-4: sparse transformation matrices P^i (spdp_set_transform)
+    bool sparse = false;
+    std::vector<int32_t> h_pptr, h_pv;            // caller's rows (i, w): i * V + w
+    std::vector<double> h_pp;
+    std::vector<uint32_t> dev_of_user;             // caller's entry -> device entry (segment order)
+    std::vector<uint32_t> h_sptr;                  // device rows (segments w * I + i)
+    uint32_t E_sp = 0;
+    uint32_t* d_sptr = nullptr;
+    int32_t *d_spv = nullptr, *d_best = nullptr, *d_q = nullptr, *d_dq = nullptr;
+    float* d_spp = nullptr;
+    int16_t* d_src = nullptr;
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
     int colstart[8] = {0};
@@ -504,6 +516,8 @@ spdp_status ensure_host_plan(spdp_ctx* c) {
     return SPDP_OK;
 }
 
+void sparse_install(spdp_ctx* c);
+
 // Upload (z, r or tables) as the sampler state; counts from z
 // are built on the device.
 spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in, const int32_t* tables) {
@@ -568,6 +582,7 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
     if (c->d_Dloc) CU(cudaMemsetAsync(c->d_Dloc, 0, c->dbytes(), c->stream));
     launch_merge(c, c->d_dm, c->d_dt);    // zero deltas: recomputes Q and the sums
+    if (c->sparse) sparse_install(c);
     s = check_launch(c, "install_state kernels");
     if (s) return s;
     return sync(c, "install_state");
@@ -584,6 +599,116 @@ spdp_status ensure_events(spdp_ctx* c) {
 }
 inline void rec(spdp_ctx* c, size_t j) {
     if (c->profiling) cudaEventRecord(c->ev[j], c->stream);
+}
+
+// ---------------------------------------------------------------- NEXT-4: sparse P^i
+SparseP sparse_args(spdp_ctx* c) {
+    SparseP P{};
+    P.sptr = c->d_sptr; P.pv = c->d_spv; P.pp = c->d_spp; P.best = c->d_best; P.q = c->d_q; P.dq = c->d_dq;
+    return P;
+}
+
+// device copy of P in segment order (seg = w * I + i), q / dq / source buffers
+spdp_status sparse_upload(spdp_ctx* c) {
+    const int I = c->I, V = c->V, Kp = c->Kp;
+    const uint32_t segs = (uint32_t)V * I;
+    c->h_sptr.assign((size_t)segs + 1, 0);
+    for (int w = 0; w < V; ++w)
+        for (int i = 0; i < I; ++i) {
+            const int r = i * V + w;
+            c->h_sptr[(size_t)w * I + i + 1] = (uint32_t)(c->h_pptr[(size_t)r + 1] - c->h_pptr[(size_t)r]);
+        }
+    for (uint32_t sg = 0; sg < segs; ++sg) c->h_sptr[sg + 1] += c->h_sptr[sg];
+    c->E_sp = c->h_sptr[segs];
+    std::vector<int32_t> pv(c->E_sp), best(segs);
+    std::vector<float> pp(c->E_sp);
+    c->dev_of_user.assign(c->E_sp, 0);
+    for (int w = 0; w < V; ++w)
+        for (int i = 0; i < I; ++i) {
+            const int r = i * V + w;
+            const uint32_t sg = (uint32_t)w * I + i;
+            uint32_t d = c->h_sptr[sg];
+            int32_t b = c->h_pptr[(size_t)r];
+            for (int32_t e = c->h_pptr[(size_t)r]; e < c->h_pptr[(size_t)r + 1]; ++e, ++d) {
+                pv[d] = c->h_pv[(size_t)e];
+                pp[d] = (float)c->h_pp[(size_t)e];
+                c->dev_of_user[(size_t)e] = d;
+                if (c->h_pp[(size_t)e] > c->h_pp[(size_t)b]) b = e;
+            }
+            best[sg] = (int32_t)(c->h_sptr[sg] + (uint32_t)(b - c->h_pptr[(size_t)r]));
+        }
+    ALLOC(c->d_sptr, (size_t)segs + 1); ALLOC(c->d_spv, c->E_sp); ALLOC(c->d_spp, c->E_sp); ALLOC(c->d_best, segs);
+    ALLOC(c->d_q, (size_t)c->E_sp * Kp); ALLOC(c->d_dq, (size_t)c->E_sp * Kp);
+    ALLOC(c->d_src, (size_t)std::max<int64_t>(c->Nloc, 1));
+    CU(cudaMemcpy(c->d_sptr, c->h_sptr.data(), sizeof(uint32_t) * c->h_sptr.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_spv, pv.data(), sizeof(int32_t) * pv.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_spp, pp.data(), sizeof(float) * pp.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(c->d_best, best.data(), sizeof(int32_t) * best.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemset(c->d_dq, 0, sizeof(int32_t) * (size_t)c->E_sp * Kp));
+    CU(cudaMemset(c->d_src, 0xFF, sizeof(int16_t) * (size_t)std::max<int64_t>(c->Nloc, 1)));
+    return SPDP_OK;
+}
+
+// after the identity-P state installation: sources of the tables (reading c25), Q[v][k] from q
+void sparse_install(spdp_ctx* c) {
+    const int Kp = c->Kp;
+    SparseP P = sparse_args(c);
+    cudaMemsetAsync(c->d_q, 0, sizeof(int32_t) * (size_t)c->E_sp * Kp, c->stream);
+    const uint32_t segs = (uint32_t)c->V * c->I;
+    sp_init_q_kernel<<<148 * 8, 256, 0, c->stream>>>(P, c->d_t, segs, Kp);
+    cudaMemsetAsync(c->d_Q, 0, sizeof(int32_t) * (size_t)c->V * Kp, c->stream);
+    sp_shadow_kernel<<<148 * 8, 256, 0, c->stream>>>(P, c->E_sp, c->K, Kp, c->d_Q);
+}
+
+// one wave of the sparse sweep: factors of the wave's segments, tokens, n, merge
+void sparse_wave(spdp_ctx* c, int w) {
+    const uint32_t r0 = c->wave_seg_begin[(size_t)w], r1 = c->wave_seg_begin[(size_t)w + 1];
+    const uint32_t tb = c->wave_tok_begin[(size_t)w], te = c->wave_tok_begin[(size_t)w + 1];
+    if (te <= tb) return;
+    SparseP P = sparse_args(c);
+    const int Kp = c->Kp;
+    const float beta = (float)c->cfg.beta, vbeta = (float)((double)c->V * c->cfg.beta);
+    const size_t nf = (size_t)(r1 - r0) * Kp;
+    sp_factor_kernel<<<(int)std::max<size_t>(1, std::min<size_t>((nf + 255) / 256, (size_t)148 * 16)), 256, 0, c->stream>>>(
+        P, c->d_wave_segs, r0, r1, c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->d_disc, c->d_conc, c->d_tab,
+        c->d_tab_off, beta, vbeta, c->I, c->K, Kp, c->d_F, c->d_R1);
+    SpTokenArgs t{};
+    t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
+    t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.src = c->d_src; t.F = c->d_F; t.R1 = c->d_R1; t.n = c->d_n;
+    t.sigma = c->d_sigma;
+    const int nbl = c->KPL / 4;
+    for (int B = 0; B < 256; ++B) t.bpos[B] = (B < Kp / 4) ? c->colstart[B % nbl] + B / nbl : 0;
+    t.m = c->d_m; t.t = c->d_t; t.Q = c->d_Q; t.M = c->d_M; t.Tt = c->d_Tt; t.T = c->d_T; t.dm = c->d_dm;
+    t.alpha = c->d_alpha; t.disc = c->d_disc; t.conc = c->d_conc; t.tab = c->d_tab; t.tab_off = c->d_tab_off;
+    t.beta = beta; t.vbeta = vbeta; t.I = c->I; t.K = c->K; t.Kp = Kp;
+    t.key0 = (uint32_t)c->cfg.seed; t.key1 = (uint32_t)(c->cfg.seed >> 32);
+    t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats; t.P = P;
+    const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
+    if (c->row16) sp_token_kernel<uint16_t><<<std::max(grid, 1), 256, 0, c->stream>>>(t);
+    else sp_token_kernel<float><<<std::max(grid, 1), 256, 0, c->stream>>>(t);
+    if (c->W == 1) {
+        const size_t smem = sizeof(int) * 8 * (size_t)Kp;
+        if (c->row16)
+            recount_docs_kernel<uint16_t><<<148 * 8, 256, smem, c->stream>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
+                                                                             c->d_sigma, c->Dloc, Kp, (uint16_t*)c->d_n);
+        else
+            recount_docs_kernel<float><<<148 * 8, 256, smem, c->stream>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
+                                                                          c->d_sigma, c->Dloc, Kp, (float*)c->d_n);
+        std::swap(c->d_zr, c->d_zr_next);
+    } else {
+        const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
+        if (c->row16)
+            apply_tokens_kernel<uint16_t><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
+                c->d_tok_doc, c->d_zr, c->d_zr_next, (uint16_t*)c->d_n, c->d_sigma, Kp, tb, te);
+        else
+            apply_tokens_kernel<float><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
+                c->d_tok_doc, c->d_zr, c->d_zr_next, (float*)c->d_n, c->d_sigma, Kp, tb, te);
+    }
+    const int blocks = (int)std::min<uint32_t>((r1 - r0 + 7) / 8, 148u * 4u);
+    sp_merge_kernel<<<std::max(blocks, 1), 256, 0, c->stream>>>(P, c->d_wave_segs + r0, (int)(r1 - r0), c->d_m, c->d_t,
+                                                                c->d_dm, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->I, c->K, Kp,
+                                                                c->d_stats);
+    c->launches += 4;
 }
 
 // W = 1 in P word-range parts (DESIGN.md §5 "exchange pipelining").  Semantics are those of the
@@ -713,6 +838,15 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
         return check_launch(c, "async sweep");
     }
     if (c->P > 1) return run_parts(c, a);
+    if (c->sparse) {
+        for (int w = w0; w < w1; ++w) {
+            rec(c, 4 * (size_t)w);
+            sparse_wave(c, w);
+            rec(c, 4 * (size_t)w + 1); rec(c, 4 * (size_t)w + 2); rec(c, 4 * (size_t)w + 3);
+            c->acc[5] += 1;
+        }
+        return check_launch(c, "sparse sweep");
+    }
     for (int w = w0; w < w1; ++w) {
         const uint32_t cb = c->wave_chunk_begin[(size_t)w], ce = c->wave_chunk_begin[(size_t)w + 1];
         rec(c, 4 * (size_t)w);
@@ -920,6 +1054,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     spdp_status s = guard(c, false);
     if (s) return s;
     if (c->loaded) return fail(c, SPDP_ESTATE, "spdp_load_corpus may be called once per context");
+    if (c->sparse && (c->G > 1 || c->async))
+        return fail(c, SPDP_EINVAL, "a transformation matrix needs world_size == 1 and SPDP_UPDATE_WAVE in this version");
     if (num_tokens < 1 || num_docs < 1 || !group || !doc || !word)
         return fail(c, SPDP_EINVAL, "need num_tokens >= 1, num_docs >= 1 and the three token arrays");
     if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
@@ -1007,7 +1143,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         c->P = (W == 1 && c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL && !c->async &&
                 num_tokens / c->G >= (int64_t)8000000) ? 4 : 1;
         if (const char* e = getenv("SPDP_EXCHANGE_PARTS")) c->P = std::min(std::max(atoi(e), 1), 16);
-        if (W != 1 || c->async) c->P = 1;
+        if (W != 1 || c->async || c->sparse) c->P = 1;
         c->part_word.assign((size_t)c->P + 1, (uint32_t)V);
         c->part_word[0] = 0;
         if (c->P > 1) {
@@ -1023,7 +1159,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
     }
     // small K: the token kernel (packed per-wave deltas need |delta| <= count(i,w) < 2^15)
-    c->token_kernel = !c->async && c->K <= 64 && c->mmax < 32768;
+    c->token_kernel = !c->async && !c->sparse && c->K <= 64 && c->mmax < 32768;
     if (const char* e = getenv("SPDP_TOKEN_KERNEL")) c->token_kernel = c->token_kernel && atoi(e) != 0;
     // documents -> ranks
     if (c->G > 1) partition_docs(c->cfg.seed, c->G, num_tokens, num_docs, c->doclen, c->shard_of_doc);
@@ -1109,7 +1245,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, drlen.p, droff.p, (int)R, st); },
                              "segment offsets")))
                 return s;
-            if (c->token_kernel) {
+            if (c->token_kernel || c->sparse) {
                 ALLOC(c->d_tok_run, nl);
                 ALLOC(c->d_F, (size_t)R * Kp);
                 ALLOC(c->d_R1, (size_t)R * Kp);
@@ -1336,6 +1472,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         if (s) return s;
     }
     lt.mark("Stirling-ratio tables");
+    if (c->sparse && (s = sparse_upload(c))) return s;
     s = install_state(c, z_init, r_init, nullptr);
     if (s) return s;
     lt.mark("initial state (counts)");
@@ -1522,6 +1659,63 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
     return SPDP_OK;
 }
 
+spdp_status spdp_set_transform(spdp_ctx* c, const int32_t* pptr, const int32_t* pv, const double* pp) {
+    spdp_status s = guard(c, false);
+    if (s) return s;
+    if (c->loaded) return fail(c, SPDP_ESTATE, "spdp_set_transform must precede spdp_load_corpus");
+    if (!pptr || !pv || !pp) return fail(c, SPDP_EINVAL, "null transformation arrays");
+    const int I = c->I, V = c->V;
+    const int64_t rows = (int64_t)I * V;
+    if (pptr[0] != 0) return fail(c, SPDP_EINVAL, "pptr[0] must be 0");
+    std::vector<double> col((size_t)rows, 0.0);
+    for (int64_t r = 0; r < rows; ++r) {
+        if (pptr[r + 1] <= pptr[r]) return fail(c, SPDP_EINVAL, "row (i=%lld, w=%lld) of P has no entry", (long long)(r / V), (long long)(r % V));
+        if (pptr[r + 1] - pptr[r] > 32767) return fail(c, SPDP_EINVAL, "a row of P has more than 32767 entries");
+        for (int32_t e = pptr[r]; e < pptr[r + 1]; ++e) {
+            if (pv[e] < 0 || pv[e] >= V || !(pp[e] > 0.0)) return fail(c, SPDP_EINVAL, "entry %d of P is invalid", e);
+            col[(size_t)(r / V) * V + pv[e]] += pp[e];
+        }
+    }
+    for (size_t j = 0; j < col.size(); ++j)
+        if (std::fabs(col[j] - 1.0) > 1e-9)
+            return fail(c, SPDP_EINVAL, "column %zu of P^%zu sums to %.12g, not 1", j % (size_t)V, j / (size_t)V, col[j]);
+    c->h_pptr.assign(pptr, pptr + rows + 1);
+    c->h_pv.assign(pv, pv + pptr[rows]);
+    c->h_pp.assign(pp, pp + pptr[rows]);
+    c->sparse = true;
+    return SPDP_OK;
+}
+
+spdp_status spdp_sparse_state(spdp_ctx* c, int32_t* q, int32_t* shadow, int16_t* src) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!c->sparse) return fail(c, SPDP_ESTATE, "no transformation matrix (spdp_set_transform)");
+    const int K = c->K, Kp = c->Kp, V = c->V;
+    if (q) {
+        std::vector<int32_t> dq((size_t)c->E_sp * Kp);
+        CU(cudaMemcpyAsync(dq.data(), c->d_q, sizeof(int32_t) * dq.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "sparse q"))) return s;
+        for (size_t e = 0; e < c->dev_of_user.size(); ++e)
+            for (int k = 0; k < K; ++k) q[e * K + k] = dq[(size_t)c->dev_of_user[e] * Kp + k];
+    }
+    if (shadow) {
+        std::vector<int32_t> Q((size_t)V * Kp);
+        CU(cudaMemcpyAsync(Q.data(), c->d_Q, sizeof(int32_t) * Q.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "sparse Q"))) return s;
+        for (int v = 0; v < V; ++v)
+            for (int k = 0; k < K; ++k) shadow[(size_t)k * V + v] = Q[(size_t)v * Kp + k];
+    }
+    if (src) {
+        if ((s = ensure_host_plan(c))) return s;
+        std::vector<int16_t> d((size_t)c->Nloc);
+        if (c->Nloc) CU(cudaMemcpyAsync(d.data(), c->d_src, sizeof(int16_t) * d.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "sparse src"))) return s;
+        for (int64_t p = 0; p < c->N; ++p) src[p] = -1;
+        for (int64_t q2 = 0; q2 < c->Nloc; ++q2) src[c->sorted_tok[(size_t)q2]] = d[(size_t)q2];
+    }
+    return SPDP_OK;
+}
+
 spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
     spdp_status s = guard(c, true);
     if (s) return s;
@@ -1548,6 +1742,7 @@ spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
 spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
+    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
     const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
     if (perplexity) {
         SweepArgs a = base_args(c);
@@ -1636,6 +1831,7 @@ spdp_status launch_phi_table(spdp_ctx* c, double* phi, double* phi0) {
 spdp_status spdp_topics(spdp_ctx* c, double* phi0, double* phi) {
     spdp_status s = guard(c, true);
     if (s) return s;
+    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     TempBuf<double> dphi(c->cells), dphi0((size_t)K * V);
     if (!dphi.p || !dphi0.p) return fail(c, SPDP_ENOMEM, "spdp_topics buffers");
@@ -1662,6 +1858,7 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
                          const int32_t* z_init, int32_t* z_out, double* theta, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
+    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     if (num_tokens < 0 || num_tokens > (int64_t)UINT32_MAX || num_docs < 1 || iterations < 0 || first_iteration < 0 ||
         (num_tokens > 0 && (!group || !doc || !word)))
@@ -1787,6 +1984,7 @@ spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t
 spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, double* probs, int32_t* info) {
     spdp_status s = guard(c, true);
     if (s) return s;
+    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
     if (n < 0 || (n > 0 && (!tok_ids || !probs))) return fail(c, SPDP_EINVAL, "bad debug_probs arguments");
     if (n == 0) return SPDP_OK;
     const int I = c->I, K = c->K;

@@ -1,0 +1,77 @@
+"""GPU parity of NEXT-4 (sparse transformation matrices P^i)
+through the C ABI: spdp_set_transform + spdp_sweep against the oracle's
+sparse sampler (tests/test_oracle_sparse_p.py pins it), in lock-step: the
+oracle replays each sweep with every draw forced to the GPU's (topic, table
+indicator and source entry) and reports its own; mismatches only within 1e-6
+of a CDF boundary; counts (m, t, q, Q) bit-exact when the draws agree."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1510_06549_b200 as spdp
+from gpu_util import HYPER, corpus, require_gpu
+from test_oracle_sparse_p import identity_P, mixing_P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    require_gpu()
+
+
+def _pair(c, K, P, waves):
+    g = spdp.sampler_for(c, K, num_waves=waves, transform=P, **HYPER)
+    o = oracle.from_corpus(c, K, **HYPER)
+    return g, o, oracle.SparseOracle(o, *P)
+
+
+def _lockstep(g, sp, P, waves):
+    pptr = np.asarray(P[0])
+    g.sweep(1)
+    gc = g.counts()
+    gs = g.sparse_state()
+    rows = pptr[np.asarray(sp.base._tok[0]) * sp.base.V + np.asarray(sp.base._tok[2])]
+    S = pptr[np.asarray(sp.base._tok[0]) * sp.base.V + np.asarray(sp.base._tok[2]) + 1] - rows
+    force = gc["z"] * (S + 1) + np.where(gc["r"] == 1, gs["src"], S)
+    force = np.where(gs["src"] == -1, np.where(gc["r"] == 1, -1, force), force)   # kept tokens: no draw
+    mg, own = sp.sweep_par(waves=waves, force=force.astype(np.int32), want_margin=True, want_own=True)
+    drawn = force >= 0
+    mism = np.nonzero(drawn & (own != force))[0]
+    return gc, gs, mism, mg
+
+
+@pytest.mark.parametrize("K,waves,kind", [(10, 1, "mix"), (10, 3, "mix"), (10, 1, "id"), (100, 1, "mix"),
+                                          (37, 2, "mix")])
+def test_sparse_sweep_lockstep(K, waves, kind):
+    c = corpus("C1")
+    P = identity_P(c.num_groups, c.vocab) if kind == "id" else mixing_P(c.num_groups, c.vocab, np.random.default_rng(1))
+    g, o, sp = _pair(c, K, P, waves)
+    for s in range(3):
+        gc, gs, mism, mg = _lockstep(g, sp, P, waves)
+        assert len(mism) <= max(1, 1e-4 * c.num_tokens), len(mism)
+        assert (mg[mism] <= 1e-6).all(), mg[mism]
+        st = sp.state()
+        if len(mism) == 0:
+            for k in ("z", "r", "n", "m", "t"):
+                np.testing.assert_array_equal(gc[k], st[k], err_msg=k)
+            np.testing.assert_array_equal(gs["q"], st["q"])
+            np.testing.assert_array_equal(gs["Qs"], st["Qs"])
+    assert (gs["q"] >= 0).all()
+
+
+def test_sparse_transform_validation():
+    c = corpus("C1")
+    g = spdp.Sampler(c.num_groups, c.vocab, 10, **HYPER)
+    pptr, pv, pp = mixing_P(c.num_groups, c.vocab, np.random.default_rng(2))
+    bad = pp.copy(); bad[0] *= 0.5
+    with pytest.raises(spdp.SPDPError) as e:
+        g.set_transform(pptr, pv, bad)
+    assert e.value.code == spdp.SPDP_EINVAL
+    g.set_transform(pptr, pv, pp)
+    g.load_corpus(c.group, c.doc, c.word, c.num_docs)
+    with pytest.raises(spdp.SPDPError) as e:
+        g.set_transform(pptr, pv, pp)
+    assert e.value.code == spdp.SPDP_ESTATE
+    with pytest.raises(spdp.SPDPError):
+        g.perplexity()
