@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--mode", default="sweep", choices=["sweep", "heldout"],
                     help="heldout: NEXT-1 fold-in + held-out perplexity of the 10%% hold-out (separate line)")
     ap.add_argument("--foldin-iters", type=int, default=20)
+    ap.add_argument("--transform", default="none", choices=["none", "mix"],
+                    help="mix: NEXT-4 sparse P^i = (1-e) I + e Perm_i (2 sources per word, seeded)")
     ap.add_argument("--update", default="wave", choices=["wave", "async"],
                     help="async: NEXT-2, the paper's immediate-update in-GPU scheme (nondeterministic)")
     ap.add_argument("--train-sweeps", type=int, default=20)
@@ -162,6 +164,22 @@ def cpu_baseline(corpus, cfg, K, waves, sample_tokens):
                       f"{dt:.1f} s incl. the sweep's fixed per-wave passes"}
 
 
+def mixing_transform(I, V, seed):
+    """NEXT-4 workload: P^i = (1 - e_i) Id + e_i Perm_i (doubly stochastic, 2 sources per word)."""
+    rng = np.random.default_rng(seed)
+    pptr, pv, pp = [0], [], []
+    for i in range(I):
+        perm = rng.permutation(V)
+        eps = 0.1 + 0.05 * (i % 4)
+        for w in range(V):
+            ent = {w: 1.0 - eps}
+            ent[int(perm[w])] = ent.get(int(perm[w]), 0.0) + eps
+            for v in sorted(ent):
+                pv.append(v); pp.append(ent[v])
+            pptr.append(len(pv))
+    return np.array(pptr, np.int32), np.array(pv, np.int32), np.array(pp)
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -182,7 +200,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     workload = f"{cfg.name}: I={cfg.groups} groups x {cfg.docs_per_group} docs, mean len {cfg.mean_len}, " \
-               f"V={cfg.vocab}, K={K}, W={args.waves}" + (", async updates (NEXT-2)" if args.update == "async" else "")
+               f"V={cfg.vocab}, K={K}, W={args.waves}" + (", async updates (NEXT-2)" if args.update == "async" else "") \
+               + (", sparse P^i with 2 sources per word (NEXT-4)" if args.transform == "mix" else "")
 
     if args.impl == "reference":
         return run_reference(args, cfg, K, world, rank, workload)
@@ -225,7 +244,10 @@ def main():
             dist.barrier()
 
     # ---------------- device-resident throughput (value) ----------------
+    transform = mixing_transform(cfg.groups, cfg.vocab, cfg.seed) if args.transform == "mix" else None
     g = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
+    if transform is not None:
+        g.set_transform(*transform)
     g.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs)
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     for _ in range(args.warmup):
@@ -254,7 +276,7 @@ def main():
         ms = float(t.item())
     value = N / (ms / 1e3)
     stats = g.stats()
-    _, ppl = g.loglik(log_joint=False)
+    ppl = g.loglik(log_joint=False)[1] if transform is None else None
     g.close()
 
     # roofline of the dominant kernel (sample_kernel), from this run's CUDA events
@@ -267,7 +289,7 @@ def main():
     sample_ms = tm["sample_ms"] / max(tm["sample_launches"], 1) * args.waves   # per sweep (all waves)
     bytes_sweep = alg_bytes(plan, K)
     achieved = bytes_sweep / (sample_ms / 1e3) / 1e9
-    kname = "token_kernel" if stats.get("token_kernel") else "sample_kernel"
+    kname = "sp_token_kernel" if transform is not None else ("token_kernel" if stats.get("token_kernel") else "sample_kernel")
     traffic = load_traffic(cfg.name, K, kname.split("_")[0])
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
@@ -283,6 +305,8 @@ def main():
     e2e_steps = args.steps
     t0 = time.perf_counter()
     h = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
+    if transform is not None:
+        h.set_transform(*transform)
     h.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs)     # H2D of the job's inputs
     zr = torch.empty(N, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16)   # caller-owned pinned buffer
     for _ in range(e2e_steps):
@@ -313,11 +337,11 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(tm["launches"]),
         "clocks": clk.summary(),
-        "perplexity_after": round(ppl, 4),
+        "perplexity_after": round(ppl, 4) if ppl is not None else None,
         "stats": stats,
         "timings_ms": {k: round(v, 4) for k, v in tm.items()},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and transform is None:
         st = args.cpu_sample_tokens or min(N, 400_000 if K <= 100 else 100_000)
         line["cpu_baseline"] = cpu_baseline(corpus, cfg, K, args.waves, st)
         line["cpu_baseline"]["cpu"] = cpu_model()
