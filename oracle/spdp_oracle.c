@@ -37,6 +37,9 @@
  *      held-out perplexity or_heldout_perplexity; Hellinger
  *      distance and greedy topic alignment or_hellinger / or_topic_align
  *      (§4.2.6, reading c22).
+ *  - NEXT-3 exchange cadence or_sweep_par_e.
+ *  - NEXT-4 sparse transformation matrices P^i: or_sp_* (P:985-1014,
+ *      P:1455-1468; readings c24-c26).
  */
 #include <math.h>
 #include <stdint.h>
