@@ -103,6 +103,13 @@ def lib():
         L.or_sp_set_q.argtypes = [P, P]
         L.or_sp_conditional.argtypes = [P, C.c_int64, C.c_int, C.c_int32, P]
         L.or_sp_chain_codes.argtypes = [P, C.c_int64, C.c_int, C.c_int, P]
+        L.or_sp_topics.argtypes = [P, P, P]
+        L.or_sp_topics.restype = None
+        L.or_sp_foldin.argtypes = [P, C.c_int64, C.c_int32, P, P, P, C.c_uint64, C.c_int32, C.c_int32, C.c_int, P, P, P, P]
+        L.or_sp_heldout_perplexity.argtypes = [P, C.c_int64, C.c_int32, P, P, P, P, P]
+        L.or_sp_heldout_perplexity.restype = C.c_double
+        L.or_sp_perplexity.argtypes = [P]
+        L.or_sp_perplexity.restype = C.c_double
         _lib = L
     return _lib
 
@@ -350,6 +357,37 @@ class SparseOracle:
         out = np.zeros(self.base.K * (S + 1))
         rc = lib().or_sp_conditional(self.h, int(tok), int(r_rem), int(e_rem), _ptr(out))
         return None if rc != 0 else out
+
+    def topics(self):
+        p0 = np.zeros((self.base.K, self.base.V)); p = np.zeros((self.base.I, self.base.K, self.base.V))
+        lib().or_sp_topics(self.h, _ptr(p0), _ptr(p))
+        return p0, p
+
+    def perplexity(self):
+        return float(lib().or_sp_perplexity(self.h))
+
+    def foldin(self, group, doc, word, num_docs, seed, iterations, first_iteration=0, z=None, force_z=None,
+               want_margin=False):
+        g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
+        w = np.ascontiguousarray(word, np.int32)
+        init = z is None
+        zz = np.full(len(g), -1, np.int32) if init else np.array(z, np.int32, copy=True)
+        fz = None if force_z is None else np.ascontiguousarray(force_z, np.int32)
+        mg = np.zeros(len(g)) if want_margin else None
+        own = np.zeros(len(g), np.int32) if want_margin else None
+        rc = lib().or_sp_foldin(self.h, len(g), int(num_docs), _ptr(g), _ptr(d), _ptr(w), int(seed) & (2**64 - 1),
+                                int(first_iteration), int(iterations), int(init), _ptr(zz), _ptr(fz), _ptr(mg), _ptr(own))
+        if rc != 0:
+            raise RuntimeError(f"or_sp_foldin failed ({rc})")
+        return (zz, mg, own) if want_margin else zz
+
+    def heldout_perplexity(self, group, doc, word, num_docs, z, want_theta=False):
+        g = np.ascontiguousarray(group, np.int32); d = np.ascontiguousarray(doc, np.int32)
+        w = np.ascontiguousarray(word, np.int32); zz = np.ascontiguousarray(z, np.int32)
+        th = np.zeros((int(num_docs), self.base.K)) if want_theta else None
+        ppl = float(lib().or_sp_heldout_perplexity(self.h, len(g), int(num_docs), _ptr(g), _ptr(d), _ptr(w),
+                                                   _ptr(zz), _ptr(th)))
+        return (ppl, th) if want_theta else ppl
 
     def chain_codes(self, nsweeps, waves=-1, qbase=5):
         out = np.zeros(int(nsweeps), np.int64)

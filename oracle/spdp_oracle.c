@@ -841,9 +841,14 @@ double or_phi(const ostate *s, int i, int k, int w) {
  * z_p = floor(x0 K / 2^32) of Philox(seed; p, 0xFFFFFFFF, 1, 0).
  * force_z / margin / own: lock-step testing as in or_sweep_par (own = the
  * oracle's draw before it is replaced by force_z). */
-int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
-              const int32_t *word, uint64_t seed, int32_t first_iter, int32_t iters, int init, int32_t *z,
-              const int32_t *force_z, double *margin, int32_t *own) {
+/* the word likelihood phi~^i_{kw} used by the estimators: or_phi here, the
+ * sparse-P version for NEXT-4 (or_sp_foldin / or_sp_heldout_perplexity) */
+typedef double (*phi_fn)(const void *ctx, int i, int k, int w);
+static double phi_identity(const void *ctx, int i, int k, int w) { return or_phi((const ostate *)ctx, i, k, w); }
+
+static int foldin_impl(const ostate *s, phi_fn phi, const void *pctx, int64_t Nh, int32_t Dh, const int32_t *group,
+                       const int32_t *doc, const int32_t *word, uint64_t seed, int32_t first_iter, int32_t iters,
+                       int init, int32_t *z, const int32_t *force_z, double *margin, int32_t *own) {
     int K = s->K;
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     for (int64_t p = 0; p < Nh; p++) {
@@ -865,7 +870,7 @@ int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, con
             n[(size_t)d * K + z[p]]--;
             double tot = 0.0;
             for (int k = 0; k < K; k++) {
-                w[k] = (s->alpha[(size_t)i * K + k] + (double)n[(size_t)d * K + k]) * or_phi(s, i, k, word[p]);
+                w[k] = (s->alpha[(size_t)i * K + k] + (double)n[(size_t)d * K + k]) * phi(pctx, i, k, word[p]);
                 tot += w[k];
             }
             for (int k = 0; k < K; k++) prob[k] = w[k] / tot;
@@ -883,13 +888,20 @@ int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, con
     free(n); free(w); free(prob);
     return 0;
 }
+int or_foldin(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
+              const int32_t *word, uint64_t seed, int32_t first_iter, int32_t iters, int init, int32_t *z,
+              const int32_t *force_z, double *margin, int32_t *own) {
+    return foldin_impl(s, phi_identity, s, Nh, Dh, group, doc, word, seed, first_iter, iters, init, z, force_z,
+                       margin, own);
+}
 
 /* Held-out perplexity (§3.2.2, reading c17 for the exponent):
  *   exp(- sum_p log sum_k theta~_dk phi~^i_{k w_p} / Nh),
  * theta~_dk = (n_dk + alpha_ik) / sum_k (n_dk + alpha_ik)   Eq. spdp-topic-doc-estimate
  * with n_dk counted from the held-out z.  theta (optional) receives [Dh*K]. */
-double or_heldout_perplexity(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
-                             const int32_t *word, const int32_t *z, double *theta) {
+static double heldout_impl(const ostate *s, phi_fn phi, const void *pctx, int64_t Nh, int32_t Dh,
+                           const int32_t *group, const int32_t *doc, const int32_t *word, const int32_t *z,
+                           double *theta) {
     int K = s->K;
     int32_t *n = (int32_t *)calloc((size_t)Dh * K, sizeof(int32_t));
     int32_t *len = (int32_t *)calloc((size_t)Dh, sizeof(int32_t));
@@ -913,12 +925,16 @@ double or_heldout_perplexity(const ostate *s, int64_t Nh, int32_t Dh, const int3
         double pw = 0.0;
         for (int k = 0; k < K; k++) {
             double th = ((double)n[(size_t)d * K + k] + s->alpha[(size_t)i * K + k]) / ((double)len[d] + asum);
-            pw += th * or_phi(s, i, k, word[p]);
+            pw += th * phi(pctx, i, k, word[p]);
         }
         ll += log(pw);
     }
     free(n); free(len); free(dg);
     return exp(-ll / (double)Nh);
+}
+double or_heldout_perplexity(const ostate *s, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
+                             const int32_t *word, const int32_t *z, double *theta) {
+    return heldout_impl(s, phi_identity, s, Nh, Dh, group, doc, word, z, theta);
 }
 
 /* Hellinger distance between two discrete distributions (§4.2.6
@@ -1324,4 +1340,47 @@ int or_sp_chain_codes(spstate *sp, int64_t nsweeps, int W, int qbase, int64_t *c
         codes[it] = code + mul * qc;
     }
     return 0;
+}
+
+/* NEXT-4 estimators: phi0~_{kv} = (beta + Q_kv)/(V beta + T_k) (P:1753 with the
+ * sparse shadow counts) and phi~^i_{kw} of P:1754 with its printed
+ * sum_v p^i_{w,v} phi0~_{kv} (reading c16 for the mixing weight).  Rows of
+ * phi~^i sum to 1 because the columns of P^i do. */
+double or_sp_phi0(const spstate *sp, int k, int v) {
+    const ostate *s = sp->o;
+    return (s->beta + (double)sp->Qs[(size_t)k * s->V + v]) / ((double)s->V * s->beta + (double)s->T[k]);
+}
+double or_sp_phi(const spstate *sp, int i, int k, int w) {
+    const ostate *s = sp->o;
+    double a = s->a[i], b = s->b[i];
+    double Mk = (double)s->M[(size_t)i * s->K + k], Tk = (double)s->Tt[(size_t)i * s->K + k];
+    size_t c = IDX3(s, i, w, k);
+    double base = 0.0;
+    for (int32_t e = sp->pptr[i * s->V + w]; e < sp->pptr[i * s->V + w + 1]; e++) base += sp->pp[e] * or_sp_phi0(sp, k, sp->pv[e]);
+    return ((double)s->m[c] - a * (double)s->t[c]) / (b + Mk) + (b + a * Tk) / (b + Mk) * base;
+}
+static double phi_sparse(const void *ctx, int i, int k, int w) { return or_sp_phi((const spstate *)ctx, i, k, w); }
+void or_sp_topics(const spstate *sp, double *phi0, double *phi) {
+    const ostate *s = sp->o;
+    for (int k = 0; k < s->K; k++)
+        for (int w = 0; w < s->V; w++) {
+            if (phi0) phi0[(size_t)k * s->V + w] = or_sp_phi0(sp, k, w);
+            if (phi)
+                for (int i = 0; i < s->I; i++) phi[((size_t)i * s->K + k) * s->V + w] = or_sp_phi(sp, i, k, w);
+        }
+}
+int or_sp_foldin(const spstate *sp, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
+                 const int32_t *word, uint64_t seed, int32_t first_iter, int32_t iters, int init, int32_t *z,
+                 const int32_t *force_z, double *margin, int32_t *own) {
+    return foldin_impl(sp->o, phi_sparse, sp, Nh, Dh, group, doc, word, seed, first_iter, iters, init, z, force_z,
+                       margin, own);
+}
+double or_sp_heldout_perplexity(const spstate *sp, int64_t Nh, int32_t Dh, const int32_t *group, const int32_t *doc,
+                                const int32_t *word, const int32_t *z, double *theta) {
+    return heldout_impl(sp->o, phi_sparse, sp, Nh, Dh, group, doc, word, z, theta);
+}
+/* training perplexity (P:1978-2007 on the training tokens, theta~ from n_d) */
+double or_sp_perplexity(const spstate *sp) {
+    const ostate *s = sp->o;
+    return heldout_impl(s, phi_sparse, sp, s->N, s->D, s->group, s->doc, s->word, s->z, NULL);
 }

@@ -187,3 +187,31 @@ def test_wave_mode_keeps_a_valid_state_with_P(waves):
         assert (t <= m).all() and ((t > 0) == (m > 0)).all()
         assert np.array_equal(Qs, st["Qs"])
         assert m.sum() == c.num_tokens
+
+
+def test_sparse_estimators_normalised_and_identity_reduction():
+    """With P^i = I the estimators are those of P:1753-1754 (pinned in
+    test_oracle_heldout.py); with a sparse doubly-stochastic P^i the rows of
+    phi~^i still sum to 1 (because the columns of P^i do), and the training
+    perplexity equals the held-out perplexity of the training documents."""
+    c = synth.generate(2, 8, 12.0, 30, 3, seed=3)
+    a = oracle.from_corpus(c, 4)
+    b = oracle.from_corpus(c, 4)
+    sp = oracle.SparseOracle(b, *identity_P(2, 30))
+    for _ in range(2):
+        a.sweep_par(waves=1); sp.sweep_par(waves=1)
+    p0a, pa = a.topics(); p0b, pb = sp.topics()
+    assert np.array_equal(p0a, p0b) and np.array_equal(pa, pb)
+    assert sp.perplexity() == a.perplexity()
+    o = oracle.from_corpus(c, 4)
+    P = mixing_P(2, 30, np.random.default_rng(5))
+    s2 = oracle.SparseOracle(o, *P)
+    for _ in range(3):
+        s2.sweep_par(waves=2)
+    p0, ph = s2.topics()
+    assert np.allclose(p0.sum(axis=1), 1.0, atol=1e-12) and np.allclose(ph.sum(axis=2), 1.0, atol=1e-12)
+    z = s2.state()["z"]
+    assert s2.heldout_perplexity(c.group, c.doc, c.word, c.num_docs, z) == pytest.approx(s2.perplexity(), rel=1e-12)
+    te = synth.generate(2, 3, 9.0, 30, 3, seed=6)
+    zf = s2.foldin(te.group, te.doc, te.word, te.num_docs, seed=2, iterations=3)
+    assert np.isfinite(s2.heldout_perplexity(te.group, te.doc, te.word, te.num_docs, zf))
