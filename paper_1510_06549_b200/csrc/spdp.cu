@@ -151,6 +151,7 @@ struct spdp_ctx {
     uint32_t* d_sptr = nullptr;
     int32_t *d_spv = nullptr, *d_best = nullptr, *d_q = nullptr, *d_dq = nullptr;
     float* d_spp = nullptr;
+    double* d_spp64 = nullptr;                     // fp64 weights for the estimators
     int16_t* d_src = nullptr;
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
@@ -638,6 +639,12 @@ spdp_status sparse_upload(spdp_ctx* c) {
             best[sg] = (int32_t)(c->h_sptr[sg] + (uint32_t)(b - c->h_pptr[(size_t)r]));
         }
     ALLOC(c->d_sptr, (size_t)segs + 1); ALLOC(c->d_spv, c->E_sp); ALLOC(c->d_spp, c->E_sp); ALLOC(c->d_best, segs);
+    ALLOC(c->d_spp64, c->E_sp);
+    {
+        std::vector<double> pp64(c->E_sp);
+        for (size_t e = 0; e < c->dev_of_user.size(); ++e) pp64[c->dev_of_user[e]] = c->h_pp[e];
+        CU(cudaMemcpy(c->d_spp64, pp64.data(), sizeof(double) * pp64.size(), cudaMemcpyHostToDevice));
+    }
     ALLOC(c->d_q, (size_t)c->E_sp * Kp); ALLOC(c->d_dq, (size_t)c->E_sp * Kp);
     ALLOC(c->d_src, (size_t)std::max<int64_t>(c->Nloc, 1));
     CU(cudaMemcpy(c->d_sptr, c->h_sptr.data(), sizeof(uint32_t) * c->h_sptr.size(), cudaMemcpyHostToDevice));
@@ -1742,7 +1749,17 @@ spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
 spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
+    if (c->sparse) {
+        // NEXT-4: training perplexity = the held-out computation on the training tokens with their own z
+        // (theta~ from n_d, phi~ with the sources); log p(W, Z, T, Q) is not provided in this version
+        if (log_joint) return fail(c, SPDP_ESTATE, "log_joint is not available with a transformation matrix in this version");
+        if (!perplexity) return SPDP_OK;
+        if ((s = ensure_host_plan(c))) return s;
+        std::vector<int32_t> z((size_t)c->N);
+        if ((s = spdp_counts(c, z.data(), nullptr, nullptr, nullptr, nullptr, nullptr))) return s;
+        return spdp_heldout(c, c->N, c->D, c->group.data(), c->doc.data(), c->word.data(), 0, 0, 0, z.data(), nullptr,
+                            nullptr, perplexity);
+    }
     const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
     if (perplexity) {
         SweepArgs a = base_args(c);
@@ -1822,7 +1839,8 @@ spdp_status launch_phi_table(spdp_ctx* c, double* phi, double* phi0) {
     phi_table_kernel<<<std::max(grid, 1), 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T,
                                                               c->d_disc64, c->d_conc64, c->cfg.beta,
                                                               (double)c->V * c->cfg.beta, c->V, c->I, c->K, c->Kp,
-                                                              phi, phi0);
+                                                              phi, phi0, c->sparse ? c->d_sptr : nullptr,
+                                                              c->d_spv, c->d_spp64);
     c->launches += 1;
     return check_launch(c, "phi_table_kernel");
 }
@@ -1831,7 +1849,6 @@ spdp_status launch_phi_table(spdp_ctx* c, double* phi, double* phi0) {
 spdp_status spdp_topics(spdp_ctx* c, double* phi0, double* phi) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     TempBuf<double> dphi(c->cells), dphi0((size_t)K * V);
     if (!dphi.p || !dphi0.p) return fail(c, SPDP_ENOMEM, "spdp_topics buffers");
@@ -1858,7 +1875,6 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
                          const int32_t* z_init, int32_t* z_out, double* theta, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    if (c->sparse) return fail(c, SPDP_ESTATE, "not available with a transformation matrix in this version");
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     if (num_tokens < 0 || num_tokens > (int64_t)UINT32_MAX || num_docs < 1 || iterations < 0 || first_iteration < 0 ||
         (num_tokens > 0 && (!group || !doc || !word)))

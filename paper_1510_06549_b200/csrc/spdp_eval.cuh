@@ -26,7 +26,8 @@ __global__ void phi_table_kernel(const int32_t* __restrict__ m, const int32_t* _
                                  const int32_t* __restrict__ Tt, const int32_t* __restrict__ T,
                                  const double* __restrict__ disc, const double* __restrict__ conc, double beta,
                                  double vbeta, int V, int I, int K, int Kp, double* __restrict__ phi,
-                                 double* __restrict__ phi0) {
+                                 double* __restrict__ phi0, const uint32_t* __restrict__ sptr = nullptr,
+                                 const int32_t* __restrict__ spv = nullptr, const double* __restrict__ spp = nullptr) {
     const size_t cells = (size_t)V * I * Kp;
     for (size_t c = blockIdx.x * (size_t)blockDim.x + threadIdx.x; c < cells; c += (size_t)gridDim.x * blockDim.x) {
         const int k = (int)(c % Kp);
@@ -35,9 +36,16 @@ __global__ void phi_table_kernel(const int32_t* __restrict__ m, const int32_t* _
         double v = 0.0;
         if (k < K) {
             const double p0 = (beta + (double)Q[(size_t)w * Kp + k]) / (vbeta + (double)T[k]);
+            double base = p0;
+            if (sptr) {                               // NEXT-4: sum_v p^i_{w,v} phi0~_{kv}
+                base = 0.0;
+                const uint32_t seg = (uint32_t)wi;
+                for (uint32_t e = sptr[seg]; e < sptr[seg + 1]; ++e)
+                    base += spp[e] * ((beta + (double)Q[(size_t)spv[e] * Kp + k]) / (vbeta + (double)T[k]));
+            }
             const double a = disc[i], b = conc[i];
             const double Mk = M[(size_t)i * Kp + k], Tk = Tt[(size_t)i * Kp + k];
-            v = ((double)m[c] - a * (double)t[c]) / (b + Mk) + (b + a * Tk) / (b + Mk) * p0;
+            v = ((double)m[c] - a * (double)t[c]) / (b + Mk) + (b + a * Tk) / (b + Mk) * base;
             if (phi0 && i == 0) phi0[(size_t)k * V + w] = p0;
         }
         if (phi) phi[c] = v;

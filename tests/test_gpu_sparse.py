@@ -74,4 +74,30 @@ def test_sparse_transform_validation():
         g.set_transform(pptr, pv, pp)
     assert e.value.code == spdp.SPDP_ESTATE
     with pytest.raises(spdp.SPDPError):
-        g.perplexity()
+        g.log_joint()
+
+
+@pytest.mark.parametrize("K", [10, 37])
+def test_sparse_estimators_match_oracle(K):
+    """phi~ with sum_v p phi0~, training perplexity and held-out fold-in
+    with a sparse P, GPU vs the oracle on the same state."""
+    import synth
+    train, test = synth.holdout_split(corpus("C1"), 0.1, seed=1)
+    P = mixing_P(train.num_groups, train.vocab, np.random.default_rng(4))
+    g, o, sp = _pair(train, K, P, 1)
+    for s in range(2):
+        gc, gs, mism, mg = _lockstep(g, sp, P, 1)
+        assert len(mism) == 0
+    p0g, pg = g.topics()
+    p0o, po = sp.topics()
+    np.testing.assert_allclose(p0g, p0o, rtol=1e-12)
+    np.testing.assert_allclose(pg, po, rtol=1e-11)
+    assert np.allclose(pg.sum(axis=2), 1.0, atol=1e-12)
+    assert g.perplexity() == pytest.approx(sp.perplexity(), rel=1e-10)
+    r = g.heldout(test, 3, 0)
+    z = r["z"]
+    zf, margin, own = sp.foldin(test.group, test.doc, test.word, test.num_docs, seed=3, iterations=1, z=z,
+                                force_z=g.heldout(test, 3, 1, z_init=z)["z"], want_margin=True)
+    res = g.heldout(test, 3, 0, z_init=zf)
+    assert res["perplexity"] == pytest.approx(sp.heldout_perplexity(test.group, test.doc, test.word, test.num_docs, zf),
+                                              rel=1e-10)
