@@ -254,8 +254,10 @@ spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t
  * in [0, V) and weight pp[e] > 0; every row needs >= 1 entry (<= 32767) and
  * every column of every P^i must sum to 1 (±1e-9; P^i phi0 is a distribution,
  * P:990-993).  Host arrays, copied.  Call after spdp_create and before
- * spdp_load_corpus.  This version: world_size == 1, SPDP_UPDATE_WAVE; the
- * likelihood / held-out / diagnostics calls return SPDP_ESTATE.  Readings:
+ * spdp_load_corpus.  The estimators (spdp_topics, spdp_heldout, the
+ * perplexity of spdp_loglik) then use phi~^i with sum_v p_{i,w,v} phi0~_{k,v}
+ * (P:1754).  This version: world_size == 1, SPDP_UPDATE_WAVE; log_joint and
+ * spdp_debug_probs return SPDP_ESTATE.  Readings:
  * DESIGN.md §13 (c24 wave correction of the sources, c25 initial sources,
  * c26 the removed table's source).  Errors: SPDP_EINVAL, SPDP_ESTATE.
  *
