@@ -691,8 +691,9 @@ void sparse_wave(spdp_ctx* c, int w) {
     t.key0 = (uint32_t)c->cfg.seed; t.key1 = (uint32_t)(c->cfg.seed >> 32);
     t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats; t.P = P;
     const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
-    if (c->row16) sp_token_kernel<uint16_t><<<std::max(grid, 1), 256, 0, c->stream>>>(t);
-    else sp_token_kernel<float><<<std::max(grid, 1), 256, 0, c->stream>>>(t);
+    const size_t ssm = ((Kp / 4) <= kSpSmemBlocks) ? sizeof(float) * 256 * (size_t)(Kp / 4) : 0;
+    if (c->row16) sp_token_kernel<uint16_t><<<std::max(grid, 1), 256, ssm, c->stream>>>(t);
+    else sp_token_kernel<float><<<std::max(grid, 1), 256, ssm, c->stream>>>(t);
     if (c->W == 1) {
         const size_t smem = sizeof(int) * 8 * (size_t)Kp;
         if (c->row16)

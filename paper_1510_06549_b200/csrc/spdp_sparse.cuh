@@ -120,8 +120,11 @@ __device__ __forceinline__ float sp_block_sum(const NT* nrow, const float* Frow,
            (__fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)) + __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w)));
 }
 
+constexpr int kSpSmemBlocks = 32;   // block sums of up to 32 4-topic blocks per thread in shared memory
+
 template <typename NT>
 __global__ void __launch_bounds__(256) sp_token_kernel(SpTokenArgs A) {
+    extern __shared__ float s_bs[];   // [kSpSmemBlocks][blockDim.x] (only when K <= 128)
     const int I = A.I, K = A.K, Kp = A.Kp;
     const int nbk = (K + 3) >> 2;
     const uint32_t sweep = *A.sweep;
@@ -175,12 +178,14 @@ __global__ void __launch_bounds__(256) sp_token_kernel(SpTokenArgs A) {
             const float wold = __fmaf_rn(n0, F0k, __fmul_rn(al0, F0k));
             const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
             const float dlt = wnew - wold;
-            // pass 1: total, last positive block
+            // pass 1: total, last positive block (block sums kept in shared memory for K <= 128)
+            const bool keep_bs = nbk <= kSpSmemBlocks;
             double total = 0.0, lastbeg = 0.0;
             int qlast = 0;
             for (int B = 0; B < nbk; ++B) {
                 float bs = sp_block_sum<NT>(nrow, Frow, al, A.bpos[B], B);
                 if ((k0 >> 2) == B) bs += dlt;
+                if (keep_bs) s_bs[B * blockDim.x + threadIdx.x] = bs;
                 if (bs > 0.f) { qlast = B; lastbeg = total; }
                 total += (double)bs;
             }
@@ -189,8 +194,12 @@ __global__ void __launch_bounds__(256) sp_token_kernel(SpTokenArgs A) {
             double run2 = 0.0, bbeg = 0.0;
             int qs = -1;
             for (int B = 0; B < nbk; ++B) {
-                float bs = sp_block_sum<NT>(nrow, Frow, al, A.bpos[B], B);
-                if ((k0 >> 2) == B) bs += dlt;
+                float bs;
+                if (keep_bs) bs = s_bs[B * blockDim.x + threadIdx.x];
+                else {
+                    bs = sp_block_sum<NT>(nrow, Frow, al, A.bpos[B], B);
+                    if ((k0 >> 2) == B) bs += dlt;
+                }
                 const double nxt = run2 + (double)bs;
                 if (nxt > target) { qs = B; bbeg = run2; break; }
                 run2 = nxt;
