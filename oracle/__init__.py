@@ -109,6 +109,7 @@ def lib():
         L.or_sp_heldout_perplexity.argtypes = [P, C.c_int64, C.c_int32, P, P, P, P, P]
         L.or_sp_heldout_perplexity.restype = C.c_double
         L.or_sp_perplexity.argtypes = [P]
+        L.or_sp_sweep_shards.argtypes = [P, C.c_int, C.c_int]
         L.or_sp_perplexity.restype = C.c_double
         _lib = L
     return _lib
@@ -338,6 +339,11 @@ class SparseOracle:
         if lib().or_sp_sweep_par(self.h, int(waves), _ptr(f), _ptr(mg), _ptr(own)) != 0:
             raise RuntimeError("or_sp_sweep_par failed")
         return mg, own
+
+    def sweep_shards(self, waves=1, shards=1):
+        """Mode P over several shards with one exchange per sweep (NEXT-4 on several GPUs)."""
+        if lib().or_sp_sweep_shards(self.h, int(waves), int(shards)) != 0:
+            raise RuntimeError("or_sp_sweep_shards failed")
 
     def state(self):
         st = self.base.state()

@@ -1203,14 +1203,24 @@ int or_sp_sweep_seq(spstate *sp) {
  * wave's deltas and the q correction (reading c24).  force (optional, [N]):
  * lock-step replay of another sampler's draws, as slot index
  * (k (S+1) + within); own/margin as in or_sweep_par. */
+static int sp_waves(spstate *sp, int W, const int32_t *shard, int g, const int32_t *force, double *margin,
+                    int32_t *own);
 int or_sp_sweep_par(spstate *sp, int W, const int32_t *force, double *margin, int32_t *own) {
+    int rc = sp_waves(sp, W, NULL, 0, force, margin, own);
+    if (rc == 0) sp->o->sweep++;
+    return rc;
+}
+
+/* the waves of one shard (shard == NULL: every token) against the current arrays of sp */
+static int sp_waves(spstate *sp, int W, const int32_t *shard, int g, const int32_t *force, double *margin,
+                    int32_t *own) {
     ostate *s = sp->o;
     int I = s->I, V = s->V, K = s->K;
     int64_t N = s->N;
     size_t cells = (size_t)I * V * K;
     int32_t Smax = sp_max_row(sp);
     if (W < 1) return -1;
-    memset(s->stats, 0, sizeof(s->stats));
+    if (!shard) memset(s->stats, 0, sizeof(s->stats));
     int32_t *m0 = (int32_t *)malloc(sizeof(int32_t) * cells), *t0 = (int32_t *)malloc(sizeof(int32_t) * cells);
     int64_t *M0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K), *Tt0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K);
     int64_t *Q0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)K * V), *T0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
@@ -1231,6 +1241,7 @@ int or_sp_sweep_par(spstate *sp, int W, const int32_t *force, double *margin, in
         /* (1) every token of the wave decides against the wave-start snapshot */
         for (int64_t p = 0; p < N; p++) {
             if (s->pos[p] % W != wave) continue;
+            if (shard && shard[s->doc[p]] != g) continue;
             int i = s->group[p], w = s->word[p], k0 = s->z[p];
             int32_t e0 = sp->pptr[i * V + w], S = sp->pptr[i * V + w + 1] - e0;
             size_t c = IDX3(s, i, w, k0);
@@ -1252,6 +1263,7 @@ int or_sp_sweep_par(spstate *sp, int W, const int32_t *force, double *margin, in
         /* (2) apply the wave's deltas, correct q (reading c24), recompute t and the sums */
         for (int64_t p = 0; p < N; p++) {
             if (s->pos[p] % W != wave) continue;
+            if (shard && shard[s->doc[p]] != g) continue;
             if (kept[p]) { s->r[p] = 1; s->stats[0]++; continue; }
             int i = s->group[p], w = s->word[p], d = s->doc[p], k0 = s->z[p];
             int32_t e0 = sp->pptr[i * V + w], S = sp->pptr[i * V + w + 1] - e0;
@@ -1294,7 +1306,6 @@ int or_sp_sweep_par(spstate *sp, int W, const int32_t *force, double *margin, in
                 }
         sp_recompute(sp);
     }
-    s->sweep++;
     rc = 0;
 out:
     free(m0); free(t0); free(M0); free(Tt0); free(Q0); free(T0); free(dq); free(dm); free(slot); free(erem); free(rr);
@@ -1383,4 +1394,76 @@ double or_sp_heldout_perplexity(const spstate *sp, int64_t Nh, int32_t Dh, const
 double or_sp_perplexity(const spstate *sp) {
     const ostate *s = sp->o;
     return heldout_impl(s, phi_sparse, sp, s->N, s->D, s->group, s->doc, s->word, s->z, NULL);
+}
+
+/* Mode P over G shards (NEXT-4 on several GPUs): every shard samples its
+ * documents' waves from the sweep-start state (its own replica of m, q and the
+ * derived counts), then S1 = S0 + sum_g (L_g - S0) on m and q, corrected by
+ * reading c24 on every cell, t, Q and the sums recomputed (Alg.3
+ * with the sources). */
+int or_sp_sweep_shards(spstate *sp, int W, int G) {
+    ostate *s = sp->o;
+    int I = s->I, V = s->V, K = s->K;
+    size_t cells = (size_t)I * V * K, qn = (size_t)sp->E * K;
+    if (G < 1 || W < 1) return -1;
+    int32_t *shard = (int32_t *)malloc(sizeof(int32_t) * (size_t)s->D);
+    int32_t *m0 = (int32_t *)malloc(sizeof(int32_t) * cells), *q0 = (int32_t *)malloc(sizeof(int32_t) * qn);
+    int64_t *Dm = (int64_t *)calloc(cells, sizeof(int64_t)), *Dq = (int64_t *)calloc(qn, sizeof(int64_t));
+    int32_t *Lm = (int32_t *)malloc(sizeof(int32_t) * cells), *Lt = (int32_t *)malloc(sizeof(int32_t) * cells);
+    int32_t *Lq = (int32_t *)malloc(sizeof(int32_t) * qn);
+    int64_t *LM = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K), *LTt = (int64_t *)malloc(sizeof(int64_t) * (size_t)I * K);
+    int64_t *LQ = (int64_t *)malloc(sizeof(int64_t) * (size_t)K * V), *LT = (int64_t *)malloc(sizeof(int64_t) * (size_t)K);
+    int rc = -2;
+    if (!shard || !m0 || !q0 || !Dm || !Dq || !Lm || !Lt || !Lq || !LM || !LTt || !LQ || !LT) goto out;
+    or_partition(s, G, shard);
+    memcpy(m0, s->m, sizeof(int32_t) * cells);
+    memcpy(q0, sp->q, sizeof(int32_t) * qn);
+    memset(s->stats, 0, sizeof(s->stats));
+    for (int g = 0; g < G; g++) {
+        int32_t *gm = s->m, *gt = s->t, *gq = sp->q;
+        int64_t *gM = s->M, *gTt = s->Tt, *gQ = sp->Qs, *gT = s->T;
+        memcpy(Lm, m0, sizeof(int32_t) * cells);
+        memcpy(Lq, q0, sizeof(int32_t) * qn);
+        s->m = Lm; s->t = Lt; sp->q = Lq; s->M = LM; s->Tt = LTt; sp->Qs = LQ; s->T = LT;
+        sp_recompute(sp);                                  /* the shard's replica of the sweep-start state */
+        int r = sp_waves(sp, W, shard, g, NULL, NULL, NULL);
+        for (size_t c = 0; c < cells; c++) Dm[c] += Lm[c] - m0[c];
+        for (size_t j = 0; j < qn; j++) Dq[j] += Lq[j] - q0[j];
+        s->m = gm; s->t = gt; sp->q = gq; s->M = gM; s->Tt = gTt; sp->Qs = gQ; s->T = gT;
+        if (r) { rc = r; goto out; }
+    }
+    /* merge + correction (reading c24) on every cell */
+    for (size_t c = 0; c < cells; c++) s->m[c] = (int32_t)(m0[c] + Dm[c]);
+    for (size_t j = 0; j < qn; j++) sp->q[j] = (int32_t)(q0[j] + Dq[j]);
+    for (int i = 0; i < I; i++)
+        for (int w = 0; w < V; w++)
+            for (int k = 0; k < K; k++) {
+                size_t c = IDX3(s, i, w, k);
+                int32_t eb = sp->pptr[i * V + w], ee = sp->pptr[i * V + w + 1];
+                int changed = 0;
+                int32_t t = 0;
+                for (int32_t e = eb; e < ee; e++) {
+                    int32_t *qe = &sp->q[(size_t)e * K + k];
+                    if (*qe < 0) { *qe = 0; changed = 1; }
+                    t += *qe;
+                }
+                if (s->m[c] == 0) {
+                    for (int32_t e = eb; e < ee; e++) if (sp->q[(size_t)e * K + k]) { sp->q[(size_t)e * K + k] = 0; changed = 1; }
+                } else if (t == 0) {
+                    sp->q[(size_t)sp->best[i * V + w] * K + k] = 1; changed = 1;
+                } else {
+                    while (t > s->m[c]) {
+                        int32_t eb2 = eb;
+                        for (int32_t e = eb; e < ee; e++) if (sp->q[(size_t)e * K + k] > sp->q[(size_t)eb2 * K + k]) eb2 = e;
+                        sp->q[(size_t)eb2 * K + k]--; t--; changed = 1;
+                    }
+                }
+                s->stats[2] += changed;
+            }
+    sp_recompute(sp);
+    s->sweep++;
+    rc = 0;
+out:
+    free(shard); free(m0); free(q0); free(Dm); free(Dq); free(Lm); free(Lt); free(Lq); free(LM); free(LTt); free(LQ); free(LT);
+    return rc;
 }

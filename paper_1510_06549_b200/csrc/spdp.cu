@@ -125,7 +125,8 @@ struct spdp_ctx {
     cudaEvent_t comm_done = nullptr;
     int32_t *d_Mn = nullptr, *d_Ttn = nullptr, *d_Tn = nullptr;    // deferred local sums (sampling reads the snapshot)
     int32_t *d_Mf = nullptr, *d_Ttf = nullptr, *d_Tf = nullptr;    // sums after the pipelined exchange
-    size_t dbytes() const { return cells * (pack32 ? 4 : 8); }
+    size_t xcount() const { return sparse ? cells + (size_t)E_sp * Kp : cells; }   // exchange buffer elements
+    size_t dbytes() const { return xcount() * (pack32 ? 4 : 8); }
 
     // device
     uint32_t *d_tok_doc = nullptr, *d_tok_id = nullptr, *d_chunk_start = nullptr, *d_chunk_end = nullptr,
@@ -399,7 +400,9 @@ void launch_exchange_merge_range(spdp_ctx* c, int w0, int w1, int32_t* M, int32_
             c->d_m, c->d_t, (long long*)c->d_Dloc, (const long long*)c->d_Dsum, c->d_Q, M, Tt, T, w0, w1, c->I, c->Kp,
             use_smem, c->d_stats);
 }
+void sparse_exchange_merge(spdp_ctx* c);
 void launch_exchange_merge(spdp_ctx* c) {
+    if (c->sparse) { sparse_exchange_merge(c); return; }
     cudaMemsetAsync(c->d_M, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
     cudaMemsetAsync(c->d_Tt, 0, sizeof(int32_t) * (size_t)c->I * c->Kp, c->stream);
     cudaMemsetAsync(c->d_T, 0, sizeof(int32_t) * (size_t)c->Kp, c->stream);
@@ -653,6 +656,13 @@ spdp_status sparse_upload(spdp_ctx* c) {
     CU(cudaMemcpy(c->d_best, best.data(), sizeof(int32_t) * best.size(), cudaMemcpyHostToDevice));
     CU(cudaMemset(c->d_dq, 0, sizeof(int32_t) * (size_t)c->E_sp * Kp));
     CU(cudaMemset(c->d_src, 0xFF, sizeof(int16_t) * (size_t)std::max<int64_t>(c->Nloc, 1)));
+    if (c->G > 1) {            // net changes of m (cells) then of q (E x Kp), int32, summed over ranks
+        c->pack32 = true;
+        int32_t *dl = nullptr, *ds = nullptr;
+        ALLOC(dl, c->xcount()); ALLOC(ds, c->xcount());
+        c->d_Dloc = dl; c->d_Dsum = ds;
+        CU(cudaMemset(c->d_Dloc, 0, c->dbytes()));
+    }
     return SPDP_OK;
 }
 
@@ -665,6 +675,18 @@ void sparse_install(spdp_ctx* c) {
     sp_init_q_kernel<<<148 * 8, 256, 0, c->stream>>>(P, c->d_t, segs, Kp);
     cudaMemsetAsync(c->d_Q, 0, sizeof(int32_t) * (size_t)c->V * Kp, c->stream);
     sp_shadow_kernel<<<148 * 8, 256, 0, c->stream>>>(P, c->E_sp, c->K, Kp, c->d_Q);
+}
+
+// after the all-reduce: m, q = local - Dloc + Dsum, correction (reading c24), t; then the sums and Q from scratch
+void sparse_exchange_merge(spdp_ctx* c) {
+    SparseP P = sparse_args(c);
+    const uint32_t segs = (uint32_t)c->V * c->I;
+    sp_exchange_merge_kernel<<<148 * 4, 256, 0, c->stream>>>(P, segs, c->d_m, c->d_t, (int32_t*)c->d_Dloc,
+                                                            (const int32_t*)c->d_Dsum, c->cells, c->K, c->Kp, c->d_stats);
+    launch_merge(c, nullptr, nullptr);                       // M, Tt, T from the rows (Q there assumes identity P)
+    cudaMemsetAsync(c->d_Q, 0, sizeof(int32_t) * (size_t)c->V * c->Kp, c->stream);
+    sp_shadow_kernel<<<148 * 8, 256, 0, c->stream>>>(P, c->E_sp, c->K, c->Kp, c->d_Q);
+    c->launches += 3;
 }
 
 // one wave of the sparse sweep: factors of the wave's segments, tokens, n, merge
@@ -713,9 +735,11 @@ void sparse_wave(spdp_ctx* c, int w) {
                 c->d_tok_doc, c->d_zr, c->d_zr_next, (float*)c->d_n, c->d_sigma, Kp, tb, te);
     }
     const int blocks = (int)std::min<uint32_t>((r1 - r0 + 7) / 8, 148u * 4u);
+    int32_t* Dm = c->G > 1 ? (int32_t*)c->d_Dloc : nullptr;
+    int32_t* Dq = c->G > 1 ? (int32_t*)c->d_Dloc + c->cells : nullptr;
     sp_merge_kernel<<<std::max(blocks, 1), 256, 0, c->stream>>>(P, c->d_wave_segs + r0, (int)(r1 - r0), c->d_m, c->d_t,
                                                                 c->d_dm, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->I, c->K, Kp,
-                                                                c->d_stats);
+                                                                c->d_stats, Dm, Dq);
     c->launches += 4;
 }
 
@@ -1062,8 +1086,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     spdp_status s = guard(c, false);
     if (s) return s;
     if (c->loaded) return fail(c, SPDP_ESTATE, "spdp_load_corpus may be called once per context");
-    if (c->sparse && (c->G > 1 || c->async))
-        return fail(c, SPDP_EINVAL, "a transformation matrix needs world_size == 1 and SPDP_UPDATE_WAVE in this version");
+    if (c->sparse && c->async)
+        return fail(c, SPDP_EINVAL, "a transformation matrix needs SPDP_UPDATE_WAVE in this version");
     if (num_tokens < 1 || num_docs < 1 || !group || !doc || !word)
         return fail(c, SPDP_EINVAL, "need num_tokens >= 1, num_docs >= 1 and the three token arrays");
     if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
@@ -1390,7 +1414,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     ALLOC(c->d_work, (size_t)std::max(W, c->P) + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
     ALLOC(c->d_dm, c->cells); ALLOC(c->d_dt, c->cells);
-    if (c->G > 1) {
+    if (c->G > 1 && !c->sparse) {
         // |sum over ranks of dt| <= count(i,w) <= M_max, so 16-bit halves suffice below 2^15
         c->pack32 = c->mmax < 32768 && !getenv("SPDP_EXCHANGE_PACK64");
         const size_t words = c->cells * (c->pack32 ? 1 : 2);
@@ -1519,7 +1543,7 @@ spdp_status spdp_exchange_buffer(spdp_ctx* c, void** ptr, int64_t* count, int32_
     if (!ptr || !count || !elem_bytes) return fail(c, SPDP_EINVAL, "null output");
     if (c->G == 1) return fail(c, SPDP_ESTATE, "world_size == 1 has no exchange buffer");
     *ptr = c->d_Dsum;
-    *count = (int64_t)c->cells;
+    *count = (int64_t)c->xcount();
     *elem_bytes = c->pack32 ? 4 : 8;
     return SPDP_OK;
 }
@@ -1561,7 +1585,7 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
         if ((s = run_waves(c, block_w0(c, b), block_w1(c, b), b == 0))) return s;
         if (c->G > 1 && !c->overlap) {
             rec(c, 4 * (size_t)c->W);
-            if ((s = nccl_check(c, c->nccl.AllReduce(c->d_Dloc, c->d_Dsum, c->cells, c->pack32 ? kNcclInt32 : kNcclInt64,
+            if ((s = nccl_check(c, c->nccl.AllReduce(c->d_Dloc, c->d_Dsum, c->xcount(), c->pack32 ? kNcclInt32 : kNcclInt64,
                                                      kNcclSum, c->comm, c->stream),
                                 "ncclAllReduce(packed deltas)")))
                 return s;

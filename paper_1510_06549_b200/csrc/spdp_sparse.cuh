@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(256) sp_token_kernel(SpTokenArgs A) {
 __global__ void sp_merge_kernel(SparseP P, const uint32_t* __restrict__ segs, int nseg, int32_t* __restrict__ m,
                                 int32_t* __restrict__ t, int32_t* __restrict__ dm, int32_t* __restrict__ Q,
                                 int32_t* __restrict__ M, int32_t* __restrict__ Tt, int32_t* __restrict__ T, int I, int K,
-                                int Kp, unsigned long long* __restrict__ stats) {
+                                int Kp, unsigned long long* __restrict__ stats, int32_t* __restrict__ Dm = nullptr,
+                                int32_t* __restrict__ Dq = nullptr) {
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     unsigned clamped = 0;
     for (int j = blockIdx.x * wpb + (threadIdx.x >> 5); j < nseg; j += gridDim.x * wpb) {
@@ -319,10 +320,14 @@ __global__ void sp_merge_kernel(SparseP P, const uint32_t* __restrict__ segs, in
                 const size_t qe = (size_t)e * Kp + k;
                 const int d = P.q[qe] - P.dq[qe];
                 P.dq[qe] = 0;
-                if (d) atomicAdd(Q + (size_t)P.pv[e] * Kp + k, d);
+                if (d) {
+                    atomicAdd(Q + (size_t)P.pv[e] * Kp + k, d);
+                    if (Dq) Dq[qe] += d;                                 // net change since the sweep start (ranks)
+                }
             }
             clamped += changed;
             t[c] = tv;
+            if (Dm && mv != mold) Dm[c] += mv - mold;
             if (mv != mold) atomicAdd(M + (size_t)i * Kp + k, mv - mold);
             if (tv != told) { atomicAdd(Tt + (size_t)i * Kp + k, tv - told); atomicAdd(T + k, tv - told); }
         }
@@ -353,4 +358,56 @@ __global__ void sp_init_q_kernel(SparseP P, const int32_t* __restrict__ t, uint3
     }
 }
 
+}  // namespace spdp
+
+namespace spdp {
+// multi-rank merge with sources: m, q = local - Dloc + Dsum (Dloc: this rank's net change of m (cells) then
+// of q (E x Kp); Dsum: the sum over ranks), correction c24, t = sum q; Dloc zeroed.  Sums and Q afterwards.
+__global__ void sp_exchange_merge_kernel(SparseP P, uint32_t segs, int32_t* __restrict__ m, int32_t* __restrict__ t,
+                                         int32_t* __restrict__ Dloc, const int32_t* __restrict__ Dsum, size_t cells,
+                                         int K, int Kp, unsigned long long* __restrict__ stats) {
+    const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+    int32_t* dlq = Dloc + cells;
+    const int32_t* dsq = Dsum + cells;
+    unsigned clamped = 0;
+    for (uint32_t seg = blockIdx.x * wpb + (threadIdx.x >> 5); seg < segs; seg += gridDim.x * wpb) {
+        const uint32_t e0 = P.sptr[seg], e1 = P.sptr[seg + 1];
+        const int eb = P.best[seg];
+        for (int k = lane; k < K; k += 32) {
+            const size_t c = (size_t)seg * Kp + k;
+            bool any = Dloc[c] != 0 || Dsum[c] != 0;
+            for (uint32_t e = e0; e < e1; ++e) any |= dlq[(size_t)e * Kp + k] != 0 || dsq[(size_t)e * Kp + k] != 0;
+            if (!any) continue;
+            const int mv = m[c] - Dloc[c] + Dsum[c];
+            Dloc[c] = 0;
+            m[c] = mv;
+            int tv = 0, changed = 0;
+            for (uint32_t e = e0; e < e1; ++e) {
+                const size_t qe = (size_t)e * Kp + k;
+                int x = P.q[qe] - dlq[qe] + dsq[qe];
+                dlq[qe] = 0;
+                if (x < 0) { x = 0; changed = 1; }
+                P.q[qe] = x;
+                tv += x;
+            }
+            if (mv == 0) {
+                for (uint32_t e = e0; e < e1; ++e) { const size_t qe = (size_t)e * Kp + k; if (P.q[qe]) { P.q[qe] = 0; changed = 1; } }
+                tv = 0;
+            } else if (tv == 0) {
+                P.q[(size_t)eb * Kp + k] = 1; tv = 1; changed = 1;
+            } else {
+                while (tv > mv) {
+                    uint32_t eb2 = e0;
+                    for (uint32_t e = e0; e < e1; ++e) if (P.q[(size_t)e * Kp + k] > P.q[(size_t)eb2 * Kp + k]) eb2 = e;
+                    P.q[(size_t)eb2 * Kp + k] -= 1; --tv; changed = 1;
+                }
+            }
+            clamped += changed;
+            t[c] = tv;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) clamped += __shfl_xor_sync(0xffffffffu, clamped, off);
+    if (lane == 0 && clamped) atomicAdd(stats + 2, (unsigned long long)clamped);
+}
 }  // namespace spdp

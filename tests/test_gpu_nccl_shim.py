@@ -75,3 +75,32 @@ def test_nccl_path_equals_external_exchange(shim, K, waves, E, parts):
     for k in ("z", "r", "n", "m", "t", "Q"):
         np.testing.assert_array_equal(got[k], want[k], err_msg=k)
     assert np.isfinite(got["lj"]) and got["ppl"] > 1
+
+
+def test_nccl_path_sparse_transform(shim):
+    """NEXT-4 with NCCL: 2 processes, sparse P, vs the in-process external exchange."""
+    from test_oracle_sparse_p import mixing_P
+    K, sweeps = 10, 2
+    with tempfile.TemporaryDirectory() as d:
+        env = dict(os.environ, SPDP_NCCL_LIB=shim)
+        uid = os.path.join(d, "uid"); out = os.path.join(d, "out.npz")
+        procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "nccl_shim_worker.py"), str(r), "2", uid, out,
+                                   str(K), "1", "0", str(sweeps), "sparse"], env=env) for r in range(2)]
+        for p in procs:
+            assert p.wait(timeout=300) == 0
+        got = dict(np.load(out))
+    c = corpus("C1")
+    P = mixing_P(c.num_groups, c.vocab, np.random.default_rng(3))
+    ranks = [spdp.sampler_for(c, K, rank=r, world_size=2, exchange=spdp.SPDP_EXCHANGE_EXTERNAL, transform=P, **HYPER)
+             for r in range(2)]
+    for _ in range(sweeps):
+        for r in ranks:
+            r.sweep_local()
+        tot = sum(r.exchange_get().astype(np.int64) for r in ranks).astype(np.int32)
+        for r in ranks:
+            r.exchange_put(tot)
+            r.sweep_merge()
+    want = ranks[0].counts()
+    for k in ("m", "t", "Q"):
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    np.testing.assert_array_equal(got["q"], ranks[0].sparse_state()["q"])

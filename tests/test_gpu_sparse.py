@@ -101,3 +101,41 @@ def test_sparse_estimators_match_oracle(K):
     res = g.heldout(test, 3, 0, z_init=zf)
     assert res["perplexity"] == pytest.approx(sp.heldout_perplexity(test.group, test.doc, test.word, test.num_docs, zf),
                                               rel=1e-10)
+
+
+@pytest.mark.parametrize("G,waves", [(2, 1), (3, 2)])
+def test_sparse_multi_rank_matches_oracle_shards(G, waves):
+    """NEXT-4 on several ranks (G contexts on one GPU, external exchange of the
+    m and q net changes): the oracle's G-shard sweep with sources, bit for bit
+    when the draws agree."""
+    c = corpus("C1")
+    P = mixing_P(c.num_groups, c.vocab, np.random.default_rng(3))
+    ranks = [spdp.sampler_for(c, 10, num_waves=waves, rank=r, world_size=G, exchange=spdp.SPDP_EXCHANGE_EXTERNAL,
+                              transform=P, **HYPER) for r in range(G)]
+    o = oracle.from_corpus(c, 10, **HYPER)
+    sp = oracle.SparseOracle(o, *P)
+    part = np.asarray(spdp.spdp_partition(7, G, c.doc, c.num_docs))[c.doc]
+    for s in range(2):
+        for r in ranks:
+            r.sweep_local()
+        bufs = [r.exchange_get() for r in ranks]
+        tot = sum(b.astype(np.int64) for b in bufs).astype(np.int32)
+        for r in ranks:
+            r.exchange_put(tot)
+            r.sweep_merge()
+        sp.sweep_shards(waves=waves, shards=G)
+        st = sp.state()
+        z = np.full(c.num_tokens, -1, np.int32)
+        for j, r in enumerate(ranks):
+            z[part == j] = r.counts()["z"][part == j]
+        mism = np.count_nonzero(z != st["z"])
+        assert mism <= max(1, 1e-4 * c.num_tokens), mism
+        if mism == 0:
+            g0 = ranks[0].counts()
+            for k in ("m", "t"):
+                np.testing.assert_array_equal(g0[k], st[k], err_msg=k)
+            gs = ranks[0].sparse_state()
+            np.testing.assert_array_equal(gs["q"], st["q"])
+            np.testing.assert_array_equal(gs["Qs"], st["Qs"])
+            for r in ranks[1:]:
+                np.testing.assert_array_equal(r.sparse_state()["q"], gs["q"])

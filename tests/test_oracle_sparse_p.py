@@ -215,3 +215,32 @@ def test_sparse_estimators_normalised_and_identity_reduction():
     te = synth.generate(2, 3, 9.0, 30, 3, seed=6)
     zf = s2.foldin(te.group, te.doc, te.word, te.num_docs, seed=2, iterations=3)
     assert np.isfinite(s2.heldout_perplexity(te.group, te.doc, te.word, te.num_docs, zf))
+
+
+@pytest.mark.parametrize("G,waves", [(1, 1), (2, 1), (3, 2)])
+def test_sharded_sweep_identity_reduction_and_validity(G, waves):
+    """Several shards with one exchange per sweep: with P^i = I exactly the pinned
+    G-shard identity sampler (or_sweep_par); with a sparse P a valid state."""
+    c = synth.generate(2, 10, 12.0, 30, 4, seed=5)
+    a = oracle.from_corpus(c, 4)
+    b = oracle.from_corpus(c, 4)
+    sp = oracle.SparseOracle(b, *identity_P(2, 30))
+    for _ in range(3):
+        a.sweep_par(waves=waves, shards=G)
+        sp.sweep_shards(waves=waves, shards=G)
+        sa, sb = a.state(), sp.state()
+        for k in ("z", "r", "n", "m", "t"):
+            assert np.array_equal(sa[k], sb[k]), k
+        assert np.array_equal(sa["Q"], sb["Qs"])
+    o = oracle.from_corpus(c, 4)
+    s2 = oracle.SparseOracle(o, *mixing_P(2, 30, np.random.default_rng(7)))
+    if G == 1:
+        o2 = oracle.from_corpus(c, 4)
+        s3 = oracle.SparseOracle(o2, *mixing_P(2, 30, np.random.default_rng(7)))
+    for _ in range(3):
+        s2.sweep_shards(waves=waves, shards=G)
+        st = s2.state()
+        assert (st["q"] >= 0).all() and (st["t"] <= st["m"]).all() and ((st["t"] > 0) == (st["m"] > 0)).all()
+        if G == 1:
+            s3.sweep_par(waves=waves)
+            assert all(np.array_equal(st[k], s3.state()[k]) for k in ("z", "r", "m", "t", "q"))
