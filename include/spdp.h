@@ -257,8 +257,10 @@ spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t
  * spdp_load_corpus.  The estimators (spdp_topics, spdp_heldout, the
  * perplexity of spdp_loglik) then use phi~^i with sum_v p_{i,w,v} phi0~_{k,v}
  * (P:1754).  Several ranks exchange the net changes of m and q (the external
- * exchange buffer is int32: cells, then E x Kp source cells).  This version:
- * SPDP_UPDATE_WAVE; log_joint and spdp_debug_probs return SPDP_ESTATE.  Readings:
+ * exchange buffer is int32: cells, then E x Kp source cells); log_joint is
+ * then log p(W, Z, T, Q) (the sources' multinomial and p terms added).  This
+ * version: SPDP_UPDATE_WAVE; spdp_debug_probs and, with several ranks, the
+ * perplexity of spdp_loglik return SPDP_ESTATE.  Readings:
  * DESIGN.md §13 (c24 wave correction of the sources, c25 initial sources,
  * c26 the removed table's source).  Errors: SPDP_EINVAL, SPDP_ESTATE.
  *

@@ -110,6 +110,8 @@ def lib():
         L.or_sp_heldout_perplexity.restype = C.c_double
         L.or_sp_perplexity.argtypes = [P]
         L.or_sp_sweep_shards.argtypes = [P, C.c_int, C.c_int]
+        L.or_sp_log_joint.argtypes = [P]
+        L.or_sp_log_joint.restype = C.c_double
         L.or_sp_perplexity.restype = C.c_double
         _lib = L
     return _lib
@@ -371,6 +373,9 @@ class SparseOracle:
 
     def perplexity(self):
         return float(lib().or_sp_perplexity(self.h))
+
+    def log_joint(self):
+        return float(lib().or_sp_log_joint(self.h))
 
     def foldin(self, group, doc, word, num_docs, seed, iterations, first_iteration=0, z=None, force_z=None,
                want_margin=False):

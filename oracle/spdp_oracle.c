@@ -1467,3 +1467,27 @@ out:
     free(shard); free(m0); free(q0); free(Dm); free(Dq); free(Lm); free(Lt); free(Lq); free(LM); free(LTt); free(LQ); free(LT);
     return rc;
 }
+
+/* log p(W, Z, T, Q) with sparse P^i (P:1649-1660 summed over the seatings R and
+ * the per-table source orders V consistent with (T, Q)): the identity-P joint
+ * above with Q_kv = sum_{i,w} q_{ikwv} in the shadow term, plus, per cell,
+ * ln multinomial(t; q) + sum_e q_e ln p_e. */
+double or_sp_log_joint(const spstate *sp) {
+    ostate *s = sp->o;
+    int64_t *Qsave = s->Q;
+    s->Q = sp->Qs;                              /* same [K*V] layout */
+    double lp = or_log_joint(s);
+    s->Q = Qsave;
+    int I = s->I, V = s->V, K = s->K;
+    for (int i = 0; i < I; i++)
+        for (int w = 0; w < V; w++)
+            for (int k = 0; k < K; k++) {
+                size_t c = IDX3(s, i, w, k);
+                lp += lgamma((double)s->t[c] + 1.0);
+                for (int32_t e = sp->pptr[i * V + w]; e < sp->pptr[i * V + w + 1]; e++) {
+                    int32_t qv = sp->q[(size_t)e * K + k];
+                    lp += -lgamma((double)qv + 1.0) + (double)qv * log(sp->pp[e]);
+                }
+            }
+    return lp;
+}

@@ -1774,16 +1774,17 @@ spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
 spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    if (c->sparse) {
+    if (c->sparse && perplexity) {
         // NEXT-4: training perplexity = the held-out computation on the training tokens with their own z
-        // (theta~ from n_d, phi~ with the sources); log p(W, Z, T, Q) is not provided in this version
-        if (log_joint) return fail(c, SPDP_ESTATE, "log_joint is not available with a transformation matrix in this version");
-        if (!perplexity) return SPDP_OK;
+        // (theta~ from n_d, phi~ with the sources)
+        if (c->G > 1) return fail(c, SPDP_ESTATE, "the perplexity with a transformation matrix is per rank: use spdp_heldout");
         if ((s = ensure_host_plan(c))) return s;
         std::vector<int32_t> z((size_t)c->N);
         if ((s = spdp_counts(c, z.data(), nullptr, nullptr, nullptr, nullptr, nullptr))) return s;
-        return spdp_heldout(c, c->N, c->D, c->group.data(), c->doc.data(), c->word.data(), 0, 0, 0, z.data(), nullptr,
-                            nullptr, perplexity);
+        if ((s = spdp_heldout(c, c->N, c->D, c->group.data(), c->doc.data(), c->word.data(), 0, 0, 0, z.data(), nullptr,
+                              nullptr, perplexity)))
+            return s;
+        perplexity = nullptr;
     }
     const bool gather = c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL;
     if (perplexity) {
@@ -1833,7 +1834,13 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
                                                                    c->K, c->Kp, part + grid);
         loglik_small_kernel<<<1, 1024, 0, c->stream>>>(c->d_M, c->d_Tt, c->d_T, c->d_disc64, c->d_conc64, c->I, c->K, c->Kp,
                                                       (double)c->V * c->cfg.beta, part + 2 * grid);
-        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(part, 2 * grid + 1, c->d_scalar + 1);   // words + docs + small
+        int nterms = 2 * grid + 1;
+        if (c->sparse) {   // NEXT-4: ln multinomial(t; q) + sum q ln p per cell (Q of the shadow term is Q[v][k])
+            sp_source_terms_kernel<<<grid, 256, 0, c->stream>>>(sparse_args(c), c->d_spp64, (uint32_t)c->V * c->I, c->K,
+                                                                c->Kp, c->d_t, part + 2 * grid + 1);
+            nterms = 3 * grid + 1;
+        }
+        reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(part, nterms, c->d_scalar + 1);   // words + docs + small (+ sources)
         reduce_fixed_kernel<<<1, 1024, 0, c->stream>>>(part + grid, grid, c->d_scalar + 2);    // docs only
         if ((s = check_launch(c, "loglik kernels"))) { cudaFree(ls); cudaFree(d_off); return s; }
         double v[2] = {0, 0};

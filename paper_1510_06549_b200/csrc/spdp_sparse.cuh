@@ -411,3 +411,33 @@ __global__ void sp_exchange_merge_kernel(SparseP P, uint32_t segs, int32_t* __re
     if (lane == 0 && clamped) atomicAdd(stats + 2, (unsigned long long)clamped);
 }
 }  // namespace spdp
+
+namespace spdp {
+// log p(W, Z, T, Q) source terms per block: sum over cells of ln t! - sum_e ln q_e! + sum_e q_e ln p_e (fp64)
+__global__ void sp_source_terms_kernel(SparseP P, const double* __restrict__ pp64, uint32_t segs, int K, int Kp,
+                                       const int32_t* __restrict__ t, double* __restrict__ partial) {
+    __shared__ double sh[32];
+    double acc = 0.0;
+    const size_t n = (size_t)segs * Kp;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(j % Kp);
+        if (k >= K) continue;
+        const uint32_t seg = (uint32_t)(j / Kp);
+        double v = lgamma((double)t[j] + 1.0);
+        for (uint32_t e = P.sptr[seg]; e < P.sptr[seg + 1]; ++e) {
+            const int qv = P.q[(size_t)e * Kp + k];
+            v += -lgamma((double)qv + 1.0) + (double)qv * log(pp64[e]);
+        }
+        acc += v;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+        partial[blockIdx.x] = s;
+    }
+}
+}  // namespace spdp

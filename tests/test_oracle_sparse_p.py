@@ -244,3 +244,23 @@ def test_sharded_sweep_identity_reduction_and_validity(G, waves):
         if G == 1:
             s3.sweep_par(waves=waves)
             assert all(np.array_equal(st[k], s3.state()[k]) for k in ("z", "r", "m", "t", "q"))
+
+
+@pytest.mark.parametrize("spec,hyper", [(TINY[0], HYPER), (TINY[1], HYPER2)])
+def test_sparse_log_joint_is_exact(spec, hyper):
+    """log p(W, Z, T, Q) of the oracle equals the brute-force joint of the
+    generative process with P (TinyCorpusP) on every state."""
+    tc, g, d, w, (pptr, pv, pp) = _tiny(spec, hyper=hyper)
+    n = 0
+    for z, t, q in tc.states_q():
+        o = oracle.Oracle(tc.I, tc.V, tc.K, **hyper, seed=1)
+        tarr = np.zeros((tc.I, tc.V, tc.K), np.int32)
+        for (i, ww, k), tv in t.items():
+            tarr[i, ww, k] = tv
+        o.load(g, d, w, tc.D, z_init=np.array(z, np.int32), t_init=tarr)
+        sp = oracle.SparseOracle(o, pptr, pv, pp)
+        sp.set_q(_q_array(tc, q, pptr, tc.K))
+        want = math.log(float(tc.joint_WZTQ(z, t, q)))
+        assert sp.log_joint() == pytest.approx(want, abs=1e-9), (z, t, q)
+        n += 1
+    assert n > 20
