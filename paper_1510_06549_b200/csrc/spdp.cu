@@ -318,7 +318,7 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
     t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.F = c->d_F; t.R1 = c->d_R1; t.n = c->d_n;
     t.sigma = c->d_sigma;
-    for (int B = 0; B < 16; ++B) {
+    for (int B = 0; B < 32; ++B) {
         const int nbl = c->KPL / 4;
         t.bpos[B] = (B < c->Kp / 4) ? c->colstart[B % nbl] + B / nbl : 0;
     }
@@ -330,14 +330,16 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats;
     const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
     const int nbk = (c->K + 3) / 4;
+    const size_t tsm = nbk > 16 ? sizeof(float) * 256 * 32 : 0;
 #define SPDP_TOK(NBK)                                                                                   \
     do {                                                                                                \
-        if (c->row16) token_kernel<NBK, uint16_t><<<std::max(grid, 1), 256, 0, c->stream>>>(t);         \
-        else token_kernel<NBK, float><<<std::max(grid, 1), 256, 0, c->stream>>>(t);                     \
+        if (c->row16) token_kernel<NBK, uint16_t><<<std::max(grid, 1), 256, tsm, c->stream>>>(t);       \
+        else token_kernel<NBK, float><<<std::max(grid, 1), 256, tsm, c->stream>>>(t);                   \
     } while (0)
     if (nbk <= 4) SPDP_TOK(4);
     else if (nbk <= 8) SPDP_TOK(8);
-    else SPDP_TOK(16);
+    else if (nbk <= 16) SPDP_TOK(16);
+    else SPDP_TOK(32);
 #undef SPDP_TOK
     c->launches += 1;
 }
@@ -1191,8 +1193,13 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
     }
     // small K: the token kernel (packed per-wave deltas need |delta| <= count(i,w) < 2^15)
-    c->token_kernel = !c->async && !c->sparse && c->K <= 64 && c->mmax < 32768;
-    if (const char* e = getenv("SPDP_TOKEN_KERNEL")) c->token_kernel = c->token_kernel && atoi(e) != 0;
+    // (64 < K <= 128: only with several waves, where the chunk kernel's segments get short)
+    c->token_kernel = !c->async && !c->sparse && c->mmax < 32768 && (c->K <= 64 || (c->K <= 128 && W > 1));
+    if (const char* e = getenv("SPDP_TOKEN_KERNEL")) {   // 0: never; 2: also K <= 128 with one wave
+        const int v = atoi(e);
+        if (v == 0) c->token_kernel = false;
+        if (v == 2) c->token_kernel = !c->async && !c->sparse && c->mmax < 32768 && c->K <= 128;
+    }
     // documents -> ranks
     if (c->G > 1) partition_docs(c->cfg.seed, c->G, num_tokens, num_docs, c->doclen, c->shard_of_doc);
     else c->shard_of_doc.assign((size_t)num_docs, 0);

@@ -67,7 +67,7 @@ struct TokenArgs {
     const float* R1;               // [run][Kp] r = 1 share F1 / F at the snapshot
     const void* n;                 // doc-topic rows (sigma layout of the chunk kernel)
     const int* sigma;              // [Kp] in-row position of topic k
-    int bpos[16];                  // in-row position (float4 units) of 4-topic block B
+    int bpos[32];                  // in-row position (float4 units) of 4-topic block B
     const int32_t *m, *t, *Q, *M, *Tt, *T;
     int32_t* dmt;                  // packed wave deltas dm * 2^16 + dt per cell
     const float* alpha;            // [I][Kp]
@@ -84,8 +84,11 @@ struct TokenArgs {
 
 
 // NBK: 4-topic blocks of the topic range (K <= 4 NBK)
+// NBK > 16 (K <= 128): the block sums live in shared memory [NBK][blockDim.x] instead of registers
 template <int NBK, typename NT>
 __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A) {
+    constexpr bool kSm = NBK > 16;
+    extern __shared__ float s_tbs[];
     const int I = A.I, K = A.K, Kp = A.Kp;
     const int nbk = (K + 3) >> 2;
     const uint32_t sweep = *A.sweep;
@@ -121,19 +124,21 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
             const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
             const float dlt = wnew - wold;
             // a4/a5: masses in 4-topic blocks
-            float bs[NBK];
+            float bsr[kSm ? 1 : NBK];
+#define BS(B) (*(kSm ? &s_tbs[(B) * blockDim.x + threadIdx.x] : &bsr[kSm ? 0 : (B)]))
             double total = 0.0;
 #pragma unroll
             for (int B = 0; B < NBK; ++B) {
-                bs[B] = 0.f;
+                BS(B) = 0.f;
                 if (B < nbk) {
                     const float4 n4 = Row<NT>::load4(nrow + 4 * A.bpos[B]);
                     const float4 F4 = *reinterpret_cast<const float4*>(Frow + 4 * B);
                     const float4 a4 = *reinterpret_cast<const float4*>(al + 4 * B);
-                    bs[B] = (__fmaf_rn(n4.x, F4.x, __fmul_rn(a4.x, F4.x)) + __fmaf_rn(n4.y, F4.y, __fmul_rn(a4.y, F4.y))) +
-                            (__fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)) + __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w)));
-                    if ((k0 >> 2) == B) bs[B] += dlt;
-                    total += (double)bs[B];
+                    float bsv = (__fmaf_rn(n4.x, F4.x, __fmul_rn(a4.x, F4.x)) + __fmaf_rn(n4.y, F4.y, __fmul_rn(a4.y, F4.y))) +
+                                (__fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)) + __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w)));
+                    if ((k0 >> 2) == B) bsv += dlt;
+                    BS(B) = bsv;
+                    total += (double)bsv;
                 }
             }
             // a6: target = u * total; the block, then the topic, where the prefix first exceeds it
@@ -143,12 +148,14 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
 #pragma unroll
             for (int B = 0; B < NBK; ++B) {
                 if (B < nbk) {
-                    const double nxt = run2 + (double)bs[B];
+                    const float bsv = BS(B);
+                    const double nxt = run2 + (double)bsv;
                     if (qs < 0 && nxt > target) { qs = B; bbeg = run2; }
-                    if (bs[B] > 0.f) { qlast = B; lastbeg = run2; }
+                    if (bsv > 0.f) { qlast = B; lastbeg = run2; }
                     run2 = nxt;
                 }
             }
+#undef BS
             bool fb = qs < 0;
             if (fb) { qs = qlast; bbeg = lastbeg; }                                // rounding: last positive block
             int bq = 0;

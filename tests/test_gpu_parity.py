@@ -50,7 +50,7 @@ def test_conditionals_match_oracle(name, K):
 
 
 @pytest.mark.parametrize("name,K,waves", [("C1", 10, 1), ("C1", 10, 4), ("C1", 10, 200), ("C2", 50, 1),
-                                          ("C2", 50, 3)])
+                                          ("C2", 50, 3), ("C1", 100, 3), ("C1", 128, 2)])
 def test_one_sweep_from_identical_state(name, K, waves):
     c = corpus(name)
     g, o = pair(c, K, waves=waves)
