@@ -302,3 +302,39 @@ def test_packed_assignments_match_counts():
     zr = g.zr()
     np.testing.assert_array_equal(zr & 0x7FFF, cnt["z"])
     np.testing.assert_array_equal(zr >> 15, cnt["r"])
+
+
+def test_call_order_and_input_errors():
+    """The boundary's error behaviour (include/spdp.h): state errors for calls out of
+    order, SPDP_EINVAL for invalid inputs, and the context stays usable after a
+    rejected call."""
+    c = corpus("C1")
+    g = spdp.Sampler(c.num_groups, c.vocab, 10, **HYPER)
+    for call in (lambda: g.sweep(1), lambda: g.counts(), lambda: g.loglik(), lambda: g.zr()):
+        with pytest.raises(spdp.SPDPError) as e:
+            call()
+        assert e.value.code == spdp.SPDP_ESTATE
+    bad = c.word.copy(); bad[5] = c.vocab
+    with pytest.raises(spdp.SPDPError) as e:
+        g.load_corpus(c.group, c.doc, bad, c.num_docs)
+    assert e.value.code == spdp.SPDP_EINVAL
+    g.close()
+    g = spdp.Sampler(c.num_groups, c.vocab, 10, **HYPER)
+    span = c.group.copy(); span[0] = 1 - span[0]           # document 0 now spans two groups
+    with pytest.raises(spdp.SPDPError) as e:
+        g.load_corpus(span, c.doc, c.word, c.num_docs)
+    assert e.value.code == spdp.SPDP_EINVAL
+    g.close()
+    g = spdp.sampler_for(c, 10, **HYPER)
+    with pytest.raises(spdp.SPDPError) as e:
+        g.load_corpus(c.group, c.doc, c.word, c.num_docs)   # once per context
+    assert e.value.code == spdp.SPDP_ESTATE
+    z = np.full(c.num_tokens, 10, np.int32)                # z out of [0, K)
+    with pytest.raises(spdp.SPDPError) as e:
+        g.set_state(z)
+    assert e.value.code == spdp.SPDP_EINVAL
+    with pytest.raises(spdp.SPDPError) as e:
+        g.sweep(-1)
+    assert e.value.code == spdp.SPDP_EINVAL
+    g.sweep(2)                                             # still usable
+    assert g.counts()["m"].sum() == c.num_tokens
