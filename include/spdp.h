@@ -2,8 +2,9 @@
  * spdp.h — C ABI of the B200-native SPDP Gibbs sweep (libspdp.so).
  *
  * The library samples the collapsed blocked-Gibbs chain of the Shadow
- * Poisson–Dirichlet Process topic model with identity transformation
- * matrices (§3.4), i.e. Algorithm 1 "SPDP Full Gibbs
+ * Poisson–Dirichlet Process topic model — with identity transformation
+ * matrices by default (§3.4; sparse P^i through
+ * spdp_set_transform, NEXT-4), i.e. Algorithm 1 "SPDP Full Gibbs
  * Sampling" with the conditionals of
  * Eq. SPDP-sampling-w-z-r0 and
  * Eq. SPDP-sampling-w-z-r1, parallelised the way §3.3
@@ -25,9 +26,11 @@
  *     copied during the call; outputs are caller-allocated and written before
  *     the call returns.  The context owns all device memory and the NCCL
  *     communicator.
- *   - Call order: spdp_create -> spdp_load_corpus -> {spdp_sweep, spdp_counts,
- *     spdp_loglik, spdp_set_state, spdp_debug_probs}* -> spdp_destroy.
- *     Anything else returns SPDP_ESTATE.
+ *   - Call order: spdp_create -> [spdp_set_transform] -> spdp_load_corpus ->
+ *     {spdp_sweep (or spdp_sweep_local / spdp_sweep_merge), spdp_counts,
+ *     spdp_zr, spdp_loglik, spdp_set_state, spdp_topics, spdp_heldout,
+ *     spdp_debug_probs, ...}* -> spdp_destroy.  Anything else returns
+ *     SPDP_ESTATE.
  *   - A context is not thread-safe.  Calls are synchronous with respect to
  *     the host (they return after the work on the context's stream is done).
  *   - Determinism: outputs are bit-identical for identical (config, corpus,
@@ -146,6 +149,7 @@ spdp_status spdp_set_state(spdp_ctx* ctx, const int32_t* z, const uint8_t* r, co
 spdp_status spdp_sweep(spdp_ctx* ctx, int32_t num_sweeps);
 
 /* Split sweep for SPDP_EXCHANGE_EXTERNAL: spdp_sweep_local runs every wave
+ * (with merge_every, the next exchange block of waves; see spdp_exchange_blocks)
  * on this rank and leaves the rank's net (customer, table) count change of
  * every cell since the sweep start in the device buffer returned by
  * spdp_exchange_buffer (*count elements of *elem_bytes bytes, device pointer
@@ -156,7 +160,9 @@ spdp_status spdp_sweep(spdp_ctx* ctx, int32_t num_sweeps);
  * elements over ranks (wrapping) is the packed sum of dm and dt.  The caller
  * replaces the buffer's content by that element-wise sum over ranks, then
  * calls spdp_sweep_merge (Alg.3: rows = sweep-start
- * state + summed changes, t clamped, Q and the sums recomputed). */
+ * state + summed changes, t clamped, Q and the sums recomputed).  With a
+ * transformation matrix the buffer is int32 m changes (cells) followed by
+ * the source changes q (E x Kp), see spdp_set_transform. */
 spdp_status spdp_sweep_local(spdp_ctx* ctx);
 /* Exchange blocks per sweep (merge_every): the caller repeats
  * {spdp_sweep_local, sum over ranks, spdp_sweep_merge} *nblocks times per
