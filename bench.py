@@ -327,10 +327,11 @@ def main():
     line = {
         "metric": "sampled tokens/sec per sweep", "value": round(value, 1), "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32 weights / fp64 CDF / int32 counts",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic SPDP-generated corpus (synth/, seeded)",
         "config": {"workload": workload, "tokens": N, "groups": cfg.groups, "docs": corpus.num_docs,
                    "vocab": cfg.vocab, "topics": K, "waves": args.waves, "parallelism": f"doc-shard x{world}",
+                   "arithmetic": "f32 slot masses, f64 CDF prefix and uniform, int32 counts, exact integer removal draw",
                    "l2": "flushed between timed sweeps (256 MiB write outside the events)" if flush is not None else "not flushed",
                    "sweep_ms": [round(x, 4) for x in step_ms]},
         "roofline": roof,
