@@ -1211,6 +1211,10 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             c->global_of_local.push_back(d);
         }
     c->Dloc = (int32_t)c->global_of_local.size();
+    // the kernels address a doc-topic row by a 32-bit element offset (doc * Kp)
+    if ((uint64_t)c->Dloc * (uint64_t)Kp >= (1ull << 32) - 4096)
+        return fail(c, SPDP_EINVAL, "%d local documents x %d topic slots exceed 2^32 doc-topic cells per rank: "
+                    "use more ranks", c->Dloc, Kp);
     lt.mark("M_max + partition");
     // this rank's tokens, canonical order
     TempBuf<uint32_t> dlocal(n);
