@@ -177,6 +177,17 @@ struct spdp_ctx {
     std::vector<void*> allocs;
     // profiling (spdp_profile)
     bool profiling = false;
+    // one sweep captured as a CUDA graph and replayed (single rank): keyed by the zr buffer the sweep
+    // starts from (W = 1 paths swap zr / zr_next every sweep) and by profiling (event nodes)
+    struct SweepGraph {
+        uint16_t* zr_at_start;
+        bool prof, swaps;
+        cudaGraphExec_t exec;
+        int64_t launches;
+        double sample_launches;
+    };
+    std::vector<SweepGraph> graphs;
+    bool graphs_off = false;
     std::vector<cudaEvent_t> ev;          // 4 per wave + 2 for the exchange
     double acc[10] = {0};
     int64_t launches = 0;
@@ -1591,7 +1602,60 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
     if (num_sweeps < 0) return fail(c, SPDP_EINVAL, "num_sweeps must be >= 0");
     if (c->G > 1 && c->cfg.exchange != SPDP_EXCHANGE_NCCL)
         return fail(c, SPDP_ESTATE, "SPDP_EXCHANGE_EXTERNAL: use spdp_sweep_local / spdp_sweep_merge");
+    const bool graphs = c->G == 1 && !c->cfg.debug_checks && !c->graphs_off && !c->profiling &&
+                        !(getenv("SPDP_GRAPHS") && atoi(getenv("SPDP_GRAPHS")) == 0);
     for (int it = 0; it < num_sweeps; ++it) {
+      if (graphs && !c->graphs_off) {
+        if (c->profiling && (s = ensure_events(c))) return s;
+        spdp_ctx::SweepGraph* ge = nullptr;
+        for (auto& g : c->graphs)
+            if (g.zr_at_start == c->d_zr && g.prof == c->profiling) ge = &g;
+        bool ran = false;
+        if (ge) {
+            CU(cudaGraphLaunch(ge->exec, c->stream));
+            if (ge->swaps) std::swap(c->d_zr, c->d_zr_next);
+            c->sweeps_done++;
+            c->launches += ge->launches;
+            c->acc[5] += ge->sample_launches;
+            ran = true;
+        } else {
+            // capture one sweep (the host bookkeeping runs during the capture, the work at the launch)
+            uint16_t *zr0 = c->d_zr, *zn0 = c->d_zr_next;
+            const uint32_t sw0 = c->sweeps_done;
+            const int64_t l0 = c->launches;
+            const double a50 = c->acc[5];
+            cudaGraph_t graph = nullptr;
+            cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+            spdp_status sc = SPDP_OK;
+            if (e == cudaSuccess) {
+                sc = run_waves(c, 0, c->W, true);
+                if (!sc) sc = finish_sweep(c);
+                e = cudaStreamEndCapture(c->stream, &graph);
+            }
+            cudaGraphExec_t exec = nullptr;
+            if (e == cudaSuccess && !sc && graph) e = cudaGraphInstantiate(&exec, graph, 0);
+            if (graph) cudaGraphDestroy(graph);
+            if (e == cudaSuccess && !sc && exec) {
+                c->graphs.push_back({zr0, c->profiling, c->d_zr != zr0, exec, c->launches - l0, c->acc[5] - a50});
+                CU(cudaGraphLaunch(exec, c->stream));
+                ran = true;
+            } else {                          // not capturable here: undo the bookkeeping, run directly
+                cudaGetLastError();
+                c->poisoned = false;          // capture-time API errors executed no work
+                c->err.clear();
+                if (exec) cudaGraphExecDestroy(exec);
+                c->d_zr = zr0; c->d_zr_next = zn0; c->sweeps_done = sw0; c->launches = l0; c->acc[5] = a50;
+                c->graphs_off = true;
+            }
+        }
+        if (ran) {
+            if (c->profiling) {
+                if ((s = sync(c, "spdp_sweep"))) return s;
+                collect_times(c, false);
+            }
+            continue;
+        }
+      }
       for (int b = 0; b < c->nblocks; ++b) {
         if ((s = run_waves(c, block_w0(c, b), block_w1(c, b), b == 0))) return s;
         if (c->G > 1 && !c->overlap) {
@@ -2152,6 +2216,7 @@ void spdp_destroy(spdp_ctx* c) {
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->h_zr_canon) cudaFreeHost(c->h_zr_canon);
     if (c->comm && c->nccl.CommDestroy) c->nccl.CommDestroy(c->comm);
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
     for (cudaEvent_t e : c->part_ev) cudaEventDestroy(e);
     if (c->comm_done) cudaEventDestroy(c->comm_done);
