@@ -298,12 +298,13 @@ def main():
     bytes_sweep = alg_bytes(plan, K)
     achieved = bytes_sweep / (sample_ms / 1e3) / 1e9
     kname = "sp_token_kernel" if transform is not None else ("token_kernel" if stats.get("token_kernel") else "sample_kernel")
-    traffic = load_traffic(cfg.name, K, kname.split("_")[0])
+    pkey = kname.split("_")[0] + ("_async" if args.update == "async" else "")   # which committed ncu capture
+    traffic = load_traffic(cfg.name, K, pkey)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
             "alg_bytes_per_launch": int(bytes_sweep / max(args.waves, 1)), "peak_source": peak_src,
             "sample_ms_per_sweep": round(sample_ms, 4), "share_of_step": round(sample_ms / ms, 3)}
-    nc = ncu_summary(cfg.name, K, kname.split("_")[0])
+    nc = ncu_summary(cfg.name, K, pkey)
     if nc:   # what actually limits the kernel (from the committed ncu capture, not this run)
         roof["ncu"] = {k: nc.get(k) for k in ("file", "l2_hit_pct", "l1_pct_of_peak", "issue_active_pct",
                                                "achieved_occupancy_pct", "warp_instructions", "duration_ms")}

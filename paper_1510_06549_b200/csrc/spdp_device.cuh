@@ -166,16 +166,43 @@ __device__ __forceinline__ unsigned short ld_relaxed_u16(const uint16_t* p) {
     asm volatile("ld.relaxed.gpu.global.b16 %0, [%1];" : "=h"(v) : "l"(p));
     return v;
 }
+// SPDP_ASYNC_WEAK_ROWS: the async mode reads doc-topic rows with plain (weak, L1-cacheable) loads.
+// The paper's scheme reads the global counts without synchronisation while other threads update
+// them ("spinlocks or semaphores ... totally optional"); a weak load may return a
+// stale value, which the scheme tolerates by design.  0: coherent ld.relaxed.gpu (L2) instead.
+#ifndef SPDP_ASYNC_WEAK_ROWS
+#define SPDP_ASYNC_WEAK_ROWS 1
+#endif
+constexpr bool kAsyncWeakRows = SPDP_ASYNC_WEAK_ROWS != 0;
+__device__ __forceinline__ float4 ld_weak_f4(const float* p) {
+    float4 v;
+    asm("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_weak_u2(const void* p) {
+    uint2 v;
+    asm("ld.global.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int ld_weak(const int32_t* p) {
+    int v;
+    asm("ld.global.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 template <bool AS>
 __device__ __forceinline__ int ldc(const int32_t* p) {   // count read: snapshot (wave mode) or live (async)
-    if constexpr (AS) return ld_relaxed(p);
+    if constexpr (AS) return kAsyncWeakRows ? ld_weak(p) : ld_relaxed(p);
     else return *p;
 }
 
 template <>
 struct Row<float> {
     __device__ __forceinline__ static float4 load4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-    __device__ __forceinline__ static float4 load4_live(const float* p) { return ld_relaxed_f4(p); }
+    __device__ __forceinline__ static float4 load4_live(const float* p) {
+        if constexpr (kAsyncWeakRows) return ld_weak_f4(p);
+        else return ld_relaxed_f4(p);
+    }
     __device__ __forceinline__ static float load1_live(const float* p) { return ld_relaxed_f(p); }
     __device__ __forceinline__ static float load1(const float* p) { return __ldg(p); }
     __device__ __forceinline__ static void add(float* base, size_t idx, int d) { atomicAdd(base + idx, (float)d); }
@@ -197,7 +224,7 @@ struct Row<uint16_t> {
         return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y));
     }
     __device__ __forceinline__ static float4 load4_live(const uint16_t* p) {
-        const uint2 v = ld_relaxed_u2(p);
+        const uint2 v = kAsyncWeakRows ? ld_weak_u2(p) : ld_relaxed_u2(p);
         return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y));
     }
     __device__ __forceinline__ static float load1_live(const uint16_t* p) { return (float)ld_relaxed_u16(p); }
