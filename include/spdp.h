@@ -194,6 +194,20 @@ spdp_status spdp_counts(spdp_ctx* ctx, int32_t* z, uint8_t* r, int32_t* doc_topi
  * SPDP_EXCHANGE_EXTERNAL; gathered from every rank (collective) with
  * SPDP_EXCHANGE_NCCL.  Caller-owned host buffer. */
 spdp_status spdp_zr(spdp_ctx* ctx, uint16_t* zr);
+/* spdp_zr without the wait: the canonical-order scatter is queued on the
+ * context's stream and the device->host copy on a library-owned copy stream,
+ * so the copy overlaps whatever the caller queues next (typically the next
+ * spdp_sweep, which does not touch the staging buffer).  The caller's buffer
+ * holds the assignments as of this call only after spdp_wait (or
+ * spdp_destroy); it must stay allocated until then, and should be pinned
+ * (pageable memory makes the copy synchronous).  A later spdp_zr_async,
+ * spdp_zr or spdp_counts orders itself after the pending copy on the device.
+ * With world_size > 1 and SPDP_EXCHANGE_NCCL this is spdp_zr (collective,
+ * blocking).  Errors as spdp_zr. */
+spdp_status spdp_zr_async(spdp_ctx* ctx, uint16_t* zr);
+/* Block until every copy queued by spdp_zr_async has landed and the
+ * context's stream is idle.  SPDP_ECUDA on a device fault. */
+spdp_status spdp_wait(spdp_ctx* ctx);
 
 /* log_joint = log p(W, Z, T | alpha, beta, a, b) (PAPER.md:1654-1665 summed over
  * the seatings R of each T, Eq. SPDP-table-to-head);

@@ -36,7 +36,7 @@ EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "s
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
            "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr",
-           "spdp_set_transform", "spdp_sparse_state"]
+           "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -86,7 +86,7 @@ def lib():
             "spdp_partition": [C.c_uint64, I32, I64, I32, P, P], "spdp_nccl_unique_id": [P],
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
-            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
+            "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_zr_async": [P, P], "spdp_wait": [P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -221,6 +221,18 @@ def spdp_zr(ctx, N, out=None):
     return out
 
 
+def spdp_zr_async(ctx, N, out):
+    """Queue the packed assignments' copy into out (caller-owned, pinned, kept alive
+    until spdp_wait); returns at once (include/spdp.h)."""
+    assert out.dtype == np.uint16 and out.shape == (N,) and out.flags["C_CONTIGUOUS"]
+    _check(lib().spdp_zr_async(ctx, _p(out)), ctx)
+    return out
+
+
+def spdp_wait(ctx):
+    _check(lib().spdp_wait(ctx), ctx)
+
+
 def spdp_loglik(ctx, log_joint=True, perplexity=True):
     lj, pp = C.c_double(np.nan), C.c_double(np.nan)
     _check(lib().spdp_loglik(ctx, C.byref(lj) if log_joint else None, C.byref(pp) if perplexity else None), ctx)
@@ -297,6 +309,7 @@ class Sampler:
         self.I, self.V, self.K = int(num_groups), int(vocab_size), int(num_topics)
         self.ctx = spdp_create(num_groups, vocab_size, num_topics, **kw)
         self.N = self.D = 0
+        self._zr_pending = []        # host buffers of queued zr_async copies (alive until wait/close)
 
     def load_corpus(self, group, doc, word, num_docs, z_init=None, r_init=None):
         spdp_load_corpus(self.ctx, group, doc, word, num_docs, z_init, r_init)
@@ -351,6 +364,15 @@ class Sampler:
     def zr(self, out=None):
         return spdp_zr(self.ctx, self.N, out)
 
+    def zr_async(self, out):
+        """Copy of the assignments into out, landing by the next wait() (overlaps the next sweep)."""
+        self._zr_pending.append(spdp_zr_async(self.ctx, self.N, out))
+        return out
+
+    def wait(self):
+        spdp_wait(self.ctx)
+        self._zr_pending.clear()
+
     def loglik(self, log_joint=True, perplexity=True):
         return spdp_loglik(self.ctx, log_joint, perplexity)
 
@@ -384,8 +406,9 @@ class Sampler:
 
     def close(self):
         if self.ctx:
-            spdp_destroy(self.ctx)
+            spdp_destroy(self.ctx)       # waits for queued copies
             self.ctx = None
+            self._zr_pending.clear()
 
     def __del__(self):
         try:

@@ -159,6 +159,9 @@ struct spdp_ctx {
     int colstart[8] = {0};
     int prefetch_rows = 0;
     uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
+    cudaStream_t d2h_stream = nullptr;            // spdp_zr_async's copies (overlap the next sweep)
+    cudaEvent_t zr_ready = nullptr, zr_copied = nullptr;
+    bool zr_pending = false;                      // a queued copy may still read d_zr_canon
     uint16_t* h_zr_canon = nullptr;               // pinned host copy
     uint32_t* d_work = nullptr;                   // [W + 1] persistent-warp counters
     int sample_grid = 0;
@@ -376,11 +379,26 @@ SweepArgs base_args(spdp_ctx* c) {
 
 int merge_grid() { return 148 * 4; }
 
+// Temporaries of the setup calls: stream-ordered (cudaMallocAsync / cudaFreeAsync
+// on the call's stream) inside a TempStream scope, so freeing one does not
+// synchronise the device; plain cudaMalloc elsewhere.
+thread_local cudaStream_t tl_temp_stream = nullptr;
+struct TempStream {
+    cudaStream_t prev;
+    explicit TempStream(cudaStream_t s) : prev(tl_temp_stream) { tl_temp_stream = s; }
+    ~TempStream() { tl_temp_stream = prev; }
+};
+
 template <typename T>
 struct TempBuf {
     T* p = nullptr;
-    explicit TempBuf(size_t n) { if (cudaMalloc((void**)&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) p = nullptr; }
-    ~TempBuf() { if (p) cudaFree(p); }
+    cudaStream_t st = nullptr;
+    explicit TempBuf(size_t n) : st(tl_temp_stream) {
+        const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+        const cudaError_t e = st ? cudaMallocAsync((void**)&p, bytes, st) : cudaMalloc((void**)&p, bytes);
+        if (e != cudaSuccess) { p = nullptr; cudaGetLastError(); }
+    }
+    ~TempBuf() { if (p) { if (st) cudaFreeAsync(p, st); else cudaFree(p); } }
     TempBuf(const TempBuf&) = delete;
     TempBuf& operator=(const TempBuf&) = delete;
 };
@@ -1105,6 +1123,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         return fail(c, SPDP_EINVAL, "need num_tokens >= 1, num_docs >= 1 and the three token arrays");
     if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
     const int I = c->I, V = c->V, Kp = c->Kp, W = c->W;
+    TempStream temp_scope(c->stream);
     c->N = num_tokens; c->D = num_docs;
     // the token triples stay on the device (state installation); host copies only on demand (diagnostics)
     c->group.clear(); c->doc.clear(); c->word.clear();
@@ -1538,6 +1557,7 @@ spdp_status spdp_set_state(spdp_ctx* c, const int32_t* z, const uint8_t* r, cons
     spdp_status s = guard(c, true);
     if (s) return s;
     if (!z || (!r && !tables)) return fail(c, SPDP_EINVAL, "spdp_set_state needs z and (r or tables)");
+    TempStream temp_scope(c->stream);
     std::vector<uint8_t> ones;
     if (!r) { ones.assign((size_t)c->N, 1); r = ones.data(); }
     return install_state(c, z, r, tables);
@@ -1691,6 +1711,7 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
     if (z || r) {
         // canonical order on the device (z | r<<15, +1 so that 0 marks other ranks' tokens)
         if (!c->d_zr_canon) ALLOC(c->d_zr_canon, c->N);
+        if (c->zr_pending) CU(cudaStreamWaitEvent(c->stream, c->zr_copied, 0));
         CU(cudaMemsetAsync(c->d_zr_canon, 0, sizeof(uint16_t) * (size_t)c->N, c->stream));
         if (c->Nloc > 0)
             scatter_zr_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_tok_id, c->d_zr, (uint32_t)c->Nloc, c->d_zr_canon);
@@ -1823,6 +1844,50 @@ spdp_status spdp_sparse_state(spdp_ctx* c, int32_t* q, int32_t* shadow, int16_t*
     return SPDP_OK;
 }
 
+namespace {
+// Scatter the packed assignments into canonical order in d_zr_canon (c->stream).
+spdp_status zr_stage(spdp_ctx* c) {
+    spdp_status s;
+    if (!c->d_zr_canon) ALLOC(c->d_zr_canon, c->N);
+    if (c->zr_pending) CU(cudaStreamWaitEvent(c->stream, c->zr_copied, 0));   // the previous copy has read it
+    if (c->Nloc < c->N) CU(cudaMemsetAsync(c->d_zr_canon, 0xFF, sizeof(uint16_t) * (size_t)c->N, c->stream));
+    if (c->Nloc > 0)
+        scatter_zr_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_tok_id, c->d_zr, (uint32_t)c->Nloc, c->d_zr_canon, 0u);
+    if ((s = check_launch(c, "scatter_zr_kernel"))) return s;
+    c->launches += 1;
+    return SPDP_OK;
+}
+}  // namespace
+
+spdp_status spdp_zr_async(spdp_ctx* c, uint16_t* zr) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!zr) return fail(c, SPDP_EINVAL, "null output");
+    if (c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL) return spdp_zr(c, zr);   // gathered: collective, blocking
+    if (!c->d2h_stream) {
+        CU(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&c->zr_ready, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->zr_copied, cudaEventDisableTiming));
+    }
+    if ((s = zr_stage(c))) return s;
+    CU(cudaEventRecord(c->zr_ready, c->stream));
+    CU(cudaStreamWaitEvent(c->d2h_stream, c->zr_ready, 0));
+    CU(cudaMemcpyAsync(zr, c->d_zr_canon, sizeof(uint16_t) * (size_t)c->N, cudaMemcpyDeviceToHost, c->d2h_stream));
+    CU(cudaEventRecord(c->zr_copied, c->d2h_stream));
+    c->zr_pending = true;
+    return SPDP_OK;
+}
+
+spdp_status spdp_wait(spdp_ctx* c) {
+    spdp_status s = guard(c, false);
+    if (s) return s;
+    if (c->zr_pending) {
+        CU(cudaEventSynchronize(c->zr_copied));
+        c->zr_pending = false;
+    }
+    return sync(c, "spdp_wait");
+}
+
 spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
     spdp_status s = guard(c, true);
     if (s) return s;
@@ -1835,12 +1900,7 @@ spdp_status spdp_zr(spdp_ctx* c, uint16_t* zr) {
         for (int64_t p = 0; p < c->N; ++p) zr[p] = (uint16_t)(z[(size_t)p] | (r[(size_t)p] << 15));
         return SPDP_OK;
     }
-    if (!c->d_zr_canon) ALLOC(c->d_zr_canon, c->N);
-    if (c->Nloc < c->N) CU(cudaMemsetAsync(c->d_zr_canon, 0xFF, sizeof(uint16_t) * (size_t)c->N, c->stream));
-    if (c->Nloc > 0)
-        scatter_zr_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_tok_id, c->d_zr, (uint32_t)c->Nloc, c->d_zr_canon, 0u);
-    if ((s = check_launch(c, "scatter_zr_kernel"))) return s;
-    c->launches += 1;
+    if ((s = zr_stage(c))) return s;
     // straight into the caller's buffer (pinned memory makes this a full-speed DMA)
     CU(cudaMemcpyAsync(zr, c->d_zr_canon, sizeof(uint16_t) * (size_t)c->N, cudaMemcpyDeviceToHost, c->stream));
     return sync(c, "spdp_zr");
@@ -1982,6 +2042,7 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
                          const int32_t* z_init, int32_t* z_out, double* theta, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
+    TempStream temp_scope(c->stream);
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     if (num_tokens < 0 || num_tokens > (int64_t)UINT32_MAX || num_docs < 1 || iterations < 0 || first_iteration < 0 ||
         (num_tokens > 0 && (!group || !doc || !word)))
@@ -2212,6 +2273,9 @@ void spdp_destroy(spdp_ctx* c) {
     if (!c) return;
     if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->d2h_stream) { cudaStreamSynchronize(c->d2h_stream); cudaStreamDestroy(c->d2h_stream); }
+    if (c->zr_ready) cudaEventDestroy(c->zr_ready);
+    if (c->zr_copied) cudaEventDestroy(c->zr_copied);
     for (void* p : c->allocs) cudaFree(p);
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->h_zr_canon) cudaFreeHost(c->h_zr_canon);

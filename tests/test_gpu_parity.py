@@ -304,6 +304,33 @@ def test_packed_assignments_match_counts():
     np.testing.assert_array_equal(zr >> 15, cnt["r"])
 
 
+def test_async_assignment_copies_overlap_sweeps():
+    """spdp_zr_async (include/spdp.h): copies queued between sweeps land by
+    spdp_wait, each holding the state of its own step; a synchronous spdp_zr and
+    spdp_counts after a pending copy see the current state."""
+    import torch
+    c = corpus("C2")
+    g = spdp.sampler_for(c, 50, **HYPER)
+    ref = spdp.sampler_for(c, 50, **HYPER)
+    bufs = [torch.empty(c.num_tokens, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16)
+            for _ in range(3)]
+    for s in range(3):
+        g.sweep(1)
+        g.zr_async(bufs[s])
+    cnt = g.counts(doc_topic=False, customers=False, tables=False, shadow=False)   # ordered after the copies
+    g.wait()
+    for s in range(3):
+        ref.sweep(1)
+        np.testing.assert_array_equal(bufs[s], ref.zr())
+    np.testing.assert_array_equal(bufs[2] & 0x7FFF, cnt["z"])
+    g.sweep(1)
+    g.zr_async(bufs[0])
+    now = g.zr()                                             # after the queued copy, same state
+    g.wait()
+    np.testing.assert_array_equal(bufs[0], now)
+    g.close(); ref.close()
+
+
 def test_call_order_and_input_errors():
     """The boundary's error behaviour (include/spdp.h): state errors for calls out of
     order, SPDP_EINVAL for invalid inputs, and the context stays usable after a
