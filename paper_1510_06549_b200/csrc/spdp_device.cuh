@@ -19,6 +19,9 @@
 namespace spdp {
 
 constexpr int kWarps = 4;          // warps per block of the sample kernel
+#ifndef SPDP_BLOCK_ALPHA
+#define SPDP_BLOCK_ALPHA 1         // dense pass: block sum = sum_k n_k F_k + (sum_k alpha_k F_k), the latter per chunk
+#endif
 #ifndef SPDP_PREFETCH_NEXT
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
@@ -314,8 +317,8 @@ __device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
 //   phase 1 (lane = token): record, Philox (a2), removal draw against the
 //     snapshot and the own-removal correction of topic k0 (a3);
 //   phase 2 (LPT lanes per token, 32/LPT tokens per step): the doc-topic row
-//     (a4), topic masses w_k = (alpha_ik + n_dk) F_k (one FFMA each), fp32
-//     4-topic block sums and lane totals, one fp64 scan over the group's lanes,
+//     (a4), fp32 4-topic block sums of w_k = (alpha_ik + n_dk) F_k (a chain of 4
+//     FFMA from the chunk's sum of alpha_ik F_k over the block) and lane totals, one fp64 scan over the group's lanes,
 //     target = u * total, the lane holding it (a5, a6);
 //   phase 3 (lane = token): the block and the topic where the prefix first
 //     exceeds the target, slots in the paper's order j = 2k (r = 1), 2k+1 (r = 0),
@@ -344,7 +347,7 @@ __device__ __forceinline__ float row_load1(const NT* p) {
 // configuration on B200 — 8x32 (C5) runs 13 % faster with 5 blocks (<= 96 registers), while
 // 4x32 (C3) and 16x32 lose 20-30 % there
 template <int LPT, int KPL>
-constexpr int sample_minb() { return (LPT == 8 && KPL == 32) ? SPDP_MINB_8X32 : SPDP_MINB; }
+__host__ __device__ constexpr int sample_minb() { return (LPT == 8 && KPL == 32) ? SPDP_MINB_8X32 : SPDP_MINB; }
 
 template <int LPT, int KPL, bool DEBUG, typename NT, bool ASYNC = false>
 __global__ void __launch_bounds__(kWarps * 32, sample_minb<LPT, KPL>())
@@ -356,6 +359,9 @@ sample_kernel(SweepArgs A) {
     // skipping the loads of blocks past K saves bytes but changes register allocation and
     // scheduling; measured (B200): a gain at 4x32 and 16x32, a loss at 8x32 (C5) and 32x32 (K = 1000)
     constexpr bool kSkipPad = SPDP_SKIP_PAD_BLOCKS && (LPT == 4 || LPT == 16);
+    // per-block alpha sums: 2.5-3.5 % faster at C3, K = 300, K = 1000 (B200); not under the
+    // 5-blocks register cap of 8x32, where the 8 extra registers spill (C5 +2.7 %)
+    constexpr bool kBlockAlpha = SPDP_BLOCK_ALPHA != 0 && sample_minb<LPT, KPL>() <= 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
@@ -413,6 +419,14 @@ sample_kernel(SweepArgs A) {
         F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
     }
     const float* aFl = &S.aF[skew<KPL>(kb)];
+    float aSF[NB];                                   // per block: sum of alpha_ik F_k (SPDP_BLOCK_ALPHA)
+    if constexpr (kBlockAlpha) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
+            aSF[q] = (af.x + af.y) + (af.z + af.w);
+        }
+    }
     const uint32_t sweep = *A.sweep;
 
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
@@ -471,12 +485,20 @@ sample_kernel(SweepArgs A) {
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
-                const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
-                const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], af.x);
-                const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], af.y);
-                const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
-                const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
-                sb[q] = (w0 + w1) + (w2 + w3);
+                if constexpr (kBlockAlpha) {
+                    // no per-topic alpha term: 4 FFMA per block, no shared-memory load
+                    float x = __fmaf_rn(v[q].x, F[4 * q + 0], aSF[q]);
+                    x = __fmaf_rn(v[q].y, F[4 * q + 1], x);
+                    x = __fmaf_rn(v[q].z, F[4 * q + 2], x);
+                    sb[q] = __fmaf_rn(v[q].w, F[4 * q + 3], x);
+                } else {
+                    const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
+                    const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], af.x);
+                    const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], af.y);
+                    const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
+                    const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
+                    sb[q] = (w0 + w1) + (w2 + w3);
+                }
             }
             float lt32;                                    // tree sum of the block sums
             {
@@ -539,7 +561,8 @@ sample_kernel(SweepArgs A) {
                 float pre32 = 0.f;
 #pragma unroll
                 for (int q = 0; q < NB; ++q) if (q < qs) pre32 += bsv[q];
-                // the block's 4 topic masses, recomputed exactly as the dense pass did
+                // the block's 4 topic masses (their fp32 sum may differ from the dense pass's block
+                // sum by a few ulps; a target in that gap takes the last positive topic below)
                 const int kq = wg * KPL + 4 * qs;
                 int cs = 0;
 #pragma unroll
