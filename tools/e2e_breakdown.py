@@ -16,6 +16,8 @@ cfg = synth.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"]
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 c = synth.corpus_for(cfg)
 kw = dict(alpha=0.1, beta=0.1, discount=0.7, concentration=100.0, seed=7)
+if len(sys.argv) > 3 and sys.argv[3] == "async":
+    kw["update_mode"] = spdp.SPDP_UPDATE_ASYNC
 zr = torch.empty(c.num_tokens, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16)
 for rep in range(2):
     torch.cuda.synchronize()
