@@ -46,6 +46,16 @@ for rep in range(2):
         h.zr_async(zb[s % 2])
     h.wait()
     pipe = (time.perf_counter() - a) / steps
+    a = time.perf_counter()
+    for s in range(steps):
+        h.sweep(1)
+    sw_only = (time.perf_counter() - a) / steps
+    a = time.perf_counter()
+    for s in range(steps):
+        h.zr_async(zb[s % 2])
+        h.wait()
+    zr_only = (time.perf_counter() - a) / steps
+    print(f"   sweep alone {1e3*sw_only:.3f} ms; zr_async+wait alone {1e3*zr_only:.3f} ms")
     h.close()
     t.append(time.perf_counter())
     print(f"   one more sweep {1e3*first:.3f} ms; pipelined sweep+zr_async {1e3*pipe:.3f} ms/step")
