@@ -22,6 +22,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_BLOCK_ALPHA
 #define SPDP_BLOCK_ALPHA 1         // dense pass: block sum = sum_k n_k F_k + (sum_k alpha_k F_k), the latter per chunk
 #endif
+#ifndef SPDP_ROW_PIPELINE
+#define SPDP_ROW_PIPELINE 1        // dense pass: issue the next step's row loads once this step's block sums are formed
+#endif
 #ifndef SPDP_PREFETCH_NEXT
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
@@ -362,6 +365,9 @@ sample_kernel(SweepArgs A) {
     // per-block alpha sums: 2.5-3.5 % faster at C3, K = 300, K = 1000 (B200); not under the
     // 5-blocks register cap of 8x32, where the 8 extra registers spill (C5 +2.7 %)
     constexpr bool kBlockAlpha = SPDP_BLOCK_ALPHA != 0 && sample_minb<LPT, KPL>() <= 4;
+    // software-pipelined row loads: C3 -3 %, K = 300 -7 %, K = 1000 +-0 (B200); spills under the
+    // 8x32 register cap (C5 +30 %), so not there
+    constexpr bool kRowPipe = SPDP_ROW_PIPELINE != 0 && sample_minb<LPT, KPL>() <= 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
@@ -470,18 +476,22 @@ sample_kernel(SweepArgs A) {
         const float dlt = wnew - wold;
 
         // ======== phase 2: LPT lanes per token
-        for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
-            const uint32_t src = (s0 + g) & 31;
-            const uint32_t snoff = __shfl_sync(0xffffffffu, noff, src);
-            const int sk0 = __shfl_sync(0xffffffffu, k0, src);
-            const float sdlt = __shfl_sync(0xffffffffu, dlt, src);
-            const double su = __shfl_sync(0xffffffffu, u, src);
-            const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + snoff + 4 * gl;
-            float4 v[NB];
+        float4 v[NB];
+        auto load_rows = [&](uint32_t s) {            // the doc-topic rows of step s's tokens
+            const uint32_t so = __shfl_sync(0xffffffffu, noff, (s + g) & 31);
+            const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + so + 4 * gl;
 #pragma unroll
             for (int q = 0; q < NB; ++q)   // blocks past K hold no topic (zero mass): optionally no load
                 v[q] = (!kSkipPad || kb + 4 * q < K) ? row_load4<NT, ASYNC>(nl + 4 * A.colstart[q])
                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
+        if constexpr (kRowPipe) load_rows(0);
+        for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
+            const uint32_t src = (s0 + g) & 31;
+            const int sk0 = __shfl_sync(0xffffffffu, k0, src);
+            const float sdlt = __shfl_sync(0xffffffffu, dlt, src);
+            const double su = __shfl_sync(0xffffffffu, u, src);
+            if constexpr (!kRowPipe) load_rows(s0);
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
@@ -500,6 +510,8 @@ sample_kernel(SweepArgs A) {
                     sb[q] = (w0 + w1) + (w2 + w3);
                 }
             }
+            if constexpr (kRowPipe)
+                if (s0 + TPW < nb) load_rows(s0 + TPW);   // warp-uniform; overlaps the scan and hand-over below
             float lt32;                                    // tree sum of the block sums
             {
                 float t8[NB];
