@@ -1223,8 +1223,12 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
     }
     // small K: the token kernel (packed per-wave deltas need |delta| <= count(i,w) < 2^15)
-    // (64 < K <= 128: only with several waves, where the chunk kernel's segments get short)
-    c->token_kernel = !c->async && !c->sparse && c->mmax < 32768 && (c->K <= 64 || (c->K <= 128 && W > 1));
+    // (64 < K <= 128: only with several waves whose (w, i) segments hold < 32 tokens on average, where
+    // the chunk kernel cannot fill its chunks; B200: C3 W = 2 (42 per segment) 1.61 ms chunk vs 1.72
+    // token, C3 W = 3 (28) 2.04 vs 1.91, C4 K = 100 W = 2 (21) 1.20 vs 1.06)
+    const double seg_fill = (double)num_tokens / c->G / ((double)V * I * W);
+    c->token_kernel = !c->async && !c->sparse && c->mmax < 32768 &&
+                      (c->K <= 64 || (c->K <= 128 && W > 1 && seg_fill < 32.0));
     if (const char* e = getenv("SPDP_TOKEN_KERNEL")) {   // 0: never; 2: also K <= 128 with one wave
         const int v = atoi(e);
         if (v == 0) c->token_kernel = false;

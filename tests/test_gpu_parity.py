@@ -81,6 +81,22 @@ def test_topic_counts_edge_cases(K):
         assert_counts_equal(gc, o.state())
 
 
+@pytest.mark.parametrize("forced,waves", [("0", 2), ("2", 1)])
+def test_kernel_choice_override_lockstep(monkeypatch, forced, waves):
+    """Both sample paths at 64 < K <= 128 whatever the automatic choice (it
+    depends on the tokens per segment and wave): the chunk kernel with several
+    waves (SPDP_TOKEN_KERNEL=0) and the token kernel with one (=2) stay in
+    lock-step with the oracle."""
+    monkeypatch.setenv("SPDP_TOKEN_KERNEL", forced)
+    c = synth.generate(2, 40, 60.0, 200, 8, seed=5)
+    g, o = pair(c, 100, waves=waves)
+    assert g.stats()["token_kernel"] == (1 if forced == "2" else 0)
+    for _ in range(2):
+        rep, gc = lockstep_sweep(g, o, waves=waves)
+        assert_draw_parity(rep)
+        assert_counts_equal(gc, o.state())
+
+
 def test_tiny_and_degenerate_corpora():
     # single-token docs, a doc with one repeated word, unused words and groups
     c = synth.tiny_corpus(3, [[0], [1, 1, 1, 1], [2, 0, 2], [5]], [0, 0, 1, 1], vocab=7)
