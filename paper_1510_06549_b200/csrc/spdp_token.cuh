@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
         const uint32_t seg = A.run_seg[run];
         const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
         const uint32_t zr0 = A.zr[p];
+        const uint32_t doc = A.tok_doc[p];              // issued with the record: the row address is ready early
         const int k0 = (int)(zr0 & 0x7FFFu);
         const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);      // a2
         const size_t cell0 = (size_t)seg * Kp + k0;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
             const int32_t* Qw = A.Q + (size_t)w * Kp;
             float Fk0, R1k0;
             removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
-            const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[p] * Kp;
+            const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * Kp;
             const float* Frow = A.F + (size_t)run * Kp;
             const float* al = A.alpha + (size_t)i * Kp;
             // own topic: the after-removal mass replaces the snapshot mass (block sum + difference,
