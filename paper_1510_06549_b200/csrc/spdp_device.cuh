@@ -25,6 +25,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_ROW_PIPELINE
 #define SPDP_ROW_PIPELINE 1        // dense pass: issue the next step's row loads once this step's block sums are formed
 #endif
+#ifndef SPDP_PRE_TAB
+#define SPDP_PRE_TAB 1             // own-removal table entries (both r_rem candidates) loaded before the Philox rounds
+#endif
 #ifndef SPDP_PREFETCH_NEXT
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
@@ -134,6 +137,20 @@ __device__ __forceinline__ void removal_factors(int rrem, int mv, int tv, int Mv
         const int mm = mv - 1;
         if (rrem) slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, tab[tri(mm) + max(tv - 1, 0)], a, b, beta, vbeta, x0, x1);
         else slot_factors(Mv - 1, Ttv, Qv, Tv, tab[tri(mm) + min(tv, mm)], a, b, beta, vbeta, x0, x1);
+    }
+    Fsum = x0 + x1;
+    R1 = (x1 > 0.f) ? __fdiv_rn(x1, Fsum) : 0.f;
+}
+
+// removal_factors with both candidate table entries already loaded (issued before the token's
+// Philox, so the table latency overlaps it): A_r1 at (m-1, max(t-1, 0)), A_r0 at (m-1, min(t, m-1)).
+__device__ __forceinline__ void removal_factors_pre(int rrem, int mv, int Mv, int Ttv, int Qv, int Tv, float2 A_r1,
+                                                    float2 A_r0, float a, float b, float beta, float vbeta,
+                                                    float& Fsum, float& R1) {
+    float x0 = 0.f, x1 = 0.f;
+    if (mv > 0) {
+        if (rrem) slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, A_r1, a, b, beta, vbeta, x0, x1);
+        else slot_factors(Mv - 1, Ttv, Qv, Tv, A_r0, a, b, beta, vbeta, x0, x1);
     }
     Fsum = x0 + x1;
     R1 = (x1 > 0.f) ? __fdiv_rn(x1, Fsum) : 0.f;
@@ -368,6 +385,8 @@ sample_kernel(SweepArgs A) {
     // software-pipelined row loads: C3 -3 %, K = 300 -7 %, K = 1000 +-0 (B200); spills under the
     // 8x32 register cap (C5 +30 %), so not there
     constexpr bool kRowPipe = SPDP_ROW_PIPELINE != 0 && sample_minb<LPT, KPL>() <= 4;
+    // own-removal inputs before the Philox rounds: C3 -1 %, K = 300 -1.8 %, C5 (8x32) +1 % (B200)
+    constexpr bool kPreTab = SPDP_PRE_TAB != 0 && sample_minb<LPT, KPL>() <= 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
@@ -445,6 +464,23 @@ sample_kernel(SweepArgs A) {
         if (mine) {
             noff = A.tok_doc[p] * (uint32_t)Kp;            // doc-topic row offset (fits 32 bits)
             zr0 = A.zr[p];
+        }
+        // the own-removal inputs of topic k0 (both table candidates: r_rem is drawn below), issued
+        // before the Philox rounds so that their latency overlaps them
+        const int k0 = (int)(zr0 & 0x7FFFu);
+        const uint32_t mt0 = S.mt[k0];
+        const int m0 = (int)(mt0 >> 16), t0 = (int)(mt0 & 0xFFFFu);
+        const int mm0 = max(m0 - 1, 0);
+        float2 tab_r1 = make_float2(0.f, 0.f), tab_r0 = make_float2(0.f, 0.f);
+        int Mk0 = 0, Ttk0 = 0, Qk0 = 0, Tk0 = 0;
+        if constexpr (kPreTab) {
+            if (mine) {
+                tab_r1 = tab[tri(mm0) + max(t0 - 1, 0)];
+                tab_r0 = tab[tri(mm0) + min(t0, mm0)];
+                Mk0 = ldc<ASYNC>(Mi + k0); Ttk0 = ldc<ASYNC>(Tti + k0); Qk0 = ldc<ASYNC>(Qw + k0); Tk0 = ldc<ASYNC>(A.T + k0);
+            }
+        }
+        if (mine) {
             const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);   // a2
             x0 = x.x;
             u = u53(x);
@@ -460,14 +496,15 @@ sample_kernel(SweepArgs A) {
                 for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
             }
         }
-        const int k0 = (int)(zr0 & 0x7FFFu);
-        const uint32_t mt0 = S.mt[k0];
-        const int m0 = (int)(mt0 >> 16), t0 = (int)(mt0 & 0xFFFFu);
         const int rrem = removal_draw(x0, m0, t0);                                            // a3
         const bool keep = rrem && t0 == 1 && m0 > 1;   // DESIGN.md reading c5
         float Fk0 = 0.f, R1k0 = 0.f;                    // topic k0's factors after the own removal
-        if (mine) removal_factors(rrem, m0, t0, ldc<ASYNC>(Mi + k0), ldc<ASYNC>(Tti + k0), ldc<ASYNC>(Qw + k0),
-                                  ldc<ASYNC>(A.T + k0), tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        if constexpr (kPreTab) {
+            if (mine) removal_factors_pre(rrem, m0, Mk0, Ttk0, Qk0, Tk0, tab_r1, tab_r0, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        } else {
+            if (mine) removal_factors(rrem, m0, t0, ldc<ASYNC>(Mi + k0), ldc<ASYNC>(Tti + k0), ldc<ASYNC>(Qw + k0),
+                                      ldc<ASYNC>(A.T + k0), tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        }
         float n0 = mine ? row_load1<NT, ASYNC>(nrow + A.sigma[k0]) : 0.f;
         if constexpr (ASYNC) n0 = fmaxf(n0, 1.f);    // the token itself is counted in its row
         const float al0 = alpha_i[k0];
