@@ -150,6 +150,39 @@ def load_traffic(cfg_name, K, kernel="sample"):
     return ncu_summary(cfg_name, K, kernel).get("dram_bytes_per_launch")
 
 
+class LoadPhases:
+    """Captures spdp_load_corpus's SPDP_VERBOSE phase times (written by the library to fd 2)
+    for the JSON line: where the e2e setup time goes."""
+
+    def __enter__(self):
+        import tempfile
+        self.ms = {}
+        self.prev = os.environ.get("SPDP_VERBOSE")
+        os.environ["SPDP_VERBOSE"] = "1"
+        sys.stderr.flush()
+        self.tmp = tempfile.TemporaryFile(mode="w+b")
+        self.saved = os.dup(2)
+        os.dup2(self.tmp.fileno(), 2)
+        return self
+
+    def __exit__(self, *a):
+        os.dup2(self.saved, 2)
+        os.close(self.saved)
+        if self.prev is None:
+            os.environ.pop("SPDP_VERBOSE", None)
+        else:
+            os.environ["SPDP_VERBOSE"] = self.prev
+        self.tmp.seek(0)
+        for line in self.tmp.read().decode(errors="replace").splitlines():
+            if line.startswith("[spdp] load "):
+                name, _, val = line[len("[spdp] load "):].rpartition("  ")
+                try:
+                    self.ms[name.strip()] = float(val.strip().split()[0])
+                except ValueError:
+                    pass
+        self.tmp.close()
+
+
 def cpu_baseline(corpus, cfg, K, waves, sample_tokens):
     """The oracle as it stands, single thread, on a bounded sample of the same
     workload: the first `sample_tokens` tokens of one mode-P sweep."""
@@ -321,9 +354,11 @@ def main():
     t_pin = time.perf_counter() - t_pin
     t0 = time.perf_counter()
     h = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
+    t_create = time.perf_counter() - t0
     if transform is not None:
         h.set_transform(*transform)
-    h.load_corpus(hin[0], hin[1], hin[2], corpus.num_docs)     # H2D of the job's inputs (pinned)
+    with LoadPhases() as phases:                                 # the library's own phase timer (stderr)
+        h.load_corpus(hin[0], hin[1], hin[2], corpus.num_docs)     # H2D of the job's inputs (pinned)
     t_setup = time.perf_counter() - t0
     for s in range(e2e_steps):
         h.sweep(1)
@@ -337,7 +372,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h.close()
-    e2e = {"value": N * e2e_steps / e2e_s, "unit": "tokens/s", "setup_ms": round(t_setup * 1e3, 2),
+    e2e = {"value": N * e2e_steps / e2e_s, "unit": "tokens/s", "setup_ms": round(t_setup * 1e3, 2), "create_ms": round(t_create * 1e3, 2),
+           "load_phases_ms": phases.ms,
            "host_buffer_pin_ms_untimed": round(t_pin * 1e3, 2),
            "ms_per_step_after_setup": round((e2e_s - t_setup) * 1e3 / e2e_steps, 4),
            "h2d_bytes_per_step": int(N * 12 / e2e_steps), "d2h_bytes_per_step": int(plan["tokens"] * 2),
