@@ -109,11 +109,13 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def alg_bytes(plan, K):
+def alg_bytes(plan, K, row_bytes=4):
     """Algorithmic HBM bytes of one sample-kernel pass:
-    per token 12 B of token record (doc, id, zr in; zr out) + 4K B doc-topic row;
+    per token 12 B of token record (doc, id, zr in; zr out) + row_bytes*K B doc-topic row
+    (4: the canonical int32 model of SURVEY §8(d); 2: the uint16 rows the library stores when
+    the doc-topic array exceeds half of L2, i.e. the bytes the kernel actually has to move);
     per (w, i) segment 28K B (m, t, Q rows, A0/A1 table row in; dm, dt rows out)."""
-    return plan["tokens"] * (12 + 4 * K) + plan["segments"] * 28 * K
+    return plan["tokens"] * (12 + row_bytes * K) + plan["segments"] * 28 * K
 
 
 def plan_stats(corpus, shard_docs, waves):
@@ -328,7 +330,9 @@ def main():
     plan = plan_stats(corpus, shard_docs, args.waves)
     peak, peak_src = measured_peaks()
     sample_ms = tm["sample_ms"] / max(tm["sweeps"], 1)       # per sweep (all waves), from the profiled pass
-    bytes_sweep = alg_bytes(plan, K)
+    row_bytes = 2 if stats.get("row16") else 4
+    bytes_sweep = alg_bytes(plan, K, row_bytes)                 # the bytes this kernel has to move
+    bytes_i32 = alg_bytes(plan, K, 4)                           # SURVEY §8(d)'s canonical int32 model
     achieved = bytes_sweep / (sample_ms / 1e3) / 1e9
     kname = "sp_token_kernel" if transform is not None else ("token_kernel" if stats.get("token_kernel") else "sample_kernel")
     pkey = kname.split("_")[0] + ("_async" if args.update == "async" else "")   # which committed ncu capture
@@ -336,7 +340,15 @@ def main():
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kname,
             "alg_bytes_per_launch": int(bytes_sweep / max(args.waves, 1)), "peak_source": peak_src,
+            "doc_topic_row_bytes_per_topic": row_bytes,
+            "int32_model": {"alg_bytes_per_launch": int(bytes_i32 / max(args.waves, 1)),
+                            "achieved": round(bytes_i32 / (sample_ms / 1e3) / 1e9, 1),
+                            "frac": round(bytes_i32 / (sample_ms / 1e3) / 1e9 / peak, 4)},
             "sample_ms_per_sweep": round(sample_ms, 4), "share_of_step": round(sample_ms / ms, 3)}
+    if traffic:   # measured DRAM bytes (committed ncu capture) over this run's kernel time
+        roof["traffic_source"] = "committed ncu --set full capture (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+        roof["dram_achieved"] = round(traffic / (sample_ms / max(args.waves, 1) / 1e3) / 1e9, 1)
+        roof["dram_frac"] = round(roof["dram_achieved"] / peak, 4)
     nc = ncu_summary(cfg.name, K, pkey)
     if nc:   # what actually limits the kernel (from the committed ncu capture, not this run)
         roof["ncu"] = {k: nc.get(k) for k in ("file", "l2_hit_pct", "l1_pct_of_peak", "issue_active_pct",

@@ -300,6 +300,16 @@ spdp_status spdp_sparse_state(spdp_ctx* ctx, int32_t* q, int32_t* shadow, int16_
  * r_new}.  No state change.  SPDP_EINVAL for tokens of other ranks. */
 spdp_status spdp_debug_probs(spdp_ctx* ctx, int64_t n, const int64_t* tok_ids, double* probs, int32_t* info);
 
+/* Diagnostics (parity tests, SURVEY §8(c) "A0/A1 folding" pin): the device
+ * Stirling-ratio table of group `group` (one per distinct discount a_i),
+ * A0(m,t) = (m-t+1)/(m+1) S^{m+1}_t / S^m_t (Eq. r0) and
+ * A1(m,t) = (t+1)/(m+1) S^{m+1}_{t+1} / S^m_t (Eq. r1), with
+ * S from the recursion PAPER.md:1454-1455, exactly as the sweep reads it.
+ * out [(mmax+1)(mmax+2)/2 * 2] fp32, pairs (A0, A1) at index m(m+1)/2 + t for
+ * 0 <= t <= m <= mmax (t = 0 < m is not a state and holds 0).  mmax <= the
+ * table's M_max (stats out[6]), else SPDP_EINVAL.  No state change. */
+spdp_status spdp_debug_ratio_table(spdp_ctx* ctx, int32_t group, int32_t mmax, float* out);
+
 /* Counters of the last sweep on this rank: out[0] keeps, out[1] moved
  * tokens, out[2] clamped cells, out[3] sweeps done, out[4] local tokens,
  * out[5] local docs, out[6] M_max (largest count(i,w)), out[7] chunks,

@@ -42,6 +42,8 @@ def lib():
         L.or_philox.argtypes = [P, P, P]
         L.or_log_stirling.restype = C.c_double
         L.or_log_stirling.argtypes = [C.c_double, C.c_int, C.c_int]
+        L.or_ratio_table.restype = C.c_int
+        L.or_ratio_table.argtypes = [C.c_double, C.c_int, P, P]
         L.or_create.restype = P
         L.or_create.argtypes = [C.c_int, C.c_int, C.c_int, P, C.c_double, P, P, C.c_uint64]
         L.or_destroy.argtypes = [P]
@@ -126,6 +128,15 @@ def philox(ctr, key):
     c = np.asarray(ctr, np.uint32); k = np.asarray(key, np.uint32); out = np.zeros(4, np.uint32)
     lib().or_philox(_ptr(c), _ptr(k), _ptr(out))
     return out
+
+
+def ratio_table(a: float, mmax: int):
+    """(A0, A1) fp64 at m(m+1)/2 + t, 0 <= t <= m <= mmax (spdp_oracle.c or_ratio_table)."""
+    n = (mmax + 1) * (mmax + 2) // 2
+    A0, A1 = np.zeros(n), np.zeros(n)
+    if lib().or_ratio_table(float(a), int(mmax), _ptr(A0), _ptr(A1)) != 0:
+        raise MemoryError("or_ratio_table")
+    return A0, A1
 
 
 def log_stirling(a: float, n: int, m: int) -> float:

@@ -125,6 +125,27 @@ double or_log_stirling(double a, int N, int M) {
     return r;
 }
 
+/* The Stirling ratios the conditional of Eqs. r0/r1 multiplies
+ * by, written out from the log table above:
+ *   A0(m,t) = (m-t+1)/(m+1) * S^{m+1}_t / S^m_t        (r = 0, Eq. r0)
+ *   A1(m,t) = (t+1)/(m+1)   * S^{m+1}_{t+1} / S^m_t    (r = 1, Eq. r1)
+ * for 0 <= t <= m <= mmax at index m(m+1)/2 + t.  t = 0 < m (S^m_0 = 0) is not
+ * a state and gets 0.  Returns 0, or -1 if the table cannot be allocated. */
+int or_ratio_table(double a, int mmax, double *A0, double *A1) {
+    stable_t S;
+    if (mmax < 0 || stable_build(&S, a, mmax + 1) != 0) return -1;
+    for (int m = 0; m <= mmax; m++)
+        for (int t = 0; t <= m; t++) {
+            size_t j = (size_t)m * (m + 1) / 2 + t;
+            double lS = stable_get(&S, m, t);
+            if (lS == -INFINITY) { A0[j] = 0.0; A1[j] = 0.0; continue; }
+            A0[j] = (double)(m - t + 1) / (double)(m + 1) * exp(stable_get(&S, m + 1, t) - lS);
+            A1[j] = (double)(t + 1) / (double)(m + 1) * exp(stable_get(&S, m + 1, t + 1) - lS);
+        }
+    free(S.v);
+    return 0;
+}
+
 /* ln (x|y)_n = sum_{j<n} ln(x + j y) */
 static double log_poch(double x, double y, int64_t n) {
     double s = 0.0;

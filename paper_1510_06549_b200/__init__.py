@@ -11,6 +11,7 @@ library is missing or cannot be loaded.
 from __future__ import annotations
 
 import ctypes as C
+import glob
 import os
 import subprocess
 
@@ -19,7 +20,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.environ.get("SPDP_LIB") or os.path.join(_HERE, "libspdp.so")   # SPDP_LIB: tuning variants
-_SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("spdp.cu", "spdp_device.cuh", "spdp_loglik.cuh", "spdp_eval.cuh", "spdp_plan.cuh", "spdp_token.cuh")] + [
+# every source the library is compiled from (spdp.cu includes the headers): a change to any of them rebuilds it
+_SOURCES = sorted(glob.glob(os.path.join(_HERE, "csrc", "*.cu")) + glob.glob(os.path.join(_HERE, "csrc", "*.cuh"))) + [
     os.path.join(_ROOT, "include", "spdp.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -36,7 +38,7 @@ EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "s
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
            "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr",
-           "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait"]
+           "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait", "spdp_debug_ratio_table"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -87,6 +89,7 @@ def lib():
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
             "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_zr_async": [P, P], "spdp_wait": [P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
+            "spdp_debug_ratio_table": [P, I32, I32, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -275,6 +278,13 @@ def spdp_debug_probs(ctx, tok_ids, K):
     return probs, info
 
 
+def spdp_debug_ratio_table(ctx, group, mmax):
+    """The device A0/A1 table of a group: (A0, A1) fp32 arrays at m(m+1)/2 + t, m <= mmax."""
+    out = np.zeros(((mmax + 1) * (mmax + 2) // 2, 2), np.float32)
+    _check(lib().spdp_debug_ratio_table(ctx, int(group), int(mmax), _p(out)), ctx)
+    return out[:, 0], out[:, 1]
+
+
 def spdp_stats(ctx):
     out = np.zeros(16, np.int64)
     _check(lib().spdp_stats(ctx, _p(out)), ctx)
@@ -384,6 +394,9 @@ class Sampler:
 
     def debug_probs(self, tok_ids):
         return spdp_debug_probs(self.ctx, tok_ids, self.K)
+
+    def debug_ratio_table(self, group, mmax):
+        return spdp_debug_ratio_table(self.ctx, group, mmax)
 
     def topics(self, phi0=True, phi=True):
         return spdp_topics(self.ctx, self.I, self.V, self.K, phi0, phi)

@@ -2171,6 +2171,17 @@ spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t
     return SPDP_OK;
 }
 
+spdp_status spdp_debug_ratio_table(spdp_ctx* c, int32_t group, int32_t mmax, float* out) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (group < 0 || group >= c->I || mmax < 0 || mmax > c->mmax || !out)
+        return fail(c, SPDP_EINVAL, "bad debug_ratio_table arguments (group %d, mmax %d > M_max %d?)", group, mmax, c->mmax);
+    const size_t cnt = (size_t)(mmax + 1) * (size_t)(mmax + 2) / 2;
+    CU(cudaMemcpyAsync(out, c->d_tab + c->tab_off_host[(size_t)group], sizeof(float2) * cnt, cudaMemcpyDeviceToHost,
+                       c->stream));
+    return sync(c, "debug_ratio_table");
+}
+
 spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, double* probs, int32_t* info) {
     spdp_status s = guard(c, true);
     if (s) return s;
@@ -2297,12 +2308,17 @@ void spdp_destroy(spdp_ctx* c) {
 }  // extern "C"
 
 namespace {
-// debug_checks: recount n and m from z, check 0 <= t <= m, t > 0 iff m > 0, Q = sum_i t.
+// debug_checks: n and m recounted from z equal the maintained
+// tables (m gathered over the ranks with an NCCL sum; an external exchange cannot be
+// gathered here, so there m is checked through its sums only); 0 <= t <= m and
+// t > 0 iff m > 0; Q = sum_i t (identity P); M = sum_w m, Tt = sum_w t, T = sum_w Q;
+// sum m = N.
 spdp_status debug_verify(spdp_ctx* c) {
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     std::vector<uint16_t> zr((size_t)c->Nloc);
     std::vector<float> nf;
     std::vector<int32_t> n((size_t)c->Dloc * Kp), m(c->cells), t(c->cells), Q((size_t)V * Kp);
+    std::vector<int32_t> M((size_t)I * Kp), Tt((size_t)I * Kp), T((size_t)Kp);
     {
         spdp_status s0 = ensure_host_plan(c);
         if (s0) return s0;
@@ -2317,26 +2333,68 @@ spdp_status debug_verify(spdp_ctx* c) {
     CU(cudaMemcpy(m.data(), c->d_m, 4 * m.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(t.data(), c->d_t, 4 * t.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(Q.data(), c->d_Q, 4 * Q.size(), cudaMemcpyDeviceToHost));
-    std::vector<int32_t> n2((size_t)c->Dloc * Kp, 0);
+    CU(cudaMemcpy(M.data(), c->d_M, 4 * M.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(Tt.data(), c->d_Tt, 4 * Tt.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(T.data(), c->d_T, 4 * T.size(), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> n2((size_t)c->Dloc * Kp, 0), m2(c->cells, 0);
     for (int64_t q = 0; q < c->Nloc; ++q) {
         const uint32_t p = c->sorted_tok[(size_t)q];
-        n2[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + (zr[(size_t)q] & 0x7FFF)]++;
+        const int k = zr[(size_t)q] & 0x7FFF;
+        if (k >= K) return fail(c, SPDP_EINTEGRITY, "topic %d out of range at token %u", k, p);
+        n2[(size_t)c->local_of_doc[(size_t)c->doc[p]] * Kp + k]++;
+        m2[((size_t)c->word[p] * I + (size_t)c->group[p]) * Kp + k]++;
     }
     if (n2 != n) return fail(c, SPDP_EINTEGRITY, "doc-topic counts differ from a recount of z");
+    bool m_checked = c->G == 1;
+    if (c->G > 1 && c->comm) {   // every rank's recount, summed
+        TempBuf<int32_t> tb(c->cells);
+        if (!tb.p) return fail(c, SPDP_ENOMEM, "debug_verify buffer");
+        CU(cudaMemcpyAsync(tb.p, m2.data(), 4 * m2.size(), cudaMemcpyHostToDevice, c->stream));
+        spdp_status s0 = nccl_check(c, c->nccl.AllReduce(tb.p, tb.p, c->cells, kNcclInt32, kNcclSum, c->comm, c->stream),
+                                    "allreduce m recount");
+        if (s0) return s0;
+        CU(cudaMemcpyAsync(m2.data(), tb.p, 4 * m2.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s0 = sync(c, "debug_verify"))) return s0;
+        m_checked = true;
+    }
+    if (m_checked && m2 != m) {
+        for (size_t j = 0; j < c->cells; ++j)
+            if (m2[j] != m[j]) {
+                const size_t k = j % Kp, wi = j / Kp;
+                return fail(c, SPDP_EINTEGRITY, "customer count m differs from a recount of z at (i=%d, w=%d, k=%d): %d vs %d",
+                            (int)(wi % I), (int)(wi / I), (int)k, m[j], m2[j]);
+            }
+    }
+    std::vector<int64_t> M2((size_t)I * Kp, 0), Tt2((size_t)I * Kp, 0), T2((size_t)Kp, 0);
     int64_t sm = 0;
     for (int w = 0; w < V; ++w)
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < Kp; ++k) {
             int64_t q = 0;
             for (int i = 0; i < I; ++i) {
                 const size_t cell = ((size_t)w * I + i) * Kp + k;
+                if (k >= K) {
+                    if (m[cell] || t[cell]) return fail(c, SPDP_EINTEGRITY, "nonzero padding cell at (i=%d, w=%d)", i, w);
+                    continue;
+                }
                 if (t[cell] < 0 || t[cell] > m[cell] || ((t[cell] > 0) != (m[cell] > 0)))
                     return fail(c, SPDP_EINTEGRITY, "t out of [min(1,m), m] at (i=%d, w=%d, k=%d)", i, w, k);
                 q += t[cell];
                 sm += m[cell];
+                M2[(size_t)i * Kp + k] += m[cell];
+                Tt2[(size_t)i * Kp + k] += t[cell];
             }
-            if (q != Q[(size_t)w * Kp + k]) return fail(c, SPDP_EINTEGRITY, "Q != sum_i t at (w=%d, k=%d)", w, k);
+            if (!c->sparse && q != Q[(size_t)w * Kp + k]) return fail(c, SPDP_EINTEGRITY, "Q != sum_i t at (w=%d, k=%d)", w, k);
+            T2[(size_t)k] += Q[(size_t)w * Kp + k];
         }
-    if (c->G == 1 && sm != c->N) return fail(c, SPDP_EINTEGRITY, "sum m = %lld != N", (long long)sm);
+    for (int i = 0; i < I; ++i)
+        for (int k = 0; k < K; ++k) {
+            const size_t j = (size_t)i * Kp + k;
+            if (M2[j] != M[j]) return fail(c, SPDP_EINTEGRITY, "M != sum_w m at (i=%d, k=%d)", i, k);
+            if (Tt2[j] != Tt[j]) return fail(c, SPDP_EINTEGRITY, "Tt != sum_w t at (i=%d, k=%d)", i, k);
+        }
+    for (int k = 0; k < K; ++k)
+        if (T2[(size_t)k] != T[(size_t)k]) return fail(c, SPDP_EINTEGRITY, "T != sum_w Q at k=%d", k);
+    if (sm != c->N) return fail(c, SPDP_EINTEGRITY, "sum m = %lld != N", (long long)sm);
     return SPDP_OK;
 }
 }  // namespace

@@ -219,6 +219,18 @@ __device__ __forceinline__ int ldc(const int32_t* p) {   // count read: snapshot
     else return *p;
 }
 
+// The marginal counts of topic k that a token's factors read: M_ik, Tt_ik, Q_kw, T_k.  In the
+// async mode they are live and may be transiently out of range (another chunk's changes land
+// cell by cell), so the local copy is corrected into the range the segment's own (clamped)
+// cell (m, t) implies (Alg.4 "correct local counts copied ... to ensure they are in valid
+// range"): M >= m, Tt >= t, Q >= t, T >= Q.  Wave mode reads a consistent snapshot: no-op.
+template <bool AS>
+__device__ __forceinline__ void load_sums(const int32_t* Mi, const int32_t* Tti, const int32_t* Qw, const int32_t* T,
+                                          int k, int mv, int tv, int& Mv, int& Ttv, int& Qv, int& Tv) {
+    Mv = ldc<AS>(Mi + k); Ttv = ldc<AS>(Tti + k); Qv = ldc<AS>(Qw + k); Tv = ldc<AS>(T + k);
+    if constexpr (AS) { Mv = max(Mv, mv); Ttv = max(Ttv, tv); Qv = max(Qv, tv); Tv = max(Tv, Qv); }
+}
+
 template <>
 struct Row<float> {
     __device__ __forceinline__ static float4 load4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
@@ -426,8 +438,9 @@ sample_kernel(SweepArgs A) {
                 tv = mv > 0 ? min(max(tv, 1), mv) : 0;
             }
             al = alpha_i[k];
-            slot_factors(ldc<ASYNC>(Mi + k), ldc<ASYNC>(Tti + k), ldc<ASYNC>(Qw + k), ldc<ASYNC>(A.T + k),
-                         tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+            int Mv, Ttv, Qv, Tv;
+            load_sums<ASYNC>(Mi, Tti, Qw, A.T, k, mv, tv, Mv, Ttv, Qv, Tv);
+            slot_factors(Mv, Ttv, Qv, Tv, tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
         }
         const float Fk = F0 + F1;
         S.F[k] = Fk;
@@ -477,7 +490,7 @@ sample_kernel(SweepArgs A) {
             if (mine) {
                 tab_r1 = tab[tri(mm0) + max(t0 - 1, 0)];
                 tab_r0 = tab[tri(mm0) + min(t0, mm0)];
-                Mk0 = ldc<ASYNC>(Mi + k0); Ttk0 = ldc<ASYNC>(Tti + k0); Qk0 = ldc<ASYNC>(Qw + k0); Tk0 = ldc<ASYNC>(A.T + k0);
+                load_sums<ASYNC>(Mi, Tti, Qw, A.T, k0, m0, t0, Mk0, Ttk0, Qk0, Tk0);
             }
         }
         if (mine) {
@@ -502,8 +515,10 @@ sample_kernel(SweepArgs A) {
         if constexpr (kPreTab) {
             if (mine) removal_factors_pre(rrem, m0, Mk0, Ttk0, Qk0, Tk0, tab_r1, tab_r0, a, b, A.beta, A.vbeta, Fk0, R1k0);
         } else {
-            if (mine) removal_factors(rrem, m0, t0, ldc<ASYNC>(Mi + k0), ldc<ASYNC>(Tti + k0), ldc<ASYNC>(Qw + k0),
-                                      ldc<ASYNC>(A.T + k0), tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+            if (mine) {
+                load_sums<ASYNC>(Mi, Tti, Qw, A.T, k0, m0, t0, Mk0, Ttk0, Qk0, Tk0);
+                removal_factors(rrem, m0, t0, Mk0, Ttk0, Qk0, Tk0, tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+            }
         }
         float n0 = mine ? row_load1<NT, ASYNC>(nrow + A.sigma[k0]) : 0.f;
         if constexpr (ASYNC) n0 = fmaxf(n0, 1.f);    // the token itself is counted in its row
@@ -642,8 +657,9 @@ sample_kernel(SweepArgs A) {
                 float R1s = R1k0;
                 if (!own) {                                // r = 1 share of topic ks at the snapshot
                     float f0, f1;
-                    slot_factors(ldc<ASYNC>(Mi + ks), ldc<ASYNC>(Tti + ks), ldc<ASYNC>(Qw + ks), ldc<ASYNC>(A.T + ks),
-                                 tab[tri((int)(mts >> 16)) + (mts & 0xFFFFu)], a, b, A.beta, A.vbeta, f0, f1);
+                    int Ms, Tts, Qs, Ts;
+                    load_sums<ASYNC>(Mi, Tti, Qw, A.T, ks, (int)(mts >> 16), (int)(mts & 0xFFFFu), Ms, Tts, Qs, Ts);
+                    slot_factors(Ms, Tts, Qs, Ts, tab[tri((int)(mts >> 16)) + (mts & 0xFFFFu)], a, b, A.beta, A.vbeta, f0, f1);
                     R1s = (f1 > 0.f) ? __fdiv_rn(f1, f0 + f1) : 0.f;
                 }
                 const float w1 = wsel * R1s;

@@ -28,7 +28,7 @@ _lib = None
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", _SRC, "-o", _LIB, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC", _SRC, "-o", _LIB, "-lm"])
     return _LIB
 
 
@@ -38,11 +38,11 @@ def _load():
         build()
         lib = ctypes.CDLL(_LIB)
         lib.synth_num_tokens.restype = ctypes.c_int64
-        lib.synth_num_tokens.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint64]
+        lib.synth_num_tokens.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_uint64, ctypes.c_int]
         lib.synth_spdp_corpus.restype = ctypes.c_int
         lib.synth_spdp_corpus.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
-                                          ctypes.c_uint64] + [ctypes.c_void_p] * 4
+                                          ctypes.c_uint64, ctypes.c_int] + [ctypes.c_void_p] * 4
         _lib = lib
     return _lib
 
@@ -67,6 +67,8 @@ class CorpusConfig:
     # generator hyper-parameters
     alpha_gen: float = 0.1
     beta_gen: float = 0.1
+    # one generator per document / topic / restaurant, drawn in parallel (synth/gen.c per_unit)
+    per_unit_streams: bool = False
 
     def with_k(self, k: int) -> "CorpusConfig":
         return replace(self, k=k, name=f"{self.name}_K{k}")
@@ -77,7 +79,9 @@ CONFIGS = {
     "C2": CorpusConfig("C2", 3, 3_000, 111.0, 10_000, 50, 50, 102, sweeps=20),
     "C3": CorpusConfig("C3", 4, 20_000, 125.0, 30_000, 100, 100, 103, sweeps=20),
     "C4": CorpusConfig("C4", 4, 10_000, 125.0, 30_000, 100, 100, 104, sweeps=10),
-    "C5": CorpusConfig("C5", 16, 200_000, 62.5, 100_000, 200, 200, 105, sweeps=10),
+    # C5 (~200 M tokens) is drawn with per-unit generator streams, in parallel (round 2; round 1's C5
+    # used the single-stream draw, ~110 s on 8 cores: same process and shape, a different draw)
+    "C5": CorpusConfig("C5", 16, 200_000, 62.5, 100_000, 200, 200, 105, sweeps=10, per_unit_streams=True),
 }
 
 
@@ -98,14 +102,14 @@ class Corpus:
 
 def generate(groups: int, docs_per_group: int, mean_len: float, vocab: int, k_gen: int,
              seed: int, alpha_gen: float = 0.1, beta_gen: float = 0.1,
-             discount: float = 0.7, concentration: float = 100.0) -> Corpus:
+             discount: float = 0.7, concentration: float = 100.0, per_unit_streams: bool = False) -> Corpus:
     lib = _load()
-    n = lib.synth_num_tokens(groups, docs_per_group, mean_len, seed)
+    n = lib.synth_num_tokens(groups, docs_per_group, mean_len, seed, int(per_unit_streams))
     if n < 0:
         raise MemoryError("synth_num_tokens failed")
     g = np.empty(n, np.int32); d = np.empty(n, np.int32); w = np.empty(n, np.int32); z = np.empty(n, np.int32)
     rc = lib.synth_spdp_corpus(groups, docs_per_group, mean_len, vocab, k_gen, alpha_gen, beta_gen,
-                               discount, concentration, seed,
+                               discount, concentration, seed, int(per_unit_streams),
                                g.ctypes.data, d.ctypes.data, w.ctypes.data, z.ctypes.data)
     if rc != 0:
         raise MemoryError("synth_spdp_corpus failed")
@@ -114,7 +118,7 @@ def generate(groups: int, docs_per_group: int, mean_len: float, vocab: int, k_ge
 
 def corpus_for(cfg: CorpusConfig) -> Corpus:
     return generate(cfg.groups, cfg.docs_per_group, cfg.mean_len, cfg.vocab, cfg.k_gen, cfg.gen_seed,
-                    cfg.alpha_gen, cfg.beta_gen, cfg.discount, cfg.concentration)
+                    cfg.alpha_gen, cfg.beta_gen, cfg.discount, cfg.concentration, cfg.per_unit_streams)
 
 
 def tiny_corpus(groups: int, docs: list[list[int]], doc_group: list[int], vocab: int) -> Corpus:

@@ -20,6 +20,13 @@
  * Streams (independent xoshiro256** generators seeded by splitmix64 of
  * (seed, stream)):  0 = document lengths, 1 = phi0, 2 = theta and z,
  * 3 = restaurant seating / words.
+ *
+ * per_unit != 0 (the ~200 M-token C5): one generator per unit instead — per
+ * document for its length and for theta_d, z (streams 0, 2), per topic for
+ * phi0_k (stream 1), per restaurant (group, topic) for its words (stream 3) —
+ * seeded by (seed, stream, unit), so the units are drawn in parallel (OpenMP)
+ * and the corpus does not depend on the thread count.  Same generative
+ * process, a different (equally distributed) draw than per_unit = 0.
  */
 #include <math.h>
 #include <stdint.h>
@@ -36,6 +43,11 @@ static uint64_t splitmix64(uint64_t *x) {
 }
 static void xo_seed(xo_t *g, uint64_t seed, uint64_t stream) {
     uint64_t x = seed * 0x2545F4914F6CDD1Dull + stream * 0x9E3779B97F4A7C15ull + 0x1234567ull;
+    for (int i = 0; i < 4; i++) g->s[i] = splitmix64(&x);
+}
+static void xo_seed_unit(xo_t *g, uint64_t seed, uint64_t stream, uint64_t unit) {
+    uint64_t x = seed * 0x2545F4914F6CDD1Dull + stream * 0x9E3779B97F4A7C15ull + 0x1234567ull;
+    x = splitmix64(&x) ^ (unit * 0xD6E8FEB86659FD93ull);
     for (int i = 0; i < 4; i++) g->s[i] = splitmix64(&x);
 }
 static inline uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
@@ -88,9 +100,18 @@ static int cdf_search(const double *cdf, int n, double u) {
     return lo;
 }
 
-static void doc_lengths(int I, int docs_per_group, double lambda, uint64_t seed, int32_t *len) {
-    xo_t g; xo_seed(&g, seed, 0);
+static void doc_lengths(int I, int docs_per_group, double lambda, uint64_t seed, int per_unit, int32_t *len) {
     int64_t D = (int64_t)I * docs_per_group;
+    if (per_unit) {
+        #pragma omp parallel for schedule(static)
+        for (int64_t d = 0; d < D; d++) {
+            xo_t g; xo_seed_unit(&g, seed, 0, (uint64_t)d);
+            int64_t L = xo_poisson(&g, lambda);
+            len[d] = (int32_t)(L < 1 ? 1 : L);
+        }
+        return;
+    }
+    xo_t g; xo_seed(&g, seed, 0);
     for (int64_t d = 0; d < D; d++) {
         int64_t L = xo_poisson(&g, lambda);
         len[d] = (int32_t)(L < 1 ? 1 : L);
@@ -98,11 +119,11 @@ static void doc_lengths(int I, int docs_per_group, double lambda, uint64_t seed,
 }
 
 /* Number of tokens the corpus with these parameters will have. */
-int64_t synth_num_tokens(int I, int docs_per_group, double lambda, uint64_t seed) {
+int64_t synth_num_tokens(int I, int docs_per_group, double lambda, uint64_t seed, int per_unit) {
     int64_t D = (int64_t)I * docs_per_group, N = 0;
     int32_t *len = (int32_t *)malloc(sizeof(int32_t) * (size_t)D);
     if (!len) return -1;
-    doc_lengths(I, docs_per_group, lambda, seed, len);
+    doc_lengths(I, docs_per_group, lambda, seed, per_unit, len);
     for (int64_t d = 0; d < D; d++) N += len[d];
     free(len);
     return N;
@@ -110,9 +131,16 @@ int64_t synth_num_tokens(int I, int docs_per_group, double lambda, uint64_t seed
 
 /* Fill group/doc/word (and the generating topic z_gen, may be NULL) for the
  * N = synth_num_tokens(...) tokens.  Returns 0 on success. */
+static int spdp_corpus_per_unit(int I, int docs_per_group, double lambda, int V, int K_gen,
+                                double alpha_gen, double beta_gen, double a, double b, uint64_t seed,
+                                int32_t *group, int32_t *doc, int32_t *word, int32_t *z_gen);
+
 int synth_spdp_corpus(int I, int docs_per_group, double lambda, int V, int K_gen,
-                      double alpha_gen, double beta_gen, double a, double b, uint64_t seed,
+                      double alpha_gen, double beta_gen, double a, double b, uint64_t seed, int per_unit,
                       int32_t *group, int32_t *doc, int32_t *word, int32_t *z_gen) {
+    if (per_unit)
+        return spdp_corpus_per_unit(I, docs_per_group, lambda, V, K_gen, alpha_gen, beta_gen, a, b, seed,
+                                    group, doc, word, z_gen);
     int64_t D = (int64_t)I * docs_per_group;
     int32_t *len = (int32_t *)malloc(sizeof(int32_t) * (size_t)D);
     double *phi_cdf = (double *)malloc(sizeof(double) * (size_t)K_gen * V);
@@ -120,7 +148,7 @@ int synth_spdp_corpus(int I, int docs_per_group, double lambda, int V, int K_gen
     int32_t *zz = z_gen ? z_gen : NULL;
     int rc = -1;
     if (!len || !phi_cdf || !theta) goto out;
-    doc_lengths(I, docs_per_group, lambda, seed, len);
+    doc_lengths(I, docs_per_group, lambda, seed, 0, len);
 
     /* phi0_k ~ Dir(beta_gen), stored as CDFs */
     {
@@ -205,5 +233,122 @@ int synth_spdp_corpus(int I, int docs_per_group, double lambda, int V, int K_gen
 out:
     if (zz && zz != z_gen) free(zz);
     free(len); free(phi_cdf); free(theta);
+    return rc;
+}
+
+/* Pitman–Yor seating of one restaurant's n customers (the rule above), words
+ * written to word[order[j]]; nv, tv: zeroed [V] scratch, left zeroed; seq [n]. */
+static void seat_restaurant(xo_t *g, const double *cdf, int V, double a, double b, int64_t n,
+                            const int64_t *order, int32_t *nv, int32_t *tv, int32_t *seq, int32_t *word) {
+    int64_t T = 0;
+    for (int64_t j = 0; j < n; j++) {
+        int32_t v;
+        double pnew = (b + a * (double)T) / (b + (double)j);
+        if (j == 0 || xo_unif(g) < pnew) {
+            v = cdf_search(cdf, V, xo_unif(g));
+            tv[v]++; T++;
+        } else {
+            for (;;) {
+                int32_t c = seq[xo_below(g, (uint64_t)j)];
+                if (xo_unif(g) * nv[c] < (double)nv[c] - a * tv[c]) { v = c; break; }
+            }
+        }
+        nv[v]++;
+        seq[j] = v;
+        word[order[j]] = v;
+    }
+    for (int64_t j = 0; j < n; j++) { nv[seq[j]] = 0; tv[seq[j]] = 0; }
+}
+
+static int spdp_corpus_per_unit(int I, int docs_per_group, double lambda, int V, int K_gen,
+                                double alpha_gen, double beta_gen, double a, double b, uint64_t seed,
+                                int32_t *group, int32_t *doc, int32_t *word, int32_t *z_gen) {
+    int64_t D = (int64_t)I * docs_per_group, R = (int64_t)I * K_gen;
+    int32_t *len = (int32_t *)malloc(sizeof(int32_t) * (size_t)D);
+    int64_t *start = (int64_t *)malloc(sizeof(int64_t) * (size_t)(D + 1));
+    double *phi_cdf = (double *)malloc(sizeof(double) * (size_t)K_gen * V);
+    int64_t *cnt = (int64_t *)calloc((size_t)R + 1, sizeof(int64_t));
+    int32_t *zz = z_gen;
+    int64_t *order = NULL;
+    int rc = -1;
+    if (!len || !start || !phi_cdf || !cnt) goto out;
+    doc_lengths(I, docs_per_group, lambda, seed, 1, len);
+    start[0] = 0;
+    for (int64_t d = 0; d < D; d++) start[d + 1] = start[d] + len[d];
+    int64_t N = start[D];
+    if (!zz) { zz = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1)); if (!zz) goto out; }
+    order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N > 0 ? N : 1));
+    if (!order) goto out;
+    /* phi0_k ~ Dir(beta_gen) as CDFs, one generator per topic */
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int k = 0; k < K_gen; k++) {
+        xo_t g; xo_seed_unit(&g, seed, 1, (uint64_t)k);
+        double *row = phi_cdf + (size_t)k * V;
+        xo_dirichlet(&g, beta_gen, V, row);
+        double c = 0.0;
+        for (int w = 0; w < V; w++) { c += row[w]; row[w] = c; }
+        row[V - 1] = 2.0;
+    }
+    /* theta_d ~ Dir(alpha_gen), z ~ theta_d, one generator per document */
+    int fail = 0;
+    #pragma omp parallel
+    {
+        double *theta = (double *)malloc(sizeof(double) * (size_t)K_gen);
+        if (!theta) {
+            #pragma omp atomic write
+            fail = 1;
+        } else {
+            #pragma omp for schedule(dynamic, 4096)
+            for (int64_t d = 0; d < D; d++) {
+                xo_t g; xo_seed_unit(&g, seed, 2, (uint64_t)d);
+                xo_dirichlet(&g, alpha_gen, K_gen, theta);
+                double c = 0.0;
+                for (int k = 0; k < K_gen; k++) { c += theta[k]; theta[k] = c; }
+                theta[K_gen - 1] = 2.0;
+                for (int64_t p = start[d]; p < start[d + 1]; p++) {
+                    group[p] = (int32_t)(d / docs_per_group);
+                    doc[p] = (int32_t)d;
+                    zz[p] = cdf_search(theta, K_gen, xo_unif(&g));
+                }
+            }
+            free(theta);
+        }
+    }
+    if (fail) goto out;
+    /* customers of each restaurant (group, topic) in canonical order */
+    for (int64_t p = 0; p < N; p++) cnt[(int64_t)group[p] * K_gen + zz[p] + 1]++;
+    for (int64_t r = 0; r < R; r++) cnt[r + 1] += cnt[r];
+    {
+        int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(R > 0 ? R : 1));
+        if (!fill) goto out;
+        memcpy(fill, cnt, sizeof(int64_t) * (size_t)R);
+        for (int64_t p = 0; p < N; p++) order[fill[(int64_t)group[p] * K_gen + zz[p]]++] = p;
+        free(fill);
+    }
+    /* words: one generator per restaurant */
+    #pragma omp parallel
+    {
+        int32_t *nv = (int32_t *)calloc((size_t)V, sizeof(int32_t));
+        int32_t *tv = (int32_t *)calloc((size_t)V, sizeof(int32_t));
+        int64_t mx = 1;
+        for (int64_t r = 0; r < R; r++) if (cnt[r + 1] - cnt[r] > mx) mx = cnt[r + 1] - cnt[r];
+        int32_t *seq = (int32_t *)malloc(sizeof(int32_t) * (size_t)mx);
+        if (!nv || !tv || !seq) {
+            #pragma omp atomic write
+            fail = 1;
+        } else {
+            #pragma omp for schedule(dynamic, 1)
+            for (int64_t r = 0; r < R; r++) {
+                xo_t g; xo_seed_unit(&g, seed, 3, (uint64_t)r);
+                seat_restaurant(&g, phi_cdf + (size_t)(r % K_gen) * V, V, a, b, cnt[r + 1] - cnt[r], order + cnt[r],
+                                nv, tv, seq, word);
+            }
+        }
+        free(nv); free(tv); free(seq);
+    }
+    if (!fail) rc = 0;
+out:
+    if (zz && zz != z_gen) free(zz);
+    free(len); free(start); free(phi_cdf); free(cnt); free(order);
     return rc;
 }

@@ -4,7 +4,9 @@ Alg.4) as SPDP_UPDATE_ASYNC, through the C ABI.
 The scheme is nondeterministic by construction (racing immediate updates), so
 there is no element-wise oracle to match.  What is fixed, and tested:
   * the count invariants after every sweep (library debug_checks: n and m equal
-    the recount from z, 0 <= t <= m, t > 0 iff m > 0, Q = sum_i t, the sums),
+    the recount from z — m summed over the ranks when the library owns the
+    exchange; with an external exchange the test recounts m from the ranks' z —,
+    0 <= t <= m, t > 0 iff m > 0, Q = sum_i t, M/Tt/T equal the sums of m/t/Q),
     i.e. the paper's "error correction" leaves a valid state (P:2411-2419);
   * statistical agreement with the oracle's exact sequential sampler (Alg.1,
     pinned against exact enumeration): training perplexity after 100 sweeps,
@@ -66,6 +68,12 @@ def test_async_multi_rank_exchange_keeps_invariants():
     for k in ("m", "t", "Q"):
         np.testing.assert_array_equal(a[k], b[k])            # replicated state identical after the merge
     assert a["m"].sum() == c.num_tokens
+    # m recounted from z: each token's z from the rank that owns its document
+    owner = spdp.spdp_partition(7, G, c.doc, c.num_docs)[c.doc]
+    z = np.where(owner == 0, a["z"], b["z"])
+    m = np.zeros_like(a["m"])
+    np.add.at(m, (c.group, c.word, z), 1)
+    np.testing.assert_array_equal(m, a["m"])
     assert (a["t"] <= a["m"]).all() and ((a["t"] > 0) == (a["m"] > 0)).all()
 
 

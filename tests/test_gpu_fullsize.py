@@ -66,8 +66,8 @@ def test_maximum_K_and_ragged_tiny_corpus_lockstep():
     one segment longer than a chunk): one sweep from identical state is the
     oracle's, bit for bit when the draws agree."""
     docs = [[0], [1, 1], [2, 0, 1], [3] * 7, [0, 4, 4, 4, 1], [5]]
-    docs += [[6] * 3 for _ in range(120)]            # word 6 in group 0: a 360-token segment (> 256)
-    c = synth.tiny_corpus(2, docs, [0, 1, 0, 1, 1, 0] + [0] * 120, 8)
+    docs += [[6] * 3 for _ in range(200)]            # word 6 in group 0: a 600-token segment (> 512-token chunks)
+    c = synth.tiny_corpus(2, docs, [0, 1, 0, 1, 1, 0] + [0] * 200, 8)
     from gpu_util import assert_counts_equal, assert_draw_parity, lockstep_sweep, pair
     for K in (1024, 1):
         g, o = pair(c, K)

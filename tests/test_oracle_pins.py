@@ -67,6 +67,51 @@ def test_stirling_closed_forms(a):
         assert oracle.log_stirling(a, N, N + 1) == -math.inf
 
 
+def _stirling_explicit(N, M, a):
+    """S^N_{M,a} from the explicit alternating sum of generalised Stirling numbers
+    (a > 0): S^N_M = 1/(a^M M!) * sum_{j=1}^{M} (-1)^j C(M, j) (-j a)_N with the rising
+    factorial (x)_N — a route independent of the recursion P:1454-1455."""
+    tot = sum((-1) ** j * math.comb(M, j) * rising(-j * a, N) for j in range(1, M + 1))
+    return tot / (a ** M * math.factorial(M))
+
+
+def test_ratio_table_exact_rationals():
+    """A0/A1 (Eqs. r0/r1 P:1683) against exact rationals
+    from the explicit Stirling sum, every cell m <= 40 at a = 7/10 and 3/10."""
+    for a in (Fraction(7, 10), Fraction(3, 10)):
+        mmax = 40
+        S = {(N, M): _stirling_explicit(N, M, a) for N in range(0, mmax + 2) for M in range(1, N + 1)}
+        A0, A1 = oracle.ratio_table(float(a), mmax)
+        assert (A0[0], A1[0]) == (0.0, 1.0)                  # A0(0,0) = 0, A1(0,0) = 1
+        for m in range(1, mmax + 1):
+            base = m * (m + 1) // 2
+            assert (A0[base], A1[base]) == (0.0, 0.0)        # t = 0 < m: not a state
+            for t in range(1, m + 1):
+                w0 = Fraction(m - t + 1, m + 1) * S[(m + 1, t)] / S[(m, t)]
+                w1 = Fraction(t + 1, m + 1) * S[(m + 1, t + 1)] / S[(m, t)]
+                assert A0[base + t] == pytest.approx(float(w0), rel=1e-12), (m, t)
+                assert A1[base + t] == pytest.approx(float(w1), rel=1e-12), (m, t)
+
+
+@pytest.mark.parametrize("a", [0.0, 0.7])
+def test_ratio_table_closed_forms_to_large_m(a):
+    """Closed forms on every row up to m = 5000 (> C5's M_max 4898):
+    A1(m,m) = 1, A0(m,m) = (1-a) m / 2, A0(m,1) = m (m - a) / (m + 1); all entries finite, > 0."""
+    mmax = 5000
+    A0, A1 = oracle.ratio_table(a, mmax)
+    m = np.arange(1, mmax + 1)
+    base = m * (m + 1) // 2
+    np.testing.assert_allclose(A1[base + m], 1.0, rtol=1e-9)
+    np.testing.assert_allclose(A0[base + m], (1 - a) * m / 2, rtol=1e-9)
+    np.testing.assert_allclose(A0[base + 1], m * (m - a) / (m + 1), rtol=1e-9)
+    valid = np.ones_like(A0, bool)
+    valid[base] = False
+    valid[0] = False                                          # (0, 0): A0 = 0, A1 = 1
+    assert (A0[0], A1[0]) == (0.0, 1.0)
+    assert np.isfinite(A0).all() and np.isfinite(A1).all()
+    assert (A0[valid] > 0).all() and (A1[valid] > 0).all()
+
+
 @pytest.mark.parametrize("a,b", [(0.7, 100.0), (0.7, 0.5), (0.3, 3.0), (0.0, 2.0)])
 def test_stirling_pdp_normalisation(a, b):
     """Sum over table counts of the PDP joint is one (Cor.17):
@@ -321,13 +366,39 @@ def test_k1_only_tables_move():
 # --------------------------------------------------------------------------
 # b -> infinity limit: SPDP becomes textbook collapsed-Gibbs LDA
 # --------------------------------------------------------------------------
-def _textbook_lda(group, doc, word, V, K, alpha, beta, z, seed, sweeps, jacobi):
+def _textbook_lda(group, doc, word, V, K, alpha, beta, z, seed, sweeps, jacobi, waves=1):
     """Collapsed Gibbs LDA (Griffiths & Steyvers; PAPER.md:1217-1304 background)
     on group-pooled word-topic counts, p(k) ∝ (alpha+n_dk)(beta+n_kw)/(V beta+n_k),
-    drawing with the same Philox uniform u and the first-exceeding-CDF rule."""
+    drawing with the same Philox uniform u and the first-exceeding-CDF rule.
+    jacobi: every token of a wave decides against the wave-start counts; the
+    waves are the in-document positions l mod `waves` (the paper's round-robin
+    reorder P:2289-2299), run in order 0 .. waves-1."""
     z = np.array(z, np.int64)
     N = len(word)
     key = [seed & 0xFFFFFFFF, seed >> 32]
+    seen = {}
+    pos = np.zeros(N, np.int64)                      # in-document position: order of appearance
+    for p in range(N):
+        pos[p] = seen.get(int(doc[p]), 0)
+        seen[int(doc[p])] = pos[p] + 1
+    if jacobi and waves > 1:
+        for s in range(sweeps):
+            for wv in range(waves):
+                ndk = np.zeros((doc.max() + 1, K), np.int64)
+                nkw = np.zeros((K, V), np.int64)
+                for p in range(N):
+                    ndk[doc[p], z[p]] += 1; nkw[z[p], word[p]] += 1
+                nk = nkw.sum(axis=1)
+                newz = z.copy()
+                for p in np.nonzero(pos % waves == wv)[0]:
+                    x = oracle.philox([int(p), s, 0, 0], key)
+                    u = (float(x[1]) * 2097152.0 + float(int(x[2]) >> 11)) / 9007199254740992.0
+                    A, B, C_ = ndk.copy(), nkw.copy(), nk.copy()
+                    A[doc[p], z[p]] -= 1; B[z[p], word[p]] -= 1; C_[z[p]] -= 1
+                    pk = (alpha + A[doc[p]]) * (beta + B[:, word[p]]) / (V * beta + C_)
+                    newz[p] = int(np.argmax(np.cumsum(pk / pk.sum()) > u))
+                z = newz
+        return z
     for s in range(sweeps):
         ndk = np.zeros((doc.max() + 1, K), np.int64)
         nkw = np.zeros((K, V), np.int64)
@@ -356,8 +427,11 @@ def _textbook_lda(group, doc, word, V, K, alpha, beta, z, seed, sweeps, jacobi):
     return z
 
 
-@pytest.mark.parametrize("jacobi", [False, True])
-def test_infinite_concentration_is_collapsed_lda(jacobi):
+@pytest.mark.parametrize("jacobi,waves", [(False, 1), (True, 1), (True, 2), (True, 3), (True, 4)])
+def test_infinite_concentration_is_collapsed_lda(jacobi, waves):
+    """b -> infinity (SURVEY §8(c) pin): the SPDP sweep is textbook collapsed-Gibbs
+    LDA; for waves > 1 this also pins the wave membership pos % W (an index slip,
+    e.g. the canonical token index instead of the in-document position, fails)."""
     import synth
     c = synth.generate(2, 4, 15.0, 25, 3, seed=3)
     K, seed = 3, 99
@@ -367,10 +441,10 @@ def test_infinite_concentration_is_collapsed_lda(jacobi):
     sweeps = 6
     for _ in range(sweeps):
         if jacobi:
-            o.sweep_par(waves=1)
+            o.sweep_par(waves=waves)
         else:
             o.sweep_seq()
-    want = _textbook_lda(c.group, c.doc, c.word, c.vocab, K, 0.1, 0.1, z0, seed, sweeps, jacobi)
+    want = _textbook_lda(c.group, c.doc, c.word, c.vocab, K, 0.1, 0.1, z0, seed, sweeps, jacobi, waves)
     np.testing.assert_array_equal(o.state()["z"], want)
     assert (o.state()["r"] == 1).all()
 
