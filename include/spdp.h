@@ -91,7 +91,8 @@ typedef struct {
     const double* discount;        /* [I] a_i in [0, 1)      (paper 0.7) */
     const double* concentration;   /* [I] b_i > 0            (paper 100) */
     uint64_t seed;                 /* Philox4x32-10 key (low word, high word) */
-    int32_t num_waves;             /* W >= 1: token of in-document position l is in wave l mod W */
+    int32_t num_waves;             /* W >= 1: token of in-document position l is in wave l mod W;
+                                      0: exact sequential sampler (test mode, world_size 1; spdp_debug_chain) */
     int32_t device;                /* CUDA ordinal used by this rank */
     int32_t rank, world_size;      /* 0, 1 for a single GPU */
     int32_t exchange;              /* SPDP_EXCHANGE_* (ignored when world_size == 1) */
@@ -299,6 +300,17 @@ spdp_status spdp_sparse_state(spdp_ctx* ctx, int32_t* q, int32_t* shadow, int16_
  * device code.  probs [n*2K] fp64; info [n*4] int32 = {r_rem, keep, z_new,
  * r_new}.  No state change.  SPDP_EINVAL for tokens of other ranks. */
 spdp_status spdp_debug_probs(spdp_ctx* ctx, int64_t n, const int64_t* tok_ids, double* probs, int32_t* info);
+
+/* Test mode W = 0 (num_waves = 0): the exact sequential
+ * sampler, Algorithm 1 with the keep rule, on the
+ * device (one warp, tokens in canonical order, counts updated after every
+ * token; no snapshot, no clamp).  spdp_sweep(n) runs n such sweeps in one
+ * launch.  spdp_debug_chain runs nsweeps of them and writes, after each, the
+ * state code sum_p z_p K^p + K^N * sum_j t_j tbase^j (cells j in (i, w, k)
+ * order) to codes [nsweeps] int64 — for exact-enumeration tests on tiny
+ * corpora (SPDP_EINVAL unless N log2 K + I V K log2 tbase < 62).
+ * SPDP_ESTATE unless the context was created with num_waves = 0. */
+spdp_status spdp_debug_chain(spdp_ctx* ctx, int32_t nsweeps, int32_t tbase, int64_t* codes);
 
 /* Diagnostics (parity tests, SURVEY §8(c) "A0/A1 folding" pin): the device
  * Stirling-ratio table of group `group` (one per distinct discount a_i),

@@ -38,7 +38,8 @@ EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "s
            "spdp_exchange_buffer", "spdp_exchange_copy", "spdp_sweep_merge", "spdp_counts", "spdp_loglik", "spdp_debug_probs",
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
            "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr",
-           "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait", "spdp_debug_ratio_table"]
+           "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait", "spdp_debug_ratio_table",
+           "spdp_debug_chain"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -89,7 +90,7 @@ def lib():
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
             "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_zr_async": [P, P], "spdp_wait": [P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
-            "spdp_debug_ratio_table": [P, I32, I32, P],
+            "spdp_debug_ratio_table": [P, I32, I32, P], "spdp_debug_chain": [P, I32, I32, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -285,6 +286,13 @@ def spdp_debug_ratio_table(ctx, group, mmax):
     return out[:, 0], out[:, 1]
 
 
+def spdp_debug_chain(ctx, nsweeps, tbase=5):
+    """W = 0 test mode: nsweeps exact sequential sweeps; the state code after each (int64 [nsweeps])."""
+    out = np.zeros(int(nsweeps), np.int64)
+    _check(lib().spdp_debug_chain(ctx, int(nsweeps), int(tbase), _p(out)), ctx)
+    return out
+
+
 def spdp_stats(ctx):
     out = np.zeros(16, np.int64)
     _check(lib().spdp_stats(ctx, _p(out)), ctx)
@@ -394,6 +402,9 @@ class Sampler:
 
     def debug_probs(self, tok_ids):
         return spdp_debug_probs(self.ctx, tok_ids, self.K)
+
+    def debug_chain(self, nsweeps, tbase=5):
+        return spdp_debug_chain(self.ctx, nsweeps, tbase)
 
     def debug_ratio_table(self, group, mmax):
         return spdp_debug_ratio_table(self.ctx, group, mmax)

@@ -13,6 +13,7 @@
 #include "spdp_plan.cuh"
 #include "spdp_token.cuh"
 #include "spdp_sparse.cuh"
+#include "spdp_seq.cuh"
 
 #include <dlfcn.h>
 
@@ -138,6 +139,8 @@ struct spdp_ctx {
     void* d_n = nullptr;                          // n_dk rows in sigma order: fp32 or uint16 (row16)
     bool row16 = false;                           // uint16 doc-topic rows (HBM-resident arrays)
     bool async = false;                           // SPDP_UPDATE_ASYNC (NEXT-2): immediate count updates
+    bool seq = false;                             // num_waves = 0: exact sequential sampler (test mode, spdp_seq.cuh)
+    uint32_t* d_pos = nullptr;                    // seq: canonical id -> sorted position
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
@@ -983,6 +986,25 @@ void collect_times(spdp_ctx* c, bool exchanged) {
     c->acc[7] += 1;
 }
 
+// W = 0: num_sweeps exact sequential sweeps in one single-warp launch (spdp_seq.cuh); codes: the
+// state code after each sweep (spdp_debug_chain), or null
+spdp_status seq_sweeps(spdp_ctx* c, int32_t num_sweeps, int64_t* d_codes, int tbase) {
+    if (num_sweeps <= 0) return SPDP_OK;
+    CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    SweepArgs a = base_args(c);
+    SeqArgs q{};
+    q.group = c->d_group; q.word = c->d_word; q.pos = c->d_pos; q.N = c->N; q.V = c->V;
+    q.nsweeps = num_sweeps; q.codes = d_codes; q.tbase = tbase;
+    const size_t smem = sizeof(float2) * (size_t)c->Kp;
+    if (c->row16) seq_kernel<uint16_t><<<1, 32, smem, c->stream>>>(a, q);
+    else seq_kernel<float><<<1, 32, smem, c->stream>>>(a, q);
+    spdp_status s = check_launch(c, "seq_kernel");
+    if (s) return s;
+    c->launches += 1;
+    c->sweeps_done += num_sweeps;
+    return sync(c, "seq sweeps");
+}
+
 spdp_status finish_sweep(spdp_ctx* c) {
     inc_sweep_kernel<<<1, 1, 0, c->stream>>>(c->d_sweep);
     c->launches += 1;
@@ -1027,14 +1049,19 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     if (cfg->num_topics < 1 || cfg->num_topics > 1024) return bad("num_topics must be in [1, 1024]");
     if (!(cfg->beta > 0.0)) return bad("beta must be > 0");
     if (!cfg->discount || !cfg->concentration) return bad("discount and concentration arrays are required");
-    if (cfg->num_waves < 1) return bad("num_waves must be >= 1");
+    if (cfg->num_waves < 0) return bad("num_waves must be >= 0");
+    if (cfg->num_waves == 0) {   // W = 0: the exact sequential sampler (test mode; one rank, wave updates)
+        if (cfg->world_size != 1) return bad("num_waves = 0 (sequential test mode) needs world_size == 1");
+        if (cfg->update_mode != SPDP_UPDATE_WAVE) return bad("num_waves = 0 needs SPDP_UPDATE_WAVE");
+    }
     if (cfg->merge_every < 0) return bad("merge_every must be >= 0");
     if (cfg->update_mode != SPDP_UPDATE_WAVE && cfg->update_mode != SPDP_UPDATE_ASYNC) return bad("unknown update_mode");
     if (cfg->update_mode == SPDP_UPDATE_ASYNC && cfg->num_waves != 1) return bad("SPDP_UPDATE_ASYNC needs num_waves == 1");
     c->async = cfg->update_mode == SPDP_UPDATE_ASYNC;
     if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size) return bad("rank / world_size out of range");
     c->I = cfg->num_groups; c->V = cfg->vocab_size; c->K = cfg->num_topics;
-    c->Kp = (c->K + 3) & ~3; c->W = cfg->num_waves; c->rank = cfg->rank; c->G = cfg->world_size;
+    c->Kp = (c->K + 3) & ~3; c->W = std::max(cfg->num_waves, 1); c->rank = cfg->rank; c->G = cfg->world_size;
+    c->seq = cfg->num_waves == 0;                      // the plan is the W = 1 plan; the sweep is seq_kernel
     c->alpha_ik.resize((size_t)c->I * c->K);
     for (size_t j = 0; j < c->alpha_ik.size(); ++j) {
         c->alpha_ik[j] = cfg->alpha_ik ? cfg->alpha_ik[j] : cfg->alpha;
@@ -1554,6 +1581,13 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     if (c->sparse && (s = sparse_upload(c))) return s;
     s = install_state(c, z_init, r_init, nullptr);
     if (s) return s;
+    if (c->seq) {   // canonical id -> sorted position, for the canonical-order walk of seq_kernel
+        ALLOC(c->d_pos, std::max<int64_t>(c->N, 1));
+        if (c->Nloc > 0)
+            invert_perm_kernel<<<148 * 4, 256, 0, c->stream>>>(c->d_tok_id, (uint32_t)c->Nloc, c->d_pos);
+        if ((s = check_launch(c, "invert_perm_kernel"))) return s;
+        if ((s = sync(c, "seq positions"))) return s;
+    }
     lt.mark("initial state (counts)");
     c->loaded = true;
     return SPDP_OK;
@@ -1572,6 +1606,7 @@ spdp_status spdp_set_state(spdp_ctx* c, const int32_t* z, const uint8_t* r, cons
 spdp_status spdp_sweep_local(spdp_ctx* c) {
     spdp_status s = guard(c, true);
     if (s) return s;
+    if (c->seq) return fail(c, SPDP_ESTATE, "num_waves = 0 (sequential test mode): use spdp_sweep");
     if ((s = run_waves(c, block_w0(c, c->block), block_w1(c, c->block), c->block == 0))) return s;
     if (c->G > 1) CU(cudaMemcpyAsync(c->d_Dsum, c->d_Dloc, c->dbytes(), cudaMemcpyDeviceToDevice, c->stream));
     return sync(c, "spdp_sweep_local");
@@ -1628,6 +1663,11 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
     if (num_sweeps < 0) return fail(c, SPDP_EINVAL, "num_sweeps must be >= 0");
     if (c->G > 1 && c->cfg.exchange != SPDP_EXCHANGE_NCCL)
         return fail(c, SPDP_ESTATE, "SPDP_EXCHANGE_EXTERNAL: use spdp_sweep_local / spdp_sweep_merge");
+    if (c->seq) {
+        if ((s = seq_sweeps(c, num_sweeps, nullptr, 0))) return s;
+        if (c->cfg.debug_checks) return debug_verify(c);
+        return SPDP_OK;
+    }
     const bool graphs = c->G == 1 && !c->cfg.debug_checks && !c->graphs_off && !c->profiling &&
                         !(getenv("SPDP_GRAPHS") && atoi(getenv("SPDP_GRAPHS")) == 0);
     for (int it = 0; it < num_sweeps; ++it) {
@@ -1797,6 +1837,7 @@ spdp_status spdp_set_transform(spdp_ctx* c, const int32_t* pptr, const int32_t* 
     spdp_status s = guard(c, false);
     if (s) return s;
     if (c->loaded) return fail(c, SPDP_ESTATE, "spdp_set_transform must precede spdp_load_corpus");
+    if (c->seq) return fail(c, SPDP_ESTATE, "num_waves = 0 (sequential test mode) has no transformation-matrix path");
     if (!pptr || !pv || !pp) return fail(c, SPDP_EINVAL, "null transformation arrays");
     const int I = c->I, V = c->V;
     const int64_t rows = (int64_t)I * V;
@@ -2169,6 +2210,26 @@ spdp_status spdp_topic_hellinger(spdp_ctx* a, spdp_ctx* b, double* dist, int32_t
         }
     }
     return SPDP_OK;
+}
+
+spdp_status spdp_debug_chain(spdp_ctx* c, int32_t nsweeps, int32_t tbase, int64_t* codes) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!c->seq) return fail(c, SPDP_ESTATE, "spdp_debug_chain needs num_waves = 0 (sequential test mode)");
+    if (nsweeps < 0 || tbase < 2 || (nsweeps > 0 && !codes)) return fail(c, SPDP_EINVAL, "bad debug_chain arguments");
+    // the code must fit: N log2 K + I V K log2 tbase < 62 bits
+    const double bits = (double)c->N * std::log2((double)std::max(c->K, 1)) +
+                        (double)c->I * c->V * c->K * std::log2((double)tbase);
+    if (bits >= 62.0) return fail(c, SPDP_EINVAL, "corpus too large for a 64-bit state code (%.1f bits)", bits);
+    if (nsweeps == 0) return SPDP_OK;
+    TempBuf<int64_t> d((size_t)nsweeps);
+    if (!d.p) return fail(c, SPDP_ENOMEM, "debug_chain buffer");
+    s = seq_sweeps(c, nsweeps, d.p, tbase);
+    if (!s) {
+        CU(cudaMemcpyAsync(codes, d.p, sizeof(int64_t) * (size_t)nsweeps, cudaMemcpyDeviceToHost, c->stream));
+        s = sync(c, "debug_chain");
+    }
+    return s;
 }
 
 spdp_status spdp_debug_ratio_table(spdp_ctx* c, int32_t group, int32_t mmax, float* out) {

@@ -1117,6 +1117,11 @@ __global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restri
 
 __global__ void inc_sweep_kernel(uint32_t* sweep) { *sweep += 1; }
 
+// pos[perm[q]] = q (canonical id -> sorted position)
+__global__ void invert_perm_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t* __restrict__ pos) {
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) pos[perm[q]] = q;
+}
+
 // ---------------------------------------------------------------- state installation
 // initial topics z_p = floor(x0 K / 2^32) of Philox(seed; p, 0xFFFFFFFF, 0, 0) (reading c11)
 __global__ void init_z_kernel(int32_t* __restrict__ z, uint32_t n, int K, uint32_t k0, uint32_t k1) {
