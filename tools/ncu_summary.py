@@ -52,9 +52,15 @@ def summarise(rep):
             d["dram_bytes_per_launch"] = d["dram_read"] + d.get("dram_write", 0.0)
         stalls = {}
         for h, v in zip(hdr, vals):
+            # warp-state breakdown: cycles stalled per issued instruction, by reason
+            name = None
             if h.startswith("smsp__average_warp_latency_issue_stalled_") and h.endswith(".ratio"):
+                name = h.split("stalled_")[1][:-len(".ratio")]
+            elif h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio"):
+                name = h.split("stalled_")[1][:-len("_per_issue_active.ratio")]
+            if name and not name.endswith("_not_issued"):
                 try:
-                    stalls[h.split("stalled_")[1][:-6]] = float(v)
+                    stalls[name] = float(v.replace(",", ""))
                 except ValueError:
                     pass
         if stalls:
