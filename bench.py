@@ -330,7 +330,7 @@ def main():
     plan = plan_stats(corpus, shard_docs, args.waves)
     peak, peak_src = measured_peaks()
     sample_ms = tm["sample_ms"] / max(tm["sweeps"], 1)       # per sweep (all waves), from the profiled pass
-    row_bytes = 2 if stats.get("row16") else 4
+    row_bytes = stats.get("row_bytes", 4)
     bytes_sweep = alg_bytes(plan, K, row_bytes)                 # the bytes this kernel has to move
     bytes_i32 = alg_bytes(plan, K, 4)                           # SURVEY §8(d)'s canonical int32 model
     achieved = bytes_sweep / (sample_ms / 1e3) / 1e9

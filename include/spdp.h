@@ -328,7 +328,7 @@ spdp_status spdp_debug_ratio_table(spdp_ctx* ctx, int32_t group, int32_t mmax, f
  * out[8] lanes per token, out[9] topics per lane, out[10] tokens per chunk,
  * out[11] resident sample-kernel blocks (persistent grid), out[12] 1 if the
  * token kernel samples (K <= 64), out[13] word-range parts of the sweep
- * (exchange pipelining), out[14] 1 if doc-topic rows are uint16, out[15] 1
+ * (exchange pipelining), out[14] bytes per doc-topic count (4 fp32, 2 uint16, 1 uint8), out[15] 1
  * for SPDP_UPDATE_ASYNC.  out has 16 slots. */
 spdp_status spdp_stats(spdp_ctx* ctx, int64_t* out);
 

@@ -15,6 +15,15 @@
 #include "spdp_sparse.cuh"
 #include "spdp_seq.cuh"
 
+// Doc-topic row element type of the context: fp32 (L2-resident arrays), uint16 or uint8 (HBM-bound
+// arrays; uint8 when every document has < 256 tokens).  Runs the statement with NT bound to it.
+#define SPDP_ROWS(rowb, ...)                                   \
+    do {                                                       \
+        if ((rowb) == 1) { using NT = uint8_t; __VA_ARGS__; }  \
+        else if ((rowb) == 2) { using NT = uint16_t; __VA_ARGS__; } \
+        else { using NT = float; __VA_ARGS__; }                \
+    } while (0)
+
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -136,8 +145,8 @@ struct spdp_ctx {
     uint16_t *d_zr = nullptr, *d_zr_next = nullptr;
     int32_t *d_group = nullptr, *d_doc = nullptr, *d_word = nullptr;   // canonical token triples (all ranks' tokens)
     uint32_t *d_doc_ptr = nullptr, *d_doc_pos = nullptr;   // CSR: sorted-token positions of each local doc
-    void* d_n = nullptr;                          // n_dk rows in sigma order: fp32 or uint16 (row16)
-    bool row16 = false;                           // uint16 doc-topic rows (HBM-resident arrays)
+    void* d_n = nullptr;                          // n_dk rows in sigma order: fp32, uint16 or uint8 (row_elem)
+    int row_elem = 4;                             // bytes per doc-topic count: 4 (fp32), 2 (uint16), 1 (uint8)
     bool async = false;                           // SPDP_UPDATE_ASYNC (NEXT-2): immediate count updates
     bool seq = false;                             // num_waves = 0: exact sequential sampler (test mode, spdp_seq.cuh)
     uint32_t* d_pos = nullptr;                    // seq: canonical id -> sorted position
@@ -241,19 +250,17 @@ spdp_status nccl_check(spdp_ctx* c, int r, const char* what) {
 
 // ------------------------------------------------------------------ kernel dispatch
 template <int LPT, int KPL, bool DBG>
-void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks, bool row16, bool async) {
+void launch_sample_t(const SweepArgs& a, cudaStream_t s, int max_blocks, int rowb, bool async) {
     const size_t smem = sample_smem_bytes<LPT, KPL>();
     const int blocks = std::min((a.nchunks + kWarps - 1) / kWarps, max_blocks);
     if (blocks <= 0) return;
     if constexpr (!DBG) {
         if (async) {
-            if (row16) sample_kernel<LPT, KPL, false, uint16_t, true><<<blocks, kWarps * 32, smem, s>>>(a);
-            else sample_kernel<LPT, KPL, false, float, true><<<blocks, kWarps * 32, smem, s>>>(a);
+            SPDP_ROWS(rowb, sample_kernel<LPT, KPL, false, NT, true><<<blocks, kWarps * 32, smem, s>>>(a));
             return;
         }
     }
-    if (row16) sample_kernel<LPT, KPL, DBG, uint16_t><<<blocks, kWarps * 32, smem, s>>>(a);
-    else sample_kernel<LPT, KPL, DBG, float><<<blocks, kWarps * 32, smem, s>>>(a);
+    SPDP_ROWS(rowb, sample_kernel<LPT, KPL, DBG, NT><<<blocks, kWarps * 32, smem, s>>>(a));
 }
 template <int LPT, int KPL>
 int resident_blocks_t() {
@@ -273,32 +280,52 @@ void set_attr_t() {
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, true, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, true, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(sample_kernel<LPT, KPL, false, uint8_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int psm = kWarps * LPT * KPL * (int)sizeof(double);
     cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
     cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
+    cudaFuncSetAttribute(perplexity_kernel<LPT, KPL, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, psm);
 }
 template <int LPT, int KPL>
 void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum, double* partial, cudaStream_t s,
-                  bool row16) {
+                  int rowb) {
     const size_t smem = (size_t)kWarps * LPT * KPL * sizeof(double);
     const int blocks = (a.nchunks + kWarps - 1) / kWarps;
     if (blocks <= 0) return;
-    if (row16) perplexity_kernel<LPT, KPL, uint16_t><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
-    else perplexity_kernel<LPT, KPL, float><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial);
+    SPDP_ROWS(rowb, perplexity_kernel<LPT, KPL, NT><<<blocks, kWarps * 32, smem, s>>>(a, doclen, asum, partial));
 }
 
-#define SPDP_DISPATCH(LPT_, KPL_, CALL)                     \
-    switch (LPT_ * 100 + KPL_) {                            \
+// The (lanes per token) x (topics per lane) configurations pick_lpt / pick_kpl choose; the
+// SPDP_KERNEL_CFG tuning shapes (1x16 ... 16x16) only with -DSPDP_TUNING_CFGS (compile time).
+#ifdef SPDP_TUNING_CFGS
+#define SPDP_DISPATCH_TUNING(CALL)                          \
         case 116: CALL(1, 16); break;                       \
         case 132: CALL(1, 32); break;                       \
         case 216: CALL(2, 16); break;                       \
         case 232: CALL(2, 32); break;                       \
+        case 816: CALL(8, 16); break;                       \
+        case 1616: CALL(16, 16); break;
+#else
+#define SPDP_DISPATCH_TUNING(CALL)
+#endif
+bool cfg_compiled(int lpt, int kpl) {
+    switch (lpt * 100 + kpl) {
+        case 404: case 408: case 416: case 432: case 832: case 1632: case 3232: return true;
+#ifdef SPDP_TUNING_CFGS
+        case 116: case 132: case 216: case 232: case 816: case 1616: return true;
+#endif
+        default: return false;
+    }
+}
+#define SPDP_DISPATCH(LPT_, KPL_, CALL)                     \
+    switch (LPT_ * 100 + KPL_) {                            \
+        SPDP_DISPATCH_TUNING(CALL)                          \
         case 404: CALL(4, 4); break;                        \
         case 408: CALL(4, 8); break;                        \
         case 416: CALL(4, 16); break;                       \
         case 432: CALL(4, 32); break;                       \
-        case 816: CALL(8, 16); break;                       \
-        case 1616: CALL(16, 16); break;                     \
         case 832: CALL(8, 32); break;                       \
         case 1632: CALL(16, 32); break;                     \
         case 3232: CALL(32, 32); break;                     \
@@ -306,7 +333,7 @@ void launch_ppl_t(const SweepArgs& a, const int32_t* doclen, const double* asum,
     }
 
 void launch_sample(spdp_ctx* c, const SweepArgs& a, bool dbg) {
-#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid, c->row16, false) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid, c->row16, c->async))
+#define CALL_S(L, P) (dbg ? launch_sample_t<L, P, true>(a, c->stream, c->sample_grid, c->row_elem, false) : launch_sample_t<L, P, false>(a, c->stream, c->sample_grid, c->row_elem, c->async))
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_S)
 #undef CALL_S
 }
@@ -319,7 +346,7 @@ void set_attrs(spdp_ctx* c) {
 #undef CALL_R
 }
 void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
-#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream, c->row16)
+#define CALL_P(L, P) launch_ppl_t<L, P>(a, c->d_doclen, c->d_alpha_sum64, partial, c->stream, c->row_elem)
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_P)
 #undef CALL_P
 }
@@ -350,8 +377,7 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     const size_t tsm = nbk > 16 ? sizeof(float) * 256 * 32 : 0;
 #define SPDP_TOK(NBK)                                                                                   \
     do {                                                                                                \
-        if (c->row16) token_kernel<NBK, uint16_t><<<std::max(grid, 1), 256, tsm, c->stream>>>(t);       \
-        else token_kernel<NBK, float><<<std::max(grid, 1), 256, tsm, c->stream>>>(t);                   \
+        SPDP_ROWS(c->row_elem, token_kernel<NBK, NT><<<std::max(grid, 1), 256, tsm, c->stream>>>(t));  \
     } while (0)
     if (nbk <= 4) SPDP_TOK(4);
     else if (nbk <= 8) SPDP_TOK(8);
@@ -501,16 +527,22 @@ void partition_docs(uint64_t seed, int G, int64_t N, int32_t D, const std::vecto
 
 // Upload (z, r or tables) as the sampler state: counts from z.
 size_t row_bytes(const spdp_ctx* c) {
-    return ((size_t)c->Dloc * c->Kp + 1024) * (c->row16 ? sizeof(uint16_t) : sizeof(float));
+    return ((size_t)c->Dloc * c->Kp + 1024) * (size_t)c->row_elem;
 }
 
 // doc-topic rows to the host as floats (sigma order, [Dloc][Kp])
 spdp_status read_rows(spdp_ctx* c, std::vector<float>& out) {
     const size_t n = (size_t)c->Dloc * c->Kp;
     out.assign(n, 0.f);
-    if (c->row16) {
+    if (c->row_elem == 2) {
         std::vector<uint16_t> tmp(n);
         CU(cudaMemcpyAsync(tmp.data(), c->d_n, sizeof(uint16_t) * n, cudaMemcpyDeviceToHost, c->stream));
+        spdp_status s = sync(c, "read rows");
+        if (s) return s;
+        for (size_t j = 0; j < n; ++j) out[j] = (float)tmp[j];
+    } else if (c->row_elem == 1) {
+        std::vector<uint8_t> tmp(n);
+        CU(cudaMemcpyAsync(tmp.data(), c->d_n, n, cudaMemcpyDeviceToHost, c->stream));
         spdp_status s = sync(c, "read rows");
         if (s) return s;
         for (size_t j = 0; j < n; ++j) out[j] = (float)tmp[j];
@@ -608,13 +640,9 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     if (nbad) return fail(c, SPDP_EINVAL, "table counts violate 1 <= t <= m on %llu occupied cell(s) (or t > 0 on an empty one)", nbad);
     CU(cudaMemsetAsync(c->d_n, 0, row_bytes(c), c->stream));
     if (c->Nloc > 0) {
-        if (c->row16)
-            init_local_kernel<uint16_t><<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc,
-                                                                     Kp, c->d_sigma, c->d_zr, c->d_zr_next,
-                                                                     (uint16_t*)c->d_n);
-        else
-            init_local_kernel<float><<<grid, 256, 0, c->stream>>>(c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc,
-                                                                  Kp, c->d_sigma, c->d_zr, c->d_zr_next, (float*)c->d_n);
+        SPDP_ROWS(c->row_elem, init_local_kernel<NT><<<grid, 256, 0, c->stream>>>(
+                                   c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc, Kp, c->d_sigma, c->d_zr,
+                                   c->d_zr_next, (NT*)c->d_n));
     }
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
@@ -748,25 +776,16 @@ void sparse_wave(spdp_ctx* c, int w) {
     t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats; t.P = P;
     const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
     const size_t ssm = ((Kp / 4) <= kSpSmemBlocks) ? sizeof(float) * 256 * (size_t)(Kp / 4) : 0;
-    if (c->row16) sp_token_kernel<uint16_t><<<std::max(grid, 1), 256, ssm, c->stream>>>(t);
-    else sp_token_kernel<float><<<std::max(grid, 1), 256, ssm, c->stream>>>(t);
+    SPDP_ROWS(c->row_elem, sp_token_kernel<NT><<<std::max(grid, 1), 256, ssm, c->stream>>>(t));
     if (c->W == 1) {
         const size_t smem = sizeof(int) * 8 * (size_t)Kp;
-        if (c->row16)
-            recount_docs_kernel<uint16_t><<<148 * 8, 256, smem, c->stream>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
-                                                                             c->d_sigma, c->Dloc, Kp, (uint16_t*)c->d_n);
-        else
-            recount_docs_kernel<float><<<148 * 8, 256, smem, c->stream>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
-                                                                          c->d_sigma, c->Dloc, Kp, (float*)c->d_n);
+        SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
+                                   c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, Kp, (NT*)c->d_n));
         std::swap(c->d_zr, c->d_zr_next);
     } else {
         const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
-        if (c->row16)
-            apply_tokens_kernel<uint16_t><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
-                c->d_tok_doc, c->d_zr, c->d_zr_next, (uint16_t*)c->d_n, c->d_sigma, Kp, tb, te);
-        else
-            apply_tokens_kernel<float><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
-                c->d_tok_doc, c->d_zr, c->d_zr_next, (float*)c->d_n, c->d_sigma, Kp, tb, te);
+        SPDP_ROWS(c->row_elem, apply_tokens_kernel<NT><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
+                                   c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, Kp, tb, te));
     }
     const int blocks = (int)std::min<uint32_t>((r1 - r0 + 7) / 8, 148u * 4u);
     int32_t* Dm = c->G > 1 ? (int32_t*)c->d_Dloc : nullptr;
@@ -841,12 +860,8 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
     }
     rec(c, 1);
     const size_t rsm = sizeof(int) * 8 * (size_t)c->Kp;      // every token moved to zr_next: rebuild n, swap
-    if (c->row16)
-        recount_docs_kernel<uint16_t><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
-                                                                c->Dloc, c->Kp, (uint16_t*)c->d_n);
-    else
-        recount_docs_kernel<float><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
-                                                             c->Dloc, c->Kp, (float*)c->d_n);
+    SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
+                                                                            c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n));
     std::swap(c->d_zr, c->d_zr_next);
     rec(c, 2);
     if (c->overlap) {
@@ -932,21 +947,13 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
-            if (c->row16)
-                recount_docs_kernel<uint16_t><<<148 * 8, 256, smem, c->stream>>>(
-                    c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (uint16_t*)c->d_n);
-            else
-                recount_docs_kernel<float><<<148 * 8, 256, smem, c->stream>>>(
-                    c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (float*)c->d_n);
+            SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
+                                       c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n));
             std::swap(c->d_zr, c->d_zr_next);
         } else {
             const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
-            if (c->row16)
-                apply_tokens_kernel<uint16_t><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
-                    c->d_tok_doc, c->d_zr, c->d_zr_next, (uint16_t*)c->d_n, c->d_sigma, c->Kp, tb, te);
-            else
-                apply_tokens_kernel<float><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
-                    c->d_tok_doc, c->d_zr, c->d_zr_next, (float*)c->d_n, c->d_sigma, c->Kp, tb, te);
+            SPDP_ROWS(c->row_elem, apply_tokens_kernel<NT><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
+                                       c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, c->Kp, tb, te));
         }
         rec(c, 4 * (size_t)w + 2);
         {
@@ -996,8 +1003,7 @@ spdp_status seq_sweeps(spdp_ctx* c, int32_t num_sweeps, int64_t* d_codes, int tb
     q.group = c->d_group; q.word = c->d_word; q.pos = c->d_pos; q.N = c->N; q.V = c->V;
     q.nsweeps = num_sweeps; q.codes = d_codes; q.tbase = tbase;
     const size_t smem = sizeof(float2) * (size_t)c->Kp;
-    if (c->row16) seq_kernel<uint16_t><<<1, 32, smem, c->stream>>>(a, q);
-    else seq_kernel<float><<<1, 32, smem, c->stream>>>(a, q);
+    SPDP_ROWS(c->row_elem, seq_kernel<NT><<<1, 32, smem, c->stream>>>(a, q));
     spdp_status s = check_launch(c, "seq_kernel");
     if (s) return s;
     c->launches += 1;
@@ -1078,7 +1084,10 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
     c->KPL = pick_kpl(c->K);
     if (const char* e = getenv("SPDP_KERNEL_CFG")) {       // tuning override "LPTxKPL", e.g. "8x16"
         int l = 0, p = 0;
-        if (sscanf(e, "%dx%d", &l, &p) == 2 && l * p >= c->K) { c->LPT = l; c->KPL = p; }
+        if (sscanf(e, "%dx%d", &l, &p) == 2 && l * p >= c->K) {
+            if (!cfg_compiled(l, p)) return bad("SPDP_KERNEL_CFG: configuration not compiled (build with -DSPDP_TUNING_CFGS)");
+            c->LPT = l; c->KPL = p;
+        }
     }
     if (c->LPT * c->KPL < c->K) return bad("internal: no kernel configuration for K");
     // tokens per chunk: 512 vs 256 measured -0.5..-1.2 % at C3, C4 K = 100/300, C5 (B200); the async
@@ -1471,11 +1480,18 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         c->prefetch_rows = ((double)c->Dloc * Kp * sizeof(float) > 0.5 * (double)l2) ? 1 : 0;
         if (const char* e = getenv("SPDP_PREFETCH_ROWS")) c->prefetch_rows = atoi(e);
-        c->row16 = c->prefetch_rows != 0;                // HBM-resident rows: half the bytes
-        if (const char* e = getenv("SPDP_ROW16")) c->row16 = atoi(e) != 0;
+        // HBM-resident rows: the narrowest exact count type (n_dk <= L_d): uint8 when every document has
+        // < 256 tokens, else uint16 (< 2^16); fp32 rows (no conversion) when the array lives in L2.
+        // Overrides: SPDP_ROW_BYTES=4|2|1, SPDP_ROW16=0|1, SPDP_ROW8=0|1 (tests force each path).
         int32_t maxlen = 0;
         for (int32_t dl : c->doclen) maxlen = std::max(maxlen, dl);
-        if (maxlen >= 65536) c->row16 = false;           // uint16 needs L_d < 2^16
+        int rb = c->prefetch_rows ? (maxlen < 256 ? 1 : 2) : 4;
+        if (const char* e = getenv("SPDP_ROW16")) rb = atoi(e) ? 2 : (rb == 2 ? 4 : rb);
+        if (const char* e = getenv("SPDP_ROW8")) rb = atoi(e) ? 1 : (rb == 1 ? 2 : rb);
+        if (const char* e = getenv("SPDP_ROW_BYTES")) { const int v = atoi(e); if (v == 1 || v == 2 || v == 4) rb = v; }
+        if (rb == 1 && maxlen >= 256) rb = 2;            // uint8 needs L_d < 2^8
+        if (rb == 2 && maxlen >= 65536) rb = 4;          // uint16 needs L_d < 2^16
+        c->row_elem = rb;
     }
     ALLOC(c->d_sigma, Kp);
     CU(cudaMemcpy(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice));
@@ -2006,14 +2022,9 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
         double* part = c->d_partial;       // [0, grid) words, [grid, 2 grid) docs
         loglik_words_kernel<<<grid, 256, 0, c->stream>>>(c->d_m, c->d_t, c->d_Q, ls, d_off, c->V, c->I, c->K, c->Kp,
                                                         c->cfg.beta, part);
-        if (c->row16)
-            loglik_docs_kernel<uint16_t><<<grid, 256, 0, c->stream>>>((const uint16_t*)c->d_n, c->d_sigma, c->d_doclen,
-                                                                      c->d_docgroup, c->d_alpha64, c->d_alpha_sum64, c->Dloc,
-                                                                      c->K, c->Kp, part + grid);
-        else
-            loglik_docs_kernel<float><<<grid, 256, 0, c->stream>>>((const float*)c->d_n, c->d_sigma, c->d_doclen,
-                                                                   c->d_docgroup, c->d_alpha64, c->d_alpha_sum64, c->Dloc,
-                                                                   c->K, c->Kp, part + grid);
+        SPDP_ROWS(c->row_elem, loglik_docs_kernel<NT><<<grid, 256, 0, c->stream>>>((const NT*)c->d_n, c->d_sigma, c->d_doclen,
+                                                                            c->d_docgroup, c->d_alpha64, c->d_alpha_sum64,
+                                                                            c->Dloc, c->K, c->Kp, part + grid));
         loglik_small_kernel<<<1, 1024, 0, c->stream>>>(c->d_M, c->d_Tt, c->d_T, c->d_disc64, c->d_conc64, c->I, c->K, c->Kp,
                                                       (double)c->V * c->cfg.beta, part + 2 * grid);
         int nterms = 2 * grid + 1;
@@ -2343,7 +2354,7 @@ spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
     out[0] = (int64_t)st[0]; out[1] = (int64_t)st[1]; out[2] = (int64_t)st[2];
     out[3] = c->sweeps_done; out[4] = c->Nloc; out[5] = c->Dloc; out[6] = c->mmax; out[7] = (int64_t)(size_t)c->nchunks;
     out[8] = c->LPT; out[9] = c->KPL; out[10] = c->chunk_tokens; out[11] = c->sample_grid;
-    out[12] = c->token_kernel ? 1 : 0; out[13] = c->P; out[14] = c->row16 ? 1 : 0; out[15] = c->async ? 1 : 0;
+    out[12] = c->token_kernel ? 1 : 0; out[13] = c->P; out[14] = c->row_elem; out[15] = c->async ? 1 : 0;
     return SPDP_OK;
 }
 

@@ -31,6 +31,15 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_PREFETCH_NEXT
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
+#ifndef SPDP_BULK_PREFETCH
+#define SPDP_BULK_PREFETCH 1       // HBM-resident rows: exact-byte cp.async.bulk.prefetch.L2 instead of 128-B line prefetches
+#endif
+#ifndef SPDP_PREFETCH_AHEAD
+#define SPDP_PREFETCH_AHEAD 1      // bulk prefetch: batches of 32 tokens ahead of the one being sampled
+#endif
+#ifndef SPDP_PAD_SELECT
+#define SPDP_PAD_SELECT 1          // loads of 4-topic blocks past K read the row's first block (no bytes past the row)
+#endif
 #ifndef SPDP_SKIP_PAD_BLOCKS
 #define SPDP_SKIP_PAD_BLOCKS 1     // sample kernel: no row loads for 4-topic blocks past K
 #endif
@@ -65,6 +74,14 @@ __device__ __forceinline__ int removal_draw(uint32_t x0, int m, int t) {
 }
 
 __device__ __forceinline__ uint64_t tri(int m) { return (uint64_t)m * (uint64_t)(m + 1) / 2; }
+
+// Pull the bytes [p, p + bytes) into L2 with one bulk (TMA-unit) prefetch: 16-byte granularity, so a
+// row costs its own sectors and no more (a 128-B line prefetch per line over-fetches ~25 % on 400-B rows).
+__device__ __forceinline__ void prefetch_bytes_l2(const void* p, uint32_t bytes) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uintptr_t lo = a & ~(uintptr_t)15, hi = (a + bytes + 15) & ~(uintptr_t)15;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
+}
 
 // ---------------------------------------------------------------- Stirling ratio table
 // A0(m,t) = (m-t+1)/(m+1) * S^{m+1}_t / S^m_t      (Eq. r0)
@@ -213,6 +230,10 @@ __device__ __forceinline__ int ld_weak(const int32_t* p) {
     return v;
 }
 
+__device__ __forceinline__ int ld_weak_or_relaxed(const void* p) {
+    return kAsyncWeakRows ? ld_weak(reinterpret_cast<const int32_t*>(p)) : ld_relaxed(reinterpret_cast<const int32_t*>(p));
+}
+
 template <bool AS>
 __device__ __forceinline__ int ldc(const int32_t* p) {   // count read: snapshot (wave mode) or live (async)
     if constexpr (AS) return kAsyncWeakRows ? ld_weak(p) : ld_relaxed(p);
@@ -270,6 +291,35 @@ struct Row<uint16_t> {
     }
     __device__ __forceinline__ static void store(uint16_t* p, int v) { *p = (uint16_t)v; }
     __device__ __forceinline__ static int get(const uint16_t* p) { return (int)*p; }
+};
+
+// uint8 counts (every document < 256 tokens): a quarter of the fp32 bytes for HBM-resident rows.
+// Exact u8 -> f32 on the full-rate pipes, as for uint16: byte j into 2^23 + x, minus 2^23.
+__device__ __forceinline__ float u8at(uint32_t x, uint32_t j) {
+    return __int_as_float((int)__byte_perm(x, 0x4B000000u, 0x7440u | j)) - 8388608.f;
+}
+template <>
+struct Row<uint8_t> {
+    __device__ __forceinline__ static float4 load4(const uint8_t* p) {
+        const uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(p));
+        return make_float4(u8at(v, 0), u8at(v, 1), u8at(v, 2), u8at(v, 3));
+    }
+    __device__ __forceinline__ static float4 load4_live(const uint8_t* p) {
+        const uint32_t v = (uint32_t)ld_weak_or_relaxed(p);
+        return make_float4(u8at(v, 0), u8at(v, 1), u8at(v, 2), u8at(v, 3));
+    }
+    __device__ __forceinline__ static float load1_live(const uint8_t* p) {
+        const uint32_t v = (uint32_t)ld_relaxed(reinterpret_cast<const int32_t*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)3));
+        return (float)((v >> (8 * (reinterpret_cast<uintptr_t>(p) & 3))) & 0xFFu);
+    }
+    __device__ __forceinline__ static float load1(const uint8_t* p) { return (float)__ldg(p); }
+    // +-1 on one byte of the containing 32-bit word (a byte never leaves [0, L_d] with L_d < 256: no carry
+    // into, or borrow from, its neighbours)
+    __device__ __forceinline__ static void add(uint8_t* base, size_t idx, int d) {
+        atomicAdd(reinterpret_cast<unsigned int*>(base) + (idx >> 2), (unsigned int)d << ((idx & 3) * 8));
+    }
+    __device__ __forceinline__ static void store(uint8_t* p, int v) { *p = (uint8_t)v; }
+    __device__ __forceinline__ static int get(const uint8_t* p) { return (int)*p; }
 };
 
 struct SweepArgs {
@@ -500,13 +550,27 @@ sample_kernel(SweepArgs A) {
         }
         const NT* __restrict__ nrow = reinterpret_cast<const NT*>(A.n) + noff;
         if (A.prefetch_rows) {   // rows not L2-resident: pull rows of this batch (first) and the next towards L2
-            constexpr int PER_LINE = 128 / (int)sizeof(NT);
-            if (mine && (b0 == start || !SPDP_PREFETCH_NEXT))
-                for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
-            const uint32_t pn = p + 32;
-            if (SPDP_PREFETCH_NEXT && pn < end) {
-                const NT* nn = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp;
-                for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
+            if constexpr (SPDP_BULK_PREFETCH) {
+                // one exact-size bulk prefetch per row: at the chunk's first batch the rows of batches
+                // 0 .. AHEAD, afterwards those of batch b + AHEAD (the copy engine runs ahead of the sampling)
+                const uint32_t rbytes = (uint32_t)((size_t)Kp * sizeof(NT));
+                if (b0 == start) {
+#pragma unroll
+                    for (int j = 0; j < SPDP_PREFETCH_AHEAD; ++j)
+                        if (p + 32u * j < end)
+                            prefetch_bytes_l2(reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[p + 32u * j] * Kp, rbytes);
+                }
+                const uint32_t pn = p + 32u * SPDP_PREFETCH_AHEAD;
+                if (pn < end) prefetch_bytes_l2(reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp, rbytes);
+            } else {
+                constexpr int PER_LINE = 128 / (int)sizeof(NT);
+                if (mine && (b0 == start || !SPDP_PREFETCH_NEXT))
+                    for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
+                const uint32_t pn = p + 32;
+                if (SPDP_PREFETCH_NEXT && pn < end) {
+                    const NT* nn = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp;
+                    for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
+                }
             }
         }
         const int rrem = removal_draw(x0, m0, t0);                                            // a3
@@ -533,9 +597,15 @@ sample_kernel(SweepArgs A) {
             const uint32_t so = __shfl_sync(0xffffffffu, noff, (s + g) & 31);
             const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + so + 4 * gl;
 #pragma unroll
-            for (int q = 0; q < NB; ++q)   // blocks past K hold no topic (zero mass): optionally no load
-                v[q] = (!kSkipPad || kb + 4 * q < K) ? row_load4<NT, ASYNC>(nl + 4 * A.colstart[q])
-                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < NB; ++q) {   // blocks past K hold no topic (zero mass): no load, or one inside the row
+                if constexpr (kSkipPad)
+                    v[q] = (kb + 4 * q < K) ? row_load4<NT, ASYNC>(nl + 4 * A.colstart[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                else if constexpr (SPDP_PAD_SELECT)
+                    v[q] = row_load4<NT, ASYNC>((kb + 4 * q < K) ? nl + 4 * A.colstart[q]
+                                                                 : reinterpret_cast<const NT*>(A.n) + so);
+                else
+                    v[q] = row_load4<NT, ASYNC>(nl + 4 * A.colstart[q]);
+            }
         };
         if constexpr (kRowPipe) load_rows(0);
         for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {

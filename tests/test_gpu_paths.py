@@ -3,8 +3,8 @@ weak" 1-2): north_star (5) checks — draw mismatches <= 1e-4 of tokens, each
 within 1e-6 of a CDF boundary; counts bit-exact once the draws agree (lock-step)
 — on
 
-  * uint16 doc-topic rows with L2 prefetch (the HBM-bound C4 K >= 300 / C5
-    path), forced on small corpora at every lanes-per-token x topics-per-lane
+  * uint16 and uint8 doc-topic rows with L2 prefetch (the HBM-bound C4
+    K = 1000 / C5 path), forced on small corpora at every lanes-per-token x topics-per-lane
     instantiation, including 8 x 32 (C5's K = 200, compiled for 5 blocks/SM)
     and 32 x 32 (K = 1000);
   * (w, i) segments split across several chunks (C3 and C5 split segments on
@@ -42,24 +42,27 @@ def _lockstep(c, K, waves, sweeps, **kw):
 
 # K -> instantiation: 20/50 token kernel; 100 -> 4x32; 200 -> 8x32 (C5's, 5 blocks/SM); 300 -> 16x32;
 # 1000 -> 32x32 (C4 K = 1000's)
+@pytest.mark.parametrize("rowb", [2, 1])
 @pytest.mark.parametrize("K,waves", [(20, 1), (50, 2), (100, 1), (100, 2), (200, 1), (200, 3), (300, 1),
                                      (1000, 1), (1000, 2)])
-def test_uint16_rows_with_prefetch_lockstep(monkeypatch, K, waves):
-    monkeypatch.setenv("SPDP_ROW16", "1")
+def test_narrow_rows_with_prefetch_lockstep(monkeypatch, K, waves, rowb):
+    """uint16 (rowb = 2) and uint8 (rowb = 1, documents < 256 tokens: C5, C4) rows."""
+    monkeypatch.setenv("SPDP_ROW_BYTES", str(rowb))
     monkeypatch.setenv("SPDP_PREFETCH_ROWS", "1")
     c = synth.generate(2, 30, 40.0, 300, 8, seed=K + waves)
     g = _lockstep(c, K, waves, 3)
     st = g.stats()
-    assert st["row16"] == 1
+    assert st["row_bytes"] == rowb
     if K > 64:
         assert (st["lanes_per_token"], st["topics_per_lane"]) == {100: (4, 32), 200: (8, 32), 300: (16, 32),
                                                                   1000: (32, 32)}[K]
 
 
-def test_uint16_rows_conditionals(monkeypatch):
-    """The uint16 path's own conditionals (spdp_debug_probs runs the sweep's device
-    code with uint16 rows) match the oracle to 1e-5 at K = 200 (C5's instantiation)."""
-    monkeypatch.setenv("SPDP_ROW16", "1")
+@pytest.mark.parametrize("rowb", [2, 1])
+def test_narrow_rows_conditionals(monkeypatch, rowb):
+    """The narrow-row path's own conditionals (spdp_debug_probs runs the sweep's device
+    code with uint16 / uint8 rows) match the oracle to 1e-5 at K = 200 (C5's instantiation)."""
+    monkeypatch.setenv("SPDP_ROW_BYTES", str(rowb))
     monkeypatch.setenv("SPDP_PREFETCH_ROWS", "1")
     c = synth.generate(3, 40, 50.0, 400, 10, seed=3)
     K = 200
@@ -76,7 +79,7 @@ def test_uint16_rows_conditionals(monkeypatch):
         assert (np.abs(gp[j][big] - d["prob"][big]) / d["prob"][big]).max() <= 1e-5
 
 
-@pytest.mark.parametrize("name,K,extra", [("C1", 100, {}), ("C1", 200, {"SPDP_ROW16": "1"}),
+@pytest.mark.parametrize("name,K,extra", [("C1", 100, {}), ("C1", 200, {"SPDP_ROW16": "1"}), ("C1", 200, {"SPDP_ROW8": "1"}),
                                           ("C2", 50, {"SPDP_TOKEN_KERNEL": "0"}), ("C2", 130, {})])
 def test_segments_split_across_chunks_lockstep(monkeypatch, name, K, extra):
     """64-token chunks: every (w, i) segment longer than 64 tokens is sampled by
@@ -150,11 +153,11 @@ def test_full_size_library_recount(name, K, sweeps):
     """debug_checks at full size: after every sweep the library recounts n and m
     from z and checks 0 <= t <= m, t > 0 iff m > 0, Q = sum_i t, M/Tt/T = sums
     (SPDP_EINTEGRITY otherwise), on the bench configuration of each size — C5
-    with uint16 rows (its doc-topic array exceeds half of L2)."""
+    with uint8 rows (its doc-topic array exceeds half of L2, documents < 256 tokens)."""
     c = corpus(name)
     g = spdp.sampler_for(c, K, debug_checks=True, **HYPER)
     g.sweep(sweeps)
     st = g.stats()
     assert st["sweeps"] == sweeps and st["moved"] > 0
     if name == "C5":
-        assert st["row16"] == 1 and (st["lanes_per_token"], st["topics_per_lane"]) == (8, 32)
+        assert st["row_bytes"] == 1 and (st["lanes_per_token"], st["topics_per_lane"]) == (8, 32)

@@ -44,7 +44,7 @@ def test_sequential_mode_ragged_and_uint16(monkeypatch):
     monkeypatch.setenv("SPDP_ROW16", "1")
     c = synth.tiny_corpus(3, [[0], [1, 1, 1, 1], [2, 0, 2], [5], [4] * 40], [0, 0, 1, 1, 2], vocab=7)
     g, o = pair(c, 3, waves=0)
-    assert g.stats()["row16"] == 1
+    assert g.stats()["row_bytes"] == 2
     for _ in range(5):
         rep, gc = lockstep_sweep(g, o, waves=0)
         assert_draw_parity(rep)

@@ -1,40 +1,37 @@
-"""Top source lines of an ncu report by warp-stall samples (needs -lineinfo and --import-source on).
-Usage: python tools/ncu_source_top.py REPORT [N]  -> CSV rows: samples, share, file:line, source text."""
+"""Top CUDA source lines of an ncu report by warp-stall samples, with executed warp instructions
+(needs -lineinfo and --import-source on).
+Usage: python tools/ncu_source_top.py REPORT [N]
+Output CSV: stall_samples, share, warp_instructions, share, file:line, source text."""
 import csv
 import io
+import os
 import subprocess
 import sys
 
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-if not rows:
-    sys.exit("no source page")
-hdr = rows[0]
-def col(*names):
-    for n in names:
-        for j, h in enumerate(hdr):
-            if h.strip().lower() == n.lower():
-                return j
-    for n in names:
-        for j, h in enumerate(hdr):
-            if n.lower() in h.lower():
-                return j
-    return None
-cs = col("Warp Stall Sampling (All Samples)", "Warp Stall Sampling")
-cl = col("Line", "#")
-cf = col("Source", "Address")
-print("# columns:", "|".join(hdr[:12]))
-data = []
-for r in rows[1:]:
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+fname, hdr, data = "?", None, []
+for r in csv.reader(io.StringIO(raw)):
+    if not r:
+        continue
+    if r[0] == "File Path":
+        fname = os.path.basename(r[1]) if len(r) > 1 else "?"
+        continue
+    if r[0] == "Line No":
+        hdr = r
+        continue
+    if hdr is None or not r[0]:
+        continue
     try:
-        v = float(r[cs].replace(",", "")) if cs is not None else 0.0
+        samp = float(r[hdr.index("Warp Stall Sampling (All Samples)")].replace(",", ""))
+        inst = float(r[hdr.index("Instructions Executed")].replace(",", ""))
     except (ValueError, IndexError):
         continue
-    data.append((v, r))
-tot = sum(v for v, _ in data) or 1.0
-for v, r in sorted(data, key=lambda x: -x[0])[:N]:
-    line = r[cl] if cl is not None else "?"
-    src = (r[cf] if cf is not None else "").strip()[:140]
-    print(f"{int(v)},{v / tot:.3f},{line},{src}")
+    data.append((samp, inst, f"{fname}:{r[0]}", r[1].strip()[:120]))
+ts = sum(d[0] for d in data) or 1.0
+ti = sum(d[1] for d in data) or 1.0
+print("stall_samples,share,warp_instructions,share,line,source")
+for s, i, loc, src in sorted(data, key=lambda d: -d[0])[:N]:
+    print(f"{int(s)},{s / ts:.3f},{int(i)},{i / ti:.3f},{loc},\"{src}\"")
