@@ -185,18 +185,32 @@ class LoadPhases:
         self.tmp.close()
 
 
-def cpu_baseline(corpus, cfg, K, waves, sample_tokens):
-    """The oracle as it stands, single thread, on a bounded sample of the same
-    workload: the first `sample_tokens` tokens of one mode-P sweep."""
-    import oracle
-    o = oracle.from_corpus(corpus, K, cfg.alpha, cfg.beta, cfg.discount, cfg.concentration, cfg.seed)
-    t0 = time.perf_counter()
-    o.sweep_par(waves=waves, shards=1, max_tokens=sample_tokens)
-    dt = time.perf_counter() - t0
-    return {"value": sample_tokens / dt, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {sample_tokens} tokens of one mode-P (W={waves}) sweep of {cfg.name} "
-                      f"(N={corpus.num_tokens}, K={K}); plain C oracle, fp64 log space, 1 thread; "
-                      f"{dt:.1f} s incl. the sweep's fixed per-wave passes"}
+def cpu_baseline(corpus, cfg, K, waves, sample_tokens, topics_arg):
+    """The oracle as it stands, timed on this host: the -fopenmp build of the same
+    source on all host cores for one whole mode-P sweep of the workload (the headline baseline),
+    plus single-thread samples of mode P and mode S (Algorithm 1) on the first `sample_tokens`
+    tokens.  The OpenMP leg runs in a subprocess (its library is process-global)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from oracle_timing import time_oracle
+    one = time_oracle(corpus, cfg, K, waves, "P", sample_tokens)
+    seq = time_oracle(corpus, cfg, K, waves, "S", sample_tokens)
+    out = None
+    try:
+        env = dict(os.environ, ORACLE_OPENMP="1")
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "oracle_timing.py"), "--config", cfg.name,
+                            "--topics", str(topics_arg), "--waves", str(waves), "--mode", "P"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        out = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:   # the single-thread numbers still stand
+        out = {"error": f"{type(e).__name__}: {e}"}
+    if "value" in out:
+        line = dict(out)
+        line["single_thread_mode_P"] = one
+        line["single_thread_mode_S"] = seq
+        return line
+    one["all_cores"] = out
+    one["single_thread_mode_S"] = seq
+    return one
 
 
 def mixing_transform(I, V, seed):
@@ -416,7 +430,7 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and transform is None:
         st = args.cpu_sample_tokens or min(N, 400_000 if K <= 100 else 100_000)
-        line["cpu_baseline"] = cpu_baseline(corpus, cfg, K, args.waves, st)
+        line["cpu_baseline"] = cpu_baseline(corpus, cfg, K, args.waves, st, K)
         line["cpu_baseline"]["cpu"] = cpu_model()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -487,9 +501,12 @@ def run_reference(args, cfg, K, world, rank, workload):
     no code; the CPU oracle is this tier's reference arm).  Rank 0 only."""
     if rank != 0:
         return
+    os.environ.setdefault("ORACLE_OPENMP", "1")      # the -fopenmp build of the same source, all host cores
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from oracle_timing import threads_used
     import synth
     corpus = synth.corpus_for(cfg)
-    sample = args.cpu_sample_tokens or min(corpus.num_tokens, 60_000 if K <= 100 else 20_000)
+    sample = args.cpu_sample_tokens or min(corpus.num_tokens, 1_000_000 if K <= 100 else 200_000)
     import oracle
     o = oracle.from_corpus(corpus, K, cfg.alpha, cfg.beta, cfg.discount, cfg.concentration, cfg.seed)
     for _ in range(args.warmup):
@@ -501,8 +518,9 @@ def run_reference(args, cfg, K, world, rank, workload):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
     value = sample / (ms / 1e3)
-    cb = {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-          "sample": f"first {sample} tokens of a mode-P (W={args.waves}) sweep of {cfg.name} per step"}
+    cb = {"value": value, "unit": "tokens/s", "cores": threads_used(), "kind": "oracle",
+          "sample": f"first {sample} tokens of a mode-P (W={args.waves}) sweep of {cfg.name} per step "
+                    f"(plain C oracle, fp64 log space; -fopenmp build over the wave's decisions)"}
     line = {"impl": "reference", "metric": "sampled tokens/sec per sweep", "value": round(value, 1),
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

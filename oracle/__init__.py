@@ -28,17 +28,26 @@ _lib = None
 P = C.c_void_p
 
 
-def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", _SRC, "-o", _LIB, "-lm"])
-    return _LIB
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
+def build(force: bool = False, openmp: bool = False) -> str:
+    """gcc -O2 build of spdp_oracle.c.  openmp=True: the same source with -fopenmp (mode P's
+    per-wave decisions over the host cores; the timing protocol of SURVEY §8(d) item (2))."""
+    out = _LIB_OMP if openmp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c11", *(["-fopenmp"] if openmp else []), "-shared", "-fPIC", _SRC,
+                               "-o", out, "-lm"])
+    return out
 
 
 def lib():
+    """The oracle library; ORACLE_OPENMP=1 loads the -fopenmp build (timing only)."""
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(_LIB)
+        omp = os.environ.get("ORACLE_OPENMP") == "1"
+        path = build(openmp=omp)
+        L = C.CDLL(path)
         L.or_philox.argtypes = [P, P, P]
         L.or_log_stirling.restype = C.c_double
         L.or_log_stirling.argtypes = [C.c_double, C.c_int, C.c_int]

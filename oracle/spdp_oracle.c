@@ -549,11 +549,22 @@ static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *forc
                 for (int64_t p = 0; p < N; p++)
                     if (shard[s->doc[p]] == g && s->pos[p] % W == wave) inwave[cnt++] = p;
             }
-            /* (1) every token decides against the wave-start snapshot */
-            for (int64_t q = 0; q < cnt; q++) {
+            /* (1) every token decides against the wave-start snapshot.  A max_tokens bound lets
+             * the shard's first max_tokens tokens (canonical order within each wave) through.
+             * The decisions are independent given the snapshot: the -fopenmp timing build
+             * (oracle.build(openmp=True)) spreads them over the host cores. */
+            int64_t take = cnt;
+            if (max_tokens >= 0) {
+                int64_t room = max_tokens - seen[g];
+                if (room < 0) room = 0;
+                if (take > room) take = room;
+            }
+            for (int64_t q = take; q < cnt; q++) kept[inwave[q]] = 2;   /* not sampled */
+            seen[g] += take;
+            #pragma omp parallel for schedule(dynamic, 64)
+            for (int64_t q = 0; q < take; q++) {
                 int64_t p = inwave[q];
-                if (max_tokens >= 0 && seen[g] >= max_tokens) { kept[p] = 2; continue; } /* not sampled */
-                seen[g]++;
+                double lw[2 * K], prob[2 * K];
                 int i = s->group[p], w = s->word[p], k0 = s->z[p];
                 size_t c = IDX3(s, i, w, k0);
                 uint32_t x[4];
@@ -569,7 +580,10 @@ static int sweep_par_impl(ostate *s, int W, int G, int only, const int32_t *forc
                 if (own_zr) own_zr[p] = newz[p] | (newr[p] << 15);
                 if (force_zr && force_zr[p] >= 0) {
                     int fz = force_zr[p] & 0x7FFF, fr = (force_zr[p] >> 15) & 1;
-                    if (fz != newz[p] || fr != newr[p]) s->stats[3]++;
+                    if (fz != newz[p] || fr != newr[p]) {
+                        #pragma omp atomic
+                        s->stats[3]++;
+                    }
                     newz[p] = fz; newr[p] = (int8_t)fr;
                 }
             }
