@@ -32,13 +32,16 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
 #ifndef SPDP_BULK_PREFETCH
-#define SPDP_BULK_PREFETCH 1       // HBM-resident rows: exact-byte cp.async.bulk.prefetch.L2 instead of 128-B line prefetches
+#define SPDP_BULK_PREFETCH 0       // 1: exact-byte cp.async.bulk.prefetch.L2 of the next batch instead of this batch's
+                                   // 128-B lines (B200, C5: 37.4 vs 34.7 ms per sweep with uint8 rows: fewer bytes, but
+                                   // the kernel is issue- and latency-bound and the extra record loads cost more)
 #endif
 #ifndef SPDP_PREFETCH_AHEAD
 #define SPDP_PREFETCH_AHEAD 1      // bulk prefetch: batches of 32 tokens ahead of the one being sampled
 #endif
 #ifndef SPDP_PAD_SELECT
-#define SPDP_PAD_SELECT 1          // loads of 4-topic blocks past K read the row's first block (no bytes past the row)
+#define SPDP_PAD_SELECT 0          // 1: loads of 4-topic blocks past K read the row's first block (no bytes past the
+                                   // row); B200, C5: 37.4 vs 33.8 ms per sweep (the address selects cost more)
 #endif
 #ifndef SPDP_SKIP_PAD_BLOCKS
 #define SPDP_SKIP_PAD_BLOCKS 1     // sample kernel: no row loads for 4-topic blocks past K
