@@ -294,11 +294,11 @@ def spdp_debug_chain(ctx, nsweeps, tbase=5):
 
 
 def spdp_stats(ctx):
-    out = np.zeros(16, np.int64)
+    out = np.zeros(20, np.int64)
     _check(lib().spdp_stats(ctx, _p(out)), ctx)
     keys = ["keeps", "moved", "clamped", "sweeps", "local_tokens", "local_docs", "m_max", "chunks",
             "lanes_per_token", "topics_per_lane", "chunk_tokens", "sample_grid", "token_kernel", "parts", "row_bytes",
-            "async"]
+            "async", "sparse_rows", "sparse_rows_lanes", "sparse_row_entries", "reserved"]
     return dict(zip(keys, (int(x) for x in out)))
 
 

@@ -14,6 +14,7 @@
 #include "spdp_token.cuh"
 #include "spdp_sparse.cuh"
 #include "spdp_seq.cuh"
+#include "spdp_sprows.cuh"
 
 // Doc-topic row element type of the context: fp32 (L2-resident arrays), uint16 or uint8 (HBM-bound
 // arrays; uint8 when every document has < 256 tokens).  Runs the statement with NT bound to it.
@@ -148,6 +149,11 @@ struct spdp_ctx {
     void* d_n = nullptr;                          // n_dk rows in sigma order: fp32, uint16 or uint8 (row_elem)
     int row_elem = 4;                             // bytes per doc-topic count: 4 (fp32), 2 (uint16), 1 (uint8)
     bool async = false;                           // SPDP_UPDATE_ASYNC (NEXT-2): immediate count updates
+    bool sprows = false;                          // sample from sparse doc-topic rows (spdp_sprows.cuh)
+    int sp_lpt = 8, sp_kspan = 256, sprows_grid = 0;
+    uint32_t* d_cap_ptr = nullptr;                // [D_local] first entry slot of each document (capacity min(L_d, K))
+    uint32_t* d_ent = nullptr;                    // entries k | n << 16
+    uint2* d_dinfo = nullptr;                     // {first entry, nonzero topics}
     bool seq = false;                             // num_waves = 0: exact sequential sampler (test mode, spdp_seq.cuh)
     uint32_t* d_pos = nullptr;                    // seq: canonical id -> sorted position
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
@@ -403,7 +409,48 @@ SweepArgs base_args(spdp_ctx* c) {
     a.I = c->I; a.K = c->K; a.Kp = c->Kp;
     a.key0 = (uint32_t)c->cfg.seed; a.key1 = (uint32_t)(c->cfg.seed >> 32);
     a.sweep = c->d_sweep; a.stats = c->d_stats;
+    a.dinfo = c->d_dinfo; a.ent = c->d_ent;
     return a;
+}
+
+// ---- sparse doc-topic rows
+#define SPDP_SPROWS_DISPATCH(LPT_, KS_, CALL)               \
+    switch ((LPT_) * 10000 + (KS_)) {                       \
+        case 80256: CALL(8, 256); break;                    \
+        case 160256: CALL(16, 256); break;                  \
+        case 320256: CALL(32, 256); break;                  \
+        case 81024: CALL(8, 1024); break;                   \
+        case 161024: CALL(16, 1024); break;                 \
+        case 321024: CALL(32, 1024); break;                 \
+        default: break;                                     \
+    }
+template <int LPT, int KS>
+void sprows_setup_t(spdp_ctx* c) {
+    const int smem = (int)sprow_smem_bytes<LPT, KS>();
+    cudaFuncSetAttribute(sample_sprows_kernel<LPT, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int nb = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sample_sprows_kernel<LPT, KS>, kSpWarps * 32, smem);
+    c->sprows_grid = std::max(nb, 1) * std::max(sms, 1);
+}
+template <int LPT, int KS>
+void launch_sprows_t(spdp_ctx* c, const SweepArgs& a) {
+    const int blocks = std::min((a.nchunks + kSpWarps - 1) / kSpWarps, c->sprows_grid);
+    if (blocks <= 0) return;
+    sample_sprows_kernel<LPT, KS><<<blocks, kSpWarps * 32, sprow_smem_bytes<LPT, KS>(), c->stream>>>(a);
+}
+void launch_sprows(spdp_ctx* c, const SweepArgs& a) {
+#define CALL_SR(L, KS) launch_sprows_t<L, KS>(c, a)
+    SPDP_SPROWS_DISPATCH(c->sp_lpt, c->sp_kspan, CALL_SR)
+#undef CALL_SR
+}
+// entries of every local document from its dense row (after the W = 1 recount and state installation)
+void rebuild_entries(spdp_ctx* c, cudaStream_t st) {
+    if (!c->sprows || c->Dloc == 0) return;
+    SPDP_ROWS(c->row_elem, rows_to_entries_kernel<NT><<<148 * 8, 256, 0, st>>>(
+                               (const NT*)c->d_n, c->d_sigma, c->Dloc, c->K, c->Kp, c->d_cap_ptr, c->d_ent, c->d_dinfo));
+    c->launches += 1;
 }
 
 int merge_grid() { return 148 * 4; }
@@ -648,6 +695,7 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     CU(cudaMemsetAsync(c->d_dt, 0, sizeof(int32_t) * c->cells, c->stream));
     if (c->d_Dloc) CU(cudaMemsetAsync(c->d_Dloc, 0, c->dbytes(), c->stream));
     launch_merge(c, c->d_dm, c->d_dt);    // zero deltas: recomputes Q and the sums
+    rebuild_entries(c, c->stream);
     if (c->sparse) sparse_install(c);
     s = check_launch(c, "install_state kernels");
     if (s) return s;
@@ -834,7 +882,8 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
                 a.chunk_seg = c->d_chunk_seg + cb;
                 a.nchunks = (int)(ce - cb);
                 a.work = c->d_work + p;
-                launch_sample(c, a, false);
+                if (c->sprows) launch_sprows(c, a);
+                else launch_sample(c, a, false);
             }
             const int blocks = (int)std::min<uint32_t>((re - rb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, st>>>(
@@ -862,6 +911,7 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
     const size_t rsm = sizeof(int) * 8 * (size_t)c->Kp;      // every token moved to zr_next: rebuild n, swap
     SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
                                                                             c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n));
+    rebuild_entries(c, st);
     std::swap(c->d_zr, c->d_zr_next);
     rec(c, 2);
     if (c->overlap) {
@@ -941,7 +991,8 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             a.chunk_seg = c->d_chunk_seg + cb;
             a.nchunks = (int)(ce - cb);
             a.work = c->d_work + w;
-            launch_sample(c, a, false);
+            if (c->sprows) launch_sprows(c, a);
+            else launch_sample(c, a, false);
         }
         rec(c, 4 * (size_t)w + 1);
         if (c->W == 1) {
@@ -949,6 +1000,7 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
             SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
                                        c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n));
+            rebuild_entries(c, c->stream);
             std::swap(c->d_zr, c->d_zr_next);
         } else {
             const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
@@ -1492,6 +1544,43 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         if (rb == 1 && maxlen >= 256) rb = 2;            // uint8 needs L_d < 2^8
         if (rb == 2 && maxlen >= 65536) rb = 4;          // uint16 needs L_d < 2^16
         c->row_elem = rb;
+    }
+    {   // sparse doc-topic rows: when the documents' expected nonzero topics (at a uniform random z, the
+        // start of every chain) cover < 40 % of a row; W = 1 wave updates, K > 64 (the chunk kernel's range)
+        const int K = c->K;
+        double exp_nnz = 0.0, cap = 0.0;
+        std::vector<uint32_t> capp((size_t)c->Dloc + 1, 0);
+        for (int32_t j = 0; j < c->Dloc; ++j) {
+            const int32_t L = c->doclen[(size_t)c->global_of_local[(size_t)j]];
+            exp_nnz += (double)K * (1.0 - std::pow(1.0 - 1.0 / K, (double)L));
+            const uint32_t cj = (uint32_t)std::min<int32_t>(L, K);
+            capp[(size_t)j + 1] = capp[(size_t)j] + cj;
+            cap += cj;
+        }
+        const double frac = c->Dloc ? exp_nnz / ((double)c->Dloc * K) : 1.0;
+        int32_t maxlen = 0;
+        for (int32_t dl : c->doclen) maxlen = std::max(maxlen, dl);
+        c->sprows = K > 64 && c->W == 1 && !c->async && !c->sparse && !c->seq && frac < 0.4 && maxlen < 65536 &&
+                    !c->token_kernel;
+        if (const char* e = getenv("SPDP_SPARSE_ROWS"))
+            c->sprows = atoi(e) != 0 && K > 64 && c->W == 1 && !c->async && !c->sparse && !c->seq && maxlen < 65536 &&
+                        !c->token_kernel;
+        if (c->sprows) {
+            const double mean_nnz = c->Dloc ? exp_nnz / c->Dloc : 0.0;
+            c->sp_lpt = mean_nnz <= 64 ? 8 : (mean_nnz <= 160 ? 16 : 32);
+            if (const char* e = getenv("SPDP_SPROWS_LPT")) {
+                const int v = atoi(e);
+                if (v == 8 || v == 16 || v == 32) c->sp_lpt = v;
+            }
+            c->sp_kspan = K <= 256 ? 256 : 1024;
+            ALLOC(c->d_cap_ptr, (size_t)c->Dloc + 1);
+            ALLOC(c->d_ent, std::max<size_t>((size_t)cap, 1));
+            ALLOC(c->d_dinfo, std::max<int32_t>(c->Dloc, 1));
+            CU(cudaMemcpy(c->d_cap_ptr, capp.data(), sizeof(uint32_t) * capp.size(), cudaMemcpyHostToDevice));
+#define CALL_SS(L, KS) sprows_setup_t<L, KS>(c)
+            SPDP_SPROWS_DISPATCH(c->sp_lpt, c->sp_kspan, CALL_SS)
+#undef CALL_SS
+        }
     }
     ALLOC(c->d_sigma, Kp);
     CU(cudaMemcpy(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice));
@@ -2355,6 +2444,15 @@ spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
     out[3] = c->sweeps_done; out[4] = c->Nloc; out[5] = c->Dloc; out[6] = c->mmax; out[7] = (int64_t)(size_t)c->nchunks;
     out[8] = c->LPT; out[9] = c->KPL; out[10] = c->chunk_tokens; out[11] = c->sample_grid;
     out[12] = c->token_kernel ? 1 : 0; out[13] = c->P; out[14] = c->row_elem; out[15] = c->async ? 1 : 0;
+    out[16] = c->sprows ? 1 : 0; out[17] = c->sprows ? c->sp_lpt : 0; out[18] = 0; out[19] = 0;
+    if (c->sprows && c->Dloc > 0) {   // entries of the last rebuild (sum of nonzero doc-topic counts)
+        std::vector<uint2> di((size_t)c->Dloc);
+        CU(cudaMemcpyAsync(di.data(), c->d_dinfo, sizeof(uint2) * di.size(), cudaMemcpyDeviceToHost, c->stream));
+        if ((s = sync(c, "stats entries"))) return s;
+        int64_t tot = 0;
+        for (const uint2& x : di) tot += x.y;
+        out[18] = tot;
+    }
     return SPDP_OK;
 }
 

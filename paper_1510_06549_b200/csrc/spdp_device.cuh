@@ -368,6 +368,9 @@ struct SweepArgs {
     // debug_probs
     double* dbg_w;                 // [ntok][2K] unnormalised weights, or null
     int32_t* dbg_info;             // [ntok][4]
+    // sparse doc-topic rows (spdp_sprows.cuh)
+    const uint2* dinfo;            // [D_local] {first entry, nonzero topics}
+    const uint32_t* ent;           // entries k | n << 16, topic order per document
 };
 
 // ---------------------------------------------------------------- the sample kernel

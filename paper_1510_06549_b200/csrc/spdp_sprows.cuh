@@ -1,0 +1,281 @@
+// spdp_sprows.cuh — the sample step on sparse doc-topic rows (HBM-bound, large-K configurations).
+//
+// Same method and same draw as sample_kernel (wave snapshot; Alg.1 with the keep
+// rule; Eqs. r0/r1; slot order j = 2k (r = 1), 2k + 1 (r = 0); j* = min{ j :
+// CDF_j > u * total }, reading c10), computed from a document's NONZERO counts:
+// a document of L_d tokens touches at most min(L_d, K) topics, so at K = 200 with
+// 62-token documents (C5) or K = 1000 with 125-token documents (C4) most of a dense
+// row is zeros.  With F_k the segment's slot factor and PA(k) = sum_{k' <= k}
+// alpha_ik' F_k' (a per-chunk fp64 prefix in shared memory), the topic-level CDF is
+//     C(k) = PA(k) + NS(k),   NS(k) = sum over the document's entries k_e <= k of n_e F_{k_e},
+// with the token's own topic k0 entering NS with its after-removal mass
+// (n0 - 1) Fk0 + alpha (Fk0 - F_k0) (Alg.1 lines 4-10).  C is increasing; its first
+// crossing of u * total is found entry by entry (LPT lanes per token, contiguous
+// entry ranges, one fp64 group scan), then inside the gap before the crossing entry
+// by binary search on PA (lane = token).  The r split uses the exact r = 1 share of
+// the chosen topic, as the dense kernel does.  Entries (k | n << 16, topic order) are
+// rebuilt from the dense rows after every sweep (rows_to_entries_kernel); the dense
+// rows stay the canonical state for every other consumer.
+#pragma once
+#include "spdp_device.cuh"
+
+namespace spdp {
+
+constexpr int kSpWarps = 4;
+
+template <int KSPAN>
+struct SpRowSmem {
+    double PA[KSPAN];       // inclusive prefix over k of alpha_ik F_k (fp64)
+    float F[KSPAN];         // F0 + F1 at the snapshot
+    float R1[KSPAN];        // r = 1 share F1 / F at the snapshot
+    uint32_t mt[KSPAN];     // snapshot m << 16 | t
+    int dmt[KSPAN];         // chunk deltas dm * 2^16 + dt
+    double target[32];      // hand-over, one per token of the batch
+    double base[32];        // NS before the gap
+    float hterm[32];        // NS term of the crossing entry (topic hi)
+    int lo[32], hi[32];     // gap [lo, hi); hi = the crossing entry's topic, or K (tail)
+};
+
+template <int LPT, int KSPAN>
+constexpr size_t sprow_smem_bytes() { return kSpWarps * sizeof(SpRowSmem<KSPAN>); }
+
+template <int LPT, int KSPAN>
+__global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs A) {
+    constexpr int TPW = 32 / LPT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    SpRowSmem<KSPAN>& S = reinterpret_cast<SpRowSmem<KSPAN>*>(smem_raw)[wid];
+    const int I = A.I, K = A.K, Kp = A.Kp;
+    unsigned keeps = 0, moved = 0;
+    const int g = lane / LPT, gl = lane % LPT;
+    const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
+    const uint32_t* __restrict__ ent = A.ent;
+
+  for (;;) {
+    uint32_t cc = 0;
+    if (lane == 0) cc = atomicAdd(A.work, 1u);
+    const int c = (int)__shfl_sync(0xffffffffu, cc, 0);
+    if (c >= A.nchunks) break;
+    __syncwarp();
+    const uint32_t seg = A.chunk_seg[c];
+    const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
+    const size_t row = (size_t)seg * Kp;
+    const float a = A.disc[i], b = A.conc[i];
+    const float2* __restrict__ tab = A.tab + A.tab_off[i];
+    const int32_t* __restrict__ Mi = A.M + (size_t)i * Kp;
+    const int32_t* __restrict__ Tti = A.Tt + (size_t)i * Kp;
+    const int32_t* __restrict__ Qw = A.Q + (size_t)w * Kp;
+    const float* __restrict__ alpha_i = A.alpha + (size_t)i * Kp;
+    const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
+
+    // ---- prologue: slot factors, r = 1 shares, alpha F into PA (prefix below)
+    for (int k = lane; k < KSPAN; k += 32) {
+        float F0 = 0.f, F1 = 0.f, al = 0.f;
+        int mv = 0, tv = 0;
+        if (k < K) {
+            mv = A.m[row + k];
+            tv = A.t[row + k];
+            al = alpha_i[k];
+            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+        }
+        const float Fk = F0 + F1;
+        S.F[k] = Fk;
+        S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
+        S.PA[k] = (double)__fmul_rn(al, Fk);
+        S.mt[k] = ((uint32_t)mv << 16) | (uint32_t)tv;
+        S.dmt[k] = 0;
+    }
+    __syncwarp();
+    {   // PA: lane-contiguous blocks of KSPAN/32, local prefix + warp exclusive scan (fp64)
+        constexpr int B = KSPAN / 32;
+        double run = 0.0;
+#pragma unroll
+        for (int j = 0; j < B; ++j) { run += S.PA[lane * B + j]; S.PA[lane * B + j] = run; }
+        double incl = run;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += y;
+        }
+        const double ex = incl - run;
+#pragma unroll
+        for (int j = 0; j < B; ++j) S.PA[lane * B + j] += ex;
+    }
+    __syncwarp();
+    const double PAtot = S.PA[K - 1];
+    const uint32_t sweep = *A.sweep;
+
+    for (uint32_t b0 = start; b0 < end; b0 += 32) {
+        const uint32_t nb = min(32u, end - b0);
+        // ======== phase 1: lane = token
+        const bool mine = (uint32_t)lane < nb;
+        const uint32_t p = b0 + lane;
+        uint32_t zr0 = 0, x0 = 0;
+        uint2 di = make_uint2(0u, 0u);
+        double u = 0.0;
+        if (mine) {
+            di = A.dinfo[A.tok_doc[p]];                      // {first entry, nonzero topics}
+            zr0 = A.zr[p];
+        }
+        const int k0 = (int)(zr0 & 0x7FFFu);
+        const uint32_t mt0 = S.mt[k0];
+        const int m0 = (int)(mt0 >> 16), t0 = (int)(mt0 & 0xFFFFu);
+        const int mm0 = max(m0 - 1, 0);
+        float2 tab_r1 = make_float2(0.f, 0.f), tab_r0 = make_float2(0.f, 0.f);
+        int Mk0 = 0, Ttk0 = 0, Qk0 = 0, Tk0 = 0;
+        if (mine) {
+            tab_r1 = tab[tri(mm0) + max(t0 - 1, 0)];
+            tab_r0 = tab[tri(mm0) + min(t0, mm0)];
+            Mk0 = Mi[k0]; Ttk0 = Tti[k0]; Qk0 = Qw[k0]; Tk0 = A.T[k0];
+            const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);    // a2
+            x0 = x.x;
+            u = u53(x);
+            if (A.prefetch_rows) {   // the document's entries towards L2 (1-2 lines)
+                const char* e0 = reinterpret_cast<const char*>(ent + di.x);
+                const char* e1 = reinterpret_cast<const char*>(ent + di.x + di.y);
+                for (const char* q = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(e0) & ~(uintptr_t)127); q < e1; q += 128)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+            }
+        }
+        const int rrem = removal_draw(x0, m0, t0);                                             // a3
+        const bool keep = rrem && t0 == 1 && m0 > 1;                                             // reading c5
+        float Fk0 = 0.f, R1k0 = 0.f;
+        if (mine) removal_factors_pre(rrem, m0, Mk0, Ttk0, Qk0, Tk0, tab_r1, tab_r0, a, b, A.beta, A.vbeta, Fk0, R1k0);
+        const float al0 = alpha_i[k0];
+        const float corr = __fmul_rn(al0, Fk0 - S.F[k0]);    // the alpha part of topic k0's change
+
+        // ======== phase 2: LPT lanes per token, contiguous entry ranges
+        for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
+            const uint32_t src = (s0 + g) & 31;
+            const bool valid = s0 + g < nb;
+            const int sk0 = __shfl_sync(0xffffffffu, k0, src);
+            const float sFk0 = __shfl_sync(0xffffffffu, Fk0, src);
+            const float scorr = __shfl_sync(0xffffffffu, corr, src);
+            const double su = __shfl_sync(0xffffffffu, u, src);
+            const uint32_t ptr = __shfl_sync(0xffffffffu, di.x, src);
+            const int nnz = valid ? (int)__shfl_sync(0xffffffffu, di.y, src) : 0;
+            const int cnt = (nnz + LPT - 1) / LPT;
+            const int j0 = min(gl * cnt, nnz), j1 = min(j0 + cnt, nnz);
+            // NS term of entry e: n F_k, or topic k0's after-removal change
+            auto term_of = [&](uint32_t e, int& k) {
+                k = (int)(e & 0xFFFFu);
+                const float n = (float)(e >> 16);
+                return (k == sk0) ? __fmaf_rn(n - 1.f, sFk0, scorr) : __fmul_rn(n, S.F[k]);
+            };
+            double loc = 0.0;
+            for (int j = j0; j < j1; ++j) {
+                int k;
+                loc += (double)term_of(ent[ptr + j], k);
+            }
+            double incl = loc;
+#pragma unroll
+            for (int off = 1; off < LPT; off <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
+                if (gl >= off) incl += y;
+            }
+            const double nstot = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
+            const double target = su * (PAtot + nstot);
+            // the first entry whose inclusive CDF C(k_e) = PA(k_e) + NS(k_e) exceeds the target
+            double run = incl - loc;
+            int prevk = -1, ck = -1, clo = 0;
+            float cterm = 0.f;
+            double cbase = 0.0;
+            if (j0 > 0 && j0 < j1) prevk = (int)(ent[ptr + j0 - 1] & 0xFFFFu);
+            for (int j = j0; j < j1; ++j) {
+                int k;
+                const float tm = term_of(ent[ptr + j], k);
+                if (ck < 0 && S.PA[k] + run + (double)tm > target) { ck = k; clo = prevk + 1; cbase = run; cterm = tm; }
+                run += (double)tm;
+                prevk = k;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, ck >= 0) & gmask;
+            const int last_gl = nnz > 0 ? (nnz - 1) / max(cnt, 1) : 0;   // the lane holding the last entry
+            const int winner = hit ? (__ffs(hit) - 1) : (g * LPT + last_gl);
+            if (lane == winner && valid) {
+                S.target[src] = target;
+                if (hit) { S.lo[src] = clo; S.hi[src] = ck; S.base[src] = cbase; S.hterm[src] = cterm; }
+                else { S.lo[src] = prevk + 1; S.hi[src] = K; S.base[src] = nstot; S.hterm[src] = 0.f; }   // tail gap
+            }
+        }
+        __syncwarp();
+
+        // ======== phase 3: lane = token; binary search in the gap, r split
+        if (mine) {
+            int ks = k0, rs = 1;
+            if (!keep) {
+                const double target = S.target[lane], base = S.base[lane];
+                const int lo = S.lo[lane], hi = S.hi[lane];
+                int L = lo, H = hi;                         // first k in [lo, hi) with PA(k) + base > target
+                while (L < H) {
+                    const int mid = (L + H) >> 1;
+                    if (S.PA[mid] + base > target) H = mid; else L = mid + 1;
+                }
+                if (L < K) {
+                    ks = L;
+                    const double before = (ks > 0 ? S.PA[ks - 1] : 0.0) + base;
+                    const float mass = __fmaf_rn(alpha_i[ks], S.F[ks], (ks == hi) ? S.hterm[lane] : 0.f);
+                    const float R1s = (ks == k0) ? R1k0 : S.R1[ks];
+                    rs = (before + (double)__fmul_rn(mass, R1s) > target) ? 1 : 0;
+                } else {                                    // rounding: the last positive slot
+                    ks = K - 1;
+                    rs = (((ks == k0) ? m0 - 1 : (int)(S.mt[ks] >> 16)) > 0) ? 0 : 1;
+                }
+            }
+            A.zr_next[p] = (uint16_t)(ks | (rs << 15));                                         // a7
+            if (keep) ++keeps;
+            else {
+                atomicAdd(&S.dmt[k0], -65536 - rrem);
+                atomicAdd(&S.dmt[ks], 65536 + rs);
+                moved += (ks != k0);
+            }
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    for (int k = lane; k < K; k += 32) {
+        const int x = S.dmt[k];
+        if (x) {
+            const int dtv = (int)(short)(x & 0xFFFF);
+            const int dmv = (x - dtv) >> 16;
+            if (dmv) atomicAdd(A.dm + row + k, dmv);
+            if (dtv) atomicAdd(A.dt + row + k, dtv);
+        }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        keeps += __shfl_xor_sync(0xffffffffu, keeps, off);
+        moved += __shfl_xor_sync(0xffffffffu, moved, off);
+    }
+    if (lane == 0 && (keeps | moved)) {
+        atomicAdd(A.stats + 0, (unsigned long long)keeps);
+        atomicAdd(A.stats + 1, (unsigned long long)moved);
+    }
+}
+
+// After every W = 1 sweep (and at state installation): a document's dense row (sigma order) ->
+// its nonzero counts as entries k | n << 16 in topic order at ent[cap_ptr[d] ...]; dinfo[d] =
+// {first entry, count}.  One warp per document.
+template <typename NT>
+__global__ void rows_to_entries_kernel(const NT* __restrict__ n, const int* __restrict__ sigma, int D, int K, int Kp,
+                                       const uint32_t* __restrict__ cap_ptr, uint32_t* __restrict__ ent,
+                                       uint2* __restrict__ dinfo) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int d = blockIdx.x * wpb + (threadIdx.x >> 5); d < D; d += gridDim.x * wpb) {
+        const NT* row = n + (size_t)d * Kp;
+        const uint32_t e0 = cap_ptr[d];
+        uint32_t cnt = 0;
+        for (int kb = 0; kb < K; kb += 32) {
+            const int k = kb + lane;
+            const int v = (k < K) ? Row<NT>::get(row + sigma[k]) : 0;
+            const unsigned bal = __ballot_sync(0xffffffffu, v > 0);
+            if (v > 0) ent[e0 + cnt + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)k | ((uint32_t)v << 16);
+            cnt += __popc(bal);
+        }
+        if (lane == 0) dinfo[d] = make_uint2(e0, cnt);
+    }
+}
+
+}  // namespace spdp

@@ -11,6 +11,7 @@ within 1e-6 of a CDF boundary; counts bit-exact once the draws agree (lock-step)
     every sweep: M_max 1870 / 4898 > 512-token chunks);
   * the full-size bench workload C3 (one lock-step sweep of all 10 M tokens),
     and the library's recount of n and m from z at full size (C3, C5);
+  * the sparse-row sample kernel (C5, C4 K >= 300 default) at every shape;
   * every cell of the device Stirling-ratio table (Eqs. r0/r1 P:1683)
     against the oracle's log-space table up to m = 5000 (> C5's M_max).
 """
@@ -77,6 +78,30 @@ def test_narrow_rows_conditionals(monkeypatch, rowb):
         assert (info[j, 0], info[j, 1]) == (d["r_rem"], d["keep"])
         big = d["prob"] >= 1e-30
         assert (np.abs(gp[j][big] - d["prob"][big]) / d["prob"][big]).max() <= 1e-5
+
+
+@pytest.mark.parametrize("rowb", [4, 2, 1])
+@pytest.mark.parametrize("K,lpt", [(100, 8), (200, 8), (200, 16), (300, 16), (1000, 32), (1000, 8)])
+def test_sparse_rows_lockstep(monkeypatch, K, lpt, rowb):
+    """The sparse-row sample kernel (spdp_sprows.cuh: nonzero doc-topic counts + a per-chunk alpha-F
+    prefix, crossing entry then binary search) at every lanes-per-token and topic span, each row type."""
+    monkeypatch.setenv("SPDP_SPARSE_ROWS", "1")
+    monkeypatch.setenv("SPDP_SPROWS_LPT", str(lpt))
+    monkeypatch.setenv("SPDP_ROW_BYTES", str(rowb))
+    c = synth.generate(2, 30, 40.0, 300, 8, seed=K + lpt)
+    g = _lockstep(c, K, 1, 3)
+    st = g.stats()
+    assert st["sparse_rows"] == 1 and st["sparse_rows_lanes"] == lpt and st["row_bytes"] == rowb
+    n = g.counts(z=False, r=False, customers=False, tables=False, shadow=False)["n"]
+    assert st["sparse_row_entries"] == int((n > 0).sum())
+
+
+@pytest.mark.parametrize("name,K", [("C1", 200), ("C2", 300)])
+def test_sparse_rows_split_segments_lockstep(monkeypatch, name, K):
+    monkeypatch.setenv("SPDP_SPARSE_ROWS", "1")
+    monkeypatch.setenv("SPDP_CHUNK_TOKENS", "64")
+    g = _lockstep(corpus(name), K, 1, 2)
+    assert g.stats()["sparse_rows"] == 1
 
 
 @pytest.mark.parametrize("name,K,extra", [("C1", 100, {}), ("C1", 200, {"SPDP_ROW16": "1"}), ("C1", 200, {"SPDP_ROW8": "1"}),
