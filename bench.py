@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--update", default="wave", choices=["wave", "async"],
                     help="async: NEXT-2, the paper's immediate-update in-GPU scheme (nondeterministic)")
     ap.add_argument("--train-sweeps", type=int, default=20)
+    ap.add_argument("--largest", default="C5", help="also time the largest config on the same GPUs ('' = skip)")
+    ap.add_argument("--largest-steps", type=int, default=10)
+    ap.add_argument("--largest-warmup", type=int, default=3)
     return ap.parse_args()
 
 
@@ -239,9 +242,110 @@ def cpu_model():
     return "unknown"
 
 
+def recorded_ppl_gap(waves, update):
+    """The BASELINE metric's third part, from the latest committed measurement (tools/ppl_gap.py:
+    training perplexity after 100 sweeps of C2, 3 seeds per schedule, against the exact sequential
+    sampler, i.e. the oracle's Algorithm 1); not re-measured here (the oracle chains take ~10 CPU-minutes)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ppl_gap_C2*.jsonl")))
+    summary, src = {}, []
+    for f in files:                     # later files refine earlier ones (same corpus, seeds, oracle chains)
+        for ln in open(f):
+            d = json.loads(ln)
+            if "summary" in d:
+                summary.update(d["summary"]["final"])
+                src.append(os.path.relpath(f, ROOT))
+    if not summary:
+        return None
+    this = "gpu async (NEXT-2)" if update == "async" else f"gpu W={waves}"
+    return {"config": "C2 (1 M tokens, K = 50), 100 sweeps, seeds 7/8/9", "reference": "oracle sequential (Alg.1)",
+            "this_schedule": this, "this_schedule_gap_pct": summary.get(this, {}).get("gap_vs_sequential_pct"),
+            "by_schedule": summary, "files": src}
+
+
+def measure_largest(args, spdp, torch, dist, world, rank, local_rank, stream, barrier, peak):
+    """The largest BASELINE config (C5, ~200 M tokens, K = 200) on the same GPUs: device-resident sweep
+    throughput and the sample kernel's roofline (no e2e / CPU legs), so that every driver run records it."""
+    import synth
+    cfg = synth.CONFIGS[args.largest]
+    corpus = synth.corpus_for(cfg)
+    N = corpus.num_tokens
+    uid = None
+    if world > 1:
+        t = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            t = torch.tensor(list(spdp.spdp_nccl_unique_id()), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        uid = bytes(t.tolist())
+    g = spdp.Sampler(cfg.groups, cfg.vocab, cfg.k, alpha=cfg.alpha, beta=cfg.beta, discount=cfg.discount,
+                     concentration=cfg.concentration, seed=cfg.seed, num_waves=1, device=local_rank, rank=rank,
+                     world_size=world, nccl_unique_id=uid, stream=stream.cuda_stream)
+    t0 = time.perf_counter()
+    g.load_corpus(corpus.group, corpus.doc, corpus.word, corpus.num_docs)
+    load_s = time.perf_counter() - t0
+    for _ in range(args.largest_warmup):
+        g.sweep(1)
+
+    def timed(steps):
+        evs = []
+        torch.cuda.synchronize(); barrier()
+        for _ in range(steps):
+            s_ = torch.cuda.Event(enable_timing=True); e_ = torch.cuda.Event(enable_timing=True)
+            s_.record(stream); g.sweep(1); e_.record(stream)
+            evs.append((s_, e_))
+        torch.cuda.synchronize(); barrier()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    step_ms = timed(args.largest_steps)
+    g.profile(True)
+    timed(max(3, min(args.largest_steps, 10)))
+    tm = g.timings()
+    g.profile(False)
+    stats = g.stats()
+    g.close()
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sample_ms = tm["sample_ms"] / max(tm["sweeps"], 1)
+    shard_docs = None
+    if world > 1:
+        part = spdp.spdp_partition(cfg.seed, world, corpus.doc, corpus.num_docs)
+        shard_docs = np.nonzero(part == rank)[0]
+    plan = plan_stats(corpus, shard_docs, 1)
+    if stats.get("sparse_rows"):       # entries (4 B each) + the document's {first entry, count} record
+        bytes_sweep = plan["tokens"] * (12 + 8) + stats["sparse_row_entries_read"] * 4 + plan["segments"] * 28 * cfg.k
+        model = "sparse rows: per token 12 B record + 8 B doc record + (its document's entries x 4 B); per segment 28K B"
+    else:
+        bytes_sweep = alg_bytes(plan, cfg.k, stats.get("row_bytes", 4))
+        model = f"dense rows: per token 12 B + {stats.get('row_bytes', 4)}K B; per segment 28K B"
+    bytes_i32 = alg_bytes(plan, cfg.k, 4)
+    ach = bytes_sweep / (sample_ms / 1e3) / 1e9
+    nc = ncu_summary(cfg.name, cfg.k, "sample")
+    return {"workload": f"{cfg.name}: I={cfg.groups} groups x {cfg.docs_per_group} docs, mean len {cfg.mean_len}, "
+                        f"V={cfg.vocab}, K={cfg.k}, W=1", "tokens": N, "value": round(N / (ms / 1e3), 1), "unit": "tokens/s",
+            "ms_per_step": round(ms, 4), "steps": args.largest_steps, "warmup": args.largest_warmup,
+            "sweep_ms": [round(x, 3) for x in step_ms], "load_s": round(load_s, 3),
+            "sample_ms_per_sweep": round(sample_ms, 4),
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "byte_model": model,
+                         "int32_model": {"achieved": round(bytes_i32 / (sample_ms / 1e3) / 1e9, 1),
+                                         "frac": round(bytes_i32 / (sample_ms / 1e3) / 1e9 / peak, 4)},
+                         "traffic": nc.get("dram_bytes_per_launch"), "ncu": {k: nc.get(k) for k in (
+                             "file", "kernel", "duration_ms", "dram_bytes_per_launch", "l2_hit_pct", "issue_active_pct",
+                             "warp_instructions")} if nc else None},
+            "stats": {k: stats.get(k) for k in ("row_bytes", "sparse_rows", "sparse_rows_lanes", "sparse_row_entries",
+                                                "lanes_per_token", "topics_per_lane", "m_max", "parts", "local_tokens")},
+            "timings_ms": {k: round(v, 3) for k, v in tm.items()}}
+
+
 # ------------------------------------------------------------------ main
 def main():
     args = parse()
+    world0 = int(os.environ.get("WORLD_SIZE", "1"))
+    if world0 > 1 and "OMP_NUM_THREADS" not in os.environ:   # corpus generation threads: share the host cores
+        os.environ["OMP_NUM_THREADS"] = str(max(1, (os.cpu_count() or 1) // world0))
     import synth
     cfg = synth.CONFIGS[args.config]
     K = args.topics or cfg.k
@@ -428,10 +532,17 @@ def main():
         "stats": stats,
         "timings_ms": {k: round(v, 4) for k, v in tm.items()},
     }
+    line["perplexity_gap"] = recorded_ppl_gap(args.waves, args.update)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and transform is None:
         st = args.cpu_sample_tokens or min(N, 400_000 if K <= 100 else 100_000)
         line["cpu_baseline"] = cpu_baseline(corpus, cfg, K, args.waves, st, K)
         line["cpu_baseline"]["cpu"] = cpu_model()
+    if args.largest and args.largest != args.config and transform is None and args.update == "wave":
+        del corpus
+        try:
+            line["largest_config"] = measure_largest(args, spdp, torch, dist, world, rank, local_rank, stream, barrier, peak)
+        except Exception as e:   # the headline line stands without it
+            line["largest_config"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -330,7 +330,8 @@ spdp_status spdp_debug_ratio_table(spdp_ctx* ctx, int32_t group, int32_t mmax, f
  * token kernel samples (K <= 64), out[13] word-range parts of the sweep
  * (exchange pipelining), out[14] bytes per doc-topic count (4 fp32, 2 uint16, 1 uint8), out[15] 1
  * for SPDP_UPDATE_ASYNC, out[16] 1 if the sweep samples from sparse doc-topic rows, out[17] their
- * lanes per token, out[18] their entries (nonzero doc-topic counts of this rank), out[19] 0 (reserved).
+ * lanes per token, out[18] their entries (nonzero doc-topic counts of this rank), out[19] the entries
+ * one sweep reads (sum over documents of length x entries).
  * out has 20 slots. */
 spdp_status spdp_stats(spdp_ctx* ctx, int64_t* out);
 

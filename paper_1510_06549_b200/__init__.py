@@ -298,7 +298,7 @@ def spdp_stats(ctx):
     _check(lib().spdp_stats(ctx, _p(out)), ctx)
     keys = ["keeps", "moved", "clamped", "sweeps", "local_tokens", "local_docs", "m_max", "chunks",
             "lanes_per_token", "topics_per_lane", "chunk_tokens", "sample_grid", "token_kernel", "parts", "row_bytes",
-            "async", "sparse_rows", "sparse_rows_lanes", "sparse_row_entries", "reserved"]
+            "async", "sparse_rows", "sparse_rows_lanes", "sparse_row_entries", "sparse_row_entries_read"]
     return dict(zip(keys, (int(x) for x in out)))
 
 

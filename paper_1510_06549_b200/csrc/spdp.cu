@@ -160,6 +160,9 @@ struct spdp_ctx {
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
     float* d_R1 = nullptr;                        // token kernel: r = 1 shares [run][Kp]
+    float* d_aF = nullptr;                        // token kernel: alpha F [run][Kp]
+    uint32_t* d_MT = nullptr;                     // token kernel: snapshot m << 16 | t [run][Kp]
+    float4* d_FR = nullptr;                       // token kernel: own-removal factor parts [run][Kp]
     // NEXT-4: sparse transformation matrices P^i (spdp_set_transform)
     bool sparse = false;
     std::vector<int32_t> h_pptr, h_pv;            // caller's rows (i, w): i * V + w
@@ -363,8 +366,10 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     const int fgrid = (int)std::min<size_t>((nf + 255) / 256, 148u * 16u);
     factor_kernel<<<std::max(fgrid, 1), 256, 0, c->stream>>>(
         c->d_wave_segs, r0, r1, c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->d_disc, c->d_conc, c->d_tab,
-        c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F, c->d_R1);
+        c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F, c->d_R1,
+        c->d_alpha, c->d_aF, c->d_MT, c->d_FR);
     TokenArgs t{};
+    t.aF = c->d_aF; t.MT = c->d_MT; t.FR = c->d_FR;
     t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
     t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.F = c->d_F; t.R1 = c->d_R1; t.n = c->d_n;
     t.sigma = c->d_sigma;
@@ -1416,6 +1421,11 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
                 ALLOC(c->d_tok_run, nl);
                 ALLOC(c->d_F, (size_t)R * Kp);
                 ALLOC(c->d_R1, (size_t)R * Kp);
+                if (c->token_kernel) {
+                    ALLOC(c->d_aF, (size_t)R * Kp);
+                    ALLOC(c->d_MT, (size_t)R * Kp);
+                    ALLOC(c->d_FR, (size_t)R * Kp);
+                }
                 token_run_kernel<<<grid, 256, 0, st>>>(droff.p, drlen.p, R, c->d_tok_run);
             }
             chunk_count_kernel<<<grid, 256, 0, st>>>(drlen.p, R, chunk, dnch.p);
@@ -2449,9 +2459,13 @@ spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
         std::vector<uint2> di((size_t)c->Dloc);
         CU(cudaMemcpyAsync(di.data(), c->d_dinfo, sizeof(uint2) * di.size(), cudaMemcpyDeviceToHost, c->stream));
         if ((s = sync(c, "stats entries"))) return s;
-        int64_t tot = 0;
-        for (const uint2& x : di) tot += x.y;
+        int64_t tot = 0, per_tok = 0;
+        for (size_t j = 0; j < di.size(); ++j) {
+            tot += di[j].y;
+            per_tok += (int64_t)di[j].y * c->doclen[(size_t)c->global_of_local[j]];   // entries read per sweep
+        }
         out[18] = tot;
+        out[19] = per_tok;
     }
     return SPDP_OK;
 }

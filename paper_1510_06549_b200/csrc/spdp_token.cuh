@@ -27,32 +27,55 @@
 
 namespace spdp {
 
-// F[r][k] for the runs (segments) [r0, r1) of one wave
+#ifndef SPDP_TOKEN_PRE
+#define SPDP_TOKEN_PRE 1            // factor_kernel also writes alpha F, the packed (m, t) and topic k's own-removal
+                                    // factor parts per (run, k): the token kernel's dependent-load chain loses the
+                                    // (m, t) -> Stirling-table -> sums levels
+#endif
+
+// F[r][k] (and R1, aF, MT, FR) for the runs (segments) [r0, r1) of one wave
 __global__ void factor_kernel(const uint32_t* __restrict__ run_seg, uint32_t r0, uint32_t r1,
                               const int32_t* __restrict__ m, const int32_t* __restrict__ t,
                               const int32_t* __restrict__ Q, const int32_t* __restrict__ M,
                               const int32_t* __restrict__ Tt, const int32_t* __restrict__ T,
                               const float* __restrict__ disc, const float* __restrict__ conc,
                               const float2* __restrict__ tab, const uint64_t* __restrict__ tab_off, float beta,
-                              float vbeta, int I, int K, int Kp, float* __restrict__ F, float* __restrict__ R1) {
+                              float vbeta, int I, int K, int Kp, float* __restrict__ F, float* __restrict__ R1,
+                              const float* __restrict__ alpha, float* __restrict__ aF, uint32_t* __restrict__ MT,
+                              float4* __restrict__ FR) {
     const size_t n = (size_t)(r1 - r0) * Kp;
     for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
         const uint32_t r = r0 + (uint32_t)(j / Kp);
         const int k = (int)(j % Kp);
-        float Fk = 0.f, Rk = 0.f;
+        float Fk = 0.f, Rk = 0.f, al = 0.f;
+        int mv = 0, tv = 0;
+        float4 fr = make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < K) {
             const uint32_t seg = run_seg[r];
             const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
             const size_t cell = (size_t)seg * Kp + k;
-            const int mv = m[cell], tv = t[cell];
+            mv = m[cell]; tv = t[cell];
+            const int Mv = M[(size_t)i * Kp + k], Ttv = Tt[(size_t)i * Kp + k], Qv = Q[(size_t)w * Kp + k], Tv = T[k];
+            const float2* tb = tab + tab_off[i];
+            const float a = disc[i], b = conc[i];
             float F0, F1;
-            slot_factors(M[(size_t)i * Kp + k], Tt[(size_t)i * Kp + k], Q[(size_t)w * Kp + k], T[k],
-                         tab[tab_off[i] + tri(mv) + tv], disc[i], conc[i], beta, vbeta, F0, F1);
+            slot_factors(Mv, Ttv, Qv, Tv, tb[tri(mv) + tv], a, b, beta, vbeta, F0, F1);
             Fk = F0 + F1;
             Rk = (F1 > 0.f) ? __fdiv_rn(F1, F0 + F1) : 0.f;     // exact r = 1 share of the slot pair
+            al = alpha[(size_t)i * Kp + k];
+            if (SPDP_TOKEN_PRE && mv > 0) {   // a token of topic k leaving this segment (Alg.1 lines 4-10)
+                const int mm = mv - 1;
+                slot_factors(Mv - 1, Ttv, Qv, Tv, tb[tri(mm) + min(tv, mm)], a, b, beta, vbeta, fr.x, fr.y);         // r_rem = 0
+                slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, tb[tri(mm) + max(tv - 1, 0)], a, b, beta, vbeta, fr.z, fr.w);  // r_rem = 1
+            }
         }
         F[(size_t)r * Kp + k] = Fk;
         R1[(size_t)r * Kp + k] = Rk;
+        if (SPDP_TOKEN_PRE) {
+            aF[(size_t)r * Kp + k] = __fmul_rn(al, Fk);
+            MT[(size_t)r * Kp + k] = ((uint32_t)mv << 16) | (uint32_t)tv;
+            FR[(size_t)r * Kp + k] = fr;
+        }
     }
 }
 
@@ -65,6 +88,9 @@ struct TokenArgs {
     uint16_t* zr_next;
     const float* F;                // [run][Kp]
     const float* R1;               // [run][Kp] r = 1 share F1 / F at the snapshot
+    const float* aF;               // [run][Kp] alpha_ik F (SPDP_TOKEN_PRE)
+    const uint32_t* MT;            // [run][Kp] snapshot m << 16 | t
+    const float4* FR;              // [run][Kp] own-removal factor parts (F0, F1) for r_rem = 0, then r_rem = 1
     const void* n;                 // doc-topic rows (sigma layout of the chunk kernel)
     const int* sigma;              // [Kp] in-row position of topic k
     int bpos[32];                  // in-row position (float4 units) of 4-topic block B
@@ -102,26 +128,40 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
         const int k0 = (int)(zr0 & 0x7FFFu);
         const uint4 x = philox(make_uint4(A.tok_id[p], sweep, 0u, 0u), A.key0, A.key1);      // a2
         const size_t cell0 = (size_t)seg * Kp + k0;
-        const int m0 = A.m[cell0], t0 = A.t[cell0];
+        int m0, t0;
+        if constexpr (SPDP_TOKEN_PRE) {
+            const uint32_t mt = A.MT[(size_t)run * Kp + k0];
+            m0 = (int)(mt >> 16); t0 = (int)(mt & 0xFFFFu);
+        } else {
+            m0 = A.m[cell0]; t0 = A.t[cell0];
+        }
         const int rrem = removal_draw(x.x, m0, t0);                                             // a3
         const bool keep = rrem && t0 == 1 && m0 > 1;                                             // reading c5
         int ks = k0, rs = 1;
         if (!keep) {
-            const float a = A.disc[i], b = A.conc[i];
-            const float2* __restrict__ tab = A.tab + A.tab_off[i];
-            const int32_t* Mi = A.M + (size_t)i * Kp;
-            const int32_t* Tti = A.Tt + (size_t)i * Kp;
-            const int32_t* Qw = A.Q + (size_t)w * Kp;
             float Fk0, R1k0;
-            removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+            if constexpr (SPDP_TOKEN_PRE) {   // the factor kernel's own-removal parts for this r_rem
+                const float4 fr = A.FR[(size_t)run * Kp + k0];
+                const float x0 = rrem ? fr.z : fr.x, x1 = rrem ? fr.w : fr.y;
+                Fk0 = x0 + x1;
+                R1k0 = (x1 > 0.f) ? __fdiv_rn(x1, Fk0) : 0.f;
+            } else {
+                const float a = A.disc[i], b = A.conc[i];
+                const float2* __restrict__ tab = A.tab + A.tab_off[i];
+                const int32_t* Mi = A.M + (size_t)i * Kp;
+                const int32_t* Tti = A.Tt + (size_t)i * Kp;
+                const int32_t* Qw = A.Q + (size_t)w * Kp;
+                removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
+            }
             const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * Kp;
             const float* Frow = A.F + (size_t)run * Kp;
+            const float* aFrow = A.aF + (size_t)run * Kp;
             const float* al = A.alpha + (size_t)i * Kp;
             // own topic: the after-removal mass replaces the snapshot mass (block sum + difference,
             // as the chunk kernel does)
             const float n0 = Row<NT>::load1(nrow + A.sigma[k0]);
             const float al0 = al[k0], F0k = Frow[k0];
-            const float wold = __fmaf_rn(n0, F0k, __fmul_rn(al0, F0k));
+            const float wold = SPDP_TOKEN_PRE ? __fmaf_rn(n0, F0k, aFrow[k0]) : __fmaf_rn(n0, F0k, __fmul_rn(al0, F0k));
             const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
             const float dlt = wnew - wold;
             // a4/a5: masses in 4-topic blocks
@@ -134,9 +174,16 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
                 if (B < nbk) {
                     const float4 n4 = Row<NT>::load4(nrow + 4 * A.bpos[B]);
                     const float4 F4 = *reinterpret_cast<const float4*>(Frow + 4 * B);
-                    const float4 a4 = *reinterpret_cast<const float4*>(al + 4 * B);
-                    float bsv = (__fmaf_rn(n4.x, F4.x, __fmul_rn(a4.x, F4.x)) + __fmaf_rn(n4.y, F4.y, __fmul_rn(a4.y, F4.y))) +
-                                (__fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)) + __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w)));
+                    float bsv;
+                    if constexpr (SPDP_TOKEN_PRE) {
+                        const float4 f4 = *reinterpret_cast<const float4*>(aFrow + 4 * B);
+                        bsv = (__fmaf_rn(n4.x, F4.x, f4.x) + __fmaf_rn(n4.y, F4.y, f4.y)) +
+                              (__fmaf_rn(n4.z, F4.z, f4.z) + __fmaf_rn(n4.w, F4.w, f4.w));
+                    } else {
+                        const float4 a4 = *reinterpret_cast<const float4*>(al + 4 * B);
+                        bsv = (__fmaf_rn(n4.x, F4.x, __fmul_rn(a4.x, F4.x)) + __fmaf_rn(n4.y, F4.y, __fmul_rn(a4.y, F4.y))) +
+                              (__fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)) + __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w)));
+                    }
                     if ((k0 >> 2) == B) bsv += dlt;
                     BS(B) = bsv;
                     total += (double)bsv;
@@ -164,9 +211,16 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
             for (int B = 0; B < NBK; ++B) if (B == qs) bq = A.bpos[B];
             const float4 n4 = Row<NT>::load4(nrow + 4 * bq);
             const float4 F4 = *reinterpret_cast<const float4*>(Frow + 4 * qs);
-            const float4 a4 = *reinterpret_cast<const float4*>(al + 4 * qs);
-            float wq[4] = {__fmaf_rn(n4.x, F4.x, __fmul_rn(a4.x, F4.x)), __fmaf_rn(n4.y, F4.y, __fmul_rn(a4.y, F4.y)),
-                           __fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)), __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w))};
+            float wq[4];
+            if constexpr (SPDP_TOKEN_PRE) {
+                const float4 f4 = *reinterpret_cast<const float4*>(aFrow + 4 * qs);
+                wq[0] = __fmaf_rn(n4.x, F4.x, f4.x); wq[1] = __fmaf_rn(n4.y, F4.y, f4.y);
+                wq[2] = __fmaf_rn(n4.z, F4.z, f4.z); wq[3] = __fmaf_rn(n4.w, F4.w, f4.w);
+            } else {
+                const float4 a4 = *reinterpret_cast<const float4*>(al + 4 * qs);
+                wq[0] = __fmaf_rn(n4.x, F4.x, __fmul_rn(a4.x, F4.x)); wq[1] = __fmaf_rn(n4.y, F4.y, __fmul_rn(a4.y, F4.y));
+                wq[2] = __fmaf_rn(n4.z, F4.z, __fmul_rn(a4.z, F4.z)); wq[3] = __fmaf_rn(n4.w, F4.w, __fmul_rn(a4.w, F4.w));
+            }
 #pragma unroll
             for (int e = 0; e < 4; ++e) if (4 * qs + e == k0) wq[e] = wnew;
             double r3 = bbeg, bes = bbeg, blast = bbeg;
@@ -188,7 +242,7 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
             const float w1 = wsel * R1s;
             if (!fb) rs = (bes + (double)w1 > target) ? 1 : 0;
             else {                                                                  // last positive slot
-                const int ms = own ? m0 - 1 : A.m[(size_t)seg * Kp + ks];
+                const int ms = own ? m0 - 1 : (SPDP_TOKEN_PRE ? (int)(A.MT[(size_t)run * Kp + ks] >> 16) : A.m[(size_t)seg * Kp + ks]);
                 rs = (ms > 0) ? 0 : 1;
             }
             // a7: packed deltas (dm * 2^16 + dt) of the two cells
