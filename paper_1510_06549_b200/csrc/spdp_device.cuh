@@ -31,6 +31,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_PREFETCH_NEXT
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
+#ifndef SPDP_PRO_GROUP
+#define SPDP_PRO_GROUP 4           // chunk prologue: topics per lane whose loads are issued together
+#endif
 #ifndef SPDP_BULK_PREFETCH
 #define SPDP_BULK_PREFETCH 0       // 1: exact-byte cp.async.bulk.prefetch.L2 of the next batch instead of this batch's
                                    // 128-B lines (B200, C5: 37.4 vs 34.7 ms per sweep with uint8 rows: fewer bytes, but
@@ -482,27 +485,53 @@ sample_kernel(SweepArgs A) {
     const float* __restrict__ alpha_i = A.alpha + (size_t)i * Kp;
 
     const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
-    // ---- prologue: the segment's slot factors at the wave-start snapshot
-    for (int k = lane; k < KSPAN; k += 32) {
-        float F0 = 0.f, F1 = 0.f, al = 0.f;
-        int mv = 0, tv = 0;
-        if (k < K) {
-            mv = ldc<ASYNC>(A.m + row + k);
-            tv = ldc<ASYNC>(A.t + row + k);
-            if constexpr (ASYNC) {                    // valid range of the local copy (reading c14)
-                mv = max(mv, 0);
-                tv = mv > 0 ? min(max(tv, 1), mv) : 0;
+    // ---- prologue: the segment's slot factors at the wave-start snapshot.  Topics in groups of
+    // PG per lane: all count loads of a group first, then its Stirling-table loads, then the math,
+    // so each group costs two memory round trips instead of two per topic.
+    {
+        constexpr int PER = (KSPAN + 31) / 32;
+        constexpr int PG = SPDP_PRO_GROUP < PER ? SPDP_PRO_GROUP : PER;
+        static_assert(PER % PG == 0, "prologue group must divide the topics per lane");
+#pragma unroll 1
+        for (int k0g = 0; k0g < PER; k0g += PG) {
+            int mv[PG], tv[PG], Mv[PG], Ttv[PG], Qv[PG], Tv[PG];
+            float al[PG];
+            float2 tb[PG];
+#pragma unroll
+            for (int j = 0; j < PG; ++j) {
+                const int k = lane + 32 * (k0g + j);
+                mv[j] = tv[j] = Mv[j] = Ttv[j] = Qv[j] = Tv[j] = 0;
+                al[j] = 0.f;
+                if (k < K) {
+                    mv[j] = ldc<ASYNC>(A.m + row + k);
+                    tv[j] = ldc<ASYNC>(A.t + row + k);
+                    al[j] = alpha_i[k];
+                    Mv[j] = ldc<ASYNC>(Mi + k); Ttv[j] = ldc<ASYNC>(Tti + k); Qv[j] = ldc<ASYNC>(Qw + k); Tv[j] = ldc<ASYNC>(A.T + k);
+                }
             }
-            al = alpha_i[k];
-            int Mv, Ttv, Qv, Tv;
-            load_sums<ASYNC>(Mi, Tti, Qw, A.T, k, mv, tv, Mv, Ttv, Qv, Tv);
-            slot_factors(Mv, Ttv, Qv, Tv, tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+#pragma unroll
+            for (int j = 0; j < PG; ++j) {
+                const int k = lane + 32 * (k0g + j);
+                if constexpr (ASYNC) {                // valid range of the local copy (reading c14), then of the sums
+                    mv[j] = max(mv[j], 0);
+                    tv[j] = mv[j] > 0 ? min(max(tv[j], 1), mv[j]) : 0;
+                    Mv[j] = max(Mv[j], mv[j]); Ttv[j] = max(Ttv[j], tv[j]); Qv[j] = max(Qv[j], tv[j]); Tv[j] = max(Tv[j], Qv[j]);
+                }
+                tb[j] = (k < K) ? tab[tri(mv[j]) + tv[j]] : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < PG; ++j) {
+                const int k = lane + 32 * (k0g + j);
+                float F0 = 0.f, F1 = 0.f;
+                if (k < K) slot_factors(Mv[j], Ttv[j], Qv[j], Tv[j], tb[j], a, b, A.beta, A.vbeta, F0, F1);
+                if (k >= KSPAN) continue;            // KSPAN < 32 (K <= 16)
+                const float Fk = F0 + F1;
+                S.F[k] = Fk;
+                S.aF[skew<KPL>(k)] = __fmul_rn(al[j], Fk);
+                S.mt[k] = ((uint32_t)mv[j] << 16) | (uint32_t)tv[j];
+                S.dmt[k] = 0;
+            }
         }
-        const float Fk = F0 + F1;
-        S.F[k] = Fk;
-        S.aF[skew<KPL>(k)] = __fmul_rn(al, Fk);
-        S.mt[k] = ((uint32_t)mv << 16) | (uint32_t)tv;
-        S.dmt[k] = 0;
     }
     __syncwarp();
 

@@ -69,21 +69,42 @@ __global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs 
     const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
 
     // ---- prologue: slot factors, r = 1 shares, alpha F into PA (prefix below)
-    for (int k = lane; k < KSPAN; k += 32) {
-        float F0 = 0.f, F1 = 0.f, al = 0.f;
-        int mv = 0, tv = 0;
-        if (k < K) {
-            mv = A.m[row + k];
-            tv = A.t[row + k];
-            al = alpha_i[k];
-            slot_factors(Mi[k], Tti[k], Qw[k], A.T[k], tab[tri(mv) + tv], a, b, A.beta, A.vbeta, F0, F1);
+    {   // topics in groups of PG per lane: the group's count loads, then its table loads, then the math
+        constexpr int PER = (KSPAN + 31) / 32;
+        constexpr int PG = SPDP_PRO_GROUP < PER ? SPDP_PRO_GROUP : PER;
+#pragma unroll 1
+        for (int k0g = 0; k0g < PER; k0g += PG) {
+            int mv[PG], tv[PG], Mv[PG], Ttv[PG], Qv[PG], Tv[PG];
+            float al[PG];
+            float2 tb[PG];
+#pragma unroll
+            for (int j = 0; j < PG; ++j) {
+                const int k = lane + 32 * (k0g + j);
+                mv[j] = tv[j] = Mv[j] = Ttv[j] = Qv[j] = Tv[j] = 0;
+                al[j] = 0.f;
+                if (k < K) {
+                    mv[j] = A.m[row + k]; tv[j] = A.t[row + k]; al[j] = alpha_i[k];
+                    Mv[j] = Mi[k]; Ttv[j] = Tti[k]; Qv[j] = Qw[k]; Tv[j] = A.T[k];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < PG; ++j) {
+                const int k = lane + 32 * (k0g + j);
+                tb[j] = (k < K) ? tab[tri(mv[j]) + tv[j]] : make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < PG; ++j) {
+                const int k = lane + 32 * (k0g + j);
+                float F0 = 0.f, F1 = 0.f;
+                if (k < K) slot_factors(Mv[j], Ttv[j], Qv[j], Tv[j], tb[j], a, b, A.beta, A.vbeta, F0, F1);
+                const float Fk = F0 + F1;
+                S.F[k] = Fk;
+                S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
+                S.PA[k] = (double)__fmul_rn(al[j], Fk);
+                S.mt[k] = ((uint32_t)mv[j] << 16) | (uint32_t)tv[j];
+                S.dmt[k] = 0;
+            }
         }
-        const float Fk = F0 + F1;
-        S.F[k] = Fk;
-        S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
-        S.PA[k] = (double)__fmul_rn(al, Fk);
-        S.mt[k] = ((uint32_t)mv << 16) | (uint32_t)tv;
-        S.dmt[k] = 0;
     }
     __syncwarp();
     {   // PA: lane-contiguous blocks of KSPAN/32, local prefix + warp exclusive scan (fp64)
