@@ -1011,6 +1011,7 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
             SPDP_ROWS(c->row_elem, apply_tokens_kernel<NT><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
                                        c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, c->Kp, tb, te));
+            rebuild_entries(c, c->stream);                 // the next wave reads the updated rows
         }
         rec(c, 4 * (size_t)w + 2);
         {
@@ -1421,7 +1422,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
                 ALLOC(c->d_tok_run, nl);
                 ALLOC(c->d_F, (size_t)R * Kp);
                 ALLOC(c->d_R1, (size_t)R * Kp);
-                if (c->token_kernel) {
+                if (c->token_kernel && SPDP_TOKEN_PRE) {
                     ALLOC(c->d_aF, (size_t)R * Kp);
                     ALLOC(c->d_MT, (size_t)R * Kp);
                     ALLOC(c->d_FR, (size_t)R * Kp);
@@ -1556,7 +1557,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         c->row_elem = rb;
     }
     {   // sparse doc-topic rows: when the documents' expected nonzero topics (at a uniform random z, the
-        // start of every chain) cover < 40 % of a row; W = 1 wave updates, K > 64 (the chunk kernel's range)
+        // start of every chain) cover < 40 % of a row; wave updates, K > 64 (the chunk kernel's range)
         const int K = c->K;
         double exp_nnz = 0.0, cap = 0.0;
         std::vector<uint32_t> capp((size_t)c->Dloc + 1, 0);
@@ -1570,11 +1571,9 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         const double frac = c->Dloc ? exp_nnz / ((double)c->Dloc * K) : 1.0;
         int32_t maxlen = 0;
         for (int32_t dl : c->doclen) maxlen = std::max(maxlen, dl);
-        c->sprows = K > 64 && c->W == 1 && !c->async && !c->sparse && !c->seq && frac < 0.4 && maxlen < 65536 &&
-                    !c->token_kernel;
+        c->sprows = K > 64 && !c->async && !c->sparse && !c->seq && frac < 0.4 && maxlen < 65536 && !c->token_kernel;
         if (const char* e = getenv("SPDP_SPARSE_ROWS"))
-            c->sprows = atoi(e) != 0 && K > 64 && c->W == 1 && !c->async && !c->sparse && !c->seq && maxlen < 65536 &&
-                        !c->token_kernel;
+            c->sprows = atoi(e) != 0 && K > 64 && !c->async && !c->sparse && !c->seq && maxlen < 65536 && !c->token_kernel;
         if (c->sprows) {
             const double mean_nnz = c->Dloc ? exp_nnz / c->Dloc : 0.0;
             c->sp_lpt = mean_nnz <= 64 ? 8 : (mean_nnz <= 160 ? 16 : 32);

@@ -32,8 +32,8 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
 #ifndef SPDP_PRO_GROUP
-#define SPDP_PRO_GROUP 4           // chunk prologue: topics per lane whose loads are issued together
-#endif
+#define SPDP_PRO_GROUP 1           // chunk prologue: topics per lane whose loads are issued together (B200, C3:
+#endif                             // 4 -> 1.102 ms, 1 -> 1.053 ms: the register-capped 4x32 kernel schedules worse)
 #ifndef SPDP_BULK_PREFETCH
 #define SPDP_BULK_PREFETCH 0       // 1: exact-byte cp.async.bulk.prefetch.L2 of the next batch instead of this batch's
                                    // 128-B lines (B200, C5: 37.4 vs 34.7 ms per sweep with uint8 rows: fewer bytes, but

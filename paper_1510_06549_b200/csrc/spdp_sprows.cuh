@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs 
             const float scorr = __shfl_sync(0xffffffffu, corr, src);
             const double su = __shfl_sync(0xffffffffu, u, src);
             const uint32_t ptr = __shfl_sync(0xffffffffu, di.x, src);
-            const int nnz = valid ? (int)__shfl_sync(0xffffffffu, di.y, src) : 0;
+            const uint32_t snnz = __shfl_sync(0xffffffffu, di.y, src);   // every lane takes part in the shuffle
+            const int nnz = valid ? (int)snnz : 0;
             const int cnt = (nnz + LPT - 1) / LPT;
             const int j0 = min(gl * cnt, nnz), j1 = min(j0 + cnt, nnz);
             // NS term of entry e: n F_k, or topic k0's after-removal change

@@ -28,9 +28,10 @@
 namespace spdp {
 
 #ifndef SPDP_TOKEN_PRE
-#define SPDP_TOKEN_PRE 1            // factor_kernel also writes alpha F, the packed (m, t) and topic k's own-removal
-                                    // factor parts per (run, k): the token kernel's dependent-load chain loses the
-                                    // (m, t) -> Stirling-table -> sums levels
+#define SPDP_TOKEN_PRE 0            // 1: factor_kernel also writes alpha F, the packed (m, t) and topic k's own-removal
+                                    // factor parts per (run, k), shortening the token kernel's dependent-load chain;
+                                    // B200: C2 0.165 vs 0.159 ms, C4 K = 20 0.276 vs 0.277 ms (the extra factor-table
+                                    // writes cost what the shorter chain saves), so off
 #endif
 
 // F[r][k] (and R1, aF, MT, FR) for the runs (segments) [r0, r1) of one wave

@@ -96,6 +96,15 @@ def test_sparse_rows_lockstep(monkeypatch, K, lpt, rowb):
     assert st["sparse_row_entries"] == int((n > 0).sum())
 
 
+@pytest.mark.parametrize("K,waves", [(200, 2), (1000, 3)])
+def test_sparse_rows_several_waves_lockstep(monkeypatch, K, waves):
+    """W > 1: the entries are rebuilt after every wave's doc-topic update."""
+    monkeypatch.setenv("SPDP_SPARSE_ROWS", "1")
+    c = synth.generate(2, 30, 40.0, 300, 8, seed=K + waves)
+    g = _lockstep(c, K, waves, 3)
+    assert g.stats()["sparse_rows"] == 1
+
+
 @pytest.mark.parametrize("name,K", [("C1", 200), ("C2", 300)])
 def test_sparse_rows_split_segments_lockstep(monkeypatch, name, K):
     monkeypatch.setenv("SPDP_SPARSE_ROWS", "1")
