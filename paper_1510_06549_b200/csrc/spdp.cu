@@ -424,6 +424,9 @@ SweepArgs base_args(spdp_ctx* c) {
         case 80256: CALL(8, 256); break;                    \
         case 160256: CALL(16, 256); break;                  \
         case 320256: CALL(32, 256); break;                  \
+        case 80512: CALL(8, 512); break;                    \
+        case 160512: CALL(16, 512); break;                  \
+        case 320512: CALL(32, 512); break;                  \
         case 81024: CALL(8, 1024); break;                   \
         case 161024: CALL(16, 1024); break;                 \
         case 321024: CALL(32, 1024); break;                 \
@@ -1581,7 +1584,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
                 const int v = atoi(e);
                 if (v == 8 || v == 16 || v == 32) c->sp_lpt = v;
             }
-            c->sp_kspan = K <= 256 ? 256 : 1024;
+            c->sp_kspan = K <= 256 ? 256 : (K <= 512 ? 512 : 1024);
             ALLOC(c->d_cap_ptr, (size_t)c->Dloc + 1);
             ALLOC(c->d_ent, std::max<size_t>((size_t)cap, 1));
             ALLOC(c->d_dinfo, std::max<int32_t>(c->Dloc, 1));

@@ -31,9 +31,9 @@ struct SpRowSmem {
     uint32_t mt[KSPAN];     // snapshot m << 16 | t
     int dmt[KSPAN];         // chunk deltas dm * 2^16 + dt
     double target[32];      // hand-over, one per token of the batch
-    double base[32];        // NS before the gap
-    float hterm[32];        // NS term of the crossing entry (topic hi)
-    int lo[32], hi[32];     // gap [lo, hi); hi = the crossing entry's topic, or K (tail)
+    double base[32];        // NS before the winner lane's range (or all of it: tail gap)
+    int lo[32];             // first topic after the previous lane's last entry
+    uint32_t e0[32], e1[32];// the winner lane's entry range (empty: the tail gap [lo, K))
 };
 
 template <int LPT, int KSPAN>
@@ -165,7 +165,10 @@ __global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs 
         const float al0 = alpha_i[k0];
         const float corr = __fmul_rn(al0, Fk0 - S.F[k0]);    // the alpha part of topic k0's change
 
-        // ======== phase 2: LPT lanes per token, contiguous entry ranges
+        // ======== phase 2: LPT lanes per token, contiguous entry ranges.  Each lane sums its
+        // entries' NS terms in fp32; one fp64 group scan; the first lane whose range ends above the
+        // target, C(last k of its range) > u * total, holds the crossing (in its range or in the gap
+        // before it): it hands over its entry range and the NS before it.
         for (uint32_t s0 = 0; s0 < nb; s0 += TPW) {
             const uint32_t src = (s0 + g) & 31;
             const bool valid = s0 + g < nb;
@@ -178,64 +181,77 @@ __global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs 
             const int nnz = valid ? (int)snnz : 0;
             const int cnt = (nnz + LPT - 1) / LPT;
             const int j0 = min(gl * cnt, nnz), j1 = min(j0 + cnt, nnz);
-            // NS term of entry e: n F_k, or topic k0's after-removal change
-            auto term_of = [&](uint32_t e, int& k) {
-                k = (int)(e & 0xFFFFu);
-                const float n = (float)(e >> 16);
-                return (k == sk0) ? __fmaf_rn(n - 1.f, sFk0, scorr) : __fmul_rn(n, S.F[k]);
-            };
-            double loc = 0.0;
+            float lsum = 0.f;
+            int lastk = -1;
             for (int j = j0; j < j1; ++j) {
-                int k;
-                loc += (double)term_of(ent[ptr + j], k);
+                const uint32_t e = ent[ptr + j];
+                const int k = (int)(e & 0xFFFFu);
+                const float n = (float)(e >> 16);
+                lsum += (k == sk0) ? __fmaf_rn(n - 1.f, sFk0, scorr) : __fmul_rn(n, S.F[k]);
+                lastk = k;
             }
-            double incl = loc;
+            double incl = (double)lsum;
 #pragma unroll
             for (int off = 1; off < LPT; off <<= 1) {
                 const double y = __shfl_up_sync(0xffffffffu, incl, off, LPT);
                 if (gl >= off) incl += y;
             }
+            double excl = __shfl_up_sync(0xffffffffu, incl, 1, LPT);
+            if (gl == 0) excl = 0.0;
+            int prevk = __shfl_up_sync(0xffffffffu, lastk, 1, LPT);    // last entry topic before my range
+            if (gl == 0) prevk = -1;
             const double nstot = __shfl_sync(0xffffffffu, incl, LPT - 1, LPT);
             const double target = su * (PAtot + nstot);
-            // the first entry whose inclusive CDF C(k_e) = PA(k_e) + NS(k_e) exceeds the target
-            double run = incl - loc;
-            int prevk = -1, ck = -1, clo = 0;
-            float cterm = 0.f;
-            double cbase = 0.0;
-            if (j0 > 0 && j0 < j1) prevk = (int)(ent[ptr + j0 - 1] & 0xFFFFu);
-            for (int j = j0; j < j1; ++j) {
-                int k;
-                const float tm = term_of(ent[ptr + j], k);
-                if (ck < 0 && S.PA[k] + run + (double)tm > target) { ck = k; clo = prevk + 1; cbase = run; cterm = tm; }
-                run += (double)tm;
-                prevk = k;
-            }
-            const unsigned hit = __ballot_sync(0xffffffffu, ck >= 0) & gmask;
-            const int last_gl = nnz > 0 ? (nnz - 1) / max(cnt, 1) : 0;   // the lane holding the last entry
-            const int winner = hit ? (__ffs(hit) - 1) : (g * LPT + last_gl);
+            const bool crossed = (j1 > j0) && (S.PA[lastk] + (excl + (double)lsum) > target);
+            const unsigned hit = __ballot_sync(0xffffffffu, crossed) & gmask;
+            // the entry ranges are contiguous: the lane owning the last entry gives the tail gap's start
+            const int last_gl = nnz > 0 ? (nnz - 1) / max(cnt, 1) : 0;
+            const int tail_lastk = __shfl_sync(0xffffffffu, lastk, last_gl, LPT);
+            const int winner = hit ? (__ffs(hit) - 1) : g * LPT;
+            // (ranges fill from lane 0, so the winner's predecessor lanes are full and prevk is exact)
             if (lane == winner && valid) {
                 S.target[src] = target;
-                if (hit) { S.lo[src] = clo; S.hi[src] = ck; S.base[src] = cbase; S.hterm[src] = cterm; }
-                else { S.lo[src] = prevk + 1; S.hi[src] = K; S.base[src] = nstot; S.hterm[src] = 0.f; }   // tail gap
+                if (hit) { S.base[src] = excl; S.lo[src] = prevk + 1; S.e0[src] = ptr + j0; S.e1[src] = ptr + j1; }
+                else { S.base[src] = nstot; S.lo[src] = tail_lastk + 1; S.e0[src] = 0; S.e1[src] = 0; }   // tail gap
             }
         }
         __syncwarp();
 
-        // ======== phase 3: lane = token; binary search in the gap, r split
+        // ======== phase 3: lane = token; walk the winner's entries (the gap before each, then the
+        // entry), binary search inside the gap that holds the crossing; r split
         if (mine) {
             int ks = k0, rs = 1;
             if (!keep) {
                 const double target = S.target[lane], base = S.base[lane];
-                const int lo = S.lo[lane], hi = S.hi[lane];
-                int L = lo, H = hi;                         // first k in [lo, hi) with PA(k) + base > target
-                while (L < H) {
-                    const int mid = (L + H) >> 1;
-                    if (S.PA[mid] + base > target) H = mid; else L = mid + 1;
+                int lo = S.lo[lane];
+                const uint32_t e0 = S.e0[lane], e1 = S.e1[lane];
+                float run32 = 0.f;
+                double cum = base;                         // C(k) - PA(k) on the current gap: base + NS so far
+                int found = -1, hi = K;
+                float hterm = 0.f;
+                for (uint32_t j = e0; j < e1 && found < 0; ++j) {
+                    const uint32_t e = ent[j];
+                    const int k = (int)(e & 0xFFFFu);
+                    const float n = (float)(e >> 16);
+                    const float tm = (k == k0) ? __fmaf_rn(n - 1.f, Fk0, corr) : __fmul_rn(n, S.F[k]);
+                    if (k > lo && S.PA[k - 1] + cum > target) { hi = k; found = 0; break; }   // in the gap [lo, k)
+                    run32 += tm;
+                    const double cnext = base + (double)run32;
+                    if (S.PA[k] + cnext > target) { found = 1; ks = k; hterm = tm; break; }   // the entry itself
+                    cum = cnext;
+                    lo = k + 1;
                 }
-                if (L < K) {
+                if (found != 1) {                          // first k in [lo, hi) with PA(k) + cum > target
+                    int L = lo, H = hi;
+                    while (L < H) {
+                        const int mid = (L + H) >> 1;
+                        if (S.PA[mid] + cum > target) H = mid; else L = mid + 1;
+                    }
                     ks = L;
-                    const double before = (ks > 0 ? S.PA[ks - 1] : 0.0) + base;
-                    const float mass = __fmaf_rn(alpha_i[ks], S.F[ks], (ks == hi) ? S.hterm[lane] : 0.f);
+                }
+                if (ks < K) {
+                    const double before = (ks > 0 ? S.PA[ks - 1] : 0.0) + cum;
+                    const float mass = __fmaf_rn(alpha_i[ks], S.F[ks], found == 1 ? hterm : 0.f);
                     const float R1s = (ks == k0) ? R1k0 : S.R1[ks];
                     rs = (before + (double)__fmul_rn(mass, R1s) > target) ? 1 : 0;
                 } else {                                    // rounding: the last positive slot
