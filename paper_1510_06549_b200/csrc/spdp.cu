@@ -157,6 +157,7 @@ struct spdp_ctx {
     bool seq = false;                             // num_waves = 0: exact sequential sampler (test mode, spdp_seq.cuh)
     uint32_t* d_pos = nullptr;                    // seq: canonical id -> sorted position
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
+    bool pack_dmt = false;                        // chunk kernels flush packed dm * 2^16 + dt words (M_max < 2^15)
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
     float* d_R1 = nullptr;                        // token kernel: r = 1 shares [run][Kp]
@@ -415,10 +416,14 @@ SweepArgs base_args(spdp_ctx* c) {
     a.key0 = (uint32_t)c->cfg.seed; a.key1 = (uint32_t)(c->cfg.seed >> 32);
     a.sweep = c->d_sweep; a.stats = c->d_stats;
     a.dinfo = c->d_dinfo; a.ent = c->d_ent;
+    a.packed_dmt = c->pack_dmt ? 1 : 0;
     return a;
 }
 
 // ---- sparse doc-topic rows
+#ifndef SPDP_SPROWS_AUTO
+#define SPDP_SPROWS_AUTO 0            // choose the sparse-row kernel automatically (else only SPDP_SPARSE_ROWS=1)
+#endif
 #define SPDP_SPROWS_DISPATCH(LPT_, KS_, CALL)               \
     switch ((LPT_) * 10000 + (KS_)) {                       \
         case 80256: CALL(8, 256); break;                    \
@@ -896,7 +901,7 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
             const int blocks = (int)std::min<uint32_t>((re - rb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, st>>>(
                 c->d_wave_segs + rb, (int)(re - rb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q,
-                c->d_Mn, c->d_Ttn, c->d_Tn, c->I, c->Kp, use_smem, c->d_stats, (int)c->token_kernel);
+                c->d_Mn, c->d_Ttn, c->d_Tn, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt));
             c->launches += 2;
         }
         if (c->overlap) {                                   // rows of part p: all-reduce + merge on comm_stream
@@ -1024,7 +1029,7 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             const int blocks = (int)std::min<uint32_t>((se - sb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, c->stream>>>(
                 c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q, c->d_M,
-                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats, (int)c->token_kernel);
+                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt));
         }
         rec(c, 4 * (size_t)w + 3);
         c->launches += 3;
@@ -1328,6 +1333,9 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     const double seg_fill = (double)num_tokens / c->G / ((double)V * I * W);
     c->token_kernel = !c->async && !c->sparse && c->mmax < 32768 &&
                       (c->K <= 64 || (c->K <= 128 && W > 1 && seg_fill < 32.0));
+    // wave deltas of the chunk kernels as one packed word per cell: |sum of a wave's deltas| <= count(i,w)
+    // <= M_max < 2^15 (the token kernel's argument); halves the flush atomics and the merge's delta bytes
+    c->pack_dmt = !c->async && c->mmax < 32768 && !(getenv("SPDP_PACK_DELTAS") && atoi(getenv("SPDP_PACK_DELTAS")) == 0);
     if (const char* e = getenv("SPDP_TOKEN_KERNEL")) {   // 0: never; 2: also K <= 128 with one wave
         const int v = atoi(e);
         if (v == 0) c->token_kernel = false;
@@ -1574,7 +1582,11 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         const double frac = c->Dloc ? exp_nnz / ((double)c->Dloc * K) : 1.0;
         int32_t maxlen = 0;
         for (int32_t dl : c->doclen) maxlen = std::max(maxlen, dl);
-        c->sprows = K > 64 && !c->async && !c->sparse && !c->seq && frac < 0.4 && maxlen < 65536 && !c->token_kernel;
+        // measured (B200, sample + rebuild vs the dense kernel): C5 30.2 + 5.2 vs 31.2 + 4.1 ms, C4 K = 1000
+        // 6.4 vs 4.2 ms, K = 300 2.3 vs 1.5 ms, C3 1.6 vs 1.05 ms: the dense kernel wins or ties, so the sparse
+        // path is opt-in (SPDP_SPARSE_ROWS=1)
+        c->sprows = SPDP_SPROWS_AUTO && K > 64 && !c->async && !c->sparse && !c->seq && frac < 0.4 && maxlen < 65536 &&
+                    !c->token_kernel;
         if (const char* e = getenv("SPDP_SPARSE_ROWS"))
             c->sprows = atoi(e) != 0 && K > 64 && !c->async && !c->sparse && !c->seq && maxlen < 65536 && !c->token_kernel;
         if (c->sprows) {

@@ -269,6 +269,9 @@ struct Row<float> {
     __device__ __forceinline__ static float load1(const float* p) { return __ldg(p); }
     __device__ __forceinline__ static void add(float* base, size_t idx, int d) { atomicAdd(base + idx, (float)d); }
     __device__ __forceinline__ static void store(float* p, int v) { *p = (float)v; }
+    __device__ __forceinline__ static void store4(float* p, int a, int b, int c, int d) {
+        *reinterpret_cast<float4*>(p) = make_float4((float)a, (float)b, (float)c, (float)d);
+    }
     __device__ __forceinline__ static int get(const float* p) { return (int)*p; }
 };
 #ifdef SPDP_CVT_I2F
@@ -296,6 +299,9 @@ struct Row<uint16_t> {
         atomicAdd(reinterpret_cast<unsigned int*>(base) + (idx >> 1), (unsigned int)d << ((idx & 1) * 16));
     }
     __device__ __forceinline__ static void store(uint16_t* p, int v) { *p = (uint16_t)v; }
+    __device__ __forceinline__ static void store4(uint16_t* p, int a, int b, int c, int d) {
+        *reinterpret_cast<uint2*>(p) = make_uint2((uint32_t)a | ((uint32_t)b << 16), (uint32_t)c | ((uint32_t)d << 16));
+    }
     __device__ __forceinline__ static int get(const uint16_t* p) { return (int)*p; }
 };
 
@@ -325,6 +331,9 @@ struct Row<uint8_t> {
         atomicAdd(reinterpret_cast<unsigned int*>(base) + (idx >> 2), (unsigned int)d << ((idx & 3) * 8));
     }
     __device__ __forceinline__ static void store(uint8_t* p, int v) { *p = (uint8_t)v; }
+    __device__ __forceinline__ static void store4(uint8_t* p, int a, int b, int c, int d) {
+        *reinterpret_cast<uint32_t*>(p) = (uint32_t)a | ((uint32_t)b << 8) | ((uint32_t)c << 16) | ((uint32_t)d << 24);
+    }
     __device__ __forceinline__ static int get(const uint8_t* p) { return (int)*p; }
 };
 
@@ -371,6 +380,7 @@ struct SweepArgs {
     // debug_probs
     double* dbg_w;                 // [ntok][2K] unnormalised weights, or null
     int32_t* dbg_info;             // [ntok][4]
+    int packed_dmt;                // wave deltas as one packed dm * 2^16 + dt word per cell in dm (M_max < 2^15)
     // sparse doc-topic rows (spdp_sprows.cuh)
     const uint2* dinfo;            // [D_local] {first entry, nonzero topics}
     const uint32_t* ent;           // entries k | n << 16, topic order per document
@@ -823,6 +833,8 @@ sample_kernel(SweepArgs A) {
                         atomicAdd(A.t + row + k, dtv); atomicAdd(A.Q + (size_t)w * Kp + k, dtv);
                         atomicAdd(A.Tt + (size_t)i * Kp + k, dtv); atomicAdd(A.T + k, dtv);
                     }
+                } else if (A.packed_dmt) {                 // one packed dm * 2^16 + dt word per cell
+                    atomicAdd(A.dm + row + k, x);
                 } else {
                     if (dmv) atomicAdd(A.dm + row + k, dmv);
                     if (dtv) atomicAdd(A.dt + row + k, dtv);
@@ -963,10 +975,24 @@ __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const 
         for (int j = lane; j < Kp; j += 32) h[j] = 0;
         __syncwarp();
         const uint32_t e = doc_ptr[d + 1];
-        for (uint32_t t = doc_ptr[d] + lane; t < e; t += 32) atomicAdd(&h[sigma[zr[doc_pos[t]] & 0x7FFFu]], 1);
+        // 4 tokens per lane in flight: the positions, then the scattered assignments, then the histogram
+        for (uint32_t t0 = doc_ptr[d]; t0 < e; t0 += 128) {
+            uint32_t pos[4];
+            uint32_t zv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t t = t0 + lane + 32u * j;
+                pos[j] = t < e ? doc_pos[t] : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) zv[j] = pos[j] != 0xFFFFFFFFu ? (uint32_t)zr[pos[j]] : 0xFFFFFFFFu;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (zv[j] != 0xFFFFFFFFu) atomicAdd(&h[sigma[zv[j] & 0x7FFFu]], 1);
+        }
         __syncwarp();
         NT* row = n + (size_t)d * Kp;
-        for (int j = lane; j < Kp; j += 32) Row<NT>::store(row + j, h[j]);
+        for (int j = lane * 4; j < Kp; j += 128) Row<NT>::store4(row + j, h[j], h[j + 1], h[j + 2], h[j + 3]);
         __syncwarp();
     }
 }

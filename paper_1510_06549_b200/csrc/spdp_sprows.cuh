@@ -275,8 +275,11 @@ __global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs 
         if (x) {
             const int dtv = (int)(short)(x & 0xFFFF);
             const int dmv = (x - dtv) >> 16;
-            if (dmv) atomicAdd(A.dm + row + k, dmv);
-            if (dtv) atomicAdd(A.dt + row + k, dtv);
+            if (A.packed_dmt) atomicAdd(A.dm + row + k, x);
+            else {
+                if (dmv) atomicAdd(A.dm + row + k, dmv);
+                if (dtv) atomicAdd(A.dt + row + k, dtv);
+            }
         }
     }
     __syncwarp();
