@@ -158,6 +158,7 @@ struct spdp_ctx {
     uint32_t* d_pos = nullptr;                    // seq: canonical id -> sorted position
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
     bool pack_dmt = false;                        // chunk kernels flush packed dm * 2^16 + dt words (M_max < 2^15)
+    bool chunk_ft = false;                        // chunk kernel reads per-wave factor tables (SPDP_CHUNK_FACTORS)
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
     float* d_R1 = nullptr;                        // token kernel: r = 1 shares [run][Kp]
@@ -368,7 +369,7 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     factor_kernel<<<std::max(fgrid, 1), 256, 0, c->stream>>>(
         c->d_wave_segs, r0, r1, c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->d_disc, c->d_conc, c->d_tab,
         c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F, c->d_R1,
-        c->d_alpha, c->d_aF, c->d_MT, c->d_FR);
+        c->d_alpha, SPDP_TOKEN_PRE ? c->d_aF : nullptr, SPDP_TOKEN_PRE ? c->d_MT : nullptr, SPDP_TOKEN_PRE ? c->d_FR : nullptr);
     TokenArgs t{};
     t.aF = c->d_aF; t.MT = c->d_MT; t.FR = c->d_FR;
     t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
@@ -399,6 +400,19 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     c->launches += 1;
 }
 
+// chunk kernel with factor tables: the slot factors, r = 1 shares, alpha F and packed (m, t) of the runs
+// [r0, r1) of a wave, written by one throughput kernel before the sample kernel reads them
+void launch_chunk_factors(spdp_ctx* c, uint32_t r0, uint32_t r1) {
+    const size_t nf = (size_t)(r1 - r0) * c->Kp;
+    if (nf == 0) return;
+    const int fgrid = (int)std::min<size_t>((nf + 255) / 256, 148u * 16u);
+    factor_kernel<<<std::max(fgrid, 1), 256, 0, c->stream>>>(
+        c->d_wave_segs, r0, r1, c->d_m, c->d_t, c->d_Q, c->d_M, c->d_Tt, c->d_T, c->d_disc, c->d_conc, c->d_tab,
+        c->d_tab_off, (float)c->cfg.beta, (float)((double)c->V * c->cfg.beta), c->I, c->K, c->Kp, c->d_F, c->d_R1,
+        c->d_alpha, c->d_aF, c->d_MT, nullptr);
+    c->launches += 1;
+}
+
 SweepArgs base_args(spdp_ctx* c) {
     SweepArgs a{};
     a.tok_doc = c->d_tok_doc; a.tok_id = c->d_tok_id; a.zr = c->d_zr; a.zr_next = c->d_zr_next;
@@ -417,10 +431,15 @@ SweepArgs base_args(spdp_ctx* c) {
     a.sweep = c->d_sweep; a.stats = c->d_stats;
     a.dinfo = c->d_dinfo; a.ent = c->d_ent;
     a.packed_dmt = c->pack_dmt ? 1 : 0;
+    a.chunk_ft = c->chunk_ft ? 1 : 0;
+    a.tok_run = c->d_tok_run; a.Ft = c->d_F; a.R1t = c->d_R1; a.aFt = c->d_aF; a.MTt = c->d_MT;
     return a;
 }
 
 // ---- sparse doc-topic rows
+#ifndef SPDP_CHUNK_FACTORS
+#define SPDP_CHUNK_FACTORS 0          // default of c->chunk_ft (env SPDP_CHUNK_FACTORS overrides)
+#endif
 #ifndef SPDP_SPROWS_AUTO
 #define SPDP_SPROWS_AUTO 0            // choose the sparse-row kernel automatically (else only SPDP_SPARSE_ROWS=1)
 #endif
@@ -895,6 +914,7 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
                 a.chunk_seg = c->d_chunk_seg + cb;
                 a.nchunks = (int)(ce - cb);
                 a.work = c->d_work + p;
+                if (c->chunk_ft) launch_chunk_factors(c, rb, re);
                 if (c->sprows) launch_sprows(c, a);
                 else launch_sample(c, a, false);
             }
@@ -1004,6 +1024,7 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             a.chunk_seg = c->d_chunk_seg + cb;
             a.nchunks = (int)(ce - cb);
             a.work = c->d_work + w;
+            if (c->chunk_ft) launch_chunk_factors(c, c->wave_seg_begin[(size_t)w], c->wave_seg_begin[(size_t)w + 1]);
             if (c->sprows) launch_sprows(c, a);
             else launch_sample(c, a, false);
         }
@@ -1336,6 +1357,10 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     // wave deltas of the chunk kernels as one packed word per cell: |sum of a wave's deltas| <= count(i,w)
     // <= M_max < 2^15 (the token kernel's argument); halves the flush atomics and the merge's delta bytes
     c->pack_dmt = !c->async && c->mmax < 32768 && !(getenv("SPDP_PACK_DELTAS") && atoi(getenv("SPDP_PACK_DELTAS")) == 0);
+    // the chunk kernel's per-chunk slot factors from per-wave factor tables (a throughput kernel) instead of the
+    // chunk prologue's dependent load chain (counts -> Stirling table); wave updates, no transform, no async
+    c->chunk_ft = SPDP_CHUNK_FACTORS && !c->async && !c->sparse && !c->seq;
+    if (const char* e = getenv("SPDP_CHUNK_FACTORS")) c->chunk_ft = atoi(e) != 0 && !c->async && !c->sparse && !c->seq;
     if (const char* e = getenv("SPDP_TOKEN_KERNEL")) {   // 0: never; 2: also K <= 128 with one wave
         const int v = atoi(e);
         if (v == 0) c->token_kernel = false;
@@ -1429,11 +1454,11 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             if ((s = cub_run([&](void* t, size_t& b) { return cub::DeviceScan::ExclusiveSum(t, b, drlen.p, droff.p, (int)R, st); },
                              "segment offsets")))
                 return s;
-            if (c->token_kernel || c->sparse) {
+            if (c->token_kernel || c->sparse || c->chunk_ft) {
                 ALLOC(c->d_tok_run, nl);
                 ALLOC(c->d_F, (size_t)R * Kp);
                 ALLOC(c->d_R1, (size_t)R * Kp);
-                if (c->token_kernel && SPDP_TOKEN_PRE) {
+                if ((c->token_kernel && SPDP_TOKEN_PRE) || c->chunk_ft) {
                     ALLOC(c->d_aF, (size_t)R * Kp);
                     ALLOC(c->d_MT, (size_t)R * Kp);
                     ALLOC(c->d_FR, (size_t)R * Kp);
@@ -2404,6 +2429,7 @@ spdp_status spdp_debug_probs(spdp_ctx* c, int64_t n, const int64_t* tok_ids, dou
     CU(cudaMemcpyAsync(d_seg, seg.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     CU(cudaMemcpyAsync(d_zr, zr.data(), 2 * (size_t)n, cudaMemcpyHostToDevice, c->stream));
     SweepArgs a = base_args(c);
+    a.chunk_ft = 0;                                   // one-token "chunks" of this call: factors computed in place
     a.tok_doc = d_doc; a.tok_id = d_id; a.zr = d_zr; a.zr_next = nullptr;
     a.chunk_start = d_cs; a.chunk_end = d_ce; a.chunk_seg = d_seg; a.nchunks = (int)n;
     a.work = c->d_work + c->W + 1;

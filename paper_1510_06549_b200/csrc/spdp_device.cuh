@@ -381,6 +381,13 @@ struct SweepArgs {
     double* dbg_w;                 // [ntok][2K] unnormalised weights, or null
     int32_t* dbg_info;             // [ntok][4]
     int packed_dmt;                // wave deltas as one packed dm * 2^16 + dt word per cell in dm (M_max < 2^15)
+    // per-wave factor tables (chunk_ft): [run][Kp] slot factors F0 + F1, r = 1 shares, alpha F, packed (m, t)
+    int chunk_ft;
+    const uint32_t* tok_run;       // run (segment of the wave) of each sorted token
+    const float* Ft;
+    const float* R1t;
+    const float* aFt;
+    const uint32_t* MTt;
     // sparse doc-topic rows (spdp_sprows.cuh)
     const uint2* dinfo;            // [D_local] {first entry, nonzero topics}
     const uint32_t* ent;           // entries k | n << 16, topic order per document
@@ -495,10 +502,23 @@ sample_kernel(SweepArgs A) {
     const float* __restrict__ alpha_i = A.alpha + (size_t)i * Kp;
 
     const uint32_t start = A.chunk_start[c], end = A.chunk_end[c];
-    // ---- prologue: the segment's slot factors at the wave-start snapshot.  Topics in groups of
-    // PG per lane: all count loads of a group first, then its Stirling-table loads, then the math,
-    // so each group costs two memory round trips instead of two per topic.
-    {
+    // ---- prologue: the segment's slot factors at the wave-start snapshot: from the wave's factor
+    // tables (chunk_ft: coalesced row loads, no dependent chain), or computed here.  Computed: topics in
+    // groups of PG per lane, all count loads of a group first, then its Stirling-table loads, then the math.
+    uint32_t crun = 0;
+    if (!ASYNC && A.chunk_ft) {
+        crun = A.tok_run[start];
+        const size_t rrow = (size_t)crun * Kp;
+        for (int k = lane; k < KSPAN; k += 32) {
+            float Fk = 0.f, aFk = 0.f;
+            uint32_t mt = 0;
+            if (k < K) { Fk = A.Ft[rrow + k]; aFk = A.aFt[rrow + k]; mt = A.MTt[rrow + k]; }
+            S.F[k] = Fk;
+            S.aF[skew<KPL>(k)] = aFk;
+            S.mt[k] = mt;
+            S.dmt[k] = 0;
+        }
+    } else {
         constexpr int PER = (KSPAN + 31) / 32;
         constexpr int PG = SPDP_PRO_GROUP < PER ? SPDP_PRO_GROUP : PER;
         static_assert(PER % PG == 0, "prologue group must divide the topics per lane");
@@ -542,7 +562,7 @@ sample_kernel(SweepArgs A) {
                 S.dmt[k] = 0;
             }
         }
-    }
+    }   // computed prologue
     __syncwarp();
 
     float F[KPL];                                    // aF stays in smem (conflict-free broadcast loads)
@@ -770,7 +790,8 @@ sample_kernel(SweepArgs A) {
                 const bool own = (ks == k0);
                 const uint32_t mts = S.mt[ks];
                 float R1s = R1k0;
-                if (!own) {                                // r = 1 share of topic ks at the snapshot
+                if (!own && !ASYNC && A.chunk_ft) R1s = A.R1t[(size_t)crun * Kp + ks];   // from the factor table
+                else if (!own) {                           // r = 1 share of topic ks at the snapshot
                     float f0, f1;
                     int Ms, Tts, Qs, Ts;
                     load_sums<ASYNC>(Mi, Tti, Qw, A.T, ks, (int)(mts >> 16), (int)(mts & 0xFFFFu), Ms, Tts, Qs, Ts);

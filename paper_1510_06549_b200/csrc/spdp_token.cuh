@@ -34,7 +34,7 @@ namespace spdp {
                                     // writes cost what the shorter chain saves), so off
 #endif
 
-// F[r][k] (and R1, aF, MT, FR) for the runs (segments) [r0, r1) of one wave
+// F[r][k] and R1 (and, when the pointers are set, aF, MT, FR) for the runs (segments) [r0, r1) of one wave
 __global__ void factor_kernel(const uint32_t* __restrict__ run_seg, uint32_t r0, uint32_t r1,
                               const int32_t* __restrict__ m, const int32_t* __restrict__ t,
                               const int32_t* __restrict__ Q, const int32_t* __restrict__ M,
@@ -64,7 +64,7 @@ __global__ void factor_kernel(const uint32_t* __restrict__ run_seg, uint32_t r0,
             Fk = F0 + F1;
             Rk = (F1 > 0.f) ? __fdiv_rn(F1, F0 + F1) : 0.f;     // exact r = 1 share of the slot pair
             al = alpha[(size_t)i * Kp + k];
-            if (SPDP_TOKEN_PRE && mv > 0) {   // a token of topic k leaving this segment (Alg.1 lines 4-10)
+            if (FR && mv > 0) {               // a token of topic k leaving this segment (Alg.1 lines 4-10)
                 const int mm = mv - 1;
                 slot_factors(Mv - 1, Ttv, Qv, Tv, tb[tri(mm) + min(tv, mm)], a, b, beta, vbeta, fr.x, fr.y);         // r_rem = 0
                 slot_factors(Mv - 1, Ttv - 1, Qv - 1, Tv - 1, tb[tri(mm) + max(tv - 1, 0)], a, b, beta, vbeta, fr.z, fr.w);  // r_rem = 1
@@ -72,11 +72,9 @@ __global__ void factor_kernel(const uint32_t* __restrict__ run_seg, uint32_t r0,
         }
         F[(size_t)r * Kp + k] = Fk;
         R1[(size_t)r * Kp + k] = Rk;
-        if (SPDP_TOKEN_PRE) {
-            aF[(size_t)r * Kp + k] = __fmul_rn(al, Fk);
-            MT[(size_t)r * Kp + k] = ((uint32_t)mv << 16) | (uint32_t)tv;
-            FR[(size_t)r * Kp + k] = fr;
-        }
+        if (aF) aF[(size_t)r * Kp + k] = __fmul_rn(al, Fk);       // optional tables (token kernel with
+        if (MT) MT[(size_t)r * Kp + k] = ((uint32_t)mv << 16) | (uint32_t)tv;   // SPDP_TOKEN_PRE; chunk
+        if (FR) FR[(size_t)r * Kp + k] = fr;                      // kernel with factor tables)
     }
 }
 

@@ -105,6 +105,19 @@ def test_sparse_rows_several_waves_lockstep(monkeypatch, K, waves):
     assert g.stats()["sparse_rows"] == 1
 
 
+@pytest.mark.parametrize("K,waves,extra", [(100, 1, {}), (100, 3, {}), (200, 1, {"SPDP_ROW_BYTES": "1"}),
+                                           (300, 2, {"SPDP_ROW_BYTES": "2"}), (1000, 1, {}),
+                                           (130, 1, {"SPDP_CHUNK_TOKENS": "16"}), (50, 1, {"SPDP_TOKEN_KERNEL": "0"})])
+def test_chunk_factor_tables_lockstep(monkeypatch, K, waves, extra):
+    """The chunk kernel reading per-wave factor tables (SPDP_CHUNK_FACTORS=1: slot factors, r = 1 shares,
+    alpha F and packed (m, t) of every (wave, w, i) run from one throughput kernel) instead of its prologue."""
+    monkeypatch.setenv("SPDP_CHUNK_FACTORS", "1")
+    for k, v in extra.items():
+        monkeypatch.setenv(k, v)
+    c = synth.generate(2, 30, 40.0, 300, 8, seed=K + 7 * waves)
+    _lockstep(c, K, waves, 3)
+
+
 @pytest.mark.parametrize("name,K", [("C1", 200), ("C2", 300)])
 def test_sparse_rows_split_segments_lockstep(monkeypatch, name, K):
     monkeypatch.setenv("SPDP_SPARSE_ROWS", "1")
