@@ -159,6 +159,9 @@ struct spdp_ctx {
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
     bool pack_dmt = false;                        // chunk kernels flush packed dm * 2^16 + dt words (M_max < 2^15)
     bool chunk_ft = false;                        // chunk kernel reads per-wave factor tables (SPDP_CHUNK_FACTORS)
+    bool doc_scatter = false;                     // W = 1 chunk kernel also writes zr in document order (recount streams it)
+    uint32_t* d_slot = nullptr;                   // document-order slot of each sorted token
+    uint16_t* d_zr_doc = nullptr;
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
     float* d_F = nullptr;                         // token kernel: slot factors [run][Kp]
     float* d_R1 = nullptr;                        // token kernel: r = 1 shares [run][Kp]
@@ -432,6 +435,8 @@ SweepArgs base_args(spdp_ctx* c) {
     a.dinfo = c->d_dinfo; a.ent = c->d_ent;
     a.packed_dmt = c->pack_dmt ? 1 : 0;
     a.chunk_ft = c->chunk_ft ? 1 : 0;
+    a.slot = c->doc_scatter ? c->d_slot : nullptr;
+    a.zr_doc = c->doc_scatter ? c->d_zr_doc : nullptr;
     a.tok_run = c->d_tok_run; a.Ft = c->d_F; a.R1t = c->d_R1; a.aFt = c->d_aF; a.MTt = c->d_MT;
     return a;
 }
@@ -860,7 +865,7 @@ void sparse_wave(spdp_ctx* c, int w) {
     if (c->W == 1) {
         const size_t smem = sizeof(int) * 8 * (size_t)Kp;
         SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
-                                   c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, Kp, (NT*)c->d_n));
+                                   c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, Kp, (NT*)c->d_n, nullptr));
         std::swap(c->d_zr, c->d_zr_next);
     } else {
         const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
@@ -943,7 +948,8 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
     rec(c, 1);
     const size_t rsm = sizeof(int) * 8 * (size_t)c->Kp;      // every token moved to zr_next: rebuild n, swap
     SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
-                                                                            c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n));
+                                                                            c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n,
+                                                                            c->doc_scatter ? c->d_zr_doc : nullptr));
     rebuild_entries(c, st);
     std::swap(c->d_zr, c->d_zr_next);
     rec(c, 2);
@@ -1033,7 +1039,8 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
             SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
-                                       c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n));
+                                       c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n,
+                                       c->doc_scatter ? c->d_zr_doc : nullptr));
             rebuild_entries(c, c->stream);
             std::swap(c->d_zr, c->d_zr_next);
         } else {
@@ -1546,6 +1553,15 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         for (int32_t j = 0; j < c->Dloc; ++j)
             dptr[(size_t)j + 1] = dptr[(size_t)j] + (uint32_t)c->doclen[(size_t)c->global_of_local[(size_t)j]];
         CU(cudaMemcpyAsync(c->d_doc_ptr, dptr.data(), sizeof(uint32_t) * dptr.size(), cudaMemcpyHostToDevice, st));
+        // W = 1 with the chunk kernel: it also writes each new assignment to its document-order slot (a
+        // fire-and-forget scattered store), so the recount streams them instead of gathering through doc_pos
+        c->doc_scatter = W == 1 && !c->token_kernel && !c->async && !c->sparse && !c->seq && !c->sprows;
+        if (const char* e = getenv("SPDP_DOC_SCATTER")) c->doc_scatter = c->doc_scatter && atoi(e) != 0;
+        if (c->doc_scatter) {
+            ALLOC(c->d_slot, nl);
+            ALLOC(c->d_zr_doc, nl);
+            if (nloc > 0) invert_perm_kernel<<<grid, 256, 0, st>>>(c->d_doc_pos, nloc, c->d_slot);
+        }
     }
     if ((s = check_launch(c, "load planning kernels"))) return s;
     if ((s = sync(c, "load planning"))) return s;
@@ -1615,6 +1631,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         if (const char* e = getenv("SPDP_SPARSE_ROWS"))
             c->sprows = atoi(e) != 0 && K > 64 && !c->async && !c->sparse && !c->seq && maxlen < 65536 && !c->token_kernel;
         if (c->sprows) {
+            c->doc_scatter = false;                       // its recount gathers (the sparse kernel writes zr_next only)
             const double mean_nnz = c->Dloc ? exp_nnz / c->Dloc : 0.0;
             c->sp_lpt = mean_nnz <= 64 ? 8 : (mean_nnz <= 160 ? 16 : 32);
             if (const char* e = getenv("SPDP_SPROWS_LPT")) {

@@ -381,6 +381,8 @@ struct SweepArgs {
     double* dbg_w;                 // [ntok][2K] unnormalised weights, or null
     int32_t* dbg_info;             // [ntok][4]
     int packed_dmt;                // wave deltas as one packed dm * 2^16 + dt word per cell in dm (M_max < 2^15)
+    const uint32_t* slot;          // W = 1: document-order slot of each sorted token, or null
+    uint16_t* zr_doc;              // W = 1: the new assignments in document order (the recount streams them)
     // per-wave factor tables (chunk_ft): [run][Kp] slot factors F0 + F1, r = 1 shares, alpha F, packed (m, t)
     int chunk_ft;
     const uint32_t* tok_run;       // run (segment of the wave) of each sorted token
@@ -824,6 +826,7 @@ sample_kernel(SweepArgs A) {
                 inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
             } else {
                 A.zr_next[p] = (uint16_t)(ks | (rs << 15));                                   // a7
+                if constexpr (!ASYNC) if (A.zr_doc) A.zr_doc[A.slot[p]] = (uint16_t)(ks | (rs << 15));
                 if (keep) ++keeps;
                 else {
                     atomicAdd(&S.dmt[k0], -65536 - rrem);
@@ -988,7 +991,7 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
 template <typename NT>
 __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const uint32_t* __restrict__ doc_pos,
                                     const uint16_t* __restrict__ zr, const int* __restrict__ sigma, int D, int Kp,
-                                    NT* __restrict__ n) {
+                                    NT* __restrict__ n, const uint16_t* __restrict__ zr_doc) {
     extern __shared__ int hist[];                    // [warps][Kp]
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
     int* h = hist + (size_t)(threadIdx.x >> 5) * Kp;
@@ -996,6 +999,9 @@ __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const 
         for (int j = lane; j < Kp; j += 32) h[j] = 0;
         __syncwarp();
         const uint32_t e = doc_ptr[d + 1];
+        if (zr_doc) {   // the sample kernel already wrote the assignments in document order: stream them
+            for (uint32_t t = doc_ptr[d] + lane; t < e; t += 32) atomicAdd(&h[sigma[zr_doc[t] & 0x7FFFu]], 1);
+        } else
         // 4 tokens per lane in flight: the positions, then the scattered assignments, then the histogram
         for (uint32_t t0 = doc_ptr[d]; t0 < e; t0 += 128) {
             uint32_t pos[4];
