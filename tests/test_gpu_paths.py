@@ -118,6 +118,16 @@ def test_chunk_factor_tables_lockstep(monkeypatch, K, waves, extra):
     _lockstep(c, K, waves, 3)
 
 
+@pytest.mark.parametrize("K,rowb", [(100, 4), (200, 1), (1000, 2)])
+def test_document_order_scatter_lockstep(monkeypatch, K, rowb):
+    """W = 1 with the assignments also scattered to their document-order slots (the HBM-bound default:
+    SPDP_DOC_SCATTER) and the recount streaming them; forced on small corpora."""
+    monkeypatch.setenv("SPDP_DOC_SCATTER", "1")
+    monkeypatch.setenv("SPDP_ROW_BYTES", str(rowb))
+    c = synth.generate(2, 30, 40.0, 300, 8, seed=K + rowb)
+    _lockstep(c, K, 1, 3)
+
+
 @pytest.mark.parametrize("name,K", [("C1", 200), ("C2", 300)])
 def test_sparse_rows_split_segments_lockstep(monkeypatch, name, K):
     monkeypatch.setenv("SPDP_SPARSE_ROWS", "1")
