@@ -480,7 +480,9 @@ def main():
     t_pin = time.perf_counter()
     hin = [torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).pin_memory().numpy()
            for a in (corpus.group, corpus.doc, corpus.word)]
-    zr = [torch.empty(N, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16) for _ in range(2)]
+    narrow = K <= 128                                            # the step's result in one byte per token
+    zr = [torch.empty(N, dtype=torch.uint8, pin_memory=True).numpy() if narrow else
+          torch.empty(N, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16) for _ in range(2)]
     t_pin = time.perf_counter() - t_pin
     t0 = time.perf_counter()
     h = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
@@ -493,7 +495,10 @@ def main():
     for s in range(e2e_steps):
         h.sweep(1)
         h.wait()                                        # step s-1's assignments have landed in zr[(s-1) % 2]
-        h.zr_async(zr[s % 2])                           # D2H of step s's z | r << 15, overlapping sweep s+1
+        if narrow:
+            h.zr8_async(zr[s % 2])                      # D2H of step s's z | r << 7, overlapping sweep s+1
+        else:
+            h.zr_async(zr[s % 2])                       # D2H of step s's z | r << 15, overlapping sweep s+1
     h.wait()
     torch.cuda.synchronize(); barrier()
     e2e_s = time.perf_counter() - t0
@@ -506,9 +511,11 @@ def main():
            "load_phases_ms": phases.ms,
            "host_buffer_pin_ms_untimed": round(t_pin * 1e3, 2),
            "ms_per_step_after_setup": round((e2e_s - t_setup) * 1e3 / e2e_steps, 4),
-           "h2d_bytes_per_step": int(N * 12 / e2e_steps), "d2h_bytes_per_step": int(plan["tokens"] * 2),
+           "h2d_bytes_per_step": int(N * 12 / e2e_steps), "d2h_bytes_per_step": int(N * (1 if narrow else 2)),
            "includes": "spdp_create + spdp_load_corpus (host token arrays) + per step spdp_sweep(1) + "
-                       "spdp_zr_async (packed z, r of every token) into pinned host memory, the copy of step s overlapping "
+                       + ("spdp_zr8_async (z | r << 7, one byte per token)" if narrow else
+                          "spdp_zr_async (z | r << 15, two bytes per token)")
+                       + " of every token into pinned host memory, the copy of step s overlapping "
                        "sweep s+1, spdp_wait each step; wall clock, max over ranks"}
 
     line = {

@@ -206,6 +206,11 @@ spdp_status spdp_zr(spdp_ctx* ctx, uint16_t* zr);
  * With world_size > 1 and SPDP_EXCHANGE_NCCL this is spdp_zr (collective,
  * blocking).  Errors as spdp_zr. */
 spdp_status spdp_zr_async(spdp_ctx* ctx, uint16_t* zr);
+/* spdp_zr_async with one byte per token, zr [N] uint8 = z | r << 7 (K <= 128,
+ * else SPDP_EINVAL): half the device->host bytes of the step's result.
+ * Tokens of other ranks read 0xFF with SPDP_EXCHANGE_EXTERNAL; with
+ * SPDP_EXCHANGE_NCCL and world_size > 1 it is collective and blocking. */
+spdp_status spdp_zr8_async(spdp_ctx* ctx, uint8_t* zr);
 /* Block until every copy queued by spdp_zr_async has landed and the
  * context's stream is idle.  SPDP_ECUDA on a device fault. */
 spdp_status spdp_wait(spdp_ctx* ctx);

@@ -39,7 +39,7 @@ EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "s
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
            "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr",
            "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait", "spdp_debug_ratio_table",
-           "spdp_debug_chain"]
+           "spdp_debug_chain", "spdp_zr8_async"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -90,7 +90,7 @@ def lib():
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
             "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_zr_async": [P, P], "spdp_wait": [P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
-            "spdp_debug_ratio_table": [P, I32, I32, P], "spdp_debug_chain": [P, I32, I32, P],
+            "spdp_debug_ratio_table": [P, I32, I32, P], "spdp_debug_chain": [P, I32, I32, P], "spdp_zr8_async": [P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -230,6 +230,13 @@ def spdp_zr_async(ctx, N, out):
     until spdp_wait); returns at once (include/spdp.h)."""
     assert out.dtype == np.uint16 and out.shape == (N,) and out.flags["C_CONTIGUOUS"]
     _check(lib().spdp_zr_async(ctx, _p(out)), ctx)
+    return out
+
+
+def spdp_zr8_async(ctx, N, out):
+    """spdp_zr_async with one byte per token (z | r << 7, K <= 128)."""
+    assert out.dtype == np.uint8 and out.shape == (N,) and out.flags["C_CONTIGUOUS"]
+    _check(lib().spdp_zr8_async(ctx, _p(out)), ctx)
     return out
 
 
@@ -385,6 +392,11 @@ class Sampler:
     def zr_async(self, out):
         """Copy of the assignments into out, landing by the next wait() (overlaps the next sweep)."""
         self._zr_pending.append(spdp_zr_async(self.ctx, self.N, out))
+        return out
+
+    def zr8_async(self, out):
+        """One byte per token (z | r << 7, K <= 128), landing by the next wait()."""
+        self._zr_pending.append(spdp_zr8_async(self.ctx, self.N, out))
         return out
 
     def wait(self):

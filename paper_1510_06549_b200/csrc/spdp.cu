@@ -186,6 +186,7 @@ struct spdp_ctx {
     int prefetch_rows = 0;
     uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
     cudaStream_t d2h_stream = nullptr;            // spdp_zr_async's copies (overlap the next sweep)
+    uint8_t* d_zr8_canon = nullptr;               // spdp_zr8_async's staging buffer (z | r << 7)
     cudaEvent_t zr_ready = nullptr, zr_copied = nullptr;
     bool zr_pending = false;                      // a queued copy may still read d_zr_canon
     uint16_t* h_zr_canon = nullptr;               // pinned host copy
@@ -2083,6 +2084,37 @@ spdp_status zr_stage(spdp_ctx* c) {
     return SPDP_OK;
 }
 }  // namespace
+
+spdp_status spdp_zr8_async(spdp_ctx* c, uint8_t* zr) {
+    spdp_status s = guard(c, true);
+    if (s) return s;
+    if (!zr) return fail(c, SPDP_EINVAL, "null output");
+    if (c->K > 128) return fail(c, SPDP_EINVAL, "spdp_zr8_async needs K <= 128 (z | r << 7 in one byte)");
+    if (c->G > 1 && c->cfg.exchange == SPDP_EXCHANGE_NCCL) {   // gathered: collective, blocking
+        std::vector<uint16_t> w((size_t)c->N);
+        if ((s = spdp_zr(c, w.data()))) return s;
+        for (int64_t p = 0; p < c->N; ++p) zr[p] = (uint8_t)((w[(size_t)p] & 0x7Fu) | ((w[(size_t)p] >> 15) << 7));
+        return SPDP_OK;
+    }
+    if (!c->d2h_stream) {
+        CU(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&c->zr_ready, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&c->zr_copied, cudaEventDisableTiming));
+    }
+    if (!c->d_zr8_canon) ALLOC(c->d_zr8_canon, c->N);
+    if (c->zr_pending) CU(cudaStreamWaitEvent(c->stream, c->zr_copied, 0));   // the previous copy has read it
+    if (c->Nloc < c->N) CU(cudaMemsetAsync(c->d_zr8_canon, 0xFF, (size_t)c->N, c->stream));
+    if (c->Nloc > 0)
+        scatter_zr8_kernel<<<148 * 8, 256, 0, c->stream>>>(c->d_tok_id, c->d_zr, (uint32_t)c->Nloc, c->d_zr8_canon);
+    if ((s = check_launch(c, "scatter_zr8_kernel"))) return s;
+    c->launches += 1;
+    CU(cudaEventRecord(c->zr_ready, c->stream));
+    CU(cudaStreamWaitEvent(c->d2h_stream, c->zr_ready, 0));
+    CU(cudaMemcpyAsync(zr, c->d_zr8_canon, (size_t)c->N, cudaMemcpyDeviceToHost, c->d2h_stream));
+    CU(cudaEventRecord(c->zr_copied, c->d2h_stream));
+    c->zr_pending = true;
+    return SPDP_OK;
+}
 
 spdp_status spdp_zr_async(spdp_ctx* c, uint16_t* zr) {
     spdp_status s = guard(c, true);

@@ -1359,6 +1359,15 @@ __global__ void scatter_zr_kernel(const uint32_t* __restrict__ id, const uint16_
         out[id[p]] = (uint16_t)(zr[p] + add);
 }
 
+// one byte per token (K <= 128): z | r << 7
+__global__ void scatter_zr8_kernel(const uint32_t* __restrict__ id, const uint16_t* __restrict__ zr, uint32_t n,
+                                   uint8_t* __restrict__ out) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        const uint32_t v = zr[p];
+        out[id[p]] = (uint8_t)((v & 0x7Fu) | ((v >> 15) << 7));
+    }
+}
+
 // ---------------------------------------------------------------- training perplexity
 // One warp per chunk (all waves): phi^i_kw = (m - a t)/(b + M) + (b + a Tt)/(b + M) phi0_kw,
 // phi0_kw = (beta + Q)/(V beta + T) (reading c16);

@@ -218,3 +218,19 @@ def test_full_size_library_recount(name, K, sweeps):
     assert st["sweeps"] == sweeps and st["moved"] > 0
     if name == "C5":
         assert st["row_bytes"] == 1 and (st["lanes_per_token"], st["topics_per_lane"]) == (8, 32)
+
+
+@pytest.mark.parametrize("K", [10, 100, 128])
+def test_zr8_async_matches_counts(K):
+    """spdp_zr8_async (the e2e read-back, one byte per token) equals z | r << 7 of spdp_counts."""
+    c = corpus("C1")
+    g = spdp.sampler_for(c, K, **HYPER)
+    out = np.zeros(c.num_tokens, np.uint8)
+    for _ in range(2):
+        g.sweep(1)
+        g.zr8_async(out)
+        g.wait()
+        gc = g.counts(doc_topic=False, customers=False, tables=False, shadow=False)
+        np.testing.assert_array_equal(out, (gc["z"] | (gc["r"].astype(np.int32) << 7)).astype(np.uint8))
+    with pytest.raises(spdp.SPDPError):
+        spdp.sampler_for(c, 200, **HYPER).zr8_async(np.zeros(c.num_tokens, np.uint8))
