@@ -17,7 +17,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     spdp.build()
     L = spdp.lib()
     header = open(os.path.join(ROOT, "include", "spdp.h")).read()
-    declared = set(re.findall(r"^\s*(?:spdp_status|void|const char\*)\s+(spdp_[a-z_]+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:spdp_status|void|const char\*)\s+(spdp_[a-z0-9_]+)\s*\(", header, re.M))
     assert declared == set(spdp.EXPORTS), declared ^ set(spdp.EXPORTS)
     for name in declared:
         assert hasattr(L, name), name
