@@ -148,6 +148,13 @@ spdp_status spdp_set_state(spdp_ctx* ctx, const int32_t* z, const uint8_t* r, co
  * PAPER.md:2960-2965).  Collective.  SPDP_ESTATE for
  * SPDP_EXCHANGE_EXTERNAL contexts (use the split calls below). */
 spdp_status spdp_sweep(spdp_ctx* ctx, int32_t num_sweeps);
+/* spdp_sweep without the final wait: the sweeps are queued on the context's
+ * stream and the call returns (the host-synchronous contract of the other
+ * calls is kept by them: spdp_counts, spdp_loglik, spdp_stats, ... order
+ * themselves after the queued work; spdp_zr_async / spdp_zr8_async queue
+ * their copy behind it).  Device faults surface at the next synchronising
+ * call.  With debug_checks it is spdp_sweep. */
+spdp_status spdp_sweep_async(spdp_ctx* ctx, int32_t num_sweeps);
 
 /* Split sweep for SPDP_EXCHANGE_EXTERNAL: spdp_sweep_local runs every wave
  * (with merge_every, the next exchange block of waves; see spdp_exchange_blocks)
@@ -211,7 +218,10 @@ spdp_status spdp_zr_async(spdp_ctx* ctx, uint16_t* zr);
  * Tokens of other ranks read 0xFF with SPDP_EXCHANGE_EXTERNAL; with
  * SPDP_EXCHANGE_NCCL and world_size > 1 it is collective and blocking. */
 spdp_status spdp_zr8_async(spdp_ctx* ctx, uint8_t* zr);
-/* Block until every copy queued by spdp_zr_async has landed and the
+/* Block until every copy queued by spdp_zr_async / spdp_zr8_async has
+ * landed (the copies follow their staging on the context's stream, so the
+ * work queued before them is done too; work queued after them, e.g. a
+ * spdp_sweep_async, may still run).  With no copy pending: until the
  * context's stream is idle.  SPDP_ECUDA on a device fault. */
 spdp_status spdp_wait(spdp_ctx* ctx);
 

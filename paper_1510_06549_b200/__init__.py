@@ -39,7 +39,7 @@ EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "s
            "spdp_stats", "spdp_profile", "spdp_timings", "spdp_partition", "spdp_nccl_unique_id", "spdp_destroy", "spdp_last_error",
            "spdp_version", "spdp_topics", "spdp_heldout", "spdp_topic_hellinger", "spdp_exchange_blocks", "spdp_zr",
            "spdp_set_transform", "spdp_sparse_state", "spdp_zr_async", "spdp_wait", "spdp_debug_ratio_table",
-           "spdp_debug_chain", "spdp_zr8_async"]
+           "spdp_debug_chain", "spdp_zr8_async", "spdp_sweep_async"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -90,7 +90,7 @@ def lib():
             "spdp_topics": [P, P, P],
             "spdp_heldout": [P, I64, I32, P, P, P, C.c_uint64, I32, I32, P, P, P, P],
             "spdp_topic_hellinger": [P, P, P, P], "spdp_exchange_blocks": [P, P], "spdp_zr": [P, P], "spdp_zr_async": [P, P], "spdp_wait": [P], "spdp_set_transform": [P, P, P, P], "spdp_sparse_state": [P, P, P, P],
-            "spdp_debug_ratio_table": [P, I32, I32, P], "spdp_debug_chain": [P, I32, I32, P], "spdp_zr8_async": [P, P],
+            "spdp_debug_ratio_table": [P, I32, I32, P], "spdp_debug_chain": [P, I32, I32, P], "spdp_zr8_async": [P, P], "spdp_sweep_async": [P, I32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -233,6 +233,10 @@ def spdp_zr_async(ctx, N, out):
     return out
 
 
+def spdp_sweep_async(ctx, num_sweeps):
+    _check(lib().spdp_sweep_async(ctx, int(num_sweeps)), ctx)
+
+
 def spdp_zr8_async(ctx, N, out):
     """spdp_zr_async with one byte per token (z | r << 7, K <= 128)."""
     assert out.dtype == np.uint8 and out.shape == (N,) and out.flags["C_CONTIGUOUS"]
@@ -346,6 +350,10 @@ class Sampler:
 
     def sweep(self, n=1):
         spdp_sweep(self.ctx, n)
+
+    def sweep_async(self, n=1):
+        """Queue n sweeps and return (see spdp_sweep_async)."""
+        spdp_sweep_async(self.ctx, n)
 
     def sweep_local(self):
         spdp_sweep_local(self.ctx)

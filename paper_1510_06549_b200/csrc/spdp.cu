@@ -1836,7 +1836,17 @@ spdp_status spdp_sweep_merge(spdp_ctx* c) {
     return SPDP_OK;
 }
 
-spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
+namespace {
+spdp_status sweep_impl(spdp_ctx* c, int32_t num_sweeps, bool wait);
+}
+
+spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) { return sweep_impl(c, num_sweeps, true); }
+spdp_status spdp_sweep_async(spdp_ctx* c, int32_t num_sweeps) { return sweep_impl(c, num_sweeps, false); }
+
+}  // extern "C"
+
+namespace {
+spdp_status sweep_impl(spdp_ctx* c, int32_t num_sweeps, bool wait) {
     spdp_status s = guard(c, true);
     if (s) return s;
     if (num_sweeps < 0) return fail(c, SPDP_EINVAL, "num_sweeps must be >= 0");
@@ -1924,8 +1934,12 @@ spdp_status spdp_sweep(spdp_ctx* c, int32_t num_sweeps) {
             if ((s = debug_verify(c))) return s;
         }
     }
+    if (!wait && !c->cfg.debug_checks) return check_launch(c, "spdp_sweep_async");
     return sync(c, "spdp_sweep");
 }
+}  // namespace
+
+extern "C" {
 
 spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic, int32_t* customers, int32_t* tables,
                         int32_t* shadow) {
@@ -2138,9 +2152,10 @@ spdp_status spdp_zr_async(spdp_ctx* c, uint16_t* zr) {
 spdp_status spdp_wait(spdp_ctx* c) {
     spdp_status s = guard(c, false);
     if (s) return s;
-    if (c->zr_pending) {
+    if (c->zr_pending) {                 // the copy (and the work before its staging) only
         CU(cudaEventSynchronize(c->zr_copied));
         c->zr_pending = false;
+        return check_launch(c, "spdp_wait");
     }
     return sync(c, "spdp_wait");
 }

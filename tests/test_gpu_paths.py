@@ -234,3 +234,28 @@ def test_zr8_async_matches_counts(K):
         np.testing.assert_array_equal(out, (gc["z"] | (gc["r"].astype(np.int32) << 7)).astype(np.uint8))
     with pytest.raises(spdp.SPDPError):
         spdp.sampler_for(c, 200, **HYPER).zr8_async(np.zeros(c.num_tokens, np.uint8))
+
+
+def test_sweep_async_pipeline_equals_sweep():
+    """The e2e loop of bench.py (spdp_sweep_async, then the wait for the previous step's copy, then
+    spdp_zr8_async into alternating buffers) gives the same chain and every step's assignments."""
+    c = corpus("C2")
+    K = 50
+    ref = spdp.sampler_for(c, K, **HYPER)
+    g = spdp.sampler_for(c, K, **HYPER)
+    bufs = [np.zeros(c.num_tokens, np.uint8) for _ in range(2)]
+    want = []
+    for s in range(4):
+        ref.sweep(1)
+        gc = ref.counts(doc_topic=False, customers=False, tables=False, shadow=False)
+        want.append((gc["z"] | (gc["r"].astype(np.int32) << 7)).astype(np.uint8))
+        g.sweep_async(1)
+        g.wait()
+        if s > 0:
+            np.testing.assert_array_equal(bufs[(s - 1) % 2], want[s - 1])
+        g.zr8_async(bufs[s % 2])
+    g.wait()
+    np.testing.assert_array_equal(bufs[3 % 2], want[3])
+    a, b = ref.counts(), g.counts()
+    for k in ("z", "r", "n", "m", "t", "Q"):
+        np.testing.assert_array_equal(a[k], b[k])
