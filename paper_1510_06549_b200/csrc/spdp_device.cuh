@@ -34,6 +34,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_PRO_GROUP
 #define SPDP_PRO_GROUP 1           // chunk prologue: topics per lane whose loads are issued together (B200, C3:
 #endif                             // 4 -> 1.102 ms, 1 -> 1.053 ms: the register-capped 4x32 kernel schedules worse)
+#ifndef SPDP_SMEM_R1
+#define SPDP_SMEM_R1 1             // chunk prologue keeps every topic's r = 1 share in shared memory (KSPAN <= 256)
+#endif
 #ifndef SPDP_BULK_PREFETCH
 #define SPDP_BULK_PREFETCH 0       // 1: exact-byte cp.async.bulk.prefetch.L2 of the next batch instead of this batch's
                                    // 128-B lines (B200, C5: 37.4 vs 34.7 ms per sweep with uint8 rows: fewer bytes, but
@@ -411,6 +414,7 @@ struct WarpSmem {
     float F[KSPAN];      // F0 + F1 at the snapshot counts
     float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
     uint32_t mt[KSPAN];  // snapshot m << 16 | t of the segment's cells (M_max < 2^16)
+    float R1[SPDP_SMEM_R1 && KSPAN <= 256 ? KSPAN : 1];   // r = 1 share F1 / F at the snapshot (phase 3's r split)
     int dmt[KSPAN];      // the chunk's delta m * 2^16 + delta t (|delta| <= chunk length)
     // hand-over from the dense pass to the per-token search (one entry per token of the batch)
     float bs[KPL / 4][32];   // the winning lane's block sums (without the own-removal fix)
@@ -477,6 +481,9 @@ sample_kernel(SweepArgs A) {
     constexpr bool kRowPipe = SPDP_ROW_PIPELINE != 0 && sample_minb<LPT, KPL>() <= 4;
     // own-removal inputs before the Philox rounds: C3 -1 %, K = 300 -1.8 %, C5 (8x32) +1 % (B200)
     constexpr bool kPreTab = SPDP_PRE_TAB != 0 && sample_minb<LPT, KPL>() <= 4;
+    // r = 1 shares from the prologue in shared memory (not in the async mode: its copy is per chunk too,
+    // but the live sums it reads in phase 3 are fresher); KSPAN <= 256 (smem budget of 16x32 / 32x32)
+    constexpr bool kSmemR1 = SPDP_SMEM_R1 != 0 && KSPAN <= 256 && !ASYNC;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
@@ -515,6 +522,7 @@ sample_kernel(SweepArgs A) {
             float Fk = 0.f, aFk = 0.f;
             uint32_t mt = 0;
             if (k < K) { Fk = A.Ft[rrow + k]; aFk = A.aFt[rrow + k]; mt = A.MTt[rrow + k]; }
+            if constexpr (kSmemR1) S.R1[k] = (k < K) ? A.R1t[rrow + k] : 0.f;
             S.F[k] = Fk;
             S.aF[skew<KPL>(k)] = aFk;
             S.mt[k] = mt;
@@ -558,6 +566,7 @@ sample_kernel(SweepArgs A) {
                 if (k < K) slot_factors(Mv[j], Ttv[j], Qv[j], Tv[j], tb[j], a, b, A.beta, A.vbeta, F0, F1);
                 if (k >= KSPAN) continue;            // KSPAN < 32 (K <= 16)
                 const float Fk = F0 + F1;
+                if constexpr (kSmemR1) S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
                 S.F[k] = Fk;
                 S.aF[skew<KPL>(k)] = __fmul_rn(al[j], Fk);
                 S.mt[k] = ((uint32_t)mv[j] << 16) | (uint32_t)tv[j];
@@ -792,7 +801,9 @@ sample_kernel(SweepArgs A) {
                 const bool own = (ks == k0);
                 const uint32_t mts = S.mt[ks];
                 float R1s = R1k0;
-                if (!own && !ASYNC && A.chunk_ft) R1s = A.R1t[(size_t)crun * Kp + ks];   // from the factor table
+                if constexpr (kSmemR1) {
+                    if (!own) R1s = S.R1[ks];              // the chunk prologue's share
+                } else if (!own && !ASYNC && A.chunk_ft) R1s = A.R1t[(size_t)crun * Kp + ks];   // from the factor table
                 else if (!own) {                           // r = 1 share of topic ks at the snapshot
                     float f0, f1;
                     int Ms, Tts, Qs, Ts;
@@ -826,7 +837,8 @@ sample_kernel(SweepArgs A) {
                 inf[0] = rrem; inf[1] = keep; inf[2] = ks; inf[3] = rs;
             } else {
                 A.zr_next[p] = (uint16_t)(ks | (rs << 15));                                   // a7
-                if constexpr (!ASYNC) if (A.zr_doc) A.zr_doc[A.slot[p]] = (uint16_t)(ks | (rs << 15));
+                if constexpr (!ASYNC && KSPAN <= 256)   // (the host enables it for K <= 256 only)
+                    if (A.zr_doc) A.zr_doc[A.slot[p]] = (uint16_t)(ks | (rs << 15));
                 if (keep) ++keeps;
                 else {
                     atomicAdd(&S.dmt[k0], -65536 - rrem);

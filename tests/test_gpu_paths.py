@@ -118,7 +118,7 @@ def test_chunk_factor_tables_lockstep(monkeypatch, K, waves, extra):
     _lockstep(c, K, waves, 3)
 
 
-@pytest.mark.parametrize("K,rowb", [(100, 4), (200, 1), (1000, 2)])
+@pytest.mark.parametrize("K,rowb", [(100, 4), (200, 1), (256, 2)])
 def test_document_order_scatter_lockstep(monkeypatch, K, rowb):
     """W = 1 with the assignments also scattered to their document-order slots (the HBM-bound default:
     SPDP_DOC_SCATTER) and the recount streaming them; forced on small corpora."""
