@@ -160,6 +160,7 @@ struct spdp_ctx {
     bool pack_dmt = false;                        // chunk kernels flush packed dm * 2^16 + dt words (M_max < 2^15)
     bool chunk_ft = false;                        // chunk kernel reads per-wave factor tables (SPDP_CHUNK_FACTORS)
     bool doc_scatter = false;                     // W = 1 chunk kernel also writes zr in document order (recount streams it)
+    bool fold_merge = false;                      // several ranks, W = 1: the local merge writes only the net change
     uint32_t* d_slot = nullptr;                   // document-order slot of each sorted token
     uint16_t* d_zr_doc = nullptr;
     uint32_t* d_tok_run = nullptr;                // run (segment of a wave) of each sorted token
@@ -539,11 +540,11 @@ void launch_exchange_merge_range(spdp_ctx* c, int w0, int w1, int32_t* M, int32_
     if (c->pack32)
         exchange_merge_kernel<int32_t><<<grid, 256, use_smem ? smem : 0, st>>>(
             c->d_m, c->d_t, (int32_t*)c->d_Dloc, (const int32_t*)c->d_Dsum, c->d_Q, M, Tt, T, w0, w1, c->I, c->Kp,
-            use_smem, c->d_stats);
+            use_smem, c->d_stats, (int)c->fold_merge);
     else
         exchange_merge_kernel<long long><<<grid, 256, use_smem ? smem : 0, st>>>(
             c->d_m, c->d_t, (long long*)c->d_Dloc, (const long long*)c->d_Dsum, c->d_Q, M, Tt, T, w0, w1, c->I, c->Kp,
-            use_smem, c->d_stats);
+            use_smem, c->d_stats, (int)c->fold_merge);
 }
 void sparse_exchange_merge(spdp_ctx* c);
 void launch_exchange_merge(spdp_ctx* c) {
@@ -927,7 +928,7 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
             const int blocks = (int)std::min<uint32_t>((re - rb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, st>>>(
                 c->d_wave_segs + rb, (int)(re - rb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q,
-                c->d_Mn, c->d_Ttn, c->d_Tn, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt));
+                c->d_Mn, c->d_Ttn, c->d_Tn, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt), 0);
             c->launches += 2;
         }
         if (c->overlap) {                                   // rows of part p: all-reduce + merge on comm_stream
@@ -1058,7 +1059,8 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             const int blocks = (int)std::min<uint32_t>((se - sb + 7) / 8, 148u * 4u);
             merge_segments_kernel<<<std::max(blocks, 1), 256, use_smem ? smem : 0, c->stream>>>(
                 c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q, c->d_M,
-                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt));
+                c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt),
+                (int)c->fold_merge);
         }
         rec(c, 4 * (size_t)w + 3);
         c->launches += 3;
@@ -1677,6 +1679,10 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         ALLOC(dl, words); ALLOC(ds, words);
         c->d_Dloc = dl; c->d_Dsum = ds;
     }
+    // several ranks with one wave and no part pipelining: the local merge before the exchange writes only the
+    // rank's net change (the exchange merge installs S0 + sum and rebuilds Q and the sums)
+    c->fold_merge = c->G > 1 && W == 1 && !c->overlap && !c->sparse && !c->async && c->P <= 1 &&
+                    !(getenv("SPDP_FOLD_MERGE") && atoi(getenv("SPDP_FOLD_MERGE")) == 0);
     ALLOC(c->d_Q, (size_t)V * Kp);
     ALLOC(c->d_M, (size_t)I * Kp); ALLOC(c->d_Tt, (size_t)I * Kp); ALLOC(c->d_T, (size_t)Kp);
     if (c->P > 1) {

@@ -410,7 +410,7 @@ struct SweepArgs {
 
 // Per-warp shared memory (KSPAN entries each unless noted).
 template <int KSPAN, int KPL>
-struct WarpSmem {
+struct __align__(16) WarpSmem {   // 16-byte multiple: every warp's F rows are read as float4
     float F[KSPAN];      // F0 + F1 at the snapshot counts
     float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
     uint32_t mt[KSPAN];  // snapshot m << 16 | t of the segment's cells (M_max < 2^16)
@@ -1111,7 +1111,10 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
                                       void* __restrict__ D, int pack32,
                                       int32_t* __restrict__ Q, int32_t* __restrict__ M, int32_t* __restrict__ Tt,
                                       int32_t* __restrict__ T, int I, int Kp, int use_smem_sums,
-                                      unsigned long long* __restrict__ stats, int packed_deltas) {
+                                      unsigned long long* __restrict__ stats, int packed_deltas, int fold) {
+    // fold (several ranks, W = 1, the exchange follows): the rows keep the sweep-start S0 and only the
+    // rank's net change D = clamp(S0 + delta) - S0 is written; the exchange merge installs clamp(S0 + sum D)
+    // and rebuilds Q and the sums, so the local row writes and sum updates would be overwritten anyway
     extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
     int* sM = ssum;
     int* sT = ssum + (size_t)I * Kp;
@@ -1154,8 +1157,10 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
                 clamped += (tv != raw);
                 pm[e] = mv; pt[e] = tv;
             }
-            *reinterpret_cast<int4*>(m + off) = vm;
-            *reinterpret_cast<int4*>(t + off) = vt;
+            if (!fold) {
+                *reinterpret_cast<int4*>(m + off) = vm;
+                *reinterpret_cast<int4*>(t + off) = vt;
+            }
             *reinterpret_cast<int4*>(dm + off) = make_int4(0, 0, 0, 0);
             if (!packed_deltas) *reinterpret_cast<int4*>(dt + off) = make_int4(0, 0, 0, 0);
             const int cm[4] = {vm.x - om.x, vm.y - om.y, vm.z - om.z, vm.w - om.w};
@@ -1164,6 +1169,7 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
                 if (pack32) Packed<int32_t>::add4(reinterpret_cast<int32_t*>(D) + off, cm, ct);
                 else Packed<long long>::add4(reinterpret_cast<long long*>(D) + off, cm, ct);
             }
+            if (fold) continue;
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (ct[e]) {
@@ -1217,7 +1223,7 @@ template <typename P>
 __global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restrict__ t, P* __restrict__ Dloc,
                                       const P* __restrict__ Dsum, int32_t* __restrict__ Q, int32_t* __restrict__ M,
                                       int32_t* __restrict__ Tt, int32_t* __restrict__ T, int w0, int w1, int I, int Kp,
-                                      int use_smem_sums, unsigned long long* __restrict__ stats) {
+                                      int use_smem_sums, unsigned long long* __restrict__ stats, int rows_s0) {
     extern __shared__ __align__(16) int ssum[];      // [2][I][Kp] + [Kp] when use_smem_sums
     int* sM = ssum;
     int* sT = ssum + (size_t)I * Kp;
@@ -1244,8 +1250,8 @@ __global__ void exchange_merge_kernel(int32_t* __restrict__ m, int32_t* __restri
                     int* pm = &vm.x; int* pt = &vt.x;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        const int mv = pm[e] - lm[e] + gm[e];
-                        const int raw = pt[e] - lt[e] + gt[e];
+                        const int mv = pm[e] - (rows_s0 ? 0 : lm[e]) + gm[e];   // rows_s0: the rows are S0 (fold)
+                        const int raw = pt[e] - (rows_s0 ? 0 : lt[e]) + gt[e];
                         int tv = min(raw, mv);
                         tv = (mv > 0) ? max(tv, 1) : 0;
                         clamped += (tv != raw);
