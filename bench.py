@@ -242,6 +242,13 @@ def cpu_model():
     return "unknown"
 
 
+def static_config(cfg, corpus, K, waves, world, workload):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": workload, "tokens": corpus.num_tokens, "groups": cfg.groups, "docs": corpus.num_docs,
+            "vocab": cfg.vocab, "topics": K, "waves": waves, "parallelism": f"doc-shard x{world}",
+            "l2": "flushed between timed sweeps"}
+
+
 def recorded_ppl_gap(waves, update):
     """The BASELINE metric's third part, from the latest committed measurement (tools/ppl_gap.py:
     training perplexity after 100 sweeps of C2, 3 seeds per schedule, against the exact sequential
@@ -523,9 +530,8 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic SPDP-generated corpus (synth/, seeded)",
-        "config": {"workload": workload, "tokens": N, "groups": cfg.groups, "docs": corpus.num_docs,
-                   "vocab": cfg.vocab, "topics": K, "waves": args.waves, "parallelism": f"doc-shard x{world}",
-                   "arithmetic": "f32 slot masses, f64 CDF prefix and uniform, int32 counts, exact integer removal draw",
+        "config": static_config(cfg, corpus, K, args.waves, world, workload),
+        "timing": {"arithmetic": "f32 slot masses, f64 CDF prefix and uniform, int32 counts, exact integer removal draw",
                    "l2": "flushed between timed sweeps (256 MiB write outside the events)" if flush is not None else "not flushed",
                    "sweep_ms": [round(x, 4) for x in step_ms],
                    "sweep": "one CUDA-graph replay per step (single rank); the roofline's kernel time comes from "
@@ -539,6 +545,13 @@ def main():
         "stats": stats,
         "timings_ms": {k: round(v, 4) for k, v in tm.items()},
     }
+    if world > 1:   # the exchange of this run: one packed int32 per (w, i, k) cell, all-reduced per sweep
+        kp = (K + 3) // 4 * 4
+        line["multi_gpu"] = {"ranks": world, "backend": "NCCL all-reduce over NVLink (library-owned communicator)",
+                             "exchange_bytes_per_sweep": cfg.vocab * cfg.groups * kp * 4,
+                             "parts": stats.get("parts"), "exchange_ms_per_sweep": round(tm["exchange_ms"] / max(tm["sweeps"], 1), 4),
+                             "merge_ms_per_sweep": round(tm["merge_ms"] / max(tm["sweeps"], 1), 4),
+                             "sample_ms_per_sweep": round(tm["sample_ms"] / max(tm["sweeps"], 1), 4)}
     line["perplexity_gap"] = recorded_ppl_gap(args.waves, args.update)
     if rank == 0 and world == 1 and not args.no_cpu_baseline and transform is None:
         st = args.cpu_sample_tokens or min(N, 400_000 if K <= 100 else 100_000)
@@ -624,7 +637,9 @@ def run_reference(args, cfg, K, world, rank, workload):
     from oracle_timing import threads_used
     import synth
     corpus = synth.corpus_for(cfg)
-    sample = args.cpu_sample_tokens or min(corpus.num_tokens, 1_000_000 if K <= 100 else 200_000)
+    # whole sweeps (C3 on 16 cores: ~4 s each) unless the workload is larger; per-call fixed passes over the
+    # count tables make short prefixes understate the oracle's throughput
+    sample = args.cpu_sample_tokens or min(corpus.num_tokens, 12_000_000 if K <= 100 else 2_000_000)
     import oracle
     o = oracle.from_corpus(corpus, K, cfg.alpha, cfg.beta, cfg.discount, cfg.concentration, cfg.seed)
     for _ in range(args.warmup):
@@ -637,13 +652,13 @@ def run_reference(args, cfg, K, world, rank, workload):
     ms = 1e3 * float(np.mean(times))
     value = sample / (ms / 1e3)
     cb = {"value": value, "unit": "tokens/s", "cores": threads_used(), "kind": "oracle",
-          "sample": f"first {sample} tokens of a mode-P (W={args.waves}) sweep of {cfg.name} per step "
+          "sample": f"{'all' if sample >= corpus.num_tokens else 'first ' + str(sample)} tokens of a mode-P (W={args.waves}) sweep of {cfg.name} per step "
                     f"(plain C oracle, fp64 log space; -fopenmp build over the wave's decisions)"}
     line = {"impl": "reference", "metric": "sampled tokens/sec per sweep", "value": round(value, 1),
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic SPDP-generated corpus (synth/, seeded)",
-            "config": {"workload": workload, "tokens": corpus.num_tokens, "topics": K, "waves": args.waves},
+            "config": static_config(cfg, corpus, K, args.waves, world, workload),
             "cpu_baseline": cb,
             "e2e": {"value": round(value, 1), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
