@@ -37,6 +37,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_SMEM_R1
 #define SPDP_SMEM_R1 1             // chunk prologue keeps every topic's r = 1 share in shared memory (KSPAN <= 256)
 #endif
+#ifndef SPDP_NARROW_FULL
+#define SPDP_NARROW_FULL 1         // uint8/uint16 rows at 8x32: block alpha sums and row pipelining as at 4 blocks/SM
+#endif
 #ifndef SPDP_BULK_PREFETCH
 #define SPDP_BULK_PREFETCH 0       // 1: exact-byte cp.async.bulk.prefetch.L2 of the next batch instead of this batch's
                                    // 128-B lines (B200, C5: 37.4 vs 34.7 ms per sweep with uint8 rows: fewer bytes, but
@@ -263,6 +266,12 @@ __device__ __forceinline__ void load_sums(const int32_t* Mi, const int32_t* Tti,
 
 template <>
 struct Row<float> {
+    // raw block of 4 counts as loaded (converted to fp32 at use: narrow rows keep fewer registers live)
+    using raw_t = float4;
+    __device__ __forceinline__ static raw_t load_raw(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+    __device__ __forceinline__ static raw_t load_raw_live(const float* p) { return load4_live(p); }
+    __device__ __forceinline__ static float4 cvt(raw_t v) { return v; }
+    __device__ __forceinline__ static raw_t zero_raw() { return make_float4(0.f, 0.f, 0.f, 0.f); }
     __device__ __forceinline__ static float4 load4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
     __device__ __forceinline__ static float4 load4_live(const float* p) {
         if constexpr (kAsyncWeakRows) return ld_weak_f4(p);
@@ -287,6 +296,13 @@ __device__ __forceinline__ float u16hi(uint32_t x) { return __int_as_float((int)
 #endif
 template <>
 struct Row<uint16_t> {
+    using raw_t = uint2;
+    __device__ __forceinline__ static raw_t load_raw(const uint16_t* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+    __device__ __forceinline__ static raw_t load_raw_live(const uint16_t* p) {
+        return kAsyncWeakRows ? ld_weak_u2(p) : ld_relaxed_u2(p);
+    }
+    __device__ __forceinline__ static float4 cvt(raw_t v) { return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y)); }
+    __device__ __forceinline__ static raw_t zero_raw() { return make_uint2(0u, 0u); }
     __device__ __forceinline__ static float4 load4(const uint16_t* p) {
         const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
         return make_float4(u16lo(v.x), u16hi(v.x), u16lo(v.y), u16hi(v.y));
@@ -315,6 +331,11 @@ __device__ __forceinline__ float u8at(uint32_t x, uint32_t j) {
 }
 template <>
 struct Row<uint8_t> {
+    using raw_t = uint32_t;
+    __device__ __forceinline__ static raw_t load_raw(const uint8_t* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
+    __device__ __forceinline__ static raw_t load_raw_live(const uint8_t* p) { return (uint32_t)ld_weak_or_relaxed(p); }
+    __device__ __forceinline__ static float4 cvt(raw_t v) { return make_float4(u8at(v, 0), u8at(v, 1), u8at(v, 2), u8at(v, 3)); }
+    __device__ __forceinline__ static raw_t zero_raw() { return 0u; }
     __device__ __forceinline__ static float4 load4(const uint8_t* p) {
         const uint32_t v = __ldg(reinterpret_cast<const unsigned int*>(p));
         return make_float4(u8at(v, 0), u8at(v, 1), u8at(v, 2), u8at(v, 3));
@@ -445,6 +466,11 @@ __device__ __forceinline__ float4 row_load4(const NT* p) {
     else return Row<NT>::load4(p);
 }
 template <typename NT, bool AS>
+__device__ __forceinline__ typename Row<NT>::raw_t row_load_raw(const NT* p) {
+    if constexpr (AS) return Row<NT>::load_raw_live(p);
+    else return Row<NT>::load_raw(p);
+}
+template <typename NT, bool AS>
 __device__ __forceinline__ float row_load1(const NT* p) {
     if constexpr (AS) return Row<NT>::load1_live(p);
     else return Row<NT>::load1(p);
@@ -475,10 +501,13 @@ sample_kernel(SweepArgs A) {
     constexpr bool kSkipPad = SPDP_SKIP_PAD_BLOCKS && (LPT == 4 || LPT == 16);
     // per-block alpha sums: 2.5-3.5 % faster at C3, K = 300, K = 1000 (B200); not under the
     // 5-blocks register cap of 8x32, where the 8 extra registers spill (C5 +2.7 %)
-    constexpr bool kBlockAlpha = SPDP_BLOCK_ALPHA != 0 && sample_minb<LPT, KPL>() <= 4;
+    // narrow rows keep their raw blocks (1-2 registers per 4 counts instead of 4), which frees the registers the
+    // 5-blocks/SM 8x32 build needs for the block alpha sums and the row pipeline (SPDP_NARROW_FULL)
+    constexpr bool kNarrowFull = SPDP_NARROW_FULL != 0 && sizeof(NT) < 4;
+    constexpr bool kBlockAlpha = SPDP_BLOCK_ALPHA != 0 && (sample_minb<LPT, KPL>() <= 4 || kNarrowFull);
     // software-pipelined row loads: C3 -3 %, K = 300 -7 %, K = 1000 +-0 (B200); spills under the
     // 8x32 register cap (C5 +30 %), so not there
-    constexpr bool kRowPipe = SPDP_ROW_PIPELINE != 0 && sample_minb<LPT, KPL>() <= 4;
+    constexpr bool kRowPipe = SPDP_ROW_PIPELINE != 0 && (sample_minb<LPT, KPL>() <= 4 || kNarrowFull);
     // own-removal inputs before the Philox rounds: C3 -1 %, K = 300 -1.8 %, C5 (8x32) +1 % (B200)
     constexpr bool kPreTab = SPDP_PRE_TAB != 0 && sample_minb<LPT, KPL>() <= 4;
     // r = 1 shares from the prologue in shared memory (not in the async mode: its copy is per chunk too,
@@ -668,19 +697,19 @@ sample_kernel(SweepArgs A) {
         const float dlt = wnew - wold;
 
         // ======== phase 2: LPT lanes per token
-        float4 v[NB];
+        typename Row<NT>::raw_t v[NB];               // raw blocks (fp32 at use: narrow rows keep few registers)
         auto load_rows = [&](uint32_t s) {            // the doc-topic rows of step s's tokens
             const uint32_t so = __shfl_sync(0xffffffffu, noff, (s + g) & 31);
             const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + so + 4 * gl;
 #pragma unroll
             for (int q = 0; q < NB; ++q) {   // blocks past K hold no topic (zero mass): no load, or one inside the row
                 if constexpr (kSkipPad)
-                    v[q] = (kb + 4 * q < K) ? row_load4<NT, ASYNC>(nl + 4 * A.colstart[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    v[q] = (kb + 4 * q < K) ? row_load_raw<NT, ASYNC>(nl + 4 * A.colstart[q]) : Row<NT>::zero_raw();
                 else if constexpr (SPDP_PAD_SELECT)
-                    v[q] = row_load4<NT, ASYNC>((kb + 4 * q < K) ? nl + 4 * A.colstart[q]
-                                                                 : reinterpret_cast<const NT*>(A.n) + so);
+                    v[q] = row_load_raw<NT, ASYNC>((kb + 4 * q < K) ? nl + 4 * A.colstart[q]
+                                                                    : reinterpret_cast<const NT*>(A.n) + so);
                 else
-                    v[q] = row_load4<NT, ASYNC>(nl + 4 * A.colstart[q]);
+                    v[q] = row_load_raw<NT, ASYNC>(nl + 4 * A.colstart[q]);
             }
         };
         if constexpr (kRowPipe) load_rows(0);
@@ -693,18 +722,19 @@ sample_kernel(SweepArgs A) {
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
+                const float4 n4 = Row<NT>::cvt(v[q]);
                 if constexpr (kBlockAlpha) {
                     // no per-topic alpha term: 4 FFMA per block, no shared-memory load
-                    float x = __fmaf_rn(v[q].x, F[4 * q + 0], aSF[q]);
-                    x = __fmaf_rn(v[q].y, F[4 * q + 1], x);
-                    x = __fmaf_rn(v[q].z, F[4 * q + 2], x);
-                    sb[q] = __fmaf_rn(v[q].w, F[4 * q + 3], x);
+                    float x = __fmaf_rn(n4.x, F[4 * q + 0], aSF[q]);
+                    x = __fmaf_rn(n4.y, F[4 * q + 1], x);
+                    x = __fmaf_rn(n4.z, F[4 * q + 2], x);
+                    sb[q] = __fmaf_rn(n4.w, F[4 * q + 3], x);
                 } else {
                     const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
-                    const float w0 = __fmaf_rn(v[q].x, F[4 * q + 0], af.x);
-                    const float w1 = __fmaf_rn(v[q].y, F[4 * q + 1], af.y);
-                    const float w2 = __fmaf_rn(v[q].z, F[4 * q + 2], af.z);
-                    const float w3 = __fmaf_rn(v[q].w, F[4 * q + 3], af.w);
+                    const float w0 = __fmaf_rn(n4.x, F[4 * q + 0], af.x);
+                    const float w1 = __fmaf_rn(n4.y, F[4 * q + 1], af.y);
+                    const float w2 = __fmaf_rn(n4.z, F[4 * q + 2], af.z);
+                    const float w3 = __fmaf_rn(n4.w, F[4 * q + 3], af.w);
                     sb[q] = (w0 + w1) + (w2 + w3);
                 }
             }
