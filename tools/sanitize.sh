@@ -28,3 +28,6 @@ run C1_K10_seq X=1 -- --config C1 --waves 0
 run C1_K10_sparseP X=1 -- --config C1 --transform mix
 run C1_K100_chunk64 SPDP_CHUNK_TOKENS=64 -- --config C1 --topics 100
 run C2_K50 X=1 -- --config C2
+run C1_K200_row8_scatter SPDP_ROW_BYTES=1 SPDP_PREFETCH_ROWS=1 SPDP_DOC_SCATTER=1 -- --config C1 --topics 200
+run C1_K200_sprows SPDP_SPARSE_ROWS=1 -- --config C1 --topics 200
+run C1_K100_chunkft SPDP_CHUNK_FACTORS=1 -- --config C1 --topics 100
