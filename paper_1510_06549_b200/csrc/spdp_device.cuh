@@ -40,6 +40,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_NARROW_FULL
 #define SPDP_NARROW_FULL 1         // uint8/uint16 rows at 8x32: block alpha sums and row pipelining as at 4 blocks/SM
 #endif
+#ifndef SPDP_NARROW_PRETAB
+#define SPDP_NARROW_PRETAB 0       // ... and the own-removal inputs before the Philox rounds (opt-in)
+#endif
 #ifndef SPDP_BULK_PREFETCH
 #define SPDP_BULK_PREFETCH 0       // 1: exact-byte cp.async.bulk.prefetch.L2 of the next batch instead of this batch's
                                    // 128-B lines (B200, C5: 37.4 vs 34.7 ms per sweep with uint8 rows: fewer bytes, but
@@ -509,7 +512,7 @@ sample_kernel(SweepArgs A) {
     // 8x32 register cap (C5 +30 %), so not there
     constexpr bool kRowPipe = SPDP_ROW_PIPELINE != 0 && (sample_minb<LPT, KPL>() <= 4 || kNarrowFull);
     // own-removal inputs before the Philox rounds: C3 -1 %, K = 300 -1.8 %, C5 (8x32) +1 % (B200)
-    constexpr bool kPreTab = SPDP_PRE_TAB != 0 && sample_minb<LPT, KPL>() <= 4;
+    constexpr bool kPreTab = SPDP_PRE_TAB != 0 && (sample_minb<LPT, KPL>() <= 4 || (kNarrowFull && SPDP_NARROW_PRETAB));
     // r = 1 shares from the prologue in shared memory (not in the async mode: its copy is per chunk too,
     // but the live sums it reads in phase 3 are fresher); KSPAN <= 256 (smem budget of 16x32 / 32x32)
     constexpr bool kSmemR1 = SPDP_SMEM_R1 != 0 && KSPAN <= 256 && !ASYNC;
