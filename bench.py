@@ -386,13 +386,16 @@ def main():
             dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local_rank))
     corpus = synth.corpus_for(cfg)
     N = corpus.num_tokens
-    uid = None
-    if world > 1:
+    def new_uid():   # one fresh NCCL unique id per communicator (an id bootstraps exactly one ncclCommInitRank)
+        if world == 1:
+            return None
         t = torch.zeros(128, dtype=torch.uint8)
         if rank == 0:
             t = torch.tensor(list(spdp.spdp_nccl_unique_id()), dtype=torch.uint8)
         dist.broadcast(t, 0)
-        uid = bytes(t.tolist())
+        return bytes(t.tolist())
+
+    uid = new_uid()
     stream = torch.cuda.current_stream()
     kw = dict(alpha=cfg.alpha, beta=cfg.beta, discount=cfg.discount, concentration=cfg.concentration,
               seed=cfg.seed, num_waves=args.waves, device=local_rank, rank=rank, world_size=world,
@@ -491,6 +494,7 @@ def main():
     zr = [torch.empty(N, dtype=torch.uint8, pin_memory=True).numpy() if narrow else
           torch.empty(N, dtype=torch.int16, pin_memory=True).numpy().view(np.uint16) for _ in range(2)]
     t_pin = time.perf_counter() - t_pin
+    kw["nccl_unique_id"] = new_uid()                            # (a collective: outside the clock)
     t0 = time.perf_counter()
     h = spdp.Sampler(cfg.groups, cfg.vocab, K, **kw)
     t_create = time.perf_counter() - t0
