@@ -188,6 +188,8 @@ struct spdp_ctx {
     uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
     cudaStream_t d2h_stream = nullptr;            // spdp_zr_async's copies (overlap the next sweep)
     uint8_t* d_zr8_canon = nullptr;               // spdp_zr8_async's staging buffer (z | r << 7)
+    cudaStream_t side_stream = nullptr;           // W = 1: the recount beside the merge
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t zr_ready = nullptr, zr_copied = nullptr;
     bool zr_pending = false;                      // a queued copy may still read d_zr_canon
     uint16_t* h_zr_canon = nullptr;               // pinned host copy
@@ -1037,13 +1039,22 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
             else launch_sample(c, a, false);
         }
         rec(c, 4 * (size_t)w + 1);
+        // W = 1: the doc-topic recount (n from zr_next) and the segment merge (m, t, Q, sums from the deltas)
+        // touch disjoint data, so outside profiling the recount runs on a side stream beside the merge
+        // (a fork/join the CUDA graph capture records as parallel branches)
+        const bool side = c->W == 1 && !c->profiling && c->side_stream;
+        if (side) {
+            CU(cudaEventRecord(c->ev_fork, c->stream));
+            CU(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+        }
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
+            cudaStream_t rs = side ? c->side_stream : c->stream;
             const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
-            SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
+            SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, rs>>>(
                                        c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n,
                                        c->doc_scatter ? c->d_zr_doc : nullptr));
-            rebuild_entries(c, c->stream);
+            rebuild_entries(c, rs);
             std::swap(c->d_zr, c->d_zr_next);
         } else {
             const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
@@ -1061,6 +1072,10 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
                 c->d_wave_segs + sb, (int)(se - sb), c->d_m, c->d_t, c->d_dm, c->d_dt, Dnet, (int)c->pack32, c->d_Q, c->d_M,
                 c->d_Tt, c->d_T, c->I, c->Kp, use_smem, c->d_stats, (int)(c->token_kernel || c->pack_dmt),
                 (int)c->fold_merge);
+        }
+        if (side) {
+            CU(cudaEventRecord(c->ev_join, c->side_stream));
+            CU(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
         }
         rec(c, 4 * (size_t)w + 3);
         c->launches += 3;
@@ -1216,6 +1231,14 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
         c->own_stream = true;
     }
     set_attrs(c);
+    if (!(getenv("SPDP_SIDE_STREAM") && atoi(getenv("SPDP_SIDE_STREAM")) == 0) &&
+        (cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+        fail(c, SPDP_ECUDA, "side stream / events");
+        *out = c;
+        return SPDP_ECUDA;
+    }
     if (c->G > 1 && cfg->exchange == SPDP_EXCHANGE_NCCL) {
         if (!cfg->nccl_unique_id) return bad("nccl_unique_id is required for SPDP_EXCHANGE_NCCL with world_size > 1");
         c->nccl.lib = open_nccl();
@@ -2604,6 +2627,9 @@ void spdp_destroy(spdp_ctx* c) {
     if (c->comm_stream) { cudaStreamSynchronize(c->comm_stream); cudaStreamDestroy(c->comm_stream); }
     for (cudaEvent_t e : c->part_ev) cudaEventDestroy(e);
     if (c->comm_done) cudaEventDestroy(c->comm_done);
+    if (c->side_stream) { cudaStreamSynchronize(c->side_stream); cudaStreamDestroy(c->side_stream); }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
