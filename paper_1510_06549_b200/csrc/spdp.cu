@@ -392,7 +392,8 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     t.I = c->I; t.K = c->K; t.Kp = c->Kp;
     t.key0 = (uint32_t)c->cfg.seed; t.key1 = (uint32_t)(c->cfg.seed >> 32);
     t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats;
-    const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
+    // two full waves of the resident blocks (grid-stride loop)
+    const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 2u * SPDP_TOKEN_MINB);
     const int nbk = (c->K + 3) / 4;
     const size_t tsm = nbk > 16 ? sizeof(float) * 256 * 32 : 0;
 #define SPDP_TOK(NBK)                                                                                   \
