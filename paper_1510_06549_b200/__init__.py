@@ -44,8 +44,10 @@ EXPORTS = ["spdp_create", "spdp_load_corpus", "spdp_set_state", "spdp_sweep", "s
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libspdp.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
-    stale = force or not os.path.exists(LIB_PATH) or any(
-        os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in _SOURCES)
+    # a variant library named by SPDP_LIB (tuning A/B) is used as built, never recompiled from the tree
+    variant = bool(os.environ.get("SPDP_LIB")) and os.path.exists(LIB_PATH)
+    stale = force or not os.path.exists(LIB_PATH) or (not variant and any(
+        os.path.getmtime(s) > os.path.getmtime(LIB_PATH) for s in _SOURCES))
     if stale:
         cmd = ["nvcc", *NVCC_FLAGS, os.path.join(_HERE, "csrc", "spdp.cu"), "-o", LIB_PATH, "-ldl", "-lpthread"]
         if verbose:

@@ -183,7 +183,7 @@ struct spdp_ctx {
     int16_t* d_src = nullptr;
     int* d_sigma = nullptr;                       // [Kp] in-row position of topic k
     std::vector<int> sigma;
-    int colstart[8] = {0};
+    int LA = 1, Kn = 4;                           // doc-topic rows: lanes with storage, row length (spdp_device.cuh)
     int prefetch_rows = 0;
     uint16_t* d_zr_canon = nullptr;               // spdp_counts staging (canonical order)
     cudaStream_t d2h_stream = nullptr;            // spdp_zr_async's copies (overlap the next sweep)
@@ -208,6 +208,10 @@ struct spdp_ctx {
     size_t partial_len = 0;
     uint32_t sweeps_done = 0;
     std::vector<void*> allocs;
+    // the setup calls' temporaries come from this pool, which keeps freed memory mapped (release threshold
+    // = max): the planning code synchronises after every CUB call, and the default pool would unmap and
+    // remap the freed temporaries at each of those points
+    cudaMemPool_t pool = nullptr;
     // profiling (spdp_profile)
     bool profiling = false;
     // one sweep captured as a CUDA graph and replayed (single rank): keyed by the zr buffer the sweep
@@ -382,14 +386,11 @@ void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t t
     t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
     t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.F = c->d_F; t.R1 = c->d_R1; t.n = c->d_n;
     t.sigma = c->d_sigma;
-    for (int B = 0; B < 32; ++B) {
-        const int nbl = c->KPL / 4;
-        t.bpos[B] = (B < c->Kp / 4) ? c->colstart[B % nbl] + B / nbl : 0;
-    }
+    for (int B = 0; B < 32; ++B) t.bpos[B] = (B < c->Kp / 4) ? c->sigma[(size_t)4 * B] / 4 : 0;
     t.m = c->d_m; t.t = c->d_t; t.Q = c->d_Q; t.M = c->d_M; t.Tt = c->d_Tt; t.T = c->d_T; t.dmt = c->d_dm;
     t.alpha = c->d_alpha; t.disc = c->d_disc; t.conc = c->d_conc; t.tab = c->d_tab; t.tab_off = c->d_tab_off;
     t.beta = (float)c->cfg.beta; t.vbeta = (float)((double)c->V * c->cfg.beta);
-    t.I = c->I; t.K = c->K; t.Kp = c->Kp;
+    t.I = c->I; t.K = c->K; t.Kp = c->Kp; t.Kn = c->Kn;
     t.key0 = (uint32_t)c->cfg.seed; t.key1 = (uint32_t)(c->cfg.seed >> 32);
     t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats;
     // two full waves of the resident blocks (grid-stride loop)
@@ -426,7 +427,7 @@ SweepArgs base_args(spdp_ctx* c) {
     a.tok_doc = c->d_tok_doc; a.tok_id = c->d_tok_id; a.zr = c->d_zr; a.zr_next = c->d_zr_next;
     a.chunk_start = c->d_chunk_start; a.chunk_end = c->d_chunk_end; a.chunk_seg = c->d_chunk_seg; a.nchunks = 0;
     a.n = c->d_n; a.sigma = c->d_sigma;
-    for (int q = 0; q < 8; ++q) a.colstart[q] = c->colstart[q];
+    a.LA = c->LA; a.Kn = c->Kn;
     a.prefetch_rows = c->prefetch_rows;
     a.m = c->d_m; a.t = c->d_t; a.Q = c->d_Q; a.M = c->d_M; a.Tt = c->d_Tt; a.T = c->d_T;
     a.dm = c->d_dm; a.dt = c->d_dt;
@@ -491,7 +492,7 @@ void launch_sprows(spdp_ctx* c, const SweepArgs& a) {
 void rebuild_entries(spdp_ctx* c, cudaStream_t st) {
     if (!c->sprows || c->Dloc == 0) return;
     SPDP_ROWS(c->row_elem, rows_to_entries_kernel<NT><<<148 * 8, 256, 0, st>>>(
-                               (const NT*)c->d_n, c->d_sigma, c->Dloc, c->K, c->Kp, c->d_cap_ptr, c->d_ent, c->d_dinfo));
+                               (const NT*)c->d_n, c->d_sigma, c->Dloc, c->K, c->Kn, c->d_cap_ptr, c->d_ent, c->d_dinfo));
     c->launches += 1;
 }
 
@@ -501,10 +502,15 @@ int merge_grid() { return 148 * 4; }
 // on the call's stream) inside a TempStream scope, so freeing one does not
 // synchronise the device; plain cudaMalloc elsewhere.
 thread_local cudaStream_t tl_temp_stream = nullptr;
+thread_local cudaMemPool_t tl_temp_pool = nullptr;
 struct TempStream {
     cudaStream_t prev;
-    explicit TempStream(cudaStream_t s) : prev(tl_temp_stream) { tl_temp_stream = s; }
-    ~TempStream() { tl_temp_stream = prev; }
+    cudaMemPool_t prev_pool;
+    explicit TempStream(cudaStream_t s, cudaMemPool_t pool = nullptr) : prev(tl_temp_stream), prev_pool(tl_temp_pool) {
+        tl_temp_stream = s;
+        tl_temp_pool = pool;
+    }
+    ~TempStream() { tl_temp_stream = prev; tl_temp_pool = prev_pool; }
 };
 
 template <typename T>
@@ -513,7 +519,8 @@ struct TempBuf {
     cudaStream_t st = nullptr;
     explicit TempBuf(size_t n) : st(tl_temp_stream) {
         const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
-        const cudaError_t e = st ? cudaMallocAsync((void**)&p, bytes, st) : cudaMalloc((void**)&p, bytes);
+        const cudaError_t e = (st && tl_temp_pool) ? cudaMallocFromPoolAsync((void**)&p, bytes, tl_temp_pool, st)
+                              : st ? cudaMallocAsync((void**)&p, bytes, st) : cudaMalloc((void**)&p, bytes);
         if (e != cudaSuccess) { p = nullptr; cudaGetLastError(); }
     }
     ~TempBuf() { if (p) { if (st) cudaFreeAsync(p, st); else cudaFree(p); } }
@@ -561,9 +568,11 @@ void launch_exchange_merge(spdp_ctx* c) {
 // SPDP_VERBOSE=1: phase times of spdp_load_corpus on stderr
 struct LoadTimer {
     bool on = getenv("SPDP_VERBOSE") != nullptr;
+    bool drain = on && atoi(getenv("SPDP_VERBOSE")) >= 2;   // SPDP_VERBOSE=2: wait for the device at each mark
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     void mark(const char* what) {
         if (!on) return;
+        if (drain) cudaDeviceSynchronize();
         auto t1 = std::chrono::steady_clock::now();
         fprintf(stderr, "[spdp] load %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
         t0 = t1;
@@ -616,12 +625,12 @@ void partition_docs(uint64_t seed, int G, int64_t N, int32_t D, const std::vecto
 
 // Upload (z, r or tables) as the sampler state: counts from z.
 size_t row_bytes(const spdp_ctx* c) {
-    return ((size_t)c->Dloc * c->Kp + 1024) * (size_t)c->row_elem;
+    return ((size_t)c->Dloc * c->Kn + 1024) * (size_t)c->row_elem;
 }
 
-// doc-topic rows to the host as floats (sigma order, [Dloc][Kp])
+// doc-topic rows to the host as floats (sigma order, [Dloc][Kn])
 spdp_status read_rows(spdp_ctx* c, std::vector<float>& out) {
-    const size_t n = (size_t)c->Dloc * c->Kp;
+    const size_t n = (size_t)c->Dloc * c->Kn;
     out.assign(n, 0.f);
     if (c->row_elem == 2) {
         std::vector<uint16_t> tmp(n);
@@ -730,7 +739,7 @@ spdp_status install_state(spdp_ctx* c, const int32_t* z_in, const uint8_t* r_in,
     CU(cudaMemsetAsync(c->d_n, 0, row_bytes(c), c->stream));
     if (c->Nloc > 0) {
         SPDP_ROWS(c->row_elem, init_local_kernel<NT><<<grid, 256, 0, c->stream>>>(
-                                   c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc, Kp, c->d_sigma, c->d_zr,
+                                   c->d_tok_id, c->d_tok_doc, dz.p, dr.p, (uint32_t)c->Nloc, c->Kn, c->d_sigma, c->d_zr,
                                    c->d_zr_next, (NT*)c->d_n));
     }
     CU(cudaMemsetAsync(c->d_dm, 0, sizeof(int32_t) * c->cells, c->stream));
@@ -857,25 +866,24 @@ void sparse_wave(spdp_ctx* c, int w) {
     t.tok_doc = c->d_tok_doc; t.tok_id = c->d_tok_id; t.tok_run = c->d_tok_run; t.run_seg = c->d_wave_segs;
     t.zr = c->d_zr; t.zr_next = c->d_zr_next; t.src = c->d_src; t.F = c->d_F; t.R1 = c->d_R1; t.n = c->d_n;
     t.sigma = c->d_sigma;
-    const int nbl = c->KPL / 4;
-    for (int B = 0; B < 256; ++B) t.bpos[B] = (B < Kp / 4) ? c->colstart[B % nbl] + B / nbl : 0;
+    for (int B = 0; B < 256; ++B) t.bpos[B] = (B < Kp / 4) ? c->sigma[(size_t)4 * B] / 4 : 0;
     t.m = c->d_m; t.t = c->d_t; t.Q = c->d_Q; t.M = c->d_M; t.Tt = c->d_Tt; t.T = c->d_T; t.dm = c->d_dm;
     t.alpha = c->d_alpha; t.disc = c->d_disc; t.conc = c->d_conc; t.tab = c->d_tab; t.tab_off = c->d_tab_off;
-    t.beta = beta; t.vbeta = vbeta; t.I = c->I; t.K = c->K; t.Kp = Kp;
+    t.beta = beta; t.vbeta = vbeta; t.I = c->I; t.K = c->K; t.Kp = Kp; t.Kn = c->Kn;
     t.key0 = (uint32_t)c->cfg.seed; t.key1 = (uint32_t)(c->cfg.seed >> 32);
     t.sweep = c->d_sweep; t.begin = tb; t.end = te; t.stats = c->d_stats; t.P = P;
     const int grid = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 8u);
     const size_t ssm = ((Kp / 4) <= kSpSmemBlocks) ? sizeof(float) * 256 * (size_t)(Kp / 4) : 0;
     SPDP_ROWS(c->row_elem, sp_token_kernel<NT><<<std::max(grid, 1), 256, ssm, c->stream>>>(t));
     if (c->W == 1) {
-        const size_t smem = sizeof(int) * 8 * (size_t)Kp;
+        const size_t smem = sizeof(int) * 8 * (size_t)c->Kn;
         SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
-                                   c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, Kp, (NT*)c->d_n, nullptr));
+                                   c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n, nullptr));
         std::swap(c->d_zr, c->d_zr_next);
     } else {
         const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
         SPDP_ROWS(c->row_elem, apply_tokens_kernel<NT><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
-                                   c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, Kp, tb, te));
+                                   c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, c->Kn, tb, te));
     }
     const int blocks = (int)std::min<uint32_t>((r1 - r0 + 7) / 8, 148u * 4u);
     int32_t* Dm = c->G > 1 ? (int32_t*)c->d_Dloc : nullptr;
@@ -951,9 +959,9 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
         }
     }
     rec(c, 1);
-    const size_t rsm = sizeof(int) * 8 * (size_t)c->Kp;      // every token moved to zr_next: rebuild n, swap
+    const size_t rsm = sizeof(int) * 8 * (size_t)c->Kn;      // every token moved to zr_next: rebuild n, swap
     SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
-                                                                            c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n,
+                                                                            c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n,
                                                                             c->doc_scatter ? c->d_zr_doc : nullptr));
     rebuild_entries(c, st);
     std::swap(c->d_zr, c->d_zr_next);
@@ -1051,16 +1059,16 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             cudaStream_t rs = side ? c->side_stream : c->stream;
-            const size_t smem = sizeof(int) * 8 * (size_t)c->Kp;
+            const size_t smem = sizeof(int) * 8 * (size_t)c->Kn;
             SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, rs>>>(
-                                       c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kp, (NT*)c->d_n,
+                                       c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n,
                                        c->doc_scatter ? c->d_zr_doc : nullptr));
             rebuild_entries(c, rs);
             std::swap(c->d_zr, c->d_zr_next);
         } else {
             const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
             SPDP_ROWS(c->row_elem, apply_tokens_kernel<NT><<<std::max(tblocks, 1), 256, 0, c->stream>>>(
-                                       c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, c->Kp, tb, te));
+                                       c->d_tok_doc, c->d_zr, c->d_zr_next, (NT*)c->d_n, c->d_sigma, c->Kn, tb, te));
             rebuild_entries(c, c->stream);                 // the next wave reads the updated rows
         }
         rec(c, 4 * (size_t)w + 2);
@@ -1203,6 +1211,10 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
         }
     }
     if (c->LPT * c->KPL < c->K) return bad("internal: no kernel configuration for K");
+    // doc-topic row layout (sigma order, see spdp_device.cuh): LA lanes of a group hold topics, rows of
+    // Kn = LA * KPL elements (the unit positions are set at load, once the row element type is known)
+    c->LA = (c->K + c->KPL - 1) / c->KPL;
+    c->Kn = c->LA * c->KPL;
     // tokens per chunk: 512 vs 256 measured -0.5..-1.2 % at C3, C4 K = 100/300, C5 (B200); the async
     // mode keeps 256 (its tokens share the chunk-start copy of the segment's counts, reading c23)
     int chunk = c->async ? 256 : 512;
@@ -1232,6 +1244,19 @@ spdp_status spdp_create(const spdp_config* cfg, spdp_ctx** out) {
         c->own_stream = true;
     }
     set_attrs(c);
+    if (!(getenv("SPDP_TEMP_POOL") && atoi(getenv("SPDP_TEMP_POOL")) == 0)) {
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = cfg->device;
+        if (cudaMemPoolCreate(&c->pool, &pp) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            c->pool = nullptr;
+            cudaGetLastError();
+        }
+    }
     if (!(getenv("SPDP_SIDE_STREAM") && atoi(getenv("SPDP_SIDE_STREAM")) == 0) &&
         (cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -1282,7 +1307,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         return fail(c, SPDP_EINVAL, "need num_tokens >= 1, num_docs >= 1 and the three token arrays");
     if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
     const int I = c->I, V = c->V, Kp = c->Kp, W = c->W;
-    TempStream temp_scope(c->stream);
+    TempStream temp_scope(c->stream, c->pool);
     c->N = num_tokens; c->D = num_docs;
     // the token triples stay on the device (state installation); host copies only on demand (diagnostics)
     c->group.clear(); c->doc.clear(); c->word.clear();
@@ -1292,9 +1317,10 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     auto bits = [](uint64_t x) { int b = 1; while (b < 64 && (x >> b)) ++b; return b; };
     ALLOC(c->d_group, n); ALLOC(c->d_doc, n); ALLOC(c->d_word, n);
     struct { int32_t* p; } dgrp{c->d_group}, ddoc{c->d_doc}, dwrd{c->d_word};
-    TempBuf<int32_t> dpos(n), ddg((size_t)num_docs), ddl((size_t)num_docs);
-    TempBuf<uint32_t> diota(n), dbydoc(n), dstart((size_t)num_docs);
-    TempBuf<int32_t> dkeyd(n);
+    const size_t npos = W > 1 ? (size_t)n : 1;      // in-document positions: only with several waves
+    TempBuf<int32_t> dpos(npos), ddg((size_t)num_docs), ddl((size_t)num_docs);
+    TempBuf<uint32_t> diota(n), dbydoc(npos), dstart(W > 1 ? (size_t)num_docs : 1);
+    TempBuf<int32_t> dkeyd(npos);
     TempBuf<unsigned long long> derr(2);
     if (!dpos.p || !ddg.p || !ddl.p || !diota.p || !dbydoc.p || !dstart.p ||
         !dkeyd.p || !derr.p)
@@ -1313,6 +1339,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     CU(cudaMemcpyAsync(c->doclen.data(), ddl.p, sizeof(int32_t) * (size_t)num_docs, cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(c->docgroup.data(), ddg.p, sizeof(int32_t) * (size_t)num_docs, cudaMemcpyDeviceToHost, st));
     if ((s = sync(c, "validate tokens"))) return s;
+    lt.mark("upload + validate");
     if (herr[0] != ~0ull) {
         const size_t q = (size_t)herr[0];
         return fail(c, SPDP_EINVAL, "token %lld = (%d, %d, %d) out of range", (long long)q, group[q], doc[q], word[q]);
@@ -1335,16 +1362,19 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         return SPDP_OK;
     };
     iota_kernel<<<grid, 256, 0, st>>>(diota.p, n);
-    if ((s = cub_run([&](void* t, size_t& b) {
-             return cub::DeviceRadixSort::SortPairs(t, b, ddoc.p, dkeyd.p, diota.p, dbydoc.p, (int)n, 0, bits((uint64_t)num_docs), st);
-         }, "sort by document")))
-        return s;
-    if ((s = cub_run([&](void* t, size_t& b) {
-             return cub::DeviceScan::ExclusiveSum(t, b, reinterpret_cast<const uint32_t*>(ddl.p), dstart.p, num_docs, st);
-         }, "document offsets")))
-        return s;
-    positions_kernel<<<grid, 256, 0, st>>>(dbydoc.p, ddoc.p, dstart.p, n, dpos.p);
-    lt.mark("validate + positions");
+    if (W > 1) {   // in-document positions decide the waves (pos mod W); W = 1 needs none
+        if ((s = cub_run([&](void* t, size_t& b) {
+                 return cub::DeviceRadixSort::SortPairs(t, b, ddoc.p, dkeyd.p, diota.p, dbydoc.p, (int)n, 0,
+                                                        bits((uint64_t)num_docs), st);
+             }, "sort by document")))
+            return s;
+        if ((s = cub_run([&](void* t, size_t& b) {
+                 return cub::DeviceScan::ExclusiveSum(t, b, reinterpret_cast<const uint32_t*>(ddl.p), dstart.p, num_docs, st);
+             }, "document offsets")))
+            return s;
+        positions_kernel<<<grid, 256, 0, st>>>(dbydoc.p, ddoc.p, dstart.p, n, dpos.p);
+    }
+    lt.mark("positions");
     // M_max = largest count(i, w): bounds every m_{ikw} the chain can reach
     {
         TempBuf<int32_t> dcnt((size_t)I * V), dmx(1);
@@ -1411,10 +1441,41 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             c->global_of_local.push_back(d);
         }
     c->Dloc = (int32_t)c->global_of_local.size();
-    // the kernels address a doc-topic row by a 32-bit element offset (doc * Kp)
-    if ((uint64_t)c->Dloc * (uint64_t)Kp >= (1ull << 32) - 4096)
+    // the kernels address a doc-topic row by a 32-bit element offset (doc * Kn)
+    if ((uint64_t)c->Dloc * (uint64_t)c->Kn >= (1ull << 32) - 4096)
         return fail(c, SPDP_EINVAL, "%d local documents x %d topic slots exceed 2^32 doc-topic cells per rank: "
-                    "use more ranks", c->Dloc, Kp);
+                    "use more ranks", c->Dloc, c->Kn);
+    // Stirling-ratio tables, one per distinct discount (M_max rows): a sequential row recursion on one SM,
+    // built on the side stream while the wave plan sorts run on the main stream (joined after the uploads)
+    cudaStream_t tab_stream = c->side_stream ? c->side_stream : c->stream;
+    struct EventGuard {
+        cudaEvent_t e = nullptr;
+        ~EventGuard() { if (e) cudaEventDestroy(e); }
+    } tab_done;
+    {
+        CU(cudaEventCreateWithFlags(&tab_done.e, cudaEventDisableTiming));
+        std::vector<double> distinct;
+        std::vector<int> which((size_t)I);
+        for (int i = 0; i < I; ++i) {
+            size_t j = 0;
+            while (j < distinct.size() && distinct[j] != c->disc[(size_t)i]) ++j;
+            if (j == distinct.size()) distinct.push_back(c->disc[(size_t)i]);
+            which[(size_t)i] = (int)j;
+        }
+        const uint64_t per = (uint64_t)(c->mmax + 1) * (uint64_t)(c->mmax + 2) / 2;
+        ALLOC(c->d_tab, per * distinct.size());
+        ALLOC(c->d_tab_off, I);
+        c->tab_off_host.resize((size_t)I);
+        for (int i = 0; i < I; ++i) c->tab_off_host[(size_t)i] = per * (uint64_t)which[(size_t)i];
+        CU(cudaMemcpyAsync(c->d_tab_off, c->tab_off_host.data(), sizeof(uint64_t) * I, cudaMemcpyHostToDevice, tab_stream));
+        double* scratch = nullptr;
+        ALLOC(scratch, 2 * (size_t)(c->mmax + 2) * distinct.size());
+        for (size_t j = 0; j < distinct.size(); ++j)
+            build_ratio_table<<<1, 1024, 0, tab_stream>>>(c->d_tab + per * j, scratch + 2 * (size_t)(c->mmax + 2) * j,
+                                                          c->mmax, distinct[j]);
+        s = check_launch(c, "build_ratio_table");
+        if (s) return s;
+    }
     lt.mark("M_max + partition");
     // this rank's tokens, canonical order
     TempBuf<uint32_t> dlocal(n);
@@ -1568,18 +1629,15 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         ALLOC(c->d_tok_doc, nl);
         ALLOC(c->d_doc_pos, nl);
         ALLOC(c->d_doc_ptr, (size_t)c->Dloc + 1);
-        TempBuf<uint32_t> dq(nl), dk2(nl);
-        if (!dq.p || !dk2.p) return fail(c, SPDP_ENOMEM, "CSR buffers");
+        TempBuf<uint32_t> dq(nl), dcur((size_t)std::max(c->Dloc, 1));
+        if (!dq.p || !dcur.p) return fail(c, SPDP_ENOMEM, "CSR buffers");
         tdoc_kernel<<<grid, 256, 0, st>>>(c->d_tok_id, nloc, ddoc.p, c->G > 1 ? dlod.p : nullptr, c->d_tok_doc, dq.p);
-        if (nloc > 0 && (s = cub_run([&](void* t, size_t& b) {
-                             return cub::DeviceRadixSort::SortPairs(t, b, c->d_tok_doc, dk2.p, dq.p, c->d_doc_pos, (int)nloc,
-                                                                    0, bits((uint64_t)std::max(c->Dloc, 1)), st);
-                         }, "CSR")))
-            return s;
         std::vector<uint32_t> dptr((size_t)c->Dloc + 1, 0);
         for (int32_t j = 0; j < c->Dloc; ++j)
             dptr[(size_t)j + 1] = dptr[(size_t)j] + (uint32_t)c->doclen[(size_t)c->global_of_local[(size_t)j]];
         CU(cudaMemcpyAsync(c->d_doc_ptr, dptr.data(), sizeof(uint32_t) * dptr.size(), cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(dcur.p, 0, sizeof(uint32_t) * (size_t)std::max(c->Dloc, 1), st));
+        if (nloc > 0) csr_scatter_kernel<<<grid, 256, 0, st>>>(c->d_tok_doc, nloc, c->d_doc_ptr, dcur.p, c->d_doc_pos);
         // W = 1 with the chunk kernel: it also writes each new assignment to its document-order slot (a
         // fire-and-forget scattered store), so the recount streams them instead of gathering through doc_pos
         // (B200: C5 recount 3.89 -> 0.76 ms, sample +2.25 ms, step -0.86 ms; C3, whose rows and zr live in L2,
@@ -1587,7 +1645,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         int l2b = 0, dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2b, cudaDevAttrL2CacheSize, dev);
-        const bool hbm_rows = (double)c->Dloc * Kp * sizeof(float) > 0.5 * (double)l2b;
+        const bool hbm_rows = (double)c->Dloc * c->Kn * sizeof(float) > 0.5 * (double)l2b;
         // (K > 256: the 16x32 / 32x32 kernels do not carry the store; C4 K = 1000 measured 5.31 vs 5.24 ms anyway)
         c->doc_scatter = W == 1 && !c->token_kernel && !c->async && !c->sparse && !c->seq && !c->sprows && hbm_rows &&
                          c->K <= 256;
@@ -1605,23 +1663,6 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     c->pos_of_tok.clear();
     lt.mark("wave plan + chunks (device)");
     c->cells = (size_t)V * I * Kp;
-    // doc-topic row layout (sigma order, see spdp_device.cuh): lane gl owns canonical
-    // blocks [gl*NB, gl*NB + NB); block q of each lane is stored column-major over lanes
-    {
-        const int NBLK = Kp / 4, NB = c->KPL / 4;
-        int run = 0;
-        for (int q = 0; q < 8; ++q) {
-            c->colstart[q] = run;
-            if (q < NB)
-                for (int gl = 0; gl < c->LPT; ++gl) run += (gl * NB + q < NBLK) ? 1 : 0;
-        }
-        c->sigma.assign((size_t)Kp, 0);
-        for (int k = 0; k < Kp; ++k) {
-            const int B = k / 4, gl = B / NB, q = B % NB;
-            c->sigma[(size_t)k] = 4 * (c->colstart[q] + gl) + (k & 3);
-        }
-    }
-
     // device allocations
     ALLOC(c->d_zr, std::max<int64_t>(c->Nloc, 1)); ALLOC(c->d_zr_next, std::max<int64_t>(c->Nloc, 1));
     ALLOC(c->d_sweep, 1);
@@ -1629,7 +1670,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         int dev = 0, l2 = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        c->prefetch_rows = ((double)c->Dloc * Kp * sizeof(float) > 0.5 * (double)l2) ? 1 : 0;
+        c->prefetch_rows = ((double)c->Dloc * c->Kn * sizeof(float) > 0.5 * (double)l2) ? 1 : 0;
         if (const char* e = getenv("SPDP_PREFETCH_ROWS")) c->prefetch_rows = atoi(e);
         // HBM-resident rows: the narrowest exact count type (n_dk <= L_d): uint8 when every document has
         // < 256 tokens, else uint16 (< 2^16); fp32 rows (no conversion) when the array lives in L2.
@@ -1682,6 +1723,14 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
 #define CALL_SS(L, KS) sprows_setup_t<L, KS>(c)
             SPDP_SPROWS_DISPATCH(c->sp_lpt, c->sp_kspan, CALL_SS)
 #undef CALL_SS
+        }
+    }
+    {   // unit j of lane gl at unit index j * LA + gl; UT topics (16 bytes, or the lane's span) per unit
+        const int UT = std::min(16 / c->row_elem, c->KPL);
+        c->sigma.assign((size_t)Kp, 0);
+        for (int k = 0; k < Kp; ++k) {
+            const int gl = k / c->KPL, kk = k % c->KPL;
+            c->sigma[(size_t)k] = ((kk / UT) * c->LA + gl) * UT + kk % UT;
         }
     }
     ALLOC(c->d_sigma, Kp);
@@ -1763,31 +1812,13 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     // order after the legacy stream, so settle every upload before the stream reads them
     CU(cudaDeviceSynchronize());
     lt.mark("device alloc + upload");
-    // Stirling-ratio tables, one per distinct discount (M_max rows)
-    {
-        std::vector<double> distinct;
-        std::vector<int> which((size_t)I);
-        for (int i = 0; i < I; ++i) {
-            size_t j = 0;
-            while (j < distinct.size() && distinct[j] != c->disc[(size_t)i]) ++j;
-            if (j == distinct.size()) distinct.push_back(c->disc[(size_t)i]);
-            which[(size_t)i] = (int)j;
-        }
-        const uint64_t per = (uint64_t)(c->mmax + 1) * (uint64_t)(c->mmax + 2) / 2;
-        ALLOC(c->d_tab, per * distinct.size());
-        ALLOC(c->d_tab_off, I);
-        c->tab_off_host.resize((size_t)I);
-        for (int i = 0; i < I; ++i) c->tab_off_host[(size_t)i] = per * (uint64_t)which[(size_t)i];
-        CU(cudaMemcpyAsync(c->d_tab_off, c->tab_off_host.data(), sizeof(uint64_t) * I, cudaMemcpyHostToDevice, c->stream));
-        double* scratch = nullptr;
-        ALLOC(scratch, 2 * (size_t)(c->mmax + 2));
-        for (size_t j = 0; j < distinct.size(); ++j)
-            build_ratio_table<<<1, 1024, 0, c->stream>>>(c->d_tab + per * j, scratch, c->mmax, distinct[j]);
-        s = check_launch(c, "build_ratio_table");
-        if (s) return s;
-        s = sync(c, "build_ratio_table");
-        if (s) return s;
+    // Stirling-ratio tables (launched on the side stream once M_max was known): join
+    if (tab_stream != c->stream) {
+        CU(cudaEventRecord(tab_done.e, tab_stream));
+        CU(cudaStreamWaitEvent(c->stream, tab_done.e, 0));
     }
+    s = sync(c, "build_ratio_table");
+    if (s) return s;
     lt.mark("Stirling-ratio tables");
     if (c->sparse && (s = sparse_upload(c))) return s;
     s = install_state(c, z_init, r_init, nullptr);
@@ -1808,7 +1839,7 @@ spdp_status spdp_set_state(spdp_ctx* c, const int32_t* z, const uint8_t* r, cons
     spdp_status s = guard(c, true);
     if (s) return s;
     if (!z || (!r && !tables)) return fail(c, SPDP_EINVAL, "spdp_set_state needs z and (r or tables)");
-    TempStream temp_scope(c->stream);
+    TempStream temp_scope(c->stream, c->pool);
     std::vector<uint8_t> ones;
     if (!r) { ones.assign((size_t)c->N, 1); r = ones.data(); }
     return install_state(c, z, r, tables);
@@ -2023,7 +2054,7 @@ spdp_status spdp_counts(spdp_ctx* c, int32_t* z, uint8_t* r, int32_t* doc_topic,
         int32_t* dst = gather ? full.data() : doc_topic;
         for (int32_t j = 0; j < c->Dloc; ++j)
             for (int k = 0; k < K; ++k)
-                dst[(size_t)c->global_of_local[(size_t)j] * K + k] = (int32_t)nf[(size_t)j * Kp + c->sigma[(size_t)k]];
+                dst[(size_t)c->global_of_local[(size_t)j] * K + k] = (int32_t)nf[(size_t)j * c->Kn + c->sigma[(size_t)k]];
         if (gather) {
             TempBuf<int32_t> tb(full.size());
             if (!tb.p) return fail(c, SPDP_ENOMEM, "gather buffer");
@@ -2265,7 +2296,7 @@ spdp_status spdp_loglik(spdp_ctx* c, double* log_joint, double* perplexity) {
                                                         c->cfg.beta, part);
         SPDP_ROWS(c->row_elem, loglik_docs_kernel<NT><<<grid, 256, 0, c->stream>>>((const NT*)c->d_n, c->d_sigma, c->d_doclen,
                                                                             c->d_docgroup, c->d_alpha64, c->d_alpha_sum64,
-                                                                            c->Dloc, c->K, c->Kp, part + grid));
+                                                                            c->Dloc, c->K, c->Kp, c->Kn, part + grid));
         loglik_small_kernel<<<1, 1024, 0, c->stream>>>(c->d_M, c->d_Tt, c->d_T, c->d_disc64, c->d_conc64, c->I, c->K, c->Kp,
                                                       (double)c->V * c->cfg.beta, part + 2 * grid);
         int nterms = 2 * grid + 1;
@@ -2341,7 +2372,7 @@ spdp_status spdp_heldout(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, cons
                          const int32_t* z_init, int32_t* z_out, double* theta, double* perplexity) {
     spdp_status s = guard(c, true);
     if (s) return s;
-    TempStream temp_scope(c->stream);
+    TempStream temp_scope(c->stream, c->pool);
     const int I = c->I, V = c->V, K = c->K, Kp = c->Kp;
     if (num_tokens < 0 || num_tokens > (int64_t)UINT32_MAX || num_docs < 1 || iterations < 0 || first_iteration < 0 ||
         (num_tokens > 0 && (!group || !doc || !word)))
@@ -2632,6 +2663,7 @@ void spdp_destroy(spdp_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (c->pool) cudaMemPoolDestroy(c->pool);
     delete c;
 }
 
@@ -2659,7 +2691,16 @@ spdp_status debug_verify(spdp_ctx* c) {
         if (s0) return s0;
     }
     for (int32_t j = 0; j < c->Dloc; ++j)
-        for (int k = 0; k < Kp; ++k) n[(size_t)j * Kp + k] = (int32_t)nf[(size_t)j * Kp + c->sigma[(size_t)k]];
+        for (int k = 0; k < Kp; ++k) n[(size_t)j * Kp + k] = (int32_t)nf[(size_t)j * c->Kn + c->sigma[(size_t)k]];
+    {   // positions of the rows that hold no topic (padding) must stay zero
+        std::vector<char> used((size_t)c->Kn, 0);
+        for (int k = 0; k < K; ++k) used[(size_t)c->sigma[(size_t)k]] = 1;
+        for (int32_t j = 0; j < c->Dloc; ++j)
+            for (int x = 0; x < c->Kn; ++x)
+                if (!used[(size_t)x] && nf[(size_t)j * c->Kn + x] != 0.f)
+                    return fail(c, SPDP_EINTEGRITY, "doc-topic row %d holds %g at padding position %d", (int)j,
+                                (double)nf[(size_t)j * c->Kn + x], x);
+    }
     CU(cudaMemcpy(m.data(), c->d_m, 4 * m.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(t.data(), c->d_t, 4 * t.size(), cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(Q.data(), c->d_Q, 4 * Q.size(), cudaMemcpyDeviceToHost));

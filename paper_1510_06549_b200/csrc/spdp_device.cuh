@@ -7,7 +7,7 @@
 //
 // Layout in HBM: every count row is padded to Kp = round_up(K, 4)
 // int32 so rows are 16-byte aligned for vector loads.
-//   n  [D_local][Kp]      doc-topic, this rank's documents
+//   n  [D_local][Kn]      doc-topic, this rank's documents (unit layout below, Kn = LA * KPL)
 //   m,t[V][I][Kp]          word-major: the rows of one (w, i) segment are adjacent
 //   Q  [V][Kp]             shadow counts, word-major
 //   M,Tt [I][Kp], T [Kp]   marginal sums
@@ -50,13 +50,6 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #endif
 #ifndef SPDP_PREFETCH_AHEAD
 #define SPDP_PREFETCH_AHEAD 1      // bulk prefetch: batches of 32 tokens ahead of the one being sampled
-#endif
-#ifndef SPDP_PAD_SELECT
-#define SPDP_PAD_SELECT 0          // 1: loads of 4-topic blocks past K read the row's first block (no bytes past the
-                                   // row); B200, C5: 37.4 vs 33.8 ms per sweep (the address selects cost more)
-#endif
-#ifndef SPDP_SKIP_PAD_BLOCKS
-#define SPDP_SKIP_PAD_BLOCKS 1     // sample kernel: no row loads for 4-topic blocks past K
 #endif
 #ifndef SPDP_MINB_8X32
 #define SPDP_MINB_8X32 5
@@ -364,6 +357,54 @@ struct Row<uint8_t> {
     __device__ __forceinline__ static int get(const uint8_t* p) { return (int)*p; }
 };
 
+// ---------------------------------------------------------------- row units (the sample kernel's dense pass)
+// A lane reads its topics as units of UB = min(16, KPL * sizeof(NT)) bytes: one 16-byte load holds 4 fp32,
+// 8 uint16 or 16 uint8 counts.  Unit j of lane gl sits at unit index j * LA + gl of the row (column-major
+// over the LA lanes that hold topics), so one load instruction of a lane group reads LA * UB consecutive
+// bytes, and unit j is a fixed stride j * LA * UB from the lane's first unit.
+template <int UB> struct UnitT;
+template <> struct UnitT<16> { using type = uint4; };
+template <> struct UnitT<8> { using type = uint2; };
+template <> struct UnitT<4> { using type = uint32_t; };
+template <typename NT, int KPL>
+struct RowUnit {
+    static constexpr int UT = (16 / (int)sizeof(NT)) < KPL ? 16 / (int)sizeof(NT) : KPL;   // topics per unit
+    static constexpr int UB = UT * (int)sizeof(NT);                                          // bytes per unit
+    static constexpr int NU = KPL / UT;                                                      // units per lane
+    static constexpr int QPU = UT / 4;                                                       // 4-topic blocks per unit
+    using type = typename UnitT<UB>::type;
+};
+__device__ __forceinline__ uint4 ld_unit_nc(const uint4* p) { return __ldg(p); }
+__device__ __forceinline__ uint2 ld_unit_nc(const uint2* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ld_unit_nc(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint4 ld_unit_live(const uint4* p) {
+    uint4 v;
+    if constexpr (kAsyncWeakRows)
+        asm volatile("ld.global.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else
+        asm volatile("ld.relaxed.gpu.global.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_unit_live(const uint2* p) { return kAsyncWeakRows ? ld_weak_u2(p) : ld_relaxed_u2(p); }
+__device__ __forceinline__ uint32_t ld_unit_live(const uint32_t* p) { return (uint32_t)ld_weak_or_relaxed(p); }
+__device__ __forceinline__ uint32_t unit_word(const uint4& u, int s) { return s == 0 ? u.x : s == 1 ? u.y : s == 2 ? u.z : u.w; }
+__device__ __forceinline__ uint32_t unit_word(const uint2& u, int s) { return s == 0 ? u.x : u.y; }
+__device__ __forceinline__ uint32_t unit_word(const uint32_t& u, int) { return u; }
+// the 4 counts of 4-topic block s of a unit, as fp32 (s is a compile-time index after unrolling)
+template <typename NT, typename U>
+__device__ __forceinline__ float4 unit_block(const U& u, int s) {
+    if constexpr (sizeof(NT) == 4) {
+        return make_float4(__uint_as_float(unit_word(u, 4 * s)), __uint_as_float(unit_word(u, 4 * s + 1)),
+                           __uint_as_float(unit_word(u, 4 * s + 2)), __uint_as_float(unit_word(u, 4 * s + 3)));
+    } else if constexpr (sizeof(NT) == 2) {
+        const uint32_t a = unit_word(u, 2 * s), b = unit_word(u, 2 * s + 1);
+        return make_float4(u16lo(a), u16hi(a), u16lo(b), u16hi(b));
+    } else {
+        const uint32_t a = unit_word(u, s);
+        return make_float4(u8at(a, 0), u8at(a, 1), u8at(a, 2), u8at(a, 3));
+    }
+}
+
 struct SweepArgs {
     // tokens of this rank, sorted by (wave, w, i, doc)
     const uint32_t* tok_doc;
@@ -379,7 +420,8 @@ struct SweepArgs {
     // counts
     void* n;                       // doc-topic counts n_dk (Row<NT>), rows in sigma order
     const int* sigma;              // [Kp] in-row position of topic k
-    int colstart[8];               // first block of column q in the sigma order
+    int LA;                        // lanes of a group that hold topics: ceil(K / KPL)
+    int Kn;                        // doc-topic row length (elements): LA * KPL
     int prefetch_rows;             // the doc-topic array exceeds L2: prefetch rows in phase 1
     int32_t* m;
     int32_t* t;
@@ -424,13 +466,16 @@ struct SweepArgs {
 
 // ---------------------------------------------------------------- the sample kernel
 // Doc-topic row layout ("sigma order").  A token's dense pass uses LPT lanes;
-// lane gl owns the canonical topics [gl*KPL, gl*KPL + KPL) as NB = KPL/4 blocks
-// of 4.  In memory the blocks are stored column-major over the lanes: block q of
-// lane gl sits at position colstart[q] + gl (colstart = prefix of the number of
-// lanes that have a block q), so one 16-byte load instruction of the group reads
-// consecutive bytes, rows keep length Kp, and each lane's topics are contiguous
-// in the canonical order — the CDF is one scan over lanes.  sigma[k] is the
-// in-row position of topic k (host table); every kernel touching n uses it.
+// lane gl owns the canonical topics [gl*KPL, gl*KPL + KPL), read as NU units of
+// UT topics (RowUnit: 16 bytes, or the whole span if smaller).  Only the
+// LA = ceil(K / KPL) lanes that hold topics have storage: unit j of lane gl sits
+// at unit index j * LA + gl (column-major over the active lanes), so one load
+// instruction of the group reads LA consecutive units, unit j is at a fixed
+// stride from unit 0 (one address add per load), and rows have Kn = LA * KPL
+// elements (the last active lane's topics past K are zero padding).  Each lane's
+// topics are contiguous in the canonical order — the CDF is one scan over lanes.
+// sigma[k] is the in-row position of topic k (host table); every other kernel
+// touching n uses it with the row length Kn.
 
 // Per-warp shared memory (KSPAN entries each unless noted).
 template <int KSPAN, int KPL>
@@ -440,12 +485,41 @@ struct __align__(16) WarpSmem {   // 16-byte multiple: every warp's F rows are r
     uint32_t mt[KSPAN];  // snapshot m << 16 | t of the segment's cells (M_max < 2^16)
     float R1[SPDP_SMEM_R1 && KSPAN <= 256 ? KSPAN : 1];   // r = 1 share F1 / F at the snapshot (phase 3's r split)
     int dmt[KSPAN];      // the chunk's delta m * 2^16 + delta t (|delta| <= chunk length)
-    // hand-over from the dense pass to the per-token search (one entry per token of the batch)
-    float bs[KPL / 4][32];   // the winning lane's block sums (without the own-removal fix)
-    double lbeg[32];         // prefix before the winning lane
-    double target[32];       // u * total
+    // hand-over from the dense pass to the per-token search (one entry per token of the batch), written
+    // and read with vector accesses: a token's block sums are one row (8 sums: 48-byte rows, so the
+    // 16-byte reads of 8 consecutive tokens hit distinct banks)
+    static constexpr int NB = KPL / 4, BSROW = NB == 8 ? 12 : NB;
+    alignas(16) float bs[32][BSROW];   // the winning lane's block sums (without the own-removal fix)
+    alignas(16) double2 lt[32];        // {prefix before the winning lane, u * total}
     int wgl[32];             // winning lane within the group (negative: fall back to the last positive slot)
 };
+// NB fp32 values to / from a shared-memory row (16-, 8- or 4-byte accesses)
+template <int NB>
+__device__ __forceinline__ void store_row(float* r, const float* v) {
+    if constexpr (NB >= 4) {
+#pragma unroll
+        for (int q = 0; q < NB; q += 4) *reinterpret_cast<float4*>(r + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+    } else if constexpr (NB == 2) {
+        *reinterpret_cast<float2*>(r) = make_float2(v[0], v[1]);
+    } else {
+        r[0] = v[0];
+    }
+}
+template <int NB>
+__device__ __forceinline__ void load_row(const float* r, float* v) {
+    if constexpr (NB >= 4) {
+#pragma unroll
+        for (int q = 0; q < NB; q += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(r + q);
+            v[q] = x.x; v[q + 1] = x.y; v[q + 2] = x.z; v[q + 3] = x.w;
+        }
+    } else if constexpr (NB == 2) {
+        const float2 x = *reinterpret_cast<const float2*>(r);
+        v[0] = x.x; v[1] = x.y;
+    } else {
+        v[0] = r[0];
+    }
+}
 template <int KPL>
 __device__ __forceinline__ int skew(int k) { return k + 4 * (k / KPL); }
 
@@ -499,9 +573,9 @@ sample_kernel(SweepArgs A) {
     constexpr int KSPAN = LPT * KPL;
     constexpr int NB = KPL / 4;                      // 4-topic blocks per lane
     static_assert(KPL % 4 == 0 && NB <= 8, "KPL must be a multiple of 4, at most 32");
-    // skipping the loads of blocks past K saves bytes but changes register allocation and
-    // scheduling; measured (B200): a gain at 4x32 and 16x32, a loss at 8x32 (C5) and 32x32 (K = 1000)
-    constexpr bool kSkipPad = SPDP_SKIP_PAD_BLOCKS && (LPT == 4 || LPT == 16);
+    using RU = RowUnit<NT, KPL>;
+    using unit_t = typename RU::type;
+    constexpr int NU = RU::NU, QPU = RU::QPU, UT = RU::UT;
     // per-block alpha sums: 2.5-3.5 % faster at C3, K = 300, K = 1000 (B200); not under the
     // 5-blocks register cap of 8x32, where the 8 extra registers spill (C5 +2.7 %)
     // narrow rows keep their raw blocks (1-2 registers per 4 counts instead of 4), which frees the registers the
@@ -524,6 +598,9 @@ sample_kernel(SweepArgs A) {
     const int g = lane / LPT, gl = lane % LPT;
     const int kb = gl * KPL;                         // this lane's first canonical topic (phase 2)
     const unsigned gmask = (LPT == 32) ? 0xffffffffu : (((1u << LPT) - 1u) << (g * LPT));
+    const int LA = A.LA, Kn = A.Kn;
+    const bool lane_rows = gl < LA;                  // this lane's topics have row storage
+    const size_t ustride = (size_t)LA * RU::UB;      // bytes from unit j to unit j + 1 of a lane
 
   // persistent warps: grab chunks (sorted longest first on the host) from a counter
   for (;;) {
@@ -633,7 +710,7 @@ sample_kernel(SweepArgs A) {
         uint32_t noff = 0, zr0 = 0, x0 = 0;
         double u = 0.0;
         if (mine) {
-            noff = A.tok_doc[p] * (uint32_t)Kp;            // doc-topic row offset (fits 32 bits)
+            noff = A.tok_doc[p] * (uint32_t)Kn;            // doc-topic row offset (fits 32 bits)
             zr0 = A.zr[p];
         }
         // the own-removal inputs of topic k0 (both table candidates: r_rem is drawn below), issued
@@ -661,23 +738,23 @@ sample_kernel(SweepArgs A) {
             if constexpr (SPDP_BULK_PREFETCH) {
                 // one exact-size bulk prefetch per row: at the chunk's first batch the rows of batches
                 // 0 .. AHEAD, afterwards those of batch b + AHEAD (the copy engine runs ahead of the sampling)
-                const uint32_t rbytes = (uint32_t)((size_t)Kp * sizeof(NT));
+                const uint32_t rbytes = (uint32_t)((size_t)Kn * sizeof(NT));
                 if (b0 == start) {
 #pragma unroll
                     for (int j = 0; j < SPDP_PREFETCH_AHEAD; ++j)
                         if (p + 32u * j < end)
-                            prefetch_bytes_l2(reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[p + 32u * j] * Kp, rbytes);
+                            prefetch_bytes_l2(reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[p + 32u * j] * Kn, rbytes);
                 }
                 const uint32_t pn = p + 32u * SPDP_PREFETCH_AHEAD;
-                if (pn < end) prefetch_bytes_l2(reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp, rbytes);
+                if (pn < end) prefetch_bytes_l2(reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kn, rbytes);
             } else {
                 constexpr int PER_LINE = 128 / (int)sizeof(NT);
                 if (mine && (b0 == start || !SPDP_PREFETCH_NEXT))
-                    for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
+                    for (int l = 0; l * PER_LINE < Kn; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nrow + PER_LINE * l));
                 const uint32_t pn = p + 32;
                 if (SPDP_PREFETCH_NEXT && pn < end) {
-                    const NT* nn = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kp;
-                    for (int l = 0; l * PER_LINE < Kp; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
+                    const NT* nn = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[pn] * Kn;
+                    for (int l = 0; l * PER_LINE < Kn; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(nn + PER_LINE * l));
                 }
             }
         }
@@ -700,19 +777,19 @@ sample_kernel(SweepArgs A) {
         const float dlt = wnew - wold;
 
         // ======== phase 2: LPT lanes per token
-        typename Row<NT>::raw_t v[NB];               // raw blocks (fp32 at use: narrow rows keep few registers)
+        unit_t v[NU];                                // raw row units (fp32 at use: narrow rows keep few registers);
+#pragma unroll                                       // lanes without storage keep zeros (F = 0 there)
+        for (int j = 0; j < NU; ++j) v[j] = unit_t{};
         auto load_rows = [&](uint32_t s) {            // the doc-topic rows of step s's tokens
             const uint32_t so = __shfl_sync(0xffffffffu, noff, (s + g) & 31);
-            const NT* __restrict__ nl = reinterpret_cast<const NT*>(A.n) + so + 4 * gl;
+            const unsigned char* nl = reinterpret_cast<const unsigned char*>(A.n) + (size_t)so * sizeof(NT) + gl * RU::UB;
+            if (lane_rows) {
 #pragma unroll
-            for (int q = 0; q < NB; ++q) {   // blocks past K hold no topic (zero mass): no load, or one inside the row
-                if constexpr (kSkipPad)
-                    v[q] = (kb + 4 * q < K) ? row_load_raw<NT, ASYNC>(nl + 4 * A.colstart[q]) : Row<NT>::zero_raw();
-                else if constexpr (SPDP_PAD_SELECT)
-                    v[q] = row_load_raw<NT, ASYNC>((kb + 4 * q < K) ? nl + 4 * A.colstart[q]
-                                                                    : reinterpret_cast<const NT*>(A.n) + so);
-                else
-                    v[q] = row_load_raw<NT, ASYNC>(nl + 4 * A.colstart[q]);
+                for (int j = 0; j < NU; ++j) {
+                    const unit_t* up = reinterpret_cast<const unit_t*>(nl + (size_t)j * ustride);
+                    if constexpr (ASYNC) v[j] = ld_unit_live(up);
+                    else v[j] = ld_unit_nc(up);
+                }
             }
         };
         if constexpr (kRowPipe) load_rows(0);
@@ -725,7 +802,7 @@ sample_kernel(SweepArgs A) {
             float sb[NB];
 #pragma unroll
             for (int q = 0; q < NB; ++q) {
-                const float4 n4 = Row<NT>::cvt(v[q]);
+                const float4 n4 = unit_block<NT>(v[q / QPU], q % QPU);
                 if constexpr (kBlockAlpha) {
                     // no per-topic alpha term: 4 FFMA per block, no shared-memory load
                     float x = __fmaf_rn(n4.x, F[4 * q + 0], aSF[q]);
@@ -768,10 +845,8 @@ sample_kernel(SweepArgs A) {
             const unsigned posl = __ballot_sync(0xffffffffu, acc > 0.0) & gmask;
             const int winner = hit ? (__ffs(hit) - 1) : (posl ? 31 - __clz(posl) : g * LPT);
             if (lane == winner && s0 + g < nb) {
-#pragma unroll
-                for (int q = 0; q < NB; ++q) S.bs[q][src] = sb[q];
-                S.lbeg[src] = incl - acc;
-                S.target[src] = target;
+                store_row<NB>(S.bs[src], sb);
+                S.lt[src] = make_double2(incl - acc, target);
                 S.wgl[src] = hit ? gl : -1 - gl;
             }
         }
@@ -781,15 +856,16 @@ sample_kernel(SweepArgs A) {
         if (mine) {
             int ks = k0, rs = 1;
             if (!keep) {
-                const double target = S.target[lane];
-                const double lbeg = S.lbeg[lane];
+                const double2 ltv = S.lt[lane];
+                const double lbeg = ltv.x, target = ltv.y;
                 const int wv = S.wgl[lane];
                 bool fb = wv < 0;
                 const int wg = fb ? -1 - wv : wv;
                 const int own_q = (k0 >= wg * KPL && k0 < wg * KPL + KPL) ? ((k0 - wg * KPL) >> 2) : -1;
                 float bsv[NB];
+                load_row<NB>(S.bs[lane], bsv);
 #pragma unroll
-                for (int q = 0; q < NB; ++q) bsv[q] = S.bs[q][lane] + ((q == own_q) ? dlt : 0.f);
+                for (int q = 0; q < NB; ++q) bsv[q] += (q == own_q) ? dlt : 0.f;
                 // block: count the blocks whose fp32 prefix does not exceed the target
                 const float rel = (float)(target - lbeg);
                 float run = 0.f;
@@ -807,10 +883,7 @@ sample_kernel(SweepArgs A) {
                 // the block's 4 topic masses (their fp32 sum may differ from the dense pass's block
                 // sum by a few ulps; a target in that gap takes the last positive topic below)
                 const int kq = wg * KPL + 4 * qs;
-                int cs = 0;
-#pragma unroll
-                for (int q = 0; q < NB; ++q) if (q == qs) cs = A.colstart[q];
-                const float4 n4 = row_load4<NT, ASYNC>(nrow + 4 * (cs + wg));
+                const float4 n4 = row_load4<NT, ASYNC>(nrow + ((qs / QPU) * LA + wg) * UT + 4 * (qs % QPU));
                 const float4 F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
                 const float4 a4 = *reinterpret_cast<const float4*>(&S.aF[skew<KPL>(kq)]);
                 float wq[4] = {__fmaf_rn(n4.x, F4.x, a4.x), __fmaf_rn(n4.y, F4.y, a4.y),
@@ -937,12 +1010,12 @@ template <typename NT>
 __global__ void apply_tokens_kernel(const uint32_t* __restrict__ tok_doc, uint16_t* __restrict__ zr,
                                     const uint16_t* __restrict__ zr_next, NT* __restrict__ n,
                                     const int* __restrict__ sigma,
-                                    int Kp, uint32_t begin, uint32_t end) {
+                                    int Kn, uint32_t begin, uint32_t end) {
     for (uint32_t p = begin + blockIdx.x * blockDim.x + threadIdx.x; p < end; p += gridDim.x * blockDim.x) {
         const uint32_t zo = zr[p], zn = zr_next[p];
         const uint32_t ko = zo & 0x7FFFu, kn = zn & 0x7FFFu;
         if (ko != kn) {
-            const size_t r0 = (size_t)tok_doc[p] * Kp;
+            const size_t r0 = (size_t)tok_doc[p] * Kn;
             Row<NT>::add(n, r0 + sigma[ko], -1);   // exact integer arithmetic
             Row<NT>::add(n, r0 + sigma[kn], 1);
         }
@@ -1035,13 +1108,13 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
 // sorted-token positions), one coalesced row write in sigma order.
 template <typename NT>
 __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const uint32_t* __restrict__ doc_pos,
-                                    const uint16_t* __restrict__ zr, const int* __restrict__ sigma, int D, int Kp,
+                                    const uint16_t* __restrict__ zr, const int* __restrict__ sigma, int D, int Kn,
                                     NT* __restrict__ n, const uint16_t* __restrict__ zr_doc) {
-    extern __shared__ int hist[];                    // [warps][Kp]
+    extern __shared__ int hist[];                    // [warps][Kn] (row positions; the padding stays 0)
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    int* h = hist + (size_t)(threadIdx.x >> 5) * Kp;
+    int* h = hist + (size_t)(threadIdx.x >> 5) * Kn;
     for (int d = blockIdx.x * wpb + (threadIdx.x >> 5); d < D; d += gridDim.x * wpb) {
-        for (int j = lane; j < Kp; j += 32) h[j] = 0;
+        for (int j = lane; j < Kn; j += 32) h[j] = 0;
         __syncwarp();
         const uint32_t e = doc_ptr[d + 1];
         if (zr_doc) {   // the sample kernel already wrote the assignments in document order: stream them
@@ -1063,8 +1136,8 @@ __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const 
                 if (zv[j] != 0xFFFFFFFFu) atomicAdd(&h[sigma[zv[j] & 0x7FFFu]], 1);
         }
         __syncwarp();
-        NT* row = n + (size_t)d * Kp;
-        for (int j = lane * 4; j < Kp; j += 128) Row<NT>::store4(row + j, h[j], h[j + 1], h[j + 2], h[j + 3]);
+        NT* row = n + (size_t)d * Kn;
+        for (int j = lane * 4; j < Kn; j += 128) Row<NT>::store4(row + j, h[j], h[j + 1], h[j + 2], h[j + 3]);
         __syncwarp();
     }
 }
@@ -1392,14 +1465,14 @@ __global__ void check_cells_kernel(const int32_t* __restrict__ m, const int32_t*
 // this rank's token records (sorted order) and doc-topic counts
 template <typename NT>
 __global__ void init_local_kernel(const uint32_t* __restrict__ tok_id, const uint32_t* __restrict__ tok_doc,
-                                  const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t nloc, int Kp,
+                                  const int32_t* __restrict__ z, const uint8_t* __restrict__ r, uint32_t nloc, int Kn,
                                   const int* __restrict__ sigma,
                                   uint16_t* __restrict__ zr, uint16_t* __restrict__ zr_next, NT* __restrict__ n) {
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += gridDim.x * blockDim.x) {
         const uint32_t p = tok_id[q];
         const uint16_t v = (uint16_t)(z[p] | (r[p] << 15));
         zr[q] = v; zr_next[q] = v;
-        Row<NT>::add(n, (size_t)tok_doc[q] * Kp + sigma[z[p]], 1);
+        Row<NT>::add(n, (size_t)tok_doc[q] * Kn + sigma[z[p]], 1);
     }
 }
 
@@ -1461,7 +1534,7 @@ perplexity_kernel(SweepArgs A, const int32_t* __restrict__ doclen, const double*
         const uint32_t tok = base + g;
         const bool valid = tok < end;
         const uint32_t doc = valid ? A.tok_doc[tok] : 0u;
-        const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * Kp;
+        const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * A.Kn;
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < KPL; ++j)

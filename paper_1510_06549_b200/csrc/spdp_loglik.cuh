@@ -80,7 +80,7 @@ template <typename NT>
 __global__ void loglik_docs_kernel(const NT* __restrict__ n, const int* __restrict__ sigma,
                                    const int32_t* __restrict__ doclen,
                                    const int32_t* __restrict__ docgroup, const double* __restrict__ alpha,
-                                   const double* __restrict__ alpha_sum, int D, int K, int Kp,
+                                   const double* __restrict__ alpha_sum, int D, int K, int Kp, int Kn,
                                    double* __restrict__ partial) {
     __shared__ double sh[32];
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
@@ -89,7 +89,7 @@ __global__ void loglik_docs_kernel(const NT* __restrict__ n, const int* __restri
         const int i = docgroup[d];
         if (doclen[d] == 0) continue;      // empty document: p(z_d) = 1
         for (int k = lane; k < K; k += 32) {
-            const int nv = Row<NT>::get(n + (size_t)d * Kp + sigma[k]);
+            const int nv = Row<NT>::get(n + (size_t)d * Kn + sigma[k]);
             if (nv) {
                 const double al = alpha[(size_t)i * Kp + k];
                 acc += lgamma(al + (double)nv) - lgamma(al);

@@ -66,7 +66,8 @@ __global__ void plan_keys_kernel(const uint32_t* __restrict__ local, uint32_t nl
                                  uint64_t S, uint64_t* __restrict__ key) {
     for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nloc; q += gridDim.x * blockDim.x) {
         const uint32_t p = local[q];
-        key[q] = (uint64_t)(pos[p] % W) * S + (uint64_t)word[p] * (uint64_t)I + (uint64_t)group[p];
+        const uint64_t wave = (W == 1) ? 0u : (uint64_t)(pos[p] % W);   // (W = 1: positions not computed)
+        key[q] = wave * S + (uint64_t)word[p] * (uint64_t)I + (uint64_t)group[p];
     }
 }
 
@@ -138,6 +139,17 @@ __global__ void seg_of_key_kernel(const uint64_t* __restrict__ key, uint32_t n, 
 }
 
 // doc index (local) of every sorted position, and 0..n-1 for the CSR sort
+// doc -> sorted-positions CSR by counting: slot j of document d's range gets one of d's sorted positions.
+// The order inside a document's range is arbitrary (atomics); its one consumer, the W = 1 recount, builds
+// an order-independent histogram from it, so every count stays deterministic.
+__global__ void csr_scatter_kernel(const uint32_t* __restrict__ tdoc, uint32_t n, const uint32_t* __restrict__ doc_ptr,
+                                   uint32_t* __restrict__ cursor, uint32_t* __restrict__ doc_pos) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        const uint32_t d = tdoc[j];
+        doc_pos[doc_ptr[d] + atomicAdd(cursor + d, 1u)] = j;
+    }
+}
+
 __global__ void tdoc_kernel(const uint32_t* __restrict__ tok_id, uint32_t n, const int32_t* __restrict__ doc,
                             const int32_t* __restrict__ local_of_doc, uint32_t* __restrict__ tdoc,
                             uint32_t* __restrict__ q) {

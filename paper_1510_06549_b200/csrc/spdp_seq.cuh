@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(32, 1) seq_kernel(SweepArgs A, SeqArgs S) {
             const uint32_t zr0 = A.zr[q];
             const int k0 = (int)(zr0 & 0x7FFFu);
             const size_t row = ((size_t)w * I + i) * Kp;
-            const size_t noff = (size_t)A.tok_doc[q] * Kp;
+            const size_t noff = (size_t)A.tok_doc[q] * A.Kn;
             const int mc = A.m[row + k0], tc = A.t[row + k0];
             const uint4 x = philox(make_uint4((uint32_t)p, sweep, 0u, 0u), A.key0, A.key1);   // a2
             const int rrem = removal_draw(x.x, mc, tc);                                        // a3, Alg.1 l.3

@@ -102,6 +102,7 @@ struct SpTokenArgs {
     const uint64_t* tab_off;
     float beta, vbeta;
     int I, K, Kp;
+    int Kn;                        // doc-topic row length
     uint32_t key0, key1;
     const uint32_t* sweep;
     uint32_t begin, end;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(256) sp_token_kernel(SpTokenArgs A) {
                 Fk0 = x0 + x1;
                 R1k0 = (x1 > 0.f) ? __fdiv_rn(x1, Fk0) : 0.f;
             }
-            const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[p] * Kp;
+            const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)A.tok_doc[p] * A.Kn;
             const float* Frow = A.F + (size_t)run * Kp;
             const float* al = A.alpha + (size_t)i * Kp;
             const float n0 = Row<NT>::load1(nrow + A.sigma[k0]);

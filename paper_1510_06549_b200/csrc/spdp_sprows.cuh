@@ -299,13 +299,13 @@ __global__ void __launch_bounds__(kSpWarps * 32) sample_sprows_kernel(SweepArgs 
 // its nonzero counts as entries k | n << 16 in topic order at ent[cap_ptr[d] ...]; dinfo[d] =
 // {first entry, count}.  One warp per document.
 template <typename NT>
-__global__ void rows_to_entries_kernel(const NT* __restrict__ n, const int* __restrict__ sigma, int D, int K, int Kp,
+__global__ void rows_to_entries_kernel(const NT* __restrict__ n, const int* __restrict__ sigma, int D, int K, int Kn,
                                        const uint32_t* __restrict__ cap_ptr, uint32_t* __restrict__ ent,
                                        uint2* __restrict__ dinfo) {
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     for (int d = blockIdx.x * wpb + (threadIdx.x >> 5); d < D; d += gridDim.x * wpb) {
-        const NT* row = n + (size_t)d * Kp;
+        const NT* row = n + (size_t)d * Kn;
         const uint32_t e0 = cap_ptr[d];
         uint32_t cnt = 0;
         for (int kb = 0; kb < K; kb += 32) {

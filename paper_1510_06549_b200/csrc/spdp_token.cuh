@@ -101,6 +101,7 @@ struct TokenArgs {
     const uint64_t* tab_off;
     float beta, vbeta;
     int I, K, Kp;
+    int Kn;                        // doc-topic row length
     uint32_t key0, key1;
     const uint32_t* sweep;
     uint32_t begin, end;           // sorted-token range of the wave
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(256, SPDP_TOKEN_MINB) token_kernel(TokenArgs A
                 const int32_t* Qw = A.Q + (size_t)w * Kp;
                 removal_factors(rrem, m0, t0, Mi[k0], Tti[k0], Qw[k0], A.T[k0], tab, a, b, A.beta, A.vbeta, Fk0, R1k0);
             }
-            const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * Kp;
+            const NT* nrow = reinterpret_cast<const NT*>(A.n) + (size_t)doc * A.Kn;
             const float* Frow = A.F + (size_t)run * Kp;
             const float* aFrow = A.aF + (size_t)run * Kp;
             const float* al = A.alpha + (size_t)i * Kp;

@@ -5,12 +5,12 @@
 mkdir -p gpurun_out
 cap() {  # tag kernel-regex args...
   local tag=$1 kre=$2; shift 2
-  local rep=/tmp/r2_ncu_$tag
+  local rep=/tmp/${NCU_PREFIX:-r2}_ncu_$tag
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$kre -s 2 -c 1 \
-    -o $rep -f python tools/prof_sweeps.py --sweeps 3 "$@" > gpurun_out/r2_ncu_$tag.log 2>&1 \
-    || echo "ncu $tag failed" >> gpurun_out/r2_ncu_failures.txt
-  python tools/ncu_summary.py $rep.ncu-rep gpurun_out/r2_ncu_$tag.json > /dev/null 2>>gpurun_out/r2_ncu_$tag.log
-  python tools/ncu_source_top.py $rep.ncu-rep 50 > gpurun_out/r2_ncu_${tag}_src.txt 2>>gpurun_out/r2_ncu_$tag.log
+    -o $rep -f python tools/prof_sweeps.py --sweeps 3 "$@" > gpurun_out/${NCU_PREFIX:-r2}_ncu_$tag.log 2>&1 \
+    || echo "ncu $tag failed" >> gpurun_out/${NCU_PREFIX:-r2}_ncu_failures.txt
+  python tools/ncu_summary.py $rep.ncu-rep gpurun_out/${NCU_PREFIX:-r2}_ncu_$tag.json > /dev/null 2>>gpurun_out/${NCU_PREFIX:-r2}_ncu_$tag.log
+  python tools/ncu_source_top.py $rep.ncu-rep 50 > gpurun_out/${NCU_PREFIX:-r2}_ncu_${tag}_src.txt 2>>gpurun_out/${NCU_PREFIX:-r2}_ncu_$tag.log
   if [ "$KEEP_REP" = "1" ]; then cp $rep.ncu-rep gpurun_out/; fi
 }
 for spec in "$@"; do
