@@ -1725,8 +1725,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
 #undef CALL_SS
         }
     }
-    {   // unit j of lane gl at unit index j * LA + gl; UT topics (16 bytes, or the lane's span) per unit
-        const int UT = std::min(16 / c->row_elem, c->KPL);
+    {   // unit j of lane gl at unit index j * LA + gl; UT topics (32 bytes, or the lane's span) per unit
+        const int UT = std::min(32 / c->row_elem, c->KPL);
         c->sigma.assign((size_t)Kp, 0);
         for (int k = 0; k < Kp; ++k) {
             const int gl = k / c->KPL, kk = k % c->KPL;

@@ -51,6 +51,12 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #ifndef SPDP_PREFETCH_AHEAD
 #define SPDP_PREFETCH_AHEAD 1      // bulk prefetch: batches of 32 tokens ahead of the one being sampled
 #endif
+#ifndef SPDP_STAGE_NEXT
+#define SPDP_STAGE_NEXT 0          // 1: the next chunk's counts and Stirling entries staged during this chunk (B200: C3 +5 %, C5 +3 %)
+#endif
+#ifndef SPDP_F_SMEM
+#define SPDP_F_SMEM 0              // dense pass reads F_k from shared memory instead of KPL registers per lane
+#endif
 #ifndef SPDP_MINB_8X32
 #define SPDP_MINB_8X32 5
 #endif
@@ -358,25 +364,48 @@ struct Row<uint8_t> {
 };
 
 // ---------------------------------------------------------------- row units (the sample kernel's dense pass)
-// A lane reads its topics as units of UB = min(16, KPL * sizeof(NT)) bytes: one 16-byte load holds 4 fp32,
-// 8 uint16 or 16 uint8 counts.  Unit j of lane gl sits at unit index j * LA + gl of the row (column-major
+// A lane reads its topics as units of UB = min(32, KPL * sizeof(NT)) bytes: one 32-byte load (sm_100's
+// 256-bit LDG) holds 8 fp32, 16 uint16 or 32 uint8 counts.  Unit j of lane gl sits at unit index j * LA + gl of the row (column-major
 // over the LA lanes that hold topics), so one load instruction of a lane group reads LA * UB consecutive
 // bytes, and unit j is a fixed stride j * LA * UB from the lane's first unit.
+struct __align__(32) uint8x32 { uint32_t w[8]; };
 template <int UB> struct UnitT;
+template <> struct UnitT<32> { using type = uint8x32; };
 template <> struct UnitT<16> { using type = uint4; };
 template <> struct UnitT<8> { using type = uint2; };
 template <> struct UnitT<4> { using type = uint32_t; };
 template <typename NT, int KPL>
 struct RowUnit {
-    static constexpr int UT = (16 / (int)sizeof(NT)) < KPL ? 16 / (int)sizeof(NT) : KPL;   // topics per unit
+    static constexpr int UT = (32 / (int)sizeof(NT)) < KPL ? 32 / (int)sizeof(NT) : KPL;   // topics per unit
     static constexpr int UB = UT * (int)sizeof(NT);                                          // bytes per unit
     static constexpr int NU = KPL / UT;                                                      // units per lane
     static constexpr int QPU = UT / 4;                                                       // 4-topic blocks per unit
     using type = typename UnitT<UB>::type;
 };
+__device__ __forceinline__ uint8x32 ld_unit_nc(const uint8x32* p) {
+    uint8x32 v;
+    asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]), "=r"(v.w[7])
+        : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint4 ld_unit_nc(const uint4* p) { return __ldg(p); }
 __device__ __forceinline__ uint2 ld_unit_nc(const uint2* p) { return __ldg(p); }
 __device__ __forceinline__ uint32_t ld_unit_nc(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ uint8x32 ld_unit_live(const uint8x32* p) {
+    uint8x32 v;
+    if constexpr (kAsyncWeakRows)
+        asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                       "=r"(v.w[7])
+                     : "l"(p));
+    else
+        asm volatile("ld.relaxed.gpu.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                       "=r"(v.w[7])
+                     : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint4 ld_unit_live(const uint4* p) {
     uint4 v;
     if constexpr (kAsyncWeakRows)
@@ -387,6 +416,7 @@ __device__ __forceinline__ uint4 ld_unit_live(const uint4* p) {
 }
 __device__ __forceinline__ uint2 ld_unit_live(const uint2* p) { return kAsyncWeakRows ? ld_weak_u2(p) : ld_relaxed_u2(p); }
 __device__ __forceinline__ uint32_t ld_unit_live(const uint32_t* p) { return (uint32_t)ld_weak_or_relaxed(p); }
+__device__ __forceinline__ uint32_t unit_word(const uint8x32& u, int s) { return u.w[s]; }
 __device__ __forceinline__ uint32_t unit_word(const uint4& u, int s) { return s == 0 ? u.x : s == 1 ? u.y : s == 2 ? u.z : u.w; }
 __device__ __forceinline__ uint32_t unit_word(const uint2& u, int s) { return s == 0 ? u.x : u.y; }
 __device__ __forceinline__ uint32_t unit_word(const uint32_t& u, int) { return u; }
@@ -480,7 +510,7 @@ struct SweepArgs {
 // Per-warp shared memory (KSPAN entries each unless noted).
 template <int KSPAN, int KPL>
 struct __align__(16) WarpSmem {   // 16-byte multiple: every warp's F rows are read as float4
-    float F[KSPAN];      // F0 + F1 at the snapshot counts
+    float F[KSPAN + 4 * (KSPAN / KPL)];    // F0 + F1 at the snapshot counts, skewed like aF
     float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
     uint32_t mt[KSPAN];  // snapshot m << 16 | t of the segment's cells (M_max < 2^16)
     float R1[SPDP_SMEM_R1 && KSPAN <= 256 ? KSPAN : 1];   // r = 1 share F1 / F at the snapshot (phase 3's r split)
@@ -492,7 +522,27 @@ struct __align__(16) WarpSmem {   // 16-byte multiple: every warp's F rows are r
     alignas(16) float bs[32][BSROW];   // the winning lane's block sums (without the own-removal fix)
     alignas(16) double2 lt[32];        // {prefix before the winning lane, u * total}
     int wgl[32];             // winning lane within the group (negative: fall back to the last positive slot)
+    // the next chunk's snapshot m and t rows, copied asynchronously during this chunk's last batch
+    // (KSPAN <= 256); its Stirling-table entries land in the hand-over region (bs, lt), which is free
+    // between the end of the last batch and the next chunk's first
+    static constexpr bool kStage = SPDP_STAGE_NEXT != 0 && KSPAN <= 256;
+    alignas(16) int nm[kStage ? KSPAN : 4];
+    alignas(16) int nt[kStage ? KSPAN : 4];
+    uint32_t nxc, nseg;      // the next chunk's index and segment (kept here, not in registers)
+    __device__ __forceinline__ float2* ntab() { return reinterpret_cast<float2*>(&bs[0][0]); }
 };
+template <typename WS>
+__host__ __device__ constexpr bool stage_fits() { return sizeof(WS::bs) + sizeof(WS::lt) >= 8 * sizeof(WS::nm) / sizeof(int); }
+
+// asynchronous global -> shared copies (cp.async, sm_80+): no registers held while in flight
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // NB fp32 values to / from a shared-memory row (16-, 8- or 4-byte accesses)
 template <int NB>
 __device__ __forceinline__ void store_row(float* r, const float* v) {
@@ -590,6 +640,11 @@ sample_kernel(SweepArgs A) {
     // r = 1 shares from the prologue in shared memory (not in the async mode: its copy is per chunk too,
     // but the live sums it reads in phase 3 are fresher); KSPAN <= 256 (smem budget of 16x32 / 32x32)
     constexpr bool kSmemR1 = SPDP_SMEM_R1 != 0 && KSPAN <= 256 && !ASYNC;
+    constexpr bool kFSmem = SPDP_F_SMEM != 0;
+    // the next chunk's prologue inputs staged during this chunk (wave mode: snapshot counts do not change
+    // within a wave; the async mode copies live counts at chunk start by design)
+    constexpr bool kStage = SPDP_STAGE_NEXT != 0 && WarpSmem<KSPAN, KPL>::kStage && !ASYNC && !DEBUG;
+    static_assert(!kStage || stage_fits<WarpSmem<KSPAN, KPL>>(), "staged table entries must fit the hand-over region");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpSmem<KSPAN, KPL>& S = reinterpret_cast<WarpSmem<KSPAN, KPL>*>(smem_raw)[wid];
@@ -602,14 +657,31 @@ sample_kernel(SweepArgs A) {
     const bool lane_rows = gl < LA;                  // this lane's topics have row storage
     const size_t ustride = (size_t)LA * RU::UB;      // bytes from unit j to unit j + 1 of a lane
 
-  // persistent warps: grab chunks (sorted longest first on the host) from a counter
-  for (;;) {
-    uint32_t cc = 0;
-    if (lane == 0) cc = atomicAdd(A.work, 1u);
-    const int c = (int)__shfl_sync(0xffffffffu, cc, 0);
-    if (c >= A.nchunks) break;                       // warp-uniform
+  // persistent warps: grab chunks (sorted longest first on the host) from a counter.  Staged mode: the
+  // next chunk's index is taken when this one starts, and its descriptor, m and t rows and Stirling-table
+  // entries are copied to shared memory during this chunk's last batch, off the prologue's critical path.
+  const bool stage = kStage && !A.chunk_ft;
+  bool staged = false;                               // the current chunk's prologue inputs are in S.nm, S.nt, S.ntab
+  if (stage) {
+    if (lane == 0) S.nxc = atomicAdd(A.work, 1u);
     __syncwarp();
-    const uint32_t seg = A.chunk_seg[c];
+  }
+  for (;;) {
+    uint32_t nx = 0;                                 // lane 0: the next chunk's index (in flight during the prologue)
+    int c;
+    if (stage) {
+      c = (int)S.nxc;
+      if (c >= A.nchunks) break;                     // warp-uniform
+      __syncwarp();
+      if (lane == 0) nx = atomicAdd(A.work, 1u);
+    } else {
+      uint32_t cc = 0;
+      if (lane == 0) cc = atomicAdd(A.work, 1u);
+      c = (int)__shfl_sync(0xffffffffu, cc, 0);
+      if (c >= A.nchunks) break;                     // warp-uniform
+    }
+    __syncwarp();
+    const uint32_t seg = staged ? S.nseg : A.chunk_seg[c];
     const int w = (int)(seg / (uint32_t)I), i = (int)(seg % (uint32_t)I);
     const size_t row = (size_t)seg * Kp;
     const float a = A.disc[i], b = A.conc[i];
@@ -624,6 +696,10 @@ sample_kernel(SweepArgs A) {
     // tables (chunk_ft: coalesced row loads, no dependent chain), or computed here.  Computed: topics in
     // groups of PG per lane, all count loads of a group first, then its Stirling-table loads, then the math.
     uint32_t crun = 0;
+    if (staged) {                                    // this chunk's staged copies have landed
+        cp_async_wait_all();
+        __syncwarp();
+    }
     if (!ASYNC && A.chunk_ft) {
         crun = A.tok_run[start];
         const size_t rrow = (size_t)crun * Kp;
@@ -632,7 +708,7 @@ sample_kernel(SweepArgs A) {
             uint32_t mt = 0;
             if (k < K) { Fk = A.Ft[rrow + k]; aFk = A.aFt[rrow + k]; mt = A.MTt[rrow + k]; }
             if constexpr (kSmemR1) S.R1[k] = (k < K) ? A.R1t[rrow + k] : 0.f;
-            S.F[k] = Fk;
+            S.F[skew<KPL>(k)] = Fk;
             S.aF[skew<KPL>(k)] = aFk;
             S.mt[k] = mt;
             S.dmt[k] = 0;
@@ -646,6 +722,20 @@ sample_kernel(SweepArgs A) {
             int mv[PG], tv[PG], Mv[PG], Ttv[PG], Qv[PG], Tv[PG];
             float al[PG];
             float2 tb[PG];
+            if (staged) {                            // staged during the previous chunk: m, t and the table entries
+#pragma unroll
+                for (int j = 0; j < PG; ++j) {
+                    const int k = lane + 32 * (k0g + j);
+                    mv[j] = tv[j] = Mv[j] = Ttv[j] = Qv[j] = Tv[j] = 0;
+                    al[j] = 0.f;
+                    tb[j] = make_float2(0.f, 0.f);
+                    if (k < K) {
+                        mv[j] = S.nm[k]; tv[j] = S.nt[k]; tb[j] = S.ntab()[k];
+                        al[j] = alpha_i[k];
+                        Mv[j] = Mi[k]; Ttv[j] = Tti[k]; Qv[j] = Qw[k]; Tv[j] = A.T[k];
+                    }
+                }
+            } else {
 #pragma unroll
             for (int j = 0; j < PG; ++j) {
                 const int k = lane + 32 * (k0g + j);
@@ -668,6 +758,7 @@ sample_kernel(SweepArgs A) {
                 }
                 tb[j] = (k < K) ? tab[tri(mv[j]) + tv[j]] : make_float2(0.f, 0.f);
             }
+            }   // computed loads
 #pragma unroll
             for (int j = 0; j < PG; ++j) {
                 const int k = lane + 32 * (k0g + j);
@@ -676,21 +767,27 @@ sample_kernel(SweepArgs A) {
                 if (k >= KSPAN) continue;            // KSPAN < 32 (K <= 16)
                 const float Fk = F0 + F1;
                 if constexpr (kSmemR1) S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
-                S.F[k] = Fk;
+                S.F[skew<KPL>(k)] = Fk;
                 S.aF[skew<KPL>(k)] = __fmul_rn(al[j], Fk);
                 S.mt[k] = ((uint32_t)mv[j] << 16) | (uint32_t)tv[j];
                 S.dmt[k] = 0;
             }
         }
     }   // computed prologue
+    if (stage && lane == 0) S.nxc = nx;              // (the atomic has returned by now)
     __syncwarp();
 
-    float F[KPL];                                    // aF stays in smem (conflict-free broadcast loads)
+    // the lane's F_k: registers, or (SPDP_F_SMEM) read from shared memory per block in the dense pass
+    // (conflict-free broadcast loads; frees KPL registers for more resident warps)
+    float F[kFSmem ? 1 : KPL];
+    if constexpr (!kFSmem) {
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-        const float4 f4 = *reinterpret_cast<const float4*>(&S.F[kb + 4 * q]);
-        F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
+        for (int q = 0; q < NB; ++q) {
+            const float4 f4 = *reinterpret_cast<const float4*>(&S.F[skew<KPL>(kb + 4 * q)]);
+            F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
+        }
     }
+    const float* Fl = &S.F[skew<KPL>(kb)];
     const float* aFl = &S.aF[skew<KPL>(kb)];
     float aSF[NB];                                   // per block: sum of alpha_ik F_k (SPDP_BLOCK_ALPHA)
     if constexpr (kBlockAlpha) {
@@ -704,6 +801,9 @@ sample_kernel(SweepArgs A) {
 
     for (uint32_t b0 = start; b0 < end; b0 += 32) {
         const uint32_t nb = min(32u, end - b0);
+        uint32_t seg_next = 0;                       // last batch: the next chunk's segment (its copies follow)
+        const bool stage_now = stage && b0 + 32u >= end && S.nxc < (uint32_t)A.nchunks;
+        if (stage_now) seg_next = A.chunk_seg[S.nxc];
         // ======== phase 1: lane = token
         const bool mine = (uint32_t)lane < nb;
         const uint32_t p = b0 + lane;
@@ -772,10 +872,19 @@ sample_kernel(SweepArgs A) {
         float n0 = mine ? row_load1<NT, ASYNC>(nrow + A.sigma[k0]) : 0.f;
         if constexpr (ASYNC) n0 = fmaxf(n0, 1.f);    // the token itself is counted in its row
         const float al0 = alpha_i[k0];
-        const float wold = __fmaf_rn(n0, S.F[k0], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
+        const float wold = __fmaf_rn(n0, S.F[skew<KPL>(k0)], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
         const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
         const float dlt = wnew - wold;
 
+        if (stage_now) {                             // the next chunk's snapshot m and t rows -> shared memory
+            if (lane == 0) S.nseg = seg_next;
+            const size_t rn = (size_t)seg_next * Kp;
+            for (int q = lane; 4 * q < K; q += 32) {
+                cp_async16(&S.nm[4 * q], A.m + rn + 4 * q);
+                cp_async16(&S.nt[4 * q], A.t + rn + 4 * q);
+            }
+            cp_async_commit();
+        }
         // ======== phase 2: LPT lanes per token
         unit_t v[NU];                                // raw row units (fp32 at use: narrow rows keep few registers);
 #pragma unroll                                       // lanes without storage keep zeros (F = 0 there)
@@ -805,16 +914,22 @@ sample_kernel(SweepArgs A) {
                 const float4 n4 = unit_block<NT>(v[q / QPU], q % QPU);
                 if constexpr (kBlockAlpha) {
                     // no per-topic alpha term: 4 FFMA per block, no shared-memory load
-                    float x = __fmaf_rn(n4.x, F[4 * q + 0], aSF[q]);
-                    x = __fmaf_rn(n4.y, F[4 * q + 1], x);
-                    x = __fmaf_rn(n4.z, F[4 * q + 2], x);
-                    sb[q] = __fmaf_rn(n4.w, F[4 * q + 3], x);
+                    float4 f4;
+                    if constexpr (kFSmem) f4 = *reinterpret_cast<const float4*>(Fl + 4 * q);
+                    else f4 = make_float4(F[4 * q + 0], F[4 * q + 1], F[4 * q + 2], F[4 * q + 3]);
+                    float x = __fmaf_rn(n4.x, f4.x, aSF[q]);
+                    x = __fmaf_rn(n4.y, f4.y, x);
+                    x = __fmaf_rn(n4.z, f4.z, x);
+                    sb[q] = __fmaf_rn(n4.w, f4.w, x);
                 } else {
                     const float4 af = *reinterpret_cast<const float4*>(aFl + 4 * q);
-                    const float w0 = __fmaf_rn(n4.x, F[4 * q + 0], af.x);
-                    const float w1 = __fmaf_rn(n4.y, F[4 * q + 1], af.y);
-                    const float w2 = __fmaf_rn(n4.z, F[4 * q + 2], af.z);
-                    const float w3 = __fmaf_rn(n4.w, F[4 * q + 3], af.w);
+                    float4 f4;
+                    if constexpr (kFSmem) f4 = *reinterpret_cast<const float4*>(Fl + 4 * q);
+                    else f4 = make_float4(F[4 * q + 0], F[4 * q + 1], F[4 * q + 2], F[4 * q + 3]);
+                    const float w0 = __fmaf_rn(n4.x, f4.x, af.x);
+                    const float w1 = __fmaf_rn(n4.y, f4.y, af.y);
+                    const float w2 = __fmaf_rn(n4.z, f4.z, af.z);
+                    const float w3 = __fmaf_rn(n4.w, f4.w, af.w);
                     sb[q] = (w0 + w1) + (w2 + w3);
                 }
             }
@@ -884,7 +999,7 @@ sample_kernel(SweepArgs A) {
                 // sum by a few ulps; a target in that gap takes the last positive topic below)
                 const int kq = wg * KPL + 4 * qs;
                 const float4 n4 = row_load4<NT, ASYNC>(nrow + ((qs / QPU) * LA + wg) * UT + 4 * (qs % QPU));
-                const float4 F4 = *reinterpret_cast<const float4*>(&S.F[kq]);
+                const float4 F4 = *reinterpret_cast<const float4*>(&S.F[skew<KPL>(kq)]);
                 const float4 a4 = *reinterpret_cast<const float4*>(&S.aF[skew<KPL>(kq)]);
                 float wq[4] = {__fmaf_rn(n4.x, F4.x, a4.x), __fmaf_rn(n4.y, F4.y, a4.y),
                                __fmaf_rn(n4.z, F4.z, a4.z), __fmaf_rn(n4.w, F4.w, a4.w)};
@@ -962,6 +1077,15 @@ sample_kernel(SweepArgs A) {
         }
         __syncwarp();
     }
+    const bool staged_next = stage && S.nxc < (uint32_t)A.nchunks;
+    if (staged_next) {                               // the next chunk's Stirling-table entries (the hand-over
+        cp_async_wait_all();                         // region is free until its first batch)
+        __syncwarp();
+        const uint32_t in = S.nseg % (uint32_t)I;
+        const float2* tabn = A.tab + A.tab_off[in];
+        for (int k = lane; k < K; k += 32) cp_async8(&S.ntab()[k], tabn + tri(S.nm[k]) + S.nt[k]);
+        cp_async_commit();
+    }
     if constexpr (!DEBUG) {
         __syncwarp();
         for (int k = lane; k < K; k += 32) {
@@ -985,6 +1109,7 @@ sample_kernel(SweepArgs A) {
         }
     }
     __syncwarp();
+    staged = staged_next;
   }  // chunk loop
     if constexpr (!DEBUG) {
 #pragma unroll

@@ -4,7 +4,7 @@
 # usage: LIBS="a.so b.so" CONFIGS="C3;C5;C4 --topics 300" bash tools/ab_libs.sh
 mkdir -p gpurun_out
 IFS=';' read -ra CS <<< "${CONFIGS:-C3}"
-for rep in 1 2; do
+for rep in $(seq ${REPS:-2}); do
 for cfg in "${CS[@]}"; do
   for lib in $LIBS; do
     st=30; [[ "$cfg" == C5* ]] && st=10
