@@ -212,6 +212,8 @@ struct spdp_ctx {
     // = max): the planning code synchronises after every CUB call, and the default pool would unmap and
     // remap the freed temporaries at each of those points
     cudaMemPool_t pool = nullptr;
+    bool pooled_alloc = false;            // ALLOC from the pool (inside spdp_load_corpus)
+    std::vector<void*> pooled;            // persistent buffers from the pool (freed stream-ordered at destroy)
     // profiling (spdp_profile)
     bool profiling = false;
     // one sweep captured as a CUDA graph and replayed (single rank): keyed by the zr buffer the sweep
@@ -251,12 +253,22 @@ spdp_status fail(spdp_ctx* c, spdp_status s, const char* fmt, ...) {
         if (e_ != cudaSuccess) return fail(c, SPDP_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
+// Persistent device buffers.  Inside spdp_load_corpus (c->pooled_alloc) they come from the context's pool
+// on its stream, so they reuse the memory the planning temporaries already mapped instead of mapping more
+// (every buffer allocated there is first used on c->stream, or after the load's final synchronisation).
 template <typename T>
 spdp_status alloc(spdp_ctx* c, T*& p, size_t n) {
     cudaError_t e;
-    p = dalloc<T>(n, e);
+    if (c->pool && c->pooled_alloc) {
+        void* q = nullptr;
+        e = cudaMallocFromPoolAsync(&q, std::max<size_t>(n, 1) * sizeof(T), c->pool, c->stream);
+        p = static_cast<T*>(q);
+        if (e == cudaSuccess) c->pooled.push_back(q);
+    } else {
+        p = dalloc<T>(n, e);
+        if (e == cudaSuccess) c->allocs.push_back(p);
+    }
     if (e != cudaSuccess) return fail(c, SPDP_ENOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
-    c->allocs.push_back(p);
     return SPDP_OK;
 }
 #define ALLOC(p, n)                                   \
@@ -807,22 +819,22 @@ spdp_status sparse_upload(spdp_ctx* c) {
     {
         std::vector<double> pp64(c->E_sp);
         for (size_t e = 0; e < c->dev_of_user.size(); ++e) pp64[c->dev_of_user[e]] = c->h_pp[e];
-        CU(cudaMemcpy(c->d_spp64, pp64.data(), sizeof(double) * pp64.size(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpyAsync(c->d_spp64, pp64.data(), sizeof(double) * pp64.size(), cudaMemcpyHostToDevice, c->stream));
     }
     ALLOC(c->d_q, (size_t)c->E_sp * Kp); ALLOC(c->d_dq, (size_t)c->E_sp * Kp);
     ALLOC(c->d_src, (size_t)std::max<int64_t>(c->Nloc, 1));
-    CU(cudaMemcpy(c->d_sptr, c->h_sptr.data(), sizeof(uint32_t) * c->h_sptr.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(c->d_spv, pv.data(), sizeof(int32_t) * pv.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(c->d_spp, pp.data(), sizeof(float) * pp.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(c->d_best, best.data(), sizeof(int32_t) * best.size(), cudaMemcpyHostToDevice));
-    CU(cudaMemset(c->d_dq, 0, sizeof(int32_t) * (size_t)c->E_sp * Kp));
-    CU(cudaMemset(c->d_src, 0xFF, sizeof(int16_t) * (size_t)std::max<int64_t>(c->Nloc, 1)));
+    CU(cudaMemcpyAsync(c->d_sptr, c->h_sptr.data(), sizeof(uint32_t) * c->h_sptr.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_spv, pv.data(), sizeof(int32_t) * pv.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_spp, pp.data(), sizeof(float) * pp.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_best, best.data(), sizeof(int32_t) * best.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemsetAsync(c->d_dq, 0, sizeof(int32_t) * (size_t)c->E_sp * Kp, c->stream));
+    CU(cudaMemsetAsync(c->d_src, 0xFF, sizeof(int16_t) * (size_t)std::max<int64_t>(c->Nloc, 1), c->stream));
     if (c->G > 1) {            // net changes of m (cells) then of q (E x Kp), int32, summed over ranks
         c->pack32 = true;
         int32_t *dl = nullptr, *ds = nullptr;
         ALLOC(dl, c->xcount()); ALLOC(ds, c->xcount());
         c->d_Dloc = dl; c->d_Dsum = ds;
-        CU(cudaMemset(c->d_Dloc, 0, c->dbytes()));
+        CU(cudaMemsetAsync(c->d_Dloc, 0, c->dbytes(), c->stream));
     }
     return SPDP_OK;
 }
@@ -1308,6 +1320,11 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     if (num_tokens >= (int64_t)0xFFFFFFFF) return fail(c, SPDP_EINVAL, "num_tokens must be < 2^32 - 1");
     const int I = c->I, V = c->V, Kp = c->Kp, W = c->W;
     TempStream temp_scope(c->stream, c->pool);
+    struct PooledScope {
+        spdp_ctx* c;
+        explicit PooledScope(spdp_ctx* x) : c(x) { c->pooled_alloc = true; }
+        ~PooledScope() { c->pooled_alloc = false; }
+    } pooled_scope(c);
     c->N = num_tokens; c->D = num_docs;
     // the token triples stay on the device (state installation); host copies only on demand (diagnostics)
     c->group.clear(); c->doc.clear(); c->word.clear();
@@ -1463,6 +1480,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             which[(size_t)i] = (int)j;
         }
         const uint64_t per = (uint64_t)(c->mmax + 1) * (uint64_t)(c->mmax + 2) / 2;
+        c->pooled_alloc = false;                     // used on the side stream at once: not stream-ordered memory
         ALLOC(c->d_tab, per * distinct.size());
         ALLOC(c->d_tab_off, I);
         c->tab_off_host.resize((size_t)I);
@@ -1470,6 +1488,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         CU(cudaMemcpyAsync(c->d_tab_off, c->tab_off_host.data(), sizeof(uint64_t) * I, cudaMemcpyHostToDevice, tab_stream));
         double* scratch = nullptr;
         ALLOC(scratch, 2 * (size_t)(c->mmax + 2) * distinct.size());
+        c->pooled_alloc = true;
         for (size_t j = 0; j < distinct.size(); ++j)
             build_ratio_table<<<1, 1024, 0, tab_stream>>>(c->d_tab + per * j, scratch + 2 * (size_t)(c->mmax + 2) * j,
                                                           c->mmax, distinct[j]);
@@ -1719,7 +1738,7 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             ALLOC(c->d_cap_ptr, (size_t)c->Dloc + 1);
             ALLOC(c->d_ent, std::max<size_t>((size_t)cap, 1));
             ALLOC(c->d_dinfo, std::max<int32_t>(c->Dloc, 1));
-            CU(cudaMemcpy(c->d_cap_ptr, capp.data(), sizeof(uint32_t) * capp.size(), cudaMemcpyHostToDevice));
+            CU(cudaMemcpyAsync(c->d_cap_ptr, capp.data(), sizeof(uint32_t) * capp.size(), cudaMemcpyHostToDevice, c->stream));
 #define CALL_SS(L, KS) sprows_setup_t<L, KS>(c)
             SPDP_SPROWS_DISPATCH(c->sp_lpt, c->sp_kspan, CALL_SS)
 #undef CALL_SS
@@ -1734,12 +1753,12 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         }
     }
     ALLOC(c->d_sigma, Kp);
-    CU(cudaMemcpy(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(c->d_sigma, c->sigma.data(), sizeof(int) * (size_t)Kp, cudaMemcpyHostToDevice, c->stream));
     {   // +1024 elements: the sample kernel reads whole topic spans
         uint8_t* nb = nullptr;
         ALLOC(nb, row_bytes(c));
         c->d_n = nb;
-        CU(cudaMemset(c->d_n, 0, row_bytes(c)));
+        CU(cudaMemsetAsync(c->d_n, 0, row_bytes(c), c->stream));
     }
     ALLOC(c->d_work, (size_t)std::max(W, c->P) + 2);
     ALLOC(c->d_m, c->cells); ALLOC(c->d_t, c->cells);
@@ -1795,18 +1814,18 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
             disc[(size_t)i] = (float)c->disc[(size_t)i];
             conc[(size_t)i] = (float)c->conc[(size_t)i];
         }
-        CU(cudaMemcpy(c->d_doclen, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_docgroup, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_alpha, al.data(), sizeof(float) * al.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_alpha64, al64.data(), sizeof(double) * al64.size(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_disc, disc.data(), sizeof(float) * I, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_conc, conc.data(), sizeof(float) * I, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_disc64, c->disc.data(), sizeof(double) * I, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_conc64, c->conc.data(), sizeof(double) * I, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_alpha_sum, asum.data(), sizeof(float) * I, cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(c->d_alpha_sum64, asum64.data(), sizeof(double) * I, cudaMemcpyHostToDevice));
-        CU(cudaMemset(c->d_sweep, 0, sizeof(uint32_t)));
-        CU(cudaMemset(c->d_stats, 0, sizeof(unsigned long long) * 8));
+        CU(cudaMemcpyAsync(c->d_doclen, dl.data(), sizeof(int32_t) * dl.size(), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_docgroup, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_alpha, al.data(), sizeof(float) * al.size(), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_alpha64, al64.data(), sizeof(double) * al64.size(), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_disc, disc.data(), sizeof(float) * I, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_conc, conc.data(), sizeof(float) * I, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_disc64, c->disc.data(), sizeof(double) * I, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_conc64, c->conc.data(), sizeof(double) * I, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_alpha_sum, asum.data(), sizeof(float) * I, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemcpyAsync(c->d_alpha_sum64, asum64.data(), sizeof(double) * I, cudaMemcpyHostToDevice, c->stream));
+        CU(cudaMemsetAsync(c->d_sweep, 0, sizeof(uint32_t), c->stream));
+        CU(cudaMemsetAsync(c->d_stats, 0, sizeof(unsigned long long) * 8, c->stream));
     }
     // pageable cudaMemcpy may return before its DMA lands; the context stream does not
     // order after the legacy stream, so settle every upload before the stream reads them
@@ -2652,6 +2671,10 @@ void spdp_destroy(spdp_ctx* c) {
     if (c->zr_ready) cudaEventDestroy(c->zr_ready);
     if (c->zr_copied) cudaEventDestroy(c->zr_copied);
     for (void* p : c->allocs) cudaFree(p);
+    if (c->stream) {
+        for (void* p : c->pooled) cudaFreeAsync(p, c->stream);
+        cudaStreamSynchronize(c->stream);
+    }
     for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
     if (c->h_zr_canon) cudaFreeHost(c->h_zr_canon);
     if (c->comm && c->nccl.CommDestroy) c->nccl.CommDestroy(c->comm);

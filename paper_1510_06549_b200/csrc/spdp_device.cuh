@@ -55,11 +55,12 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #define SPDP_STAGE_NEXT 0          // 1: the next chunk's counts and Stirling entries staged during this chunk (B200: C3 +5 %, C5 +3 %)
 #endif
 #ifndef SPDP_F_SMEM
-#define SPDP_F_SMEM 0              // dense pass reads F_k from shared memory instead of KPL registers per lane
-#endif
+#define SPDP_F_SMEM 2              // dense pass reads F_k from shared memory instead of KPL registers per lane:
+#endif                             // 0 never, 1 always, 2 at 8x32 (B200, C5: 31.7 -> 27.5 ms per sweep with 6 blocks
+                                   // per SM; C3 (4x32) +4 %, K = 300 (16x32) +7 %: those keep F in registers)
 #ifndef SPDP_MINB_8X32
-#define SPDP_MINB_8X32 5
-#endif
+#define SPDP_MINB_8X32 6           // 8x32 (F in shared memory): <= 80 registers, 6 resident blocks (B200, C5: 5 blocks
+#endif                             // 30.1 ms, 6 blocks 27.5 ms, 7 blocks 29.3 ms per sweep)
 #ifndef SPDP_MINB
 #define SPDP_MINB 4                // resident blocks per SM the sample kernel is compiled for
 #endif
@@ -508,9 +509,18 @@ struct SweepArgs {
 // touching n uses it with the row length Kn.
 
 // Per-warp shared memory (KSPAN entries each unless noted).
+template <int LPT, int KPL>
+__host__ __device__ constexpr bool f_in_smem() { return SPDP_F_SMEM == 1 || (SPDP_F_SMEM == 2 && LPT == 8 && KPL == 32); }
 template <int KSPAN, int KPL>
 struct __align__(16) WarpSmem {   // 16-byte multiple: every warp's F rows are read as float4
-    float F[KSPAN + 4 * (KSPAN / KPL)];    // F0 + F1 at the snapshot counts, skewed like aF
+    // F0 + F1 at the snapshot counts, skewed like aF: the group's per-lane reads (each chunk's register
+    // copy, or every step's blocks when the dense pass reads F here) are then conflict-free broadcasts
+    // (B200: K = 300 (16x32) 1.61 -> 1.53 ms per sweep, C3 -2 %); not at 32x32, where the skew's extra
+    // 512 B per warp cost a resident block (K = 1000: 4.0 -> 5.3 ms)
+    static constexpr bool kFS = f_in_smem<KSPAN / KPL, KPL>();
+    static constexpr bool kFSkew = kFS || KSPAN <= 512;
+    float F[KSPAN + (kFSkew ? 4 * (KSPAN / KPL) : 0)];
+    __device__ __forceinline__ static int fi(int k) { return kFSkew ? k + 4 * (k / KPL) : k; }
     float aF[KSPAN + 4 * (KSPAN / KPL)];   // alpha_ik F, lane segments skewed by 16 B (conflict-free)
     uint32_t mt[KSPAN];  // snapshot m << 16 | t of the segment's cells (M_max < 2^16)
     float R1[SPDP_SMEM_R1 && KSPAN <= 256 ? KSPAN : 1];   // r = 1 share F1 / F at the snapshot (phase 3's r split)
@@ -640,7 +650,7 @@ sample_kernel(SweepArgs A) {
     // r = 1 shares from the prologue in shared memory (not in the async mode: its copy is per chunk too,
     // but the live sums it reads in phase 3 are fresher); KSPAN <= 256 (smem budget of 16x32 / 32x32)
     constexpr bool kSmemR1 = SPDP_SMEM_R1 != 0 && KSPAN <= 256 && !ASYNC;
-    constexpr bool kFSmem = SPDP_F_SMEM != 0;
+    constexpr bool kFSmem = WarpSmem<KSPAN, KPL>::kFS;
     // the next chunk's prologue inputs staged during this chunk (wave mode: snapshot counts do not change
     // within a wave; the async mode copies live counts at chunk start by design)
     constexpr bool kStage = SPDP_STAGE_NEXT != 0 && WarpSmem<KSPAN, KPL>::kStage && !ASYNC && !DEBUG;
@@ -708,7 +718,7 @@ sample_kernel(SweepArgs A) {
             uint32_t mt = 0;
             if (k < K) { Fk = A.Ft[rrow + k]; aFk = A.aFt[rrow + k]; mt = A.MTt[rrow + k]; }
             if constexpr (kSmemR1) S.R1[k] = (k < K) ? A.R1t[rrow + k] : 0.f;
-            S.F[skew<KPL>(k)] = Fk;
+            S.F[S.fi(k)] = Fk;
             S.aF[skew<KPL>(k)] = aFk;
             S.mt[k] = mt;
             S.dmt[k] = 0;
@@ -767,7 +777,7 @@ sample_kernel(SweepArgs A) {
                 if (k >= KSPAN) continue;            // KSPAN < 32 (K <= 16)
                 const float Fk = F0 + F1;
                 if constexpr (kSmemR1) S.R1[k] = (F1 > 0.f) ? __fdiv_rn(F1, Fk) : 0.f;
-                S.F[skew<KPL>(k)] = Fk;
+                S.F[S.fi(k)] = Fk;
                 S.aF[skew<KPL>(k)] = __fmul_rn(al[j], Fk);
                 S.mt[k] = ((uint32_t)mv[j] << 16) | (uint32_t)tv[j];
                 S.dmt[k] = 0;
@@ -783,11 +793,11 @@ sample_kernel(SweepArgs A) {
     if constexpr (!kFSmem) {
 #pragma unroll
         for (int q = 0; q < NB; ++q) {
-            const float4 f4 = *reinterpret_cast<const float4*>(&S.F[skew<KPL>(kb + 4 * q)]);
+            const float4 f4 = *reinterpret_cast<const float4*>(&S.F[S.fi(kb + 4 * q)]);
             F[4 * q] = f4.x; F[4 * q + 1] = f4.y; F[4 * q + 2] = f4.z; F[4 * q + 3] = f4.w;
         }
     }
-    const float* Fl = &S.F[skew<KPL>(kb)];
+    const float* Fl = &S.F[S.fi(kb)];
     const float* aFl = &S.aF[skew<KPL>(kb)];
     float aSF[NB];                                   // per block: sum of alpha_ik F_k (SPDP_BLOCK_ALPHA)
     if constexpr (kBlockAlpha) {
@@ -872,7 +882,7 @@ sample_kernel(SweepArgs A) {
         float n0 = mine ? row_load1<NT, ASYNC>(nrow + A.sigma[k0]) : 0.f;
         if constexpr (ASYNC) n0 = fmaxf(n0, 1.f);    // the token itself is counted in its row
         const float al0 = alpha_i[k0];
-        const float wold = __fmaf_rn(n0, S.F[skew<KPL>(k0)], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
+        const float wold = __fmaf_rn(n0, S.F[S.fi(k0)], S.aF[skew<KPL>(k0)]);   // == the dense pass's mass
         const float wnew = __fmaf_rn(n0 - 1.f, Fk0, __fmul_rn(al0, Fk0));
         const float dlt = wnew - wold;
 
@@ -999,7 +1009,7 @@ sample_kernel(SweepArgs A) {
                 // sum by a few ulps; a target in that gap takes the last positive topic below)
                 const int kq = wg * KPL + 4 * qs;
                 const float4 n4 = row_load4<NT, ASYNC>(nrow + ((qs / QPU) * LA + wg) * UT + 4 * (qs % QPU));
-                const float4 F4 = *reinterpret_cast<const float4*>(&S.F[skew<KPL>(kq)]);
+                const float4 F4 = *reinterpret_cast<const float4*>(&S.F[S.fi(kq)]);
                 const float4 a4 = *reinterpret_cast<const float4*>(&S.aF[skew<KPL>(kq)]);
                 float wq[4] = {__fmaf_rn(n4.x, F4.x, a4.x), __fmaf_rn(n4.y, F4.y, a4.y),
                                __fmaf_rn(n4.z, F4.z, a4.z), __fmaf_rn(n4.w, F4.w, a4.w)};
@@ -1364,6 +1374,9 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
             const size_t off = (size_t)seg * Kp + k4;
             int4 a = *reinterpret_cast<const int4*>(dm + off);
             int4 d = packed_deltas ? make_int4(0, 0, 0, 0) : *reinterpret_cast<const int4*>(dt + off);
+            // the rows are loaded with the deltas (one round trip; most touched rows change at W = 1)
+            int4 vm = *reinterpret_cast<const int4*>(m + off);
+            int4 vt = *reinterpret_cast<const int4*>(t + off);
             if ((a.x | a.y | a.z | a.w | d.x | d.y | d.z | d.w) == 0) continue;
             if (packed_deltas) {                             // dm * 2^16 + dt (token kernel)
                 int* pa = &a.x; int* pd = &d.x;
@@ -1374,8 +1387,6 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
                     pa[e] = (int)((unsigned)x - (unsigned)pd[e]) >> 16;
                 }
             }
-            int4 vm = *reinterpret_cast<const int4*>(m + off);
-            int4 vt = *reinterpret_cast<const int4*>(t + off);
             const int4 om = vm, ot = vt;
             int* pm = &vm.x; int* pt = &vt.x;
             const int* pa = &a.x; const int* pd = &d.x;
