@@ -1363,7 +1363,8 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
     }
     if (herr[1] != ~0ull) {
         const size_t q = (size_t)herr[1];
-        return fail(c, SPDP_EINVAL, "document %d spans groups (%d and %d)", doc[q], c->docgroup[(size_t)doc[q]], group[q]);
+        return fail(c, SPDP_EINVAL, "document %d spans several groups (token %lld is in group %d)", doc[q], (long long)q,
+                    group[q]);
     }
     // in-document positions: stable sort of the tokens by document (ties keep canonical order)
     auto cub_run = [&](auto f, const char* what) -> spdp_status {
@@ -1666,8 +1667,10 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         cudaDeviceGetAttribute(&l2b, cudaDevAttrL2CacheSize, dev);
         const bool hbm_rows = (double)c->Dloc * c->Kn * sizeof(float) > 0.5 * (double)l2b;
         // (K > 256: the 16x32 / 32x32 kernels do not carry the store; C4 K = 1000 measured 5.31 vs 5.24 ms anyway)
-        c->doc_scatter = W == 1 && !c->token_kernel && !c->async && !c->sparse && !c->seq && !c->sprows && hbm_rows &&
-                         c->K <= 256;
+        // (B200, round 2: once the sample kernel ran at 6 blocks per SM the scattered stores cost more than the
+        // recount gains: C5 27.6 ms with, 26.9 ms without; opt-in, SPDP_DOC_SCATTER=1)
+        c->doc_scatter = false;
+        (void)hbm_rows;
         if (const char* e = getenv("SPDP_DOC_SCATTER"))
             c->doc_scatter = W == 1 && !c->token_kernel && !c->async && !c->sparse && !c->seq && atoi(e) != 0 && c->K <= 256;
         if (c->doc_scatter) {

@@ -21,15 +21,30 @@ __global__ void validate_tokens_kernel(const int32_t* __restrict__ group, const 
                                        const int32_t* __restrict__ word, uint32_t n, int I, int V, int D,
                                        int32_t* __restrict__ docgroup, int32_t* __restrict__ doclen,
                                        unsigned long long* __restrict__ err) {
-    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-        const int32_t g = group[p], d = doc[p], w = word[p];
-        if (g < 0 || g >= I || d < 0 || d >= D || w < 0 || w >= V) {
-            atomicMin(err, (unsigned long long)p);
-            continue;
+    // the lanes of a warp that hold the same document (consecutive tokens usually do) act through one
+    // leader: one CAS of the document's group and one length add per document and warp, instead of two
+    // same-address atomics per token
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t p0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); p0 < n; p0 += stride) {   // warp-uniform
+        const uint32_t p = p0 + (threadIdx.x & 31u);
+        int32_t g = 0, d = 0, w = 0;
+        bool ok = false;
+        if (p < n) {
+            g = group[p]; d = doc[p]; w = word[p];
+            ok = !(g < 0 || g >= I || d < 0 || d >= D || w < 0 || w >= V);
+            if (!ok) atomicMin(err, (unsigned long long)p);
         }
-        const int32_t old = atomicCAS(docgroup + d, -1, g);
-        if (old != -1 && old != g) atomicMin(err + 1, (unsigned long long)p);
-        atomicAdd(doclen + d, 1);
+        const unsigned okm = __ballot_sync(0xffffffffu, ok);
+        if (!ok) continue;
+        const unsigned peers = __match_any_sync(okm, d);
+        const int leader = __ffs(peers) - 1;
+        const int32_t gl = __shfl_sync(okm, g, leader);
+        if (g != gl) atomicMin(err + 1, (unsigned long long)p);          // the document spans groups in this warp
+        if ((int)(threadIdx.x & 31u) == leader) {
+            const int32_t old = atomicCAS(docgroup + d, -1, g);
+            if (old != -1 && old != g) atomicMin(err + 1, (unsigned long long)p);
+            atomicAdd(doclen + d, __popc(peers));
+        }
     }
 }
 
