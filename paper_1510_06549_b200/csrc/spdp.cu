@@ -159,7 +159,8 @@ struct spdp_ctx {
     bool token_kernel = false;                    // K <= 64: one lane per token (spdp_token.cuh)
     bool pack_dmt = false;                        // chunk kernels flush packed dm * 2^16 + dt words (M_max < 2^15)
     bool chunk_ft = false;                        // chunk kernel reads per-wave factor tables (SPDP_CHUNK_FACTORS)
-    bool doc_scatter = false;                     // W = 1 chunk kernel also writes zr in document order (recount streams it)
+    bool doc_scatter = false;
+    int recount_lpd = 32;                         // W = 1 recount: lanes per document (16 for short documents)                     // W = 1 chunk kernel also writes zr in document order (recount streams it)
     bool fold_merge = false;                      // several ranks, W = 1: the local merge writes only the net change
     uint32_t* d_slot = nullptr;                   // document-order slot of each sorted token
     uint16_t* d_zr_doc = nullptr;
@@ -384,6 +385,22 @@ void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
     SPDP_DISPATCH(c->LPT, c->KPL, CALL_P)
 #undef CALL_P
 }
+
+// the W = 1 doc-topic recount: 32 lanes per document, or 16 (two documents per warp) for short documents
+template <typename NT>
+struct Recount {
+    spdp_ctx* c;
+    cudaStream_t st;
+    void operator()(const uint32_t* doc_ptr, const uint32_t* doc_pos, const uint16_t* zr, const int* sigma, int D,
+                    int Kn, NT* n, const uint16_t* zr_doc) const {
+        const size_t smem = sizeof(int) * 8 * 2 * (size_t)Kn;
+        if (c->recount_lpd == 16)
+            recount_docs_kernel<NT, 16><<<148 * 8, 256, smem, st>>>(doc_ptr, doc_pos, zr, sigma, D, Kn, n, zr_doc);
+        else
+            recount_docs_kernel<NT, 32><<<148 * 8, 256, smem / 2, st>>>(doc_ptr, doc_pos, zr, sigma, D, Kn, n, zr_doc);
+    }
+};
+#define RECOUNT(c, NT, st) Recount<NT>{(c), (st)}
 
 // K <= 64: factor table of the wave's segments, then one lane per token (spdp_token.cuh)
 void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t te) {
@@ -888,8 +905,7 @@ void sparse_wave(spdp_ctx* c, int w) {
     const size_t ssm = ((Kp / 4) <= kSpSmemBlocks) ? sizeof(float) * 256 * (size_t)(Kp / 4) : 0;
     SPDP_ROWS(c->row_elem, sp_token_kernel<NT><<<std::max(grid, 1), 256, ssm, c->stream>>>(t));
     if (c->W == 1) {
-        const size_t smem = sizeof(int) * 8 * (size_t)c->Kn;
-        SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, c->stream>>>(
+        SPDP_ROWS(c->row_elem, RECOUNT(c, NT, c->stream)(
                                    c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n, nullptr));
         std::swap(c->d_zr, c->d_zr_next);
     } else {
@@ -971,8 +987,8 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
         }
     }
     rec(c, 1);
-    const size_t rsm = sizeof(int) * 8 * (size_t)c->Kn;      // every token moved to zr_next: rebuild n, swap
-    SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, rsm, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
+    // every token moved to zr_next: rebuild n, swap
+    SPDP_ROWS(c->row_elem, RECOUNT(c, NT, st)(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
                                                                             c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n,
                                                                             c->doc_scatter ? c->d_zr_doc : nullptr));
     rebuild_entries(c, st);
@@ -1071,8 +1087,7 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             cudaStream_t rs = side ? c->side_stream : c->stream;
-            const size_t smem = sizeof(int) * 8 * (size_t)c->Kn;
-            SPDP_ROWS(c->row_elem, recount_docs_kernel<NT><<<148 * 8, 256, smem, rs>>>(
+            SPDP_ROWS(c->row_elem, RECOUNT(c, NT, rs)(
                                        c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n,
                                        c->doc_scatter ? c->d_zr_doc : nullptr));
             rebuild_entries(c, rs);
@@ -1673,6 +1688,9 @@ spdp_status spdp_load_corpus(spdp_ctx* c, int64_t num_tokens, int32_t num_docs, 
         (void)hbm_rows;
         if (const char* e = getenv("SPDP_DOC_SCATTER"))
             c->doc_scatter = W == 1 && !c->token_kernel && !c->async && !c->sparse && !c->seq && atoi(e) != 0 && c->K <= 256;
+        // documents of <= 64 tokens on average: the recount takes two per warp
+        c->recount_lpd = (c->Dloc > 0 && (double)nloc / c->Dloc <= 64.0) ? 16 : 32;
+        if (const char* e = getenv("SPDP_RECOUNT_LPD")) c->recount_lpd = atoi(e) == 16 ? 16 : 32;
         if (c->doc_scatter) {
             ALLOC(c->d_slot, nl);
             ALLOC(c->d_zr_doc, nl);

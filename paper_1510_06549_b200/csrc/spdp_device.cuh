@@ -1241,38 +1241,48 @@ __global__ void merge_rows_kernel(int32_t* __restrict__ m, int32_t* __restrict__
 // assignments") instead of two scattered atomics per moved token: one warp per
 // document, a shared-memory histogram over the document's tokens (CSR index in
 // sorted-token positions), one coalesced row write in sigma order.
-template <typename NT>
+// LPD lanes per document (32, or 16 for short documents: two documents per warp keep twice the
+// scattered assignment loads in flight per warp; B200, C5 (62 tokens per document) 3.6 -> see DESIGN).
+template <typename NT, int LPD = 32>
 __global__ void recount_docs_kernel(const uint32_t* __restrict__ doc_ptr, const uint32_t* __restrict__ doc_pos,
                                     const uint16_t* __restrict__ zr, const int* __restrict__ sigma, int D, int Kn,
                                     NT* __restrict__ n, const uint16_t* __restrict__ zr_doc) {
-    extern __shared__ int hist[];                    // [warps][Kn] (row positions; the padding stays 0)
+    constexpr int DPW = 32 / LPD;                    // documents per warp and step
+    extern __shared__ int hist[];                    // [warps][DPW][Kn] (row positions; the padding stays 0)
     const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-    int* h = hist + (size_t)(threadIdx.x >> 5) * Kn;
-    for (int d = blockIdx.x * wpb + (threadIdx.x >> 5); d < D; d += gridDim.x * wpb) {
-        for (int j = lane; j < Kn; j += 32) h[j] = 0;
+    const int sub = lane / LPD, sl = lane % LPD;
+    int* h = hist + ((size_t)(threadIdx.x >> 5) * DPW + sub) * Kn;
+    const int nsteps = (D + DPW - 1) / DPW;
+    for (int ds = blockIdx.x * wpb + (threadIdx.x >> 5); ds < nsteps; ds += gridDim.x * wpb) {   // warp-uniform
+        const int d = ds * DPW + sub;
+        for (int j = sl; j < Kn; j += LPD) h[j] = 0;
         __syncwarp();
-        const uint32_t e = doc_ptr[d + 1];
-        if (zr_doc) {   // the sample kernel already wrote the assignments in document order: stream them
-            for (uint32_t t = doc_ptr[d] + lane; t < e; t += 32) atomicAdd(&h[sigma[zr_doc[t] & 0x7FFFu]], 1);
-        } else
-        // 4 tokens per lane in flight: the positions, then the scattered assignments, then the histogram
-        for (uint32_t t0 = doc_ptr[d]; t0 < e; t0 += 128) {
-            uint32_t pos[4];
-            uint32_t zv[4];
+        if (d < D) {
+            const uint32_t e = doc_ptr[d + 1];
+            if (zr_doc) {   // the sample kernel already wrote the assignments in document order: stream them
+                for (uint32_t t = doc_ptr[d] + sl; t < e; t += LPD) atomicAdd(&h[sigma[zr_doc[t] & 0x7FFFu]], 1);
+            } else
+            // 4 tokens per lane in flight: the positions, then the scattered assignments, then the histogram
+            for (uint32_t t0 = doc_ptr[d]; t0 < e; t0 += 4 * LPD) {
+                uint32_t pos[4];
+                uint32_t zv[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const uint32_t t = t0 + lane + 32u * j;
-                pos[j] = t < e ? doc_pos[t] : 0xFFFFFFFFu;
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t t = t0 + sl + (uint32_t)LPD * j;
+                    pos[j] = t < e ? doc_pos[t] : 0xFFFFFFFFu;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) zv[j] = pos[j] != 0xFFFFFFFFu ? (uint32_t)zr[pos[j]] : 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (zv[j] != 0xFFFFFFFFu) atomicAdd(&h[sigma[zv[j] & 0x7FFFu]], 1);
             }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) zv[j] = pos[j] != 0xFFFFFFFFu ? (uint32_t)zr[pos[j]] : 0xFFFFFFFFu;
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (zv[j] != 0xFFFFFFFFu) atomicAdd(&h[sigma[zv[j] & 0x7FFFu]], 1);
         }
         __syncwarp();
-        NT* row = n + (size_t)d * Kn;
-        for (int j = lane * 4; j < Kn; j += 128) Row<NT>::store4(row + j, h[j], h[j + 1], h[j + 2], h[j + 3]);
+        if (d < D) {
+            NT* row = n + (size_t)d * Kn;
+            for (int j = sl * 4; j < Kn; j += 4 * LPD) Row<NT>::store4(row + j, h[j], h[j + 1], h[j + 2], h[j + 3]);
+        }
         __syncwarp();
     }
 }

@@ -259,3 +259,13 @@ def test_sweep_async_pipeline_equals_sweep():
     a, b = ref.counts(), g.counts()
     for k in ("z", "r", "n", "m", "t", "Q"):
         np.testing.assert_array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("K,rowb,lpd", [(100, 4, "16"), (200, 1, "16"), (30, 4, "16"), (100, 4, "32")])
+def test_recount_lanes_per_document_lockstep(monkeypatch, K, rowb, lpd):
+    """The W = 1 doc-topic recount with 16 lanes per document (two documents per warp, the default for
+    documents of <= 64 tokens on average, C5) and with 32: the rebuilt rows must equal the oracle's."""
+    monkeypatch.setenv("SPDP_RECOUNT_LPD", lpd)
+    monkeypatch.setenv("SPDP_ROW_BYTES", str(rowb))
+    c = synth.generate(2, 40, 50.0, 300, 8, seed=K + rowb + int(lpd))
+    _lockstep(c, K, 1, 3)
