@@ -394,7 +394,7 @@ struct Recount {
     void operator()(const uint32_t* doc_ptr, const uint32_t* doc_pos, const uint16_t* zr, const int* sigma, int D,
                     int Kn, NT* n, const uint16_t* zr_doc) const {
         const size_t smem = sizeof(int) * 8 * 2 * (size_t)Kn;
-        if (c->recount_lpd == 16)
+        if (c->recount_lpd == 16 && smem <= 48 * 1024)   // (two histograms per warp within the default smem limit)
             recount_docs_kernel<NT, 16><<<148 * 8, 256, smem, st>>>(doc_ptr, doc_pos, zr, sigma, D, Kn, n, zr_doc);
         else
             recount_docs_kernel<NT, 32><<<148 * 8, 256, smem / 2, st>>>(doc_ptr, doc_pos, zr, sigma, D, Kn, n, zr_doc);

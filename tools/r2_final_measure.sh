@@ -1,8 +1,7 @@
 #!/bin/bash
 # Round-2 final measurement pass on one B200 (outputs under gpurun_out/; summaries copied to profiles/ by hand)
 mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/g8_build.log 2>&1
-rm -f gpurun_out/ab.txt; REPS=1 LIBS="varlibs/v9.so varlibs/v10.so" CONFIGS="C3;C5;C4 --topics 300;C4 --topics 1000" bash tools/ab_libs.sh
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2_final_build.log 2>&1
 timeout 900 python bench.py > gpurun_out/r2_bench_C3.json 2> gpurun_out/r2_bench_C3.err
 timeout 300 python tools/e2e_loop.py C3 50 > gpurun_out/r2_e2e_loop.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_launches_C3.csv \
