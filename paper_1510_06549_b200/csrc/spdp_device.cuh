@@ -1425,9 +1425,7 @@ __global__ void merge_segments_kernel(const uint32_t* __restrict__ segs, int nse
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 if (ct[e]) {
-#ifndef SPDP_TIMING_NO_Q_ATOMICS
                     atomicAdd(Q + (size_t)w * Kp + k4 + e, ct[e]);
-#endif
                     if (use_smem_sums) { atomicAdd(sT + (size_t)i * Kp + k4 + e, ct[e]); atomicAdd(sK + k4 + e, ct[e]); }
                     else { atomicAdd(Tt + (size_t)i * Kp + k4 + e, ct[e]); atomicAdd(T + k4 + e, ct[e]); }
                 }
