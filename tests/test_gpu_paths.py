@@ -269,3 +269,40 @@ def test_recount_lanes_per_document_lockstep(monkeypatch, K, rowb, lpd):
     monkeypatch.setenv("SPDP_ROW_BYTES", str(rowb))
     c = synth.generate(2, 40, 50.0, 300, 8, seed=K + rowb + int(lpd))
     _lockstep(c, K, 1, 3)
+
+
+@pytest.mark.parametrize("waves,K,narrow", [(1, 50, True), (1, 100, True), (2, 50, True), (1, 200, False), (3, 100, False)])
+def test_readback_scatter_overlaps_following_sweeps(waves, K, narrow):
+    """The canonical-order scatter of spdp_zr8_async / spdp_zr_async runs on the copy stream while the
+    next sweeps run; a sweep that writes the assignment buffer it reads (two sweeps later at W = 1,
+    the next one at W > 1) waits for it.  1 or 2 sweeps between read-backs, against a plain chain."""
+    c = corpus("C2")
+    ref = spdp.sampler_for(c, K, num_waves=waves, **HYPER)
+    g = spdp.sampler_for(c, K, num_waves=waves, **HYPER)
+    dt = np.uint8 if narrow else np.uint16
+    bufs = [np.zeros(c.num_tokens, dt) for _ in range(2)]
+    want = []
+    for s in range(6):
+        nsw = 1 + (s % 2)
+        ref.sweep(nsw)
+        gc = ref.counts(doc_topic=False, customers=False, tables=False, shadow=False)
+        if narrow:
+            want.append((gc["z"] | (gc["r"].astype(np.int32) << 7)).astype(np.uint8))
+        else:
+            want.append((gc["z"] | (gc["r"].astype(np.int32) << 15)).astype(np.uint16))
+        g.sweep_async(nsw)
+        g.wait()                                      # step s-1's copy has landed
+        if s > 0:
+            np.testing.assert_array_equal(bufs[(s - 1) % 2], want[s - 1])
+        (g.zr8_async if narrow else g.zr_async)(bufs[s % 2])
+    g.wait()
+    np.testing.assert_array_equal(bufs[5 % 2], want[5])
+    (g.zr8_async if narrow else g.zr_async)(bufs[0])   # a read-back still pending at the state installation
+    a = ref.counts()
+    g.set_state(a["z"], a["r"], tables=a["t"])
+    g.wait()
+    np.testing.assert_array_equal(bufs[0], want[5])
+    b = g.counts()
+    for k in ("z", "r", "n", "m", "t", "Q"):
+        np.testing.assert_array_equal(a[k], b[k])
+    g.close(); ref.close()

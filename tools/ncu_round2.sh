@@ -21,6 +21,7 @@ for spec in "$@"; do
     C4K100) cap C4_K100_sample sample_kernel --config C4 --topics 100 ;;
     C4K20) cap C4_K20_token token_kernel --config C4 --topics 20 ;;
     C3) cap C3_K100_sample sample_kernel --config C3 ;;
+    C3W2) cap C3_K100_W2_sample sample_kernel --config C3 --waves 2 ;;
     C2) cap C2_K50_token token_kernel --config C2 ;;
   esac
 done
