@@ -32,8 +32,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #define SPDP_PREFETCH_NEXT 0       // also prefetch the next batch's doc-topic rows
 #endif
 #ifndef SPDP_PRO_GROUP
-#define SPDP_PRO_GROUP 1           // chunk prologue: topics per lane whose loads are issued together (B200, C3:
-#endif                             // 4 -> 1.102 ms, 1 -> 1.053 ms: the register-capped 4x32 kernel schedules worse)
+#define SPDP_PRO_GROUP 4           // chunk prologue: topics per lane whose loads are issued together (B200, final
+#endif                             // kernels, 1 -> 4: C3 0.997 -> 0.974 ms, C3 W = 2 1.431 -> 1.385, C5 26.64 -> 26.39;
+                                   // before the unit layout 1 was best at C3, 1.053 vs 1.102 ms)
 #ifndef SPDP_SMEM_R1
 #define SPDP_SMEM_R1 1             // chunk prologue keeps every topic's r = 1 share in shared memory (KSPAN <= 256)
 #endif
