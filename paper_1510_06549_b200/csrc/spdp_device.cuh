@@ -35,6 +35,9 @@ constexpr int kWarps = 4;          // warps per block of the sample kernel
 #define SPDP_PRO_GROUP 4           // chunk prologue: topics per lane whose loads are issued together (B200, final
 #endif                             // kernels, 1 -> 4: C3 0.997 -> 0.974 ms, C3 W = 2 1.431 -> 1.385, C5 26.64 -> 26.39;
                                    // before the unit layout 1 was best at C3, 1.053 vs 1.102 ms)
+#ifndef SPDP_PRO_GROUP_1024
+#define SPDP_PRO_GROUP_1024 8      // ... at 32x32 (B200, K = 1000: 4 -> 8 topics 3.82 -> 3.61 ms; at 16x32 8 loses 3.5 %)
+#endif
 #ifndef SPDP_SMEM_R1
 #define SPDP_SMEM_R1 1             // chunk prologue keeps every topic's r = 1 share in shared memory (KSPAN <= 256)
 #endif
@@ -726,7 +729,8 @@ sample_kernel(SweepArgs A) {
         }
     } else {
         constexpr int PER = (KSPAN + 31) / 32;
-        constexpr int PG = SPDP_PRO_GROUP < PER ? SPDP_PRO_GROUP : PER;
+        constexpr int PGS = KSPAN >= 1024 ? SPDP_PRO_GROUP_1024 : SPDP_PRO_GROUP;
+        constexpr int PG = PGS < PER ? PGS : PER;
         static_assert(PER % PG == 0, "prologue group must divide the topics per lane");
 #pragma unroll 1
         for (int k0g = 0; k0g < PER; k0g += PG) {
