@@ -2687,7 +2687,10 @@ spdp_status spdp_stats(spdp_ctx* c, int64_t* out) {
 void spdp_destroy(spdp_ctx* c) {
     if (!c) return;
     if (c->cfg.device >= 0) cudaSetDevice(c->cfg.device);
+    // every stream that may still use the buffers drains before any of them is freed
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->side_stream) cudaStreamSynchronize(c->side_stream);
+    if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
     if (c->d2h_stream) { cudaStreamSynchronize(c->d2h_stream); cudaStreamDestroy(c->d2h_stream); }
     if (c->zr_ready) cudaEventDestroy(c->zr_ready);
     if (c->zr_copied) cudaEventDestroy(c->zr_copied);
