@@ -386,21 +386,19 @@ void launch_ppl(spdp_ctx* c, const SweepArgs& a, double* partial) {
 #undef CALL_P
 }
 
-// the W = 1 doc-topic recount: 32 lanes per document, or 16 (two documents per warp) for short documents
+// the W = 1 doc-topic rows rebuilt from zr_next: 32 lanes per document, or 16 (two documents per warp)
+// for short documents; zr_doc: the assignments already in document order (SPDP_DOC_SCATTER), or null
 template <typename NT>
-struct Recount {
-    spdp_ctx* c;
-    cudaStream_t st;
-    void operator()(const uint32_t* doc_ptr, const uint32_t* doc_pos, const uint16_t* zr, const int* sigma, int D,
-                    int Kn, NT* n, const uint16_t* zr_doc) const {
-        const size_t smem = sizeof(int) * 8 * 2 * (size_t)Kn;
-        if (c->recount_lpd == 16 && smem <= 48 * 1024)   // (two histograms per warp within the default smem limit)
-            recount_docs_kernel<NT, 16><<<148 * 8, 256, smem, st>>>(doc_ptr, doc_pos, zr, sigma, D, Kn, n, zr_doc);
-        else
-            recount_docs_kernel<NT, 32><<<148 * 8, 256, smem / 2, st>>>(doc_ptr, doc_pos, zr, sigma, D, Kn, n, zr_doc);
-    }
-};
-#define RECOUNT(c, NT, st) Recount<NT>{(c), (st)}
+void launch_recount(spdp_ctx* c, cudaStream_t st, const uint16_t* zr_doc) {
+    const size_t smem = sizeof(int) * 8 * 2 * (size_t)c->Kn;
+    NT* n = reinterpret_cast<NT*>(c->d_n);
+    if (c->recount_lpd == 16 && smem <= 48 * 1024)   // (two histograms per warp within the default smem limit)
+        recount_docs_kernel<NT, 16><<<148 * 8, 256, smem, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma,
+                                                               c->Dloc, c->Kn, n, zr_doc);
+    else
+        recount_docs_kernel<NT, 32><<<148 * 8, 256, smem / 2, st>>>(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
+                                                                   c->d_sigma, c->Dloc, c->Kn, n, zr_doc);
+}
 
 // K <= 64: factor table of the wave's segments, then one lane per token (spdp_token.cuh)
 void launch_token(spdp_ctx* c, uint32_t r0, uint32_t r1, uint32_t tb, uint32_t te) {
@@ -905,8 +903,7 @@ void sparse_wave(spdp_ctx* c, int w) {
     const size_t ssm = ((Kp / 4) <= kSpSmemBlocks) ? sizeof(float) * 256 * (size_t)(Kp / 4) : 0;
     SPDP_ROWS(c->row_elem, sp_token_kernel<NT><<<std::max(grid, 1), 256, ssm, c->stream>>>(t));
     if (c->W == 1) {
-        SPDP_ROWS(c->row_elem, RECOUNT(c, NT, c->stream)(
-                                   c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n, nullptr));
+        SPDP_ROWS(c->row_elem, launch_recount<NT>(c, c->stream, nullptr));
         std::swap(c->d_zr, c->d_zr_next);
     } else {
         const int tblocks = (int)std::min<uint32_t>((te - tb + 255) / 256, 148u * 16u);
@@ -988,9 +985,7 @@ spdp_status run_parts(spdp_ctx* c, SweepArgs a) {
     }
     rec(c, 1);
     // every token moved to zr_next: rebuild n, swap
-    SPDP_ROWS(c->row_elem, RECOUNT(c, NT, st)(c->d_doc_ptr, c->d_doc_pos, c->d_zr_next,
-                                                                            c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n,
-                                                                            c->doc_scatter ? c->d_zr_doc : nullptr));
+    SPDP_ROWS(c->row_elem, launch_recount<NT>(c, st, c->doc_scatter ? c->d_zr_doc : nullptr));
     rebuild_entries(c, st);
     std::swap(c->d_zr, c->d_zr_next);
     rec(c, 2);
@@ -1087,9 +1082,7 @@ spdp_status run_waves(spdp_ctx* c, int w0, int w1, bool first) {
         if (c->W == 1) {
             // every token moved to zr_next: rebuild the doc-topic rows, then swap
             cudaStream_t rs = side ? c->side_stream : c->stream;
-            SPDP_ROWS(c->row_elem, RECOUNT(c, NT, rs)(
-                                       c->d_doc_ptr, c->d_doc_pos, c->d_zr_next, c->d_sigma, c->Dloc, c->Kn, (NT*)c->d_n,
-                                       c->doc_scatter ? c->d_zr_doc : nullptr));
+            SPDP_ROWS(c->row_elem, launch_recount<NT>(c, rs, c->doc_scatter ? c->d_zr_doc : nullptr));
             rebuild_entries(c, rs);
             std::swap(c->d_zr, c->d_zr_next);
         } else {
